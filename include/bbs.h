@@ -1,0 +1,298 @@
+/*
+ * bbs.h — C-ABI of the B200-native batched branch-and-bound scan matcher.
+ *
+ * This is the drop-in boundary for the reference's localizer path
+ * (`bnbloc`, header-only C++20 under /root/reference/proj/include/bnbloc).
+ * The reference has no FFI of its own (proj/CMakeLists.txt:14-16 declares an
+ * INTERFACE library), so every entry point below names the reference
+ * function or type it replaces (file:line, relative to
+ * /root/reference/proj/include/bnbloc/).  The C++ facade in
+ * include/bnbloc_b200.hpp re-exposes these with the reference's own names,
+ * signatures and exception types.
+ *
+ * Conventions
+ *   - Every function returns a bbs_status; 0 is success.  On failure
+ *     bbs_last_error() returns the message the reference's exception would
+ *     carry (thread-local, valid until the next call on the same thread).
+ *   - Host pointers are caller-owned and only read/written during the call.
+ *   - Points are packed xyz triples of double (the layout of
+ *     std::vector<bnbloc::Point3>, geometry.hpp:12-30).
+ *   - Nodes are bbs_node, byte-compatible with bnbloc::Node (nodes.hpp:18-29).
+ *   - A bbs_map_t is immutable after build and may be shared by host threads
+ *     (voxel_map.hpp:54-56); a search owns its own per-call workspace.
+ *   - There is no CPU fallback: every compute entry point runs on the GPU the
+ *     map was built on and fails with BBS_ERR_CUDA when there is none.
+ */
+#ifndef BBS_B200_H
+#define BBS_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BBS_ABI_VERSION 1
+
+/* Status codes, 1:1 with the exception classes of errors.hpp:11-98. */
+typedef enum bbs_status {
+  BBS_OK = 0,
+  BBS_ERR_GENERIC = 1,              /* bnbloc::Error                  errors.hpp:11 */
+  BBS_ERR_FILE_NOT_FOUND = 2,       /* bnbloc::FileNotFoundError      errors.hpp:17 */
+  BBS_ERR_PARSE = 3,                /* bnbloc::ParseError             errors.hpp:28 */
+  BBS_ERR_EMPTY_CLOUD = 4,          /* bnbloc::EmptyCloudError        errors.hpp:46 */
+  BBS_ERR_CAPACITY_EXCEEDED = 5,    /* bnbloc::CapacityExceededError  errors.hpp:53 */
+  BBS_ERR_IO = 6,                   /* bnbloc::IoError                errors.hpp:59 */
+  BBS_ERR_FORMAT = 7,               /* bnbloc::FormatError            errors.hpp:65 */
+  BBS_ERR_DEGENERATE_SCAN = 8,      /* bnbloc::DegenerateScanError    errors.hpp:71 */
+  BBS_ERR_EMPTY_SEARCH_SPACE = 9,   /* bnbloc::EmptySearchSpaceError  errors.hpp:77 */
+  BBS_ERR_TOO_LARGE = 10,           /* bnbloc::TooLargeError          errors.hpp:83 */
+  BBS_ERR_INFEASIBLE_POSE = 11,     /* bnbloc::InfeasiblePoseError    errors.hpp:89 */
+  BBS_ERR_CONFIG = 12,              /* bnbloc::ConfigError            errors.hpp:95 */
+  BBS_ERR_CUDA = 13,                /* no counterpart: device/driver failure */
+  BBS_ERR_INVALID_ARGUMENT = 14     /* no counterpart: null handle/pointer */
+} bbs_status;
+
+/* Strategy / BranchMode, same enumerator order as search_config.hpp:14-15. */
+enum { BBS_STRATEGY_DFS = 0, BBS_STRATEGY_BFS = 1 };
+enum { BBS_BRANCH_TRANS_ONLY = 0, BBS_BRANCH_ROTO_TRANS = 1 };
+
+/* Device layout of one level's occupancy set (no reference counterpart:
+ * the reference always uses LevelMap's linear-probing table,
+ * voxel_map.hpp:57-180).  Membership, and so every score, is identical for
+ * all layouts. */
+enum {
+  BBS_LAYOUT_AUTO = 0,    /* per level: bitmap when it is not larger than the hash table */
+  BBS_LAYOUT_BITMAP = 1,  /* dense bit grid over the level's voxel box, 8x8x4 bricks = one 32 B sector */
+  BBS_LAYOUT_HASH = 2     /* open addressing, packed 64-bit keys, 4-key (32 B) buckets */
+};
+
+typedef struct bbs_point3 { double x, y, z; } bbs_point3;            /* Point3  geometry.hpp:12 */
+typedef struct bbs_pose6 {                                            /* Pose6   geometry.hpp:46 */
+  double x, y, z, roll, pitch, yaw;
+} bbs_pose6;
+typedef struct bbs_aabb { bbs_point3 min, max; } bbs_aabb;            /* Aabb    point_cloud.hpp:24 */
+typedef struct bbs_node {                                             /* Node    nodes.hpp:18-29 */
+  int32_t ix, iy, iz, iroll, ipitch, iyaw, level, score;
+} bbs_node;
+
+/* SearchConfig, search_config.hpp:24-52.  std::optional members become a
+ * has_* flag plus the value. */
+typedef struct bbs_search_config {
+  double min_resolution;            /* r, default 1.0 */
+  int32_t max_level;                /* default 6 */
+  int32_t has_translation_range;    /* 0: use the map bounding box */
+  bbs_aabb translation_range;
+  double roll_pitch_half_range;     /* default 0.02 */
+  double yaw_min;                   /* default 0 */
+  double yaw_max;                   /* default 2*pi */
+  double score_threshold_fraction;  /* default 0.95 */
+  uint64_t batch_size;              /* b, default 10000 */
+  int32_t strategy;                 /* BBS_STRATEGY_*, default BFS */
+  int32_t branch_mode;              /* BBS_BRANCH_*, default RotoTrans */
+  int32_t workers;                  /* accepted and ignored: the GPU grid replaces parallel_chunks */
+  int32_t has_d_max;
+  double d_max;
+  int32_t collect_trace;
+} bbs_search_config;
+
+/* Stats, search_config.hpp:55-69. */
+typedef struct bbs_stats {
+  uint64_t nodes_generated;
+  uint64_t nodes_pruned;
+  uint64_t batches_flushed;
+  double create_voxel_maps_ms;
+  double set_source_ms;
+  double initial_nodes_ms;
+  double find_best_score_ms;
+  double pop_remaining_queue_ms;
+} bbs_stats;
+
+/* SearchResult, search_config.hpp:71-80.  The incumbent trace is written
+ * into a caller-provided buffer (trace_capacity entries); trace_length is
+ * the full length even when it exceeds the capacity. */
+typedef struct bbs_search_result {
+  bbs_pose6 best_pose;
+  int32_t best_score;
+  int32_t score_threshold;
+  uint64_t scan_points;
+  int32_t matched;
+  bbs_stats stats;
+  int32_t* best_score_trace;
+  uint64_t trace_capacity;
+  uint64_t trace_length;
+  /* Extensions (no reference counterpart). */
+  bbs_node best_node;     /* the leaf behind best_pose */
+  uint64_t epochs;        /* flushes after the root batch */
+  uint64_t lookups;       /* (node, scan point) pairs scored = nodes_generated * K */
+  double device_ms;       /* device time of the search, CUDA events */
+  double root_score_ms;   /* device time of the root-batch score kernel */
+  double epoch_score_ms;  /* device time of the per-flush score kernels (sum) */
+  uint64_t root_nodes;    /* roots scored by this rank */
+  uint64_t queue_peak;    /* largest frontier (queue) length seen */
+} bbs_search_result;
+
+/* AxisGrid, angular_grid.hpp:45-58. */
+typedef struct bbs_axis_grid {
+  double w_min, w_max, step;
+  int32_t segments;
+  int32_t periodic;
+} bbs_axis_grid;
+
+typedef struct bbs_map_options {
+  int32_t device;   /* CUDA ordinal, default 0 */
+  int32_t layout;   /* BBS_LAYOUT_*, default AUTO */
+} bbs_map_options;
+
+typedef struct bbs_level_info {
+  int32_t level;
+  int32_t layout;                /* BBS_LAYOUT_BITMAP or BBS_LAYOUT_HASH */
+  double resolution;             /* LevelMap::resolution  voxel_map.hpp:119 */
+  uint64_t occupied_count;       /* LevelMap::occupied_count voxel_map.hpp:120 */
+  uint64_t bucket_count;         /* hash slots, or bitmap bits */
+  double collision_rate;         /* of OUR table (0 for bitmaps) */
+  double load_factor;            /* occupied / bucket_count */
+  uint64_t bytes;                /* device bytes of the structure */
+  int32_t box_min[3];            /* voxel box of the level (inclusive) */
+  int32_t box_max[3];
+} bbs_level_info;
+
+typedef struct bbs_map* bbs_map_t;
+typedef struct bbs_scan* bbs_scan_t;
+
+/* ---- errors / device ------------------------------------------------- */
+const char* bbs_last_error(void);
+int bbs_abi_version(void);
+/* Number of visible CUDA devices (0 without a GPU; never fails). */
+int bbs_device_count(void);
+
+/* ---- host-side helpers (no device work) ------------------------------ */
+/* SearchConfig defaults, search_config.hpp:24-52. */
+void bbs_search_config_default(bbs_search_config* cfg);
+/* AngularGrid(cfg, d_max), angular_grid.hpp:67-99: writes 3*(max_level+1)
+ * grids, axis-major (out[axis*(max_level+1)+level]). */
+int bbs_angular_grid(const bbs_search_config* cfg, double d_max, bbs_axis_grid* out,
+                     uint64_t capacity);
+/* AngularGrid::divisions, angular_grid.hpp:111-116. */
+int bbs_angular_divisions(const bbs_search_config* cfg, double d_max, int32_t axis,
+                          int32_t level, int32_t* out);
+/* max_range, point_cloud.hpp:58-63. */
+int bbs_max_range(const double* xyz, uint64_t n, double* out);
+/* bounding_box, point_cloud.hpp:42-54. */
+int bbs_bounding_box(const double* xyz, uint64_t n, bbs_aabb* out);
+/* prepare_source, pipeline.hpp:25-41 (voxel_grid_downsample + auto_leaf,
+ * point_cloud.hpp:78-182), host C++.  Writes at most `capacity` points;
+ * *count is the full size.  leaf/converged/d_max may be NULL. */
+int bbs_prepare_source(const double* xyz, uint64_t n, uint64_t target_points, double* out_xyz,
+                       uint64_t capacity, uint64_t* count, double* leaf, int32_t* converged,
+                       double* d_max);
+/* Root node count of initial_nodes, nodes.hpp:60-85. */
+int bbs_initial_node_count(const bbs_search_config* cfg, double d_max, const bbs_aabb* range,
+                           uint64_t* count);
+
+/* ---- map (L3) -------------------------------------------------------- */
+/* MultiResVoxelMap::build, voxel_map.hpp:226-244 (and build_level /
+ * inflated_voxels :186-216, LevelMap::from_voxels :72-116), on the device.
+ * collision_target is validated and recorded; the device tables do not use
+ * the reference's sizing loop (membership is layout-independent).
+ * memory_cap_bytes caps each level's device structure
+ * (CapacityExceededError, voxel_map.hpp:91-95).  opts may be NULL. */
+int bbs_map_build(const double* xyz, uint64_t n, double min_resolution, int32_t max_level,
+                  double collision_target, uint64_t memory_cap_bytes,
+                  const bbs_map_options* opts, bbs_map_t* out);
+/* MultiResVoxelMap::from_levels, voxel_map.hpp:247-261 (map_io load path). */
+int bbs_map_from_levels(const int32_t* const* level_voxels, const uint64_t* counts,
+                        int32_t n_levels, double min_resolution, const bbs_aabb* bbox,
+                        double collision_target, uint64_t memory_cap_bytes,
+                        const bbs_map_options* opts, bbs_map_t* out);
+int bbs_map_free(bbs_map_t map);
+int bbs_map_min_resolution(bbs_map_t map, double* out);   /* voxel_map.hpp:263 */
+int bbs_map_max_level(bbs_map_t map, int32_t* out);       /* voxel_map.hpp:264 */
+int bbs_map_bbox(bbs_map_t map, bbs_aabb* out);           /* voxel_map.hpp:265 */
+/* Device time of the map build ("Create voxel maps", Stats::create_voxel_maps_ms). */
+int bbs_map_build_ms(bbs_map_t map, double* out);
+int bbs_map_level_info(bbs_map_t map, int32_t level, bbs_level_info* out);
+/* LevelMap::occupied_voxels, voxel_map.hpp:158-165: ascending (x,y,z). */
+int bbs_level_occupied(bbs_map_t map, int32_t level, int32_t* xyz, uint64_t capacity,
+                       uint64_t* count);
+/* LevelMap::contains, voxel_map.hpp:127-135, for n voxel triples. */
+int bbs_level_contains(bbs_map_t map, int32_t level, const int32_t* xyz, uint64_t n,
+                       uint8_t* out);
+/* LevelMap::score, voxel_map.hpp:142-154: rotation row-major (Transform,
+ * geometry.hpp:62-64). */
+int bbs_level_score(bbs_map_t map, int32_t level, const double rotation[9],
+                    const double translation[3], const double* scan_xyz, uint64_t k,
+                    int32_t* score);
+
+/* ---- search (L5/L6) --------------------------------------------------- */
+/* batch_evaluate, search.hpp:23-34: nodes scored in place (host buffer).
+ * The AngularGrid is built from (cfg, d_max); d_max <= 0 means
+ * max_range(scan). */
+int bbs_batch_evaluate(bbs_map_t map, const double* scan_xyz, uint64_t k,
+                       const bbs_search_config* cfg, double d_max, bbs_node* nodes, uint64_t n);
+/* search, search.hpp:72-186. */
+int bbs_search(bbs_map_t map, const double* scan_xyz, uint64_t k, const bbs_search_config* cfg,
+               bbs_search_result* result);
+/* localize_scan, pipeline.hpp:45-51. */
+int bbs_localize_scan(bbs_map_t map, const double* raw_xyz, uint64_t n,
+                      const bbs_search_config* cfg, uint64_t downsample_target,
+                      bbs_search_result* result);
+
+/* Device-resident scan: upload once, search many times with no host copy
+ * of the scan inside the call. */
+int bbs_scan_upload(bbs_map_t map, const double* xyz, uint64_t k, bbs_scan_t* out);
+int bbs_scan_free(bbs_scan_t scan);
+int bbs_search_scan(bbs_map_t map, bbs_scan_t scan, const bbs_search_config* cfg,
+                    bbs_search_result* result);
+/* batch_evaluate over DEVICE node memory (n nodes at d_nodes) on `stream`
+ * (a cudaStream_t, NULL = the map's stream).  Asynchronous. */
+int bbs_batch_evaluate_device(bbs_map_t map, bbs_scan_t scan, const bbs_search_config* cfg,
+                              double d_max, bbs_node* d_nodes, uint64_t n, void* stream);
+
+/* ---- multi-GPU (root sharding) ---------------------------- */
+/* Element-wise MAX all-reduce of `count` int64 values in place across all
+ * ranks; returns 0 on success.  Supplied by the caller (NCCL / gloo). */
+typedef int (*bbs_allreduce_max_fn)(int64_t* values, int32_t count, void* user);
+typedef struct bbs_shard {
+  int32_t rank;
+  int32_t world_size;
+  bbs_allreduce_max_fn allreduce_max;
+  void* user;
+} bbs_shard;
+/* search() over the roots with index % world_size == rank; the incumbent is
+ * max-all-reduced after every epoch and the winner elected at the end, so
+ * every rank returns the same best pose/score.  Stats are this rank's. */
+int bbs_search_sharded(bbs_map_t map, bbs_scan_t scan, const bbs_search_config* cfg,
+                       const bbs_shard* shard, bbs_search_result* result);
+
+/* ---- synthetic-input harness (not part of the matcher path) ----------- */
+/* SceneSpec, scene.hpp:21-38. */
+typedef struct bbs_scene_spec {
+  double size_x, size_y, size_z;
+  int32_t num_boxes;
+  double min_box_side, max_box_side, min_box_height;
+  double map_spacing, scan_spacing, scan_range, point_jitter;
+  int32_t tilt_noise;
+  double gt_yaw_min, gt_yaw_max;
+  uint64_t min_scan_points;
+  double feasibility_resolution;
+} bbs_scene_spec;
+void bbs_scene_spec_default(bbs_scene_spec* spec);
+/* gen_scene, scene.hpp:156-220 (bit-identical restatement).  Buffers are
+ * malloc'ed; release with bbs_free.  gt6 = x, y, z, roll, pitch, yaw. */
+int bbs_gen_scene(const bbs_scene_spec* spec, uint64_t seed, double** map_xyz, uint64_t* n_map,
+                  double** scan_xyz, uint64_t* n_scan, double* gt6);
+/* Extra scans of seed's map (poses from Rng(pose_seed_base + j)). */
+int bbs_gen_scans(const bbs_scene_spec* spec, uint64_t seed, uint64_t pose_seed_base,
+                  int32_t n_scans, double** scan_xyz, uint64_t* offsets, double* gt);
+/* First k points of a Fisher-Yates shuffle driven by Rng(seed). */
+int bbs_cut_scan(const double* xyz, uint64_t n, uint64_t k, uint64_t seed, double* out);
+const char* bbs_scene_last_error(void);
+void bbs_free(void* p);
+
+#ifdef __cplusplus
+}  /* extern "C" */
+#endif
+
+#endif  /* BBS_B200_H */

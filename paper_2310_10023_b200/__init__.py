@@ -1,0 +1,692 @@
+"""B200-native batched branch-and-bound scan matcher (3D-BBS hot path).
+
+A Python mirror of the reference's localizer API (``bnbloc``,
+/root/reference/proj/include/bnbloc) over the C-ABI of include/bbs.h: the
+same names, argument meanings and exception types, so code and tests written
+against ``bnbloc`` read the same here.  All compute runs on the GPU through
+libbbs_b200.so; there is no CPU fallback.
+
+    MultiResVoxelMap.build   voxel_map.hpp:226      (device map build, K1-K3)
+    LevelMap.score           voxel_map.hpp:142      (K4 score)
+    batch_evaluate           search.hpp:23          (K4 over node batches)
+    search                   search.hpp:72          (device frontier, K5-K6)
+    localize_scan            pipeline.hpp:45
+    AngularGrid              angular_grid.hpp:65
+"""
+import ctypes as C
+import enum
+import math
+from dataclasses import dataclass, field
+from typing import List, Optional
+
+import numpy as np
+
+from . import _abi
+from ._abi import Aabb, AxisGridC, LevelInfo, MapOptions, Node, SearchConfigC, SearchResultC, Shard
+from ._lib import lib
+
+__all__ = [
+    "Error", "FileNotFoundError_", "ParseError", "EmptyCloudError", "CapacityExceededError",
+    "IoError", "FormatError", "DegenerateScanError", "EmptySearchSpaceError", "TooLargeError",
+    "InfeasiblePoseError", "ConfigError", "CudaError", "InvalidArgumentError",
+    "Strategy", "BranchMode", "Layout", "SearchConfig", "Stats", "SearchResult", "Pose6",
+    "AxisGrid", "AngularGrid", "LevelMap", "MultiResVoxelMap", "DeviceScan", "NODE_DTYPE",
+    "batch_evaluate", "search", "search_sharded", "localize_scan", "prepare_source",
+    "max_range", "bounding_box", "pose_to_transform", "node_pose", "initial_node_count",
+    "gen_scene", "gen_scans", "cut_scan", "SceneSpec", "device_count",
+]
+
+KTWO_PI = _abi.TWO_PI
+
+
+# ---- errors (errors.hpp:11-98) ---------------------------------------------
+class Error(RuntimeError):
+    """bnbloc::Error."""
+
+
+class FileNotFoundError_(Error):
+    pass
+
+
+class ParseError(Error):
+    pass
+
+
+class EmptyCloudError(Error):
+    pass
+
+
+class CapacityExceededError(Error):
+    pass
+
+
+class IoError(Error):
+    pass
+
+
+class FormatError(Error):
+    pass
+
+
+class DegenerateScanError(Error):
+    pass
+
+
+class EmptySearchSpaceError(Error):
+    pass
+
+
+class TooLargeError(Error):
+    pass
+
+
+class InfeasiblePoseError(Error):
+    pass
+
+
+class ConfigError(Error):
+    pass
+
+
+class CudaError(Error):
+    """Device failure (no reference counterpart)."""
+
+
+class InvalidArgumentError(Error):
+    """Null handle / bad buffer (no reference counterpart)."""
+
+
+_ERRORS = {
+    1: Error, 2: FileNotFoundError_, 3: ParseError, 4: EmptyCloudError,
+    5: CapacityExceededError, 6: IoError, 7: FormatError, 8: DegenerateScanError,
+    9: EmptySearchSpaceError, 10: TooLargeError, 11: InfeasiblePoseError, 12: ConfigError,
+    13: CudaError, 14: InvalidArgumentError,
+}
+
+
+def _check(status, msg_fn=None):
+    if status != 0:
+        msg = (msg_fn or lib.bbs_last_error)()
+        raise _ERRORS.get(status, Error)(msg.decode() if isinstance(msg, bytes) else str(msg))
+
+
+def device_count():
+    return lib.bbs_device_count()
+
+
+# ---- config / results (search_config.hpp) ----------------------------------
+class Strategy(enum.IntEnum):
+    DFS = 0  # kDfs
+    BFS = 1  # kBfs
+
+
+class BranchMode(enum.IntEnum):
+    TRANS_ONLY = 0  # kTransOnly
+    ROTO_TRANS = 1  # kRotoTrans
+
+
+class Layout(enum.IntEnum):
+    AUTO = 0
+    BITMAP = 1
+    HASH = 2
+
+
+@dataclass
+class Pose6:
+    """geometry.hpp:46-60."""
+    x: float = 0.0
+    y: float = 0.0
+    z: float = 0.0
+    roll: float = 0.0
+    pitch: float = 0.0
+    yaw: float = 0.0
+
+    def normalized(self):
+        return Pose6(self.x, self.y, self.z, self.roll, self.pitch, normalize_angle(self.yaw))
+
+    def as_tuple(self):
+        return (self.x, self.y, self.z, self.roll, self.pitch, self.yaw)
+
+
+@dataclass
+class SearchConfig:
+    """search_config.hpp:24-52 (same fields and defaults)."""
+    min_resolution: float = 1.0
+    max_level: int = 6
+    translation_range: Optional[tuple] = None  # ((minx, miny, minz), (maxx, maxy, maxz))
+    roll_pitch_half_range: float = 0.02
+    yaw_min: float = 0.0
+    yaw_max: float = KTWO_PI
+    score_threshold_fraction: float = 0.95
+    batch_size: int = 10000
+    strategy: Strategy = Strategy.BFS
+    branch_mode: BranchMode = BranchMode.ROTO_TRANS
+    workers: int = 1
+    d_max: Optional[float] = None
+    collect_trace: bool = False
+
+    def to_c(self) -> SearchConfigC:
+        c = SearchConfigC()
+        lib.bbs_search_config_default(C.byref(c))
+        c.min_resolution = float(self.min_resolution)
+        c.max_level = int(self.max_level)
+        if self.translation_range is not None:
+            c.has_translation_range = 1
+            (a, b) = self.translation_range
+            c.translation_range.min.x, c.translation_range.min.y, c.translation_range.min.z = a
+            c.translation_range.max.x, c.translation_range.max.y, c.translation_range.max.z = b
+        c.roll_pitch_half_range = float(self.roll_pitch_half_range)
+        c.yaw_min = float(self.yaw_min)
+        c.yaw_max = float(self.yaw_max)
+        c.score_threshold_fraction = float(self.score_threshold_fraction)
+        c.batch_size = int(self.batch_size)
+        c.strategy = int(self.strategy)
+        c.branch_mode = int(self.branch_mode)
+        c.workers = int(self.workers)
+        if self.d_max is not None:
+            c.has_d_max = 1
+            c.d_max = float(self.d_max)
+        c.collect_trace = 1 if self.collect_trace else 0
+        return c
+
+
+@dataclass
+class Stats:
+    """search_config.hpp:55-69."""
+    nodes_generated: int = 0
+    nodes_pruned: int = 0
+    batches_flushed: int = 0
+    create_voxel_maps_ms: float = 0.0
+    set_source_ms: float = 0.0
+    initial_nodes_ms: float = 0.0
+    find_best_score_ms: float = 0.0
+    pop_remaining_queue_ms: float = 0.0
+
+    def preprocessing_total_ms(self):
+        return self.create_voxel_maps_ms + self.set_source_ms
+
+    def localization_total_ms(self):
+        return self.initial_nodes_ms + self.find_best_score_ms + self.pop_remaining_queue_ms
+
+
+@dataclass
+class SearchResult:
+    """search_config.hpp:71-80, plus device extensions."""
+    best_pose: Pose6 = field(default_factory=Pose6)
+    best_score: int = 0
+    score_threshold: int = 0
+    scan_points: int = 0
+    matched: bool = False
+    stats: Stats = field(default_factory=Stats)
+    best_score_trace: List[int] = field(default_factory=list)
+    best_node: tuple = ()
+    epochs: int = 0
+    lookups: int = 0
+    device_ms: float = 0.0
+    root_score_ms: float = 0.0
+    epoch_score_ms: float = 0.0
+    root_nodes: int = 0
+    queue_peak: int = 0
+
+
+def _result_from_c(r: SearchResultC, trace_buf=None) -> SearchResult:
+    s = r.stats
+    out = SearchResult(
+        best_pose=Pose6(*r.best_pose.as_tuple()), best_score=r.best_score,
+        score_threshold=r.score_threshold, scan_points=r.scan_points, matched=bool(r.matched),
+        stats=Stats(s.nodes_generated, s.nodes_pruned, s.batches_flushed, s.create_voxel_maps_ms,
+                    s.set_source_ms, s.initial_nodes_ms, s.find_best_score_ms,
+                    s.pop_remaining_queue_ms),
+        best_node=tuple(getattr(r.best_node, f) for f in _abi.NODE_DTYPE_FIELDS),
+        epochs=r.epochs, lookups=r.lookups, device_ms=r.device_ms, root_score_ms=r.root_score_ms,
+        epoch_score_ms=r.epoch_score_ms, root_nodes=r.root_nodes, queue_peak=r.queue_peak)
+    if trace_buf is not None:
+        out.best_score_trace = list(trace_buf[: min(r.trace_length, len(trace_buf))])
+    return out
+
+
+def _new_result(trace_cap):
+    res = SearchResultC()
+    buf = None
+    if trace_cap:
+        buf = (C.c_int32 * trace_cap)()
+        res.best_score_trace = C.cast(buf, C.POINTER(C.c_int32))
+        res.trace_capacity = trace_cap
+    return res, buf
+
+
+# ---- geometry helpers (geometry.hpp) ----------------------------------------
+def normalize_angle(a):
+    """geometry.hpp:36-43."""
+    r = math.fmod(a, KTWO_PI)
+    if r < 0.0:
+        r += KTWO_PI
+    if r >= KTWO_PI:
+        r = 0.0
+    return r
+
+
+def pose_to_transform(p: Pose6):
+    """geometry.hpp:102-112 -> (rotation row-major list of 9, translation)."""
+    ca, sa = math.cos(p.roll), math.sin(p.roll)
+    cb, sb = math.cos(p.pitch), math.sin(p.pitch)
+    cg, sg = math.cos(p.yaw), math.sin(p.yaw)
+    R = [cg * cb, cg * sb * sa - sg * ca, cg * sb * ca + sg * sa,
+         sg * cb, sg * sb * sa + cg * ca, sg * sb * ca - cg * sa,
+         -sb, cb * sa, cb * ca]
+    return R, [p.x, p.y, p.z]
+
+
+def _xyz(points):
+    a = np.ascontiguousarray(np.asarray(points, dtype=np.float64).reshape(-1, 3))
+    return a
+
+
+def _dptr(a):
+    return a.ctypes.data_as(C.POINTER(C.c_double))
+
+
+def max_range(points):
+    """point_cloud.hpp:58-63."""
+    a = _xyz(points)
+    out = C.c_double()
+    _check(lib.bbs_max_range(_dptr(a), a.shape[0], C.byref(out)))
+    return out.value
+
+
+def bounding_box(points):
+    """point_cloud.hpp:42-54 -> ((min), (max))."""
+    a = _xyz(points)
+    b = Aabb()
+    _check(lib.bbs_bounding_box(_dptr(a), a.shape[0], C.byref(b)))
+    return (b.min.x, b.min.y, b.min.z), (b.max.x, b.max.y, b.max.z)
+
+
+@dataclass
+class SourcePrep:
+    """pipeline.hpp:14-20."""
+    scan: np.ndarray
+    leaf: float
+    leaf_converged: bool
+    d_max: float
+
+
+def prepare_source(raw_scan, target_points):
+    """pipeline.hpp:25-41 (host C++ in libbbs_b200)."""
+    a = _xyz(raw_scan)
+    cnt = C.c_uint64()
+    leaf, dm = C.c_double(), C.c_double()
+    conv = C.c_int32()
+    _check(lib.bbs_prepare_source(_dptr(a), a.shape[0], int(target_points), None, 0,
+                                  C.byref(cnt), None, None, None))
+    out = np.zeros((cnt.value, 3))
+    _check(lib.bbs_prepare_source(_dptr(a), a.shape[0], int(target_points), _dptr(out), cnt.value,
+                                  C.byref(cnt), C.byref(leaf), C.byref(conv), C.byref(dm)))
+    return SourcePrep(out, leaf.value, bool(conv.value), dm.value)
+
+
+# ---- angular grid (angular_grid.hpp) ----------------------------------------
+@dataclass
+class AxisGrid:
+    """angular_grid.hpp:45-58."""
+    w_min: float
+    w_max: float
+    step: float
+    segments: int
+    periodic: bool
+
+    def max_index(self):
+        if self.segments == 0:
+            return 0
+        return self.segments - 1 if self.periodic else self.segments
+
+    def index_count(self):
+        return self.max_index() + 1
+
+    def angle(self, index):
+        return self.w_min + self.step * float(index)
+
+
+class AngularGrid:
+    """angular_grid.hpp:65-125: AngularGrid(cfg, d_max)."""
+
+    def __init__(self, cfg: SearchConfig, d_max: float):
+        self.cfg = cfg
+        self.d_max = float(d_max)
+        n = 3 * (cfg.max_level + 1)
+        out = (AxisGridC * n)()
+        c = cfg.to_c()
+        _check(lib.bbs_angular_grid(C.byref(c), self.d_max, out, n))
+        self._axes = [AxisGrid(g.w_min, g.w_max, g.step, g.segments, bool(g.periodic)) for g in out]
+        self._max_level = cfg.max_level
+
+    def max_level(self):
+        return self._max_level
+
+    def axis(self, axis, level):
+        return self._axes[axis * (self._max_level + 1) + level]
+
+    def divisions(self, axis, level):
+        parent, child = self.axis(axis, level), self.axis(axis, level - 1)
+        if child.segments <= 1:
+            return 1
+        return (child.segments + parent.segments - 1) // parent.segments
+
+
+NODE_DTYPE = np.dtype([(f, np.int32) for f in _abi.NODE_DTYPE_FIELDS])
+
+
+def node_pose(node, grids: AngularGrid, min_resolution):
+    """nodes.hpp:33-43."""
+    ix, iy, iz, ir, ip, iw, level = (int(v) for v in list(node)[:7])
+    cell = math.ldexp(min_resolution, level)
+    return Pose6(cell * float(ix), cell * float(iy), cell * float(iz),
+                 grids.axis(0, level).angle(ir), grids.axis(1, level).angle(ip),
+                 grids.axis(2, level).angle(iw))
+
+
+def initial_node_count(cfg: SearchConfig, d_max, rng):
+    """len(initial_nodes(...)), nodes.hpp:60-85."""
+    c = cfg.to_c()
+    b = Aabb()
+    (b.min.x, b.min.y, b.min.z), (b.max.x, b.max.y, b.max.z) = rng
+    out = C.c_uint64()
+    _check(lib.bbs_initial_node_count(C.byref(c), float(d_max), C.byref(b), C.byref(out)))
+    return out.value
+
+
+def _nodes_array(nodes):
+    a = np.asarray(nodes)
+    if a.dtype == NODE_DTYPE:
+        a = a.view(np.int32).reshape(-1, 8)
+    return np.ascontiguousarray(a.astype(np.int32, copy=False).reshape(-1, 8))
+
+
+# ---- voxel map (voxel_map.hpp) ----------------------------------------------
+class LevelMap:
+    """One level of a device map (voxel_map.hpp:57-180)."""
+
+    def __init__(self, parent, level):
+        self._m = parent
+        self._level = level
+        info = LevelInfo()
+        _check(lib.bbs_map_level_info(parent._h, level, C.byref(info)))
+        self._info = info
+
+    def level(self):
+        return self._level
+
+    def resolution(self):
+        return self._info.resolution
+
+    def occupied_count(self):
+        return self._info.occupied_count
+
+    def bucket_count(self):
+        return self._info.bucket_count
+
+    def collision_rate(self):
+        return self._info.collision_rate
+
+    def load_factor(self):
+        return self._info.load_factor
+
+    def layout(self):
+        return Layout(self._info.layout)
+
+    def device_bytes(self):
+        return self._info.bytes
+
+    def occupied_voxels(self):
+        """Ascending (x, y, z), voxel_map.hpp:158-165 -> (n, 3) int32."""
+        n = C.c_uint64()
+        _check(lib.bbs_level_occupied(self._m._h, self._level, None, 0, C.byref(n)))
+        out = np.zeros((n.value, 3), np.int32)
+        if n.value:
+            _check(lib.bbs_level_occupied(self._m._h, self._level,
+                                          out.ctypes.data_as(C.POINTER(C.c_int32)), n.value,
+                                          C.byref(n)))
+        return out
+
+    def contains_many(self, voxels):
+        v = np.ascontiguousarray(np.asarray(voxels, np.int32).reshape(-1, 3))
+        out = np.zeros(v.shape[0], np.uint8)
+        if v.shape[0]:
+            _check(lib.bbs_level_contains(self._m._h, self._level,
+                                          v.ctypes.data_as(C.POINTER(C.c_int32)), v.shape[0],
+                                          out.ctypes.data_as(C.POINTER(C.c_uint8))))
+        return out.astype(bool)
+
+    def contains(self, v):
+        """voxel_map.hpp:127-135."""
+        return bool(self.contains_many([v])[0])
+
+    def score(self, transform, scan):
+        """voxel_map.hpp:142-154; transform = (rotation[9] row-major, translation[3])."""
+        R, t = transform
+        Ra = np.ascontiguousarray(np.asarray(R, np.float64).ravel())
+        ta = np.ascontiguousarray(np.asarray(t, np.float64).ravel())
+        s = _xyz(scan)
+        out = C.c_int32()
+        _check(lib.bbs_level_score(self._m._h, self._level, _dptr(Ra), _dptr(ta), _dptr(s),
+                                   s.shape[0], C.byref(out)))
+        return out.value
+
+
+class MultiResVoxelMap:
+    """voxel_map.hpp:220-274, device-resident."""
+
+    kDefaultCollisionTarget = 0.001
+    kDefaultMemoryCapBytes = 2 << 30
+
+    def __init__(self, handle):
+        self._h = handle
+        r, ml = C.c_double(), C.c_int32()
+        _check(lib.bbs_map_min_resolution(self._h, C.byref(r)))
+        _check(lib.bbs_map_max_level(self._h, C.byref(ml)))
+        self._r, self._max_level = r.value, ml.value
+        self._levels = [LevelMap(self, l) for l in range(self._max_level + 1)]
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            lib.bbs_map_free(h)
+            self._h = None
+
+    @staticmethod
+    def build(map_points, min_resolution, max_level, collision_target=0.001,
+              memory_cap_bytes=2 << 30, layout=Layout.AUTO, device=0):
+        """voxel_map.hpp:226-244."""
+        a = _xyz(map_points)
+        h = C.c_void_p()
+        opts = MapOptions(int(device), int(layout))
+        _check(lib.bbs_map_build(_dptr(a), a.shape[0], float(min_resolution), int(max_level),
+                                 float(collision_target), int(memory_cap_bytes), C.byref(opts),
+                                 C.byref(h)))
+        return MultiResVoxelMap(h)
+
+    @staticmethod
+    def from_levels(per_level, min_resolution, bbox, collision_target=0.001,
+                    memory_cap_bytes=2 << 30, layout=Layout.AUTO, device=0):
+        """voxel_map.hpp:247-261; bbox = ((min), (max))."""
+        arrs = [np.ascontiguousarray(np.asarray(v, np.int32).reshape(-1, 3)) for v in per_level]
+        n = len(arrs)
+        ptrs = (C.POINTER(C.c_int32) * max(n, 1))(
+            *[a.ctypes.data_as(C.POINTER(C.c_int32)) for a in arrs])
+        counts = (C.c_uint64 * max(n, 1))(*[a.shape[0] for a in arrs])
+        b = Aabb()
+        (b.min.x, b.min.y, b.min.z), (b.max.x, b.max.y, b.max.z) = bbox
+        h = C.c_void_p()
+        opts = MapOptions(int(device), int(layout))
+        _check(lib.bbs_map_from_levels(ptrs, counts, n, float(min_resolution), C.byref(b),
+                                       float(collision_target), int(memory_cap_bytes),
+                                       C.byref(opts), C.byref(h)))
+        return MultiResVoxelMap(h)
+
+    def min_resolution(self):
+        return self._r
+
+    def max_level(self):
+        return self._max_level
+
+    def bbox(self):
+        b = Aabb()
+        _check(lib.bbs_map_bbox(self._h, C.byref(b)))
+        return (b.min.x, b.min.y, b.min.z), (b.max.x, b.max.y, b.max.z)
+
+    def level(self, l):
+        return self._levels[l]
+
+    def levels(self):
+        return list(self._levels)
+
+    def build_ms(self):
+        out = C.c_double()
+        _check(lib.bbs_map_build_ms(self._h, C.byref(out)))
+        return out.value
+
+
+class DeviceScan:
+    """A scan uploaded once to the map's GPU (SoA doubles in HBM)."""
+
+    def __init__(self, vmap: MultiResVoxelMap, scan):
+        a = _xyz(scan)
+        self._map = vmap
+        self.k = a.shape[0]
+        self._h = C.c_void_p()
+        _check(lib.bbs_scan_upload(vmap._h, _dptr(a), a.shape[0], C.byref(self._h)))
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            lib.bbs_scan_free(h)
+            self._h = None
+
+
+# ---- search (search.hpp, pipeline.hpp) --------------------------------------
+def batch_evaluate(nodes, vmap: MultiResVoxelMap, scan, grids: AngularGrid, workers=1):
+    """search.hpp:23-34.  Returns the nodes (n, 8) int32 with scores filled;
+    a writable contiguous int32 (n, 8) input is also updated in place."""
+    arr = _nodes_array(nodes)
+    s = _xyz(scan)
+    c = grids.cfg.to_c()
+    if arr.shape[0]:
+        _check(lib.bbs_batch_evaluate(vmap._h, _dptr(s), s.shape[0], C.byref(c), grids.d_max,
+                                      arr.ctypes.data_as(C.POINTER(Node)), arr.shape[0]))
+    if isinstance(nodes, np.ndarray) and nodes.dtype == np.int32 and nodes.flags.c_contiguous \
+            and nodes.shape == arr.shape and nodes is not arr:
+        nodes[...] = arr
+    return arr
+
+
+def search(vmap: MultiResVoxelMap, scan, cfg: SearchConfig, trace_capacity=1 << 16):
+    """search.hpp:72-186 (host scan buffer in, result out)."""
+    s = _xyz(scan)
+    res, buf = _new_result(trace_capacity if cfg.collect_trace else 0)
+    c = cfg.to_c()
+    _check(lib.bbs_search(vmap._h, _dptr(s), s.shape[0], C.byref(c), C.byref(res)))
+    return _result_from_c(res, buf)
+
+
+def search_scan(vmap: MultiResVoxelMap, dscan: DeviceScan, cfg: SearchConfig,
+                trace_capacity=1 << 16):
+    """search() on a device-resident scan (no host copy inside the call)."""
+    res, buf = _new_result(trace_capacity if cfg.collect_trace else 0)
+    c = cfg.to_c()
+    _check(lib.bbs_search_scan(vmap._h, dscan._h, C.byref(c), C.byref(res)))
+    return _result_from_c(res, buf)
+
+
+def search_sharded(vmap: MultiResVoxelMap, dscan: DeviceScan, cfg: SearchConfig, rank, world,
+                   allreduce_max, trace_capacity=1 << 16):
+    """Root-sharded search.  allreduce_max(list_of_int64) ->
+    element-wise max over ranks (e.g. torch.distributed all_reduce MAX)."""
+    def _cb(values, count, _user):
+        try:
+            vals = [values[i] for i in range(count)]
+            out = allreduce_max(vals)
+            for i in range(count):
+                values[i] = int(out[i])
+            return 0
+        except Exception:  # noqa: BLE001 - reported through the status code
+            return 1
+
+    cb = _abi.ALLREDUCE_MAX_FN(_cb)
+    shard = Shard(int(rank), int(world), cb, None)
+    res, buf = _new_result(trace_capacity if cfg.collect_trace else 0)
+    c = cfg.to_c()
+    _check(lib.bbs_search_sharded(vmap._h, dscan._h, C.byref(c), C.byref(shard), C.byref(res)))
+    return _result_from_c(res, buf)
+
+
+def localize_scan(vmap: MultiResVoxelMap, raw_scan, cfg: SearchConfig, downsample_target,
+                  trace_capacity=1 << 16):
+    """pipeline.hpp:45-51."""
+    s = _xyz(raw_scan)
+    res, buf = _new_result(trace_capacity if cfg.collect_trace else 0)
+    c = cfg.to_c()
+    _check(lib.bbs_localize_scan(vmap._h, _dptr(s), s.shape[0], C.byref(c), int(downsample_target),
+                                 C.byref(res)))
+    return _result_from_c(res, buf)
+
+
+# ---- synthetic inputs (scene.hpp restatement; harness, not the path) -------
+class SceneSpec(C.Structure):
+    """SceneSpec, scene.hpp:21-38 (defaults from bbs_scene_spec_default)."""
+    _fields_ = [
+        ("size_x", C.c_double), ("size_y", C.c_double), ("size_z", C.c_double),
+        ("num_boxes", C.c_int32),
+        ("min_box_side", C.c_double), ("max_box_side", C.c_double),
+        ("min_box_height", C.c_double),
+        ("map_spacing", C.c_double), ("scan_spacing", C.c_double),
+        ("scan_range", C.c_double), ("point_jitter", C.c_double),
+        ("tilt_noise", C.c_int32),
+        ("gt_yaw_min", C.c_double), ("gt_yaw_max", C.c_double),
+        ("min_scan_points", C.c_uint64),
+        ("feasibility_resolution", C.c_double),
+    ]
+
+    @staticmethod
+    def default(**kw):
+        s = SceneSpec()
+        lib.bbs_scene_spec_default(C.byref(s))
+        for k, v in kw.items():
+            setattr(s, k, v)
+        return s
+
+
+def gen_scene(spec: SceneSpec, seed):
+    """scene.hpp:156-220 -> (map (n,3), scan (k,3), gt Pose6)."""
+    mp, sp = C.POINTER(C.c_double)(), C.POINTER(C.c_double)()
+    nm, ns = C.c_uint64(), C.c_uint64()
+    gt = (C.c_double * 6)()
+    _check(lib.bbs_gen_scene(C.byref(spec), int(seed), C.byref(mp), C.byref(nm), C.byref(sp),
+                             C.byref(ns), gt), lib.bbs_scene_last_error)
+    m = np.ctypeslib.as_array(mp, shape=(nm.value, 3)).copy()
+    s = np.ctypeslib.as_array(sp, shape=(ns.value, 3)).copy()
+    lib.bbs_free(C.cast(mp, C.c_void_p))
+    lib.bbs_free(C.cast(sp, C.c_void_p))
+    return m, s, Pose6(*gt)
+
+
+def gen_scans(spec: SceneSpec, seed, pose_seed_base, n_scans):
+    """Extra scans of seed's map (C4 helper) -> (list of (k,3), list of Pose6)."""
+    sp = C.POINTER(C.c_double)()
+    offs = (C.c_uint64 * (n_scans + 1))()
+    gt = (C.c_double * (6 * max(n_scans, 1)))()
+    _check(lib.bbs_gen_scans(C.byref(spec), int(seed), int(pose_seed_base), int(n_scans),
+                             C.byref(sp), offs, gt), lib.bbs_scene_last_error)
+    allp = np.ctypeslib.as_array(sp, shape=(max(offs[n_scans], 1), 3)).copy()
+    lib.bbs_free(C.cast(sp, C.c_void_p))
+    scans = [allp[offs[j]:offs[j + 1]].copy() for j in range(n_scans)]
+    poses = [Pose6(*gt[6 * j:6 * j + 6]) for j in range(n_scans)]
+    return scans, poses
+
+
+def cut_scan(scan, k, seed):
+    """First k points of a Fisher-Yates shuffle driven by Rng(seed)."""
+    a = _xyz(scan)
+    k = int(k)
+    out = np.zeros((k, 3))
+    _check(lib.bbs_cut_scan(_dptr(a), a.shape[0], k, int(seed), _dptr(out)))
+    return out

@@ -1,0 +1,86 @@
+"""Loads libbbs_b200.so (the C-ABI of include/bbs.h) and declares signatures.
+
+The library is built in-tree by ``make -C paper_2310_10023_b200/csrc``
+(``__graft_entry__.build()``).  There is no fallback: importing the package
+without the library raises, and every compute entry point fails loudly
+(BBS_ERR_CUDA) when no GPU is present.
+"""
+import ctypes as C
+import os
+
+from ._abi import (
+    Aabb, AxisGridC, LevelInfo, MapOptions, Node, SearchConfigC, SearchResultC, Shard,
+)
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libbbs_b200.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(
+        f"{LIB_PATH} is missing: build it with `make -C {HERE}/csrc` "
+        "(or __graft_entry__.build()); the B200 path has no Python/CPU fallback")
+
+lib = C.CDLL(LIB_PATH)
+
+_d = C.c_double
+_u64 = C.c_uint64
+_i32 = C.c_int32
+_vp = C.c_void_p
+_dp = C.POINTER(C.c_double)
+_ip = C.POINTER(C.c_int32)
+
+SIGNATURES = {
+    # name: (restype, argtypes)
+    "bbs_last_error": (C.c_char_p, []),
+    "bbs_abi_version": (C.c_int, []),
+    "bbs_device_count": (C.c_int, []),
+    "bbs_search_config_default": (None, [C.POINTER(SearchConfigC)]),
+    "bbs_angular_grid": (C.c_int, [C.POINTER(SearchConfigC), _d, C.POINTER(AxisGridC), _u64]),
+    "bbs_angular_divisions": (C.c_int, [C.POINTER(SearchConfigC), _d, _i32, _i32, _ip]),
+    "bbs_max_range": (C.c_int, [_dp, _u64, _dp]),
+    "bbs_bounding_box": (C.c_int, [_dp, _u64, C.POINTER(Aabb)]),
+    "bbs_prepare_source": (C.c_int, [_dp, _u64, _u64, _dp, _u64, C.POINTER(_u64), _dp, _ip, _dp]),
+    "bbs_initial_node_count": (C.c_int, [C.POINTER(SearchConfigC), _d, C.POINTER(Aabb),
+                                         C.POINTER(_u64)]),
+    "bbs_map_build": (C.c_int, [_dp, _u64, _d, _i32, _d, _u64, C.POINTER(MapOptions),
+                                C.POINTER(_vp)]),
+    "bbs_map_from_levels": (C.c_int, [C.POINTER(_ip), C.POINTER(_u64), _i32, _d, C.POINTER(Aabb),
+                                      _d, _u64, C.POINTER(MapOptions), C.POINTER(_vp)]),
+    "bbs_map_free": (C.c_int, [_vp]),
+    "bbs_map_min_resolution": (C.c_int, [_vp, _dp]),
+    "bbs_map_max_level": (C.c_int, [_vp, _ip]),
+    "bbs_map_bbox": (C.c_int, [_vp, C.POINTER(Aabb)]),
+    "bbs_map_build_ms": (C.c_int, [_vp, _dp]),
+    "bbs_map_level_info": (C.c_int, [_vp, _i32, C.POINTER(LevelInfo)]),
+    "bbs_level_occupied": (C.c_int, [_vp, _i32, _ip, _u64, C.POINTER(_u64)]),
+    "bbs_level_contains": (C.c_int, [_vp, _i32, _ip, _u64, C.POINTER(C.c_uint8)]),
+    "bbs_level_score": (C.c_int, [_vp, _i32, _dp, _dp, _dp, _u64, _ip]),
+    "bbs_batch_evaluate": (C.c_int, [_vp, _dp, _u64, C.POINTER(SearchConfigC), _d,
+                                     C.POINTER(Node), _u64]),
+    "bbs_search": (C.c_int, [_vp, _dp, _u64, C.POINTER(SearchConfigC), C.POINTER(SearchResultC)]),
+    "bbs_localize_scan": (C.c_int, [_vp, _dp, _u64, C.POINTER(SearchConfigC), _u64,
+                                    C.POINTER(SearchResultC)]),
+    "bbs_scan_upload": (C.c_int, [_vp, _dp, _u64, C.POINTER(_vp)]),
+    "bbs_scan_free": (C.c_int, [_vp]),
+    "bbs_search_scan": (C.c_int, [_vp, _vp, C.POINTER(SearchConfigC), C.POINTER(SearchResultC)]),
+    "bbs_batch_evaluate_device": (C.c_int, [_vp, _vp, C.POINTER(SearchConfigC), _d, _vp, _u64,
+                                            _vp]),
+    "bbs_search_sharded": (C.c_int, [_vp, _vp, C.POINTER(SearchConfigC), C.POINTER(Shard),
+                                     C.POINTER(SearchResultC)]),
+    "bbs_scene_spec_default": (None, [_vp]),
+    "bbs_gen_scene": (C.c_int, [_vp, _u64, C.POINTER(_dp), C.POINTER(_u64), C.POINTER(_dp),
+                                C.POINTER(_u64), _dp]),
+    "bbs_gen_scans": (C.c_int, [_vp, _u64, _u64, _i32, C.POINTER(_dp), C.POINTER(_u64), _dp]),
+    "bbs_cut_scan": (C.c_int, [_dp, _u64, _u64, _u64, _dp]),
+    "bbs_scene_last_error": (C.c_char_p, []),
+    "bbs_free": (None, [_vp]),
+}
+
+for _name, (_res, _args) in SIGNATURES.items():
+    _f = getattr(lib, _name)
+    _f.restype = _res
+    _f.argtypes = _args
+
+
+def exported_symbols():
+    return sorted(SIGNATURES)

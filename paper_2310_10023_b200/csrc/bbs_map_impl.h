@@ -1,0 +1,61 @@
+// bbs_map_impl.h — host-side handles behind bbs_map_t / bbs_scan_t.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <vector>
+
+#include "bbs_internal.h"
+
+struct bbs_map {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  double r = 1.0;
+  int max_level = 0;
+  bbs_aabb bbox{};
+  double collision_target = 0.001;
+  uint64_t memory_cap = 0;
+  int layout_pref = BBS_LAYOUT_AUTO;
+  struct Level {
+    bbs_level_info info{};
+    unsigned long long* keys = nullptr;  // sorted unique packed keys (x-major)
+    uint64_t n_keys = 0;
+    uint32_t bits[3] = {0, 0, 0};
+    void* structure = nullptr;           // bitmap words or hash slots
+  };
+  std::vector<Level> levels;
+  bbs::MapView view{};
+  double build_ms = 0.0;
+  ~bbs_map();
+};
+
+struct bbs_scan {
+  bbs_map* map = nullptr;
+  uint64_t k = 0;
+  double d_max = 0.0;          // max_range of the scan (host libm)
+  double* soa = nullptr;       // device: x[k], y[k], z[k]
+  std::vector<double> host;    // the scan as given (AoS)
+  ~bbs_scan();
+};
+
+namespace bbs {
+
+// Device map construction (map_build.cu).
+void build_map_from_points(bbs_map* m, const double* xyz, uint64_t n);
+void build_map_from_levels(bbs_map* m, const int32_t* const* lv, const uint64_t* counts,
+                           int n_levels);
+void level_occupied(bbs_map* m, int level, int32_t* xyz, uint64_t cap, uint64_t* count);
+void level_contains(bbs_map* m, int level, const int32_t* xyz, uint64_t n, uint8_t* out);
+void level_score_transform(bbs_map* m, int level, const double* R, const double* t,
+                           const double* scan, uint64_t k, int32_t* score);
+
+// Scans (search.cu).
+bbs_scan* upload_scan(bbs_map* m, const double* xyz, uint64_t k);
+
+struct DeviceGuard {
+  int prev = 0;
+  explicit DeviceGuard(int dev);
+  ~DeviceGuard();
+};
+
+}  // namespace bbs

@@ -1,0 +1,402 @@
+// capi.cpp — the extern "C" boundary (include/bbs.h).  Every entry point
+// validates on the host in the reference's order, maps bbs::Error to a
+// status code, and keeps the message for bbs_last_error().
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <limits>
+#include <memory>
+#include <new>
+#include <string>
+
+#include "bbs_map_impl.h"
+
+namespace bbs {
+void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const bbs_shard* shard,
+                bbs_search_result* out);
+void batch_evaluate_device(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, double d_max,
+                           bbs_node* d_nodes, uint64_t n, cudaStream_t s, const int32_t* lo,
+                           const int32_t* hi);
+void set_pool_retention(int device);
+}  // namespace bbs
+
+namespace {
+
+thread_local std::string g_err;
+
+template <typename Fn>
+int guard(Fn&& fn) {
+  try {
+    fn();
+    return BBS_OK;
+  } catch (const bbs::Error& e) {
+    g_err = e.what();
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    g_err = "out of host memory";
+    return BBS_ERR_GENERIC;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return BBS_ERR_GENERIC;
+  }
+}
+
+#define REQUIRE(cond, what)                                              \
+  do {                                                                   \
+    if (!(cond)) throw bbs::Error(BBS_ERR_INVALID_ARGUMENT, what);       \
+  } while (0)
+
+void require_device(int device) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+    cudaGetLastError();
+    throw bbs::Error(BBS_ERR_CUDA, "no CUDA device available (the B200 path has no CPU fallback)");
+  }
+  if (device < 0 || device >= n) throw bbs::Error(BBS_ERR_CUDA, "CUDA device ordinal out of range");
+}
+
+bbs_map* new_map(const bbs_map_options* opts, double r, uint64_t cap, double ct) {
+  const int device = opts ? opts->device : 0;
+  require_device(device);
+  std::unique_ptr<bbs_map> m(new bbs_map());
+  m->device = device;
+  m->r = r;
+  m->memory_cap = cap;
+  m->collision_target = ct;
+  m->layout_pref = opts ? opts->layout : BBS_LAYOUT_AUTO;
+  if (m->layout_pref < BBS_LAYOUT_AUTO || m->layout_pref > BBS_LAYOUT_HASH)
+    throw bbs::Error(BBS_ERR_CONFIG, "map: unknown layout");
+  bbs::DeviceGuard g(device);
+  bbs::set_pool_retention(device);
+  BBS_CUDA(cudaStreamCreateWithFlags(&m->stream, cudaStreamNonBlocking));
+  return m.release();
+}
+
+void check_level(const bbs_map* m, int32_t level) {
+  if (level < 0 || level >= static_cast<int32_t>(m->levels.size()))
+    throw bbs::Error(BBS_ERR_CONFIG, "level out of range");
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* bbs_last_error(void) { return g_err.c_str(); }
+int bbs_abi_version(void) { return BBS_ABI_VERSION; }
+
+int bbs_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+void bbs_search_config_default(bbs_search_config* c) {
+  if (!c) return;
+  std::memset(c, 0, sizeof(*c));
+  c->min_resolution = 1.0;
+  c->max_level = 6;
+  c->roll_pitch_half_range = 0.02;
+  c->yaw_min = 0.0;
+  c->yaw_max = 6.283185307179586476925286766559;
+  c->score_threshold_fraction = 0.95;
+  c->batch_size = 10000;
+  c->strategy = BBS_STRATEGY_BFS;
+  c->branch_mode = BBS_BRANCH_ROTO_TRANS;
+  c->workers = 1;
+}
+
+int bbs_angular_grid(const bbs_search_config* cfg, double d_max, bbs_axis_grid* out,
+                     uint64_t capacity) {
+  return guard([&] {
+    REQUIRE(cfg && out, "bbs_angular_grid: null argument");
+    const bbs::HostGrid g = bbs::make_grid(*cfg, d_max);
+    const uint64_t n = 3ull * static_cast<uint64_t>(cfg->max_level + 1);
+    REQUIRE(capacity >= n, "bbs_angular_grid: capacity below 3*(max_level+1)");
+    for (uint64_t i = 0; i < n; ++i) {
+      const bbs::AxisGrid& a = g.axes[i];
+      out[i] = {a.w_min, a.w_max, a.step, a.segments, a.periodic ? 1 : 0};
+    }
+  });
+}
+
+int bbs_angular_divisions(const bbs_search_config* cfg, double d_max, int32_t axis, int32_t level,
+                          int32_t* out) {
+  return guard([&] {
+    REQUIRE(cfg && out, "bbs_angular_divisions: null argument");
+    REQUIRE(axis >= 0 && axis < 3 && level >= 1 && level <= cfg->max_level,
+            "bbs_angular_divisions: axis/level out of range");
+    *out = bbs::make_grid(*cfg, d_max).divisions(axis, level);
+  });
+}
+
+int bbs_max_range(const double* xyz, uint64_t n, double* out) {
+  return guard([&] {
+    REQUIRE(out && (xyz || n == 0), "bbs_max_range: null argument");
+    *out = bbs::host_max_range(xyz, n);
+  });
+}
+
+int bbs_bounding_box(const double* xyz, uint64_t n, bbs_aabb* out) {
+  return guard([&] {
+    REQUIRE(out && (xyz || n == 0), "bbs_bounding_box: null argument");
+    *out = bbs::host_bounding_box(xyz, n);
+  });
+}
+
+int bbs_prepare_source(const double* xyz, uint64_t n, uint64_t target, double* out_xyz,
+                       uint64_t capacity, uint64_t* count, double* leaf, int32_t* converged,
+                       double* d_max) {
+  return guard([&] {
+    REQUIRE(count && (xyz || n == 0), "bbs_prepare_source: null argument");
+    const bbs::SourcePrep p = bbs::host_prepare_source(xyz, n, target);
+    const uint64_t m = p.xyz.size() / 3;
+    *count = m;
+    if (out_xyz) std::memcpy(out_xyz, p.xyz.data(), 3 * std::min(m, capacity) * sizeof(double));
+    if (leaf) *leaf = p.leaf;
+    if (converged) *converged = p.converged ? 1 : 0;
+    if (d_max) *d_max = p.d_max;
+  });
+}
+
+int bbs_initial_node_count(const bbs_search_config* cfg, double d_max, const bbs_aabb* range,
+                           uint64_t* count) {
+  return guard([&] {
+    REQUIRE(cfg && range && count, "bbs_initial_node_count: null argument");
+    const bbs::HostGrid g = bbs::make_grid(*cfg, d_max);
+    const int L = cfg->max_level;
+    const double cell = std::ldexp(cfg->min_resolution, L);
+    auto cnt = [&](double lo, double hi) {
+      const double f = std::floor(lo / cell), c = std::ceil(hi / cell);
+      const int64_t a = (f >= -2147483648.0 && f < 2147483648.0) ? static_cast<int32_t>(f) : INT32_MIN;
+      const int64_t b = (c >= -2147483648.0 && c < 2147483648.0) ? static_cast<int32_t>(c) : INT32_MIN;
+      return b - a + 1;
+    };
+    const int64_t total = cnt(range->min.x, range->max.x) * cnt(range->min.y, range->max.y) *
+                          cnt(range->min.z, range->max.z) * g.axis(0, L).index_count() *
+                          g.axis(1, L).index_count() * g.axis(2, L).index_count();
+    if (total <= 0) throw bbs::Error(BBS_ERR_EMPTY_SEARCH_SPACE, "initial node set is empty");
+    *count = static_cast<uint64_t>(total);
+  });
+}
+
+int bbs_map_build(const double* xyz, uint64_t n, double min_resolution, int32_t max_level,
+                  double collision_target, uint64_t memory_cap_bytes, const bbs_map_options* opts,
+                  bbs_map_t* out) {
+  return guard([&] {
+    REQUIRE(out && (xyz || n == 0), "bbs_map_build: null argument");
+    *out = nullptr;
+    // voxel_map.hpp:230-233, same order and messages
+    if (n == 0) throw bbs::Error(BBS_ERR_EMPTY_CLOUD, "MultiResVoxelMap: empty map");
+    if (max_level < 1) throw bbs::Error(BBS_ERR_CONFIG, "MultiResVoxelMap: max_level must be >= 1");
+    if (!(min_resolution > 0.0))
+      throw bbs::Error(BBS_ERR_CONFIG, "MultiResVoxelMap: min_resolution must be > 0");
+    if (max_level >= bbs::kMaxLevels)
+      throw bbs::Error(BBS_ERR_CONFIG, "MultiResVoxelMap: max_level above 15 is not supported");
+    std::unique_ptr<bbs_map> m(new_map(opts, min_resolution, memory_cap_bytes, collision_target));
+    m->max_level = max_level;
+    m->bbox = bbs::host_bounding_box(xyz, n);
+    bbs::build_map_from_points(m.get(), xyz, n);
+    *out = m.release();
+  });
+}
+
+int bbs_map_from_levels(const int32_t* const* level_voxels, const uint64_t* counts, int32_t n_levels,
+                        double min_resolution, const bbs_aabb* bbox, double collision_target,
+                        uint64_t memory_cap_bytes, const bbs_map_options* opts, bbs_map_t* out) {
+  return guard([&] {
+    REQUIRE(out && bbox && (n_levels <= 0 || (level_voxels && counts)),
+            "bbs_map_from_levels: null argument");
+    *out = nullptr;
+    if (n_levels < 2) throw bbs::Error(BBS_ERR_FORMAT, "map must have at least 2 levels");
+    if (n_levels > bbs::kMaxLevels)
+      throw bbs::Error(BBS_ERR_CONFIG, "map: more than 16 levels are not supported");
+    std::unique_ptr<bbs_map> m(new_map(opts, min_resolution, memory_cap_bytes, collision_target));
+    m->max_level = n_levels - 1;
+    m->bbox = *bbox;
+    bbs::build_map_from_levels(m.get(), level_voxels, counts, n_levels);
+    *out = m.release();
+  });
+}
+
+int bbs_map_free(bbs_map_t map) {
+  return guard([&] { delete map; });
+}
+
+int bbs_map_min_resolution(bbs_map_t map, double* out) {
+  return guard([&] {
+    REQUIRE(map && out, "null argument");
+    *out = map->r;
+  });
+}
+int bbs_map_max_level(bbs_map_t map, int32_t* out) {
+  return guard([&] {
+    REQUIRE(map && out, "null argument");
+    *out = map->max_level;
+  });
+}
+int bbs_map_bbox(bbs_map_t map, bbs_aabb* out) {
+  return guard([&] {
+    REQUIRE(map && out, "null argument");
+    *out = map->bbox;
+  });
+}
+int bbs_map_build_ms(bbs_map_t map, double* out) {
+  return guard([&] {
+    REQUIRE(map && out, "null argument");
+    *out = map->build_ms;
+  });
+}
+int bbs_map_level_info(bbs_map_t map, int32_t level, bbs_level_info* out) {
+  return guard([&] {
+    REQUIRE(map && out, "null argument");
+    check_level(map, level);
+    *out = map->levels[static_cast<size_t>(level)].info;
+  });
+}
+
+int bbs_level_occupied(bbs_map_t map, int32_t level, int32_t* xyz, uint64_t capacity,
+                       uint64_t* count) {
+  return guard([&] {
+    REQUIRE(map && count, "null argument");
+    check_level(map, level);
+    bbs::level_occupied(map, level, xyz, xyz ? capacity : 0, count);
+  });
+}
+
+int bbs_level_contains(bbs_map_t map, int32_t level, const int32_t* xyz, uint64_t n, uint8_t* out) {
+  return guard([&] {
+    REQUIRE(map && (n == 0 || (xyz && out)), "null argument");
+    check_level(map, level);
+    bbs::level_contains(map, level, xyz, n, out);
+  });
+}
+
+int bbs_level_score(bbs_map_t map, int32_t level, const double rotation[9],
+                    const double translation[3], const double* scan_xyz, uint64_t k, int32_t* score) {
+  return guard([&] {
+    REQUIRE(map && rotation && translation && score && (scan_xyz || k == 0), "null argument");
+    check_level(map, level);
+    bbs::level_score_transform(map, level, rotation, translation, scan_xyz, k, score);
+  });
+}
+
+int bbs_scan_upload(bbs_map_t map, const double* xyz, uint64_t k, bbs_scan_t* out) {
+  return guard([&] {
+    REQUIRE(map && out && (xyz || k == 0), "null argument");
+    *out = bbs::upload_scan(map, xyz, k);
+  });
+}
+
+int bbs_scan_free(bbs_scan_t scan) {
+  return guard([&] { delete scan; });
+}
+
+int bbs_search_scan(bbs_map_t map, bbs_scan_t scan, const bbs_search_config* cfg,
+                    bbs_search_result* result) {
+  return guard([&] {
+    REQUIRE(map && scan && cfg && result, "null argument");
+    REQUIRE(scan->map == map, "scan was uploaded for a different map");
+    bbs::run_search(map, scan, *cfg, nullptr, result);
+  });
+}
+
+int bbs_search_sharded(bbs_map_t map, bbs_scan_t scan, const bbs_search_config* cfg,
+                       const bbs_shard* shard, bbs_search_result* result) {
+  return guard([&] {
+    REQUIRE(map && scan && cfg && result && shard, "null argument");
+    REQUIRE(scan->map == map, "scan was uploaded for a different map");
+    bbs::run_search(map, scan, *cfg, shard, result);
+  });
+}
+
+int bbs_search(bbs_map_t map, const double* scan_xyz, uint64_t k, const bbs_search_config* cfg,
+               bbs_search_result* result) {
+  return guard([&] {
+    REQUIRE(map && cfg && result && (scan_xyz || k == 0), "null argument");
+    if (k == 0) throw bbs::Error(BBS_ERR_DEGENERATE_SCAN, "search: empty scan");
+    std::unique_ptr<bbs_scan> sc(bbs::upload_scan(map, scan_xyz, k));
+    bbs::run_search(map, sc.get(), *cfg, nullptr, result);
+  });
+}
+
+int bbs_localize_scan(bbs_map_t map, const double* raw_xyz, uint64_t n, const bbs_search_config* cfg,
+                      uint64_t downsample_target, bbs_search_result* result) {
+  return guard([&] {
+    REQUIRE(map && cfg && result && (raw_xyz || n == 0), "null argument");
+    // prepare_source, pipeline.hpp:25-41 (host), then search (pipeline.hpp:48)
+    const auto t0 = std::chrono::steady_clock::now();
+    const bbs::SourcePrep prep = bbs::host_prepare_source(raw_xyz, n, downsample_target);
+    const double prep_ms =
+        std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    const uint64_t k = prep.xyz.size() / 3;
+    std::unique_ptr<bbs_scan> sc(bbs::upload_scan(map, prep.xyz.data(), k));
+    bbs::run_search(map, sc.get(), *cfg, nullptr, result);
+    result->stats.set_source_ms = prep_ms;
+  });
+}
+
+int bbs_batch_evaluate(bbs_map_t map, const double* scan_xyz, uint64_t k,
+                       const bbs_search_config* cfg, double d_max, bbs_node* nodes, uint64_t n) {
+  return guard([&] {
+    REQUIRE(map && cfg && (scan_xyz || k == 0) && (nodes || n == 0), "null argument");
+    if (n == 0) return;  // parallel_chunks(0, ...) is a no-op (parallel.hpp:17)
+    // index ranges the LUT must cover, per (level, axis)
+    int32_t lo[bbs::kMaxLevels * 3], hi[bbs::kMaxLevels * 3];
+    for (int i = 0; i < bbs::kMaxLevels * 3; ++i) {
+      lo[i] = std::numeric_limits<int32_t>::max();
+      hi[i] = std::numeric_limits<int32_t>::min();
+    }
+    for (uint64_t i = 0; i < n; ++i) {
+      const bbs_node& nd = nodes[i];
+      if (nd.level < 0 || nd.level > map->max_level || nd.level > cfg->max_level)
+        throw bbs::Error(BBS_ERR_CONFIG, "batch_evaluate: node level outside the map / grid levels");
+      const int32_t idx[3] = {nd.iroll, nd.ipitch, nd.iyaw};
+      for (int a = 0; a < 3; ++a) {
+        lo[nd.level * 3 + a] = std::min(lo[nd.level * 3 + a], idx[a]);
+        hi[nd.level * 3 + a] = std::max(hi[nd.level * 3 + a], idx[a]);
+      }
+    }
+    for (int i = 0; i < bbs::kMaxLevels * 3; ++i) {
+      if (lo[i] > hi[i]) {
+        lo[i] = 0;
+        hi[i] = 0;
+      }
+      if (static_cast<int64_t>(hi[i]) - std::min<int64_t>(lo[i], 0) >= (1 << 20))
+        throw bbs::Error(BBS_ERR_TOO_LARGE, "batch_evaluate: rotation index span above 2^20");
+    }
+    std::unique_ptr<bbs_scan> sc(bbs::upload_scan(map, scan_xyz, k));
+    if (k == 0) {
+      for (uint64_t i = 0; i < n; ++i) nodes[i].score = 0;  // empty scan scores 0
+      return;
+    }
+    bbs::DeviceGuard g(map->device);
+    cudaStream_t s = map->stream;
+    bbs_node* d_nodes = nullptr;
+    BBS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_nodes), n * sizeof(bbs_node), s));
+    BBS_CUDA(cudaMemcpyAsync(d_nodes, nodes, n * sizeof(bbs_node), cudaMemcpyHostToDevice, s));
+    bbs::batch_evaluate_device(map, sc.get(), *cfg, d_max, d_nodes, n, s, lo, hi);
+    BBS_CUDA(cudaMemcpyAsync(nodes, d_nodes, n * sizeof(bbs_node), cudaMemcpyDeviceToHost, s));
+    BBS_CUDA(cudaFreeAsync(d_nodes, s));
+    BBS_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+int bbs_batch_evaluate_device(bbs_map_t map, bbs_scan_t scan, const bbs_search_config* cfg,
+                              double d_max, bbs_node* d_nodes, uint64_t n, void* stream) {
+  return guard([&] {
+    REQUIRE(map && scan && cfg && (d_nodes || n == 0), "null argument");
+    if (n == 0) return;
+    if (scan->k == 0) throw bbs::Error(BBS_ERR_DEGENERATE_SCAN, "batch_evaluate: empty scan");
+    bbs::DeviceGuard g(map->device);
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : map->stream;
+    bbs::batch_evaluate_device(map, scan, *cfg, d_max, d_nodes, n, s, nullptr, nullptr);
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,71 @@
+// device_common.cuh — device helpers shared by the map build, score and
+// frontier kernels.  Everything here is sm_100a device code; the .cu files
+// are compiled with --fmad=false and use explicit _rn intrinsics on the
+// bit-exact path, so no FMA contraction can change a rounding
+// (SURVEY §7 "Bit-exact FP64 hit counts").
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "bbs_internal.h"
+
+namespace bbs {
+
+// voxel_index, point_cloud.hpp:38-40: (int32)floor(c / cell) with IEEE
+// division; the reference's x86 cvttsd2si gives INT32_MIN for NaN and values
+// outside [-2^31, 2^31), which cvt.rzi.s32.f64 would saturate instead.
+__device__ __forceinline__ int32_t dev_voxel_index(double c, double cell) {
+  const double f = floor(__ddiv_rn(c, cell));
+  return (f >= -2147483648.0 && f < 2147483648.0) ? static_cast<int32_t>(f) : INT32_MIN;
+}
+
+__device__ __forceinline__ uint64_t hash_bucket(unsigned long long key, uint32_t shift) {
+  // multiplicative (Fibonacci) hashing on the packed key
+  return (key * 0x9E3779B97F4A7C15ull) >> shift;
+}
+
+__device__ __forceinline__ unsigned long long pack_key(uint32_t ux, uint32_t uy, uint32_t uz,
+                                                       uint32_t by, uint32_t bz) {
+  return (static_cast<unsigned long long>(ux) << (by + bz)) |
+         (static_cast<unsigned long long>(uy) << bz) | static_cast<unsigned long long>(uz);
+}
+
+// Bitmap addressing: 8x8x4 bricks of 256 bits = one 32-byte sector.
+__device__ __forceinline__ uint32_t bitmap_word(const LevelView& L, uint32_t ux, uint32_t uy,
+                                                uint32_t uz) {
+  const uint32_t brick = ((uz >> 2) * L.nby + (uy >> 3)) * L.nbx + (ux >> 3);
+  return brick * 8u + (uz & 3u) * 2u + ((uy >> 2) & 1u);
+}
+__device__ __forceinline__ uint32_t bitmap_bit(uint32_t ux, uint32_t uy) {
+  return ((uy & 3u) << 3) | (ux & 7u);
+}
+
+// LevelMap::contains, voxel_map.hpp:127-135 — set membership on the
+// device layout.  Voxels outside the level's box are misses without a load.
+__device__ __forceinline__ bool level_contains(const LevelView& L, int32_t x, int32_t y,
+                                               int32_t z) {
+  const uint32_t ux = static_cast<uint32_t>(x) - static_cast<uint32_t>(L.box_min[0]);
+  const uint32_t uy = static_cast<uint32_t>(y) - static_cast<uint32_t>(L.box_min[1]);
+  const uint32_t uz = static_cast<uint32_t>(z) - static_cast<uint32_t>(L.box_min[2]);
+  if (ux >= L.dim[0] || uy >= L.dim[1] || uz >= L.dim[2]) return false;
+  if (L.layout == BBS_LAYOUT_BITMAP) {
+    const uint32_t w = __ldg(&L.words[bitmap_word(L, ux, uy, uz)]);
+    return (w >> bitmap_bit(ux, uy)) & 1u;
+  }
+  const unsigned long long key = pack_key(ux, uy, uz, L.bits_y, L.bits_z);
+  uint64_t b = hash_bucket(key, L.bucket_shift);
+  for (;;) {
+    // one 32-byte sector per bucket; inserts fill a bucket's slots in order,
+    // so an empty last slot ends the probe sequence
+    const ulonglong2* p = reinterpret_cast<const ulonglong2*>(L.slots + 4 * b);
+    const ulonglong2 s0 = __ldg(p);
+    const ulonglong2 s1 = __ldg(p + 1);
+    if (s0.x == key || s0.y == key || s1.x == key || s1.y == key) return true;
+    if (s1.y == ~0ull) return false;
+    b = (b + 1) & L.bucket_mask;
+  }
+}
+
+}  // namespace bbs

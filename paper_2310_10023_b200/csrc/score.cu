@@ -1,0 +1,503 @@
+// score.cu — K4: the candidate score kernels (batch_evaluate,
+// search.hpp:23-34, over LevelMap::score, voxel_map.hpp:142-154).
+//
+// Exactness.  The reference computes, per (node, scan point),
+//   q = ((r0*px + r1*py) + r2*pz) + t        (voxel_map.hpp:148-150)
+//   v = (int32)floor(q / cell)                (point_cloud.hpp:39)
+// with R from pose_to_transform (geometry.hpp:107-109) and t = cell*ix
+// (nodes.hpp:35-37).  All products/sums here use __dmul_rn/__dadd_rn in that
+// order (no FMA; the TU is also built with --fmad=false), cos/sin come from a
+// host-libm LUT, and the division is IEEE (__ddiv_rn).
+//
+// Speed.  The rotated point rp = R*p depends only on (rotation, point), and
+// the translation is added last, so all nodes that share a rotation share
+// rp.  For such a group the kernel computes w = rp * (1/cell) once per point
+// and takes floor(q / cell) = floor(w) + ix whenever frac(w) is farther than
+// eps = 2^-48 * (|w| + max|ix| + 2) from an integer.  The reference's value
+// differs from w + ix by at most ~4u(|w| + |ix|) (u = 2^-53; derivation in
+// DESIGN.md §K4), so the integer shortcut is exact; points within eps of a
+// voxel boundary ("ambiguous", ~1e-12 of them) take the exact per-node
+// divide.  A lookup is then 3 integer adds plus one membership probe.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+
+#include "device_common.cuh"
+#include "kernels.h"
+
+namespace bbs {
+
+namespace {
+
+// pose_to_transform, geometry.hpp:107-109, on LUT cos/sin (geometry.hpp:103-105).
+__device__ __forceinline__ void rotation_of(const GridView& G, int level, int ir, int ip, int iw,
+                                            double R[9]) {
+  const double2 a = G.lut[G.lut_off[level * 3 + 0] + (ir - G.lut_lo[level * 3 + 0])];
+  const double2 b = G.lut[G.lut_off[level * 3 + 1] + (ip - G.lut_lo[level * 3 + 1])];
+  const double2 g = G.lut[G.lut_off[level * 3 + 2] + (iw - G.lut_lo[level * 3 + 2])];
+  const double ca = a.x, sa = a.y, cb = b.x, sb = b.y, cg = g.x, sg = g.y;
+  R[0] = __dmul_rn(cg, cb);
+  R[1] = __dsub_rn(__dmul_rn(__dmul_rn(cg, sb), sa), __dmul_rn(sg, ca));
+  R[2] = __dadd_rn(__dmul_rn(__dmul_rn(cg, sb), ca), __dmul_rn(sg, sa));
+  R[3] = __dmul_rn(sg, cb);
+  R[4] = __dadd_rn(__dmul_rn(__dmul_rn(sg, sb), sa), __dmul_rn(cg, ca));
+  R[5] = __dsub_rn(__dmul_rn(__dmul_rn(sg, sb), ca), __dmul_rn(cg, sa));
+  R[6] = -sb;
+  R[7] = __dmul_rn(cb, sa);
+  R[8] = __dmul_rn(cb, ca);
+}
+
+// R*p in the reference's evaluation order (translation not yet added).
+__device__ __forceinline__ double rot_row(double r0, double r1, double r2, double px, double py,
+                                          double pz) {
+  return __dadd_rn(__dadd_rn(__dmul_rn(r0, px), __dmul_rn(r1, py)), __dmul_rn(r2, pz));
+}
+
+// Fast-path voxel offset of one axis; returns false when ambiguous.
+__device__ __forceinline__ bool fast_floor(double rp, double inv_cell, double tmax, int32_t* f) {
+  const double w = __dmul_rn(rp, inv_cell);
+  const double fl = floor(w);
+  const double fr = __dsub_rn(w, fl);
+  const double aw = fabs(w);
+  const double eps = __dmul_rn(__dadd_rn(aw, tmax), 0x1p-48);
+  const bool ok = (aw < 0x1p30) && (fr > eps) && (fr < __dsub_rn(1.0, eps));
+  *f = ok ? static_cast<int32_t>(fl) : 0;
+  return ok;
+}
+
+// Exact reference arithmetic for one (point, node): q = rp + cell*ix, then
+// floor(q / cell) with x86 conversion semantics, then contains().
+__device__ __forceinline__ int exact_hit(const LevelView& L, double rx, double ry, double rz,
+                                         int32_t ix, int32_t iy, int32_t iz) {
+  const int32_t vx = dev_voxel_index(__dadd_rn(rx, __dmul_rn(L.cell, static_cast<double>(ix))), L.cell);
+  const int32_t vy = dev_voxel_index(__dadd_rn(ry, __dmul_rn(L.cell, static_cast<double>(iy))), L.cell);
+  const int32_t vz = dev_voxel_index(__dadd_rn(rz, __dmul_rn(L.cell, static_cast<double>(iz))), L.cell);
+  if (vx == INT32_MIN && vy == INT32_MIN && vz == INT32_MIN) return 0;  // kEmpty probe
+  return level_contains(L, vx, vy, vz) ? 1 : 0;
+}
+
+// ---- runs kernel ------------------------------------------------------------
+// One work item = (run of <= NT same-rotation nodes, tile of scan points).
+// Each thread walks its points; per point the rotation work is shared by the
+// run's NT translations.  Counts are reduced warp -> block -> global.
+template <int NT>
+__global__ void __launch_bounds__(256) score_runs_kernel(
+    MapView map, GridView grid, ScanView scan, const bbs_node* __restrict__ nodes,
+    const uint32_t* __restrict__ perm, const uint2* __restrict__ runs, uint32_t n_runs_param,
+    const uint32_t* __restrict__ d_n, uint32_t n_nodes_param, uint32_t n_ptiles,
+    int32_t* __restrict__ scores) {
+  __shared__ int32_t s_t[NT][3];
+  __shared__ uint32_t s_idx[NT];
+  __shared__ double s_R[9];
+  __shared__ int32_t s_cnt[NT];
+  __shared__ int32_t s_level, s_count;
+  __shared__ double s_tmax;
+
+  const uint32_t n_nodes = d_n ? *d_n : n_nodes_param;
+  const uint32_t n_runs = runs ? n_runs_param : (n_nodes + NT - 1) / NT;
+  const uint64_t n_items = static_cast<uint64_t>(n_runs) * n_ptiles;
+  const uint32_t k = scan.k;
+  const uint32_t tile = (k + n_ptiles - 1) / n_ptiles;
+  const int lane = threadIdx.x & 31;
+
+  for (uint64_t item = blockIdx.x; item < n_items; item += gridDim.x) {
+    const uint32_t r = static_cast<uint32_t>(item / n_ptiles);
+    const uint32_t pt = static_cast<uint32_t>(item % n_ptiles);
+    if (threadIdx.x < 32) {
+      uint32_t first, count;
+      if (runs) {
+        const uint2 rr = runs[r];
+        first = rr.x;
+        count = rr.y;
+      } else {
+        first = r * NT;
+        count = min(static_cast<uint32_t>(NT), n_nodes - first);
+      }
+      int32_t amax = 0;
+      if (lane < static_cast<int>(count)) {
+        const uint32_t idx = perm ? perm[first + lane] : first + lane;
+        const int4 a = reinterpret_cast<const int4*>(nodes)[2 * idx];
+        s_t[lane][0] = a.x;
+        s_t[lane][1] = a.y;
+        s_t[lane][2] = a.z;
+        s_idx[lane] = idx;
+        s_cnt[lane] = 0;
+        amax = max(max(abs(a.x), abs(a.y)), abs(a.z));
+        if (amax < 0) amax = INT32_MAX;  // abs(INT32_MIN)
+      }
+      amax = __reduce_max_sync(0xffffffffu, amax);
+      if (lane == 0) {
+        const uint32_t idx = perm ? perm[first] : first;
+        const int4 a = reinterpret_cast<const int4*>(nodes)[2 * idx];
+        const int4 b = reinterpret_cast<const int4*>(nodes)[2 * idx + 1];
+        // a = (ix, iy, iz, iroll), b = (ipitch, iyaw, level, score)
+        double R[9];
+        rotation_of(grid, b.z, a.w, b.x, b.y, R);
+#pragma unroll
+        for (int i = 0; i < 9; ++i) s_R[i] = R[i];
+        s_level = b.z;
+        s_count = static_cast<int32_t>(count);
+        s_tmax = static_cast<double>(amax) + 2.0;
+      }
+    }
+    __syncthreads();
+    const LevelView L = map.level[s_level];
+    const int count = s_count;
+    const double tmax = s_tmax;
+    double R[9];
+#pragma unroll
+    for (int i = 0; i < 9; ++i) R[i] = s_R[i];
+    int32_t tx[NT], ty[NT], tz[NT];
+#pragma unroll
+    for (int j = 0; j < NT; ++j) {
+      tx[j] = s_t[j][0];
+      ty[j] = s_t[j][1];
+      tz[j] = s_t[j][2];
+    }
+    int cnt[NT];
+#pragma unroll
+    for (int j = 0; j < NT; ++j) cnt[j] = 0;
+
+    const uint32_t p0 = pt * tile;
+    const uint32_t p1 = min(k, p0 + tile);
+    for (uint32_t p = p0 + threadIdx.x; p < p1; p += blockDim.x) {
+      const double px = scan.x[p], py = scan.y[p], pz = scan.z[p];
+      const double rx = rot_row(R[0], R[1], R[2], px, py, pz);
+      const double ry = rot_row(R[3], R[4], R[5], px, py, pz);
+      const double rz = rot_row(R[6], R[7], R[8], px, py, pz);
+      int32_t fx, fy, fz;
+      const bool ok = fast_floor(rx, L.inv_cell, tmax, &fx) & fast_floor(ry, L.inv_cell, tmax, &fy) &
+                      fast_floor(rz, L.inv_cell, tmax, &fz);
+      if (ok) {
+#pragma unroll
+        for (int j = 0; j < NT; ++j)
+          if (j < count) cnt[j] += level_contains(L, fx + tx[j], fy + ty[j], fz + tz[j]) ? 1 : 0;
+      } else {
+#pragma unroll
+        for (int j = 0; j < NT; ++j)
+          if (j < count) cnt[j] += exact_hit(L, rx, ry, rz, tx[j], ty[j], tz[j]);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < NT; ++j) {
+      const int v = __reduce_add_sync(0xffffffffu, cnt[j]);
+      if (lane == 0 && j < count && v) atomicAdd(&s_cnt[j], v);
+    }
+    __syncthreads();
+    if (threadIdx.x < static_cast<unsigned>(count)) {
+      if (n_ptiles == 1)
+        scores[s_idx[threadIdx.x]] = s_cnt[threadIdx.x];
+      else if (s_cnt[threadIdx.x])
+        atomicAdd(&scores[s_idx[threadIdx.x]], s_cnt[threadIdx.x]);
+    }
+    __syncthreads();
+  }
+}
+
+// ---- root box kernel --------------------------------------------------------
+// One CTA = (root rotation, chunk of that rotation's owned translations).
+// The scan is processed in chunks of kChunk points: each chunk's fast-path
+// voxel offsets f are de-duplicated in a shared-memory hash (coarse root
+// levels put hundreds of points in one voxel), and every owned translation t
+// accumulates sum_f count(f) * contains(f + t).  Ambiguous points are kept
+// as a list and scored exactly per translation.
+constexpr int kChunk = 2048;
+constexpr int kHashSlots = 4096;
+constexpr unsigned long long kSlotEmpty = ~0ull;
+
+__device__ __forceinline__ uint32_t slot_hash(unsigned long long key) {
+  return static_cast<uint32_t>((key * 0x9E3779B97F4A7C15ull) >> 52);  // 12 bits
+}
+
+__global__ void __launch_bounds__(kBoxThreads, 2) score_box_kernel(MapView map, GridView grid,
+                                                                   ScanView scan, BoxParams bp,
+                                                                   int32_t* __restrict__ scores) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  unsigned long long* s_key = reinterpret_cast<unsigned long long*>(smem);        // 32 KB
+  int32_t* s_hcnt = reinterpret_cast<int32_t*>(s_key + kHashSlots);               // 16 KB
+  int4* s_ent = reinterpret_cast<int4*>(s_hcnt + kHashSlots);                      // 32 KB
+  uint32_t* s_amb = reinterpret_cast<uint32_t*>(s_ent + kChunk);                   // 8 KB
+  __shared__ int32_t s_nent, s_namb;
+
+  const uint32_t nrot = bp.nr * bp.np * bp.nw;
+  const uint64_t ntrans = static_cast<uint64_t>(bp.nx) * bp.ny * bp.nz;
+  const uint64_t n_items = static_cast<uint64_t>(nrot) * bp.n_tchunks;
+  const LevelView L = map.level[bp.level];
+
+  for (uint64_t item = blockIdx.x; item < n_items; item += gridDim.x) {
+    const uint32_t rot = static_cast<uint32_t>(item / bp.n_tchunks);
+    const uint32_t tc = static_cast<uint32_t>(item % bp.n_tchunks);
+    // owned translations of this rotation: (t*nrot + rot) % world == rank
+    // <=> t == t0 (mod P); P = world / gcd(nrot, world); world <= 64.
+    uint32_t P = bp.world, t0 = 0;
+    bool any = bp.world == 1;
+    if (!any) {
+      uint32_t g = bp.world, b = nrot % bp.world;
+      while (b) {
+        const uint32_t tmp = g % b;
+        g = b;
+        b = tmp;
+      }
+      P = bp.world / g;
+      for (uint32_t c = 0; c < P; ++c)
+        if ((static_cast<uint64_t>(c) * nrot + rot) % bp.world == bp.rank) {
+          t0 = c;
+          any = true;
+          break;
+        }
+    }
+    if (!any) continue;  // uniform across the CTA
+    const uint64_t n_own = ntrans > t0 ? (ntrans - t0 + P - 1) / P : 0;
+    const uint64_t own0 = static_cast<uint64_t>(tc) * kBoxTransPerCta;
+    if (own0 >= n_own) continue;
+
+    const uint32_t ir = rot / (bp.np * bp.nw);
+    const uint32_t ip = (rot / bp.nw) % bp.np;
+    const uint32_t iw = rot % bp.nw;
+    double R[9];
+    rotation_of(grid, bp.level, static_cast<int>(ir), static_cast<int>(ip), static_cast<int>(iw), R);
+
+    // this thread's translations
+    int32_t tix[kBoxTransPerThread], tiy[kBoxTransPerThread], tiz[kBoxTransPerThread];
+    uint64_t tref[kBoxTransPerThread];
+    bool tvalid[kBoxTransPerThread];
+    int acc[kBoxTransPerThread];
+#pragma unroll
+    for (int i = 0; i < kBoxTransPerThread; ++i) {
+      const uint64_t o = own0 + threadIdx.x + static_cast<uint64_t>(i) * kBoxThreads;
+      tvalid[i] = o < n_own;
+      const uint64_t t = tvalid[i] ? t0 + o * P : 0;
+      tiz[i] = bp.z0 + static_cast<int32_t>(t % bp.nz);
+      tiy[i] = bp.y0 + static_cast<int32_t>((t / bp.nz) % bp.ny);
+      tix[i] = bp.x0 + static_cast<int32_t>(t / (static_cast<uint64_t>(bp.nz) * bp.ny));
+      tref[i] = t * nrot + rot;
+      acc[i] = 0;
+    }
+
+    for (uint32_t c0 = 0; c0 < scan.k; c0 += kChunk) {
+      for (int i = threadIdx.x; i < kHashSlots; i += blockDim.x) {
+        s_key[i] = kSlotEmpty;
+        s_hcnt[i] = 0;
+      }
+      if (threadIdx.x == 0) {
+        s_nent = 0;
+        s_namb = 0;
+      }
+      __syncthreads();
+      const uint32_t c1 = min(scan.k, c0 + kChunk);
+      for (uint32_t p = c0 + threadIdx.x; p < c1; p += blockDim.x) {
+        const double px = scan.x[p], py = scan.y[p], pz = scan.z[p];
+        int32_t fx, fy, fz;
+        const bool ok = fast_floor(rot_row(R[0], R[1], R[2], px, py, pz), L.inv_cell, bp.tmax, &fx) &
+                        fast_floor(rot_row(R[3], R[4], R[5], px, py, pz), L.inv_cell, bp.tmax, &fy) &
+                        fast_floor(rot_row(R[6], R[7], R[8], px, py, pz), L.inv_cell, bp.tmax, &fz);
+        if (!ok) {
+          s_amb[atomicAdd(&s_namb, 1)] = p;
+          continue;
+        }
+        // |f| < 2^30 on the fast path: 21-bit fields hold f + 2^20 only when
+        // |f| < 2^20; larger offsets are scored exactly instead.
+        if (fx <= -(1 << 20) || fx >= (1 << 20) || fy <= -(1 << 20) || fy >= (1 << 20) ||
+            fz <= -(1 << 20) || fz >= (1 << 20)) {
+          s_amb[atomicAdd(&s_namb, 1)] = p;
+          continue;
+        }
+        const unsigned long long key =
+            (static_cast<unsigned long long>(fx + (1 << 20)) << 42) |
+            (static_cast<unsigned long long>(fy + (1 << 20)) << 21) |
+            static_cast<unsigned long long>(fz + (1 << 20));
+        uint32_t h = slot_hash(key);
+        for (;;) {
+          const unsigned long long prev = atomicCAS(&s_key[h], kSlotEmpty, key);
+          if (prev == kSlotEmpty || prev == key) {
+            atomicAdd(&s_hcnt[h], 1);
+            break;
+          }
+          h = (h + 1) & (kHashSlots - 1);
+        }
+      }
+      __syncthreads();
+      for (int i = threadIdx.x; i < kHashSlots; i += blockDim.x) {
+        const unsigned long long key = s_key[i];
+        if (key != kSlotEmpty) {
+          const int e = atomicAdd(&s_nent, 1);
+          s_ent[e] = make_int4(static_cast<int32_t>((key >> 42) & 0x1FFFFF) - (1 << 20),
+                               static_cast<int32_t>((key >> 21) & 0x1FFFFF) - (1 << 20),
+                               static_cast<int32_t>(key & 0x1FFFFF) - (1 << 20), s_hcnt[i]);
+        }
+      }
+      __syncthreads();
+      const int nent = s_nent;
+      for (int e = 0; e < nent; ++e) {
+        const int4 f = s_ent[e];
+#pragma unroll
+        for (int i = 0; i < kBoxTransPerThread; ++i)
+          acc[i] += level_contains(L, f.x + tix[i], f.y + tiy[i], f.z + tiz[i]) ? f.w : 0;
+      }
+      const int namb = s_namb;
+      for (int a = 0; a < namb; ++a) {
+        const uint32_t p = s_amb[a];
+        const double px = scan.x[p], py = scan.y[p], pz = scan.z[p];
+        const double rx = rot_row(R[0], R[1], R[2], px, py, pz);
+        const double ry = rot_row(R[3], R[4], R[5], px, py, pz);
+        const double rz = rot_row(R[6], R[7], R[8], px, py, pz);
+#pragma unroll
+        for (int i = 0; i < kBoxTransPerThread; ++i)
+          acc[i] += exact_hit(L, rx, ry, rz, tix[i], tiy[i], tiz[i]);
+      }
+      __syncthreads();
+    }
+#pragma unroll
+    for (int i = 0; i < kBoxTransPerThread; ++i)
+      if (tvalid[i]) scores[tref[i]] = acc[i];
+  }
+}
+
+__global__ void rotation_key_kernel(const bbs_node* __restrict__ nodes, uint64_t n, GridView G,
+                                    unsigned long long* __restrict__ keys,
+                                    uint32_t* __restrict__ idx) {
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
+       i += uint64_t(gridDim.x) * blockDim.x) {
+    const bbs_node nd = nodes[i];
+    const int l = nd.level;
+    keys[i] = (static_cast<unsigned long long>(l) << 60) |
+              (static_cast<unsigned long long>(nd.iroll - G.lut_lo[l * 3 + 0]) << 40) |
+              (static_cast<unsigned long long>(nd.ipitch - G.lut_lo[l * 3 + 1]) << 20) |
+              static_cast<unsigned long long>(nd.iyaw - G.lut_lo[l * 3 + 2]);
+    idx[i] = static_cast<uint32_t>(i);
+  }
+}
+
+__global__ void expand_runs_kernel(const int32_t* __restrict__ counts,
+                                   const int32_t* __restrict__ starts,
+                                   const int32_t* __restrict__ chunk_off, int32_t n_runs,
+                                   uint2* __restrict__ runs) {
+  for (int64_t r = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; r < n_runs;
+       r += int64_t(gridDim.x) * blockDim.x) {
+    const int32_t c = counts[r], s = starts[r];
+    int32_t o = chunk_off[r];
+    for (int32_t j = 0; j < c; j += 32, ++o)
+      runs[o] = make_uint2(static_cast<uint32_t>(s + j), static_cast<uint32_t>(min(32, c - j)));
+  }
+}
+
+__global__ void nchunks_kernel(const int32_t* __restrict__ counts, int32_t n,
+                               int32_t* __restrict__ out) {
+  for (int64_t r = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; r < n;
+       r += int64_t(gridDim.x) * blockDim.x)
+    out[r] = (counts[r] + 31) / 32;
+}
+
+__global__ void write_scores_kernel(bbs_node* __restrict__ nodes, const int32_t* __restrict__ sc,
+                                    uint64_t n) {
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
+       i += uint64_t(gridDim.x) * blockDim.x)
+    nodes[i].score = sc[i];
+}
+
+unsigned grid_1d(uint64_t n) {
+  return static_cast<unsigned>(std::min<uint64_t>(std::max<uint64_t>((n + 255) / 256, 1), 148ull * 32));
+}
+
+}  // namespace
+
+uint32_t choose_ptiles(uint64_t runs, uint32_t k) {
+  const uint64_t target = 148ull * 8 * 2;  // ~2 waves of 256-thread CTAs
+  uint64_t p = runs ? (target + runs - 1) / runs : 1;
+  const uint64_t pmax = std::max<uint64_t>(1, (k + 1023) / 1024);  // >= 1024 points per tile
+  p = std::min(std::max<uint64_t>(p, 1), pmax);
+  return static_cast<uint32_t>(p);
+}
+
+void launch_score_box(const MapView& map, const GridView& grid, const ScanView& scan,
+                      const BoxParams& bp, int32_t* scores, cudaStream_t s) {
+  static bool attr_done = false;
+  const int smem = kHashSlots * 8 + kHashSlots * 4 + kChunk * 16 + kChunk * 4;
+  if (!attr_done) {
+    BBS_CUDA(cudaFuncSetAttribute(score_box_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  smem));
+    attr_done = true;
+  }
+  const uint64_t items = static_cast<uint64_t>(bp.nr) * bp.np * bp.nw * bp.n_tchunks;
+  const unsigned grid_sz = static_cast<unsigned>(std::min<uint64_t>(items, 148ull * 2 * 64));
+  score_box_kernel<<<grid_sz, kBoxThreads, smem, s>>>(map, grid, scan, bp, scores);
+  BBS_CUDA(cudaGetLastError());
+}
+
+void launch_score_runs8(const MapView& map, const GridView& grid, const ScanView& scan,
+                        const bbs_node* nodes, const uint32_t* d_n, uint32_t n_max,
+                        uint32_t n_ptiles, int32_t* scores, cudaStream_t s) {
+  const uint64_t items = static_cast<uint64_t>((n_max + 7) / 8) * n_ptiles;
+  const unsigned g = static_cast<unsigned>(std::min<uint64_t>(std::max<uint64_t>(items, 1), 148ull * 8 * 8));
+  score_runs_kernel<8><<<g, 256, 0, s>>>(map, grid, scan, nodes, nullptr, nullptr, 0, d_n, n_max,
+                                         n_ptiles, scores);
+  BBS_CUDA(cudaGetLastError());
+}
+
+void score_nodes_general(const MapView& map, const GridView& grid, const ScanView& scan,
+                         bbs_node* d_nodes, uint64_t n, cudaStream_t s) {
+  if (n == 0) return;
+  if (n >= (1ull << 31)) throw Error(BBS_ERR_TOO_LARGE, "batch_evaluate: more than 2^31 nodes");
+  const int ni = static_cast<int>(n);
+  unsigned long long *keys, *keys_alt;
+  uint32_t *idx, *idx_alt;
+  BBS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&keys), n * 8, s));
+  BBS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&keys_alt), n * 8, s));
+  BBS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&idx), n * 4, s));
+  BBS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&idx_alt), n * 4, s));
+  rotation_key_kernel<<<grid_1d(n), 256, 0, s>>>(d_nodes, n, grid, keys, idx);
+  BBS_CUDA(cudaGetLastError());
+  cub::DoubleBuffer<unsigned long long> dk(keys, keys_alt);
+  cub::DoubleBuffer<uint32_t> dv(idx, idx_alt);
+  size_t t_sort = 0, t_rle = 0, t_scan = 0;
+  BBS_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, t_sort, dk, dv, ni, 0, 64, s));
+  int32_t *counts, *starts, *nch, *choff, *d_nruns;
+  unsigned long long* uniq;
+  BBS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&counts), (n + 1) * 4, s));
+  BBS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&starts), (n + 1) * 4, s));
+  BBS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&nch), (n + 1) * 4, s));
+  BBS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&choff), (n + 1) * 4, s));
+  BBS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_nruns), 4, s));
+  BBS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&uniq), n * 8, s));
+  BBS_CUDA(cub::DeviceRunLengthEncode::Encode(nullptr, t_rle, keys, uniq, counts, d_nruns, ni, s));
+  BBS_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, t_scan, counts, starts, ni, s));
+  void* temp;
+  const size_t t_all = std::max(t_sort, std::max(t_rle, t_scan));
+  BBS_CUDA(cudaMallocAsync(&temp, t_all, s));
+  BBS_CUDA(cub::DeviceRadixSort::SortPairs(temp, t_sort, dk, dv, ni, 0, 64, s));
+  BBS_CUDA(cub::DeviceRunLengthEncode::Encode(temp, t_rle, dk.Current(), uniq, counts, d_nruns, ni, s));
+  int32_t nruns = 0;
+  BBS_CUDA(cudaMemcpyAsync(&nruns, d_nruns, 4, cudaMemcpyDeviceToHost, s));
+  BBS_CUDA(cudaStreamSynchronize(s));
+  BBS_CUDA(cub::DeviceScan::ExclusiveSum(temp, t_scan, counts, starts, nruns, s));
+  nchunks_kernel<<<grid_1d(nruns), 256, 0, s>>>(counts, nruns, nch);
+  BBS_CUDA(cub::DeviceScan::ExclusiveSum(temp, t_scan, nch, choff, nruns, s));
+  int32_t last_off = 0, last_n = 0;
+  BBS_CUDA(cudaMemcpyAsync(&last_off, choff + nruns - 1, 4, cudaMemcpyDeviceToHost, s));
+  BBS_CUDA(cudaMemcpyAsync(&last_n, nch + nruns - 1, 4, cudaMemcpyDeviceToHost, s));
+  BBS_CUDA(cudaStreamSynchronize(s));
+  const uint32_t nchunks = static_cast<uint32_t>(last_off + last_n);
+  uint2* runs;
+  int32_t* sc;
+  BBS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&runs), static_cast<size_t>(nchunks) * 8, s));
+  BBS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&sc), n * 4, s));
+  expand_runs_kernel<<<grid_1d(nruns), 256, 0, s>>>(counts, starts, choff, nruns, runs);
+  BBS_CUDA(cudaGetLastError());
+  const uint32_t pt = choose_ptiles(nchunks, scan.k);
+  if (pt > 1) BBS_CUDA(cudaMemsetAsync(sc, 0, n * 4, s));
+  const uint64_t items = static_cast<uint64_t>(nchunks) * pt;
+  const unsigned g = static_cast<unsigned>(std::min<uint64_t>(std::max<uint64_t>(items, 1), 148ull * 8 * 8));
+  score_runs_kernel<32><<<g, 256, 0, s>>>(map, grid, scan, d_nodes, dv.Current(), runs, nchunks,
+                                          nullptr, ni, pt, sc);
+  BBS_CUDA(cudaGetLastError());
+  write_scores_kernel<<<grid_1d(n), 256, 0, s>>>(d_nodes, sc, n);
+  BBS_CUDA(cudaGetLastError());
+  for (void* p : {static_cast<void*>(keys), static_cast<void*>(keys_alt), static_cast<void*>(idx),
+                  static_cast<void*>(idx_alt), static_cast<void*>(counts),
+                  static_cast<void*>(starts), static_cast<void*>(nch), static_cast<void*>(choff),
+                  static_cast<void*>(d_nruns), static_cast<void*>(uniq), temp,
+                  static_cast<void*>(runs), static_cast<void*>(sc)})
+    BBS_CUDA(cudaFreeAsync(p, s));
+}
+
+}  // namespace bbs

@@ -1,0 +1,935 @@
+// search.cu — K5/K6 (branching + best-first frontier) and the search driver.
+//
+// Replaces search() (search.hpp:72-186).  The reference's loop is replayed
+// EXACTLY on the device as flush epochs:
+//   * the queue is a sorted array; keys encode EntryCompare (search.hpp:47-59):
+//       BFS  (score desc, level desc, seq asc)
+//       DFS  (level asc, score desc, seq desc)
+//   * between flushes nothing is pushed, so an epoch pops a queue PREFIX.
+//     With B_i = max(B_0, max leaf score before i), entry i is pruned when
+//     score_i < B_i, a surviving leaf sets the incumbent, a surviving inner
+//     node adds c_i = 8 * prod(in-range rotational children) to `pending`,
+//     and the flush happens at the first i with sum(c) > b (or on drain);
+//   * the flush scores pending (score.cu), keeps score >= B, assigns seq in
+//     pending order, sorts the survivors by key and merges them into the
+//     remaining queue.
+// Kernels per epoch: frontier (1 CTA scan) -> branch -> score -> survivors
+// (1 CTA compaction) -> rank-sort -> merge -> finalize.  Every kernel reads
+// its sizes from the device-resident EpochState, so epochs are enqueued back
+// to back with no host round-trip; the host reads the 100-byte state every
+// few epochs (or every epoch when an incumbent exchange is configured).
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <limits>
+#include <vector>
+
+#include "bbs_map_impl.h"
+#include "device_common.cuh"
+#include "kernels.h"
+
+namespace bbs {
+
+namespace {
+
+constexpr unsigned long long kSMax = (1ull << 20) - 1;
+constexpr unsigned long long kSeqMax = (1ull << 40) - 1;
+
+struct EpochState {
+  int32_t best;          // incumbent B (search.hpp:99)
+  int32_t matched;
+  bbs_node best_node;
+  uint32_t q_len;        // queue length (in buffer `cur`)
+  uint32_t cur;
+  unsigned long long seq;  // next insertion sequence number (search.hpp:107)
+  unsigned long long nodes_generated, nodes_pruned, batches_flushed, epochs;
+  unsigned long long trace_len;
+  int32_t last_best_epoch;  // frontier pass that set the incumbent last
+  int32_t active;
+  uint32_t n_cons, n_children, n_expand, n_surv;
+  int32_t flush_best;
+  uint32_t pass;           // frontier passes executed while active
+  uint32_t q_peak;
+  uint32_t pad;
+};
+
+struct Queue {
+  unsigned long long* key[2];
+  bbs_node* node[2];
+};
+
+__device__ __forceinline__ unsigned long long queue_key(int strategy, int32_t score, int32_t level,
+                                                        unsigned long long seq) {
+  const unsigned long long s = kSMax - static_cast<unsigned long long>(score);
+  if (strategy == BBS_STRATEGY_BFS)
+    return (s << 44) | (static_cast<unsigned long long>(15 - level) << 40) | seq;
+  return (static_cast<unsigned long long>(level) << 60) | (s << 40) | (kSeqMax - seq);
+}
+
+// Per-axis in-range rotational children of branch(), nodes.hpp:99-111.
+__device__ __forceinline__ void child_counts(const GridView& G, const bbs_node& n, int32_t a[3],
+                                             int32_t c[3]) {
+  const int l = n.level, cl = n.level - 1;
+  const int32_t idx[3] = {n.iroll, n.ipitch, n.iyaw};
+#pragma unroll
+  for (int ax = 0; ax < 3; ++ax) {
+    a[ax] = G.div[l * 3 + ax];
+    const long long room = static_cast<long long>(G.max_index[cl * 3 + ax]) -
+                           static_cast<long long>(a[ax]) * idx[ax] + 1;
+    c[ax] = static_cast<int32_t>(room < 0 ? 0 : (room > a[ax] ? a[ax] : room));
+  }
+}
+
+__device__ __forceinline__ uint32_t n_children_of(const GridView& G, const bbs_node& n) {
+  int32_t a[3], c[3];
+  child_counts(G, n, a, c);
+  return 8u * static_cast<uint32_t>(c[0]) * static_cast<uint32_t>(c[1]) * static_cast<uint32_t>(c[2]);
+}
+
+constexpr int kFT = 1024;
+constexpr int kFIPT = 4;
+constexpr int kFChunk = kFT * kFIPT;
+
+// E1: which queue prefix this epoch pops, pruning, leaf updates, children.
+__global__ void __launch_bounds__(kFT) frontier_kernel(EpochState* st, Queue q, GridView G,
+                                                       unsigned long long b,
+                                                       uint32_t* __restrict__ exp_parent,
+                                                       uint32_t* __restrict__ exp_off,
+                                                       int32_t* __restrict__ trace,
+                                                       unsigned long long trace_cap) {
+  using ScanI = cub::BlockScan<int, kFT>;
+  using ScanU = cub::BlockScan<unsigned long long, kFT>;
+  using RedI = cub::BlockReduce<int, kFT>;
+  __shared__ union {
+    typename ScanI::TempStorage si;
+    typename ScanU::TempStorage su;
+    typename RedI::TempStorage ri;
+  } tmp;
+  __shared__ int s_cut, s_lastlu;
+  __shared__ unsigned long long s_sum_at_cut;
+  __shared__ int s_active;
+
+  const int tid = threadIdx.x;
+  if (tid == 0) s_active = st->active;
+  __syncthreads();
+  if (!s_active) {
+    if (tid == 0) st->n_children = 0;
+    return;
+  }
+  const uint32_t qlen = st->q_len;
+  const bbs_node* __restrict__ nodes = q.node[st->cur];
+  int carry_best = st->best;
+  unsigned long long carry_sum = 0, carry_trace = st->trace_len;
+  uint32_t carry_exp = 0;
+  uint32_t consumed = qlen;
+  unsigned long long pruned = 0;
+  int best_i = -1;
+
+  for (uint32_t base = 0; base < qlen; base += kFChunk) {
+    bbs_node nd[kFIPT];
+    bool valid[kFIPT];
+    int lm = INT_MIN;
+#pragma unroll
+    for (int k = 0; k < kFIPT; ++k) {
+      const uint32_t i = base + tid * kFIPT + k;
+      valid[k] = i < qlen;
+      if (valid[k]) {
+        nd[k] = nodes[i];
+        if (nd[k].level == 0) lm = max(lm, nd[k].score);
+      }
+    }
+    int excl;
+    ScanI(tmp.si).ExclusiveScan(lm, excl, INT_MIN, cub::Max());
+    __syncthreads();
+    int B = max(carry_best, excl);
+    uint32_t c[kFIPT];
+    bool pr[kFIPT], lu[kFIPT];
+    unsigned long long csum = 0;
+#pragma unroll
+    for (int k = 0; k < kFIPT; ++k) {
+      c[k] = 0;
+      pr[k] = lu[k] = false;
+      if (!valid[k]) continue;
+      const int s = nd[k].score;
+      pr[k] = s < B;  // search.hpp:150-153
+      const bool leaf = nd[k].level == 0;
+      lu[k] = !pr[k] && leaf;  // search.hpp:154-160
+      if (lu[k]) B = s;
+      if (!pr[k] && !leaf) c[k] = n_children_of(G, nd[k]);
+      csum += c[k];
+    }
+    unsigned long long sexcl, stotal;
+    ScanU(tmp.su).ExclusiveSum(csum, sexcl, stotal);
+    __syncthreads();
+    unsigned long long S = carry_sum + sexcl;
+    unsigned long long sbefore[kFIPT];
+    int mycut = INT_MAX;
+#pragma unroll
+    for (int k = 0; k < kFIPT; ++k) {
+      sbefore[k] = S;
+      S += c[k];
+      if (valid[k] && c[k] && S > b && mycut == INT_MAX) mycut = static_cast<int>(base + tid * kFIPT + k);
+    }
+    const int cut = RedI(tmp.ri).Reduce(mycut, cub::Min());
+    if (tid == 0) s_cut = cut;
+    __syncthreads();
+    const int chunk_cut = s_cut;
+    if (chunk_cut != INT_MAX && static_cast<int>(base + tid * kFIPT) <= chunk_cut &&
+        chunk_cut < static_cast<int>(base + tid * kFIPT + kFIPT)) {
+      s_sum_at_cut = sbefore[chunk_cut - (base + tid * kFIPT)] + c[chunk_cut - (base + tid * kFIPT)];
+    }
+    const long long limit = chunk_cut != INT_MAX ? chunk_cut : static_cast<long long>(base) + kFChunk - 1;
+    int ne = 0, nt = 0, lastlu = -1;
+#pragma unroll
+    for (int k = 0; k < kFIPT; ++k) {
+      const long long i = base + tid * kFIPT + k;
+      if (!valid[k] || i > limit) continue;
+      if (c[k]) ++ne;
+      if (lu[k]) {
+        ++nt;
+        lastlu = static_cast<int>(i);
+      }
+      if (pr[k]) ++pruned;
+    }
+    int epos, etot;
+    ScanI(tmp.si).ExclusiveSum(ne, epos, etot);
+    __syncthreads();
+    int tpos, ttot;
+    ScanI(tmp.si).ExclusiveSum(nt, tpos, ttot);
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < kFIPT; ++k) {
+      const long long i = base + tid * kFIPT + k;
+      if (!valid[k] || i > limit) continue;
+      if (c[k]) {
+        exp_parent[carry_exp + epos] = static_cast<uint32_t>(i);
+        exp_off[carry_exp + epos] = static_cast<uint32_t>(sbefore[k]);
+        ++epos;
+      }
+      if (lu[k]) {
+        const unsigned long long t = carry_trace + tpos;
+        if (t < trace_cap) trace[t] = nd[k].score;
+        ++tpos;
+      }
+    }
+    const int chunk_last = RedI(tmp.ri).Reduce(lastlu, cub::Max());
+    if (tid == 0) s_lastlu = chunk_last;
+    __syncthreads();
+    if (s_lastlu >= 0) {
+      best_i = s_lastlu;
+      carry_best = nodes[best_i].score;  // leaf updates are non-decreasing
+    }
+    carry_exp += static_cast<uint32_t>(etot);
+    carry_trace += static_cast<unsigned long long>(ttot);
+    if (chunk_cut != INT_MAX) {
+      carry_sum = s_sum_at_cut;
+      consumed = static_cast<uint32_t>(chunk_cut) + 1;
+      break;
+    }
+    carry_sum += stotal;
+    __syncthreads();
+  }
+  __syncthreads();
+  const unsigned long long pruned_all = cub::BlockReduce<unsigned long long, kFT>(
+      *reinterpret_cast<typename cub::BlockReduce<unsigned long long, kFT>::TempStorage*>(&tmp))
+      .Sum(pruned);
+  if (tid == 0) {
+    st->nodes_pruned += pruned_all;
+    st->best = carry_best;
+    st->flush_best = carry_best;
+    st->trace_len = carry_trace;
+    st->n_cons = consumed;
+    st->n_expand = carry_exp;
+    st->n_children = static_cast<uint32_t>(carry_sum);
+    if (best_i >= 0) {
+      st->best_node = nodes[best_i];
+      st->matched = 1;
+      st->last_best_epoch = static_cast<int32_t>(st->pass);
+    }
+    st->pass += 1;
+    if (carry_sum == 0) {
+      // queue drained with nothing pending: the loop ends (search.hpp:145)
+      st->active = 0;
+      st->q_len = 0;
+    } else {
+      st->nodes_generated += carry_sum;
+      st->batches_flushed += 1;
+      st->epochs += 1;
+    }
+  }
+}
+
+// E2: branch() (nodes.hpp:91-121) for every expanding parent, children in
+// pop order, each parent's children in (jr, jp, jw, jx, jy, jz) order.
+__global__ void branch_kernel(const EpochState* st, Queue q, GridView G,
+                              const uint32_t* __restrict__ exp_parent,
+                              const uint32_t* __restrict__ exp_off, bbs_node* __restrict__ pending) {
+  const uint32_t n = st->n_children;
+  if (n == 0) return;
+  const uint32_t ne = st->n_expand;
+  const bbs_node* __restrict__ nodes = q.node[st->cur];
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    uint32_t lo = 0, hi = ne - 1;  // largest m with exp_off[m] <= i
+    while (lo < hi) {
+      const uint32_t mid = (lo + hi + 1) >> 1;
+      if (exp_off[mid] <= i)
+        lo = mid;
+      else
+        hi = mid - 1;
+    }
+    const bbs_node p = nodes[exp_parent[lo]];
+    const uint32_t local = i - exp_off[lo];
+    int32_t a[3], c[3];
+    child_counts(G, p, a, c);
+    const uint32_t kk = local >> 3, t = local & 7u;
+    const int32_t jw = static_cast<int32_t>(kk % c[2]);
+    const int32_t jp = static_cast<int32_t>((kk / c[2]) % c[1]);
+    const int32_t jr = static_cast<int32_t>(kk / (c[2] * c[1]));
+    bbs_node ch;
+    ch.ix = 2 * p.ix + static_cast<int32_t>(t >> 2);
+    ch.iy = 2 * p.iy + static_cast<int32_t>((t >> 1) & 1u);
+    ch.iz = 2 * p.iz + static_cast<int32_t>(t & 1u);
+    ch.iroll = a[0] * p.iroll + jr;
+    ch.ipitch = a[1] * p.ipitch + jp;
+    ch.iyaw = a[2] * p.iyaw + jw;
+    ch.level = p.level - 1;
+    ch.score = -1;
+    pending[i] = ch;
+  }
+}
+
+constexpr int kST = 1024;
+constexpr int kSIPT = 4;
+
+// E4a: flush pruning (search.hpp:134-140): keep score >= B in pending order
+// and give them consecutive seq numbers.
+__global__ void __launch_bounds__(kST) survivors_kernel(EpochState* st, int strategy,
+                                                        const bbs_node* __restrict__ pending,
+                                                        const int32_t* __restrict__ scores,
+                                                        unsigned long long* __restrict__ s_key,
+                                                        bbs_node* __restrict__ s_node) {
+  using ScanI = cub::BlockScan<int, kST>;
+  __shared__ typename ScanI::TempStorage tmp;
+  const uint32_t n = st->n_children;
+  if (n == 0) return;
+  const int32_t B = st->flush_best;
+  const unsigned long long seq0 = st->seq;
+  uint32_t carry = 0;
+  for (uint32_t base = 0; base < n; base += kST * kSIPT) {
+    int keep[kSIPT];
+    int cnt = 0;
+#pragma unroll
+    for (int k = 0; k < kSIPT; ++k) {
+      const uint32_t i = base + threadIdx.x * kSIPT + k;
+      keep[k] = (i < n && scores[i] >= B) ? 1 : 0;
+      cnt += keep[k];
+    }
+    int pos, tot;
+    ScanI(tmp).ExclusiveSum(cnt, pos, tot);
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < kSIPT; ++k) {
+      const uint32_t i = base + threadIdx.x * kSIPT + k;
+      if (!keep[k]) continue;
+      bbs_node nd = pending[i];
+      nd.score = scores[i];
+      const uint32_t o = carry + pos++;
+      s_node[o] = nd;
+      s_key[o] = queue_key(strategy, nd.score, nd.level, seq0 + o);
+    }
+    carry += static_cast<uint32_t>(tot);
+  }
+  if (threadIdx.x == 0) {
+    st->n_surv = carry;
+    st->seq = seq0 + carry;
+    st->nodes_pruned += n - carry;
+  }
+}
+
+// E4b: order the survivors by key.  Keys are unique (they embed seq), so a
+// survivor's rank = #keys below it; ranks are computed against smem tiles.
+constexpr int kRT = 256;
+__global__ void __launch_bounds__(kRT) rank_sort_kernel(const EpochState* st,
+                                                        const unsigned long long* __restrict__ key,
+                                                        const bbs_node* __restrict__ node,
+                                                        unsigned long long* __restrict__ out_key,
+                                                        bbs_node* __restrict__ out_node) {
+  __shared__ unsigned long long tile[kRT];
+  const uint32_t n = st->n_children ? st->n_surv : 0;
+  if (n == 0) return;
+  for (uint32_t base = blockIdx.x * kRT; base < n; base += gridDim.x * kRT) {
+    const uint32_t j = base + threadIdx.x;
+    const unsigned long long kj = j < n ? key[j] : ~0ull;
+    uint32_t rank = 0;
+    for (uint32_t t0 = 0; t0 < n; t0 += kRT) {
+      __syncthreads();
+      tile[threadIdx.x] = (t0 + threadIdx.x < n) ? key[t0 + threadIdx.x] : ~0ull;
+      __syncthreads();
+      const uint32_t lim = min(static_cast<uint32_t>(kRT), n - t0);
+#pragma unroll 8
+      for (uint32_t i = 0; i < lim; ++i) rank += tile[i] < kj ? 1u : 0u;
+    }
+    if (j < n) {
+      out_key[rank] = kj;
+      out_node[rank] = node[j];
+    }
+  }
+}
+
+__device__ __forceinline__ uint32_t lower_bound_u64(const unsigned long long* a, uint32_t n,
+                                                    unsigned long long v) {
+  uint32_t lo = 0, hi = n;
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (a[mid] < v)
+      lo = mid + 1;
+    else
+      hi = mid;
+  }
+  return lo;
+}
+
+// E6: merge the sorted survivors into the queue remainder (push, search.hpp:139).
+__global__ void merge_kernel(const EpochState* st, Queue q, const unsigned long long* __restrict__ skey,
+                             const bbs_node* __restrict__ snode) {
+  if (st->n_children == 0) return;
+  const uint32_t cur = st->cur;
+  const uint32_t n_cons = st->n_cons;
+  const uint32_t n_rem = st->q_len - n_cons;
+  const uint32_t n_s = st->n_surv;
+  const unsigned long long* __restrict__ qk = q.key[cur] + n_cons;
+  const bbs_node* __restrict__ qn = q.node[cur] + n_cons;
+  unsigned long long* __restrict__ ok = q.key[cur ^ 1];
+  bbs_node* __restrict__ on = q.node[cur ^ 1];
+  const uint32_t total = n_rem + n_s;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    if (i < n_rem) {
+      const unsigned long long k = qk[i];
+      const uint32_t pos = i + lower_bound_u64(skey, n_s, k);
+      ok[pos] = k;
+      on[pos] = qn[i];
+    } else {
+      const uint32_t j = i - n_rem;
+      const unsigned long long k = skey[j];
+      const uint32_t pos = j + lower_bound_u64(qk, n_rem, k);
+      ok[pos] = k;
+      on[pos] = snode[j];
+    }
+  }
+}
+
+// E7: swap queue buffers; the loop ends when queue and pending are empty.
+__global__ void finalize_kernel(EpochState* st) {
+  if (st->n_children == 0) return;
+  const uint32_t len = st->q_len - st->n_cons + st->n_surv;
+  st->q_len = len;
+  st->cur ^= 1u;
+  st->q_peak = max(st->q_peak, len);
+  if (len == 0) st->active = 0;
+}
+
+// Root survivors -> queue entries (seq = rank in initial_nodes order).
+__global__ void roots_to_queue_kernel(const unsigned long long* __restrict__ ref_idx, uint32_t n,
+                                      const int32_t* __restrict__ scores, BoxParams bp,
+                                      int strategy, unsigned long long* __restrict__ key,
+                                      bbs_node* __restrict__ node) {
+  const unsigned long long nrot = static_cast<unsigned long long>(bp.nr) * bp.np * bp.nw;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const unsigned long long r = ref_idx[i];
+    const unsigned long long rot = r % nrot, t = r / nrot;
+    bbs_node nd;
+    nd.iyaw = static_cast<int32_t>(rot % bp.nw);
+    nd.ipitch = static_cast<int32_t>((rot / bp.nw) % bp.np);
+    nd.iroll = static_cast<int32_t>(rot / (static_cast<unsigned long long>(bp.nw) * bp.np));
+    nd.iz = bp.z0 + static_cast<int32_t>(t % bp.nz);
+    nd.iy = bp.y0 + static_cast<int32_t>((t / bp.nz) % bp.ny);
+    nd.ix = bp.x0 + static_cast<int32_t>(t / (static_cast<unsigned long long>(bp.nz) * bp.ny));
+    nd.level = bp.level;
+    nd.score = scores[r];
+    node[i] = nd;
+    key[i] = queue_key(strategy, nd.score, nd.level, i);
+  }
+}
+
+__global__ void gather_nodes_kernel(const uint32_t* __restrict__ perm, const bbs_node* __restrict__ in,
+                                    bbs_node* __restrict__ out, uint32_t n) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    out[i] = in[perm[i]];
+}
+
+__global__ void iota_kernel(uint32_t* __restrict__ p, uint32_t n) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) p[i] = i;
+}
+
+__global__ void soa_kernel(const double* __restrict__ aos, uint64_t k, double* __restrict__ soa) {
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < k;
+       i += uint64_t(gridDim.x) * blockDim.x) {
+    soa[i] = aos[3 * i];
+    soa[k + i] = aos[3 * i + 1];
+    soa[2 * k + i] = aos[3 * i + 2];
+  }
+}
+
+// Own root predicate for DeviceSelect: ref index own(i) = i * world + rank.
+struct OwnRootSurvives {
+  const int32_t* scores;
+  int32_t threshold;
+  __host__ __device__ bool operator()(const unsigned long long& r) const {
+    return scores[r] >= threshold;
+  }
+};
+struct OwnIndex {
+  unsigned long long world, rank;
+  __host__ __device__ unsigned long long operator()(const unsigned long long& i) const {
+    return i * world + rank;
+  }
+};
+
+unsigned grid1(uint64_t n, int threads = 256) {
+  return static_cast<unsigned>(std::min<uint64_t>(std::max<uint64_t>((n + threads - 1) / threads, 1), 148ull * 16));
+}
+
+struct Events {
+  std::vector<cudaEvent_t> ev;
+  size_t used = 0;
+  cudaEvent_t next() {
+    if (used == ev.size()) {
+      cudaEvent_t e;
+      BBS_CUDA(cudaEventCreate(&e));
+      ev.push_back(e);
+    }
+    return ev[used++];
+  }
+  ~Events() {
+    for (auto e : ev) cudaEventDestroy(e);
+  }
+};
+
+float elapsed(cudaEvent_t a, cudaEvent_t b) {
+  float ms = 0;
+  BBS_CUDA(cudaEventElapsedTime(&ms, a, b));
+  return ms;
+}
+
+// trans_index_range, nodes.hpp:53-56 (x86 conversion semantics).
+void trans_index_range(double lo, double hi, double cell, int32_t* mn, int32_t* mx) {
+  const double f = std::floor(lo / cell), c = std::ceil(hi / cell);
+  *mn = (f >= -2147483648.0 && f < 2147483648.0) ? static_cast<int32_t>(f) : INT32_MIN;
+  *mx = (c >= -2147483648.0 && c < 2147483648.0) ? static_cast<int32_t>(c) : INT32_MIN;
+}
+
+template <typename T>
+T* dalloc(size_t n, cudaStream_t s) {
+  T* p = nullptr;
+  BBS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), std::max<size_t>(n, 1) * sizeof(T), s));
+  return p;
+}
+
+}  // namespace
+
+void set_pool_retention(int device) {
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+    uint64_t thr = ~0ull;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+}
+
+bbs_scan* upload_scan(bbs_map* m, const double* xyz, uint64_t k) {
+  DeviceGuard g(m->device);
+  auto* sc = new bbs_scan();
+  sc->map = m;
+  sc->k = k;
+  sc->host.assign(xyz, xyz + 3 * k);
+  sc->d_max = k ? host_max_range(xyz, k) : 0.0;
+  cudaStream_t s = m->stream;
+  sc->soa = dalloc<double>(3 * std::max<uint64_t>(k, 1), s);
+  if (k) {
+    double* aos = dalloc<double>(3 * k, s);
+    BBS_CUDA(cudaMemcpyAsync(aos, xyz, 3 * k * sizeof(double), cudaMemcpyHostToDevice, s));
+    soa_kernel<<<grid1(k), 256, 0, s>>>(aos, k, sc->soa);
+    BBS_CUDA(cudaGetLastError());
+    BBS_CUDA(cudaFreeAsync(aos, s));
+  }
+  BBS_CUDA(cudaStreamSynchronize(s));
+  return sc;
+}
+
+// search(), search.hpp:72-186, on the device.  `shard` may be null.
+void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const bbs_shard* shard,
+                bbs_search_result* out) {
+  // validation, search.hpp:79-89, same order and messages
+  if (scan->k == 0) throw Error(BBS_ERR_DEGENERATE_SCAN, "search: empty scan");
+  if (m->r != cfg.min_resolution) throw Error(BBS_ERR_CONFIG, "search: config r does not match the map");
+  if (cfg.max_level < 1 || cfg.max_level > m->max_level)
+    throw Error(BBS_ERR_CONFIG, "search: max_level must be in [1, map max level]");
+  if (cfg.batch_size < 1) throw Error(BBS_ERR_CONFIG, "search: batch_size must be >= 1");
+  if (!(cfg.score_threshold_fraction > 0.0 && cfg.score_threshold_fraction <= 1.0))
+    throw Error(BBS_ERR_CONFIG, "search: score_threshold_fraction must be in (0, 1]");
+  const double d_max = cfg.has_d_max ? cfg.d_max : scan->d_max;
+  if (!(d_max > 0.0)) throw Error(BBS_ERR_DEGENERATE_SCAN, "search: maximum scan range is zero");
+  const HostGrid grid = make_grid(cfg, d_max);
+  const bbs_aabb tr = cfg.has_translation_range ? cfg.translation_range : m->bbox;
+  if (scan->k > static_cast<uint64_t>(kMaxScorePoints))
+    throw Error(BBS_ERR_TOO_LARGE, "search: scans above 1048575 points are not supported");
+  if (cfg.batch_size > (1ull << 28))
+    throw Error(BBS_ERR_TOO_LARGE, "search: batch_size above 2^28 is not supported");
+  const int rank = shard ? shard->rank : 0;
+  const int world = shard ? std::max(1, shard->world_size) : 1;
+  if (rank < 0 || rank >= world) throw Error(BBS_ERR_CONFIG, "search: shard rank out of range");
+
+  DeviceGuard dg(m->device);
+  cudaStream_t s = m->stream;
+  const uint64_t K = scan->k;
+  const int32_t threshold =
+      static_cast<int32_t>(std::floor(cfg.score_threshold_fraction * static_cast<double>(K)));
+  const int L = cfg.max_level;
+
+  // root set, initial_nodes (nodes.hpp:60-85)
+  const double cell = std::ldexp(cfg.min_resolution, L);
+  int32_t x0, x1, y0, y1, z0, z1;
+  trans_index_range(tr.min.x, tr.max.x, cell, &x0, &x1);
+  trans_index_range(tr.min.y, tr.max.y, cell, &y0, &y1);
+  trans_index_range(tr.min.z, tr.max.z, cell, &z0, &z1);
+  const int64_t nx = static_cast<int64_t>(x1) - x0 + 1, ny = static_cast<int64_t>(y1) - y0 + 1,
+                nz = static_cast<int64_t>(z1) - z0 + 1;
+  const int64_t nr = grid.axis(0, L).index_count(), np = grid.axis(1, L).index_count(),
+                nw = grid.axis(2, L).index_count();
+  const int64_t total = nx * ny * nz * nr * np * nw;
+  if (total <= 0) throw Error(BBS_ERR_EMPTY_SEARCH_SPACE, "initial node set is empty");
+  if (nx * ny * nz >= (1ll << 32) || nr * np * nw >= (1ll << 32) || total >= (1ll << 40))
+    throw Error(BBS_ERR_TOO_LARGE, "search: root set too large");
+
+  GridView gv;
+  const std::vector<double> lut = build_lut(grid, &gv);
+  double2* d_lut = dalloc<double2>(lut.size() / 2, s);
+  BBS_CUDA(cudaMemcpyAsync(d_lut, lut.data(), lut.size() * sizeof(double), cudaMemcpyHostToDevice, s));
+  gv.lut = d_lut;
+  const ScanView sv{scan->soa, scan->soa + K, scan->soa + 2 * K, static_cast<uint32_t>(K)};
+  const uint64_t maxc = max_children(grid);
+  const uint64_t pend_cap = cfg.batch_size + maxc;
+  const int strategy = cfg.strategy;
+
+  Events evs;
+  cudaEvent_t ev_start = evs.next(), ev_roots0 = evs.next(), ev_roots1 = evs.next(),
+              ev_loop = evs.next();
+  BBS_CUDA(cudaEventRecord(ev_start, s));
+
+  // ---- root batch (search.hpp:111-124) ----
+  BoxParams bp{};
+  bp.level = L;
+  bp.x0 = x0;
+  bp.y0 = y0;
+  bp.z0 = z0;
+  bp.nx = static_cast<uint32_t>(nx);
+  bp.ny = static_cast<uint32_t>(ny);
+  bp.nz = static_cast<uint32_t>(nz);
+  bp.nr = static_cast<uint32_t>(nr);
+  bp.np = static_cast<uint32_t>(np);
+  bp.nw = static_cast<uint32_t>(nw);
+  bp.rank = static_cast<uint32_t>(rank);
+  bp.world = static_cast<uint32_t>(world);
+  {
+    const uint64_t ntrans = static_cast<uint64_t>(nx * ny * nz);
+    uint64_t g = static_cast<uint64_t>(world), b2 = static_cast<uint64_t>(nr * np * nw) % world;
+    while (b2) {
+      const uint64_t t = g % b2;
+      g = b2;
+      b2 = t;
+    }
+    const uint64_t P = static_cast<uint64_t>(world) / g;
+    const uint64_t own_max = (ntrans + P - 1) / P;
+    bp.n_tchunks = static_cast<uint32_t>((own_max + kBoxTransPerCta - 1) / kBoxTransPerCta);
+    const double tmax = std::max({std::fabs(static_cast<double>(x0)), std::fabs(static_cast<double>(x1)),
+                                  std::fabs(static_cast<double>(y0)), std::fabs(static_cast<double>(y1)),
+                                  std::fabs(static_cast<double>(z0)), std::fabs(static_cast<double>(z1))});
+    bp.tmax = tmax + 2.0;
+  }
+  const uint64_t n_own = (static_cast<uint64_t>(total) + world - 1 - rank) / world;
+  int32_t* root_scores = dalloc<int32_t>(static_cast<size_t>(total), s);
+  BBS_CUDA(cudaEventRecord(ev_roots0, s));
+  launch_score_box(m->view, gv, sv, bp, root_scores, s);
+  BBS_CUDA(cudaEventRecord(ev_roots1, s));
+
+  // survivors >= threshold among own roots, in initial_nodes order
+  unsigned long long* surv_idx = dalloc<unsigned long long>(n_own, s);
+  int* d_nsel = dalloc<int>(1, s);
+  {
+    cub::CountingInputIterator<unsigned long long> cnt(0);
+    cub::TransformInputIterator<unsigned long long, OwnIndex, cub::CountingInputIterator<unsigned long long>>
+        own(cnt, OwnIndex{static_cast<unsigned long long>(world), static_cast<unsigned long long>(rank)});
+    size_t tb = 0;
+    BBS_CUDA(cub::DeviceSelect::If(nullptr, tb, own, surv_idx, d_nsel, static_cast<int64_t>(n_own),
+                                   OwnRootSurvives{root_scores, threshold}, s));
+    void* temp = dalloc<unsigned char>(tb, s);
+    BBS_CUDA(cub::DeviceSelect::If(temp, tb, own, surv_idx, d_nsel, static_cast<int64_t>(n_own),
+                                   OwnRootSurvives{root_scores, threshold}, s));
+    BBS_CUDA(cudaFreeAsync(temp, s));
+  }
+  int n_root_surv = 0;
+  BBS_CUDA(cudaMemcpyAsync(&n_root_surv, d_nsel, sizeof(int), cudaMemcpyDeviceToHost, s));
+  BBS_CUDA(cudaStreamSynchronize(s));
+
+  // queue buffers
+  const int E = (shard && shard->allreduce_max) ? 1 : 4;  // epochs per host check
+  uint64_t qcap = static_cast<uint64_t>(n_root_surv) + static_cast<uint64_t>(E + 1) * pend_cap;
+  Queue q{};
+  for (int i = 0; i < 2; ++i) {
+    q.key[i] = dalloc<unsigned long long>(qcap, s);
+    q.node[i] = dalloc<bbs_node>(qcap, s);
+  }
+  if (n_root_surv > 0) {
+    // keys in initial_nodes order (seq = position), then sort by key
+    unsigned long long* k0 = dalloc<unsigned long long>(n_root_surv, s);
+    bbs_node* n0 = dalloc<bbs_node>(n_root_surv, s);
+    uint32_t* perm0 = dalloc<uint32_t>(n_root_surv, s);
+    uint32_t* perm1 = dalloc<uint32_t>(n_root_surv, s);
+    roots_to_queue_kernel<<<grid1(n_root_surv), 256, 0, s>>>(surv_idx, n_root_surv, root_scores, bp,
+                                                             strategy, k0, n0);
+    BBS_CUDA(cudaGetLastError());
+    iota_kernel<<<grid1(n_root_surv), 256, 0, s>>>(perm0, n_root_surv);
+    cub::DoubleBuffer<unsigned long long> dk(k0, q.key[0]);
+    cub::DoubleBuffer<uint32_t> dv(perm0, perm1);
+    size_t tb = 0;
+    BBS_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, dk, dv, n_root_surv, 0, 64, s));
+    void* temp = dalloc<unsigned char>(tb, s);
+    BBS_CUDA(cub::DeviceRadixSort::SortPairs(temp, tb, dk, dv, n_root_surv, 0, 64, s));
+    if (dk.Current() != q.key[0])
+      BBS_CUDA(cudaMemcpyAsync(q.key[0], dk.Current(), n_root_surv * 8ull, cudaMemcpyDeviceToDevice, s));
+    gather_nodes_kernel<<<grid1(n_root_surv), 256, 0, s>>>(dv.Current(), n0, q.node[0], n_root_surv);
+    BBS_CUDA(cudaGetLastError());
+    for (void* p : {static_cast<void*>(k0), static_cast<void*>(n0), static_cast<void*>(perm0),
+                    static_cast<void*>(perm1), temp})
+      BBS_CUDA(cudaFreeAsync(p, s));
+  }
+  BBS_CUDA(cudaFreeAsync(surv_idx, s));
+  BBS_CUDA(cudaFreeAsync(d_nsel, s));
+  BBS_CUDA(cudaFreeAsync(root_scores, s));
+
+  EpochState h0{};
+  h0.best = threshold;
+  h0.q_len = static_cast<uint32_t>(n_root_surv);
+  h0.cur = 0;
+  h0.seq = static_cast<unsigned long long>(n_root_surv);
+  h0.nodes_generated = n_own;
+  h0.nodes_pruned = n_own - static_cast<uint64_t>(n_root_surv);
+  h0.batches_flushed = 1;
+  h0.last_best_epoch = -1;
+  h0.active = n_root_surv > 0 ? 1 : 0;
+  h0.q_peak = h0.q_len;
+  EpochState* d_st = dalloc<EpochState>(1, s);
+  EpochState* h_st = nullptr;
+  BBS_CUDA(cudaMallocHost(reinterpret_cast<void**>(&h_st), sizeof(EpochState)));
+  BBS_CUDA(cudaMemcpyAsync(d_st, &h0, sizeof(h0), cudaMemcpyHostToDevice, s));
+  BBS_CUDA(cudaEventRecord(ev_loop, s));
+
+  bbs_node* pending = dalloc<bbs_node>(pend_cap, s);
+  int32_t* pscores = dalloc<int32_t>(pend_cap, s);
+  const uint64_t exp_cap = pend_cap / 8 + 2;
+  uint32_t* exp_parent = dalloc<uint32_t>(exp_cap, s);
+  uint32_t* exp_off = dalloc<uint32_t>(exp_cap, s);
+  unsigned long long* s_key = dalloc<unsigned long long>(pend_cap, s);
+  bbs_node* s_node = dalloc<bbs_node>(pend_cap, s);
+  unsigned long long* s_key2 = dalloc<unsigned long long>(pend_cap, s);
+  bbs_node* s_node2 = dalloc<bbs_node>(pend_cap, s);
+  const uint64_t trace_cap = cfg.collect_trace ? std::max<uint64_t>(out->trace_capacity, 1) : 0;
+  int32_t* d_trace = dalloc<int32_t>(std::max<uint64_t>(trace_cap, 1), s);
+  const uint32_t ptiles = choose_ptiles((pend_cap + 7) / 8, static_cast<uint32_t>(K));
+
+  std::vector<cudaEvent_t> pass_ev;                  // after each frontier pass
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> score_ev;
+  EpochState hs = h0;
+  bool self_active = h0.active != 0;
+  bool others_active = false;
+  auto exchange = [&]() {
+    if (!(shard && shard->allreduce_max)) return;
+    int64_t v[2] = {hs.best, self_active ? 1 : 0};
+    if (shard->allreduce_max(v, 2, shard->user) != 0)
+      throw Error(BBS_ERR_GENERIC, "search: incumbent all-reduce failed");
+    others_active = v[1] != 0;
+    if (v[0] > hs.best) {
+      const int32_t nb = static_cast<int32_t>(v[0]);
+      hs.best = nb;
+      BBS_CUDA(cudaMemcpyAsync(reinterpret_cast<char*>(d_st) + offsetof(EpochState, best), &nb,
+                               sizeof(nb), cudaMemcpyHostToDevice, s));
+      BBS_CUDA(cudaStreamSynchronize(s));  // nb lives on this stack frame
+    }
+  };
+  exchange();  // after the root batch
+
+  while (self_active || others_active) {
+    // capacity: the queue grows by at most pend_cap per epoch
+    if (static_cast<uint64_t>(hs.q_len) + static_cast<uint64_t>(E + 1) * pend_cap > qcap) {
+      const uint64_t ncap = 2 * (static_cast<uint64_t>(hs.q_len) + static_cast<uint64_t>(E + 1) * pend_cap);
+      for (int i = 0; i < 2; ++i) {
+        unsigned long long* nk = dalloc<unsigned long long>(ncap, s);
+        bbs_node* nn = dalloc<bbs_node>(ncap, s);
+        if (hs.q_len) {
+          BBS_CUDA(cudaMemcpyAsync(nk, q.key[i], hs.q_len * 8ull, cudaMemcpyDeviceToDevice, s));
+          BBS_CUDA(cudaMemcpyAsync(nn, q.node[i], hs.q_len * sizeof(bbs_node), cudaMemcpyDeviceToDevice, s));
+        }
+        BBS_CUDA(cudaFreeAsync(q.key[i], s));
+        BBS_CUDA(cudaFreeAsync(q.node[i], s));
+        q.key[i] = nk;
+        q.node[i] = nn;
+      }
+      qcap = ncap;
+    }
+    const int n_ep = self_active ? E : 1;
+    for (int e = 0; e < n_ep; ++e) {
+      frontier_kernel<<<1, kFT, 0, s>>>(d_st, q, gv, cfg.batch_size, exp_parent, exp_off, d_trace,
+                                        trace_cap);
+      BBS_CUDA(cudaGetLastError());
+      cudaEvent_t pe = evs.next();
+      BBS_CUDA(cudaEventRecord(pe, s));
+      pass_ev.push_back(pe);
+      branch_kernel<<<grid1(pend_cap), 256, 0, s>>>(d_st, q, gv, exp_parent, exp_off, pending);
+      BBS_CUDA(cudaGetLastError());
+      if (ptiles > 1) BBS_CUDA(cudaMemsetAsync(pscores, 0, pend_cap * sizeof(int32_t), s));
+      cudaEvent_t s0 = evs.next(), s1 = evs.next();
+      BBS_CUDA(cudaEventRecord(s0, s));
+      launch_score_runs8(m->view, gv, sv, pending,
+                         reinterpret_cast<const uint32_t*>(reinterpret_cast<char*>(d_st) +
+                                                           offsetof(EpochState, n_children)),
+                         static_cast<uint32_t>(pend_cap), ptiles, pscores, s);
+      BBS_CUDA(cudaEventRecord(s1, s));
+      score_ev.emplace_back(s0, s1);
+      survivors_kernel<<<1, kST, 0, s>>>(d_st, strategy, pending, pscores, s_key, s_node);
+      BBS_CUDA(cudaGetLastError());
+      rank_sort_kernel<<<grid1(pend_cap, kRT), kRT, 0, s>>>(d_st, s_key, s_node, s_key2, s_node2);
+      BBS_CUDA(cudaGetLastError());
+      merge_kernel<<<grid1(qcap), 256, 0, s>>>(d_st, q, s_key2, s_node2);
+      BBS_CUDA(cudaGetLastError());
+      finalize_kernel<<<1, 1, 0, s>>>(d_st);
+      BBS_CUDA(cudaGetLastError());
+    }
+    BBS_CUDA(cudaMemcpyAsync(h_st, d_st, sizeof(EpochState), cudaMemcpyDeviceToHost, s));
+    BBS_CUDA(cudaStreamSynchronize(s));
+    hs = *h_st;
+    self_active = hs.active != 0;
+    if (shard && shard->allreduce_max)
+      exchange();
+    else
+      others_active = false;
+  }
+  cudaEvent_t ev_end = evs.next();
+  BBS_CUDA(cudaEventRecord(ev_end, s));
+  BBS_CUDA(cudaEventSynchronize(ev_end));
+  BBS_CUDA(cudaMemcpyAsync(h_st, d_st, sizeof(EpochState), cudaMemcpyDeviceToHost, s));
+  BBS_CUDA(cudaStreamSynchronize(s));
+  hs = *h_st;
+
+  // ---- results ----
+  std::memset(&out->stats, 0, sizeof(out->stats));
+  out->scan_points = K;
+  out->score_threshold = threshold;
+  out->stats.nodes_generated = hs.nodes_generated;
+  out->stats.nodes_pruned = hs.nodes_pruned;
+  out->stats.batches_flushed = hs.batches_flushed;
+  out->stats.initial_nodes_ms = elapsed(ev_start, ev_loop);
+  const float loop_ms = elapsed(ev_loop, ev_end);
+  if (hs.matched && hs.last_best_epoch >= 0 && hs.last_best_epoch < static_cast<int>(pass_ev.size())) {
+    const float fb = elapsed(ev_loop, pass_ev[static_cast<size_t>(hs.last_best_epoch)]);
+    out->stats.find_best_score_ms = fb;
+    out->stats.pop_remaining_queue_ms = loop_ms - fb;
+  } else {
+    out->stats.find_best_score_ms = loop_ms;
+    out->stats.pop_remaining_queue_ms = 0.0;
+  }
+  out->device_ms = elapsed(ev_start, ev_end);
+  out->root_score_ms = elapsed(ev_roots0, ev_roots1);
+  double esm = 0;
+  for (auto& pr : score_ev) esm += elapsed(pr.first, pr.second);
+  out->epoch_score_ms = esm;
+  out->epochs = hs.epochs;
+  out->root_nodes = n_own;
+  out->lookups = hs.nodes_generated * K;
+  out->queue_peak = hs.q_peak;
+  out->trace_length = cfg.collect_trace ? hs.trace_len : 0;
+  if (cfg.collect_trace && out->best_score_trace && hs.trace_len) {
+    const uint64_t nt = std::min<uint64_t>(hs.trace_len, out->trace_capacity);
+    BBS_CUDA(cudaMemcpyAsync(out->best_score_trace, d_trace, nt * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+  }
+  int32_t best = hs.best;
+  bbs_node best_node = hs.best_node;
+  int matched = hs.matched;
+  // winner election across ranks: max of (score, world-1-rank) among matched
+  if (shard && shard->allreduce_max && world > 1) {
+    int64_t key[1] = {matched ? (static_cast<int64_t>(best) << 32) | static_cast<int64_t>(world - 1 - rank) : -1};
+    if (shard->allreduce_max(key, 1, shard->user) != 0)
+      throw Error(BBS_ERR_GENERIC, "search: winner election failed");
+    const int winner = key[0] < 0 ? -1 : static_cast<int>(world - 1 - (key[0] & 0xffffffff));
+    int64_t nv[8];
+    const int32_t* f = reinterpret_cast<const int32_t*>(&best_node);
+    for (int i = 0; i < 8; ++i) nv[i] = rank == winner ? static_cast<int64_t>(f[i]) : INT64_MIN;
+    if (shard->allreduce_max(nv, 8, shard->user) != 0)
+      throw Error(BBS_ERR_GENERIC, "search: winner broadcast failed");
+    if (winner >= 0) {
+      int32_t* bf = reinterpret_cast<int32_t*>(&best_node);
+      for (int i = 0; i < 8; ++i) bf[i] = static_cast<int32_t>(nv[i]);
+      best = static_cast<int32_t>(key[0] >> 32);
+      matched = 1;
+    } else {
+      matched = 0;
+    }
+  }
+  out->matched = matched;
+  out->best_score = best;
+  out->best_node = best_node;
+  std::memset(&out->best_pose, 0, sizeof(out->best_pose));
+  if (matched) {
+    // node_pose(best).normalized(), search.hpp:183, nodes.hpp:33-43
+    const double c = std::ldexp(cfg.min_resolution, best_node.level);
+    out->best_pose.x = c * static_cast<double>(best_node.ix);
+    out->best_pose.y = c * static_cast<double>(best_node.iy);
+    out->best_pose.z = c * static_cast<double>(best_node.iz);
+    out->best_pose.roll = grid.axis(0, best_node.level).angle(best_node.iroll);
+    out->best_pose.pitch = grid.axis(1, best_node.level).angle(best_node.ipitch);
+    const double two_pi = 6.283185307179586476925286766559;
+    double y = std::fmod(grid.axis(2, best_node.level).angle(best_node.iyaw), two_pi);
+    if (y < 0.0) y += two_pi;
+    if (y >= two_pi) y = 0.0;
+    out->best_pose.yaw = y;
+  }
+
+  for (void* p : {static_cast<void*>(d_lut), static_cast<void*>(q.key[0]), static_cast<void*>(q.key[1]),
+                  static_cast<void*>(q.node[0]), static_cast<void*>(q.node[1]), static_cast<void*>(d_st),
+                  static_cast<void*>(pending), static_cast<void*>(pscores),
+                  static_cast<void*>(exp_parent), static_cast<void*>(exp_off), static_cast<void*>(s_key),
+                  static_cast<void*>(s_node), static_cast<void*>(s_key2), static_cast<void*>(s_node2),
+                  static_cast<void*>(d_trace)})
+    BBS_CUDA(cudaFreeAsync(p, s));
+  BBS_CUDA(cudaStreamSynchronize(s));
+  cudaFreeHost(h_st);
+}
+
+// batch_evaluate on device nodes (search.hpp:23-34).
+void batch_evaluate_device(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, double d_max,
+                           bbs_node* d_nodes, uint64_t n, cudaStream_t s, const int32_t* lo,
+                           const int32_t* hi) {
+  const double dm = d_max > 0 ? d_max : scan->d_max;
+  const HostGrid grid = make_grid(cfg, dm);
+  GridView gv;
+  const std::vector<double> lut = build_lut(grid, &gv, lo, hi);
+  double2* d_lut = dalloc<double2>(lut.size() / 2, s);
+  BBS_CUDA(cudaMemcpyAsync(d_lut, lut.data(), lut.size() * sizeof(double), cudaMemcpyHostToDevice, s));
+  gv.lut = d_lut;
+  const uint64_t K = scan->k;
+  const ScanView sv{scan->soa, scan->soa + K, scan->soa + 2 * K, static_cast<uint32_t>(K)};
+  score_nodes_general(m->view, gv, sv, d_nodes, n, s);
+  BBS_CUDA(cudaFreeAsync(d_lut, s));
+}
+
+}  // namespace bbs
+
+bbs_scan::~bbs_scan() {
+  if (soa && map) {
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(map->device);
+    cudaFree(soa);
+    cudaSetDevice(prev);
+  }
+}
