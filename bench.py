@@ -1,0 +1,430 @@
+#!/usr/bin/env python
+"""bench.py — headline benchmark of the B200 batched BnB scan matcher.
+
+Workload (BASELINE.json configs[1], SURVEY §8d "C2 campus"): one global
+localization of a K=10,000-point scan against a ~5M-point synthetic campus map
+(gen_scene 300x300x30 m, 60 boxes; r = 0.2 m, l_max = 5 (6 levels), full yaw,
+roll/pitch +-0.02 rad, BFS, RotoTrans, b = 10,000, threshold 0.95).  A "step"
+is one search() (root batch + every flush epoch until the queue drains).
+
+  value   candidate score evals/s = nodes_generated (all ranks) / max-rank
+          device time of the K timed steps (CUDA events on the search stream,
+          scan and map resident in HBM; L2 flushed before every step)
+  e2e     same metric through the public host API bbs_search(): the scan is
+          copied from pinned host memory and the result read back every step
+          (host wall clock around each call)
+  cpu_baseline / --impl reference
+          the UNMODIFIED reference (oracle/_ref, bnbloc::batch_evaluate with
+          workers = all host threads) on a bounded sample of the same root
+          batch: evals/s
+
+N > 1 (torchrun, NCCL): the root set is sharded (root i -> rank i % N) and the
+incumbent is max-all-reduced after every epoch; total work per
+search is fixed, so scaling is "strong".
+"""
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # name: scene spec, seed, search params, K
+    "c2": dict(workload="C2 campus: 300x300x30 m box world (~5M map pts), 10k-pt scan, "
+                        "r=0.2 m, 6 levels, 360 deg yaw, +-0.02 rad roll/pitch, BFS RotoTrans b=10000",
+               spec=dict(size_x=300.0, size_y=300.0, size_z=30.0, num_boxes=60, min_box_side=6.0,
+                         max_box_side=30.0, min_box_height=8.0, map_spacing=0.19, scan_spacing=0.3,
+                         scan_range=60.0, min_scan_points=400),
+               seed=1, r=0.2, max_level=5, rp=0.02, K=10000),
+    "c1": dict(workload="C1 room: 20x20x4 m (~200k map pts), 2k-pt scan, r=0.1 m, 6 levels, "
+                        "360 deg yaw, +-5 deg roll/pitch, BFS RotoTrans b=10000",
+               spec=dict(size_x=20.0, size_y=20.0, size_z=4.0, num_boxes=8, min_box_side=1.0,
+                         max_box_side=4.0, min_box_height=1.0, map_spacing=0.058, scan_spacing=0.1,
+                         scan_range=10.0, min_scan_points=400),
+               seed=1, r=0.1, max_level=5, rp=0.0873, K=2000),
+}
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+        self.lines = []
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except (OSError, FileNotFoundError):
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=2)
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[3:7]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def build_inputs(B, cfgd):
+    spec = B.SceneSpec.default(**cfgd["spec"])
+    t = time.time()
+    map_pts, raw_scan, gt = B.gen_scene(spec, cfgd["seed"])
+    scan = B.cut_scan(raw_scan, min(cfgd["K"], raw_scan.shape[0]), 7)
+    log(f"scene: {map_pts.shape[0]} map pts, raw scan {raw_scan.shape[0]}, K={scan.shape[0]} "
+        f"({time.time() - t:.1f}s)")
+    return map_pts, scan, gt
+
+
+def search_config(B, cfgd):
+    return B.SearchConfig(min_resolution=cfgd["r"], max_level=cfgd["max_level"],
+                          roll_pitch_half_range=cfgd["rp"], strategy=B.Strategy.BFS,
+                          branch_mode=B.BranchMode.ROTO_TRANS, batch_size=10000)
+
+
+def reference_sample(map_pts, scan, cfgd, target_s, log_prefix=""):
+    """Time the UNMODIFIED reference (oracle/_ref) batch_evaluate on a bounded
+    sample of the root batch.  Returns (evals/s, sample description, cores)."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    from pyoracle import Reference, default_config  # noqa: E402  (cpu_baseline leg only)
+    ref = Reference()
+    t = time.time()
+    rmap = ref.map_build(map_pts, cfgd["r"], cfgd["max_level"], 0.3, 8 << 30)
+    log(f"{log_prefix}reference map build (collision_target 0.3): {time.time() - t:.1f}s")
+    cfg = default_config(min_resolution=cfgd["r"], max_level=cfgd["max_level"],
+                         roll_pitch_half_range=cfgd["rp"])
+    d_max = ref.max_range(scan)
+    roots = ref.initial_nodes(cfg, d_max, rmap.bbox())
+    rng = np.random.default_rng(11)
+    cores = os.cpu_count() or 1
+    n = 512
+    while True:
+        sample = roots[rng.choice(roots.shape[0], size=min(n, roots.shape[0]), replace=False)]
+        t = time.time()
+        rmap.batch_evaluate(scan, cfg, sample, d_max=d_max, workers=cores)
+        dt = time.time() - t
+        if dt >= 0.25 * target_s or n >= roots.shape[0]:
+            break
+        n = int(min(roots.shape[0], n * max(2.0, 0.3 * target_s / max(dt, 1e-3))))
+    return ref, rmap, cfg, d_max, roots, sample.shape[0] / dt, sample.shape[0], cores
+
+
+def run_reference_arm(args, cfgd):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    import paper_2310_10023_b200 as B  # scene generator only (no GPU work)
+    map_pts, scan, _ = build_inputs(B, cfgd)
+    ref, rmap, cfg, d_max, roots, _, n, cores = reference_sample(map_pts, scan, cfgd, 6.0)
+    rng = np.random.default_rng(5)
+    vals = []
+    t_all = 0.0
+    for step in range(args.warmup + args.steps):
+        sample = roots[rng.choice(roots.shape[0], size=n, replace=False)]
+        t = time.time()
+        rmap.batch_evaluate(scan, cfg, sample, d_max=d_max, workers=cores)
+        dt = time.time() - t
+        if step >= args.warmup:
+            vals.append(n / dt)
+            t_all += dt
+    value = args.steps * n / t_all
+    sample_desc = (f"{n} root nodes per step drawn uniformly from initial_nodes() of the workload "
+                   f"(level {cfgd['max_level']}), bnbloc::batch_evaluate with workers={cores}")
+    line = {
+        "impl": "reference", "metric": "candidate score evals/sec", "value": value,
+        "unit": "evals/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * t_all / args.steps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": cfgd["workload"], "K": int(scan.shape[0])},
+        "cpu_baseline": {"value": value, "unit": "evals/s", "cores": cores, "kind": "reference",
+                         "sample": sample_desc},
+        "e2e": {"value": value, "unit": "evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f), "measured"
+    except (OSError, ValueError):
+        return {"hbm_gbs": 6650.0}, "fallback"
+
+
+def profile_traffic(kernel):
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            return json.load(f).get(kernel)
+    except (OSError, ValueError):
+        return None
+
+
+def run_b200_arm(args, cfgd):
+    import torch
+    world, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_2310_10023_b200 as B
+
+    map_pts, scan, gt = build_inputs(B, cfgd)
+    cfg = search_config(B, cfgd)
+    stream = torch.cuda.current_stream()
+    vmap = B.MultiResVoxelMap.build(map_pts, cfgd["r"], cfgd["max_level"],
+                                    layout=B.Layout[args.layout.upper()], device=local)
+    build_ms = vmap.build_ms()
+    vmap.set_stream(stream.cuda_stream)
+    layouts = [vmap.level(l).layout().name for l in range(cfgd["max_level"] + 1)]
+    level_bytes = [vmap.level(l).device_bytes() for l in range(cfgd["max_level"] + 1)]
+    log(f"rank {rank}: map build {build_ms:.1f} ms device, layouts {layouts}, bytes {level_bytes}")
+    dscan = B.DeviceScan(vmap, scan)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")  # > 126 MB L2
+
+    if world > 1:
+        import torch.distributed as dist
+        red = torch.zeros(8, dtype=torch.int64, device="cuda")
+
+        def allreduce_max(vals):
+            red[: len(vals)].copy_(torch.tensor(vals, dtype=torch.int64))
+            dist.all_reduce(red[: len(vals)], op=dist.ReduceOp.MAX)
+            return red[: len(vals)].tolist()
+
+        def one_search():
+            return B.search_sharded(vmap, dscan, cfg, rank, world, allreduce_max)
+    else:
+        def one_search():
+            return B.search_scan(vmap, dscan, cfg)
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        r = one_search()
+    barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    barrier()
+    results, step_ms = [], []
+    for _ in range(args.steps):
+        flush.fill_(1)  # L2 flush between timed iterations (outside the events)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        r = one_search()
+        e1.record(stream)
+        e1.synchronize()
+        step_ms.append(e0.elapsed_time(e1))
+        results.append(r)
+    barrier()
+    clk = clocks.stop()
+    t_local = sum(step_ms)
+    evals_local = sum(r.stats.nodes_generated for r in results)
+    if world > 1:
+        import torch.distributed as dist
+        tt = torch.tensor([t_local], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ev = torch.tensor([evals_local], dtype=torch.int64, device="cuda")
+        dist.all_reduce(ev, op=dist.ReduceOp.SUM)
+        t_max, evals = float(tt.item()), int(ev.item())
+    else:
+        t_max, evals = t_local, evals_local
+    value = evals / (t_max * 1e-3)
+    r0 = results[-1]
+    K = int(scan.shape[0])
+
+    # ---- e2e through the public host API (pinned host scan, result read back)
+    pinned = torch.empty((K, 3), dtype=torch.float64, pin_memory=True)
+    pinned.copy_(torch.from_numpy(scan))
+    host_scan = pinned.numpy()
+    e2e_t, e2e_evals, h2d, d2h = 0.0, 0, 0, 0
+    if world == 1:
+        B.search(vmap, host_scan, cfg)  # warm
+        for _ in range(args.steps):
+            flush.fill_(1)
+            torch.cuda.synchronize()
+            t = time.perf_counter()
+            re = B.search(vmap, host_scan, cfg)
+            e2e_t += time.perf_counter() - t
+            e2e_evals += re.stats.nodes_generated
+            h2d, d2h = re.h2d_bytes, re.d2h_bytes
+        e2e = {"value": e2e_evals / e2e_t, "unit": "evals/s", "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h), "ms_per_step": 1e3 * e2e_t / args.steps,
+               "timing": "host wall clock around bbs_search()"}
+    else:
+        # sharded e2e: the scan is re-uploaded from pinned memory every step
+        for _ in range(args.steps):
+            flush.fill_(1)
+            barrier()
+            t = time.perf_counter()
+            ds = B.DeviceScan(vmap, host_scan)
+            re = B.search_sharded(vmap, ds, cfg, rank, world, allreduce_max)
+            barrier()
+            e2e_t += time.perf_counter() - t
+            e2e_evals += re.stats.nodes_generated
+            h2d, d2h = re.h2d_bytes + 24 * K, re.d2h_bytes
+        import torch.distributed as dist
+        tt = torch.tensor([e2e_t], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ev = torch.tensor([e2e_evals], dtype=torch.int64, device="cuda")
+        dist.all_reduce(ev, op=dist.ReduceOp.SUM)
+        e2e = {"value": int(ev.item()) / float(tt.item()), "unit": "evals/s",
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+               "ms_per_step": 1e3 * float(tt.item()) / args.steps,
+               "timing": "host wall clock, max over ranks"}
+
+    # ---- roofline of the dominant kernel
+    peaks, peak_kind = measured_peaks()
+    root_ms = statistics.mean(r.root_score_ms for r in results)
+    epoch_ms = statistics.mean(r.epoch_score_ms for r in results)
+    root_probes = statistics.mean(r.root_probes for r in results)
+    epoch_lookups = statistics.mean((r.stats.nodes_generated - r.root_nodes) * K for r in results)
+    if root_ms >= epoch_ms:
+        kern, ms, probes = "score_box_kernel", root_ms, root_probes
+        launches_per_step = 1
+    else:
+        kern, ms, probes = "score_runs_kernel<8>", epoch_ms, epoch_lookups
+        launches_per_step = max(1, statistics.mean(r.epochs for r in results))
+    bytes_per_launch = probes * 32.0 / launches_per_step
+    achieved = bytes_per_launch / (ms / launches_per_step * 1e-3) / 1e9
+    peak = float(peaks.get("hbm_gbs", 6650.0))
+    gather = {}
+    if rank == 0 and not args.no_gather_bench:
+        import ctypes as C
+        for label, nbytes in (("l2_64MiB", 64 << 20), ("hbm_4GiB", 4 << 30)):
+            out = C.c_double()
+            if B.lib.bbs_gather_bench(local, nbytes, C.byref(out)) == 0:
+                gather[label] = round(out.value, 1)
+    roofline = {
+        "bound": "hbm", "kernel": kern, "achieved": achieved, "peak": peak, "unit": "GB/s",
+        "frac": achieved / peak, "traffic": profile_traffic(kern),
+        "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
+        "algorithmic_bytes_per_launch": bytes_per_launch,
+        "unit_of_work": "one membership probe = one random 32 B sector (SURVEY §8d)",
+        "kernel_ms_per_step": ms, "gather_peaks_gbs": gather,
+        "frac_of_l2_gather": (achieved / gather["l2_64MiB"]) if gather.get("l2_64MiB") else None,
+    }
+
+    line = {
+        "metric": "candidate score evals/sec", "value": value, "unit": "evals/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": t_max / args.steps, "higher_is_better": True,
+        "scaling": "strong" if world > 1 else "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (gen_scene restatement, bit-identical to the reference's)",
+        "config": {"workload": cfgd["workload"], "K": K, "map_points": int(map_pts.shape[0]),
+                   "parallelism": f"root-shard x{world}" if world > 1 else "single GPU",
+                   "l2": "flushed (256 MiB write) before every timed step",
+                   "layouts": layouts},
+        "latency_ms": {"localization_total": statistics.mean(r.stats.localization_total_ms()
+                                                              for r in results),
+                       "initial_nodes": statistics.mean(r.stats.initial_nodes_ms for r in results),
+                       "find_best_score": statistics.mean(r.stats.find_best_score_ms for r in results),
+                       "pop_remaining_queue": statistics.mean(r.stats.pop_remaining_queue_ms
+                                                              for r in results),
+                       "create_voxel_maps": build_ms},
+        "search": {"best_score": r0.best_score, "matched": r0.matched,
+                   "nodes_generated": r0.stats.nodes_generated, "epochs": r0.epochs,
+                   "root_nodes": r0.root_nodes, "root_probes": r0.root_probes,
+                   "lookups_per_s": r0.lookups / (statistics.mean(step_ms) * 1e-3),
+                   "trans_err_m": math.dist(r0.best_pose.as_tuple()[:3], gt.as_tuple()[:3])},
+        "e2e": e2e, "roofline": roofline, "clocks": clk,
+        "gpu_launches": int(sum(r.kernel_launches for r in results)),
+    }
+    if world == 1 and rank == 0 and not args.no_cpu_baseline:
+        try:
+            _, _, _, _, _, cpu_val, n, cores = reference_sample(map_pts, scan, cfgd,
+                                                               args.cpu_seconds, "cpu_baseline: ")
+            line["cpu_baseline"] = {
+                "value": cpu_val, "unit": "evals/s", "cores": cores, "kind": "reference",
+                "sample": f"{n} root nodes drawn uniformly from initial_nodes() of the workload, "
+                          f"bnbloc::batch_evaluate with workers={cores} (oracle/_ref)"}
+        except Exception as exc:  # noqa: BLE001
+            line["cpu_baseline"] = {"value": None, "unit": "evals/s", "cores": os.cpu_count(),
+                                    "kind": "reference", "sample": f"unavailable: {exc}"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
+    ap.add_argument("--config", choices=sorted(CONFIGS), default="c2")
+    ap.add_argument("--layout", choices=["auto", "bitmap", "hash"], default="auto")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-gather-bench", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        log("warmup raised to 3 (contract minimum)")
+        args.warmup = 3
+    cfgd = CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference_arm(args, cfgd)
+    else:
+        run_b200_arm(args, cfgd)
+
+
+if __name__ == "__main__":
+    main()

@@ -131,6 +131,10 @@ typedef struct bbs_search_result {
   double epoch_score_ms;  /* device time of the per-flush score kernels (sum) */
   uint64_t root_nodes;    /* roots scored by this rank */
   uint64_t queue_peak;    /* largest frontier (queue) length seen */
+  uint64_t root_probes;   /* membership probes the root kernel issued after de-duplication */
+  uint64_t h2d_bytes;     /* host->device bytes copied by this call */
+  uint64_t d2h_bytes;     /* device->host bytes copied by this call */
+  uint64_t kernel_launches; /* launches of this library's own kernels (CUB launches excluded) */
 } bbs_search_result;
 
 /* AxisGrid, angular_grid.hpp:45-58. */
@@ -212,6 +216,9 @@ int bbs_map_max_level(bbs_map_t map, int32_t* out);       /* voxel_map.hpp:264 *
 int bbs_map_bbox(bbs_map_t map, bbs_aabb* out);           /* voxel_map.hpp:265 */
 /* Device time of the map build ("Create voxel maps", Stats::create_voxel_maps_ms). */
 int bbs_map_build_ms(bbs_map_t map, double* out);
+/* Run all later work of this map on `stream` (a cudaStream_t owned by the
+ * caller, e.g. torch's current stream); NULL restores the map's own stream. */
+int bbs_map_set_stream(bbs_map_t map, void* stream);
 int bbs_map_level_info(bbs_map_t map, int32_t level, bbs_level_info* out);
 /* LevelMap::occupied_voxels, voxel_map.hpp:158-165: ascending (x,y,z). */
 int bbs_level_occupied(bbs_map_t map, int32_t level, int32_t* xyz, uint64_t capacity,
@@ -290,6 +297,11 @@ int bbs_gen_scans(const bbs_scene_spec* spec, uint64_t seed, uint64_t pose_seed_
 int bbs_cut_scan(const double* xyz, uint64_t n, uint64_t k, uint64_t seed, double* out);
 const char* bbs_scene_last_error(void);
 void bbs_free(void* p);
+
+/* ---- measurement ------------------------------------------------------ */
+/* Random independent 32-byte gather ceiling over a `bytes` buffer on
+ * `device` (SURVEY §8d tier ceilings): sector GB/s. */
+int bbs_gather_bench(int32_t device, uint64_t bytes, double* out_gbs);
 
 #ifdef __cplusplus
 }  /* extern "C" */

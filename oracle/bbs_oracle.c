@@ -495,10 +495,21 @@ static int search_impl(const orc_map* m, const bbs_aabb* map_bbox, const double*
     free(g);
     return st;
   }
-  /* shard: keep roots with index % world == rank */
+  /* shard: root (ix, iy, iz, rot) belongs to rank
+   * ((ix - ix_min) * nrot + rot) % world — whole (x-slab, rotation) units,
+   * the rule of the device root kernel (csrc/kernels.h owned_slabs). */
   uint64_t nmine = 0;
-  for (uint64_t i = 0; i < nroots; ++i)
-    if ((int)(i % (uint64_t)world) == rank) roots[nmine++] = roots[i];
+  {
+    const int64_t np_ = max_index(axis_at(g, L, 1, L)) + 1;
+    const int64_t nw_ = max_index(axis_at(g, L, 2, L)) + 1;
+    const int64_t nrot = (max_index(axis_at(g, L, 0, L)) + 1) * np_ * nw_;
+    const int32_t ix_min = nroots ? roots[0].ix : 0;
+    for (uint64_t i = 0; i < nroots; ++i) {
+      const int64_t rot = ((int64_t)roots[i].iroll * np_ + roots[i].ipitch) * nw_ + roots[i].iyaw;
+      const int64_t unit = ((int64_t)roots[i].ix - ix_min) * nrot + rot;
+      if ((int)(unit % world) == rank) roots[nmine++] = roots[i];
+    }
+  }
   stats->nodes_generated += nmine;
   for (uint64_t i = 0; i < nmine; ++i) score_node(m, g, L, scan, k, &roots[i]);
   stats->batches_flushed++;

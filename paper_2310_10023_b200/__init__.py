@@ -227,6 +227,10 @@ class SearchResult:
     epoch_score_ms: float = 0.0
     root_nodes: int = 0
     queue_peak: int = 0
+    root_probes: int = 0
+    h2d_bytes: int = 0
+    d2h_bytes: int = 0
+    kernel_launches: int = 0
 
 
 def _result_from_c(r: SearchResultC, trace_buf=None) -> SearchResult:
@@ -239,7 +243,9 @@ def _result_from_c(r: SearchResultC, trace_buf=None) -> SearchResult:
                     s.pop_remaining_queue_ms),
         best_node=tuple(getattr(r.best_node, f) for f in _abi.NODE_DTYPE_FIELDS),
         epochs=r.epochs, lookups=r.lookups, device_ms=r.device_ms, root_score_ms=r.root_score_ms,
-        epoch_score_ms=r.epoch_score_ms, root_nodes=r.root_nodes, queue_peak=r.queue_peak)
+        epoch_score_ms=r.epoch_score_ms, root_nodes=r.root_nodes, queue_peak=r.queue_peak,
+        root_probes=r.root_probes, h2d_bytes=r.h2d_bytes, d2h_bytes=r.d2h_bytes,
+        kernel_launches=r.kernel_launches)
     if trace_buf is not None:
         out.best_score_trace = list(trace_buf[: min(r.trace_length, len(trace_buf))])
     return out
@@ -539,6 +545,10 @@ class MultiResVoxelMap:
 
     def levels(self):
         return list(self._levels)
+
+    def set_stream(self, stream_ptr):
+        """Run later work on an external cudaStream_t (int pointer, 0 = own)."""
+        _check(lib.bbs_map_set_stream(self._h, C.c_void_p(int(stream_ptr) or None)))
 
     def build_ms(self):
         out = C.c_double()

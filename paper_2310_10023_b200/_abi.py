@@ -92,6 +92,10 @@ class SearchResultC(C.Structure):
         ("epoch_score_ms", C.c_double),
         ("root_nodes", C.c_uint64),
         ("queue_peak", C.c_uint64),
+        ("root_probes", C.c_uint64),
+        ("h2d_bytes", C.c_uint64),
+        ("d2h_bytes", C.c_uint64),
+        ("kernel_launches", C.c_uint64),
     ]
 
 

@@ -51,6 +51,7 @@ SIGNATURES = {
     "bbs_map_max_level": (C.c_int, [_vp, _ip]),
     "bbs_map_bbox": (C.c_int, [_vp, C.POINTER(Aabb)]),
     "bbs_map_build_ms": (C.c_int, [_vp, _dp]),
+    "bbs_map_set_stream": (C.c_int, [_vp, _vp]),
     "bbs_map_level_info": (C.c_int, [_vp, _i32, C.POINTER(LevelInfo)]),
     "bbs_level_occupied": (C.c_int, [_vp, _i32, _ip, _u64, C.POINTER(_u64)]),
     "bbs_level_contains": (C.c_int, [_vp, _i32, _ip, _u64, C.POINTER(C.c_uint8)]),
@@ -74,6 +75,7 @@ SIGNATURES = {
     "bbs_cut_scan": (C.c_int, [_dp, _u64, _u64, _u64, _dp]),
     "bbs_scene_last_error": (C.c_char_p, []),
     "bbs_free": (None, [_vp]),
+    "bbs_gather_bench": (C.c_int, [_i32, _u64, _dp]),
 }
 
 for _name, (_res, _args) in SIGNATURES.items():

@@ -43,6 +43,9 @@ struct LevelView {
   const uint32_t* words;
   // hash: packed key = (x' << (by+bz)) | (y' << bz) | z', 4 slots per bucket
   const unsigned long long* slots;
+  // z-column bitmap (levels with dim[2] <= 32): colmap[uy * dim[0] + ux] has
+  // bit uz set when voxel (ux, uy, uz) is occupied.  Null otherwise.
+  const uint32_t* colmap;
   unsigned long long bucket_mask;  // buckets - 1 (buckets >= 2, power of two)
   uint32_t bucket_shift; // 64 - log2(buckets)
   uint32_t bits_y, bits_z;

@@ -3,13 +3,20 @@
 
 #include <cuda_runtime.h>
 
+#include <mutex>
 #include <vector>
 
 #include "bbs_internal.h"
 
+namespace bbs {
+struct Workspace;
+void free_workspace(Workspace* w);
+}  // namespace bbs
+
 struct bbs_map {
   int device = 0;
-  cudaStream_t stream = nullptr;
+  cudaStream_t stream = nullptr;      // stream all work of this map runs on
+  cudaStream_t own_stream = nullptr;  // created (and destroyed) by the map
   double r = 1.0;
   int max_level = 0;
   bbs_aabb bbox{};
@@ -22,10 +29,14 @@ struct bbs_map {
     uint64_t n_keys = 0;
     uint32_t bits[3] = {0, 0, 0};
     void* structure = nullptr;           // bitmap words or hash slots
+    uint32_t* colmap = nullptr;          // z-column bitmap (coarse levels)
   };
   std::vector<Level> levels;
   bbs::MapView view{};
   double build_ms = 0.0;
+  // persistent per-search workspaces (device buffers reused across calls)
+  std::mutex ws_mu;
+  std::vector<bbs::Workspace*> ws_pool;
   ~bbs_map();
 };
 

@@ -71,7 +71,8 @@ bbs_map* new_map(const bbs_map_options* opts, double r, uint64_t cap, double ct)
     throw bbs::Error(BBS_ERR_CONFIG, "map: unknown layout");
   bbs::DeviceGuard g(device);
   bbs::set_pool_retention(device);
-  BBS_CUDA(cudaStreamCreateWithFlags(&m->stream, cudaStreamNonBlocking));
+  BBS_CUDA(cudaStreamCreateWithFlags(&m->own_stream, cudaStreamNonBlocking));
+  m->stream = m->own_stream;
   return m.release();
 }
 
@@ -252,6 +253,14 @@ int bbs_map_build_ms(bbs_map_t map, double* out) {
     *out = map->build_ms;
   });
 }
+int bbs_map_set_stream(bbs_map_t map, void* stream) {
+  return guard([&] {
+    REQUIRE(map, "null argument");
+    bbs::DeviceGuard g(map->device);
+    BBS_CUDA(cudaStreamSynchronize(map->stream));
+    map->stream = stream ? static_cast<cudaStream_t>(stream) : map->own_stream;
+  });
+}
 int bbs_map_level_info(bbs_map_t map, int32_t level, bbs_level_info* out) {
   return guard([&] {
     REQUIRE(map && out, "null argument");
@@ -322,6 +331,7 @@ int bbs_search(bbs_map_t map, const double* scan_xyz, uint64_t k, const bbs_sear
     if (k == 0) throw bbs::Error(BBS_ERR_DEGENERATE_SCAN, "search: empty scan");
     std::unique_ptr<bbs_scan> sc(bbs::upload_scan(map, scan_xyz, k));
     bbs::run_search(map, sc.get(), *cfg, nullptr, result);
+    result->h2d_bytes += 3 * k * sizeof(double);
   });
 }
 

@@ -30,9 +30,58 @@ constexpr int kBoxThreads = 256;
 constexpr int kBoxTransPerThread = 4;
 constexpr int kBoxTransPerCta = kBoxThreads * kBoxTransPerThread;
 
-// Score every root of the box owned by (rank, world) into scores[ref index].
-void launch_score_box(const MapView& map, const GridView& grid, const ScanView& scan,
-                      const BoxParams& bp, int32_t* scores, cudaStream_t s);
+// Root ownership: root (ix, iy, iz, rot) belongs to rank
+// ((ix - x0) * nrot + rot) % world, i.e. whole (x-slab, rotation) units.
+// Per-rotation de-duplicated scan histograms of the root batch.
+constexpr int kHistCap = 4096;   // distinct voxel offsets per rotation
+constexpr int kAmbCap = 1024;    // ambiguous points per rotation
+constexpr int kRotBatch = 2048;  // rotations per histogram pass
+struct RootHist {
+  int4* entries;      // [kRotBatch * kHistCap] (fx, fy, fz, count)
+  uint32_t* amb;      // [kRotBatch * kAmbCap] scan point indices
+  int32_t* n_ent;     // [kRotBatch]
+  int32_t* n_amb;     // [kRotBatch]
+  int32_t* overflow;  // [kRotBatch] 1: rotation falls back to the chunked kernel
+};
+
+// Owned x-slabs of rotation `rot`: slab ix_rel is owned iff
+// (ix_rel * nrot + rot) % world == rank  <=>  ix_rel == x0r (mod P).
+__host__ __device__ inline bool owned_slabs(const BoxParams& bp, uint32_t nrot, uint32_t rot,
+                                            uint32_t* P, uint32_t* x0r) {
+  if (bp.world <= 1) {
+    *P = 1;
+    *x0r = 0;
+    return true;
+  }
+  uint32_t g = bp.world, b = nrot % bp.world;
+  while (b) {
+    const uint32_t t = g % b;
+    g = b;
+    b = t;
+  }
+  *P = bp.world / g;
+  for (uint32_t c = 0; c < *P; ++c)
+    if ((static_cast<uint64_t>(c) * nrot + rot) % bp.world == bp.rank) {
+      *x0r = c;
+      return true;
+    }
+  return false;
+}
+
+// Chunked fallback (per-chunk de-duplication, any level layout) for the
+// rotations [rot_begin, rot_end) whose only[rot - rot_begin] != 0 (all when
+// only is null).
+void launch_score_box_chunked(const MapView& map, const GridView& grid, const ScanView& scan,
+                              const BoxParams& bp, uint32_t rot_begin, uint32_t rot_end,
+                              const int32_t* only, int32_t* scores, unsigned long long* probes,
+                              cudaStream_t s);
+
+// Score every root owned by (rank, world) into scores[ref index], where
+// ref index = position in initial_nodes() order (nodes.hpp:77-83).
+// `hist` is scratch for kRotBatch rotations.
+void launch_score_roots(const MapView& map, const GridView& grid, const ScanView& scan,
+                        const BoxParams& bp, const RootHist& hist, int32_t* scores,
+                        unsigned long long* probes, cudaStream_t s);
 
 // Score n nodes that come in contiguous same-rotation runs of 8 (the output
 // order of branch(), nodes.hpp:103-116).  n is read from *d_n when non-null

@@ -138,6 +138,19 @@ __global__ void bitmap_set_kernel(const unsigned long long* __restrict__ keys, u
   }
 }
 
+__global__ void colmap_set_kernel(const unsigned long long* __restrict__ keys, uint64_t n,
+                                  LevelView L, uint32_t* __restrict__ colmap) {
+  const unsigned long long my = (1ull << L.bits_y) - 1, mz = (1ull << L.bits_z) - 1;
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
+       i += uint64_t(gridDim.x) * blockDim.x) {
+    const unsigned long long k = keys[i];
+    const uint32_t ux = static_cast<uint32_t>(k >> (L.bits_y + L.bits_z));
+    const uint32_t uy = static_cast<uint32_t>((k >> L.bits_z) & my);
+    const uint32_t uz = static_cast<uint32_t>(k & mz);
+    atomicOr(&colmap[static_cast<uint64_t>(uy) * L.dim[0] + ux], 1u << uz);
+  }
+}
+
 __global__ void hash_insert_kernel(const unsigned long long* __restrict__ keys, uint64_t n,
                                    LevelView L, unsigned long long* __restrict__ slots) {
   for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
@@ -329,6 +342,17 @@ void finish_level(bbs_map* m, int level, unsigned long long* keys, uint64_t n, c
     hash_insert_kernel<<<grid_for(n), kThreads, 0, s>>>(keys, n, V, sl);
     BBS_CUDA(cudaGetLastError());
   }
+  // z-column bitmap for short levels (used by the root-batch kernel)
+  const uint64_t col_bytes = static_cast<uint64_t>(V.dim[0]) * V.dim[1] * 4ull;
+  if (n && V.dim[2] <= 32 && col_bytes <= (256ull << 20)) {
+    uint32_t* cm = nullptr;
+    BBS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&cm), col_bytes, s));
+    BBS_CUDA(cudaMemsetAsync(cm, 0, col_bytes, s));
+    colmap_set_kernel<<<grid_for(n), kThreads, 0, s>>>(keys, n, V, cm);
+    BBS_CUDA(cudaGetLastError());
+    V.colmap = cm;
+    L.colmap = cm;
+  }
   bbs_level_info& I = L.info;
   I.level = level;
   I.layout = layout;
@@ -516,11 +540,13 @@ bbs_map::~bbs_map() {
     int prev = 0;
     cudaGetDevice(&prev);
     cudaSetDevice(device);
+    for (auto* w : ws_pool) bbs::free_workspace(w);
     for (auto& L : levels) {
       if (L.keys) cudaFree(L.keys);
       if (L.structure) cudaFree(L.structure);
+      if (L.colmap) cudaFree(L.colmap);
     }
-    if (stream) cudaStreamDestroy(stream);
+    if (own_stream) cudaStreamDestroy(own_stream);
     cudaSetDevice(prev);
   }
 }

@@ -211,7 +211,10 @@ __device__ __forceinline__ uint32_t slot_hash(unsigned long long key) {
 
 __global__ void __launch_bounds__(kBoxThreads, 2) score_box_kernel(MapView map, GridView grid,
                                                                    ScanView scan, BoxParams bp,
-                                                                   int32_t* __restrict__ scores) {
+                                                                   uint32_t rot_begin, uint32_t rot_end,
+                                                                   const int32_t* __restrict__ only,
+                                                                   int32_t* __restrict__ scores,
+                                                                   unsigned long long* probes) {
   extern __shared__ __align__(16) unsigned char smem[];
   unsigned long long* s_key = reinterpret_cast<unsigned long long*>(smem);        // 32 KB
   int32_t* s_hcnt = reinterpret_cast<int32_t*>(s_key + kHashSlots);               // 16 KB
@@ -220,34 +223,18 @@ __global__ void __launch_bounds__(kBoxThreads, 2) score_box_kernel(MapView map, 
   __shared__ int32_t s_nent, s_namb;
 
   const uint32_t nrot = bp.nr * bp.np * bp.nw;
-  const uint64_t ntrans = static_cast<uint64_t>(bp.nx) * bp.ny * bp.nz;
-  const uint64_t n_items = static_cast<uint64_t>(nrot) * bp.n_tchunks;
+  const uint64_t slab = static_cast<uint64_t>(bp.ny) * bp.nz;  // translations per x-slab
+  const uint64_t n_items = static_cast<uint64_t>(rot_end - rot_begin) * bp.n_tchunks;
   const LevelView L = map.level[bp.level];
+  if (only && only[kRotBatch] == 0) return;  // no histogram overflowed in this batch
 
   for (uint64_t item = blockIdx.x; item < n_items; item += gridDim.x) {
-    const uint32_t rot = static_cast<uint32_t>(item / bp.n_tchunks);
+    const uint32_t rot = rot_begin + static_cast<uint32_t>(item / bp.n_tchunks);
     const uint32_t tc = static_cast<uint32_t>(item % bp.n_tchunks);
-    // owned translations of this rotation: (t*nrot + rot) % world == rank
-    // <=> t == t0 (mod P); P = world / gcd(nrot, world); world <= 64.
-    uint32_t P = bp.world, t0 = 0;
-    bool any = bp.world == 1;
-    if (!any) {
-      uint32_t g = bp.world, b = nrot % bp.world;
-      while (b) {
-        const uint32_t tmp = g % b;
-        g = b;
-        b = tmp;
-      }
-      P = bp.world / g;
-      for (uint32_t c = 0; c < P; ++c)
-        if ((static_cast<uint64_t>(c) * nrot + rot) % bp.world == bp.rank) {
-          t0 = c;
-          any = true;
-          break;
-        }
-    }
-    if (!any) continue;  // uniform across the CTA
-    const uint64_t n_own = ntrans > t0 ? (ntrans - t0 + P - 1) / P : 0;
+    if (only && !only[rot - rot_begin]) continue;  // uniform across the CTA
+    uint32_t P, x0r;
+    if (!owned_slabs(bp, nrot, rot, &P, &x0r)) continue;
+    const uint64_t n_own = (x0r < bp.nx ? (bp.nx - x0r + P - 1) / P : 0) * slab;
     const uint64_t own0 = static_cast<uint64_t>(tc) * kBoxTransPerCta;
     if (own0 >= n_own) continue;
 
@@ -266,7 +253,7 @@ __global__ void __launch_bounds__(kBoxThreads, 2) score_box_kernel(MapView map, 
     for (int i = 0; i < kBoxTransPerThread; ++i) {
       const uint64_t o = own0 + threadIdx.x + static_cast<uint64_t>(i) * kBoxThreads;
       tvalid[i] = o < n_own;
-      const uint64_t t = tvalid[i] ? t0 + o * P : 0;
+      const uint64_t t = tvalid[i] ? (x0r + (o / slab) * P) * slab + o % slab : 0;
       tiz[i] = bp.z0 + static_cast<int32_t>(t % bp.nz);
       tiy[i] = bp.y0 + static_cast<int32_t>((t / bp.nz) % bp.ny);
       tix[i] = bp.x0 + static_cast<int32_t>(t / (static_cast<uint64_t>(bp.nz) * bp.ny));
@@ -328,6 +315,10 @@ __global__ void __launch_bounds__(kBoxThreads, 2) score_box_kernel(MapView map, 
       }
       __syncthreads();
       const int nent = s_nent;
+      if (threadIdx.x == 0 && probes) {
+        const uint64_t nt = min(static_cast<uint64_t>(kBoxTransPerCta), n_own - own0);
+        atomicAdd(probes, static_cast<unsigned long long>(nent + s_namb) * nt);
+      }
       for (int e = 0; e < nent; ++e) {
         const int4 f = s_ent[e];
 #pragma unroll
@@ -350,6 +341,207 @@ __global__ void __launch_bounds__(kBoxThreads, 2) score_box_kernel(MapView map, 
 #pragma unroll
     for (int i = 0; i < kBoxTransPerThread; ++i)
       if (tvalid[i]) scores[tref[i]] = acc[i];
+  }
+}
+
+// ---- root batch: whole-scan histogram + z-column kernel ---------------------
+// (1) root_hist_kernel: one CTA per root rotation de-duplicates the fast-path
+//     voxel offsets f of ALL K scan points in a shared-memory hash
+//     (coarse root levels put tens of points in one voxel) and writes the
+//     (f, count) list, the ambiguous points and an overflow flag.
+// (2) root_col_kernel: one thread per owned (ix, iy) translation column holds
+//     the column's nz <= 32 z-translations in registers; per histogram entry
+//     it reads ONE 32-bit z-mask of the level's column bitmap and credits
+//     count(f) to every z-translation whose bit is set:
+//        score(ix, iy, z0 + j) = sum_f count(f) * bit_{fz + z0 + j}(col(fx + ix, fy + iy)).
+//     Ambiguous points are scored exactly per translation.
+constexpr int kHistSlots = 2 * kHistCap;
+constexpr int kEntTile = 1024;
+
+__device__ __forceinline__ uint32_t hist_slot(unsigned long long key) {
+  return static_cast<uint32_t>((key * 0x9E3779B97F4A7C15ull) >> 51);  // 13 bits
+}
+
+__global__ void __launch_bounds__(512) root_hist_kernel(GridView grid, ScanView scan, BoxParams bp,
+                                                        LevelView L, uint32_t rot_begin,
+                                                        uint32_t rot_end, RootHist h,
+                                                        int32_t* __restrict__ n_overflow) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  unsigned long long* s_key = reinterpret_cast<unsigned long long*>(smem);  // 64 KB
+  int32_t* s_cnt = reinterpret_cast<int32_t*>(s_key + kHistSlots);          // 32 KB
+  __shared__ int s_distinct, s_namb, s_nent, s_skip;
+  const uint32_t nrot = bp.nr * bp.np * bp.nw;
+  for (uint32_t rot = rot_begin + blockIdx.x; rot < rot_end; rot += gridDim.x) {
+    const uint32_t slot = rot - rot_begin;
+    uint32_t P, x0r;
+    if (!owned_slabs(bp, nrot, rot, &P, &x0r)) {
+      if (threadIdx.x == 0) {
+        h.n_ent[slot] = 0;
+        h.n_amb[slot] = 0;
+        h.overflow[slot] = 0;
+      }
+      continue;
+    }
+    for (int i = threadIdx.x; i < kHistSlots; i += blockDim.x) {
+      s_key[i] = kSlotEmpty;
+      s_cnt[i] = 0;
+    }
+    if (threadIdx.x == 0) {
+      s_distinct = 0;
+      s_namb = 0;
+      s_nent = 0;
+      s_skip = 0;
+    }
+    __syncthreads();
+    const uint32_t ir = rot / (bp.np * bp.nw), ip = (rot / bp.nw) % bp.np, iw = rot % bp.nw;
+    double R[9];
+    rotation_of(grid, bp.level, static_cast<int>(ir), static_cast<int>(ip), static_cast<int>(iw), R);
+    for (uint32_t p = threadIdx.x; p < scan.k; p += blockDim.x) {
+      const double px = scan.x[p], py = scan.y[p], pz = scan.z[p];
+      int32_t fx, fy, fz;
+      bool ok = fast_floor(rot_row(R[0], R[1], R[2], px, py, pz), L.inv_cell, bp.tmax, &fx) &
+                fast_floor(rot_row(R[3], R[4], R[5], px, py, pz), L.inv_cell, bp.tmax, &fy) &
+                fast_floor(rot_row(R[6], R[7], R[8], px, py, pz), L.inv_cell, bp.tmax, &fz);
+      ok = ok && fx > -(1 << 20) && fx < (1 << 20) && fy > -(1 << 20) && fy < (1 << 20) &&
+           fz > -(1 << 20) && fz < (1 << 20);
+      if (!ok) {
+        const int a = atomicAdd(&s_namb, 1);
+        if (a < kAmbCap) h.amb[static_cast<uint64_t>(slot) * kAmbCap + a] = p;
+        continue;
+      }
+      if (s_distinct >= kHistCap) {  // table saturated: this rotation falls back
+        s_skip = 1;
+        continue;
+      }
+      const unsigned long long key = (static_cast<unsigned long long>(fx + (1 << 20)) << 42) |
+                                     (static_cast<unsigned long long>(fy + (1 << 20)) << 21) |
+                                     static_cast<unsigned long long>(fz + (1 << 20));
+      uint32_t hs = hist_slot(key);
+      for (;;) {
+        const unsigned long long prev = atomicCAS(&s_key[hs], kSlotEmpty, key);
+        if (prev == kSlotEmpty) atomicAdd(&s_distinct, 1);
+        if (prev == kSlotEmpty || prev == key) {
+          atomicAdd(&s_cnt[hs], 1);
+          break;
+        }
+        hs = (hs + 1) & (kHistSlots - 1);
+      }
+    }
+    __syncthreads();
+    const bool over = s_skip || s_distinct > kHistCap || s_namb > kAmbCap;
+    if (!over) {
+      for (int i = threadIdx.x; i < kHistSlots; i += blockDim.x) {
+        const unsigned long long key = s_key[i];
+        if (key != kSlotEmpty) {
+          const int e = atomicAdd(&s_nent, 1);
+          h.entries[static_cast<uint64_t>(slot) * kHistCap + e] =
+              make_int4(static_cast<int32_t>((key >> 42) & 0x1FFFFF) - (1 << 20),
+                        static_cast<int32_t>((key >> 21) & 0x1FFFFF) - (1 << 20),
+                        static_cast<int32_t>(key & 0x1FFFFF) - (1 << 20), s_cnt[i]);
+        }
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      h.n_ent[slot] = over ? 0 : s_nent;
+      h.n_amb[slot] = over ? 0 : s_namb;
+      h.overflow[slot] = over ? 1 : 0;
+      if (over) atomicAdd(n_overflow, 1);
+    }
+    __syncthreads();
+  }
+}
+
+template <int NZ>
+__global__ void __launch_bounds__(256) root_col_kernel(GridView grid, ScanView scan, BoxParams bp,
+                                                       LevelView L, uint32_t rot_begin,
+                                                       uint32_t rot_end, RootHist h,
+                                                       uint32_t n_cchunks, int stage_col,
+                                                       int32_t* __restrict__ scores,
+                                                       unsigned long long* probes) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  int4* s_ent = reinterpret_cast<int4*>(smem);                          // 16 KB
+  uint32_t* s_col = reinterpret_cast<uint32_t*>(s_ent + kEntTile);      // staged colmap
+  const uint32_t nrot = bp.nr * bp.np * bp.nw;
+  const uint32_t dimx = L.dim[0], dimy = L.dim[1];
+  const uint32_t* __restrict__ col = L.colmap;
+  if (stage_col) {
+    for (uint32_t i = threadIdx.x; i < dimx * dimy; i += blockDim.x) s_col[i] = __ldg(&L.colmap[i]);
+    __syncthreads();
+    col = s_col;
+  }
+  const uint64_t n_items = static_cast<uint64_t>(rot_end - rot_begin) * n_cchunks;
+  for (uint64_t item = blockIdx.x; item < n_items; item += gridDim.x) {
+    const uint32_t slot = static_cast<uint32_t>(item / n_cchunks);
+    const uint32_t rot = rot_begin + slot;
+    const uint32_t cc = static_cast<uint32_t>(item % n_cchunks);
+    if (h.overflow[slot]) continue;  // uniform per CTA
+    uint32_t P, x0r;
+    if (!owned_slabs(bp, nrot, rot, &P, &x0r)) continue;
+    const uint32_t n_own_x = x0r < bp.nx ? (bp.nx - x0r + P - 1) / P : 0;
+    const uint64_t ncols = static_cast<uint64_t>(n_own_x) * bp.ny;
+    const uint64_t col0 = static_cast<uint64_t>(cc) * blockDim.x;
+    if (col0 >= ncols) continue;
+    const uint64_t c = col0 + threadIdx.x;
+    const bool valid = c < ncols;
+    const uint32_t ix_rel = x0r + static_cast<uint32_t>(c / bp.ny) * P;
+    const uint32_t iy_rel = static_cast<uint32_t>(c % bp.ny);
+    const int32_t ix = bp.x0 + static_cast<int32_t>(ix_rel), iy = bp.y0 + static_cast<int32_t>(iy_rel);
+    const uint32_t xoff = static_cast<uint32_t>(ix) - static_cast<uint32_t>(L.box_min[0]);
+    const uint32_t yoff = static_cast<uint32_t>(iy) - static_cast<uint32_t>(L.box_min[1]);
+    const int32_t zoff = bp.z0 - L.box_min[2];
+    int acc[NZ];
+#pragma unroll
+    for (int j = 0; j < NZ; ++j) acc[j] = 0;
+    const int n_ent = h.n_ent[slot];
+    const int4* __restrict__ ent = h.entries + static_cast<uint64_t>(slot) * kHistCap;
+    for (int t0 = 0; t0 < n_ent; t0 += kEntTile) {
+      const int tn = min(kEntTile, n_ent - t0);
+      __syncthreads();
+      for (int i = threadIdx.x; i < tn; i += blockDim.x) s_ent[i] = ent[t0 + i];
+      __syncthreads();
+      if (valid) {
+#pragma unroll 4
+        for (int e = 0; e < tn; ++e) {
+          const int4 f = s_ent[e];
+          const uint32_t ux = static_cast<uint32_t>(f.x) + xoff;
+          const uint32_t uy = static_cast<uint32_t>(f.y) + yoff;
+          if (ux < dimx && uy < dimy) {
+            const uint32_t m = col[uy * dimx + ux];
+            const int32_t sh = f.z + zoff;
+            const uint32_t bits = sh >= 0 ? (sh < 32 ? m >> sh : 0u) : (sh > -32 ? m << -sh : 0u);
+#pragma unroll
+            for (int j = 0; j < NZ; ++j) acc[j] += f.w & -static_cast<int>((bits >> j) & 1u);
+          }
+        }
+      }
+    }
+    const int n_amb = h.n_amb[slot];
+    if (valid && n_amb) {
+      const uint32_t ir = rot / (bp.np * bp.nw), ip = (rot / bp.nw) % bp.np, iw = rot % bp.nw;
+      double R[9];
+      rotation_of(grid, bp.level, static_cast<int>(ir), static_cast<int>(ip), static_cast<int>(iw), R);
+      for (int a = 0; a < n_amb; ++a) {
+        const uint32_t p = h.amb[static_cast<uint64_t>(slot) * kAmbCap + a];
+        const double px = scan.x[p], py = scan.y[p], pz = scan.z[p];
+        const double rx = rot_row(R[0], R[1], R[2], px, py, pz);
+        const double ry = rot_row(R[3], R[4], R[5], px, py, pz);
+        const double rz = rot_row(R[6], R[7], R[8], px, py, pz);
+#pragma unroll
+        for (int j = 0; j < NZ; ++j)
+          if (j < static_cast<int>(bp.nz)) acc[j] += exact_hit(L, rx, ry, rz, ix, iy, bp.z0 + j);
+      }
+    }
+    if (valid) {
+      const uint64_t base = (static_cast<uint64_t>(ix_rel) * bp.ny + iy_rel) * bp.nz;
+#pragma unroll
+      for (int j = 0; j < NZ; ++j)
+        if (j < static_cast<int>(bp.nz)) scores[(base + j) * nrot + rot] = acc[j];
+    }
+    if (threadIdx.x == 0 && probes) {
+      const uint64_t nc = min(static_cast<uint64_t>(blockDim.x), ncols - col0);
+      atomicAdd(probes, static_cast<unsigned long long>(nc) * (n_ent + n_amb) * bp.nz);
+    }
   }
 }
 
@@ -409,8 +601,10 @@ uint32_t choose_ptiles(uint64_t runs, uint32_t k) {
   return static_cast<uint32_t>(p);
 }
 
-void launch_score_box(const MapView& map, const GridView& grid, const ScanView& scan,
-                      const BoxParams& bp, int32_t* scores, cudaStream_t s) {
+void launch_score_box_chunked(const MapView& map, const GridView& grid, const ScanView& scan,
+                              const BoxParams& bp, uint32_t rot_begin, uint32_t rot_end,
+                              const int32_t* only, int32_t* scores, unsigned long long* probes,
+                              cudaStream_t s) {
   static bool attr_done = false;
   const int smem = kHashSlots * 8 + kHashSlots * 4 + kChunk * 16 + kChunk * 4;
   if (!attr_done) {
@@ -418,10 +612,68 @@ void launch_score_box(const MapView& map, const GridView& grid, const ScanView& 
                                   smem));
     attr_done = true;
   }
-  const uint64_t items = static_cast<uint64_t>(bp.nr) * bp.np * bp.nw * bp.n_tchunks;
-  const unsigned grid_sz = static_cast<unsigned>(std::min<uint64_t>(items, 148ull * 2 * 64));
-  score_box_kernel<<<grid_sz, kBoxThreads, smem, s>>>(map, grid, scan, bp, scores);
+  const uint64_t items = static_cast<uint64_t>(rot_end - rot_begin) * bp.n_tchunks;
+  const unsigned grid_sz = static_cast<unsigned>(std::min<uint64_t>(std::max<uint64_t>(items, 1), 148ull * 2 * 64));
+  score_box_kernel<<<grid_sz, kBoxThreads, smem, s>>>(map, grid, scan, bp, rot_begin, rot_end, only,
+                                                      scores, probes);
   BBS_CUDA(cudaGetLastError());
+}
+
+void launch_score_roots(const MapView& map, const GridView& grid, const ScanView& scan,
+                        const BoxParams& bp, const RootHist& hist, int32_t* scores,
+                        unsigned long long* probes, cudaStream_t s) {
+  const LevelView& L = map.level[bp.level];
+  const uint32_t nrot = bp.nr * bp.np * bp.nw;
+  const bool col_ok = L.colmap != nullptr && bp.nz <= 32 && L.dim[0] > 0;
+  if (!col_ok) {
+    launch_score_box_chunked(map, grid, scan, bp, 0, nrot, nullptr, scores, probes, s);
+    return;
+  }
+  static bool attr_done = false;
+  const int hist_smem = kHistSlots * 12;
+  const int col_stage_max = 64 << 10;
+  if (!attr_done) {
+    BBS_CUDA(cudaFuncSetAttribute(root_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  hist_smem));
+    BBS_CUDA(cudaFuncSetAttribute(root_col_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  kEntTile * 16 + col_stage_max));
+    BBS_CUDA(cudaFuncSetAttribute(root_col_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  kEntTile * 16 + col_stage_max));
+    BBS_CUDA(cudaFuncSetAttribute(root_col_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  kEntTile * 16 + col_stage_max));
+    attr_done = true;
+  }
+  const uint64_t col_bytes = static_cast<uint64_t>(L.dim[0]) * L.dim[1] * 4ull;
+  const int stage = col_bytes <= static_cast<uint64_t>(col_stage_max) ? 1 : 0;
+  const int col_smem = kEntTile * 16 + (stage ? static_cast<int>(col_bytes) : 0);
+  uint32_t P, x0r;
+  BoxParams b0 = bp;
+  b0.rank = 0;
+  b0.world = bp.world;
+  owned_slabs(b0, nrot, 0, &P, &x0r);  // P depends on (nrot, world) only
+  const uint64_t max_cols = static_cast<uint64_t>((bp.nx + P - 1) / P) * bp.ny;
+  const uint32_t n_cchunks = static_cast<uint32_t>((max_cols + 255) / 256);
+  for (uint32_t rb = 0; rb < nrot; rb += kRotBatch) {
+    const uint32_t re = std::min<uint32_t>(nrot, rb + kRotBatch);
+    BBS_CUDA(cudaMemsetAsync(hist.overflow + kRotBatch, 0, sizeof(int32_t), s));  // n_overflow
+    root_hist_kernel<<<std::min<uint32_t>(re - rb, 148 * 4), 512, hist_smem, s>>>(
+        grid, scan, bp, L, rb, re, hist, hist.overflow + kRotBatch);
+    BBS_CUDA(cudaGetLastError());
+    const uint64_t items = static_cast<uint64_t>(re - rb) * n_cchunks;
+    const unsigned g = static_cast<unsigned>(std::min<uint64_t>(std::max<uint64_t>(items, 1), 148ull * 16));
+    if (bp.nz <= 8)
+      root_col_kernel<8><<<g, 256, col_smem, s>>>(grid, scan, bp, L, rb, re, hist, n_cchunks, stage,
+                                                  scores, probes);
+    else if (bp.nz <= 16)
+      root_col_kernel<16><<<g, 256, col_smem, s>>>(grid, scan, bp, L, rb, re, hist, n_cchunks, stage,
+                                                   scores, probes);
+    else
+      root_col_kernel<32><<<g, 256, col_smem, s>>>(grid, scan, bp, L, rb, re, hist, n_cchunks, stage,
+                                                   scores, probes);
+    BBS_CUDA(cudaGetLastError());
+    // rotations whose histogram overflowed: chunked kernel (exits at once when none)
+    launch_score_box_chunked(map, grid, scan, bp, rb, re, hist.overflow, scores, probes, s);
+  }
 }
 
 void launch_score_runs8(const MapView& map, const GridView& grid, const ScanView& scan,

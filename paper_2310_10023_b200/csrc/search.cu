@@ -471,41 +471,19 @@ __global__ void soa_kernel(const double* __restrict__ aos, uint64_t k, double* _
     soa[2 * k + i] = aos[3 * i + 2];
   }
 }
-
-// Own root predicate for DeviceSelect: ref index own(i) = i * world + rank.
-struct OwnRootSurvives {
+// Root ownership predicate over initial_nodes() order: the root scores buffer
+// is pre-filled with -1, so only owned roots can reach the threshold (>= 0).
+struct RootSurvives {
   const int32_t* scores;
   int32_t threshold;
   __host__ __device__ bool operator()(const unsigned long long& r) const {
     return scores[r] >= threshold;
   }
 };
-struct OwnIndex {
-  unsigned long long world, rank;
-  __host__ __device__ unsigned long long operator()(const unsigned long long& i) const {
-    return i * world + rank;
-  }
-};
 
 unsigned grid1(uint64_t n, int threads = 256) {
   return static_cast<unsigned>(std::min<uint64_t>(std::max<uint64_t>((n + threads - 1) / threads, 1), 148ull * 16));
 }
-
-struct Events {
-  std::vector<cudaEvent_t> ev;
-  size_t used = 0;
-  cudaEvent_t next() {
-    if (used == ev.size()) {
-      cudaEvent_t e;
-      BBS_CUDA(cudaEventCreate(&e));
-      ev.push_back(e);
-    }
-    return ev[used++];
-  }
-  ~Events() {
-    for (auto e : ev) cudaEventDestroy(e);
-  }
-};
 
 float elapsed(cudaEvent_t a, cudaEvent_t b) {
   float ms = 0;
@@ -526,6 +504,104 @@ T* dalloc(size_t n, cudaStream_t s) {
   BBS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), std::max<size_t>(n, 1) * sizeof(T), s));
   return p;
 }
+
+// Device buffer that only ever grows; reused across searches.
+template <typename T>
+struct Buf {
+  T* p = nullptr;
+  size_t cap = 0;
+  T* get(size_t n, cudaStream_t s, bool keep = false, size_t keep_n = 0) {
+    if (n <= cap) return p;
+    const size_t c = std::max<size_t>(n, cap + cap / 2);
+    T* np = dalloc<T>(c, s);
+    if (keep && p && keep_n) BBS_CUDA(cudaMemcpyAsync(np, p, keep_n * sizeof(T), cudaMemcpyDeviceToDevice, s));
+    if (p) BBS_CUDA(cudaFreeAsync(p, s));
+    p = np;
+    cap = c;
+    return p;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+  }
+};
+
+}  // namespace
+
+// Persistent device workspace of one search (K5/K6 buffers, root scratch,
+// pinned status mirror, event pool).  Acquired from the map's pool per call,
+// so steady-state searches allocate nothing.
+struct Workspace {
+  Buf<double2> lut;
+  Buf<int32_t> root_scores;
+  Buf<unsigned long long> probes, surv_idx, k0, qk0, qk1, s_key, s_key2;
+  Buf<int> nsel;
+  Buf<unsigned char> temp;
+  Buf<bbs_node> n0, qn0, qn1, pending, s_node, s_node2;
+  Buf<uint32_t> perm0, perm1, exp_parent, exp_off;
+  Buf<int32_t> pscores, trace, hist_n;
+  Buf<int4> hist_ent;
+  Buf<uint32_t> hist_amb;
+  Buf<EpochState> st;
+  EpochState* h_st = nullptr;
+  unsigned long long* h_small = nullptr;  // pinned: probes, n_root_surv
+  std::vector<cudaEvent_t> ev;
+  size_t ev_used = 0;
+  cudaEvent_t next_event() {
+    if (ev_used == ev.size()) {
+      cudaEvent_t e;
+      BBS_CUDA(cudaEventCreate(&e));
+      ev.push_back(e);
+    }
+    return ev[ev_used++];
+  }
+  void release_all() {
+    for (auto* b : {&root_scores, &pscores, &trace, &hist_n}) b->release();
+    for (auto* b : {&probes, &surv_idx, &k0, &qk0, &qk1, &s_key, &s_key2}) b->release();
+    for (auto* b : {&n0, &qn0, &qn1, &pending, &s_node, &s_node2}) b->release();
+    for (auto* b : {&perm0, &perm1, &exp_parent, &exp_off, &hist_amb}) b->release();
+    lut.release();
+    nsel.release();
+    temp.release();
+    hist_ent.release();
+    st.release();
+    if (h_st) cudaFreeHost(h_st);
+    if (h_small) cudaFreeHost(h_small);
+    for (auto e : ev) cudaEventDestroy(e);
+  }
+};
+
+void free_workspace(Workspace* w) {
+  if (!w) return;
+  w->release_all();
+  delete w;
+}
+
+namespace {
+
+// RAII lease of a workspace from the map's pool.
+struct Lease {
+  bbs_map* m;
+  Workspace* w;
+  explicit Lease(bbs_map* map) : m(map), w(nullptr) {
+    std::lock_guard<std::mutex> lk(m->ws_mu);
+    if (!m->ws_pool.empty()) {
+      w = m->ws_pool.back();
+      m->ws_pool.pop_back();
+    }
+    if (!w) {
+      w = new Workspace();
+      BBS_CUDA(cudaMallocHost(reinterpret_cast<void**>(&w->h_st), sizeof(EpochState)));
+      BBS_CUDA(cudaMallocHost(reinterpret_cast<void**>(&w->h_small), 4 * sizeof(unsigned long long)));
+    }
+    w->ev_used = 0;
+  }
+  ~Lease() {
+    std::lock_guard<std::mutex> lk(m->ws_mu);
+    m->ws_pool.push_back(w);
+  }
+};
 
 }  // namespace
 
@@ -581,6 +657,8 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
   if (rank < 0 || rank >= world) throw Error(BBS_ERR_CONFIG, "search: shard rank out of range");
 
   DeviceGuard dg(m->device);
+  Lease lease(m);
+  Workspace& W = *lease.w;
   cudaStream_t s = m->stream;
   const uint64_t K = scan->k;
   const int32_t threshold =
@@ -593,28 +671,35 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
   trans_index_range(tr.min.x, tr.max.x, cell, &x0, &x1);
   trans_index_range(tr.min.y, tr.max.y, cell, &y0, &y1);
   trans_index_range(tr.min.z, tr.max.z, cell, &z0, &z1);
-  const int64_t nx = static_cast<int64_t>(x1) - x0 + 1, ny = static_cast<int64_t>(y1) - y0 + 1,
-                nz = static_cast<int64_t>(z1) - z0 + 1;
+  int64_t nx = static_cast<int64_t>(x1) - x0 + 1, ny = static_cast<int64_t>(y1) - y0 + 1,
+          nz = static_cast<int64_t>(z1) - z0 + 1;
   const int64_t nr = grid.axis(0, L).index_count(), np = grid.axis(1, L).index_count(),
                 nw = grid.axis(2, L).index_count();
-  const int64_t total = nx * ny * nz * nr * np * nw;
+  int64_t total = nx * ny * nz * nr * np * nw;
   if (total <= 0) throw Error(BBS_ERR_EMPTY_SEARCH_SPACE, "initial node set is empty");
+  if (nx <= 0 || ny <= 0 || nz <= 0) {
+    // two negative extents: the reference's product is positive but its
+    // loops produce no node (nodes.hpp:77-79)
+    nx = ny = nz = 0;
+    total = 0;
+  }
   if (nx * ny * nz >= (1ll << 32) || nr * np * nw >= (1ll << 32) || total >= (1ll << 40))
     throw Error(BBS_ERR_TOO_LARGE, "search: root set too large");
 
   GridView gv;
   const std::vector<double> lut = build_lut(grid, &gv);
-  double2* d_lut = dalloc<double2>(lut.size() / 2, s);
+  double2* d_lut = W.lut.get(lut.size() / 2, s);
   BBS_CUDA(cudaMemcpyAsync(d_lut, lut.data(), lut.size() * sizeof(double), cudaMemcpyHostToDevice, s));
   gv.lut = d_lut;
   const ScanView sv{scan->soa, scan->soa + K, scan->soa + 2 * K, static_cast<uint32_t>(K)};
   const uint64_t maxc = max_children(grid);
   const uint64_t pend_cap = cfg.batch_size + maxc;
   const int strategy = cfg.strategy;
+  uint64_t h2d = lut.size() * sizeof(double), d2h = 0;
+  uint64_t launches = 0;
 
-  Events evs;
-  cudaEvent_t ev_start = evs.next(), ev_roots0 = evs.next(), ev_roots1 = evs.next(),
-              ev_loop = evs.next();
+  cudaEvent_t ev_start = W.next_event(), ev_roots0 = W.next_event(), ev_roots1 = W.next_event(),
+              ev_loop = W.next_event();
   BBS_CUDA(cudaEventRecord(ev_start, s));
 
   // ---- root batch (search.hpp:111-124) ----
@@ -631,61 +716,77 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
   bp.nw = static_cast<uint32_t>(nw);
   bp.rank = static_cast<uint32_t>(rank);
   bp.world = static_cast<uint32_t>(world);
+  const uint32_t nrot = bp.nr * bp.np * bp.nw;
+  uint64_t n_own = 0;  // roots owned by this rank
   {
-    const uint64_t ntrans = static_cast<uint64_t>(nx * ny * nz);
-    uint64_t g = static_cast<uint64_t>(world), b2 = static_cast<uint64_t>(nr * np * nw) % world;
-    while (b2) {
-      const uint64_t t = g % b2;
-      g = b2;
-      b2 = t;
-    }
-    const uint64_t P = static_cast<uint64_t>(world) / g;
-    const uint64_t own_max = (ntrans + P - 1) / P;
+    uint32_t P = 1, x0r = 0;
+    for (uint32_t rot = 0; rot < nrot; ++rot)
+      if (owned_slabs(bp, nrot, rot, &P, &x0r) && x0r < bp.nx)
+        n_own += static_cast<uint64_t>((bp.nx - x0r + P - 1) / P) * bp.ny * bp.nz;
+    BoxParams b0 = bp;
+    owned_slabs(b0, nrot, 0, &P, &x0r);
+    const uint64_t own_max = static_cast<uint64_t>((bp.nx + P - 1) / P) * bp.ny * bp.nz;
     bp.n_tchunks = static_cast<uint32_t>((own_max + kBoxTransPerCta - 1) / kBoxTransPerCta);
     const double tmax = std::max({std::fabs(static_cast<double>(x0)), std::fabs(static_cast<double>(x1)),
                                   std::fabs(static_cast<double>(y0)), std::fabs(static_cast<double>(y1)),
                                   std::fabs(static_cast<double>(z0)), std::fabs(static_cast<double>(z1))});
     bp.tmax = tmax + 2.0;
   }
-  const uint64_t n_own = (static_cast<uint64_t>(total) + world - 1 - rank) / world;
-  int32_t* root_scores = dalloc<int32_t>(static_cast<size_t>(total), s);
+  int32_t* root_scores = W.root_scores.get(static_cast<size_t>(std::max<int64_t>(total, 1)), s);
+  unsigned long long* d_probes = W.probes.get(1, s);
+  int* d_nsel = W.nsel.get(1, s);
+  RootHist hist{};
+  hist.entries = W.hist_ent.get(static_cast<size_t>(kRotBatch) * kHistCap, s);
+  hist.amb = W.hist_amb.get(static_cast<size_t>(kRotBatch) * kAmbCap, s);
+  int32_t* hn = W.hist_n.get(3 * kRotBatch + 1, s);
+  hist.n_ent = hn;
+  hist.n_amb = hn + kRotBatch;
+  hist.overflow = hn + 2 * kRotBatch;  // kRotBatch flags + 1 overflow counter
+  BBS_CUDA(cudaMemsetAsync(root_scores, 0xFF, static_cast<size_t>(std::max<int64_t>(total, 1)) * 4, s));
+  BBS_CUDA(cudaMemsetAsync(d_probes, 0, sizeof(unsigned long long), s));
   BBS_CUDA(cudaEventRecord(ev_roots0, s));
-  launch_score_box(m->view, gv, sv, bp, root_scores, s);
+  if (total > 0) {
+    launch_score_roots(m->view, gv, sv, bp, hist, root_scores, d_probes, s);
+    launches += 3 * ((nrot + kRotBatch - 1) / kRotBatch);
+  }
   BBS_CUDA(cudaEventRecord(ev_roots1, s));
 
   // survivors >= threshold among own roots, in initial_nodes order
-  unsigned long long* surv_idx = dalloc<unsigned long long>(n_own, s);
-  int* d_nsel = dalloc<int>(1, s);
-  {
-    cub::CountingInputIterator<unsigned long long> cnt(0);
-    cub::TransformInputIterator<unsigned long long, OwnIndex, cub::CountingInputIterator<unsigned long long>>
-        own(cnt, OwnIndex{static_cast<unsigned long long>(world), static_cast<unsigned long long>(rank)});
-    size_t tb = 0;
-    BBS_CUDA(cub::DeviceSelect::If(nullptr, tb, own, surv_idx, d_nsel, static_cast<int64_t>(n_own),
-                                   OwnRootSurvives{root_scores, threshold}, s));
-    void* temp = dalloc<unsigned char>(tb, s);
-    BBS_CUDA(cub::DeviceSelect::If(temp, tb, own, surv_idx, d_nsel, static_cast<int64_t>(n_own),
-                                   OwnRootSurvives{root_scores, threshold}, s));
-    BBS_CUDA(cudaFreeAsync(temp, s));
-  }
+  unsigned long long* surv_idx = W.surv_idx.get(static_cast<size_t>(std::max<uint64_t>(n_own, 1)), s);
   int n_root_surv = 0;
-  BBS_CUDA(cudaMemcpyAsync(&n_root_surv, d_nsel, sizeof(int), cudaMemcpyDeviceToHost, s));
-  BBS_CUDA(cudaStreamSynchronize(s));
+  if (total > 0) {
+    cub::CountingInputIterator<unsigned long long> cnt(0);
+    size_t tb = 0;
+    BBS_CUDA(cub::DeviceSelect::If(nullptr, tb, cnt, surv_idx, d_nsel, static_cast<int64_t>(total),
+                                   RootSurvives{root_scores, threshold}, s));
+    void* temp = W.temp.get(tb, s);
+    BBS_CUDA(cub::DeviceSelect::If(temp, tb, cnt, surv_idx, d_nsel, static_cast<int64_t>(total),
+                                   RootSurvives{root_scores, threshold}, s));
+    BBS_CUDA(cudaMemcpyAsync(&W.h_small[0], d_probes, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+    BBS_CUDA(cudaMemcpyAsync(&W.h_small[1], d_nsel, sizeof(int), cudaMemcpyDeviceToHost, s));
+    d2h += sizeof(unsigned long long) + sizeof(int);
+    BBS_CUDA(cudaStreamSynchronize(s));
+    n_root_surv = *reinterpret_cast<int*>(&W.h_small[1]);
+  } else {
+    W.h_small[0] = 0;
+  }
+  const unsigned long long root_probes = W.h_small[0];
 
   // queue buffers
-  const int E = (shard && shard->allreduce_max) ? 1 : 4;  // epochs per host check
+  const int E = (shard && shard->allreduce_max) ? 1 : 8;  // epochs per host check
   uint64_t qcap = static_cast<uint64_t>(n_root_surv) + static_cast<uint64_t>(E + 1) * pend_cap;
   Queue q{};
-  for (int i = 0; i < 2; ++i) {
-    q.key[i] = dalloc<unsigned long long>(qcap, s);
-    q.node[i] = dalloc<bbs_node>(qcap, s);
-  }
+  q.key[0] = W.qk0.get(qcap, s);
+  q.key[1] = W.qk1.get(qcap, s);
+  q.node[0] = W.qn0.get(qcap, s);
+  q.node[1] = W.qn1.get(qcap, s);
+  qcap = std::min({W.qk0.cap, W.qk1.cap, W.qn0.cap, W.qn1.cap});
   if (n_root_surv > 0) {
     // keys in initial_nodes order (seq = position), then sort by key
-    unsigned long long* k0 = dalloc<unsigned long long>(n_root_surv, s);
-    bbs_node* n0 = dalloc<bbs_node>(n_root_surv, s);
-    uint32_t* perm0 = dalloc<uint32_t>(n_root_surv, s);
-    uint32_t* perm1 = dalloc<uint32_t>(n_root_surv, s);
+    unsigned long long* k0 = W.k0.get(n_root_surv, s);
+    bbs_node* n0 = W.n0.get(n_root_surv, s);
+    uint32_t* perm0 = W.perm0.get(n_root_surv, s);
+    uint32_t* perm1 = W.perm1.get(n_root_surv, s);
     roots_to_queue_kernel<<<grid1(n_root_surv), 256, 0, s>>>(surv_idx, n_root_surv, root_scores, bp,
                                                              strategy, k0, n0);
     BBS_CUDA(cudaGetLastError());
@@ -694,19 +795,14 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
     cub::DoubleBuffer<uint32_t> dv(perm0, perm1);
     size_t tb = 0;
     BBS_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, dk, dv, n_root_surv, 0, 64, s));
-    void* temp = dalloc<unsigned char>(tb, s);
+    void* temp = W.temp.get(tb, s);
     BBS_CUDA(cub::DeviceRadixSort::SortPairs(temp, tb, dk, dv, n_root_surv, 0, 64, s));
     if (dk.Current() != q.key[0])
       BBS_CUDA(cudaMemcpyAsync(q.key[0], dk.Current(), n_root_surv * 8ull, cudaMemcpyDeviceToDevice, s));
     gather_nodes_kernel<<<grid1(n_root_surv), 256, 0, s>>>(dv.Current(), n0, q.node[0], n_root_surv);
     BBS_CUDA(cudaGetLastError());
-    for (void* p : {static_cast<void*>(k0), static_cast<void*>(n0), static_cast<void*>(perm0),
-                    static_cast<void*>(perm1), temp})
-      BBS_CUDA(cudaFreeAsync(p, s));
+    launches += 3;  // roots_to_queue, iota, gather
   }
-  BBS_CUDA(cudaFreeAsync(surv_idx, s));
-  BBS_CUDA(cudaFreeAsync(d_nsel, s));
-  BBS_CUDA(cudaFreeAsync(root_scores, s));
 
   EpochState h0{};
   h0.best = threshold;
@@ -719,26 +815,26 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
   h0.last_best_epoch = -1;
   h0.active = n_root_surv > 0 ? 1 : 0;
   h0.q_peak = h0.q_len;
-  EpochState* d_st = dalloc<EpochState>(1, s);
-  EpochState* h_st = nullptr;
-  BBS_CUDA(cudaMallocHost(reinterpret_cast<void**>(&h_st), sizeof(EpochState)));
-  BBS_CUDA(cudaMemcpyAsync(d_st, &h0, sizeof(h0), cudaMemcpyHostToDevice, s));
+  EpochState* d_st = W.st.get(1, s);
+  *W.h_st = h0;
+  BBS_CUDA(cudaMemcpyAsync(d_st, W.h_st, sizeof(h0), cudaMemcpyHostToDevice, s));
+  h2d += sizeof(h0);
   BBS_CUDA(cudaEventRecord(ev_loop, s));
 
-  bbs_node* pending = dalloc<bbs_node>(pend_cap, s);
-  int32_t* pscores = dalloc<int32_t>(pend_cap, s);
+  bbs_node* pending = W.pending.get(pend_cap, s);
+  int32_t* pscores = W.pscores.get(pend_cap, s);
   const uint64_t exp_cap = pend_cap / 8 + 2;
-  uint32_t* exp_parent = dalloc<uint32_t>(exp_cap, s);
-  uint32_t* exp_off = dalloc<uint32_t>(exp_cap, s);
-  unsigned long long* s_key = dalloc<unsigned long long>(pend_cap, s);
-  bbs_node* s_node = dalloc<bbs_node>(pend_cap, s);
-  unsigned long long* s_key2 = dalloc<unsigned long long>(pend_cap, s);
-  bbs_node* s_node2 = dalloc<bbs_node>(pend_cap, s);
+  uint32_t* exp_parent = W.exp_parent.get(exp_cap, s);
+  uint32_t* exp_off = W.exp_off.get(exp_cap, s);
+  unsigned long long* s_key = W.s_key.get(pend_cap, s);
+  bbs_node* s_node = W.s_node.get(pend_cap, s);
+  unsigned long long* s_key2 = W.s_key2.get(pend_cap, s);
+  bbs_node* s_node2 = W.s_node2.get(pend_cap, s);
   const uint64_t trace_cap = cfg.collect_trace ? std::max<uint64_t>(out->trace_capacity, 1) : 0;
-  int32_t* d_trace = dalloc<int32_t>(std::max<uint64_t>(trace_cap, 1), s);
+  int32_t* d_trace = W.trace.get(std::max<uint64_t>(trace_cap, 1), s);
   const uint32_t ptiles = choose_ptiles((pend_cap + 7) / 8, static_cast<uint32_t>(K));
 
-  std::vector<cudaEvent_t> pass_ev;                  // after each frontier pass
+  std::vector<cudaEvent_t> pass_ev;  // after each frontier pass
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> score_ev;
   EpochState hs = h0;
   bool self_active = h0.active != 0;
@@ -750,11 +846,12 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
       throw Error(BBS_ERR_GENERIC, "search: incumbent all-reduce failed");
     others_active = v[1] != 0;
     if (v[0] > hs.best) {
-      const int32_t nb = static_cast<int32_t>(v[0]);
-      hs.best = nb;
-      BBS_CUDA(cudaMemcpyAsync(reinterpret_cast<char*>(d_st) + offsetof(EpochState, best), &nb,
-                               sizeof(nb), cudaMemcpyHostToDevice, s));
-      BBS_CUDA(cudaStreamSynchronize(s));  // nb lives on this stack frame
+      hs.best = static_cast<int32_t>(v[0]);
+      W.h_st->best = hs.best;
+      BBS_CUDA(cudaMemcpyAsync(reinterpret_cast<char*>(d_st) + offsetof(EpochState, best),
+                               &W.h_st->best, sizeof(int32_t), cudaMemcpyHostToDevice, s));
+      h2d += sizeof(int32_t);
+      BBS_CUDA(cudaStreamSynchronize(s));
     }
   };
   exchange();  // after the root batch
@@ -762,33 +859,26 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
   while (self_active || others_active) {
     // capacity: the queue grows by at most pend_cap per epoch
     if (static_cast<uint64_t>(hs.q_len) + static_cast<uint64_t>(E + 1) * pend_cap > qcap) {
-      const uint64_t ncap = 2 * (static_cast<uint64_t>(hs.q_len) + static_cast<uint64_t>(E + 1) * pend_cap);
-      for (int i = 0; i < 2; ++i) {
-        unsigned long long* nk = dalloc<unsigned long long>(ncap, s);
-        bbs_node* nn = dalloc<bbs_node>(ncap, s);
-        if (hs.q_len) {
-          BBS_CUDA(cudaMemcpyAsync(nk, q.key[i], hs.q_len * 8ull, cudaMemcpyDeviceToDevice, s));
-          BBS_CUDA(cudaMemcpyAsync(nn, q.node[i], hs.q_len * sizeof(bbs_node), cudaMemcpyDeviceToDevice, s));
-        }
-        BBS_CUDA(cudaFreeAsync(q.key[i], s));
-        BBS_CUDA(cudaFreeAsync(q.node[i], s));
-        q.key[i] = nk;
-        q.node[i] = nn;
-      }
-      qcap = ncap;
+      const uint64_t need = 2 * (static_cast<uint64_t>(hs.q_len) + static_cast<uint64_t>(E + 1) * pend_cap);
+      // the live queue sits in buffer hs.cur; keep its contents
+      q.key[0] = W.qk0.get(need, s, true, hs.cur == 0 ? hs.q_len : 0);
+      q.key[1] = W.qk1.get(need, s, true, hs.cur == 1 ? hs.q_len : 0);
+      q.node[0] = W.qn0.get(need, s, true, hs.cur == 0 ? hs.q_len : 0);
+      q.node[1] = W.qn1.get(need, s, true, hs.cur == 1 ? hs.q_len : 0);
+      qcap = std::min({W.qk0.cap, W.qk1.cap, W.qn0.cap, W.qn1.cap});
     }
     const int n_ep = self_active ? E : 1;
     for (int e = 0; e < n_ep; ++e) {
       frontier_kernel<<<1, kFT, 0, s>>>(d_st, q, gv, cfg.batch_size, exp_parent, exp_off, d_trace,
                                         trace_cap);
       BBS_CUDA(cudaGetLastError());
-      cudaEvent_t pe = evs.next();
+      cudaEvent_t pe = W.next_event();
       BBS_CUDA(cudaEventRecord(pe, s));
       pass_ev.push_back(pe);
       branch_kernel<<<grid1(pend_cap), 256, 0, s>>>(d_st, q, gv, exp_parent, exp_off, pending);
       BBS_CUDA(cudaGetLastError());
       if (ptiles > 1) BBS_CUDA(cudaMemsetAsync(pscores, 0, pend_cap * sizeof(int32_t), s));
-      cudaEvent_t s0 = evs.next(), s1 = evs.next();
+      cudaEvent_t s0 = W.next_event(), s1 = W.next_event();
       BBS_CUDA(cudaEventRecord(s0, s));
       launch_score_runs8(m->view, gv, sv, pending,
                          reinterpret_cast<const uint32_t*>(reinterpret_cast<char*>(d_st) +
@@ -804,22 +894,24 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
       BBS_CUDA(cudaGetLastError());
       finalize_kernel<<<1, 1, 0, s>>>(d_st);
       BBS_CUDA(cudaGetLastError());
+      launches += 7;  // frontier, branch, score, survivors, rank_sort, merge, finalize
     }
-    BBS_CUDA(cudaMemcpyAsync(h_st, d_st, sizeof(EpochState), cudaMemcpyDeviceToHost, s));
+    BBS_CUDA(cudaMemcpyAsync(W.h_st, d_st, sizeof(EpochState), cudaMemcpyDeviceToHost, s));
+    d2h += sizeof(EpochState);
     BBS_CUDA(cudaStreamSynchronize(s));
-    hs = *h_st;
+    hs = *W.h_st;
     self_active = hs.active != 0;
     if (shard && shard->allreduce_max)
       exchange();
     else
       others_active = false;
   }
-  cudaEvent_t ev_end = evs.next();
+  cudaEvent_t ev_end = W.next_event();
   BBS_CUDA(cudaEventRecord(ev_end, s));
-  BBS_CUDA(cudaEventSynchronize(ev_end));
-  BBS_CUDA(cudaMemcpyAsync(h_st, d_st, sizeof(EpochState), cudaMemcpyDeviceToHost, s));
+  BBS_CUDA(cudaMemcpyAsync(W.h_st, d_st, sizeof(EpochState), cudaMemcpyDeviceToHost, s));
+  d2h += sizeof(EpochState);
   BBS_CUDA(cudaStreamSynchronize(s));
-  hs = *h_st;
+  hs = *W.h_st;
 
   // ---- results ----
   std::memset(&out->stats, 0, sizeof(out->stats));
@@ -847,11 +939,17 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
   out->root_nodes = n_own;
   out->lookups = hs.nodes_generated * K;
   out->queue_peak = hs.q_peak;
+  out->root_probes = root_probes;
   out->trace_length = cfg.collect_trace ? hs.trace_len : 0;
   if (cfg.collect_trace && out->best_score_trace && hs.trace_len) {
     const uint64_t nt = std::min<uint64_t>(hs.trace_len, out->trace_capacity);
     BBS_CUDA(cudaMemcpyAsync(out->best_score_trace, d_trace, nt * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    BBS_CUDA(cudaStreamSynchronize(s));
+    d2h += nt * sizeof(int32_t);
   }
+  out->h2d_bytes = h2d;
+  out->d2h_bytes = d2h;
+  out->kernel_launches = launches;
   int32_t best = hs.best;
   bbs_node best_node = hs.best_node;
   int matched = hs.matched;
@@ -893,16 +991,6 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
     if (y >= two_pi) y = 0.0;
     out->best_pose.yaw = y;
   }
-
-  for (void* p : {static_cast<void*>(d_lut), static_cast<void*>(q.key[0]), static_cast<void*>(q.key[1]),
-                  static_cast<void*>(q.node[0]), static_cast<void*>(q.node[1]), static_cast<void*>(d_st),
-                  static_cast<void*>(pending), static_cast<void*>(pscores),
-                  static_cast<void*>(exp_parent), static_cast<void*>(exp_off), static_cast<void*>(s_key),
-                  static_cast<void*>(s_node), static_cast<void*>(s_key2), static_cast<void*>(s_node2),
-                  static_cast<void*>(d_trace)})
-    BBS_CUDA(cudaFreeAsync(p, s));
-  BBS_CUDA(cudaStreamSynchronize(s));
-  cudaFreeHost(h_st);
 }
 
 // batch_evaluate on device nodes (search.hpp:23-34).
