@@ -511,6 +511,7 @@ static int search_impl(const orc_map* m, const bbs_aabb* map_bbox, const double*
     }
   }
   stats->nodes_generated += nmine;
+  out->root_nodes = nmine;
   for (uint64_t i = 0; i < nmine; ++i) score_node(m, g, L, scan, k, &roots[i]);
   stats->batches_flushed++;
   for (uint64_t i = 0; i < nmine; ++i) {
