@@ -38,14 +38,14 @@ struct LevelView {
   double inv_cell;       // RN(1 / cell), fast-path only (exactness guarded)
   int32_t box_min[3];    // inclusive voxel box of the inflated set
   uint32_t dim[3];       // box extents
-  // bitmap: 8x8x4 bricks of 256 bits (one 32 B sector), x fastest
-  uint32_t nbx, nby, nbz;
+  // bitmap (z-column major): bit (uz & 31) of
+  // words[((uz >> 5) * dim[1] + uy) * dim[0] + ux]; one 32-bit word answers
+  // 32 consecutive z-voxels of an (x, y) column, consecutive x share sectors.
+  uint32_t nwz;          // ceil(dim[2] / 32) words per column
+  uint32_t pad2;
   const uint32_t* words;
   // hash: packed key = (x' << (by+bz)) | (y' << bz) | z', 4 slots per bucket
   const unsigned long long* slots;
-  // z-column bitmap (levels with dim[2] <= 32): colmap[uy * dim[0] + ux] has
-  // bit uz set when voxel (ux, uy, uz) is occupied.  Null otherwise.
-  const uint32_t* colmap;
   unsigned long long bucket_mask;  // buckets - 1 (buckets >= 2, power of two)
   uint32_t bucket_shift; // 64 - log2(buckets)
   uint32_t bits_y, bits_z;

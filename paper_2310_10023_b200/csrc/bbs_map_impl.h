@@ -29,7 +29,6 @@ struct bbs_map {
     uint64_t n_keys = 0;
     uint32_t bits[3] = {0, 0, 0};
     void* structure = nullptr;           // bitmap words or hash slots
-    uint32_t* colmap = nullptr;          // z-column bitmap (coarse levels)
   };
   std::vector<Level> levels;
   bbs::MapView view{};

@@ -32,15 +32,12 @@ __device__ __forceinline__ unsigned long long pack_key(uint32_t ux, uint32_t uy,
          (static_cast<unsigned long long>(uy) << bz) | static_cast<unsigned long long>(uz);
 }
 
-// Bitmap addressing: 8x8x4 bricks of 256 bits = one 32-byte sector.
-__device__ __forceinline__ uint32_t bitmap_word(const LevelView& L, uint32_t ux, uint32_t uy,
+// Bitmap addressing (z-column major).
+__device__ __forceinline__ uint64_t bitmap_word(const LevelView& L, uint32_t ux, uint32_t uy,
                                                 uint32_t uz) {
-  const uint32_t brick = ((uz >> 2) * L.nby + (uy >> 3)) * L.nbx + (ux >> 3);
-  return brick * 8u + (uz & 3u) * 2u + ((uy >> 2) & 1u);
+  return (static_cast<uint64_t>(uz >> 5) * L.dim[1] + uy) * L.dim[0] + ux;
 }
-__device__ __forceinline__ uint32_t bitmap_bit(uint32_t ux, uint32_t uy) {
-  return ((uy & 3u) << 3) | (ux & 7u);
-}
+__device__ __forceinline__ uint32_t bitmap_bit(uint32_t uz) { return uz & 31u; }
 
 // LevelMap::contains, voxel_map.hpp:127-135 — set membership on the
 // device layout.  Voxels outside the level's box are misses without a load.
@@ -52,7 +49,7 @@ __device__ __forceinline__ bool level_contains(const LevelView& L, int32_t x, in
   if (ux >= L.dim[0] || uy >= L.dim[1] || uz >= L.dim[2]) return false;
   if (L.layout == BBS_LAYOUT_BITMAP) {
     const uint32_t w = __ldg(&L.words[bitmap_word(L, ux, uy, uz)]);
-    return (w >> bitmap_bit(ux, uy)) & 1u;
+    return (w >> bitmap_bit(uz)) & 1u;
   }
   const unsigned long long key = pack_key(ux, uy, uz, L.bits_y, L.bits_z);
   uint64_t b = hash_bucket(key, L.bucket_shift);

@@ -91,6 +91,12 @@ void launch_score_runs8(const MapView& map, const GridView& grid, const ScanView
                         const bbs_node* nodes, const uint32_t* d_n, uint32_t n_max,
                         uint32_t n_ptiles, int32_t* scores, cudaStream_t s);
 
+// Same contract for the epoch flush, using the 2x2x2 translation-cube
+// structure of branch()'s output (z-column bitmap: 4 loads per point).
+void launch_score_cube8(const MapView& map, const GridView& grid, const ScanView& scan,
+                        const bbs_node* nodes, const uint32_t* d_n, uint32_t n_max,
+                        uint32_t n_ptiles, int32_t* scores, cudaStream_t s);
+
 // Score arbitrary nodes in place (node.score), grouping equal rotations on
 // the device.  Host-synchronous.
 void score_nodes_general(const MapView& map, const GridView& grid, const ScanView& scan,

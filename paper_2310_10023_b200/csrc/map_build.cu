@@ -134,20 +134,7 @@ __global__ void bitmap_set_kernel(const unsigned long long* __restrict__ keys, u
     const uint32_t ux = static_cast<uint32_t>(k >> (L.bits_y + L.bits_z));
     const uint32_t uy = static_cast<uint32_t>((k >> L.bits_z) & my);
     const uint32_t uz = static_cast<uint32_t>(k & mz);
-    atomicOr(&words[bitmap_word(L, ux, uy, uz)], 1u << bitmap_bit(ux, uy));
-  }
-}
-
-__global__ void colmap_set_kernel(const unsigned long long* __restrict__ keys, uint64_t n,
-                                  LevelView L, uint32_t* __restrict__ colmap) {
-  const unsigned long long my = (1ull << L.bits_y) - 1, mz = (1ull << L.bits_z) - 1;
-  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
-       i += uint64_t(gridDim.x) * blockDim.x) {
-    const unsigned long long k = keys[i];
-    const uint32_t ux = static_cast<uint32_t>(k >> (L.bits_y + L.bits_z));
-    const uint32_t uy = static_cast<uint32_t>((k >> L.bits_z) & my);
-    const uint32_t uz = static_cast<uint32_t>(k & mz);
-    atomicOr(&colmap[static_cast<uint64_t>(uy) * L.dim[0] + ux], 1u << uz);
+    atomicOr(&words[bitmap_word(L, ux, uy, uz)], 1u << bitmap_bit(uz));
   }
 }
 
@@ -286,13 +273,11 @@ void finish_level(bbs_map* m, int level, unsigned long long* keys, uint64_t n, c
     V.box_min[a] = static_cast<int32_t>(bmin[a]);
     V.dim[a] = static_cast<uint32_t>(dims[a]);
   }
-  V.nbx = static_cast<uint32_t>((dims[0] + 7) / 8);
-  V.nby = static_cast<uint32_t>((dims[1] + 7) / 8);
-  V.nbz = static_cast<uint32_t>((dims[2] + 3) / 4);
+  V.nwz = static_cast<uint32_t>((dims[2] + 31) / 32);
 
-  const uint64_t nbricks = static_cast<uint64_t>(V.nbx) * V.nby * V.nbz;
-  const bool bitmap_ok = nbricks < (1ull << 29);
-  const uint64_t bitmap_bytes = bitmap_ok ? nbricks * 32ull : ~0ull;
+  const uint64_t nwords = dims[0] * dims[1] * V.nwz;
+  const bool bitmap_ok = nwords < (1ull << 36);
+  const uint64_t bitmap_bytes = bitmap_ok ? nwords * 4ull : ~0ull;
   const uint64_t slots = std::max<uint64_t>(8, next_pow2(2 * n));
   const uint64_t hash_bytes = slots * 8ull;
 
@@ -311,7 +296,7 @@ void finish_level(bbs_map* m, int level, unsigned long long* keys, uint64_t n, c
       bytes = ob;
     }
   }
-  const uint64_t buckets = layout == BBS_LAYOUT_BITMAP ? nbricks * 256ull : slots;
+  const uint64_t buckets = layout == BBS_LAYOUT_BITMAP ? nwords * 32ull : slots;
   if (bytes > m->memory_cap)  // voxel_map.hpp:91-95 (same message form)
     throw Error(BBS_ERR_CAPACITY_EXCEEDED,
                 "level " + std::to_string(level) + ": bucket table of " + std::to_string(buckets) +
@@ -341,17 +326,6 @@ void finish_level(bbs_map* m, int level, unsigned long long* keys, uint64_t n, c
     L.structure = sl;
     hash_insert_kernel<<<grid_for(n), kThreads, 0, s>>>(keys, n, V, sl);
     BBS_CUDA(cudaGetLastError());
-  }
-  // z-column bitmap for short levels (used by the root-batch kernel)
-  const uint64_t col_bytes = static_cast<uint64_t>(V.dim[0]) * V.dim[1] * 4ull;
-  if (n && V.dim[2] <= 32 && col_bytes <= (256ull << 20)) {
-    uint32_t* cm = nullptr;
-    BBS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&cm), col_bytes, s));
-    BBS_CUDA(cudaMemsetAsync(cm, 0, col_bytes, s));
-    colmap_set_kernel<<<grid_for(n), kThreads, 0, s>>>(keys, n, V, cm);
-    BBS_CUDA(cudaGetLastError());
-    V.colmap = cm;
-    L.colmap = cm;
   }
   bbs_level_info& I = L.info;
   I.level = level;
@@ -544,7 +518,6 @@ bbs_map::~bbs_map() {
     for (auto& L : levels) {
       if (L.keys) cudaFree(L.keys);
       if (L.structure) cudaFree(L.structure);
-      if (L.colmap) cudaFree(L.colmap);
     }
     if (own_stream) cudaStreamDestroy(own_stream);
     cudaSetDevice(prev);

@@ -344,6 +344,112 @@ __global__ void __launch_bounds__(kBoxThreads, 2) score_box_kernel(MapView map, 
   }
 }
 
+// ---- epoch flush: 2x2x2 translation cubes -----------------------------------
+// pending holds the children of branch() (nodes.hpp:103-116): every 8
+// consecutive nodes share a rotation and have translations 2c + j,
+// j = (t >> 2, (t >> 1) & 1, t & 1) for t = 0..7.  Per scan point the 8
+// probes form a 2x2x2 voxel cube = 4 (x, y) columns x 2 z-bits of the
+// z-column bitmap: 4 word loads answer all 8 children.  One work item =
+// (run, tile of scan points); counts reduce warp -> CTA -> scores.
+__global__ void __launch_bounds__(256, 4) score_cube8_kernel(MapView map, GridView grid, ScanView scan,
+                                                             const bbs_node* __restrict__ nodes,
+                                                             const uint32_t* __restrict__ d_n,
+                                                             uint32_t n_ptiles,
+                                                             int32_t* __restrict__ scores) {
+  __shared__ double s_R[9];
+  __shared__ int32_t s_hdr[4];
+  __shared__ int32_t s_cnt[8];
+  const uint32_t n_runs = *d_n / 8;
+  const uint64_t n_items = static_cast<uint64_t>(n_runs) * n_ptiles;
+  const uint32_t k = scan.k;
+  const uint32_t tile = (k + n_ptiles - 1) / n_ptiles;
+  const int lane = threadIdx.x & 31;
+  for (uint64_t item = blockIdx.x; item < n_items; item += gridDim.x) {
+    const uint32_t run = static_cast<uint32_t>(item / n_ptiles);
+    const uint32_t pt = static_cast<uint32_t>(item % n_ptiles);
+    if (threadIdx.x == 0) {
+      const int4 a = reinterpret_cast<const int4*>(nodes)[2 * (8ull * run)];
+      const int4 b = reinterpret_cast<const int4*>(nodes)[2 * (8ull * run) + 1];
+      double R[9];
+      rotation_of(grid, b.z, a.w, b.x, b.y, R);
+#pragma unroll
+      for (int i = 0; i < 9; ++i) s_R[i] = R[i];
+      s_hdr[0] = a.x;
+      s_hdr[1] = a.y;
+      s_hdr[2] = a.z;
+      s_hdr[3] = b.z;
+    }
+    if (threadIdx.x < 8) s_cnt[threadIdx.x] = 0;
+    __syncthreads();
+    const int32_t bx = s_hdr[0], by = s_hdr[1], bz = s_hdr[2];
+    const LevelView L = map.level[s_hdr[3]];
+    double R[9];
+#pragma unroll
+    for (int i = 0; i < 9; ++i) R[i] = s_R[i];
+    const double tmax =
+        static_cast<double>(max(max(abs(bx), abs(by)), abs(bz))) + 3.0;  // children: b + 1
+    const bool bitmap = L.layout == BBS_LAYOUT_BITMAP;
+    const uint32_t dimx = L.dim[0], dimy = L.dim[1], dimz = L.dim[2];
+    const uint32_t ox = static_cast<uint32_t>(bx) - static_cast<uint32_t>(L.box_min[0]);
+    const uint32_t oy = static_cast<uint32_t>(by) - static_cast<uint32_t>(L.box_min[1]);
+    const uint32_t oz = static_cast<uint32_t>(bz) - static_cast<uint32_t>(L.box_min[2]);
+    const uint64_t plane = static_cast<uint64_t>(dimx) * dimy;
+    int cnt[8];
+#pragma unroll
+    for (int t = 0; t < 8; ++t) cnt[t] = 0;
+    const uint32_t p0 = pt * tile, p1 = min(k, p0 + tile);
+    for (uint32_t p = p0 + threadIdx.x; p < p1; p += blockDim.x) {
+      const double px = scan.x[p], py = scan.y[p], pz = scan.z[p];
+      const double rx = rot_row(R[0], R[1], R[2], px, py, pz);
+      const double ry = rot_row(R[3], R[4], R[5], px, py, pz);
+      const double rz = rot_row(R[6], R[7], R[8], px, py, pz);
+      int32_t fx, fy, fz;
+      const bool ok = fast_floor(rx, L.inv_cell, tmax, &fx) & fast_floor(ry, L.inv_cell, tmax, &fy) &
+                      fast_floor(rz, L.inv_cell, tmax, &fz);
+      if (ok && bitmap) {
+        const uint32_t ux = static_cast<uint32_t>(fx) + ox;
+        const uint32_t uy = static_cast<uint32_t>(fy) + oy;
+        const uint32_t z0 = static_cast<uint32_t>(fz) + oz, z1 = z0 + 1;
+        const bool in0 = z0 < dimz, in1 = z1 < dimz;
+        const bool same = (z0 >> 5) == (z1 >> 5);
+#pragma unroll
+        for (int d = 0; d < 4; ++d) {
+          const uint32_t x = ux + (d >> 1), y = uy + (d & 1);
+          if (x < dimx && y < dimy) {
+            const uint64_t col = static_cast<uint64_t>(y) * dimx + x;
+            const uint32_t w0 = in0 ? __ldg(&L.words[(z0 >> 5) * plane + col]) : 0u;
+            const uint32_t w1 = in1 ? (same ? w0 : __ldg(&L.words[(z1 >> 5) * plane + col])) : 0u;
+            cnt[2 * d] += (w0 >> (z0 & 31)) & 1u;
+            cnt[2 * d + 1] += (w1 >> (z1 & 31)) & 1u;
+          }
+        }
+      } else if (ok) {
+#pragma unroll
+        for (int t = 0; t < 8; ++t)
+          cnt[t] += level_contains(L, fx + bx + (t >> 2), fy + by + ((t >> 1) & 1), fz + bz + (t & 1)) ? 1 : 0;
+      } else {
+#pragma unroll
+        for (int t = 0; t < 8; ++t)
+          cnt[t] += exact_hit(L, rx, ry, rz, bx + (t >> 2), by + ((t >> 1) & 1), bz + (t & 1));
+      }
+    }
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      const int v = __reduce_add_sync(0xffffffffu, cnt[t]);
+      if (lane == 0 && v) atomicAdd(&s_cnt[t], v);
+    }
+    __syncthreads();
+    if (threadIdx.x < 8) {
+      const uint64_t idx = 8ull * run + threadIdx.x;
+      if (n_ptiles == 1)
+        scores[idx] = s_cnt[threadIdx.x];
+      else if (s_cnt[threadIdx.x])
+        atomicAdd(&scores[idx], s_cnt[threadIdx.x]);
+    }
+    __syncthreads();
+  }
+}
+
 // ---- root batch: whole-scan histogram + z-column kernel ---------------------
 // (1) root_hist_kernel: one CTA per root rotation de-duplicates the fast-path
 //     voxel offsets f of ALL K scan points in a shared-memory hash
@@ -464,9 +570,9 @@ __global__ void __launch_bounds__(256) root_col_kernel(GridView grid, ScanView s
   uint32_t* s_col = reinterpret_cast<uint32_t*>(s_ent + kEntTile);      // staged colmap
   const uint32_t nrot = bp.nr * bp.np * bp.nw;
   const uint32_t dimx = L.dim[0], dimy = L.dim[1];
-  const uint32_t* __restrict__ col = L.colmap;
+  const uint32_t* __restrict__ col = L.words;  // nwz == 1: one word per (x, y) column
   if (stage_col) {
-    for (uint32_t i = threadIdx.x; i < dimx * dimy; i += blockDim.x) s_col[i] = __ldg(&L.colmap[i]);
+    for (uint32_t i = threadIdx.x; i < dimx * dimy; i += blockDim.x) s_col[i] = __ldg(&L.words[i]);
     __syncthreads();
     col = s_col;
   }
@@ -624,7 +730,8 @@ void launch_score_roots(const MapView& map, const GridView& grid, const ScanView
                         unsigned long long* probes, cudaStream_t s) {
   const LevelView& L = map.level[bp.level];
   const uint32_t nrot = bp.nr * bp.np * bp.nw;
-  const bool col_ok = L.colmap != nullptr && bp.nz <= 32 && L.dim[0] > 0;
+  const bool col_ok = L.layout == BBS_LAYOUT_BITMAP && L.nwz == 1 && L.words != nullptr &&
+                      bp.nz <= 32 && L.dim[0] > 0;
   if (!col_ok) {
     launch_score_box_chunked(map, grid, scan, bp, 0, nrot, nullptr, scores, probes, s);
     return;
@@ -674,6 +781,15 @@ void launch_score_roots(const MapView& map, const GridView& grid, const ScanView
     // rotations whose histogram overflowed: chunked kernel (exits at once when none)
     launch_score_box_chunked(map, grid, scan, bp, rb, re, hist.overflow, scores, probes, s);
   }
+}
+
+void launch_score_cube8(const MapView& map, const GridView& grid, const ScanView& scan,
+                        const bbs_node* nodes, const uint32_t* d_n, uint32_t n_max,
+                        uint32_t n_ptiles, int32_t* scores, cudaStream_t s) {
+  const uint64_t items = static_cast<uint64_t>((n_max + 7) / 8) * n_ptiles;
+  const unsigned g = static_cast<unsigned>(std::min<uint64_t>(std::max<uint64_t>(items, 1), 148ull * 4 * 8));
+  score_cube8_kernel<<<g, 256, 0, s>>>(map, grid, scan, nodes, d_n, n_ptiles, scores);
+  BBS_CUDA(cudaGetLastError());
 }
 
 void launch_score_runs8(const MapView& map, const GridView& grid, const ScanView& scan,

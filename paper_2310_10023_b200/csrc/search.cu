@@ -98,7 +98,8 @@ __global__ void __launch_bounds__(kFT) frontier_kernel(EpochState* st, Queue q, 
                                                        uint32_t* __restrict__ exp_parent,
                                                        uint32_t* __restrict__ exp_off,
                                                        int32_t* __restrict__ trace,
-                                                       unsigned long long trace_cap) {
+                                                       unsigned long long trace_cap,
+                                                       int strategy) {
   using ScanI = cub::BlockScan<int, kFT>;
   using ScanU = cub::BlockScan<unsigned long long, kFT>;
   using RedI = cub::BlockReduce<int, kFT>;
@@ -106,6 +107,7 @@ __global__ void __launch_bounds__(kFT) frontier_kernel(EpochState* st, Queue q, 
     typename ScanI::TempStorage si;
     typename ScanU::TempStorage su;
     typename RedI::TempStorage ri;
+    typename cub::BlockReduce<unsigned long long, kFT>::TempStorage ru;
   } tmp;
   __shared__ int s_cut, s_lastlu;
   __shared__ unsigned long long s_sum_at_cut;
@@ -229,12 +231,23 @@ __global__ void __launch_bounds__(kFT) frontier_kernel(EpochState* st, Queue q, 
       break;
     }
     carry_sum += stotal;
+    if (strategy == BBS_STRATEGY_BFS) {
+      // BFS pops in non-increasing score order and B never decreases, so
+      // everything after the first pruned entry is pruned too (no children,
+      // no leaf updates): the queue drains here without walking the rest.
+      bool has_pr = false;
+#pragma unroll
+      for (int k = 0; k < kFIPT; ++k) has_pr |= valid[k] && pr[k];
+      if (__syncthreads_or(has_pr)) {
+        const uint32_t end = base + kFChunk;
+        if (tid == 0 && qlen > end) pruned += qlen - end;
+        break;
+      }
+    }
     __syncthreads();
   }
   __syncthreads();
-  const unsigned long long pruned_all = cub::BlockReduce<unsigned long long, kFT>(
-      *reinterpret_cast<typename cub::BlockReduce<unsigned long long, kFT>::TempStorage*>(&tmp))
-      .Sum(pruned);
+  const unsigned long long pruned_all = cub::BlockReduce<unsigned long long, kFT>(tmp.ru).Sum(pruned);
   if (tid == 0) {
     st->nodes_pruned += pruned_all;
     st->best = carry_best;
@@ -870,7 +883,7 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
     const int n_ep = self_active ? E : 1;
     for (int e = 0; e < n_ep; ++e) {
       frontier_kernel<<<1, kFT, 0, s>>>(d_st, q, gv, cfg.batch_size, exp_parent, exp_off, d_trace,
-                                        trace_cap);
+                                        trace_cap, strategy);
       BBS_CUDA(cudaGetLastError());
       cudaEvent_t pe = W.next_event();
       BBS_CUDA(cudaEventRecord(pe, s));
@@ -880,7 +893,7 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
       if (ptiles > 1) BBS_CUDA(cudaMemsetAsync(pscores, 0, pend_cap * sizeof(int32_t), s));
       cudaEvent_t s0 = W.next_event(), s1 = W.next_event();
       BBS_CUDA(cudaEventRecord(s0, s));
-      launch_score_runs8(m->view, gv, sv, pending,
+      launch_score_cube8(m->view, gv, sv, pending,
                          reinterpret_cast<const uint32_t*>(reinterpret_cast<char*>(d_st) +
                                                            offsetof(EpochState, n_children)),
                          static_cast<uint32_t>(pend_cap), ptiles, pscores, s);

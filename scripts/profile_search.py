@@ -1,0 +1,21 @@
+"""Profiling driver: the bench workload (C2 campus) searched N times."""
+import argparse, os, sys
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import bench
+import paper_2310_10023_b200 as B
+ap = argparse.ArgumentParser()
+ap.add_argument("--searches", type=int, default=3)
+ap.add_argument("--config", default="c2")
+ap.add_argument("--layout", default="auto")
+a = ap.parse_args()
+cfgd = bench.CONFIGS[a.config]
+m, s, gt = bench.build_inputs(B, cfgd)
+vm = B.MultiResVoxelMap.build(m, cfgd["r"], cfgd["max_level"], layout=B.Layout[a.layout.upper()])
+ds = B.DeviceScan(vm, s)
+cfg = bench.search_config(B, cfgd)
+for i in range(a.searches):
+    r = B.search_scan(vm, ds, cfg)
+    print(f"search {i}: best {r.best_score} evals {r.stats.nodes_generated} epochs {r.epochs} "
+          f"device {r.device_ms:.3f} ms root {r.root_score_ms:.3f} epoch-score {r.epoch_score_ms:.3f} "
+          f"launches {r.kernel_launches}", flush=True)
