@@ -276,7 +276,7 @@ void finish_level(bbs_map* m, int level, unsigned long long* keys, uint64_t n, c
   V.nwz = static_cast<uint32_t>((dims[2] + 31) / 32);
 
   const uint64_t nwords = dims[0] * dims[1] * V.nwz;
-  const bool bitmap_ok = nwords < (1ull << 36);
+  const bool bitmap_ok = nwords < (1ull << 32);  // 32-bit word indices in the kernels
   const uint64_t bitmap_bytes = bitmap_ok ? nwords * 4ull : ~0ull;
   const uint64_t slots = std::max<uint64_t>(8, next_pow2(2 * n));
   const uint64_t hash_bytes = slots * 8ull;
