@@ -252,6 +252,14 @@ int bbs_scan_upload(bbs_map_t map, const double* xyz, uint64_t k, bbs_scan_t* ou
 int bbs_scan_free(bbs_scan_t scan);
 int bbs_search_scan(bbs_map_t map, bbs_scan_t scan, const bbs_search_config* cfg,
                     bbs_search_result* result);
+/* search_scan on a caller stream (a cudaStream_t; NULL = the map's stream):
+ * independent searches on different streams run concurrently on the GPU
+ * (each call leases its own workspace; the map is shared read-only). */
+int bbs_search_scan_on(bbs_map_t map, bbs_scan_t scan, const bbs_search_config* cfg, void* stream,
+                       bbs_search_result* result);
+/* Non-blocking stream on `device` for bbs_search_scan_on. */
+int bbs_stream_create(int32_t device, void** out);
+int bbs_stream_destroy(void* stream);
 /* batch_evaluate over DEVICE node memory (n nodes at d_nodes) on `stream`
  * (a cudaStream_t, NULL = the map's stream).  Asynchronous. */
 int bbs_batch_evaluate_device(bbs_map_t map, bbs_scan_t scan, const bbs_search_config* cfg,

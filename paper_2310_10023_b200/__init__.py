@@ -598,12 +598,32 @@ def search(vmap: MultiResVoxelMap, scan, cfg: SearchConfig, trace_capacity=1 << 
     return _result_from_c(res, buf)
 
 
+class DeviceStream:
+    """A non-blocking CUDA stream owned by the library (concurrent searches)."""
+
+    def __init__(self, device=0):
+        self._h = C.c_void_p()
+        _check(lib.bbs_stream_create(int(device), C.byref(self._h)))
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            lib.bbs_stream_destroy(h)
+            self._h = None
+
+
 def search_scan(vmap: MultiResVoxelMap, dscan: DeviceScan, cfg: SearchConfig,
-                trace_capacity=1 << 16):
-    """search() on a device-resident scan (no host copy inside the call)."""
+                trace_capacity=1 << 16, stream=None):
+    """search() on a device-resident scan (no host copy inside the call).
+    `stream`: a DeviceStream or a raw cudaStream_t (int); searches on
+    different streams run concurrently."""
     res, buf = _new_result(trace_capacity if cfg.collect_trace else 0)
     c = cfg.to_c()
-    _check(lib.bbs_search_scan(vmap._h, dscan._h, C.byref(c), C.byref(res)))
+    if stream is None:
+        _check(lib.bbs_search_scan(vmap._h, dscan._h, C.byref(c), C.byref(res)))
+    else:
+        sp = stream._h if isinstance(stream, DeviceStream) else C.c_void_p(int(stream))
+        _check(lib.bbs_search_scan_on(vmap._h, dscan._h, C.byref(c), sp, C.byref(res)))
     return _result_from_c(res, buf)
 
 

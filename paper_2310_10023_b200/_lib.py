@@ -66,6 +66,10 @@ SIGNATURES = {
     "bbs_search_scan": (C.c_int, [_vp, _vp, C.POINTER(SearchConfigC), C.POINTER(SearchResultC)]),
     "bbs_batch_evaluate_device": (C.c_int, [_vp, _vp, C.POINTER(SearchConfigC), _d, _vp, _u64,
                                             _vp]),
+    "bbs_search_scan_on": (C.c_int, [_vp, _vp, C.POINTER(SearchConfigC), _vp,
+                                     C.POINTER(SearchResultC)]),
+    "bbs_stream_create": (C.c_int, [_i32, C.POINTER(_vp)]),
+    "bbs_stream_destroy": (C.c_int, [_vp]),
     "bbs_search_sharded": (C.c_int, [_vp, _vp, C.POINTER(SearchConfigC), C.POINTER(Shard),
                                      C.POINTER(SearchResultC)]),
     "bbs_scene_spec_default": (None, [_vp]),

@@ -16,7 +16,7 @@
 
 namespace bbs {
 void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const bbs_shard* shard,
-                bbs_search_result* out);
+                bbs_search_result* out, cudaStream_t stream = nullptr);
 void batch_evaluate_device(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, double d_max,
                            bbs_node* d_nodes, uint64_t n, cudaStream_t s, const int32_t* lo,
                            const int32_t* hi);
@@ -312,6 +312,32 @@ int bbs_search_scan(bbs_map_t map, bbs_scan_t scan, const bbs_search_config* cfg
     REQUIRE(map && scan && cfg && result, "null argument");
     REQUIRE(scan->map == map, "scan was uploaded for a different map");
     bbs::run_search(map, scan, *cfg, nullptr, result);
+  });
+}
+
+int bbs_search_scan_on(bbs_map_t map, bbs_scan_t scan, const bbs_search_config* cfg, void* stream,
+                       bbs_search_result* result) {
+  return guard([&] {
+    REQUIRE(map && scan && cfg && result, "null argument");
+    REQUIRE(scan->map == map, "scan was uploaded for a different map");
+    bbs::run_search(map, scan, *cfg, nullptr, result, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int bbs_stream_create(int32_t device, void** out) {
+  return guard([&] {
+    REQUIRE(out, "null argument");
+    require_device(device);
+    bbs::DeviceGuard g(device);
+    cudaStream_t s;
+    BBS_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    *out = s;
+  });
+}
+
+int bbs_stream_destroy(void* stream) {
+  return guard([&] {
+    if (stream) BBS_CUDA(cudaStreamDestroy(static_cast<cudaStream_t>(stream)));
   });
 }
 

@@ -646,9 +646,10 @@ bbs_scan* upload_scan(bbs_map* m, const double* xyz, uint64_t k) {
   return sc;
 }
 
-// search(), search.hpp:72-186, on the device.  `shard` may be null.
+// search(), search.hpp:72-186, on the device.  `shard` may be null;
+// `stream` null = the map's stream (concurrent searches use their own).
 void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const bbs_shard* shard,
-                bbs_search_result* out) {
+                bbs_search_result* out, cudaStream_t stream) {
   // validation, search.hpp:79-89, same order and messages
   if (scan->k == 0) throw Error(BBS_ERR_DEGENERATE_SCAN, "search: empty scan");
   if (m->r != cfg.min_resolution) throw Error(BBS_ERR_CONFIG, "search: config r does not match the map");
@@ -672,7 +673,7 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
   DeviceGuard dg(m->device);
   Lease lease(m);
   Workspace& W = *lease.w;
-  cudaStream_t s = m->stream;
+  cudaStream_t s = stream ? stream : m->stream;
   const uint64_t K = scan->k;
   const int32_t threshold =
       static_cast<int32_t>(std::floor(cfg.score_threshold_fraction * static_cast<double>(K)));
