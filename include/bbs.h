@@ -33,7 +33,7 @@
 extern "C" {
 #endif
 
-#define BBS_ABI_VERSION 1
+#define BBS_ABI_VERSION 2
 
 /* Status codes, 1:1 with the exception classes of errors.hpp:11-98. */
 typedef enum bbs_status {
@@ -64,7 +64,7 @@ enum { BBS_BRANCH_TRANS_ONLY = 0, BBS_BRANCH_ROTO_TRANS = 1 };
  * all layouts. */
 enum {
   BBS_LAYOUT_AUTO = 0,    /* per level: bitmap when it is not larger than the hash table */
-  BBS_LAYOUT_BITMAP = 1,  /* dense bit grid over the level's voxel box, 8x8x4 bricks = one 32 B sector */
+  BBS_LAYOUT_BITMAP = 1,  /* dense z-column bit grid over the level's voxel box (32 z per word) */
   BBS_LAYOUT_HASH = 2     /* open addressing, packed 64-bit keys, 4-key (32 B) buckets */
 };
 
@@ -135,6 +135,7 @@ typedef struct bbs_search_result {
   uint64_t h2d_bytes;     /* host->device bytes copied by this call */
   uint64_t d2h_bytes;     /* device->host bytes copied by this call */
   uint64_t kernel_launches; /* launches of this library's own kernels (CUB launches excluded) */
+  uint64_t evals_per_level[16]; /* nodes scored per tree level (roots included) */
 } bbs_search_result;
 
 /* AxisGrid, angular_grid.hpp:45-58. */

@@ -108,6 +108,13 @@ namespace detail {
 inline void check(int st) {
   if (st != BBS_OK) throw_status(st, bbs_last_error());
 }
+// The structs of bbs.h are passed by pointer: refuse a library built from a
+// different header version.
+inline void check_abi() {
+  if (bbs_abi_version() != BBS_ABI_VERSION)
+    throw Error("libbbs_b200.so ABI version " + std::to_string(bbs_abi_version()) +
+                " does not match bbs.h version " + std::to_string(BBS_ABI_VERSION));
+}
 }  // namespace detail
 
 // ---- geometry (geometry.hpp) ------------------------------------------------
@@ -531,6 +538,7 @@ class MultiResVoxelMap {
                                 double collision_target = kDefaultCollisionTarget,
                                 std::size_t memory_cap_bytes = LevelMap::kDefaultMemoryCapBytes,
                                 int device = 0, int layout = BBS_LAYOUT_AUTO) {
+    detail::check_abi();
     auto h = std::make_shared<detail::MapHandle>();
     const bbs_map_options o{device, layout};
     detail::check(bbs_map_build(xyz(map_points), map_points.size(), min_resolution, max_level,
@@ -542,6 +550,7 @@ class MultiResVoxelMap {
                                       double collision_target = kDefaultCollisionTarget,
                                       std::size_t memory_cap_bytes = LevelMap::kDefaultMemoryCapBytes,
                                       int device = 0) {
+    detail::check_abi();
     auto h = std::make_shared<detail::MapHandle>();
     std::vector<const std::int32_t*> ptrs;
     std::vector<std::uint64_t> counts;

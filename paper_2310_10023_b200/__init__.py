@@ -231,6 +231,7 @@ class SearchResult:
     h2d_bytes: int = 0
     d2h_bytes: int = 0
     kernel_launches: int = 0
+    evals_per_level: tuple = ()
 
 
 def _result_from_c(r: SearchResultC, trace_buf=None) -> SearchResult:
@@ -245,7 +246,7 @@ def _result_from_c(r: SearchResultC, trace_buf=None) -> SearchResult:
         epochs=r.epochs, lookups=r.lookups, device_ms=r.device_ms, root_score_ms=r.root_score_ms,
         epoch_score_ms=r.epoch_score_ms, root_nodes=r.root_nodes, queue_peak=r.queue_peak,
         root_probes=r.root_probes, h2d_bytes=r.h2d_bytes, d2h_bytes=r.d2h_bytes,
-        kernel_launches=r.kernel_launches)
+        kernel_launches=r.kernel_launches, evals_per_level=tuple(r.evals_per_level))
     if trace_buf is not None:
         out.best_score_trace = list(trace_buf[: min(r.trace_length, len(trace_buf))])
     return out

@@ -96,6 +96,7 @@ class SearchResultC(C.Structure):
         ("h2d_bytes", C.c_uint64),
         ("d2h_bytes", C.c_uint64),
         ("kernel_launches", C.c_uint64),
+        ("evals_per_level", C.c_uint64 * 16),
     ]
 
 

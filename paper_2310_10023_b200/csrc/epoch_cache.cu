@@ -1,0 +1,285 @@
+// epoch_cache.cu — rotation histogram cache for the flush batches (K4).
+//
+// Every run of a flush (8 consecutive children of branch(), one rotation, a
+// 2x2x2 translation cube) needs floor(R*p / cell) for all K scan points of
+// its (level, rotation).  Rotations recur across flushes (C3 city: ~1.1M
+// level-5 runs over ~1.3k level-5 rotations), so the de-duplicated histogram
+// {(f, count)} of each (level, rotation) is built ONCE per search and kept in
+// a device pool; a run then costs one cube probe per histogram entry instead
+// of one rotation + probe per scan point.  Direct-mapped: slot = base[level]
+// + dense rotation id, no sorting.  Per flush:
+//   claim  (one thread per run)  claims empty slots, lists the builds;
+//   build  (one CTA per claimed rotation) rotates the K points, dedups the
+//          voxel offsets in shared memory (raw per-point entries when they do
+//          not fit), appends entries + ambiguous points to the pool;
+//   probe  (one warp per (run, 256-entry chunk)) cube-probes the entries;
+//   cube   (score.cu) scores the runs at uncached levels / failed builds.
+// Exactness: the cached offsets use fast_floor with tmax = the largest
+// translation index any node of that level can have in this search, so they
+// are valid for every later run (score_common.cuh).
+#include <cub/cub.cuh>
+
+#include <algorithm>
+
+#include "kernels.h"
+#include "score_common.cuh"
+
+namespace bbs {
+
+namespace {
+
+constexpr int kCacheHashSlots = 8192;
+constexpr int kCacheHashCap = 4096;   // distinct offsets kept in shared memory
+constexpr int kCacheAmbCap = 2048;    // ambiguous points buffered per build
+constexpr int kProbeChunk = 256;      // histogram entries per warp item
+constexpr unsigned long long kEmptyKey = ~0ull;
+
+__device__ __forceinline__ uint32_t cache_hash(unsigned long long key) {
+  return static_cast<uint32_t>((key * 0x9E3779B97F4A7C15ull) >> 51);  // 13 bits
+}
+
+__device__ __forceinline__ bool run_slot(const RotCache& c, const GridView& G, const int4& a,
+                                         const int4& b, uint32_t* slot) {
+  // a = (ix, iy, iz, iroll) of child 0, b = (ipitch, iyaw, level, score)
+  const int l = b.z;
+  const uint32_t base = c.base[l];
+  if (base == 0xFFFFFFFFu) return false;
+  const uint32_t np = static_cast<uint32_t>(G.max_index[l * 3 + 1]) + 1;
+  const uint32_t nw = static_cast<uint32_t>(G.max_index[l * 3 + 2]) + 1;
+  *slot = base + (static_cast<uint32_t>(a.w) * np + static_cast<uint32_t>(b.x)) * nw +
+          static_cast<uint32_t>(b.y);
+  return true;
+}
+
+__global__ void cache_claim_kernel(RotCache c, GridView G, const bbs_node* __restrict__ pending,
+                                   const uint32_t* __restrict__ d_n) {
+  const uint32_t n_runs = *d_n / 8;
+  for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < n_runs; r += gridDim.x * blockDim.x) {
+    const int4 a = __ldg(reinterpret_cast<const int4*>(pending) + 16ull * r);
+    const int4 b = __ldg(reinterpret_cast<const int4*>(pending) + 16ull * r + 1);
+    uint32_t slot;
+    if (!run_slot(c, G, a, b, &slot)) continue;
+    if (c.info[slot].x != kCacheEmpty) continue;
+    if (atomicCAS(&c.info[slot].x, kCacheEmpty, kCacheBuilding) == kCacheEmpty) {
+      const uint32_t i = atomicAdd(&c.ctl[2], 1u);
+      c.builds[i] = make_int4(static_cast<int32_t>(slot), b.z, a.w, b.x);  // slot, level, ir, ip
+      c.builds_w[i] = b.y;                                                 // iw
+    }
+  }
+}
+
+__global__ void __launch_bounds__(512) cache_build_kernel(RotCache c, MapView map, GridView G,
+                                                          ScanView scan) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  unsigned long long* s_key = reinterpret_cast<unsigned long long*>(smem);   // 64 KB
+  int32_t* s_cnt = reinterpret_cast<int32_t*>(s_key + kCacheHashSlots);      // 32 KB
+  uint32_t* s_amb = reinterpret_cast<uint32_t*>(s_cnt + kCacheHashSlots);    // 8 KB
+  __shared__ int s_distinct, s_namb, s_over;
+  __shared__ uint32_t s_off, s_aoff;
+  const uint32_t n_build = c.ctl[2];
+  for (uint32_t bi = blockIdx.x; bi < n_build; bi += gridDim.x) {
+    const int4 bd = c.builds[bi];
+    const uint32_t slot = static_cast<uint32_t>(bd.x);
+    const int l = bd.y;
+    const LevelView& L = map.level[l];
+    const double tmax = c.tmax[l];
+    double R[9];
+    rotation_of(G, l, bd.z, bd.w, c.builds_w[bi], R);
+    for (int i = threadIdx.x; i < kCacheHashSlots; i += blockDim.x) {
+      s_key[i] = kEmptyKey;
+      s_cnt[i] = 0;
+    }
+    if (threadIdx.x == 0) {
+      s_distinct = 0;
+      s_namb = 0;
+      s_over = 0;
+    }
+    __syncthreads();
+    for (uint32_t p = threadIdx.x; p < scan.k; p += blockDim.x) {
+      const double px = scan.x[p], py = scan.y[p], pz = scan.z[p];
+      int32_t fx, fy, fz;
+      bool ok = fast_floor(rot_row(R[0], R[1], R[2], px, py, pz), L.inv_cell, tmax, &fx) &
+                fast_floor(rot_row(R[3], R[4], R[5], px, py, pz), L.inv_cell, tmax, &fy) &
+                fast_floor(rot_row(R[6], R[7], R[8], px, py, pz), L.inv_cell, tmax, &fz);
+      ok = ok && fx > -(1 << 20) && fx < (1 << 20) && fy > -(1 << 20) && fy < (1 << 20) &&
+           fz > -(1 << 20) && fz < (1 << 20);
+      if (!ok) {
+        const int a = atomicAdd(&s_namb, 1);
+        if (a < kCacheAmbCap) s_amb[a] = p;
+        continue;
+      }
+      if (s_distinct >= kCacheHashCap) {
+        s_over = 1;  // too many distinct offsets: raw per-point entries below
+        continue;
+      }
+      const unsigned long long key = (static_cast<unsigned long long>(fx + (1 << 20)) << 42) |
+                                     (static_cast<unsigned long long>(fy + (1 << 20)) << 21) |
+                                     static_cast<unsigned long long>(fz + (1 << 20));
+      uint32_t h = cache_hash(key);
+      for (;;) {
+        const unsigned long long prev = atomicCAS(&s_key[h], kEmptyKey, key);
+        if (prev == kEmptyKey) atomicAdd(&s_distinct, 1);
+        if (prev == kEmptyKey || prev == key) {
+          atomicAdd(&s_cnt[h], 1);
+          break;
+        }
+        h = (h + 1) & (kCacheHashSlots - 1);
+      }
+    }
+    __syncthreads();
+    const bool raw = s_over != 0;
+    const int namb = s_namb;
+    const uint32_t n_ent = raw ? scan.k - static_cast<uint32_t>(namb) : static_cast<uint32_t>(s_distinct);
+    if (threadIdx.x == 0) {
+      s_off = atomicAdd(&c.ctl[0], n_ent);
+      s_aoff = atomicAdd(&c.ctl[1], static_cast<uint32_t>(namb));
+    }
+    __syncthreads();
+    const uint32_t off = s_off, aoff = s_aoff;
+    const bool fits = namb <= kCacheAmbCap && static_cast<uint64_t>(off) + n_ent <= c.pool_cap &&
+                      static_cast<uint64_t>(aoff) + namb <= c.amb_cap;
+    if (fits) {
+      if (!raw) {
+        __shared__ int s_e;
+        if (threadIdx.x == 0) s_e = 0;
+        __syncthreads();
+        for (int i = threadIdx.x; i < kCacheHashSlots; i += blockDim.x) {
+          const unsigned long long key = s_key[i];
+          if (key != kEmptyKey) {
+            const int e = atomicAdd(&s_e, 1);
+            c.pool[off + e] = make_int4(static_cast<int32_t>((key >> 42) & 0x1FFFFF) - (1 << 20),
+                                        static_cast<int32_t>((key >> 21) & 0x1FFFFF) - (1 << 20),
+                                        static_cast<int32_t>(key & 0x1FFFFF) - (1 << 20), s_cnt[i]);
+          }
+        }
+      } else {
+        // raw: one entry per fast-path point (count 1), in point order
+        __shared__ int s_e;
+        if (threadIdx.x == 0) s_e = 0;
+        __syncthreads();
+        for (uint32_t p = threadIdx.x; p < scan.k; p += blockDim.x) {
+          const double px = scan.x[p], py = scan.y[p], pz = scan.z[p];
+          int32_t fx, fy, fz;
+          bool ok = fast_floor(rot_row(R[0], R[1], R[2], px, py, pz), L.inv_cell, tmax, &fx) &
+                    fast_floor(rot_row(R[3], R[4], R[5], px, py, pz), L.inv_cell, tmax, &fy) &
+                    fast_floor(rot_row(R[6], R[7], R[8], px, py, pz), L.inv_cell, tmax, &fz);
+          ok = ok && fx > -(1 << 20) && fx < (1 << 20) && fy > -(1 << 20) && fy < (1 << 20) &&
+               fz > -(1 << 20) && fz < (1 << 20);
+          if (!ok) continue;
+          const int e = atomicAdd(&s_e, 1);
+          c.pool[off + e] = make_int4(fx, fy, fz, 1);
+        }
+      }
+      for (int a = threadIdx.x; a < namb; a += blockDim.x) c.amb_pool[aoff + a] = s_amb[a];
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      c.amb_off[slot] = aoff;
+      // publish: entries first, then the state (readers run in later kernels)
+      c.info[slot] = fits ? make_int4(kCacheReady, static_cast<int32_t>(off), static_cast<int32_t>(n_ent), namb)
+                          : make_int4(kCacheNone, 0, 0, 0);
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(256) cache_probe_kernel(RotCache c, MapView map, GridView G,
+                                                          ScanView scan,
+                                                          const bbs_node* __restrict__ pending,
+                                                          const uint32_t* __restrict__ d_n,
+                                                          uint32_t chunks_per_run,
+                                                          int32_t* __restrict__ scores) {
+  const uint32_t n_runs = *d_n / 8;
+  const uint64_t n_items = static_cast<uint64_t>(n_runs) * chunks_per_run;
+  const int lane = threadIdx.x & 31;
+  const uint64_t n_warps = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
+  for (uint64_t item = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+       item < n_items; item += n_warps) {
+    const uint32_t run = static_cast<uint32_t>(item / chunks_per_run);
+    const uint32_t chunk = static_cast<uint32_t>(item % chunks_per_run);
+    const int4 a = __ldg(reinterpret_cast<const int4*>(pending) + 16ull * run);
+    const int4 b = __ldg(reinterpret_cast<const int4*>(pending) + 16ull * run + 1);
+    uint32_t slot;
+    if (!run_slot(c, G, a, b, &slot)) continue;
+    const int4 inf = c.info[slot];
+    if (inf.x != kCacheReady) continue;
+    const uint32_t e0 = chunk * kProbeChunk;
+    const uint32_t n_ent = static_cast<uint32_t>(inf.z);
+    const bool amb_here = chunk == 0 && inf.w > 0;
+    if (e0 >= n_ent && !amb_here) continue;
+    const int32_t bx = a.x, by = a.y, bz = a.z;
+    const LevelView& L = map.level[b.z];
+    const bool bitmap = L.layout == BBS_LAYOUT_BITMAP;
+    const uint32_t ox = static_cast<uint32_t>(bx) - static_cast<uint32_t>(L.box_min[0]);
+    const uint32_t oy = static_cast<uint32_t>(by) - static_cast<uint32_t>(L.box_min[1]);
+    const uint32_t oz = static_cast<uint32_t>(bz) - static_cast<uint32_t>(L.box_min[2]);
+    int acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    const uint32_t e1 = min(n_ent, e0 + kProbeChunk);
+    const int4* __restrict__ ent = c.pool + static_cast<uint32_t>(inf.y);
+    for (uint32_t e = e0 + lane; e < e1; e += 32) {
+      const int4 f = __ldg(ent + e);
+      if (bitmap) {
+        cube_probe(L, static_cast<uint32_t>(f.x) + ox, static_cast<uint32_t>(f.y) + oy,
+                   static_cast<uint32_t>(f.z) + oz, f.w, acc);
+      } else {
+#pragma unroll
+        for (int t = 0; t < 8; ++t)
+          acc[t] += level_contains(L, f.x + bx + (t >> 2), f.y + by + ((t >> 1) & 1), f.z + bz + (t & 1))
+                        ? f.w : 0;
+      }
+    }
+    if (amb_here) {
+      double R[9];
+      rotation_of(G, b.z, a.w, b.x, b.y, R);
+      const uint32_t* __restrict__ amb = c.amb_pool + c.amb_off[slot];
+      for (int q = lane; q < inf.w; q += 32) {
+        const uint32_t p = amb[q];
+        const double px = scan.x[p], py = scan.y[p], pz = scan.z[p];
+        const double rx = rot_row(R[0], R[1], R[2], px, py, pz);
+        const double ry = rot_row(R[3], R[4], R[5], px, py, pz);
+        const double rz = rot_row(R[6], R[7], R[8], px, py, pz);
+#pragma unroll
+        for (int t = 0; t < 8; ++t)
+          acc[t] += exact_hit(L, rx, ry, rz, bx + (t >> 2), by + ((t >> 1) & 1), bz + (t & 1));
+      }
+    }
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      const int v = __reduce_add_sync(0xffffffffu, acc[t]);
+      if (lane == 0 && v) atomicAdd(&scores[8ull * run + t], v);
+    }
+  }
+}
+
+}  // namespace
+
+void launch_epoch_score(const MapView& map, const GridView& grid, const ScanView& scan,
+                        const bbs_node* pending, const uint32_t* d_n, uint32_t n_max,
+                        uint32_t n_ptiles, int32_t* scores, const RotCache& cache, cudaStream_t s) {
+  if (!cache.enabled) {
+    launch_score_cube8(map, grid, scan, pending, d_n, n_max, n_ptiles, scores, nullptr, s);
+    return;
+  }
+  static bool attr_done = false;
+  const int build_smem = kCacheHashSlots * 12 + kCacheAmbCap * 4;
+  if (!attr_done) {
+    BBS_CUDA(cudaFuncSetAttribute(cache_build_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  build_smem));
+    attr_done = true;
+  }
+  const uint32_t max_runs = (n_max + 7) / 8;
+  BBS_CUDA(cudaMemsetAsync(cache.ctl + 2, 0, sizeof(uint32_t), s));  // build count
+  cache_claim_kernel<<<(max_runs + 255) / 256, 256, 0, s>>>(cache, grid, pending, d_n);
+  BBS_CUDA(cudaGetLastError());
+  cache_build_kernel<<<std::min<uint32_t>(std::max<uint32_t>(max_runs, 1), 148 * 2), 512, build_smem, s>>>(
+      cache, map, grid, scan);
+  BBS_CUDA(cudaGetLastError());
+  const uint32_t chunks = (scan.k + kProbeChunk - 1) / kProbeChunk;
+  const uint64_t warp_items = static_cast<uint64_t>(max_runs) * chunks;
+  const unsigned g = static_cast<unsigned>(std::min<uint64_t>((warp_items + 7) / 8 + 1, 148ull * 16));
+  cache_probe_kernel<<<g, 256, 0, s>>>(cache, map, grid, scan, pending, d_n, chunks, scores);
+  BBS_CUDA(cudaGetLastError());
+  launch_score_cube8(map, grid, scan, pending, d_n, n_max, n_ptiles, scores, &cache, s);
+}
+
+}  // namespace bbs

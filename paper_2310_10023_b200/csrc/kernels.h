@@ -91,11 +91,37 @@ void launch_score_runs8(const MapView& map, const GridView& grid, const ScanView
                         const bbs_node* nodes, const uint32_t* d_n, uint32_t n_max,
                         uint32_t n_ptiles, int32_t* scores, cudaStream_t s);
 
+// Per-search cache of de-duplicated scan histograms per (level, rotation)
+// for the flush batches (epoch_cache.cu).  info[slot] = {state, pool offset,
+// entries, ambiguous points}; slot = base[level] + dense rotation id.
+constexpr int32_t kCacheEmpty = -1, kCacheBuilding = -2, kCacheNone = -3, kCacheReady = 0;
+struct RotCache {
+  int enabled;
+  uint32_t base[kMaxLevels];   // 0xFFFFFFFF: level not cached
+  double tmax[kMaxLevels];     // translation-index bound of the level (+2)
+  int4* info;                  // [slots]
+  uint32_t* amb_off;           // [slots]
+  int4* pool;                  // (fx, fy, fz, count) entries
+  uint32_t* amb_pool;          // ambiguous scan point indices
+  uint32_t* ctl;               // [4] pool used, amb used, builds this flush, -
+  int4* builds;                // [max runs] (slot, level, iroll, ipitch)
+  int32_t* builds_w;           // [max runs] iyaw
+  uint64_t pool_cap, amb_cap;
+};
+
 // Same contract for the epoch flush, using the 2x2x2 translation-cube
 // structure of branch()'s output (z-column bitmap: 4 loads per point).
+// With `cache`, runs whose (level, rotation) histogram is READY are skipped.
 void launch_score_cube8(const MapView& map, const GridView& grid, const ScanView& scan,
                         const bbs_node* nodes, const uint32_t* d_n, uint32_t n_max,
-                        uint32_t n_ptiles, int32_t* scores, cudaStream_t s);
+                        uint32_t n_ptiles, int32_t* scores, const RotCache* cache,
+                        cudaStream_t s);
+
+// Flush scoring: cache claim/build/probe + the cube kernel for the rest.
+// scores must be zeroed first.
+void launch_epoch_score(const MapView& map, const GridView& grid, const ScanView& scan,
+                        const bbs_node* pending, const uint32_t* d_n, uint32_t n_max,
+                        uint32_t n_ptiles, int32_t* scores, const RotCache& cache, cudaStream_t s);
 
 // Score arbitrary nodes in place (node.score), grouping equal rotations on
 // the device.  Host-synchronous.

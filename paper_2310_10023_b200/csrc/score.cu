@@ -24,57 +24,11 @@
 
 #include "device_common.cuh"
 #include "kernels.h"
+#include "score_common.cuh"
 
 namespace bbs {
 
 namespace {
-
-// pose_to_transform, geometry.hpp:107-109, on LUT cos/sin (geometry.hpp:103-105).
-__device__ __forceinline__ void rotation_of(const GridView& G, int level, int ir, int ip, int iw,
-                                            double R[9]) {
-  const double2 a = G.lut[G.lut_off[level * 3 + 0] + (ir - G.lut_lo[level * 3 + 0])];
-  const double2 b = G.lut[G.lut_off[level * 3 + 1] + (ip - G.lut_lo[level * 3 + 1])];
-  const double2 g = G.lut[G.lut_off[level * 3 + 2] + (iw - G.lut_lo[level * 3 + 2])];
-  const double ca = a.x, sa = a.y, cb = b.x, sb = b.y, cg = g.x, sg = g.y;
-  R[0] = __dmul_rn(cg, cb);
-  R[1] = __dsub_rn(__dmul_rn(__dmul_rn(cg, sb), sa), __dmul_rn(sg, ca));
-  R[2] = __dadd_rn(__dmul_rn(__dmul_rn(cg, sb), ca), __dmul_rn(sg, sa));
-  R[3] = __dmul_rn(sg, cb);
-  R[4] = __dadd_rn(__dmul_rn(__dmul_rn(sg, sb), sa), __dmul_rn(cg, ca));
-  R[5] = __dsub_rn(__dmul_rn(__dmul_rn(sg, sb), ca), __dmul_rn(cg, sa));
-  R[6] = -sb;
-  R[7] = __dmul_rn(cb, sa);
-  R[8] = __dmul_rn(cb, ca);
-}
-
-// R*p in the reference's evaluation order (translation not yet added).
-__device__ __forceinline__ double rot_row(double r0, double r1, double r2, double px, double py,
-                                          double pz) {
-  return __dadd_rn(__dadd_rn(__dmul_rn(r0, px), __dmul_rn(r1, py)), __dmul_rn(r2, pz));
-}
-
-// Fast-path voxel offset of one axis; returns false when ambiguous.
-__device__ __forceinline__ bool fast_floor(double rp, double inv_cell, double tmax, int32_t* f) {
-  const double w = __dmul_rn(rp, inv_cell);
-  const double fl = floor(w);
-  const double fr = __dsub_rn(w, fl);
-  const double aw = fabs(w);
-  const double eps = __dmul_rn(__dadd_rn(aw, tmax), 0x1p-48);
-  const bool ok = (aw < 0x1p30) && (fr > eps) && (fr < __dsub_rn(1.0, eps));
-  *f = ok ? static_cast<int32_t>(fl) : 0;
-  return ok;
-}
-
-// Exact reference arithmetic for one (point, node): q = rp + cell*ix, then
-// floor(q / cell) with x86 conversion semantics, then contains().
-__device__ __forceinline__ int exact_hit(const LevelView& L, double rx, double ry, double rz,
-                                         int32_t ix, int32_t iy, int32_t iz) {
-  const int32_t vx = dev_voxel_index(__dadd_rn(rx, __dmul_rn(L.cell, static_cast<double>(ix))), L.cell);
-  const int32_t vy = dev_voxel_index(__dadd_rn(ry, __dmul_rn(L.cell, static_cast<double>(iy))), L.cell);
-  const int32_t vz = dev_voxel_index(__dadd_rn(rz, __dmul_rn(L.cell, static_cast<double>(iz))), L.cell);
-  if (vx == INT32_MIN && vy == INT32_MIN && vz == INT32_MIN) return 0;  // kEmpty probe
-  return level_contains(L, vx, vy, vz) ? 1 : 0;
-}
 
 // ---- runs kernel ------------------------------------------------------------
 // One work item = (run of <= NT same-rotation nodes, tile of scan points).
@@ -355,7 +309,8 @@ __global__ void __launch_bounds__(256, 4) score_cube8_kernel(MapView map, GridVi
                                                              const bbs_node* __restrict__ nodes,
                                                              const uint32_t* __restrict__ d_n,
                                                              uint32_t n_ptiles,
-                                                             int32_t* __restrict__ scores) {
+                                                             int32_t* __restrict__ scores,
+                                                             RotCache cache, int use_cache) {
   __shared__ double s_R[9];
   __shared__ int32_t s_hdr[4];
   __shared__ int32_t s_cnt[8];
@@ -367,6 +322,19 @@ __global__ void __launch_bounds__(256, 4) score_cube8_kernel(MapView map, GridVi
   for (uint64_t item = blockIdx.x; item < n_items; item += gridDim.x) {
     const uint32_t run = static_cast<uint32_t>(item / n_ptiles);
     const uint32_t pt = static_cast<uint32_t>(item % n_ptiles);
+    if (use_cache) {
+      // runs scored from their rotation's cached histogram are skipped (uniform per CTA)
+      const int4 a = __ldg(reinterpret_cast<const int4*>(nodes) + 2 * (8ull * run));
+      const int4 b = __ldg(reinterpret_cast<const int4*>(nodes) + 2 * (8ull * run) + 1);
+      const uint32_t base = cache.base[b.z];
+      if (base != 0xFFFFFFFFu) {
+        const uint32_t np = static_cast<uint32_t>(grid.max_index[b.z * 3 + 1]) + 1;
+        const uint32_t nw = static_cast<uint32_t>(grid.max_index[b.z * 3 + 2]) + 1;
+        const uint32_t slot = base + (static_cast<uint32_t>(a.w) * np + static_cast<uint32_t>(b.x)) * nw +
+                              static_cast<uint32_t>(b.y);
+        if (cache.info[slot].x == kCacheReady) continue;
+      }
+    }
     if (threadIdx.x == 0) {
       const int4 a = reinterpret_cast<const int4*>(nodes)[2 * (8ull * run)];
       const int4 b = reinterpret_cast<const int4*>(nodes)[2 * (8ull * run) + 1];
@@ -785,10 +753,12 @@ void launch_score_roots(const MapView& map, const GridView& grid, const ScanView
 
 void launch_score_cube8(const MapView& map, const GridView& grid, const ScanView& scan,
                         const bbs_node* nodes, const uint32_t* d_n, uint32_t n_max,
-                        uint32_t n_ptiles, int32_t* scores, cudaStream_t s) {
+                        uint32_t n_ptiles, int32_t* scores, const RotCache* cache,
+                        cudaStream_t s) {
   const uint64_t items = static_cast<uint64_t>((n_max + 7) / 8) * n_ptiles;
   const unsigned g = static_cast<unsigned>(std::min<uint64_t>(std::max<uint64_t>(items, 1), 148ull * 4 * 8));
-  score_cube8_kernel<<<g, 256, 0, s>>>(map, grid, scan, nodes, d_n, n_ptiles, scores);
+  score_cube8_kernel<<<g, 256, 0, s>>>(map, grid, scan, nodes, d_n, n_ptiles, scores,
+                                       cache ? *cache : RotCache{}, cache ? 1 : 0);
   BBS_CUDA(cudaGetLastError());
 }
 

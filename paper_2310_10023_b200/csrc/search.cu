@@ -22,6 +22,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <vector>
@@ -53,6 +54,7 @@ struct EpochState {
   uint32_t pass;           // frontier passes executed while active
   uint32_t q_peak;
   uint32_t pad;
+  unsigned long long level_evals[kMaxLevels];  // flush evaluations per level
 };
 
 struct Queue {
@@ -325,11 +327,20 @@ __global__ void __launch_bounds__(kST) survivors_kernel(EpochState* st, int stra
                                                         bbs_node* __restrict__ s_node) {
   using ScanI = cub::BlockScan<int, kST>;
   __shared__ typename ScanI::TempStorage tmp;
+  __shared__ unsigned int s_lv[kMaxLevels];
   const uint32_t n = st->n_children;
   if (n == 0) return;
   const int32_t B = st->flush_best;
   const unsigned long long seq0 = st->seq;
   uint32_t carry = 0;
+  // evaluations per level (runs of 8 share a level)
+  if (threadIdx.x < kMaxLevels) s_lv[threadIdx.x] = 0;
+  __syncthreads();
+  for (uint32_t r = threadIdx.x; r < n / 8; r += blockDim.x)
+    atomicAdd(&s_lv[pending[8ull * r].level & (kMaxLevels - 1)], 8u);
+  __syncthreads();
+  if (threadIdx.x < kMaxLevels && s_lv[threadIdx.x])
+    st->level_evals[threadIdx.x] += s_lv[threadIdx.x];
   for (uint32_t base = 0; base < n; base += kST * kSIPT) {
     int keep[kSIPT];
     int cnt = 0;
@@ -554,7 +565,9 @@ struct Workspace {
   Buf<bbs_node> n0, qn0, qn1, pending, s_node, s_node2;
   Buf<uint32_t> perm0, perm1, exp_parent, exp_off;
   Buf<int32_t> pscores, trace, hist_n;
-  Buf<int4> hist_ent;
+  Buf<int4> hist_ent, cache_info, cache_pool, cache_builds;
+  Buf<uint32_t> cache_u32, cache_amb;
+  Buf<int32_t> cache_builds_w;
   Buf<uint32_t> hist_amb;
   Buf<EpochState> st;
   EpochState* h_st = nullptr;
@@ -578,6 +591,12 @@ struct Workspace {
     nsel.release();
     temp.release();
     hist_ent.release();
+    cache_info.release();
+    cache_pool.release();
+    cache_builds.release();
+    cache_u32.release();
+    cache_amb.release();
+    cache_builds_w.release();
     st.release();
     if (h_st) cudaFreeHost(h_st);
     if (h_small) cudaFreeHost(h_small);
@@ -847,6 +866,47 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
   const uint64_t trace_cap = cfg.collect_trace ? std::max<uint64_t>(out->trace_capacity, 1) : 0;
   int32_t* d_trace = W.trace.get(std::max<uint64_t>(trace_cap, 1), s);
   const uint32_t ptiles = choose_ptiles((pend_cap + 7) / 8, static_cast<uint32_t>(K));
+  // per-search (level, rotation) histogram cache for the flushes (epoch_cache.cu)
+  static const bool cache_on = [] {
+    const char* v = std::getenv("BBS_ROT_CACHE");  // "0" disables (A/B timing)
+    return !(v && v[0] == '0');
+  }();
+  RotCache cache{};
+  if (cache_on) {
+    uint64_t slots = 0;
+    const double M = std::max({std::fabs(static_cast<double>(x0)), std::fabs(static_cast<double>(x1)),
+                               std::fabs(static_cast<double>(y0)), std::fabs(static_cast<double>(y1)),
+                               std::fabs(static_cast<double>(z0)), std::fabs(static_cast<double>(z1))});
+    for (int l = 0; l < kMaxLevels; ++l) {
+      cache.base[l] = 0xFFFFFFFFu;
+      cache.tmax[l] = 0.0;
+    }
+    for (int l = 0; l < L; ++l) {
+      const uint64_t n_rot = static_cast<uint64_t>(grid.axis(0, l).index_count()) *
+                             grid.axis(1, l).index_count() * grid.axis(2, l).index_count();
+      // nodes at level l have |index| <= (M + 1) * 2^(L - l) (children 2c + j)
+      cache.tmax[l] = (M + 1.0) * std::ldexp(1.0, L - l) + 2.0;
+      if (n_rot <= (1ull << 20) && slots + n_rot <= (1ull << 23) && cache.tmax[l] < 0x1p28) {
+        cache.base[l] = static_cast<uint32_t>(slots);
+        slots += n_rot;
+      }
+    }
+    if (slots > 0) {
+      cache.enabled = 1;
+      cache.pool_cap = 64ull << 20;  // entries (16 B each)
+      cache.amb_cap = 8ull << 20;
+      cache.info = W.cache_info.get(slots, s);
+      cache.amb_off = W.cache_u32.get(slots + 4, s);
+      cache.ctl = cache.amb_off + slots;
+      cache.pool = W.cache_pool.get(cache.pool_cap, s);
+      cache.amb_pool = W.cache_amb.get(cache.amb_cap, s);
+      const uint64_t mr = (pend_cap + 7) / 8;
+      cache.builds = W.cache_builds.get(mr, s);
+      cache.builds_w = W.cache_builds_w.get(mr, s);
+      BBS_CUDA(cudaMemsetAsync(cache.info, 0xFF, slots * sizeof(int4), s));  // all kCacheEmpty
+      BBS_CUDA(cudaMemsetAsync(cache.ctl, 0, 4 * sizeof(uint32_t), s));
+    }
+  }
 
   std::vector<cudaEvent_t> pass_ev;  // after each frontier pass
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> score_ev;
@@ -891,13 +951,13 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
       pass_ev.push_back(pe);
       branch_kernel<<<grid1(pend_cap), 256, 0, s>>>(d_st, q, gv, exp_parent, exp_off, pending);
       BBS_CUDA(cudaGetLastError());
-      if (ptiles > 1) BBS_CUDA(cudaMemsetAsync(pscores, 0, pend_cap * sizeof(int32_t), s));
+      BBS_CUDA(cudaMemsetAsync(pscores, 0, pend_cap * sizeof(int32_t), s));
       cudaEvent_t s0 = W.next_event(), s1 = W.next_event();
       BBS_CUDA(cudaEventRecord(s0, s));
-      launch_score_cube8(m->view, gv, sv, pending,
+      launch_epoch_score(m->view, gv, sv, pending,
                          reinterpret_cast<const uint32_t*>(reinterpret_cast<char*>(d_st) +
                                                            offsetof(EpochState, n_children)),
-                         static_cast<uint32_t>(pend_cap), ptiles, pscores, s);
+                         static_cast<uint32_t>(pend_cap), ptiles, pscores, cache, s);
       BBS_CUDA(cudaEventRecord(s1, s));
       score_ev.emplace_back(s0, s1);
       survivors_kernel<<<1, kST, 0, s>>>(d_st, strategy, pending, pscores, s_key, s_node);
@@ -964,6 +1024,8 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
   out->h2d_bytes = h2d;
   out->d2h_bytes = d2h;
   out->kernel_launches = launches;
+  for (int l = 0; l < kMaxLevels; ++l) out->evals_per_level[l] = hs.level_evals[l];
+  out->evals_per_level[L] += n_own;  // the root batch
   int32_t best = hs.best;
   bbs_node best_node = hs.best_node;
   int matched = hs.matched;

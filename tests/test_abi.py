@@ -63,7 +63,8 @@ def test_struct_sizes(B):
 
 
 def test_abi_version(B):
-    assert B.lib.bbs_abi_version() == 1
+    from paper_2310_10023_b200 import _lib
+    assert B.lib.bbs_abi_version() == _lib.ABI_VERSION == 2
 
 
 def test_search_config_defaults_match_reference(B):
