@@ -58,8 +58,13 @@ __global__ void cache_claim_kernel(RotCache c, GridView G, const bbs_node* __res
     const int4 a = __ldg(reinterpret_cast<const int4*>(pending) + 16ull * r);
     const int4 b = __ldg(reinterpret_cast<const int4*>(pending) + 16ull * r + 1);
     uint32_t slot;
-    if (!run_slot(c, G, a, b, &slot)) continue;
-    if (c.info[slot].x != kCacheEmpty) continue;
+    if (!run_slot(c, G, a, b, &slot)) {
+      atomicAdd(&c.ctl[3], 1u);  // uncached level: the cube kernel scores this run
+      continue;
+    }
+    const int32_t state = c.info[slot].x;
+    if (state == kCacheNone) atomicAdd(&c.ctl[3], 1u);
+    if (state != kCacheEmpty) continue;
     if (atomicCAS(&c.info[slot].x, kCacheEmpty, kCacheBuilding) == kCacheEmpty) {
       const uint32_t i = atomicAdd(&c.ctl[2], 1u);
       c.builds[i] = make_int4(static_cast<int32_t>(slot), b.z, a.w, b.x);  // slot, level, ir, ip
@@ -95,35 +100,44 @@ __global__ void __launch_bounds__(512) cache_build_kernel(RotCache c, MapView ma
       s_over = 0;
     }
     __syncthreads();
-    for (uint32_t p = threadIdx.x; p < scan.k; p += blockDim.x) {
-      const double px = scan.x[p], py = scan.y[p], pz = scan.z[p];
-      int32_t fx, fy, fz;
-      bool ok = fast_floor(rot_row(R[0], R[1], R[2], px, py, pz), L.inv_cell, tmax, &fx) &
-                fast_floor(rot_row(R[3], R[4], R[5], px, py, pz), L.inv_cell, tmax, &fy) &
-                fast_floor(rot_row(R[6], R[7], R[8], px, py, pz), L.inv_cell, tmax, &fz);
-      ok = ok && fx > -(1 << 20) && fx < (1 << 20) && fy > -(1 << 20) && fy < (1 << 20) &&
-           fz > -(1 << 20) && fz < (1 << 20);
-      if (!ok) {
-        const int a = atomicAdd(&s_namb, 1);
-        if (a < kCacheAmbCap) s_amb[a] = p;
-        continue;
-      }
-      if (s_distinct >= kCacheHashCap) {
-        s_over = 1;  // too many distinct offsets: raw per-point entries below
-        continue;
-      }
-      const unsigned long long key = (static_cast<unsigned long long>(fx + (1 << 20)) << 42) |
-                                     (static_cast<unsigned long long>(fy + (1 << 20)) << 21) |
-                                     static_cast<unsigned long long>(fz + (1 << 20));
-      uint32_t h = cache_hash(key);
-      for (;;) {
-        const unsigned long long prev = atomicCAS(&s_key[h], kEmptyKey, key);
-        if (prev == kEmptyKey) atomicAdd(&s_distinct, 1);
-        if (prev == kEmptyKey || prev == key) {
-          atomicAdd(&s_cnt[h], 1);
-          break;
+    // all lanes stay in the loop together (warp-aggregated inserts below)
+    for (uint32_t p0 = 0; p0 < scan.k; p0 += blockDim.x) {
+      const uint32_t p = p0 + threadIdx.x;
+      const bool live = p < scan.k;
+      bool ok = false;
+      int32_t fx = 0, fy = 0, fz = 0;
+      if (live) {
+        const double px = scan.x[p], py = scan.y[p], pz = scan.z[p];
+        ok = fast_floor(rot_row(R[0], R[1], R[2], px, py, pz), L.inv_cell, tmax, &fx) &
+             fast_floor(rot_row(R[3], R[4], R[5], px, py, pz), L.inv_cell, tmax, &fy) &
+             fast_floor(rot_row(R[6], R[7], R[8], px, py, pz), L.inv_cell, tmax, &fz);
+        ok = ok && fx > -(1 << 20) && fx < (1 << 20) && fy > -(1 << 20) && fy < (1 << 20) &&
+             fz > -(1 << 20) && fz < (1 << 20);
+        if (!ok) {
+          const int a = atomicAdd(&s_namb, 1);
+          if (a < kCacheAmbCap) s_amb[a] = p;
         }
-        h = (h + 1) & (kCacheHashSlots - 1);
+      }
+      const bool ins = live && ok && s_distinct < kCacheHashCap;
+      if (live && ok && !ins) s_over = 1;  // too many distinct offsets: raw entries below
+      const unsigned long long key = ins ? (static_cast<unsigned long long>(fx + (1 << 20)) << 42) |
+                                               (static_cast<unsigned long long>(fy + (1 << 20)) << 21) |
+                                               static_cast<unsigned long long>(fz + (1 << 20))
+                                         : kEmptyKey;
+      // neighbouring scan points often share a voxel: one insert per distinct key per warp
+      const unsigned same = __match_any_sync(0xffffffffu, key);
+      if (ins && (__ffs(same) - 1) == (threadIdx.x & 31)) {
+        const int mult = __popc(same);
+        uint32_t h = cache_hash(key);
+        for (;;) {
+          const unsigned long long prev = atomicCAS(&s_key[h], kEmptyKey, key);
+          if (prev == kEmptyKey) atomicAdd(&s_distinct, 1);
+          if (prev == kEmptyKey || prev == key) {
+            atomicAdd(&s_cnt[h], mult);
+            break;
+          }
+          h = (h + 1) & (kCacheHashSlots - 1);
+        }
       }
     }
     __syncthreads();
@@ -178,6 +192,7 @@ __global__ void __launch_bounds__(512) cache_build_kernel(RotCache c, MapView ma
       // publish: entries first, then the state (readers run in later kernels)
       c.info[slot] = fits ? make_int4(kCacheReady, static_cast<int32_t>(off), static_cast<int32_t>(n_ent), namb)
                           : make_int4(kCacheNone, 0, 0, 0);
+      if (!fits) atomicAdd(&c.ctl[3], 1u);  // its runs fall back to the cube kernel
     }
     __syncthreads();
   }
@@ -268,7 +283,7 @@ void launch_epoch_score(const MapView& map, const GridView& grid, const ScanView
     attr_done = true;
   }
   const uint32_t max_runs = (n_max + 7) / 8;
-  BBS_CUDA(cudaMemsetAsync(cache.ctl + 2, 0, sizeof(uint32_t), s));  // build count
+  BBS_CUDA(cudaMemsetAsync(cache.ctl + 2, 0, 2 * sizeof(uint32_t), s));  // builds, fallback runs
   cache_claim_kernel<<<(max_runs + 255) / 256, 256, 0, s>>>(cache, grid, pending, d_n);
   BBS_CUDA(cudaGetLastError());
   cache_build_kernel<<<std::min<uint32_t>(std::max<uint32_t>(max_runs, 1), 148 * 2), 512, build_smem, s>>>(

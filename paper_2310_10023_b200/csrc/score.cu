@@ -319,6 +319,7 @@ __global__ void __launch_bounds__(256, 4) score_cube8_kernel(MapView map, GridVi
   const uint32_t k = scan.k;
   const uint32_t tile = (k + n_ptiles - 1) / n_ptiles;
   const int lane = threadIdx.x & 31;
+  if (use_cache && cache.ctl[3] == 0) return;  // every run was scored from the cache
   for (uint64_t item = blockIdx.x; item < n_items; item += gridDim.x) {
     const uint32_t run = static_cast<uint32_t>(item / n_ptiles);
     const uint32_t pt = static_cast<uint32_t>(item % n_ptiles);
@@ -470,35 +471,43 @@ __global__ void __launch_bounds__(512) root_hist_kernel(GridView grid, ScanView 
     const uint32_t ir = rot / (bp.np * bp.nw), ip = (rot / bp.nw) % bp.np, iw = rot % bp.nw;
     double R[9];
     rotation_of(grid, bp.level, static_cast<int>(ir), static_cast<int>(ip), static_cast<int>(iw), R);
-    for (uint32_t p = threadIdx.x; p < scan.k; p += blockDim.x) {
-      const double px = scan.x[p], py = scan.y[p], pz = scan.z[p];
-      int32_t fx, fy, fz;
-      bool ok = fast_floor(rot_row(R[0], R[1], R[2], px, py, pz), L.inv_cell, bp.tmax, &fx) &
-                fast_floor(rot_row(R[3], R[4], R[5], px, py, pz), L.inv_cell, bp.tmax, &fy) &
-                fast_floor(rot_row(R[6], R[7], R[8], px, py, pz), L.inv_cell, bp.tmax, &fz);
-      ok = ok && fx > -(1 << 20) && fx < (1 << 20) && fy > -(1 << 20) && fy < (1 << 20) &&
-           fz > -(1 << 20) && fz < (1 << 20);
-      if (!ok) {
-        const int a = atomicAdd(&s_namb, 1);
-        if (a < kAmbCap) h.amb[static_cast<uint64_t>(slot) * kAmbCap + a] = p;
-        continue;
-      }
-      if (s_distinct >= kHistCap) {  // table saturated: this rotation falls back
-        s_skip = 1;
-        continue;
-      }
-      const unsigned long long key = (static_cast<unsigned long long>(fx + (1 << 20)) << 42) |
-                                     (static_cast<unsigned long long>(fy + (1 << 20)) << 21) |
-                                     static_cast<unsigned long long>(fz + (1 << 20));
-      uint32_t hs = hist_slot(key);
-      for (;;) {
-        const unsigned long long prev = atomicCAS(&s_key[hs], kSlotEmpty, key);
-        if (prev == kSlotEmpty) atomicAdd(&s_distinct, 1);
-        if (prev == kSlotEmpty || prev == key) {
-          atomicAdd(&s_cnt[hs], 1);
-          break;
+    for (uint32_t p0 = 0; p0 < scan.k; p0 += blockDim.x) {
+      const uint32_t p = p0 + threadIdx.x;
+      const bool live = p < scan.k;
+      bool ok = false;
+      int32_t fx = 0, fy = 0, fz = 0;
+      if (live) {
+        const double px = scan.x[p], py = scan.y[p], pz = scan.z[p];
+        ok = fast_floor(rot_row(R[0], R[1], R[2], px, py, pz), L.inv_cell, bp.tmax, &fx) &
+             fast_floor(rot_row(R[3], R[4], R[5], px, py, pz), L.inv_cell, bp.tmax, &fy) &
+             fast_floor(rot_row(R[6], R[7], R[8], px, py, pz), L.inv_cell, bp.tmax, &fz);
+        ok = ok && fx > -(1 << 20) && fx < (1 << 20) && fy > -(1 << 20) && fy < (1 << 20) &&
+             fz > -(1 << 20) && fz < (1 << 20);
+        if (!ok) {
+          const int a = atomicAdd(&s_namb, 1);
+          if (a < kAmbCap) h.amb[static_cast<uint64_t>(slot) * kAmbCap + a] = p;
         }
-        hs = (hs + 1) & (kHistSlots - 1);
+      }
+      const bool ins = live && ok && s_distinct < kHistCap;
+      if (live && ok && !ins) s_skip = 1;  // table saturated: this rotation falls back
+      const unsigned long long key = ins ? (static_cast<unsigned long long>(fx + (1 << 20)) << 42) |
+                                               (static_cast<unsigned long long>(fy + (1 << 20)) << 21) |
+                                               static_cast<unsigned long long>(fz + (1 << 20))
+                                         : kSlotEmpty;
+      // neighbouring scan points often share a voxel: one insert per distinct key per warp
+      const unsigned same = __match_any_sync(0xffffffffu, key);
+      if (ins && (__ffs(same) - 1) == (threadIdx.x & 31)) {
+        const int mult = __popc(same);
+        uint32_t hs = hist_slot(key);
+        for (;;) {
+          const unsigned long long prev = atomicCAS(&s_key[hs], kSlotEmpty, key);
+          if (prev == kSlotEmpty) atomicAdd(&s_distinct, 1);
+          if (prev == kSlotEmpty || prev == key) {
+            atomicAdd(&s_cnt[hs], mult);
+            break;
+          }
+          hs = (hs + 1) & (kHistSlots - 1);
+        }
       }
     }
     __syncthreads();

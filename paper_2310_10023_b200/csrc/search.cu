@@ -872,7 +872,9 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
     return !(v && v[0] == '0');
   }();
   RotCache cache{};
-  if (cache_on) {
+  // a histogram build costs about one direct run; small scans (C1: K = 2000)
+  // rarely amortize it, large ones (C2/C3) reuse rotations across flushes
+  if (cache_on && K >= 4096) {
     uint64_t slots = 0;
     const double M = std::max({std::fabs(static_cast<double>(x0)), std::fabs(static_cast<double>(x1)),
                                std::fabs(static_cast<double>(y0)), std::fabs(static_cast<double>(y1)),
