@@ -90,7 +90,7 @@ __device__ __forceinline__ uint32_t n_children_of(const GridView& G, const bbs_n
   return 8u * static_cast<uint32_t>(c[0]) * static_cast<uint32_t>(c[1]) * static_cast<uint32_t>(c[2]);
 }
 
-constexpr int kFT = 1024;
+constexpr int kFT = 256;
 constexpr int kFIPT = 4;
 constexpr int kFChunk = kFT * kFIPT;
 
@@ -910,8 +910,56 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
     }
   }
 
-  std::vector<cudaEvent_t> pass_ev;  // after each frontier pass
-  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> score_ev;
+  // per-epoch-slot events of one batch; timings are harvested after each batch
+  std::vector<cudaEvent_t> ev_pass(E), ev_s0(E), ev_s1(E);
+  for (int e = 0; e < E; ++e) {
+    ev_pass[e] = W.next_event();
+    ev_s0[e] = W.next_event();
+    ev_s1[e] = W.next_event();
+  }
+  std::vector<float> pass_ms;  // loop start -> end of each frontier pass
+  double esm = 0.0;            // device time in the flush score kernels
+  const uint32_t* d_nchild = reinterpret_cast<const uint32_t*>(reinterpret_cast<char*>(d_st) +
+                                                               offsetof(EpochState, n_children));
+  bool capturing = false;
+  auto record = [&](cudaEvent_t ev) {
+    // External: a real record node when captured into the batch graph
+    BBS_CUDA(capturing ? cudaEventRecordWithFlags(ev, s, cudaEventRecordExternal)
+                       : cudaEventRecord(ev, s));
+  };
+  // one flush epoch (frontier -> branch -> score -> survivors -> sort -> merge)
+  auto enqueue_epoch = [&](int e) {
+    frontier_kernel<<<1, kFT, 0, s>>>(d_st, q, gv, cfg.batch_size, exp_parent, exp_off, d_trace,
+                                      trace_cap, strategy);
+    BBS_CUDA(cudaGetLastError());
+    record(ev_pass[e]);
+    branch_kernel<<<grid1(pend_cap), 256, 0, s>>>(d_st, q, gv, exp_parent, exp_off, pending);
+    BBS_CUDA(cudaGetLastError());
+    BBS_CUDA(cudaMemsetAsync(pscores, 0, pend_cap * sizeof(int32_t), s));
+    record(ev_s0[e]);
+    launch_epoch_score(m->view, gv, sv, pending, d_nchild, static_cast<uint32_t>(pend_cap), ptiles,
+                       pscores, cache, s);
+    record(ev_s1[e]);
+    survivors_kernel<<<1, kST, 0, s>>>(d_st, strategy, pending, pscores, s_key, s_node);
+    BBS_CUDA(cudaGetLastError());
+    rank_sort_kernel<<<grid1(pend_cap, kRT), kRT, 0, s>>>(d_st, s_key, s_node, s_key2, s_node2);
+    BBS_CUDA(cudaGetLastError());
+    merge_kernel<<<grid1(qcap), 256, 0, s>>>(d_st, q, s_key2, s_node2);
+    BBS_CUDA(cudaGetLastError());
+    finalize_kernel<<<1, 1, 0, s>>>(d_st);
+    BBS_CUDA(cudaGetLastError());
+    launches += 7;  // frontier, branch, score, survivors, rank_sort, merge, finalize
+  };
+  // E epochs as one CUDA graph (all sizes live in EpochState, so the graph is
+  // valid until the queue buffers are re-allocated)
+  cudaGraphExec_t batch_exec = nullptr;
+  uint64_t batch_qcap = 0;
+  struct ExecGuard {
+    cudaGraphExec_t* e;
+    ~ExecGuard() {
+      if (*e) cudaGraphExecDestroy(*e);
+    }
+  } exec_guard{&batch_exec};
   EpochState hs = h0;
   bool self_active = h0.active != 0;
   bool others_active = false;
@@ -944,37 +992,35 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
       qcap = std::min({W.qk0.cap, W.qk1.cap, W.qn0.cap, W.qn1.cap});
     }
     const int n_ep = self_active ? E : 1;
-    for (int e = 0; e < n_ep; ++e) {
-      frontier_kernel<<<1, kFT, 0, s>>>(d_st, q, gv, cfg.batch_size, exp_parent, exp_off, d_trace,
-                                        trace_cap, strategy);
-      BBS_CUDA(cudaGetLastError());
-      cudaEvent_t pe = W.next_event();
-      BBS_CUDA(cudaEventRecord(pe, s));
-      pass_ev.push_back(pe);
-      branch_kernel<<<grid1(pend_cap), 256, 0, s>>>(d_st, q, gv, exp_parent, exp_off, pending);
-      BBS_CUDA(cudaGetLastError());
-      BBS_CUDA(cudaMemsetAsync(pscores, 0, pend_cap * sizeof(int32_t), s));
-      cudaEvent_t s0 = W.next_event(), s1 = W.next_event();
-      BBS_CUDA(cudaEventRecord(s0, s));
-      launch_epoch_score(m->view, gv, sv, pending,
-                         reinterpret_cast<const uint32_t*>(reinterpret_cast<char*>(d_st) +
-                                                           offsetof(EpochState, n_children)),
-                         static_cast<uint32_t>(pend_cap), ptiles, pscores, cache, s);
-      BBS_CUDA(cudaEventRecord(s1, s));
-      score_ev.emplace_back(s0, s1);
-      survivors_kernel<<<1, kST, 0, s>>>(d_st, strategy, pending, pscores, s_key, s_node);
-      BBS_CUDA(cudaGetLastError());
-      rank_sort_kernel<<<grid1(pend_cap, kRT), kRT, 0, s>>>(d_st, s_key, s_node, s_key2, s_node2);
-      BBS_CUDA(cudaGetLastError());
-      merge_kernel<<<grid1(qcap), 256, 0, s>>>(d_st, q, s_key2, s_node2);
-      BBS_CUDA(cudaGetLastError());
-      finalize_kernel<<<1, 1, 0, s>>>(d_st);
-      BBS_CUDA(cudaGetLastError());
-      launches += 7;  // frontier, branch, score, survivors, rank_sort, merge, finalize
+    // graphs pay off for long searches (capture + instantiate ~0.2 ms)
+    if (n_ep == E && E > 1 && pass_ms.size() >= 3u * static_cast<size_t>(E)) {
+      if (!batch_exec || batch_qcap != qcap) {
+        if (batch_exec) BBS_CUDA(cudaGraphExecDestroy(batch_exec));
+        batch_exec = nullptr;
+        cudaGraph_t graph;
+        BBS_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeRelaxed));
+        capturing = true;
+        const uint64_t l0 = launches;
+        for (int e = 0; e < E; ++e) enqueue_epoch(e);
+        launches = l0;
+        capturing = false;
+        BBS_CUDA(cudaStreamEndCapture(s, &graph));
+        BBS_CUDA(cudaGraphInstantiate(&batch_exec, graph, 0));
+        BBS_CUDA(cudaGraphDestroy(graph));
+        batch_qcap = qcap;
+      }
+      BBS_CUDA(cudaGraphLaunch(batch_exec, s));
+      launches += 7ull * E;
+    } else {
+      for (int e = 0; e < n_ep; ++e) enqueue_epoch(e);
     }
     BBS_CUDA(cudaMemcpyAsync(W.h_st, d_st, sizeof(EpochState), cudaMemcpyDeviceToHost, s));
     d2h += sizeof(EpochState);
     BBS_CUDA(cudaStreamSynchronize(s));
+    for (int e = 0; e < n_ep; ++e) {
+      pass_ms.push_back(elapsed(ev_loop, ev_pass[e]));
+      esm += elapsed(ev_s0[e], ev_s1[e]);
+    }
     hs = *W.h_st;
     self_active = hs.active != 0;
     if (shard && shard->allreduce_max)
@@ -998,8 +1044,8 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
   out->stats.batches_flushed = hs.batches_flushed;
   out->stats.initial_nodes_ms = elapsed(ev_start, ev_loop);
   const float loop_ms = elapsed(ev_loop, ev_end);
-  if (hs.matched && hs.last_best_epoch >= 0 && hs.last_best_epoch < static_cast<int>(pass_ev.size())) {
-    const float fb = elapsed(ev_loop, pass_ev[static_cast<size_t>(hs.last_best_epoch)]);
+  if (hs.matched && hs.last_best_epoch >= 0 && hs.last_best_epoch < static_cast<int>(pass_ms.size())) {
+    const float fb = pass_ms[static_cast<size_t>(hs.last_best_epoch)];
     out->stats.find_best_score_ms = fb;
     out->stats.pop_remaining_queue_ms = loop_ms - fb;
   } else {
@@ -1008,8 +1054,6 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
   }
   out->device_ms = elapsed(ev_start, ev_end);
   out->root_score_ms = elapsed(ev_roots0, ev_roots1);
-  double esm = 0;
-  for (auto& pr : score_ev) esm += elapsed(pr.first, pr.second);
   out->epoch_score_ms = esm;
   out->epochs = hs.epochs;
   out->root_nodes = n_own;
