@@ -198,6 +198,31 @@ __global__ void __launch_bounds__(512) cache_build_kernel(RotCache c, MapView ma
   }
 }
 
+// Ambiguous points of one run (exact divide path), kept out of line so the
+// probe loop's register budget stays small.
+__device__ __forceinline__ void probe_ambiguous(const RotCache& c, const LevelView& L, const GridView& G,
+                                             const ScanView& scan, uint32_t slot, int n_amb, int l,
+                                             int ir, int ip, int iw, int32_t bx, int32_t by,
+                                             int32_t bz, int lane, int acc[8]) {
+  double R[9];
+  rotation_of(G, l, ir, ip, iw, R);
+  const uint32_t* __restrict__ amb = c.amb_pool + c.amb_off[slot];
+  for (int q = lane; q < n_amb; q += 32) {
+    const uint32_t p = amb[q];
+    const double px = scan.x[p], py = scan.y[p], pz = scan.z[p];
+    const double rx = rot_row(R[0], R[1], R[2], px, py, pz);
+    const double ry = rot_row(R[3], R[4], R[5], px, py, pz);
+    const double rz = rot_row(R[6], R[7], R[8], px, py, pz);
+#pragma unroll
+    for (int t = 0; t < 8; ++t)
+      acc[t] += exact_hit(L, rx, ry, rz, bx + (t >> 2), by + ((t >> 1) & 1), bz + (t & 1));
+  }
+}
+
+// Warp items are (run, 256-entry chunk) pairs, grid-strided.  The 32 lanes
+// first fetch the headers (run node, cache info) of 32 items in parallel and
+// the warp then walks only the items that have entries, so empty chunks and
+// uncached runs cost no serial load latency.
 __global__ void __launch_bounds__(256) cache_probe_kernel(RotCache c, MapView map, GridView G,
                                                           ScanView scan,
                                                           const bbs_node* __restrict__ pending,
@@ -208,60 +233,83 @@ __global__ void __launch_bounds__(256) cache_probe_kernel(RotCache c, MapView ma
   const uint64_t n_items = static_cast<uint64_t>(n_runs) * chunks_per_run;
   const int lane = threadIdx.x & 31;
   const uint64_t n_warps = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
-  for (uint64_t item = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-       item < n_items; item += n_warps) {
-    const uint32_t run = static_cast<uint32_t>(item / chunks_per_run);
-    const uint32_t chunk = static_cast<uint32_t>(item % chunks_per_run);
-    const int4 a = __ldg(reinterpret_cast<const int4*>(pending) + 16ull * run);
-    const int4 b = __ldg(reinterpret_cast<const int4*>(pending) + 16ull * run + 1);
-    uint32_t slot;
-    if (!run_slot(c, G, a, b, &slot)) continue;
-    const int4 inf = c.info[slot];
-    if (inf.x != kCacheReady) continue;
-    const uint32_t e0 = chunk * kProbeChunk;
-    const uint32_t n_ent = static_cast<uint32_t>(inf.z);
-    const bool amb_here = chunk == 0 && inf.w > 0;
-    if (e0 >= n_ent && !amb_here) continue;
-    const int32_t bx = a.x, by = a.y, bz = a.z;
-    const LevelView& L = map.level[b.z];
-    const bool bitmap = L.layout == BBS_LAYOUT_BITMAP;
-    const uint32_t ox = static_cast<uint32_t>(bx) - static_cast<uint32_t>(L.box_min[0]);
-    const uint32_t oy = static_cast<uint32_t>(by) - static_cast<uint32_t>(L.box_min[1]);
-    const uint32_t oz = static_cast<uint32_t>(bz) - static_cast<uint32_t>(L.box_min[2]);
-    int acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    const uint32_t e1 = min(n_ent, e0 + kProbeChunk);
-    const int4* __restrict__ ent = c.pool + static_cast<uint32_t>(inf.y);
-    for (uint32_t e = e0 + lane; e < e1; e += 32) {
-      const int4 f = __ldg(ent + e);
-      if (bitmap) {
-        cube_probe(L, static_cast<uint32_t>(f.x) + ox, static_cast<uint32_t>(f.y) + oy,
-                   static_cast<uint32_t>(f.z) + oz, f.w, acc);
+  const uint64_t gw = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  for (uint64_t k0 = 0; gw + k0 * n_warps < n_items; k0 += 32) {
+    const uint64_t item = gw + (k0 + lane) * n_warps;
+    int4 a = make_int4(0, 0, 0, 0), b = make_int4(0, 0, 0, 0), inf = make_int4(0, 0, 0, 0);
+    uint32_t slot = 0, chunk = 0, run = 0;
+    bool has = false;
+    if (item < n_items) {
+      run = static_cast<uint32_t>(item / chunks_per_run);
+      chunk = static_cast<uint32_t>(item % chunks_per_run);
+      a = __ldg(reinterpret_cast<const int4*>(pending) + 16ull * run);
+      b = __ldg(reinterpret_cast<const int4*>(pending) + 16ull * run + 1);
+      if (run_slot(c, G, a, b, &slot)) {
+        inf = c.info[slot];
+        has = inf.x == kCacheReady &&
+              (chunk * kProbeChunk < static_cast<uint32_t>(inf.z) || (chunk == 0 && inf.w > 0));
+      }
+    }
+    unsigned todo = __ballot_sync(0xffffffffu, has);
+    while (todo) {
+      const int src = __ffs(todo) - 1;
+      todo &= todo - 1;
+      const uint32_t r = __shfl_sync(0xffffffffu, run, src);
+      const uint32_t ch = __shfl_sync(0xffffffffu, chunk, src);
+      const int32_t bx = __shfl_sync(0xffffffffu, a.x, src);
+      const int32_t by = __shfl_sync(0xffffffffu, a.y, src);
+      const int32_t bz = __shfl_sync(0xffffffffu, a.z, src);
+      const int l = __shfl_sync(0xffffffffu, b.z, src);
+      const uint32_t off = static_cast<uint32_t>(__shfl_sync(0xffffffffu, inf.y, src));
+      const uint32_t n_ent = static_cast<uint32_t>(__shfl_sync(0xffffffffu, inf.z, src));
+      const int n_amb = ch == 0 ? __shfl_sync(0xffffffffu, inf.w, src) : 0;
+      const LevelView& L = map.level[l];
+      const uint32_t ox = static_cast<uint32_t>(bx) - static_cast<uint32_t>(L.box_min[0]);
+      const uint32_t oy = static_cast<uint32_t>(by) - static_cast<uint32_t>(L.box_min[1]);
+      const uint32_t oz = static_cast<uint32_t>(bz) - static_cast<uint32_t>(L.box_min[2]);
+      int acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+      const uint32_t e0 = ch * kProbeChunk;
+      const uint32_t e1 = min(n_ent, e0 + kProbeChunk);
+      const int4* __restrict__ ent = c.pool + off;
+      if (L.layout == BBS_LAYOUT_BITMAP) {
+        // two entries per lane per step: 8-16 independent column loads in flight
+        uint32_t e = e0 + lane;
+        for (; e + 32 < e1; e += 64) {
+          const int4 f0 = __ldg(ent + e);
+          const int4 f1 = __ldg(ent + e + 32);
+          cube_probe(L, static_cast<uint32_t>(f0.x) + ox, static_cast<uint32_t>(f0.y) + oy,
+                     static_cast<uint32_t>(f0.z) + oz, f0.w, acc);
+          cube_probe(L, static_cast<uint32_t>(f1.x) + ox, static_cast<uint32_t>(f1.y) + oy,
+                     static_cast<uint32_t>(f1.z) + oz, f1.w, acc);
+        }
+        if (e < e1) {
+          const int4 f = __ldg(ent + e);
+          cube_probe(L, static_cast<uint32_t>(f.x) + ox, static_cast<uint32_t>(f.y) + oy,
+                     static_cast<uint32_t>(f.z) + oz, f.w, acc);
+        }
       } else {
+        for (uint32_t e = e0 + lane; e < e1; e += 32) {
+          const int4 f = __ldg(ent + e);
 #pragma unroll
-        for (int t = 0; t < 8; ++t)
-          acc[t] += level_contains(L, f.x + bx + (t >> 2), f.y + by + ((t >> 1) & 1), f.z + bz + (t & 1))
-                        ? f.w : 0;
+          for (int t = 0; t < 8; ++t)
+            acc[t] += level_contains(L, f.x + bx + (t >> 2), f.y + by + ((t >> 1) & 1),
+                                     f.z + bz + (t & 1))
+                          ? f.w
+                          : 0;
+        }
       }
-    }
-    if (amb_here) {
-      double R[9];
-      rotation_of(G, b.z, a.w, b.x, b.y, R);
-      const uint32_t* __restrict__ amb = c.amb_pool + c.amb_off[slot];
-      for (int q = lane; q < inf.w; q += 32) {
-        const uint32_t p = amb[q];
-        const double px = scan.x[p], py = scan.y[p], pz = scan.z[p];
-        const double rx = rot_row(R[0], R[1], R[2], px, py, pz);
-        const double ry = rot_row(R[3], R[4], R[5], px, py, pz);
-        const double rz = rot_row(R[6], R[7], R[8], px, py, pz);
-#pragma unroll
-        for (int t = 0; t < 8; ++t)
-          acc[t] += exact_hit(L, rx, ry, rz, bx + (t >> 2), by + ((t >> 1) & 1), bz + (t & 1));
+      if (n_amb > 0) {
+        const uint32_t sl = __shfl_sync(0xffffffffu, slot, src);
+        const int ir = __shfl_sync(0xffffffffu, a.w, src);
+        const int ip = __shfl_sync(0xffffffffu, b.x, src);
+        const int iw = __shfl_sync(0xffffffffu, b.y, src);
+        probe_ambiguous(c, L, G, scan, sl, n_amb, l, ir, ip, iw, bx, by, bz, lane, acc);
       }
-    }
 #pragma unroll
-    for (int t = 0; t < 8; ++t) {
-      const int v = __reduce_add_sync(0xffffffffu, acc[t]);
-      if (lane == 0 && v) atomicAdd(&scores[8ull * run + t], v);
+      for (int t = 0; t < 8; ++t) {
+        const int v = __reduce_add_sync(0xffffffffu, acc[t]);
+        if (lane == 0 && v) atomicAdd(&scores[8ull * r + t], v);
+      }
     }
   }
 }

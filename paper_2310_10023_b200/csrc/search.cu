@@ -53,8 +53,10 @@ struct EpochState {
   int32_t flush_best;
   uint32_t pass;           // frontier passes executed while active
   uint32_t q_peak;
-  uint32_t pad;
+  uint32_t n_keep;         // queue remainder kept after the incumbent trim
   unsigned long long level_evals[kMaxLevels];  // flush evaluations per level
+  // kept ranges of the remainder: one per key segment (BFS: 1, DFS: level)
+  uint32_t seg_lo[kMaxLevels], seg_len[kMaxLevels], seg_pre[kMaxLevels + 1];
 };
 
 struct Queue {
@@ -320,7 +322,69 @@ constexpr int kSIPT = 4;
 
 // E4a: flush pruning (search.hpp:134-140): keep score >= B in pending order
 // and give them consecutive seq numbers.
-__global__ void __launch_bounds__(kST) survivors_kernel(EpochState* st, int strategy,
+__device__ __forceinline__ uint32_t lower_bound_u64(const unsigned long long* a, uint32_t n,
+                                                    unsigned long long v) {
+  uint32_t lo = 0, hi = n;
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (a[mid] < v)
+      lo = mid + 1;
+    else
+      hi = mid;
+  }
+  return lo;
+}
+
+// Incumbent trim (one warp).  B never decreases, so a queued entry with
+// score < B is pruned whenever it is popped (search.hpp:150-153) and never
+// branches or updates the incumbent: dropping it now and counting it as
+// pruned leaves Stats, trace and every later pop unchanged.  Within a key
+// segment (BFS: the whole key space; DFS: one level) entries are ordered by
+// descending score, so the dropped entries form a suffix of each segment.
+__device__ void trim_remainder(EpochState* st, const Queue& q, int strategy, int32_t B) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t n_cons = st->n_cons;
+  const uint32_t n_rem = st->q_len - n_cons;
+  const unsigned long long* qk = q.key[st->cur] + n_cons;
+  const int nseg = strategy == BBS_STRATEGY_BFS ? 1 : kMaxLevels;
+  uint32_t lo = 0, hi = 0;
+  if (lane < nseg) {
+    unsigned long long seg_base = 0, seg_end_key = ~0ull, cut_key;
+    const unsigned long long sb = kSMax - static_cast<unsigned long long>(B < 0 ? 0 : B) + 1;
+    if (strategy == BBS_STRATEGY_BFS) {
+      cut_key = sb << 44;  // keys below: score >= B
+      lo = 0;
+      hi = n_rem;
+    } else {
+      seg_base = static_cast<unsigned long long>(lane) << 60;
+      seg_end_key = lane + 1 < kMaxLevels ? static_cast<unsigned long long>(lane + 1) << 60 : ~0ull;
+      cut_key = seg_base | (sb << 40);
+      lo = lower_bound_u64(qk, n_rem, seg_base);
+      hi = lane + 1 < kMaxLevels ? lower_bound_u64(qk, n_rem, seg_end_key) : n_rem;
+    }
+    if (B > 0) hi = lo + lower_bound_u64(qk + lo, hi - lo, cut_key);
+  }
+  const uint32_t len = hi - lo;
+  uint32_t pre = len;  // inclusive scan over lanes
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint32_t v = __shfl_up_sync(0xffffffffu, pre, d);
+    if (lane >= d) pre += v;
+  }
+  const uint32_t kept = __shfl_sync(0xffffffffu, pre, 31);
+  if (lane < kMaxLevels) {
+    st->seg_lo[lane] = lo;
+    st->seg_len[lane] = len;
+    st->seg_pre[lane] = pre - len;
+  }
+  if (lane == 0) {
+    st->seg_pre[kMaxLevels] = kept;
+    st->n_keep = kept;
+    st->nodes_pruned += n_rem - kept;
+  }
+}
+
+__global__ void __launch_bounds__(kST) survivors_kernel(EpochState* st, Queue q, int strategy,
                                                         const bbs_node* __restrict__ pending,
                                                         const int32_t* __restrict__ scores,
                                                         unsigned long long* __restrict__ s_key,
@@ -341,6 +405,7 @@ __global__ void __launch_bounds__(kST) survivors_kernel(EpochState* st, int stra
   __syncthreads();
   if (threadIdx.x < kMaxLevels && s_lv[threadIdx.x])
     st->level_evals[threadIdx.x] += s_lv[threadIdx.x];
+  if (threadIdx.x < 32) trim_remainder(st, q, strategy, B);
   for (uint32_t base = 0; base < n; base += kST * kSIPT) {
     int keep[kSIPT];
     int cnt = 0;
@@ -402,42 +467,44 @@ __global__ void __launch_bounds__(kRT) rank_sort_kernel(const EpochState* st,
   }
 }
 
-__device__ __forceinline__ uint32_t lower_bound_u64(const unsigned long long* a, uint32_t n,
-                                                    unsigned long long v) {
-  uint32_t lo = 0, hi = n;
-  while (lo < hi) {
-    const uint32_t mid = (lo + hi) >> 1;
-    if (a[mid] < v)
-      lo = mid + 1;
-    else
-      hi = mid;
-  }
-  return lo;
-}
-
-// E6: merge the sorted survivors into the queue remainder (push, search.hpp:139).
-__global__ void merge_kernel(const EpochState* st, Queue q, const unsigned long long* __restrict__ skey,
+// E6: merge the sorted survivors into the trimmed queue remainder (push,
+// search.hpp:139).  The remainder is read through the kept segment ranges.
+__global__ void merge_kernel(const EpochState* st, Queue q, int strategy,
+                             const unsigned long long* __restrict__ skey,
                              const bbs_node* __restrict__ snode) {
+  __shared__ uint32_t s_lo[kMaxLevels], s_len[kMaxLevels], s_pre[kMaxLevels + 1];
   if (st->n_children == 0) return;
+  if (threadIdx.x < kMaxLevels) {
+    s_lo[threadIdx.x] = st->seg_lo[threadIdx.x];
+    s_len[threadIdx.x] = st->seg_len[threadIdx.x];
+    s_pre[threadIdx.x] = st->seg_pre[threadIdx.x];
+  }
+  if (threadIdx.x == 0) s_pre[kMaxLevels] = st->seg_pre[kMaxLevels];
+  __syncthreads();
   const uint32_t cur = st->cur;
-  const uint32_t n_cons = st->n_cons;
-  const uint32_t n_rem = st->q_len - n_cons;
+  const uint32_t n_keep = st->n_keep;
   const uint32_t n_s = st->n_surv;
-  const unsigned long long* __restrict__ qk = q.key[cur] + n_cons;
-  const bbs_node* __restrict__ qn = q.node[cur] + n_cons;
+  const unsigned long long* __restrict__ qk = q.key[cur] + st->n_cons;
+  const bbs_node* __restrict__ qn = q.node[cur] + st->n_cons;
   unsigned long long* __restrict__ ok = q.key[cur ^ 1];
   bbs_node* __restrict__ on = q.node[cur ^ 1];
-  const uint32_t total = n_rem + n_s;
+  const uint32_t total = n_keep + n_s;
+  const bool bfs = strategy == BBS_STRATEGY_BFS;
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
-    if (i < n_rem) {
-      const unsigned long long k = qk[i];
+    if (i < n_keep) {
+      int sg = 0;
+      if (!bfs)
+        while (s_pre[sg + 1] <= i) ++sg;
+      const uint32_t src = s_lo[sg] + (i - s_pre[sg]);
+      const unsigned long long k = qk[src];
       const uint32_t pos = i + lower_bound_u64(skey, n_s, k);
       ok[pos] = k;
-      on[pos] = qn[i];
+      on[pos] = qn[src];
     } else {
-      const uint32_t j = i - n_rem;
+      const uint32_t j = i - n_keep;
       const unsigned long long k = skey[j];
-      const uint32_t pos = j + lower_bound_u64(qk, n_rem, k);
+      const int sg = bfs ? 0 : static_cast<int>(k >> 60);
+      const uint32_t pos = j + s_pre[sg] + lower_bound_u64(qk + s_lo[sg], s_len[sg], k);
       ok[pos] = k;
       on[pos] = snode[j];
     }
@@ -447,7 +514,7 @@ __global__ void merge_kernel(const EpochState* st, Queue q, const unsigned long 
 // E7: swap queue buffers; the loop ends when queue and pending are empty.
 __global__ void finalize_kernel(EpochState* st) {
   if (st->n_children == 0) return;
-  const uint32_t len = st->q_len - st->n_cons + st->n_surv;
+  const uint32_t len = st->n_keep + st->n_surv;
   st->q_len = len;
   st->cur ^= 1u;
   st->q_peak = max(st->q_peak, len);
@@ -940,11 +1007,11 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
     launch_epoch_score(m->view, gv, sv, pending, d_nchild, static_cast<uint32_t>(pend_cap), ptiles,
                        pscores, cache, s);
     record(ev_s1[e]);
-    survivors_kernel<<<1, kST, 0, s>>>(d_st, strategy, pending, pscores, s_key, s_node);
+    survivors_kernel<<<1, kST, 0, s>>>(d_st, q, strategy, pending, pscores, s_key, s_node);
     BBS_CUDA(cudaGetLastError());
     rank_sort_kernel<<<grid1(pend_cap, kRT), kRT, 0, s>>>(d_st, s_key, s_node, s_key2, s_node2);
     BBS_CUDA(cudaGetLastError());
-    merge_kernel<<<grid1(qcap), 256, 0, s>>>(d_st, q, s_key2, s_node2);
+    merge_kernel<<<grid1(qcap), 256, 0, s>>>(d_st, q, strategy, s_key2, s_node2);
     BBS_CUDA(cudaGetLastError());
     finalize_kernel<<<1, 1, 0, s>>>(d_st);
     BBS_CUDA(cudaGetLastError());
