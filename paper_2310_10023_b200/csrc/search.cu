@@ -54,6 +54,8 @@ struct EpochState {
   uint32_t pass;           // frontier passes executed while active
   uint32_t q_peak;
   uint32_t n_keep;         // queue remainder kept after the incumbent trim
+  uint32_t surv_ticket;    // survivors tile tickets (reset by the frontier)
+  uint32_t pad2;
   unsigned long long level_evals[kMaxLevels];  // flush evaluations per level
   // kept ranges of the remainder: one per key segment (BFS: 1, DFS: level)
   uint32_t seg_lo[kMaxLevels], seg_len[kMaxLevels], seg_pre[kMaxLevels + 1];
@@ -253,6 +255,7 @@ __global__ void __launch_bounds__(kFT) frontier_kernel(EpochState* st, Queue q, 
   __syncthreads();
   const unsigned long long pruned_all = cub::BlockReduce<unsigned long long, kFT>(tmp.ru).Sum(pruned);
   if (tid == 0) {
+    st->surv_ticket = 0;
     st->nodes_pruned += pruned_all;
     st->best = carry_best;
     st->flush_best = carry_best;
@@ -317,11 +320,10 @@ __global__ void branch_kernel(const EpochState* st, Queue q, GridView G,
   }
 }
 
-constexpr int kST = 1024;
-constexpr int kSIPT = 4;
+constexpr int kST = 256;   // survivors: threads per tile
+constexpr int kSIPT = 16;  // items per thread (4096 per tile)
+constexpr int kSTile = kST * kSIPT;
 
-// E4a: flush pruning (search.hpp:134-140): keep score >= B in pending order
-// and give them consecutive seq numbers.
 __device__ __forceinline__ uint32_t lower_bound_u64(const unsigned long long* a, uint32_t n,
                                                     unsigned long long v) {
   uint32_t lo = 0, hi = n;
@@ -380,60 +382,103 @@ __device__ void trim_remainder(EpochState* st, const Queue& q, int strategy, int
   if (lane == 0) {
     st->seg_pre[kMaxLevels] = kept;
     st->n_keep = kept;
-    st->nodes_pruned += n_rem - kept;
+    atomicAdd(&st->nodes_pruned, static_cast<unsigned long long>(n_rem - kept));
   }
 }
 
+// E4a: flush pruning (search.hpp:134-140): keep score >= B in pending order
+// and give them consecutive seq numbers.  Single-pass ordered compaction:
+// tiles take tickets in order and chain their prefix through `tiles`
+// (decoupled look-back; words tagged with the epoch so nothing is cleared).
+// Block 0's first warp also trims the queue remainder.
 __global__ void __launch_bounds__(kST) survivors_kernel(EpochState* st, Queue q, int strategy,
                                                         const bbs_node* __restrict__ pending,
                                                         const int32_t* __restrict__ scores,
                                                         unsigned long long* __restrict__ s_key,
-                                                        bbs_node* __restrict__ s_node) {
+                                                        bbs_node* __restrict__ s_node,
+                                                        unsigned long long* __restrict__ tiles) {
+  using Load = cub::BlockLoad<int32_t, kST, kSIPT, cub::BLOCK_LOAD_WARP_TRANSPOSE>;
   using ScanI = cub::BlockScan<int, kST>;
-  __shared__ typename ScanI::TempStorage tmp;
-  __shared__ unsigned int s_lv[kMaxLevels];
+  __shared__ union {
+    typename Load::TempStorage load;
+    typename ScanI::TempStorage scan;
+  } tmp;
+  __shared__ uint32_t s_tile, s_excl;
+  __shared__ uint32_t s_lv[kMaxLevels];  // evaluations per level, this CTA
+  if (threadIdx.x < kMaxLevels) s_lv[threadIdx.x] = 0;
   const uint32_t n = st->n_children;
   if (n == 0) return;
   const int32_t B = st->flush_best;
   const unsigned long long seq0 = st->seq;
-  uint32_t carry = 0;
-  // evaluations per level (runs of 8 share a level)
-  if (threadIdx.x < kMaxLevels) s_lv[threadIdx.x] = 0;
-  __syncthreads();
-  for (uint32_t r = threadIdx.x; r < n / 8; r += blockDim.x)
-    atomicAdd(&s_lv[pending[8ull * r].level & (kMaxLevels - 1)], 8u);
-  __syncthreads();
-  if (threadIdx.x < kMaxLevels && s_lv[threadIdx.x])
-    st->level_evals[threadIdx.x] += s_lv[threadIdx.x];
-  if (threadIdx.x < 32) trim_remainder(st, q, strategy, B);
-  for (uint32_t base = 0; base < n; base += kST * kSIPT) {
-    int keep[kSIPT];
+  const unsigned long long tag = static_cast<unsigned long long>(st->pass & 0x3FFFFFFFu) << 34;
+  if (blockIdx.x == 0 && threadIdx.x < 32) trim_remainder(st, q, strategy, B);
+  const uint32_t n_tiles = (n + kSTile - 1) / kSTile;
+  for (;;) {
+    if (threadIdx.x == 0) s_tile = atomicAdd(&st->surv_ticket, 1u);
+    __syncthreads();
+    const uint32_t tile = s_tile;
+    if (tile >= n_tiles) {
+      if (threadIdx.x < kMaxLevels && s_lv[threadIdx.x])
+        atomicAdd(&st->level_evals[threadIdx.x], static_cast<unsigned long long>(s_lv[threadIdx.x]));
+      break;
+    }
+    const uint32_t base = tile * kSTile;
+    const uint32_t valid = min(static_cast<uint32_t>(kSTile), n - base);
+    int32_t sc[kSIPT];
+    Load(tmp.load).Load(scores + base, sc, static_cast<int>(valid), INT_MIN);
+    __syncthreads();
+    // runs of 8 share a level; kSIPT = 16 covers two runs per thread
+    static_assert(kSIPT % 8 == 0, "tile rows must hold whole runs");
+#pragma unroll
+    for (int rr = 0; rr < kSIPT / 8; ++rr) {
+      const uint32_t li = threadIdx.x * kSIPT + rr * 8;
+      const int lvl = li < valid ? pending[base + li].level & (kMaxLevels - 1) : -1;
+      const unsigned same = __match_any_sync(0xffffffffu, lvl);
+      if (lvl >= 0 && (__ffs(same) - 1) == (threadIdx.x & 31)) atomicAdd(&s_lv[lvl], 8u * __popc(same));
+    }
     int cnt = 0;
 #pragma unroll
     for (int k = 0; k < kSIPT; ++k) {
-      const uint32_t i = base + threadIdx.x * kSIPT + k;
-      keep[k] = (i < n && scores[i] >= B) ? 1 : 0;
-      cnt += keep[k];
+      if (threadIdx.x * kSIPT + k >= valid) sc[k] = INT_MIN;
+      cnt += sc[k] >= B ? 1 : 0;
     }
     int pos, tot;
-    ScanI(tmp).ExclusiveSum(cnt, pos, tot);
+    ScanI(tmp.scan).ExclusiveSum(cnt, pos, tot);
+    if (threadIdx.x == 0) {
+      uint32_t excl = 0;
+      if (tile == 0) {
+        atomicExch(&tiles[0], tag | (2ull << 32) | static_cast<uint32_t>(tot));
+      } else {
+        atomicExch(&tiles[tile], tag | (1ull << 32) | static_cast<uint32_t>(tot));
+        for (int64_t t = static_cast<int64_t>(tile) - 1; t >= 0;) {
+          const unsigned long long w = atomicAdd(&tiles[t], 0ull);
+          if ((w & ~((1ull << 34) - 1)) != tag) continue;  // not published yet
+          excl += static_cast<uint32_t>(w);
+          if (((w >> 32) & 3u) == 2u) break;                // inclusive prefix
+          --t;
+        }
+        atomicExch(&tiles[tile], tag | (2ull << 32) | (excl + static_cast<uint32_t>(tot)));
+      }
+      s_excl = excl;
+      if (tile == n_tiles - 1) {
+        const uint32_t kept = excl + static_cast<uint32_t>(tot);
+        st->n_surv = kept;
+        st->seq = seq0 + kept;
+        atomicAdd(&st->nodes_pruned, static_cast<unsigned long long>(n - kept));
+      }
+    }
     __syncthreads();
+    uint32_t o = s_excl + static_cast<uint32_t>(pos);
 #pragma unroll
     for (int k = 0; k < kSIPT; ++k) {
+      if (sc[k] < B || threadIdx.x * kSIPT + k >= valid) continue;
       const uint32_t i = base + threadIdx.x * kSIPT + k;
-      if (!keep[k]) continue;
       bbs_node nd = pending[i];
-      nd.score = scores[i];
-      const uint32_t o = carry + pos++;
+      nd.score = sc[k];
       s_node[o] = nd;
       s_key[o] = queue_key(strategy, nd.score, nd.level, seq0 + o);
+      ++o;
     }
-    carry += static_cast<uint32_t>(tot);
-  }
-  if (threadIdx.x == 0) {
-    st->n_surv = carry;
-    st->seq = seq0 + carry;
-    st->nodes_pruned += n - carry;
   }
 }
 
@@ -521,11 +566,14 @@ __global__ void finalize_kernel(EpochState* st) {
   if (len == 0) st->active = 0;
 }
 
-// Root survivors -> queue entries (seq = rank in initial_nodes order).
+// Root survivors -> queue entries (seq = rank in initial_nodes order).  All
+// roots share one level, so the queue order is (score desc, seq asc) for BFS
+// and (score desc, seq desc) for DFS: a STABLE sort on the short key
+// smax - score, fed in seq order (BFS) or reversed (DFS), yields it.
 __global__ void roots_to_queue_kernel(const unsigned long long* __restrict__ ref_idx, uint32_t n,
                                       const int32_t* __restrict__ scores, BoxParams bp,
-                                      int strategy, unsigned long long* __restrict__ key,
-                                      bbs_node* __restrict__ node) {
+                                      int strategy, int32_t smax, uint32_t* __restrict__ skey,
+                                      uint32_t* __restrict__ perm, bbs_node* __restrict__ node) {
   const unsigned long long nrot = static_cast<unsigned long long>(bp.nr) * bp.np * bp.nw;
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     const unsigned long long r = ref_idx[i];
@@ -540,18 +588,21 @@ __global__ void roots_to_queue_kernel(const unsigned long long* __restrict__ ref
     nd.level = bp.level;
     nd.score = scores[r];
     node[i] = nd;
-    key[i] = queue_key(strategy, nd.score, nd.level, i);
+    const uint32_t j = strategy == BBS_STRATEGY_BFS ? i : n - 1 - i;
+    skey[j] = static_cast<uint32_t>(smax - nd.score);
+    perm[j] = i;
   }
 }
 
 __global__ void gather_nodes_kernel(const uint32_t* __restrict__ perm, const bbs_node* __restrict__ in,
-                                    bbs_node* __restrict__ out, uint32_t n) {
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
-    out[i] = in[perm[i]];
-}
-
-__global__ void iota_kernel(uint32_t* __restrict__ p, uint32_t n) {
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) p[i] = i;
+                                    int strategy, bbs_node* __restrict__ out,
+                                    unsigned long long* __restrict__ key, uint32_t n) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const uint32_t seq = perm[i];
+    const bbs_node nd = in[seq];
+    out[i] = nd;
+    key[i] = queue_key(strategy, nd.score, nd.level, seq);
+  }
 }
 
 __global__ void soa_kernel(const double* __restrict__ aos, uint64_t k, double* __restrict__ soa) {
@@ -626,11 +677,11 @@ struct Buf {
 struct Workspace {
   Buf<double2> lut;
   Buf<int32_t> root_scores;
-  Buf<unsigned long long> probes, surv_idx, k0, qk0, qk1, s_key, s_key2;
+  Buf<unsigned long long> probes, surv_idx, qk0, qk1, s_key, s_key2, surv_tiles;
   Buf<int> nsel;
   Buf<unsigned char> temp;
   Buf<bbs_node> n0, qn0, qn1, pending, s_node, s_node2;
-  Buf<uint32_t> perm0, perm1, exp_parent, exp_off;
+  Buf<uint32_t> perm0, perm1, sk0, sk1, exp_parent, exp_off;
   Buf<int32_t> pscores, trace, hist_n;
   Buf<int4> hist_ent, cache_info, cache_pool, cache_builds;
   Buf<uint32_t> cache_u32, cache_amb;
@@ -651,9 +702,9 @@ struct Workspace {
   }
   void release_all() {
     for (auto* b : {&root_scores, &pscores, &trace, &hist_n}) b->release();
-    for (auto* b : {&probes, &surv_idx, &k0, &qk0, &qk1, &s_key, &s_key2}) b->release();
+    for (auto* b : {&probes, &surv_idx, &qk0, &qk1, &s_key, &s_key2, &surv_tiles}) b->release();
     for (auto* b : {&n0, &qn0, &qn1, &pending, &s_node, &s_node2}) b->release();
-    for (auto* b : {&perm0, &perm1, &exp_parent, &exp_off, &hist_amb}) b->release();
+    for (auto* b : {&perm0, &perm1, &sk0, &sk1, &exp_parent, &exp_off, &hist_amb}) b->release();
     lut.release();
     nsel.release();
     temp.release();
@@ -882,26 +933,30 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
   q.node[1] = W.qn1.get(qcap, s);
   qcap = std::min({W.qk0.cap, W.qk1.cap, W.qn0.cap, W.qn1.cap});
   if (n_root_surv > 0) {
-    // keys in initial_nodes order (seq = position), then sort by key
-    unsigned long long* k0 = W.k0.get(n_root_surv, s);
+    // nodes in initial_nodes order (seq = position), stable sort on the
+    // score key over only the bits it spans, then gather nodes + queue keys
+    const int32_t smax = static_cast<int32_t>(std::min<size_t>(K, 0x7FFFFFFF));
+    const uint32_t span = static_cast<uint32_t>(smax - std::max<int32_t>(0, std::min(threshold, smax)));
+    int end_bit = 1;
+    while (end_bit < 32 && (span >> end_bit) != 0) ++end_bit;
+    uint32_t* sk0 = W.sk0.get(n_root_surv, s);
+    uint32_t* sk1 = W.sk1.get(n_root_surv, s);
     bbs_node* n0 = W.n0.get(n_root_surv, s);
     uint32_t* perm0 = W.perm0.get(n_root_surv, s);
     uint32_t* perm1 = W.perm1.get(n_root_surv, s);
     roots_to_queue_kernel<<<grid1(n_root_surv), 256, 0, s>>>(surv_idx, n_root_surv, root_scores, bp,
-                                                             strategy, k0, n0);
+                                                             strategy, smax, sk0, perm0, n0);
     BBS_CUDA(cudaGetLastError());
-    iota_kernel<<<grid1(n_root_surv), 256, 0, s>>>(perm0, n_root_surv);
-    cub::DoubleBuffer<unsigned long long> dk(k0, q.key[0]);
+    cub::DoubleBuffer<uint32_t> dk(sk0, sk1);
     cub::DoubleBuffer<uint32_t> dv(perm0, perm1);
     size_t tb = 0;
-    BBS_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, dk, dv, n_root_surv, 0, 64, s));
+    BBS_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, dk, dv, n_root_surv, 0, end_bit, s));
     void* temp = W.temp.get(tb, s);
-    BBS_CUDA(cub::DeviceRadixSort::SortPairs(temp, tb, dk, dv, n_root_surv, 0, 64, s));
-    if (dk.Current() != q.key[0])
-      BBS_CUDA(cudaMemcpyAsync(q.key[0], dk.Current(), n_root_surv * 8ull, cudaMemcpyDeviceToDevice, s));
-    gather_nodes_kernel<<<grid1(n_root_surv), 256, 0, s>>>(dv.Current(), n0, q.node[0], n_root_surv);
+    BBS_CUDA(cub::DeviceRadixSort::SortPairs(temp, tb, dk, dv, n_root_surv, 0, end_bit, s));
+    gather_nodes_kernel<<<grid1(n_root_surv), 256, 0, s>>>(dv.Current(), n0, strategy, q.node[0], q.key[0],
+                                                           n_root_surv);
     BBS_CUDA(cudaGetLastError());
-    launches += 3;  // roots_to_queue, iota, gather
+    launches += 2;  // roots_to_queue, gather
   }
 
   EpochState h0{};
@@ -923,6 +978,10 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
 
   bbs_node* pending = W.pending.get(pend_cap, s);
   int32_t* pscores = W.pscores.get(pend_cap, s);
+  const uint64_t n_surv_tiles = (pend_cap + kSTile - 1) / kSTile;
+  unsigned long long* surv_tiles = W.surv_tiles.get(n_surv_tiles, s);
+  BBS_CUDA(cudaMemsetAsync(surv_tiles, 0, n_surv_tiles * sizeof(unsigned long long), s));
+  const unsigned surv_grid = static_cast<unsigned>(std::min<uint64_t>(n_surv_tiles, 148ull * 4));
   const uint64_t exp_cap = pend_cap / 8 + 2;
   uint32_t* exp_parent = W.exp_parent.get(exp_cap, s);
   uint32_t* exp_off = W.exp_off.get(exp_cap, s);
@@ -1007,7 +1066,8 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
     launch_epoch_score(m->view, gv, sv, pending, d_nchild, static_cast<uint32_t>(pend_cap), ptiles,
                        pscores, cache, s);
     record(ev_s1[e]);
-    survivors_kernel<<<1, kST, 0, s>>>(d_st, q, strategy, pending, pscores, s_key, s_node);
+    survivors_kernel<<<surv_grid, kST, 0, s>>>(d_st, q, strategy, pending, pscores, s_key, s_node,
+                                               surv_tiles);
     BBS_CUDA(cudaGetLastError());
     rank_sort_kernel<<<grid1(pend_cap, kRT), kRT, 0, s>>>(d_st, s_key, s_node, s_key2, s_node2);
     BBS_CUDA(cudaGetLastError());
@@ -1126,6 +1186,33 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
   out->root_nodes = n_own;
   out->lookups = hs.nodes_generated * K;
   out->queue_peak = hs.q_peak;
+  if (cache.enabled && std::getenv("BBS_DEBUG_CACHE")) {
+    // dev aid: built histograms per level and their mean size
+    const size_t ns = W.cache_info.cap;
+    std::vector<int4> info(ns);
+    BBS_CUDA(cudaMemcpyAsync(info.data(), cache.info, ns * sizeof(int4), cudaMemcpyDeviceToHost, s));
+    BBS_CUDA(cudaStreamSynchronize(s));
+    for (int l = 0; l <= L; ++l) {
+      if (cache.base[l] == 0xFFFFFFFFu) continue;
+      uint32_t end = static_cast<uint32_t>(ns);
+      for (int l2 = 0; l2 <= L; ++l2)
+        if (cache.base[l2] != 0xFFFFFFFFu && cache.base[l2] > cache.base[l]) end = std::min(end, cache.base[l2]);
+      uint64_t ready = 0, none = 0, ent = 0, amb = 0;
+      for (uint32_t i = cache.base[l]; i < end; ++i) {
+        if (info[i].x == 0) {
+          ++ready;
+          ent += static_cast<uint32_t>(info[i].z);
+          amb += static_cast<uint32_t>(info[i].w);
+        } else if (info[i].x == -3) {
+          ++none;
+        }
+      }
+      std::fprintf(stderr, "[cache] level %d: slots %u built %llu failed %llu mean entries %.1f mean amb %.2f (K %zu)\n",
+                   l, end - cache.base[l], static_cast<unsigned long long>(ready),
+                   static_cast<unsigned long long>(none), ready ? double(ent) / ready : 0.0,
+                   ready ? double(amb) / ready : 0.0, K);
+    }
+  }
   out->root_probes = root_probes;
   out->trace_length = cfg.collect_trace ? hs.trace_len : 0;
   if (cfg.collect_trace && out->best_score_trace && hs.trace_len) {
