@@ -10,8 +10,9 @@
 // + dense rotation id, no sorting.  Per flush:
 //   claim  (one thread per run)  claims empty slots, lists the builds;
 //   build  (one CTA per claimed rotation) rotates the K points, dedups the
-//          voxel offsets in shared memory (raw per-point entries when they do
-//          not fit), appends entries + ambiguous points to the pool;
+//          voxel offsets in shared memory, appends entries + ambiguous points
+//          to the pool; when the offsets do not de-duplicate (fine levels) it
+//          gives up early and flags the level uncached for the search;
 //   probe  (one warp per (run, 256-entry chunk)) cube-probes the entries;
 //   cube   (score.cu) scores the runs at uncached levels / failed builds.
 // Exactness: the cached offsets use fast_floor with tmax = the largest
@@ -58,13 +59,11 @@ __global__ void cache_claim_kernel(RotCache c, GridView G, const bbs_node* __res
     const int4 a = __ldg(reinterpret_cast<const int4*>(pending) + 16ull * r);
     const int4 b = __ldg(reinterpret_cast<const int4*>(pending) + 16ull * r + 1);
     uint32_t slot;
-    if (!run_slot(c, G, a, b, &slot)) {
-      atomicAdd(&c.ctl[3], 1u);  // uncached level: the cube kernel scores this run
-      continue;
-    }
-    const int32_t state = c.info[slot].x;
-    if (state == kCacheNone) atomicAdd(&c.ctl[3], 1u);
-    if (state != kCacheEmpty) continue;
+    if (!run_slot(c, G, a, b, &slot)) continue;  // uncached level: the cube kernel scores it
+    if (c.info[slot].x != kCacheEmpty) continue;
+    // the level's offsets do not de-duplicate: a build would cost more than
+    // it saves, the cube kernel scores the run directly
+    if (c.ctl[4 + (b.z & (kMaxLevels - 1))]) continue;
     if (atomicCAS(&c.info[slot].x, kCacheEmpty, kCacheBuilding) == kCacheEmpty) {
       const uint32_t i = atomicAdd(&c.ctl[2], 1u);
       c.builds[i] = make_int4(static_cast<int32_t>(slot), b.z, a.w, b.x);  // slot, level, ir, ip
@@ -73,14 +72,23 @@ __global__ void cache_claim_kernel(RotCache c, GridView G, const bbs_node* __res
   }
 }
 
-__global__ void __launch_bounds__(512) cache_build_kernel(RotCache c, MapView map, GridView G,
-                                                          ScanView scan) {
+constexpr int kBuildThreads = 512;
+
+// One CTA per claimed (level, rotation): rotate + floor every scan point
+// (fast path), de-duplicate the voxel offsets in a shared-memory hash, and
+// append (offset, count) entries + ambiguous point ids to the pool.  Two
+// points per thread per step keep two load/rotate chains in flight.
+__global__ void __launch_bounds__(kBuildThreads) cache_build_kernel(RotCache c, MapView map, GridView G,
+                                                                    ScanView scan) {
   extern __shared__ __align__(16) unsigned char smem[];
   unsigned long long* s_key = reinterpret_cast<unsigned long long*>(smem);   // 64 KB
   int32_t* s_cnt = reinterpret_cast<int32_t*>(s_key + kCacheHashSlots);      // 32 KB
   uint32_t* s_amb = reinterpret_cast<uint32_t*>(s_cnt + kCacheHashSlots);    // 8 KB
-  __shared__ int s_distinct, s_namb, s_over;
+  using ScanI = cub::BlockScan<int, kBuildThreads>;
+  __shared__ typename ScanI::TempStorage s_scan;
+  __shared__ int s_distinct, s_namb;
   __shared__ uint32_t s_off, s_aoff;
+  const int lane = threadIdx.x & 31;
   const uint32_t n_build = c.ctl[2];
   for (uint32_t bi = blockIdx.x; bi < n_build; bi += gridDim.x) {
     const int4 bd = c.builds[bi];
@@ -97,91 +105,101 @@ __global__ void __launch_bounds__(512) cache_build_kernel(RotCache c, MapView ma
     if (threadIdx.x == 0) {
       s_distinct = 0;
       s_namb = 0;
-      s_over = 0;
     }
     __syncthreads();
     // all lanes stay in the loop together (warp-aggregated inserts below)
-    for (uint32_t p0 = 0; p0 < scan.k; p0 += blockDim.x) {
-      const uint32_t p = p0 + threadIdx.x;
-      const bool live = p < scan.k;
-      bool ok = false;
-      int32_t fx = 0, fy = 0, fz = 0;
-      if (live) {
-        const double px = scan.x[p], py = scan.y[p], pz = scan.z[p];
-        ok = fast_floor(rot_row(R[0], R[1], R[2], px, py, pz), L.inv_cell, tmax, &fx) &
-             fast_floor(rot_row(R[3], R[4], R[5], px, py, pz), L.inv_cell, tmax, &fy) &
-             fast_floor(rot_row(R[6], R[7], R[8], px, py, pz), L.inv_cell, tmax, &fz);
-        ok = ok && fx > -(1 << 20) && fx < (1 << 20) && fy > -(1 << 20) && fy < (1 << 20) &&
-             fz > -(1 << 20) && fz < (1 << 20);
-        if (!ok) {
-          const int a = atomicAdd(&s_namb, 1);
-          if (a < kCacheAmbCap) s_amb[a] = p;
-        }
+    bool aborted = false;
+    for (uint32_t p0 = 0; p0 < scan.k; p0 += 2 * blockDim.x) {
+      uint32_t p[2];
+      double px[2], py[2], pz[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        p[h] = p0 + h * blockDim.x + threadIdx.x;
+        const bool live = p[h] < scan.k;
+        px[h] = live ? scan.x[p[h]] : 0.0;
+        py[h] = live ? scan.y[p[h]] : 0.0;
+        pz[h] = live ? scan.z[p[h]] : 0.0;
       }
-      const bool ins = live && ok && s_distinct < kCacheHashCap;
-      if (live && ok && !ins) s_over = 1;  // too many distinct offsets: raw entries below
-      const unsigned long long key = ins ? (static_cast<unsigned long long>(fx + (1 << 20)) << 42) |
-                                               (static_cast<unsigned long long>(fy + (1 << 20)) << 21) |
-                                               static_cast<unsigned long long>(fz + (1 << 20))
-                                         : kEmptyKey;
-      // neighbouring scan points often share a voxel: one insert per distinct key per warp
-      const unsigned same = __match_any_sync(0xffffffffu, key);
-      if (ins && (__ffs(same) - 1) == (threadIdx.x & 31)) {
-        const int mult = __popc(same);
-        uint32_t h = cache_hash(key);
-        for (;;) {
-          const unsigned long long prev = atomicCAS(&s_key[h], kEmptyKey, key);
-          if (prev == kEmptyKey) atomicAdd(&s_distinct, 1);
-          if (prev == kEmptyKey || prev == key) {
-            atomicAdd(&s_cnt[h], mult);
-            break;
+      if (s_distinct >= kCacheHashCap) {  // uniform: read after the step barrier
+        aborted = true;
+        break;
+      }
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const bool live = p[h] < scan.k;
+        bool ok = false;
+        int32_t fx = 0, fy = 0, fz = 0;
+        if (live) {
+          ok = fast_floor(rot_row(R[0], R[1], R[2], px[h], py[h], pz[h]), L.inv_cell, tmax, &fx) &
+               fast_floor(rot_row(R[3], R[4], R[5], px[h], py[h], pz[h]), L.inv_cell, tmax, &fy) &
+               fast_floor(rot_row(R[6], R[7], R[8], px[h], py[h], pz[h]), L.inv_cell, tmax, &fz);
+          ok = ok && fx > -(1 << 20) && fx < (1 << 20) && fy > -(1 << 20) && fy < (1 << 20) &&
+               fz > -(1 << 20) && fz < (1 << 20);
+          if (!ok) {
+            const int a = atomicAdd(&s_namb, 1);
+            if (a < kCacheAmbCap) s_amb[a] = p[h];
           }
-          h = (h + 1) & (kCacheHashSlots - 1);
         }
+        const bool ins = live && ok;
+        const unsigned long long key = ins ? (static_cast<unsigned long long>(fx + (1 << 20)) << 42) |
+                                                 (static_cast<unsigned long long>(fy + (1 << 20)) << 21) |
+                                                 static_cast<unsigned long long>(fz + (1 << 20))
+                                           : kEmptyKey;
+        // neighbouring scan points often share a voxel: one insert per distinct key per warp
+        const unsigned same = __match_any_sync(0xffffffffu, key);
+        int fresh = 0;
+        if (ins && (__ffs(same) - 1) == lane) {
+          const int mult = __popc(same);
+          uint32_t hh = cache_hash(key);
+          for (;;) {
+            const unsigned long long prev = atomicCAS(&s_key[hh], kEmptyKey, key);
+            if (prev == kEmptyKey || prev == key) {
+              fresh = prev == kEmptyKey;
+              atomicAdd(&s_cnt[hh], mult);
+              break;
+            }
+            hh = (hh + 1) & (kCacheHashSlots - 1);
+          }
+        }
+        // the distinct count only gates further inserts (the table has 2x room)
+        const int nf = __reduce_add_sync(0xffffffffu, fresh);
+        if (lane == 0 && nf) atomicAdd(&s_distinct, nf);
       }
+      __syncthreads();
     }
-    __syncthreads();
-    const bool raw = s_over != 0;
+    // too many distinct offsets (fine levels: about one per point): the
+    // histogram would not beat direct scoring, so give the level up
+    const bool raw = aborted;  // (a finished table holds <= cap + one step < slots)
     const int namb = s_namb;
-    const uint32_t n_ent = raw ? scan.k - static_cast<uint32_t>(namb) : static_cast<uint32_t>(s_distinct);
+    // distinct entries in slot order (block scan; deterministic layout)
+    constexpr int kPer = kCacheHashSlots / kBuildThreads;
+    int cnt = 0;
+    if (!raw) {
+#pragma unroll
+      for (int k = 0; k < kPer; ++k) cnt += s_key[threadIdx.x * kPer + k] != kEmptyKey ? 1 : 0;
+    }
+    int epos, n_dist;
+    ScanI(s_scan).ExclusiveSum(cnt, epos, n_dist);
+    const uint32_t n_ent = raw ? 0u : static_cast<uint32_t>(n_dist);
     if (threadIdx.x == 0) {
-      s_off = atomicAdd(&c.ctl[0], n_ent);
-      s_aoff = atomicAdd(&c.ctl[1], static_cast<uint32_t>(namb));
+      s_off = raw ? 0u : atomicAdd(&c.ctl[0], n_ent);
+      s_aoff = raw ? 0u : atomicAdd(&c.ctl[1], static_cast<uint32_t>(namb));
+      if (raw) c.ctl[4 + (l & (kMaxLevels - 1))] = 1u;
     }
     __syncthreads();
     const uint32_t off = s_off, aoff = s_aoff;
-    const bool fits = namb <= kCacheAmbCap && static_cast<uint64_t>(off) + n_ent <= c.pool_cap &&
+    const bool fits = !raw && namb <= kCacheAmbCap && static_cast<uint64_t>(off) + n_ent <= c.pool_cap &&
                       static_cast<uint64_t>(aoff) + namb <= c.amb_cap;
     if (fits) {
-      if (!raw) {
-        __shared__ int s_e;
-        if (threadIdx.x == 0) s_e = 0;
-        __syncthreads();
-        for (int i = threadIdx.x; i < kCacheHashSlots; i += blockDim.x) {
-          const unsigned long long key = s_key[i];
-          if (key != kEmptyKey) {
-            const int e = atomicAdd(&s_e, 1);
-            c.pool[off + e] = make_int4(static_cast<int32_t>((key >> 42) & 0x1FFFFF) - (1 << 20),
-                                        static_cast<int32_t>((key >> 21) & 0x1FFFFF) - (1 << 20),
-                                        static_cast<int32_t>(key & 0x1FFFFF) - (1 << 20), s_cnt[i]);
-          }
-        }
-      } else {
-        // raw: one entry per fast-path point (count 1), in point order
-        __shared__ int s_e;
-        if (threadIdx.x == 0) s_e = 0;
-        __syncthreads();
-        for (uint32_t p = threadIdx.x; p < scan.k; p += blockDim.x) {
-          const double px = scan.x[p], py = scan.y[p], pz = scan.z[p];
-          int32_t fx, fy, fz;
-          bool ok = fast_floor(rot_row(R[0], R[1], R[2], px, py, pz), L.inv_cell, tmax, &fx) &
-                    fast_floor(rot_row(R[3], R[4], R[5], px, py, pz), L.inv_cell, tmax, &fy) &
-                    fast_floor(rot_row(R[6], R[7], R[8], px, py, pz), L.inv_cell, tmax, &fz);
-          ok = ok && fx > -(1 << 20) && fx < (1 << 20) && fy > -(1 << 20) && fy < (1 << 20) &&
-               fz > -(1 << 20) && fz < (1 << 20);
-          if (!ok) continue;
-          const int e = atomicAdd(&s_e, 1);
-          c.pool[off + e] = make_int4(fx, fy, fz, 1);
+#pragma unroll
+      for (int k = 0; k < kPer; ++k) {
+        const int i = threadIdx.x * kPer + k;
+        const unsigned long long key = s_key[i];
+        if (key != kEmptyKey) {
+          c.pool[off + epos] = make_int4(static_cast<int32_t>((key >> 42) & 0x1FFFFF) - (1 << 20),
+                                         static_cast<int32_t>((key >> 21) & 0x1FFFFF) - (1 << 20),
+                                         static_cast<int32_t>(key & 0x1FFFFF) - (1 << 20), s_cnt[i]);
+          ++epos;
         }
       }
       for (int a = threadIdx.x; a < namb; a += blockDim.x) c.amb_pool[aoff + a] = s_amb[a];
@@ -192,7 +210,6 @@ __global__ void __launch_bounds__(512) cache_build_kernel(RotCache c, MapView ma
       // publish: entries first, then the state (readers run in later kernels)
       c.info[slot] = fits ? make_int4(kCacheReady, static_cast<int32_t>(off), static_cast<int32_t>(n_ent), namb)
                           : make_int4(kCacheNone, 0, 0, 0);
-      if (!fits) atomicAdd(&c.ctl[3], 1u);  // its runs fall back to the cube kernel
     }
     __syncthreads();
   }
@@ -236,7 +253,8 @@ __global__ void __launch_bounds__(256) cache_probe_kernel(RotCache c, MapView ma
   const uint64_t gw = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   for (uint64_t k0 = 0; gw + k0 * n_warps < n_items; k0 += 32) {
     const uint64_t item = gw + (k0 + lane) * n_warps;
-    int4 a = make_int4(0, 0, 0, 0), b = make_int4(0, 0, 0, 0), inf = make_int4(0, 0, 0, 0);
+    // inf stays NONE for runs at uncached levels (no slot)
+    int4 a = make_int4(0, 0, 0, 0), b = make_int4(0, 0, 0, 0), inf = make_int4(kCacheNone, 0, 0, 0);
     uint32_t slot = 0, chunk = 0, run = 0;
     bool has = false;
     if (item < n_items) {
@@ -249,6 +267,16 @@ __global__ void __launch_bounds__(256) cache_probe_kernel(RotCache c, MapView ma
         has = inf.x == kCacheReady &&
               (chunk * kProbeChunk < static_cast<uint32_t>(inf.z) || (chunk == 0 && inf.w > 0));
       }
+    }
+    // runs without a READY histogram go to the cube kernel's list (chunk 0 items)
+    const bool fb = item < n_items && chunk == 0 && inf.x != kCacheReady;
+    const unsigned fbm = __ballot_sync(0xffffffffu, fb);
+    if (fbm) {
+      const int leader = __ffs(fbm) - 1;
+      uint32_t at = 0;
+      if (lane == leader) at = atomicAdd(&c.ctl[3], static_cast<uint32_t>(__popc(fbm)));
+      at = __shfl_sync(0xffffffffu, at, leader);
+      if (fb) c.fb_runs[at + __popc(fbm & ((1u << lane) - 1))] = run;
     }
     unsigned todo = __ballot_sync(0xffffffffu, has);
     while (todo) {
@@ -325,6 +353,7 @@ void launch_epoch_score(const MapView& map, const GridView& grid, const ScanView
   }
   static bool attr_done = false;
   const int build_smem = kCacheHashSlots * 12 + kCacheAmbCap * 4;
+  static_assert(kCacheHashSlots % kBuildThreads == 0, "slot rows per thread");
   if (!attr_done) {
     BBS_CUDA(cudaFuncSetAttribute(cache_build_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   build_smem));
@@ -334,7 +363,7 @@ void launch_epoch_score(const MapView& map, const GridView& grid, const ScanView
   BBS_CUDA(cudaMemsetAsync(cache.ctl + 2, 0, 2 * sizeof(uint32_t), s));  // builds, fallback runs
   cache_claim_kernel<<<(max_runs + 255) / 256, 256, 0, s>>>(cache, grid, pending, d_n);
   BBS_CUDA(cudaGetLastError());
-  cache_build_kernel<<<std::min<uint32_t>(std::max<uint32_t>(max_runs, 1), 148 * 2), 512, build_smem, s>>>(
+  cache_build_kernel<<<std::min<uint32_t>(std::max<uint32_t>(max_runs, 1), 148 * 2), kBuildThreads, build_smem, s>>>(
       cache, map, grid, scan);
   BBS_CUDA(cudaGetLastError());
   const uint32_t chunks = (scan.k + kProbeChunk - 1) / kProbeChunk;

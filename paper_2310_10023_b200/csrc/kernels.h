@@ -95,6 +95,7 @@ void launch_score_runs8(const MapView& map, const GridView& grid, const ScanView
 // for the flush batches (epoch_cache.cu).  info[slot] = {state, pool offset,
 // entries, ambiguous points}; slot = base[level] + dense rotation id.
 constexpr int32_t kCacheEmpty = -1, kCacheBuilding = -2, kCacheNone = -3, kCacheReady = 0;
+constexpr int kCacheCtl = 4 + kMaxLevels;
 struct RotCache {
   int enabled;
   uint32_t base[kMaxLevels];   // 0xFFFFFFFF: level not cached
@@ -103,7 +104,9 @@ struct RotCache {
   uint32_t* amb_off;           // [slots]
   int4* pool;                  // (fx, fy, fz, count) entries
   uint32_t* amb_pool;          // ambiguous scan point indices
-  uint32_t* ctl;               // [4] pool used, amb used, builds this flush, -
+  uint32_t* ctl;               // [kCacheCtl] pool used, amb used, builds this flush,
+                               // fallback runs this flush, then per-level "raw" flags
+  uint32_t* fb_runs;           // [max runs] runs the cube kernel scores (not cached)
   int4* builds;                // [max runs] (slot, level, iroll, ipitch)
   int32_t* builds_w;           // [max runs] iyaw
   uint64_t pool_cap, amb_cap;

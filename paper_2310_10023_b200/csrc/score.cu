@@ -314,28 +314,24 @@ __global__ void __launch_bounds__(256, 4) score_cube8_kernel(MapView map, GridVi
   __shared__ double s_R[9];
   __shared__ int32_t s_hdr[4];
   __shared__ int32_t s_cnt[8];
-  const uint32_t n_runs = *d_n / 8;
-  const uint64_t n_items = static_cast<uint64_t>(n_runs) * n_ptiles;
   const uint32_t k = scan.k;
+  uint32_t n_runs = *d_n / 8;
+  const uint32_t* list = nullptr;
+  if (use_cache) {
+    // only the runs the probe kernel listed (no READY histogram); the point
+    // tiling is chosen here, for the actual number of runs
+    n_runs = cache.ctl[3];
+    if (n_runs == 0) return;
+    list = cache.fb_runs;
+    const uint32_t pmax = max(1u, (k + 1023u) / 1024u);
+    n_ptiles = min(pmax, max(1u, (2u * gridDim.x + n_runs - 1) / n_runs));
+  }
+  const uint64_t n_items = static_cast<uint64_t>(n_runs) * n_ptiles;
   const uint32_t tile = (k + n_ptiles - 1) / n_ptiles;
   const int lane = threadIdx.x & 31;
-  if (use_cache && cache.ctl[3] == 0) return;  // every run was scored from the cache
   for (uint64_t item = blockIdx.x; item < n_items; item += gridDim.x) {
-    const uint32_t run = static_cast<uint32_t>(item / n_ptiles);
+    const uint32_t run = list ? list[item / n_ptiles] : static_cast<uint32_t>(item / n_ptiles);
     const uint32_t pt = static_cast<uint32_t>(item % n_ptiles);
-    if (use_cache) {
-      // runs scored from their rotation's cached histogram are skipped (uniform per CTA)
-      const int4 a = __ldg(reinterpret_cast<const int4*>(nodes) + 2 * (8ull * run));
-      const int4 b = __ldg(reinterpret_cast<const int4*>(nodes) + 2 * (8ull * run) + 1);
-      const uint32_t base = cache.base[b.z];
-      if (base != 0xFFFFFFFFu) {
-        const uint32_t np = static_cast<uint32_t>(grid.max_index[b.z * 3 + 1]) + 1;
-        const uint32_t nw = static_cast<uint32_t>(grid.max_index[b.z * 3 + 2]) + 1;
-        const uint32_t slot = base + (static_cast<uint32_t>(a.w) * np + static_cast<uint32_t>(b.x)) * nw +
-                              static_cast<uint32_t>(b.y);
-        if (cache.info[slot].x == kCacheReady) continue;
-      }
-    }
     if (threadIdx.x == 0) {
       const int4 a = reinterpret_cast<const int4*>(nodes)[2 * (8ull * run)];
       const int4 b = reinterpret_cast<const int4*>(nodes)[2 * (8ull * run) + 1];
@@ -765,7 +761,10 @@ void launch_score_cube8(const MapView& map, const GridView& grid, const ScanView
                         uint32_t n_ptiles, int32_t* scores, const RotCache* cache,
                         cudaStream_t s) {
   const uint64_t items = static_cast<uint64_t>((n_max + 7) / 8) * n_ptiles;
-  const unsigned g = static_cast<unsigned>(std::min<uint64_t>(std::max<uint64_t>(items, 1), 148ull * 4 * 8));
+  // with the cache the run list and tiling are only known on the device:
+  // one resident wave (4 CTAs per SM), grid-strided
+  const unsigned g = cache ? 148u * 4u
+                           : static_cast<unsigned>(std::min<uint64_t>(std::max<uint64_t>(items, 1), 148ull * 4 * 8));
   score_cube8_kernel<<<g, 256, 0, s>>>(map, grid, scan, nodes, d_n, n_ptiles, scores,
                                        cache ? *cache : RotCache{}, cache ? 1 : 0);
   BBS_CUDA(cudaGetLastError());

@@ -684,7 +684,7 @@ struct Workspace {
   Buf<uint32_t> perm0, perm1, sk0, sk1, exp_parent, exp_off;
   Buf<int32_t> pscores, trace, hist_n;
   Buf<int4> hist_ent, cache_info, cache_pool, cache_builds;
-  Buf<uint32_t> cache_u32, cache_amb;
+  Buf<uint32_t> cache_u32, cache_amb, cache_fb;
   Buf<int32_t> cache_builds_w;
   Buf<uint32_t> hist_amb;
   Buf<EpochState> st;
@@ -714,6 +714,7 @@ struct Workspace {
     cache_builds.release();
     cache_u32.release();
     cache_amb.release();
+    cache_fb.release();
     cache_builds_w.release();
     st.release();
     if (h_st) cudaFreeHost(h_st);
@@ -993,8 +994,8 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
   int32_t* d_trace = W.trace.get(std::max<uint64_t>(trace_cap, 1), s);
   const uint32_t ptiles = choose_ptiles((pend_cap + 7) / 8, static_cast<uint32_t>(K));
   // per-search (level, rotation) histogram cache for the flushes (epoch_cache.cu)
-  static const bool cache_on = [] {
-    const char* v = std::getenv("BBS_ROT_CACHE");  // "0" disables (A/B timing)
+  const bool cache_on = [] {
+    const char* v = std::getenv("BBS_ROT_CACHE");  // "0" disables (A/B timing, tests)
     return !(v && v[0] == '0');
   }();
   RotCache cache{};
@@ -1024,15 +1025,16 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
       cache.pool_cap = 64ull << 20;  // entries (16 B each)
       cache.amb_cap = 8ull << 20;
       cache.info = W.cache_info.get(slots, s);
-      cache.amb_off = W.cache_u32.get(slots + 4, s);
+      cache.amb_off = W.cache_u32.get(slots + kCacheCtl, s);
       cache.ctl = cache.amb_off + slots;
       cache.pool = W.cache_pool.get(cache.pool_cap, s);
       cache.amb_pool = W.cache_amb.get(cache.amb_cap, s);
       const uint64_t mr = (pend_cap + 7) / 8;
       cache.builds = W.cache_builds.get(mr, s);
       cache.builds_w = W.cache_builds_w.get(mr, s);
+      cache.fb_runs = W.cache_fb.get(mr, s);
       BBS_CUDA(cudaMemsetAsync(cache.info, 0xFF, slots * sizeof(int4), s));  // all kCacheEmpty
-      BBS_CUDA(cudaMemsetAsync(cache.ctl, 0, 4 * sizeof(uint32_t), s));
+      BBS_CUDA(cudaMemsetAsync(cache.ctl, 0, kCacheCtl * sizeof(uint32_t), s));
     }
   }
 
@@ -1047,6 +1049,10 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
   double esm = 0.0;            // device time in the flush score kernels
   const uint32_t* d_nchild = reinterpret_cast<const uint32_t*>(reinterpret_cast<char*>(d_st) +
                                                                offsetof(EpochState, n_children));
+  const size_t graph_after = [] {
+    const char* v = std::getenv("BBS_GRAPH_AFTER");  // epochs before batches run as graphs
+    return v ? static_cast<size_t>(std::atoi(v)) : static_cast<size_t>(24);
+  }();
   bool capturing = false;
   auto record = [&](cudaEvent_t ev) {
     // External: a real record node when captured into the batch graph
@@ -1120,7 +1126,7 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
     }
     const int n_ep = self_active ? E : 1;
     // graphs pay off for long searches (capture + instantiate ~0.2 ms)
-    if (n_ep == E && E > 1 && pass_ms.size() >= 3u * static_cast<size_t>(E)) {
+    if (n_ep == E && E > 1 && pass_ms.size() >= graph_after) {
       if (!batch_exec || batch_qcap != qcap) {
         if (batch_exec) BBS_CUDA(cudaGraphExecDestroy(batch_exec));
         batch_exec = nullptr;

@@ -18,4 +18,4 @@ for i in range(a.searches):
     r = B.search_scan(vm, ds, cfg)
     print(f"search {i}: best {r.best_score} evals {r.stats.nodes_generated} epochs {r.epochs} "
           f"device {r.device_ms:.3f} ms root {r.root_score_ms:.3f} epoch-score {r.epoch_score_ms:.3f} "
-          f"launches {r.kernel_launches} qpeak {r.queue_peak} per-level {list(r.evals_per_level[:8])}", flush=True)
+          f"init {r.stats.initial_nodes_ms:.3f} launches {r.kernel_launches} qpeak {r.queue_peak} per-level {list(r.evals_per_level[:8])}", flush=True)

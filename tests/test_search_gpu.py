@@ -221,3 +221,28 @@ def test_localize_scan_matches_reference(B, ref):
         assert got.best_pose.as_tuple() == want.best_pose.as_tuple()
         assert got.stats.nodes_generated == want.stats.nodes_generated
         assert got.stats.set_source_ms >= 0
+
+
+def test_rotation_cache_is_transparent(B, golden_scenes, monkeypatch):
+    """The flush histogram cache (epoch_cache.cu) and its fallbacks (uncached
+    levels, rotations whose offsets do not de-duplicate) must not change any
+    result: campus (K = 10000 >= the cache threshold) with +-5 deg roll/pitch,
+    so level 0 has > 2^20 rotations and stays uncached while coarser levels
+    are cached."""
+    m, s, _, sc = load_case(B, golden_scenes, "campus")
+    vm = B.MultiResVoxelMap.build(m, sc["r"], sc["max_level"])
+    ds = B.DeviceScan(vm, s)
+    out = {}
+    for flag in ("1", "0"):
+        monkeypatch.setenv("BBS_ROT_CACHE", flag)
+        for strat in ("BFS", "DFS"):
+            cfg = B.SearchConfig(min_resolution=sc["r"], max_level=sc["max_level"],
+                                 roll_pitch_half_range=0.0873, collect_trace=True,
+                                 strategy=B.Strategy[strat])
+            r = B.search_scan(vm, ds, cfg)
+            out[(flag, strat)] = (r.best_score, r.best_pose.as_tuple(), r.stats.nodes_generated,
+                                  r.stats.nodes_pruned, r.stats.batches_flushed, r.best_score_trace,
+                                  tuple(r.evals_per_level))
+    for strat in ("BFS", "DFS"):
+        assert out[("1", strat)] == out[("0", strat)], strat
+    assert out[("1", "BFS")][6][0] > 0  # the search reached the uncached level 0
