@@ -22,8 +22,19 @@ struct BoxParams {
   uint32_t nr, np, nw;        // rotation index counts at the root level
   uint32_t rank, world;       // roots with ref index % world == rank
   uint32_t n_tchunks;         // translation chunks per rotation (grid = nrot * n_tchunks)
-  uint32_t pad;
+  int32_t fpad;               // bound on |voxel offset| of a rotated scan point (d_max / cell + 2)
   double tmax;                // max |translation index| in the box (fast-path guard)
+};
+
+// Padded shared-memory copy of the root level's z-column words for the
+// root column kernel: staged (x, y) in [sx0, sx0 + pitch) x [sy0, sy0 + rows),
+// zeros outside the level box, so entry offsets need no bounds checks.
+struct RootStage {
+  int32_t sx0, sy0;
+  uint32_t pitch, rows;
+  int32_t zoff;               // z0 - level box_min.z
+  uint32_t dimz;              // level z extent (<= 24: words pre-shifted by 8 bits)
+  int enabled;
 };
 
 constexpr int kBoxThreads = 256;

@@ -427,6 +427,8 @@ __global__ void __launch_bounds__(256, 4) score_cube8_kernel(MapView map, GridVi
 //        score(ix, iy, z0 + j) = sum_f count(f) * bit_{fz + z0 + j}(col(fx + ix, fy + iy)).
 //     Ambiguous points are scored exactly per translation.
 constexpr int kHistSlots = 2 * kHistCap;
+constexpr int kColGroupCap = kHistCap / 2;  // groups of 4 (2 int4 each) per rotation
+constexpr int kColPadMax = 160 << 10;       // padded column window, bytes of shared memory
 constexpr int kEntTile = 1024;
 
 __device__ __forceinline__ uint32_t hist_slot(unsigned long long key) {
@@ -435,12 +437,12 @@ __device__ __forceinline__ uint32_t hist_slot(unsigned long long key) {
 
 __global__ void __launch_bounds__(512) root_hist_kernel(GridView grid, ScanView scan, BoxParams bp,
                                                         LevelView L, uint32_t rot_begin,
-                                                        uint32_t rot_end, RootHist h,
+                                                        uint32_t rot_end, RootHist h, RootStage st,
                                                         int32_t* __restrict__ n_overflow) {
   extern __shared__ __align__(16) unsigned char smem[];
   unsigned long long* s_key = reinterpret_cast<unsigned long long*>(smem);  // 64 KB
   int32_t* s_cnt = reinterpret_cast<int32_t*>(s_key + kHistSlots);          // 32 KB
-  __shared__ int s_distinct, s_namb, s_nent, s_skip;
+  __shared__ int s_distinct, s_namb, s_nent, s_skip, s_badpad;
   const uint32_t nrot = bp.nr * bp.np * bp.nw;
   for (uint32_t rot = rot_begin + blockIdx.x; rot < rot_end; rot += gridDim.x) {
     const uint32_t slot = rot - rot_begin;
@@ -462,6 +464,7 @@ __global__ void __launch_bounds__(512) root_hist_kernel(GridView grid, ScanView 
       s_namb = 0;
       s_nent = 0;
       s_skip = 0;
+      s_badpad = 0;
     }
     __syncthreads();
     const uint32_t ir = rot / (bp.np * bp.nw), ip = (rot / bp.nw) % bp.np, iw = rot % bp.nw;
@@ -507,20 +510,70 @@ __global__ void __launch_bounds__(512) root_hist_kernel(GridView grid, ScanView 
       }
     }
     __syncthreads();
-    const bool over = s_skip || s_distinct > kHistCap || s_namb > kAmbCap;
+    bool over = s_skip || s_distinct > kHistCap || s_namb > kAmbCap;
     if (!over) {
-      for (int i = threadIdx.x; i < kHistSlots; i += blockDim.x) {
+      // staged mode (root_colpad_kernel): entries (padded column offset << 8
+      // | z shift + 8) in groups of 4 with their counts packed as bytes
+      // (counts > 255 split), dropping those whose z never meets a
+      // translation's column; otherwise plain (fx, fy, fz, count)
+      int4* ent4 = h.entries + static_cast<uint64_t>(slot) * kHistCap;
+      const int lane = threadIdx.x & 31;
+      for (int i0 = 0; i0 < kHistSlots; i0 += blockDim.x) {
+        const int i = i0 + threadIdx.x;
         const unsigned long long key = s_key[i];
-        if (key != kSlotEmpty) {
-          const int e = atomicAdd(&s_nent, 1);
-          h.entries[static_cast<uint64_t>(slot) * kHistCap + e] =
-              make_int4(static_cast<int32_t>((key >> 42) & 0x1FFFFF) - (1 << 20),
-                        static_cast<int32_t>((key >> 21) & 0x1FFFFF) - (1 << 20),
-                        static_cast<int32_t>(key & 0x1FFFFF) - (1 << 20), s_cnt[i]);
+        int parts = key != kSlotEmpty ? 1 : 0;
+        int32_t fx = 0, fy = 0, fz = 0, sh = 0, cnt = 0;
+        if (parts) {
+          fx = static_cast<int32_t>((key >> 42) & 0x1FFFFF) - (1 << 20);
+          fy = static_cast<int32_t>((key >> 21) & 0x1FFFFF) - (1 << 20);
+          fz = static_cast<int32_t>(key & 0x1FFFFF) - (1 << 20);
+          cnt = s_cnt[i];
+          if (st.enabled) {
+            if (abs(fx) > bp.fpad || abs(fy) > bp.fpad) s_badpad = 1;
+            sh = fz + st.zoff;
+            parts = (sh < static_cast<int32_t>(st.dimz) && sh > -static_cast<int32_t>(bp.nz)) ? (cnt + 254) / 255 : 0;
+          }
+        }
+        int incl = parts;  // warp inclusive scan of the parts
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+          const int v = __shfl_up_sync(0xffffffffu, incl, d);
+          if (lane >= d) incl += v;
+        }
+        const int wtot = __shfl_sync(0xffffffffu, incl, 31);
+        int at = 0;
+        if (lane == 0 && wtot) at = atomicAdd(&s_nent, wtot);
+        at = __shfl_sync(0xffffffffu, at, 0) + incl - parts;
+        if (parts) {
+          if (st.enabled) {
+            const uint32_t word = (static_cast<uint32_t>(fy * static_cast<int32_t>(st.pitch) + fx) << 8) |
+                                  static_cast<uint32_t>(sh + 8);
+            int32_t* g = reinterpret_cast<int32_t*>(ent4);
+            unsigned char* wb = reinterpret_cast<unsigned char*>(ent4);
+            for (int q = 0; q < parts; ++q) {
+              const int e = at + q;
+              if (e >= 4 * kColGroupCap) break;
+              g[(e >> 2) * 8 + (e & 3)] = static_cast<int32_t>(word);
+              wb[((e >> 2) * 8 + 4) * 4 + (e & 3)] = static_cast<unsigned char>(min(255, cnt - 255 * q));
+            }
+          } else {
+            ent4[at] = make_int4(fx, fy, fz, cnt);
+          }
         }
       }
     }
     __syncthreads();
+    // an offset beyond the padding or too many split entries: chunked fallback
+    over = over || s_badpad || (st.enabled && s_nent > 4 * kColGroupCap);
+    if (!over && st.enabled && (s_nent & 3)) {
+      // zero-weight padding of the last group
+      const int e = s_nent + static_cast<int>(threadIdx.x);
+      if (e < ((s_nent + 3) & ~3)) {
+        int32_t* g = reinterpret_cast<int32_t*>(h.entries + static_cast<uint64_t>(slot) * kHistCap);
+        g[(e >> 2) * 8 + (e & 3)] = 8;  // offset 0, shift 8
+        reinterpret_cast<unsigned char*>(g)[((e >> 2) * 8 + 4) * 4 + (e & 3)] = 0;
+      }
+    }
     if (threadIdx.x == 0) {
       h.n_ent[slot] = over ? 0 : s_nent;
       h.n_amb[slot] = over ? 0 : s_namb;
@@ -624,6 +677,113 @@ __global__ void __launch_bounds__(256) root_col_kernel(GridView grid, ScanView s
   }
 }
 
+// Staged variant: the level's z-column words sit zero-padded (and shifted
+// up by 8 bits) in shared memory; entries come in groups of 4 as
+// (padded column offset << 8 | z shift + 8) words plus their counts packed as
+// bytes.  Per group: 4 LDS + 4 funnel shifts give each entry's z-translation
+// bits, 3 PRMT pack their low bytes, and per z-translation j one LOP3 keeps
+// bit j of every byte and one IDP4A adds 2^j * sum(count) of the hits.
+constexpr int kGrpTile = 1024;  // groups per shared-memory tile (16 KB + 4 KB)
+template <int NZ>
+__global__ void __launch_bounds__(256) root_colpad_kernel(GridView grid, ScanView scan, BoxParams bp,
+                                                          LevelView L, uint32_t rot_begin,
+                                                          uint32_t rot_end, RootHist h, RootStage st,
+                                                          uint32_t n_cchunks,
+                                                          int32_t* __restrict__ scores,
+                                                          unsigned long long* probes) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  int4* s_go = reinterpret_cast<int4*>(smem);                     // group offsets/shifts
+  uint32_t* s_gw = reinterpret_cast<uint32_t*>(s_go + kGrpTile);  // group counts (bytes)
+  uint32_t* s_col = s_gw + kGrpTile;
+  const uint32_t nrot = bp.nr * bp.np * bp.nw;
+  const uint32_t dimx = L.dim[0], dimy = L.dim[1];
+  for (uint32_t i = threadIdx.x; i < st.pitch * st.rows; i += blockDim.x) {
+    const int32_t x = st.sx0 + static_cast<int32_t>(i % st.pitch);
+    const int32_t y = st.sy0 + static_cast<int32_t>(i / st.pitch);
+    s_col[i] = (x >= 0 && y >= 0 && x < static_cast<int32_t>(dimx) && y < static_cast<int32_t>(dimy))
+                   ? __ldg(&L.words[static_cast<uint32_t>(y) * dimx + static_cast<uint32_t>(x)]) << 8
+                   : 0u;
+  }
+  __syncthreads();
+  const uint64_t n_items = static_cast<uint64_t>(rot_end - rot_begin) * n_cchunks;
+  for (uint64_t item = blockIdx.x; item < n_items; item += gridDim.x) {
+    const uint32_t slot = static_cast<uint32_t>(item / n_cchunks);
+    const uint32_t rot = rot_begin + slot;
+    const uint32_t cc = static_cast<uint32_t>(item % n_cchunks);
+    if (h.overflow[slot]) continue;  // uniform per CTA
+    uint32_t P, x0r;
+    if (!owned_slabs(bp, nrot, rot, &P, &x0r)) continue;
+    const uint32_t n_own_x = x0r < bp.nx ? (bp.nx - x0r + P - 1) / P : 0;
+    const uint64_t ncols = static_cast<uint64_t>(n_own_x) * bp.ny;
+    const uint64_t col0 = static_cast<uint64_t>(cc) * blockDim.x;
+    if (col0 >= ncols) continue;
+    const uint64_t c = col0 + threadIdx.x;
+    const bool valid = c < ncols;
+    const uint32_t ix_rel = valid ? x0r + static_cast<uint32_t>(c / bp.ny) * P : x0r;
+    const uint32_t iy_rel = valid ? static_cast<uint32_t>(c % bp.ny) : 0u;
+    const int32_t ix = bp.x0 + static_cast<int32_t>(ix_rel), iy = bp.y0 + static_cast<int32_t>(iy_rel);
+    // padded index of the translation's own column
+    const int32_t base = (iy - L.box_min[1] - st.sy0) * static_cast<int32_t>(st.pitch) +
+                         (ix - L.box_min[0] - st.sx0);
+    uint32_t acc[NZ];
+#pragma unroll
+    for (int j = 0; j < NZ; ++j) acc[j] = 0;
+    const int n_grp = (h.n_ent[slot] + 3) >> 2;
+    const int4* __restrict__ grp = h.entries + static_cast<uint64_t>(slot) * kHistCap;
+    for (int t0 = 0; t0 < n_grp; t0 += kGrpTile) {
+      const int tn = min(kGrpTile, n_grp - t0);
+      __syncthreads();
+      for (int i = threadIdx.x; i < tn; i += blockDim.x) {
+        s_go[i] = grp[2 * (t0 + i)];
+        s_gw[i] = static_cast<uint32_t>(grp[2 * (t0 + i) + 1].x);
+      }
+      __syncthreads();
+#pragma unroll 2
+      for (int g = 0; g < tn; ++g) {
+        const int4 o = s_go[g];
+        const uint32_t w4 = s_gw[g];
+        // shift amounts ride in the low 5 bits (wrap funnel shift)
+        const uint32_t b0 = __funnelshift_r(s_col[base + (o.x >> 8)], 0u, static_cast<uint32_t>(o.x));
+        const uint32_t b1 = __funnelshift_r(s_col[base + (o.y >> 8)], 0u, static_cast<uint32_t>(o.y));
+        const uint32_t b2 = __funnelshift_r(s_col[base + (o.z >> 8)], 0u, static_cast<uint32_t>(o.z));
+        const uint32_t b3 = __funnelshift_r(s_col[base + (o.w >> 8)], 0u, static_cast<uint32_t>(o.w));
+        const uint32_t x = __byte_perm(__byte_perm(b0, b1, 0x0040), __byte_perm(b2, b3, 0x0040), 0x5410);
+#pragma unroll
+        for (int j = 0; j < NZ; ++j) acc[j] = __dp4a(x & (0x01010101u << j), w4, acc[j]);
+      }
+    }
+    int res[NZ];
+#pragma unroll
+    for (int j = 0; j < NZ; ++j) res[j] = static_cast<int>(acc[j] >> j);
+    const int n_amb = h.n_amb[slot];
+    if (valid && n_amb) {
+      const uint32_t ir = rot / (bp.np * bp.nw), ip = (rot / bp.nw) % bp.np, iw = rot % bp.nw;
+      double R[9];
+      rotation_of(grid, bp.level, static_cast<int>(ir), static_cast<int>(ip), static_cast<int>(iw), R);
+      for (int a = 0; a < n_amb; ++a) {
+        const uint32_t p = h.amb[static_cast<uint64_t>(slot) * kAmbCap + a];
+        const double px = scan.x[p], py = scan.y[p], pz = scan.z[p];
+        const double rx = rot_row(R[0], R[1], R[2], px, py, pz);
+        const double ry = rot_row(R[3], R[4], R[5], px, py, pz);
+        const double rz = rot_row(R[6], R[7], R[8], px, py, pz);
+#pragma unroll
+        for (int j = 0; j < NZ; ++j)
+          if (j < static_cast<int>(bp.nz)) res[j] += exact_hit(L, rx, ry, rz, ix, iy, bp.z0 + j);
+      }
+    }
+    if (valid) {
+      const uint64_t obase = (static_cast<uint64_t>(ix_rel) * bp.ny + iy_rel) * bp.nz;
+#pragma unroll
+      for (int j = 0; j < NZ; ++j)
+        if (j < static_cast<int>(bp.nz)) scores[(obase + j) * nrot + rot] = res[j];
+    }
+    if (threadIdx.x == 0 && probes) {
+      const uint64_t nc = min(static_cast<uint64_t>(blockDim.x), ncols - col0);
+      atomicAdd(probes, static_cast<unsigned long long>(nc) * (h.n_ent[slot] + n_amb) * bp.nz);
+    }
+  }
+}
+
 __global__ void rotation_key_kernel(const bbs_node* __restrict__ nodes, uint64_t n, GridView G,
                                     unsigned long long* __restrict__ keys,
                                     uint32_t* __restrict__ idx) {
@@ -698,6 +858,19 @@ void launch_score_box_chunked(const MapView& map, const GridView& grid, const Sc
   BBS_CUDA(cudaGetLastError());
 }
 
+int colpad_ctas_per_sm(uint32_t nz, int smem) {
+  int n = 1;
+  switch (nz) {
+#define BBS_OCC(NZ_)                                                                               \
+  case NZ_:                                                                                        \
+    BBS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, root_colpad_kernel<NZ_>, 256, smem)); \
+    break;
+    BBS_OCC(1) BBS_OCC(2) BBS_OCC(3) BBS_OCC(4) BBS_OCC(5) BBS_OCC(6) BBS_OCC(7) BBS_OCC(8)
+#undef BBS_OCC
+  }
+  return std::max(n, 1);
+}
+
 void launch_score_roots(const MapView& map, const GridView& grid, const ScanView& scan,
                         const BoxParams& bp, const RootHist& hist, int32_t* scores,
                         unsigned long long* probes, cudaStream_t s) {
@@ -721,11 +894,39 @@ void launch_score_roots(const MapView& map, const GridView& grid, const ScanView
                                   kEntTile * 16 + col_stage_max));
     BBS_CUDA(cudaFuncSetAttribute(root_col_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   kEntTile * 16 + col_stage_max));
+#define BBS_COLPAD_ATTR(NZ_)                                                                      \
+  BBS_CUDA(cudaFuncSetAttribute(root_colpad_kernel<NZ_>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                kGrpTile * 20 + kColPadMax));
+    BBS_COLPAD_ATTR(1) BBS_COLPAD_ATTR(2) BBS_COLPAD_ATTR(3) BBS_COLPAD_ATTR(4) BBS_COLPAD_ATTR(5)
+    BBS_COLPAD_ATTR(6) BBS_COLPAD_ATTR(7) BBS_COLPAD_ATTR(8)
+#undef BBS_COLPAD_ATTR
     attr_done = true;
   }
   const uint64_t col_bytes = static_cast<uint64_t>(L.dim[0]) * L.dim[1] * 4ull;
   const int stage = col_bytes <= static_cast<uint64_t>(col_stage_max) ? 1 : 0;
   const int col_smem = kEntTile * 16 + (stage ? static_cast<int>(col_bytes) : 0);
+  // padded staging: the staged window covers every translation column plus
+  // the largest voxel offset on each side
+  RootStage st{};
+  {
+    const int64_t R = bp.fpad;
+    const int64_t xo0 = static_cast<int64_t>(bp.x0) - L.box_min[0], xo1 = xo0 + bp.nx - 1;
+    const int64_t yo0 = static_cast<int64_t>(bp.y0) - L.box_min[1], yo1 = yo0 + bp.ny - 1;
+    const int64_t sx0 = std::min<int64_t>(0, xo0) - R, sx1 = std::max<int64_t>(L.dim[0], xo1 + 1) + R;
+    const int64_t sy0 = std::min<int64_t>(0, yo0) - R, sy1 = std::max<int64_t>(L.dim[1], yo1 + 1) + R;
+    const int64_t words = (sx1 - sx0) * (sy1 - sy0);
+    if (bp.nz <= 8 && L.dim[2] <= 24 && R < (1 << 15) && words * 4 <= kColPadMax &&
+        std::getenv("BBS_ROOT_PAD") == nullptr) {
+      st.enabled = 1;
+      st.sx0 = static_cast<int32_t>(sx0);
+      st.sy0 = static_cast<int32_t>(sy0);
+      st.pitch = static_cast<uint32_t>(sx1 - sx0);
+      st.rows = static_cast<uint32_t>(sy1 - sy0);
+      st.zoff = bp.z0 - L.box_min[2];
+      st.dimz = L.dim[2];
+    }
+  }
+  const int pad_smem = kGrpTile * 20 + static_cast<int>(st.pitch * st.rows * 4);
   uint32_t P, x0r;
   BoxParams b0 = bp;
   b0.rank = 0;
@@ -737,11 +938,24 @@ void launch_score_roots(const MapView& map, const GridView& grid, const ScanView
     const uint32_t re = std::min<uint32_t>(nrot, rb + kRotBatch);
     BBS_CUDA(cudaMemsetAsync(hist.overflow + kRotBatch, 0, sizeof(int32_t), s));  // n_overflow
     root_hist_kernel<<<std::min<uint32_t>(re - rb, 148 * 4), 512, hist_smem, s>>>(
-        grid, scan, bp, L, rb, re, hist, hist.overflow + kRotBatch);
+        grid, scan, bp, L, rb, re, hist, st, hist.overflow + kRotBatch);
     BBS_CUDA(cudaGetLastError());
     const uint64_t items = static_cast<uint64_t>(re - rb) * n_cchunks;
     const unsigned g = static_cast<unsigned>(std::min<uint64_t>(std::max<uint64_t>(items, 1), 148ull * 16));
-    if (bp.nz <= 8)
+    if (st.enabled) {
+      // persistent grid: every CTA stages the padded window once
+      const unsigned gp = std::min<unsigned>(g, 148u * static_cast<unsigned>(colpad_ctas_per_sm(bp.nz, pad_smem)));
+      switch (bp.nz) {
+#define BBS_COLPAD(NZ_)                                                                              \
+  case NZ_:                                                                                          \
+    root_colpad_kernel<NZ_><<<gp, 256, pad_smem, s>>>(grid, scan, bp, L, rb, re, hist, st, n_cchunks, \
+                                                     scores, probes);                                \
+    break;
+        BBS_COLPAD(1) BBS_COLPAD(2) BBS_COLPAD(3) BBS_COLPAD(4) BBS_COLPAD(5) BBS_COLPAD(6)
+        BBS_COLPAD(7) BBS_COLPAD(8)
+#undef BBS_COLPAD
+      }
+    } else if (bp.nz <= 8)
       root_col_kernel<8><<<g, 256, col_smem, s>>>(grid, scan, bp, L, rb, re, hist, n_cchunks, stage,
                                                   scores, probes);
     else if (bp.nz <= 16)

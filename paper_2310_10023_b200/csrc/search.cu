@@ -868,6 +868,7 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
   bp.nw = static_cast<uint32_t>(nw);
   bp.rank = static_cast<uint32_t>(rank);
   bp.world = static_cast<uint32_t>(world);
+  bp.fpad = static_cast<int32_t>(std::min(std::ceil(scan->d_max / m->view.level[L].cell) + 2.0, 1e6));
   const uint32_t nrot = bp.nr * bp.np * bp.nw;
   uint64_t n_own = 0;  // roots owned by this rank
   {
