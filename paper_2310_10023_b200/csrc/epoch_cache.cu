@@ -86,7 +86,7 @@ __global__ void __launch_bounds__(kBuildThreads) cache_build_kernel(RotCache c, 
   uint32_t* s_amb = reinterpret_cast<uint32_t*>(s_cnt + kCacheHashSlots);    // 8 KB
   using ScanI = cub::BlockScan<int, kBuildThreads>;
   __shared__ typename ScanI::TempStorage s_scan;
-  __shared__ int s_distinct, s_namb;
+  __shared__ int s_distinct, s_namb, s_oob;
   __shared__ uint32_t s_off, s_aoff;
   const int lane = threadIdx.x & 31;
   const uint32_t n_build = c.ctl[2];
@@ -98,13 +98,24 @@ __global__ void __launch_bounds__(kBuildThreads) cache_build_kernel(RotCache c, 
     const double tmax = c.tmax[l];
     double R[9];
     rotation_of(G, l, bd.z, bd.w, c.builds_w[bi], R);
-    for (int i = threadIdx.x; i < kCacheHashSlots; i += blockDim.x) {
-      s_key[i] = kEmptyKey;
-      s_cnt[i] = 0;
+    // dense box (coarse levels): direct-mapped 16-bit counters, no probing
+    const int dr = c.dn_r[l];
+    const bool dense = dr > 0;
+    const int dzlo = c.dn_zlo[l], dxy = 2 * dr + 1;
+    const int ncells = dense ? dxy * dxy * c.dn_nz[l] : 0;
+    uint32_t* s_w = reinterpret_cast<uint32_t*>(smem);  // overlays the hash table
+    if (dense) {
+      for (int i = threadIdx.x; i < (ncells + 1) >> 1; i += blockDim.x) s_w[i] = 0u;
+    } else {
+      for (int i = threadIdx.x; i < kCacheHashSlots; i += blockDim.x) {
+        s_key[i] = kEmptyKey;
+        s_cnt[i] = 0;
+      }
     }
     if (threadIdx.x == 0) {
       s_distinct = 0;
       s_namb = 0;
+      s_oob = 0;
     }
     __syncthreads();
     // all lanes stay in the loop together (warp-aggregated inserts below)
@@ -120,7 +131,7 @@ __global__ void __launch_bounds__(kBuildThreads) cache_build_kernel(RotCache c, 
         py[h] = live ? scan.y[p[h]] : 0.0;
         pz[h] = live ? scan.z[p[h]] : 0.0;
       }
-      if (s_distinct >= kCacheHashCap) {  // uniform: read after the step barrier
+      if (!dense && s_distinct >= kCacheHashCap) {  // uniform: read after the step barrier
         aborted = true;
         break;
       }
@@ -141,6 +152,20 @@ __global__ void __launch_bounds__(kBuildThreads) cache_build_kernel(RotCache c, 
           }
         }
         const bool ins = live && ok;
+        if (dense) {
+          int idx = -1;
+          if (ins) {
+            const int zz = fz - dzlo;
+            if (fx >= -dr && fx <= dr && fy >= -dr && fy <= dr && zz >= 0 && zz < c.dn_nz[l])
+              idx = (zz * dxy + (fy + dr)) * dxy + (fx + dr);
+            else
+              s_oob = 1;  // outside the box: this build gives up (cube kernel scores its runs)
+          }
+          const unsigned same = __match_any_sync(0xffffffffu, idx);
+          if (idx >= 0 && (__ffs(same) - 1) == lane)
+            atomicAdd(&s_w[idx >> 1], static_cast<uint32_t>(__popc(same)) << ((idx & 1) << 4));
+          continue;
+        }
         const unsigned long long key = ins ? (static_cast<unsigned long long>(fx + (1 << 20)) << 42) |
                                                  (static_cast<unsigned long long>(fy + (1 << 20)) << 21) |
                                                  static_cast<unsigned long long>(fz + (1 << 20))
@@ -165,32 +190,50 @@ __global__ void __launch_bounds__(kBuildThreads) cache_build_kernel(RotCache c, 
         const int nf = __reduce_add_sync(0xffffffffu, fresh);
         if (lane == 0 && nf) atomicAdd(&s_distinct, nf);
       }
-      __syncthreads();
+      if (!dense) __syncthreads();
     }
+    __syncthreads();
     // too many distinct offsets (fine levels: about one per point): the
     // histogram would not beat direct scoring, so give the level up
     const bool raw = aborted;  // (a finished table holds <= cap + one step < slots)
+    const bool oob = s_oob != 0;
     const int namb = s_namb;
-    // distinct entries in slot order (block scan; deterministic layout)
+    // entries in slot / cell order (block scan; deterministic layout)
     constexpr int kPer = kCacheHashSlots / kBuildThreads;
+    const int dper = (ncells + kBuildThreads - 1) / kBuildThreads;
+    const int dc0 = min(ncells, static_cast<int>(threadIdx.x) * dper), dc1 = min(ncells, dc0 + dper);
+    auto dcount = [&](int i) { return (s_w[i >> 1] >> ((i & 1) << 4)) & 0xFFFFu; };
     int cnt = 0;
-    if (!raw) {
+    if (dense) {
+      if (!oob)
+        for (int i = dc0; i < dc1; ++i) cnt += dcount(i) != 0u ? 1 : 0;
+    } else if (!raw) {
 #pragma unroll
       for (int k = 0; k < kPer; ++k) cnt += s_key[threadIdx.x * kPer + k] != kEmptyKey ? 1 : 0;
     }
     int epos, n_dist;
     ScanI(s_scan).ExclusiveSum(cnt, epos, n_dist);
-    const uint32_t n_ent = raw ? 0u : static_cast<uint32_t>(n_dist);
+    const uint32_t n_ent = (raw || oob) ? 0u : static_cast<uint32_t>(n_dist);
     if (threadIdx.x == 0) {
-      s_off = raw ? 0u : atomicAdd(&c.ctl[0], n_ent);
-      s_aoff = raw ? 0u : atomicAdd(&c.ctl[1], static_cast<uint32_t>(namb));
+      s_off = (raw || oob) ? 0u : atomicAdd(&c.ctl[0], n_ent);
+      s_aoff = (raw || oob) ? 0u : atomicAdd(&c.ctl[1], static_cast<uint32_t>(namb));
       if (raw) c.ctl[4 + (l & (kMaxLevels - 1))] = 1u;
     }
     __syncthreads();
     const uint32_t off = s_off, aoff = s_aoff;
-    const bool fits = !raw && namb <= kCacheAmbCap && static_cast<uint64_t>(off) + n_ent <= c.pool_cap &&
+    const bool fits = !raw && !oob && namb <= kCacheAmbCap &&
+                      static_cast<uint64_t>(off) + n_ent <= c.pool_cap &&
                       static_cast<uint64_t>(aoff) + namb <= c.amb_cap;
-    if (fits) {
+    if (fits && dense) {
+      for (int i = dc0; i < dc1; ++i) {
+        const uint32_t v = dcount(i);
+        if (v) {
+          const int fx = i % dxy - dr, fy = (i / dxy) % dxy - dr, fz = i / (dxy * dxy) + dzlo;
+          c.pool[off + epos] = make_int4(fx, fy, fz, static_cast<int32_t>(v));
+          ++epos;
+        }
+      }
+    } else if (fits) {
 #pragma unroll
       for (int k = 0; k < kPer; ++k) {
         const int i = threadIdx.x * kPer + k;
@@ -202,8 +245,9 @@ __global__ void __launch_bounds__(kBuildThreads) cache_build_kernel(RotCache c, 
           ++epos;
         }
       }
-      for (int a = threadIdx.x; a < namb; a += blockDim.x) c.amb_pool[aoff + a] = s_amb[a];
     }
+    if (fits)
+      for (int a = threadIdx.x; a < namb; a += blockDim.x) c.amb_pool[aoff + a] = s_amb[a];
     __syncthreads();
     if (threadIdx.x == 0) {
       c.amb_off[slot] = aoff;

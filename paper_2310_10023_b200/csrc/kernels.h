@@ -107,6 +107,7 @@ void launch_score_runs8(const MapView& map, const GridView& grid, const ScanView
 // entries, ambiguous points}; slot = base[level] + dense rotation id.
 constexpr int32_t kCacheEmpty = -1, kCacheBuilding = -2, kCacheNone = -3, kCacheReady = 0;
 constexpr int kCacheCtl = 4 + kMaxLevels;
+constexpr int kCacheDenseCells = 48 * 1024;  // 96 KB of 16-bit counters
 struct RotCache {
   int enabled;
   uint32_t base[kMaxLevels];   // 0xFFFFFFFF: level not cached
@@ -118,6 +119,9 @@ struct RotCache {
   uint32_t* ctl;               // [kCacheCtl] pool used, amb used, builds this flush,
                                // fallback runs this flush, then per-level "raw" flags
   uint32_t* fb_runs;           // [max runs] runs the cube kernel scores (not cached)
+  // dense-histogram box per level (dn_r = 0: hash build): offsets in
+  // [-r, r]^2 x [zlo, zlo + nz), two 16-bit counts per shared word
+  int32_t dn_r[kMaxLevels], dn_zlo[kMaxLevels], dn_nz[kMaxLevels];
   int4* builds;                // [max runs] (slot, level, iroll, ipitch)
   int32_t* builds_w;           // [max runs] iyaw
   uint64_t pool_cap, amb_cap;

@@ -771,6 +771,12 @@ bbs_scan* upload_scan(bbs_map* m, const double* xyz, uint64_t k) {
   sc->k = k;
   sc->host.assign(xyz, xyz + 3 * k);
   sc->d_max = k ? host_max_range(xyz, k) : 0.0;
+  for (uint64_t i = 0; i < k; ++i) {
+    const double x = xyz[3 * i], y = xyz[3 * i + 1], z = xyz[3 * i + 2];
+    sc->z_min = i ? std::min(sc->z_min, z) : z;
+    sc->z_max = i ? std::max(sc->z_max, z) : z;
+    sc->l1xy_max = std::max(sc->l1xy_max, std::fabs(x) + std::fabs(y));
+  }
   cudaStream_t s = m->stream;
   sc->soa = dalloc<double>(3 * std::max<uint64_t>(k, 1), s);
   if (k) {
@@ -1019,6 +1025,24 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
       if (n_rot <= (1ull << 20) && slots + n_rot <= (1ull << 23) && cache.tmax[l] < 0x1p28) {
         cache.base[l] = static_cast<uint32_t>(slots);
         slots += n_rot;
+        // dense histogram box: |fx|, |fy| <= d_max / cell + 2; the rotated z
+        // of a point moves by at most sin(t)(|x| + |y|) + (1 - cos^2 t)|z|
+        // for roll/pitch within t (third row of Rz Ry Rx is yaw-free).  A
+        // point outside the box makes that build fall back (never wrong).
+        const double cell = m->view.level[l].cell;
+        const double t = std::fabs(cfg.roll_pitch_half_range) + 1e-6;
+        const double zabs = std::max(std::fabs(scan->z_min), std::fabs(scan->z_max));
+        const double dz = std::sin(t) * scan->l1xy_max + (1.0 - std::cos(t) * std::cos(t)) * zabs + 1e-6 * (1.0 + d_max);
+        const double r = std::floor(scan->d_max / cell) + 2.0;
+        const double zlo = std::floor((scan->z_min - dz) / cell) - 1.0;
+        const double zhi = std::floor((scan->z_max + dz) / cell) + 1.0;
+        const double cells = (2.0 * r + 1.0) * (2.0 * r + 1.0) * (zhi - zlo + 1.0);
+        if (cells <= static_cast<double>(kCacheDenseCells) && K < 65536 && t < 0.5 &&
+            std::getenv("BBS_DENSE_HIST") == nullptr) {
+          cache.dn_r[l] = static_cast<int32_t>(r);
+          cache.dn_zlo[l] = static_cast<int32_t>(zlo);
+          cache.dn_nz[l] = static_cast<int32_t>(zhi - zlo + 1.0);
+        }
       }
     }
     if (slots > 0) {
