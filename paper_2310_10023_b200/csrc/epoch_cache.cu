@@ -39,39 +39,6 @@ __device__ __forceinline__ uint32_t cache_hash(unsigned long long key) {
   return static_cast<uint32_t>((key * 0x9E3779B97F4A7C15ull) >> 51);  // 13 bits
 }
 
-__device__ __forceinline__ bool run_slot(const RotCache& c, const GridView& G, const int4& a,
-                                         const int4& b, uint32_t* slot) {
-  // a = (ix, iy, iz, iroll) of child 0, b = (ipitch, iyaw, level, score)
-  const int l = b.z;
-  const uint32_t base = c.base[l];
-  if (base == 0xFFFFFFFFu) return false;
-  const uint32_t np = static_cast<uint32_t>(G.max_index[l * 3 + 1]) + 1;
-  const uint32_t nw = static_cast<uint32_t>(G.max_index[l * 3 + 2]) + 1;
-  *slot = base + (static_cast<uint32_t>(a.w) * np + static_cast<uint32_t>(b.x)) * nw +
-          static_cast<uint32_t>(b.y);
-  return true;
-}
-
-__global__ void cache_claim_kernel(RotCache c, GridView G, const bbs_node* __restrict__ pending,
-                                   const uint32_t* __restrict__ d_n) {
-  const uint32_t n_runs = *d_n / 8;
-  for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < n_runs; r += gridDim.x * blockDim.x) {
-    const int4 a = __ldg(reinterpret_cast<const int4*>(pending) + 16ull * r);
-    const int4 b = __ldg(reinterpret_cast<const int4*>(pending) + 16ull * r + 1);
-    uint32_t slot;
-    if (!run_slot(c, G, a, b, &slot)) continue;  // uncached level: the cube kernel scores it
-    if (c.info[slot].x != kCacheEmpty) continue;
-    // the level's offsets do not de-duplicate: a build would cost more than
-    // it saves, the cube kernel scores the run directly
-    if (c.ctl[4 + (b.z & (kMaxLevels - 1))]) continue;
-    if (atomicCAS(&c.info[slot].x, kCacheEmpty, kCacheBuilding) == kCacheEmpty) {
-      const uint32_t i = atomicAdd(&c.ctl[2], 1u);
-      c.builds[i] = make_int4(static_cast<int32_t>(slot), b.z, a.w, b.x);  // slot, level, ir, ip
-      c.builds_w[i] = b.y;                                                 // iw
-    }
-  }
-}
-
 constexpr int kBuildThreads = 512;
 
 // One CTA per claimed (level, rotation): rotate + floor every scan point
@@ -404,9 +371,8 @@ void launch_epoch_score(const MapView& map, const GridView& grid, const ScanView
     attr_done = true;
   }
   const uint32_t max_runs = (n_max + 7) / 8;
-  BBS_CUDA(cudaMemsetAsync(cache.ctl + 2, 0, 2 * sizeof(uint32_t), s));  // builds, fallback runs
-  cache_claim_kernel<<<(max_runs + 255) / 256, 256, 0, s>>>(cache, grid, pending, d_n);
-  BBS_CUDA(cudaGetLastError());
+  // the epoch's branch kernel already claimed the slots (cache_claim_run)
+  // after its frontier reset ctl[2..3]
   cache_build_kernel<<<std::min<uint32_t>(std::max<uint32_t>(max_runs, 1), 148 * 2), kBuildThreads, build_smem, s>>>(
       cache, map, grid, scan);
   BBS_CUDA(cudaGetLastError());

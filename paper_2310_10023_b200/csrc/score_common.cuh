@@ -78,4 +78,37 @@ __device__ __forceinline__ void cube_probe(const LevelView& L, uint32_t ux, uint
   }
 }
 
+// ---- per-search rotation cache (epoch_cache.cu) ----------------------------
+__device__ __forceinline__ bool run_slot(const RotCache& c, const GridView& G, const int4& a,
+                                         const int4& b, uint32_t* slot) {
+  // a = (ix, iy, iz, iroll) of child 0, b = (ipitch, iyaw, level, score)
+  const int l = b.z;
+  const uint32_t base = c.base[l];
+  if (base == 0xFFFFFFFFu) return false;
+  const uint32_t np = static_cast<uint32_t>(G.max_index[l * 3 + 1]) + 1;
+  const uint32_t nw = static_cast<uint32_t>(G.max_index[l * 3 + 2]) + 1;
+  *slot = base + (static_cast<uint32_t>(a.w) * np + static_cast<uint32_t>(b.x)) * nw +
+          static_cast<uint32_t>(b.y);
+  return true;
+}
+
+
+// Claim one run's (level, rotation) slot for a build in this flush (called
+// by the branch kernel for the first child of every run).  a/b are the run's
+// first child as int4 pairs: (ix, iy, iz, iroll), (ipitch, iyaw, level, score).
+__device__ __forceinline__ void cache_claim_run(const RotCache& c, const GridView& G, const int4& a,
+                                                const int4& b) {
+  uint32_t slot;
+  if (!run_slot(c, G, a, b, &slot)) return;  // uncached level: the cube kernel scores it
+  if (c.info[slot].x != kCacheEmpty) return;
+  // the level's offsets do not de-duplicate: a build would cost more than it
+  // saves, the cube kernel scores the run directly
+  if (c.ctl[4 + (b.z & (kMaxLevels - 1))]) return;
+  if (atomicCAS(&c.info[slot].x, kCacheEmpty, kCacheBuilding) == kCacheEmpty) {
+    const uint32_t i = atomicAdd(&c.ctl[2], 1u);
+    c.builds[i] = make_int4(static_cast<int32_t>(slot), b.z, a.w, b.x);  // slot, level, ir, ip
+    c.builds_w[i] = b.y;                                                 // iw
+  }
+}
+
 }  // namespace bbs

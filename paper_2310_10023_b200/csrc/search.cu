@@ -30,6 +30,7 @@
 #include "bbs_map_impl.h"
 #include "device_common.cuh"
 #include "kernels.h"
+#include "score_common.cuh"
 
 namespace bbs {
 
@@ -55,7 +56,7 @@ struct EpochState {
   uint32_t q_peak;
   uint32_t n_keep;         // queue remainder kept after the incumbent trim
   uint32_t surv_ticket;    // survivors tile tickets (reset by the frontier)
-  uint32_t pad2;
+  uint32_t merge_done;     // merge CTAs finished (the last one finalizes the epoch)
   unsigned long long level_evals[kMaxLevels];  // flush evaluations per level
   // kept ranges of the remainder: one per key segment (BFS: 1, DFS: level)
   uint32_t seg_lo[kMaxLevels], seg_len[kMaxLevels], seg_pre[kMaxLevels + 1];
@@ -105,7 +106,7 @@ __global__ void __launch_bounds__(kFT) frontier_kernel(EpochState* st, Queue q, 
                                                        uint32_t* __restrict__ exp_off,
                                                        int32_t* __restrict__ trace,
                                                        unsigned long long trace_cap,
-                                                       int strategy) {
+                                                       int strategy, uint32_t* __restrict__ cache_ctl) {
   using ScanI = cub::BlockScan<int, kFT>;
   using ScanU = cub::BlockScan<unsigned long long, kFT>;
   using RedI = cub::BlockReduce<int, kFT>;
@@ -254,6 +255,10 @@ __global__ void __launch_bounds__(kFT) frontier_kernel(EpochState* st, Queue q, 
   }
   __syncthreads();
   const unsigned long long pruned_all = cub::BlockReduce<unsigned long long, kFT>(tmp.ru).Sum(pruned);
+  if (tid == 0 && cache_ctl) {
+    cache_ctl[2] = 0;  // builds claimed this flush
+    cache_ctl[3] = 0;  // runs listed for the cube kernel
+  }
   if (tid == 0) {
     st->surv_ticket = 0;
     st->nodes_pruned += pruned_all;
@@ -285,7 +290,8 @@ __global__ void __launch_bounds__(kFT) frontier_kernel(EpochState* st, Queue q, 
 // pop order, each parent's children in (jr, jp, jw, jx, jy, jz) order.
 __global__ void branch_kernel(const EpochState* st, Queue q, GridView G,
                               const uint32_t* __restrict__ exp_parent,
-                              const uint32_t* __restrict__ exp_off, bbs_node* __restrict__ pending) {
+                              const uint32_t* __restrict__ exp_off, bbs_node* __restrict__ pending,
+                              int32_t* __restrict__ pscores, RotCache cache) {
   const uint32_t n = st->n_children;
   if (n == 0) return;
   const uint32_t ne = st->n_expand;
@@ -317,6 +323,12 @@ __global__ void branch_kernel(const EpochState* st, Queue q, GridView G,
     ch.level = p.level - 1;
     ch.score = -1;
     pending[i] = ch;
+    pscores[i] = 0;  // the flush kernels accumulate into it
+    // first child of a run (8 translation siblings): claim its rotation's
+    // histogram slot (epoch_cache.cu)
+    if (cache.enabled && t == 0)
+      cache_claim_run(cache, G, make_int4(ch.ix, ch.iy, ch.iz, ch.iroll),
+                      make_int4(ch.ipitch, ch.iyaw, ch.level, ch.score));
   }
 }
 
@@ -514,7 +526,7 @@ __global__ void __launch_bounds__(kRT) rank_sort_kernel(const EpochState* st,
 
 // E6: merge the sorted survivors into the trimmed queue remainder (push,
 // search.hpp:139).  The remainder is read through the kept segment ranges.
-__global__ void merge_kernel(const EpochState* st, Queue q, int strategy,
+__global__ void merge_kernel(EpochState* st, Queue q, int strategy,
                              const unsigned long long* __restrict__ skey,
                              const bbs_node* __restrict__ snode) {
   __shared__ uint32_t s_lo[kMaxLevels], s_len[kMaxLevels], s_pre[kMaxLevels + 1];
@@ -554,17 +566,24 @@ __global__ void merge_kernel(const EpochState* st, Queue q, int strategy,
       on[pos] = snode[j];
     }
   }
+  // E7 (last CTA): swap queue buffers; the loop ends when queue and pending
+  // are empty
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(&st->merge_done, 1u) == gridDim.x - 1) {
+      __threadfence();
+      const uint32_t len = n_keep + n_s;
+      st->q_len = len;
+      st->cur ^= 1u;
+      st->q_peak = max(st->q_peak, len);
+      if (len == 0) st->active = 0;
+      st->merge_done = 0;
+    }
+  }
 }
 
-// E7: swap queue buffers; the loop ends when queue and pending are empty.
-__global__ void finalize_kernel(EpochState* st) {
-  if (st->n_children == 0) return;
-  const uint32_t len = st->n_keep + st->n_surv;
-  st->q_len = len;
-  st->cur ^= 1u;
-  st->q_peak = max(st->q_peak, len);
-  if (len == 0) st->active = 0;
-}
+
 
 // Root survivors -> queue entries (seq = rank in initial_nodes order).  All
 // roots share one level, so the queue order is (score desc, seq asc) for BFS
@@ -1087,12 +1106,12 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
   // one flush epoch (frontier -> branch -> score -> survivors -> sort -> merge)
   auto enqueue_epoch = [&](int e) {
     frontier_kernel<<<1, kFT, 0, s>>>(d_st, q, gv, cfg.batch_size, exp_parent, exp_off, d_trace,
-                                      trace_cap, strategy);
+                                      trace_cap, strategy, cache.enabled ? cache.ctl : nullptr);
     BBS_CUDA(cudaGetLastError());
     record(ev_pass[e]);
-    branch_kernel<<<grid1(pend_cap), 256, 0, s>>>(d_st, q, gv, exp_parent, exp_off, pending);
+    branch_kernel<<<grid1(pend_cap), 256, 0, s>>>(d_st, q, gv, exp_parent, exp_off, pending, pscores,
+                                                  cache);
     BBS_CUDA(cudaGetLastError());
-    BBS_CUDA(cudaMemsetAsync(pscores, 0, pend_cap * sizeof(int32_t), s));
     record(ev_s0[e]);
     launch_epoch_score(m->view, gv, sv, pending, d_nchild, static_cast<uint32_t>(pend_cap), ptiles,
                        pscores, cache, s);
@@ -1104,9 +1123,7 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
     BBS_CUDA(cudaGetLastError());
     merge_kernel<<<grid1(qcap), 256, 0, s>>>(d_st, q, strategy, s_key2, s_node2);
     BBS_CUDA(cudaGetLastError());
-    finalize_kernel<<<1, 1, 0, s>>>(d_st);
-    BBS_CUDA(cudaGetLastError());
-    launches += 7;  // frontier, branch, score, survivors, rank_sort, merge, finalize
+    launches += 6;  // frontier, branch, score, survivors, rank_sort, merge (+ finalize)
   };
   // E epochs as one CUDA graph (all sizes live in EpochState, so the graph is
   // valid until the queue buffers are re-allocated)
@@ -1168,7 +1185,7 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
         batch_qcap = qcap;
       }
       BBS_CUDA(cudaGraphLaunch(batch_exec, s));
-      launches += 7ull * E;
+      launches += 6ull * E;
     } else {
       for (int e = 0; e < n_ep; ++e) enqueue_epoch(e);
     }
