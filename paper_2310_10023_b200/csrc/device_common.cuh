@@ -65,4 +65,10 @@ __device__ __forceinline__ bool level_contains(const LevelView& L, int32_t x, in
   }
 }
 
+// Programmatic dependent launch (launch_pdl): wait for the preceding grid
+// (complete, memory visible) before reading its output; let the next grid
+// launch once every CTA of this one has started.  No-ops without PDL.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 }  // namespace bbs

@@ -47,6 +47,8 @@ constexpr int kBuildThreads = 512;
 // points per thread per step keep two load/rotate chains in flight.
 __global__ void __launch_bounds__(kBuildThreads) cache_build_kernel(RotCache c, MapView map, GridView G,
                                                                     ScanView scan) {
+  pdl_wait();
+
   extern __shared__ __align__(16) unsigned char smem[];
   unsigned long long* s_key = reinterpret_cast<unsigned long long*>(smem);   // 64 KB
   int32_t* s_cnt = reinterpret_cast<int32_t*>(s_key + kCacheHashSlots);      // 32 KB
@@ -257,6 +259,8 @@ __global__ void __launch_bounds__(256) cache_probe_kernel(RotCache c, MapView ma
                                                           const uint32_t* __restrict__ d_n,
                                                           uint32_t chunks_per_run,
                                                           int32_t* __restrict__ scores) {
+  pdl_wait();
+
   const uint32_t n_runs = *d_n / 8;
   const uint64_t n_items = static_cast<uint64_t>(n_runs) * chunks_per_run;
   const int lane = threadIdx.x & 31;
@@ -373,13 +377,13 @@ void launch_epoch_score(const MapView& map, const GridView& grid, const ScanView
   const uint32_t max_runs = (n_max + 7) / 8;
   // the epoch's branch kernel already claimed the slots (cache_claim_run)
   // after its frontier reset ctl[2..3]
-  cache_build_kernel<<<std::min<uint32_t>(std::max<uint32_t>(max_runs, 1), 148 * 2), kBuildThreads, build_smem, s>>>(
-      cache, map, grid, scan);
+  launch_pdl(cache_build_kernel, std::min<uint32_t>(std::max<uint32_t>(max_runs, 1), 148 * 2), kBuildThreads,
+             build_smem, s, cache, map, grid, scan);
   BBS_CUDA(cudaGetLastError());
   const uint32_t chunks = (scan.k + kProbeChunk - 1) / kProbeChunk;
   const uint64_t warp_items = static_cast<uint64_t>(max_runs) * chunks;
   const unsigned g = static_cast<unsigned>(std::min<uint64_t>((warp_items + 7) / 8 + 1, 148ull * 16));
-  cache_probe_kernel<<<g, 256, 0, s>>>(cache, map, grid, scan, pending, d_n, chunks, scores);
+  launch_pdl(cache_probe_kernel, g, 256, 0, s, cache, map, grid, scan, pending, d_n, chunks, scores);
   BBS_CUDA(cudaGetLastError());
   launch_score_cube8(map, grid, scan, pending, d_n, n_max, n_ptiles, scores, &cache, s);
 }

@@ -3,6 +3,8 @@
 
 #include <cuda_runtime.h>
 
+#include <utility>
+
 #include "bbs_internal.h"
 
 namespace bbs {
@@ -148,5 +150,26 @@ void score_nodes_general(const MapView& map, const GridView& grid, const ScanVie
 
 // Choose the point-tile split for `runs` runs so the grid fills the chip.
 uint32_t choose_ptiles(uint64_t runs, uint32_t k);
+
+// Launch with programmatic stream serialization (PDL) so the kernel's launch
+// overlaps the tail of the previous kernel in the stream; the kernel must
+// call pdl_wait() before reading what its predecessor wrote.  BBS_PDL=0
+// turns it off (plain launches).
+bool pdl_enabled();
+template <typename... KArgs, typename... Args>
+void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  BBS_CUDA(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...));
+}
 
 }  // namespace bbs

@@ -311,6 +311,8 @@ __global__ void __launch_bounds__(256, 4) score_cube8_kernel(MapView map, GridVi
                                                              uint32_t n_ptiles,
                                                              int32_t* __restrict__ scores,
                                                              RotCache cache, int use_cache) {
+  pdl_wait();
+
   __shared__ double s_R[9];
   __shared__ int32_t s_hdr[4];
   __shared__ int32_t s_cnt[8];
@@ -970,6 +972,11 @@ void launch_score_roots(const MapView& map, const GridView& grid, const ScanView
   }
 }
 
+bool pdl_enabled() {
+  const char* v = std::getenv("BBS_PDL");
+  return !(v && v[0] == '0');
+}
+
 void launch_score_cube8(const MapView& map, const GridView& grid, const ScanView& scan,
                         const bbs_node* nodes, const uint32_t* d_n, uint32_t n_max,
                         uint32_t n_ptiles, int32_t* scores, const RotCache* cache,
@@ -979,8 +986,8 @@ void launch_score_cube8(const MapView& map, const GridView& grid, const ScanView
   // one resident wave (4 CTAs per SM), grid-strided
   const unsigned g = cache ? 148u * 4u
                            : static_cast<unsigned>(std::min<uint64_t>(std::max<uint64_t>(items, 1), 148ull * 4 * 8));
-  score_cube8_kernel<<<g, 256, 0, s>>>(map, grid, scan, nodes, d_n, n_ptiles, scores,
-                                       cache ? *cache : RotCache{}, cache ? 1 : 0);
+  launch_pdl(score_cube8_kernel, g, 256, 0, s, map, grid, scan, nodes, d_n, n_ptiles, scores,
+             cache ? *cache : RotCache{}, cache ? 1 : 0);
   BBS_CUDA(cudaGetLastError());
 }
 

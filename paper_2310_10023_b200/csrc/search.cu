@@ -107,6 +107,8 @@ __global__ void __launch_bounds__(kFT) frontier_kernel(EpochState* st, Queue q, 
                                                        int32_t* __restrict__ trace,
                                                        unsigned long long trace_cap,
                                                        int strategy, uint32_t* __restrict__ cache_ctl) {
+  pdl_wait();
+
   using ScanI = cub::BlockScan<int, kFT>;
   using ScanU = cub::BlockScan<unsigned long long, kFT>;
   using RedI = cub::BlockReduce<int, kFT>;
@@ -292,6 +294,8 @@ __global__ void branch_kernel(const EpochState* st, Queue q, GridView G,
                               const uint32_t* __restrict__ exp_parent,
                               const uint32_t* __restrict__ exp_off, bbs_node* __restrict__ pending,
                               int32_t* __restrict__ pscores, RotCache cache) {
+  pdl_wait();
+
   const uint32_t n = st->n_children;
   if (n == 0) return;
   const uint32_t ne = st->n_expand;
@@ -409,6 +413,8 @@ __global__ void __launch_bounds__(kST) survivors_kernel(EpochState* st, Queue q,
                                                         unsigned long long* __restrict__ s_key,
                                                         bbs_node* __restrict__ s_node,
                                                         unsigned long long* __restrict__ tiles) {
+  pdl_wait();
+
   using Load = cub::BlockLoad<int32_t, kST, kSIPT, cub::BLOCK_LOAD_WARP_TRANSPOSE>;
   using ScanI = cub::BlockScan<int, kST>;
   __shared__ union {
@@ -502,6 +508,8 @@ __global__ void __launch_bounds__(kRT) rank_sort_kernel(const EpochState* st,
                                                         const bbs_node* __restrict__ node,
                                                         unsigned long long* __restrict__ out_key,
                                                         bbs_node* __restrict__ out_node) {
+  pdl_wait();
+
   __shared__ unsigned long long tile[kRT];
   const uint32_t n = st->n_children ? st->n_surv : 0;
   if (n == 0) return;
@@ -529,6 +537,8 @@ __global__ void __launch_bounds__(kRT) rank_sort_kernel(const EpochState* st,
 __global__ void merge_kernel(EpochState* st, Queue q, int strategy,
                              const unsigned long long* __restrict__ skey,
                              const bbs_node* __restrict__ snode) {
+  pdl_wait();
+
   __shared__ uint32_t s_lo[kMaxLevels], s_len[kMaxLevels], s_pre[kMaxLevels + 1];
   if (st->n_children == 0) return;
   if (threadIdx.x < kMaxLevels) {
@@ -1105,23 +1115,23 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
   };
   // one flush epoch (frontier -> branch -> score -> survivors -> sort -> merge)
   auto enqueue_epoch = [&](int e) {
-    frontier_kernel<<<1, kFT, 0, s>>>(d_st, q, gv, cfg.batch_size, exp_parent, exp_off, d_trace,
-                                      trace_cap, strategy, cache.enabled ? cache.ctl : nullptr);
+    launch_pdl(frontier_kernel, 1, kFT, 0, s, d_st, q, gv, cfg.batch_size, exp_parent, exp_off, d_trace,
+               trace_cap, strategy, cache.enabled ? cache.ctl : nullptr);
     BBS_CUDA(cudaGetLastError());
     record(ev_pass[e]);
-    branch_kernel<<<grid1(pend_cap), 256, 0, s>>>(d_st, q, gv, exp_parent, exp_off, pending, pscores,
-                                                  cache);
+    launch_pdl(branch_kernel, grid1(pend_cap), 256, 0, s, d_st, q, gv, exp_parent, exp_off, pending, pscores,
+               cache);
     BBS_CUDA(cudaGetLastError());
     record(ev_s0[e]);
     launch_epoch_score(m->view, gv, sv, pending, d_nchild, static_cast<uint32_t>(pend_cap), ptiles,
                        pscores, cache, s);
     record(ev_s1[e]);
-    survivors_kernel<<<surv_grid, kST, 0, s>>>(d_st, q, strategy, pending, pscores, s_key, s_node,
-                                               surv_tiles);
+    launch_pdl(survivors_kernel, surv_grid, kST, 0, s, d_st, q, strategy, pending, pscores, s_key, s_node,
+               surv_tiles);
     BBS_CUDA(cudaGetLastError());
-    rank_sort_kernel<<<grid1(pend_cap, kRT), kRT, 0, s>>>(d_st, s_key, s_node, s_key2, s_node2);
+    launch_pdl(rank_sort_kernel, grid1(pend_cap, kRT), kRT, 0, s, d_st, s_key, s_node, s_key2, s_node2);
     BBS_CUDA(cudaGetLastError());
-    merge_kernel<<<grid1(qcap), 256, 0, s>>>(d_st, q, strategy, s_key2, s_node2);
+    launch_pdl(merge_kernel, grid1(qcap), 256, 0, s, d_st, q, strategy, s_key2, s_node2);
     BBS_CUDA(cudaGetLastError());
     launches += 6;  // frontier, branch, score, survivors, rank_sort, merge (+ finalize)
   };
