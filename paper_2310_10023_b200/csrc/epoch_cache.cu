@@ -172,10 +172,15 @@ __global__ void __launch_bounds__(kBuildThreads) cache_build_kernel(RotCache c, 
     const int dper = (ncells + kBuildThreads - 1) / kBuildThreads;
     const int dc0 = min(ncells, static_cast<int>(threadIdx.x) * dper), dc1 = min(ncells, dc0 + dper);
     auto dcount = [&](int i) { return (s_w[i >> 1] >> ((i & 1) << 4)) & 0xFFFFu; };
+    // the staged level stores groups of 4 byte-count entries (counts > 255 split)
+    const bool staged = dense && l == c.stg_level;
     int cnt = 0;
     if (dense) {
       if (!oob)
-        for (int i = dc0; i < dc1; ++i) cnt += dcount(i) != 0u ? 1 : 0;
+        for (int i = dc0; i < dc1; ++i) {
+          const uint32_t v = dcount(i);
+          cnt += staged ? static_cast<int>((v + 254u) / 255u) : (v != 0u ? 1 : 0);
+        }
     } else if (!raw) {
 #pragma unroll
       for (int k = 0; k < kPer; ++k) cnt += s_key[threadIdx.x * kPer + k] != kEmptyKey ? 1 : 0;
@@ -183,17 +188,44 @@ __global__ void __launch_bounds__(kBuildThreads) cache_build_kernel(RotCache c, 
     int epos, n_dist;
     ScanI(s_scan).ExclusiveSum(cnt, epos, n_dist);
     const uint32_t n_ent = (raw || oob) ? 0u : static_cast<uint32_t>(n_dist);
+    // pool space in int4 units (staged: 2 int4 per group of 4 entries)
+    const uint32_t n_slots = staged ? 2u * ((n_ent + 3u) / 4u) : n_ent;
     if (threadIdx.x == 0) {
-      s_off = (raw || oob) ? 0u : atomicAdd(&c.ctl[0], n_ent);
+      s_off = (raw || oob) ? 0u : atomicAdd(&c.ctl[0], n_slots);
       s_aoff = (raw || oob) ? 0u : atomicAdd(&c.ctl[1], static_cast<uint32_t>(namb));
       if (raw) c.ctl[4 + (l & (kMaxLevels - 1))] = 1u;
     }
     __syncthreads();
     const uint32_t off = s_off, aoff = s_aoff;
     const bool fits = !raw && !oob && namb <= kCacheAmbCap &&
-                      static_cast<uint64_t>(off) + n_ent <= c.pool_cap &&
+                      static_cast<uint64_t>(off) + n_slots <= c.pool_cap &&
                       static_cast<uint64_t>(aoff) + namb <= c.amb_cap;
-    if (fits && dense) {
+    if (fits && staged) {
+      int32_t* gw = reinterpret_cast<int32_t*>(c.pool + off);
+      unsigned char* gb = reinterpret_cast<unsigned char*>(c.pool + off);
+      for (int i = dc0; i < dc1; ++i) {
+        uint32_t v = dcount(i);
+        if (!v) continue;
+        const int fx = i % dxy - dr, fy = (i / dxy) % dxy - dr, fz = i / (dxy * dxy) + dzlo;
+        const int32_t eoff = fy * static_cast<int32_t>(c.stg_pitch) + fx;
+        for (; v; ++epos) {
+          const uint32_t w = min(v, 255u);
+          v -= w;
+          const int g = epos >> 2, k = epos & 3;
+          gw[g * 8 + k] = eoff;
+          gb[(g * 8 + 4) * 4 + k] = static_cast<unsigned char>(static_cast<int8_t>(fz));
+          gb[(g * 8 + 5) * 4 + k] = static_cast<unsigned char>(w);
+        }
+      }
+      // zero-count padding of the last group
+      const int pe = static_cast<int>(n_ent) + static_cast<int>(threadIdx.x);
+      if (pe < static_cast<int>((n_ent + 3u) & ~3u)) {
+        const int g = pe >> 2, k = pe & 3;
+        gw[g * 8 + k] = 0;
+        gb[(g * 8 + 4) * 4 + k] = 0;
+        gb[(g * 8 + 5) * 4 + k] = 0;
+      }
+    } else if (fits && dense) {
       for (int i = dc0; i < dc1; ++i) {
         const uint32_t v = dcount(i);
         if (v) {
@@ -259,7 +291,19 @@ __global__ void __launch_bounds__(256) cache_probe_kernel(RotCache c, MapView ma
                                                           const uint32_t* __restrict__ d_n,
                                                           uint32_t chunks_per_run,
                                                           int32_t* __restrict__ scores) {
+  extern __shared__ uint32_t s_win[];  // staged level's padded column window
   pdl_wait();
+  if (c.stg_level >= 0) {
+    const LevelView& SL = map.level[c.stg_level];
+    for (uint32_t i = threadIdx.x; i < c.stg_pitch * c.stg_rows; i += blockDim.x) {
+      const int32_t x = c.stg_sx0 + static_cast<int32_t>(i % c.stg_pitch);
+      const int32_t y = c.stg_sy0 + static_cast<int32_t>(i / c.stg_pitch);
+      s_win[i] = (x >= 0 && y >= 0 && x < static_cast<int32_t>(SL.dim[0]) && y < static_cast<int32_t>(SL.dim[1]))
+                     ? __ldg(&SL.words[static_cast<uint32_t>(y) * SL.dim[0] + static_cast<uint32_t>(x)]) << 8
+                     : 0u;
+    }
+    __syncthreads();
+  }
 
   const uint32_t n_runs = *d_n / 8;
   const uint64_t n_items = static_cast<uint64_t>(n_runs) * chunks_per_run;
@@ -314,7 +358,36 @@ __global__ void __launch_bounds__(256) cache_probe_kernel(RotCache c, MapView ma
       const uint32_t e0 = ch * kProbeChunk;
       const uint32_t e1 = min(n_ent, e0 + kProbeChunk);
       const int4* __restrict__ ent = c.pool + off;
-      if (L.layout == BBS_LAYOUT_BITMAP) {
+      if (l == c.stg_level) {
+        // staged: 4 LDS + 4 clamped funnel shifts give an entry's 2x2x2 child
+        // mask (bits t = dx*4 + dy*2 + dz); 4 masks are packed as bytes and
+        // per child t one LOP3 + IDP4A adds 2^t * count of the hits
+        const int32_t pitch = static_cast<int32_t>(c.stg_pitch);
+        const int32_t base = (by - L.box_min[1] - c.stg_sy0) * pitch + (bx - L.box_min[0] - c.stg_sx0);
+        const int32_t oz8 = bz - L.box_min[2] + 8;
+        uint32_t a8[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        for (uint32_t g = (e0 >> 2) + lane; g < ((e1 + 3) >> 2); g += 32) {
+          const int4 o = __ldg(ent + 2 * g);
+          const int4 q = __ldg(ent + 2 * g + 1);
+          const int32_t eo[4] = {o.x, o.y, o.z, o.w};
+          uint32_t m4 = 0;
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const int32_t i = base + eo[k];
+            const uint32_t sh = static_cast<uint32_t>(static_cast<int32_t>(static_cast<int8_t>(q.x >> (8 * k))) + oz8);
+            const uint32_t b8 = (__funnelshift_rc(s_win[i], 0u, sh) & 0x03u) |
+                                (__funnelshift_rc(s_win[i + pitch], 0u, sh - 2u) & 0x0Cu) |
+                                (__funnelshift_rc(s_win[i + 1], 0u, sh - 4u) & 0x30u) |
+                                (__funnelshift_rc(s_win[i + pitch + 1], 0u, sh - 6u) & 0xC0u);
+            m4 |= b8 << (8 * k);
+          }
+          const uint32_t w4 = static_cast<uint32_t>(q.y);
+#pragma unroll
+          for (int t = 0; t < 8; ++t) a8[t] = __dp4a(m4 & (0x01010101u << t), w4, a8[t]);
+        }
+#pragma unroll
+        for (int t = 0; t < 8; ++t) acc[t] = static_cast<int>(a8[t] >> t);
+      } else if (L.layout == BBS_LAYOUT_BITMAP) {
         // two entries per lane per step: 8-16 independent column loads in flight
         uint32_t e = e0 + lane;
         for (; e + 32 < e1; e += 64) {
@@ -383,7 +456,21 @@ void launch_epoch_score(const MapView& map, const GridView& grid, const ScanView
   const uint32_t chunks = (scan.k + kProbeChunk - 1) / kProbeChunk;
   const uint64_t warp_items = static_cast<uint64_t>(max_runs) * chunks;
   const unsigned g = static_cast<unsigned>(std::min<uint64_t>((warp_items + 7) / 8 + 1, 148ull * 16));
-  launch_pdl(cache_probe_kernel, g, 256, 0, s, cache, map, grid, scan, pending, d_n, chunks, scores);
+  const int win_smem = cache.stg_level >= 0 ? static_cast<int>(cache.stg_pitch * cache.stg_rows * 4u) : 0;
+  static bool probe_attr = false;
+  if (!probe_attr) {
+    BBS_CUDA(cudaFuncSetAttribute(cache_probe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  kStageWindowMax));
+    probe_attr = true;
+  }
+  unsigned gp = g;
+  if (win_smem > 0) {
+    // persistent: each CTA stages the window once
+    int per_sm = 1;
+    BBS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cache_probe_kernel, 256, win_smem));
+    gp = std::min<unsigned>(g, 148u * static_cast<unsigned>(std::max(per_sm, 1)));
+  }
+  launch_pdl(cache_probe_kernel, gp, 256, win_smem, s, cache, map, grid, scan, pending, d_n, chunks, scores);
   BBS_CUDA(cudaGetLastError());
   launch_score_cube8(map, grid, scan, pending, d_n, n_max, n_ptiles, scores, &cache, s);
 }

@@ -110,6 +110,7 @@ void launch_score_runs8(const MapView& map, const GridView& grid, const ScanView
 constexpr int32_t kCacheEmpty = -1, kCacheBuilding = -2, kCacheNone = -3, kCacheReady = 0;
 constexpr int kCacheCtl = 4 + kMaxLevels;
 constexpr int kCacheDenseCells = 48 * 1024;  // 96 KB of 16-bit counters
+constexpr int kStageWindowMax = 96 * 1024;   // bytes of the probe's staged column window
 struct RotCache {
   int enabled;
   uint32_t base[kMaxLevels];   // 0xFFFFFFFF: level not cached
@@ -124,6 +125,14 @@ struct RotCache {
   // dense-histogram box per level (dn_r = 0: hash build): offsets in
   // [-r, r]^2 x [zlo, zlo + nz), two 16-bit counts per shared word
   int32_t dn_r[kMaxLevels], dn_zlo[kMaxLevels], dn_nz[kMaxLevels];
+  // staged level (-1: none): its histograms are stored as groups of 4
+  // entries (column offset in the padded window, z bytes, count bytes) and
+  // the probe reads the level's z-column words from a zero-padded shared
+  // window [sx0, sx0 + pitch) x [sy0, sy0 + rows) (relative to box_min),
+  // pre-shifted up by 8 bits
+  int stg_level;
+  int32_t stg_sx0, stg_sy0;
+  uint32_t stg_pitch, stg_rows;
   int4* builds;                // [max runs] (slot, level, iroll, ipitch)
   int32_t* builds_w;           // [max runs] iyaw
   uint64_t pool_cap, amb_cap;

@@ -1035,6 +1035,7 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
     return !(v && v[0] == '0');
   }();
   RotCache cache{};
+  cache.stg_level = -1;
   // a histogram build costs about one direct run; small scans (C1: K = 2000)
   // rarely amortize it, large ones (C2/C3) reuse rotations across flushes
   if (cache_on && K >= 4096) {
@@ -1071,6 +1072,30 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
           cache.dn_r[l] = static_cast<int32_t>(r);
           cache.dn_zlo[l] = static_cast<int32_t>(zlo);
           cache.dn_nz[l] = static_cast<int32_t>(zhi - zlo + 1.0);
+        }
+      }
+    }
+    cache.stg_level = -1;
+    {
+      // stage level L-1 (it carries almost all cached flush work): needs a
+      // dense box, a single z word per column with 8 bits of headroom, and a
+      // padded window that fits shared memory
+      const int l = L - 1;
+      const LevelView& LV = m->view.level[l];
+      if (l >= 0 && cache.base[l] != 0xFFFFFFFFu && cache.dn_r[l] > 0 && LV.layout == BBS_LAYOUT_BITMAP &&
+          LV.nwz == 1 && LV.dim[2] <= 24 && cache.dn_zlo[l] >= -128 && cache.dn_zlo[l] + cache.dn_nz[l] <= 128 &&
+          std::getenv("BBS_STAGE_PROBE") == nullptr) {
+        // child translations at level L-1 span [2 x0, 2 x1 + 1] (+1 for the cube)
+        const int64_t R = cache.dn_r[l];
+        const int64_t x_lo = 2ll * x0 - LV.box_min[0] - R, x_hi = 2ll * x1 + 2 - LV.box_min[0] + R + 1;
+        const int64_t y_lo = 2ll * y0 - LV.box_min[1] - R, y_hi = 2ll * y1 + 2 - LV.box_min[1] + R + 1;
+        const int64_t words = (x_hi - x_lo) * (y_hi - y_lo);
+        if (words > 0 && words * 4 <= kStageWindowMax) {
+          cache.stg_level = l;
+          cache.stg_sx0 = static_cast<int32_t>(x_lo);
+          cache.stg_sy0 = static_cast<int32_t>(y_lo);
+          cache.stg_pitch = static_cast<uint32_t>(x_hi - x_lo);
+          cache.stg_rows = static_cast<uint32_t>(y_hi - y_lo);
         }
       }
     }
