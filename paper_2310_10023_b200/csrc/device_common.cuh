@@ -71,4 +71,30 @@ __device__ __forceinline__ bool level_contains(const LevelView& L, int32_t x, in
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
+// One-shot TMA bulk copy global -> shared (1D, bytes % 16 == 0, both
+// addresses 16-byte aligned) completing on an mbarrier.  Call from every
+// thread of the CTA: thread 0 issues, everyone waits.
+__device__ __forceinline__ void bulk_load_to_smem(void* dst, const void* src, uint32_t bytes,
+                                                  unsigned long long* mbar) {
+  const uint32_t b = static_cast<uint32_t>(__cvta_generic_to_shared(mbar));
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(b) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
+                 "l"(src), "r"(bytes), "r"(b)
+                 : "memory");
+  }
+  __syncthreads();  // the barrier is initialised before anyone polls it
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "BBS_WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n"
+      "@!p bra BBS_WAIT_%=;\n"
+      "}\n" ::"r"(b)
+      : "memory");
+}
+
 }  // namespace bbs

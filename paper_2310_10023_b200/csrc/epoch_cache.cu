@@ -32,7 +32,7 @@ namespace {
 constexpr int kCacheHashSlots = 8192;
 constexpr int kCacheHashCap = 4096;   // distinct offsets kept in shared memory
 constexpr int kCacheAmbCap = 2048;    // ambiguous points buffered per build
-constexpr int kProbeChunk = 256;      // histogram entries per warp item
+constexpr int kProbeChunk = 1024;     // histogram entries per warp item
 constexpr unsigned long long kEmptyKey = ~0ull;
 
 __device__ __forceinline__ uint32_t cache_hash(unsigned long long key) {
@@ -285,25 +285,19 @@ __device__ __forceinline__ void probe_ambiguous(const RotCache& c, const LevelVi
 // first fetch the headers (run node, cache info) of 32 items in parallel and
 // the warp then walks only the items that have entries, so empty chunks and
 // uncached runs cost no serial load latency.
-__global__ void __launch_bounds__(256) cache_probe_kernel(RotCache c, MapView map, GridView G,
+__global__ void __launch_bounds__(256, 3) cache_probe_kernel(RotCache c, MapView map, GridView G,
                                                           ScanView scan,
                                                           const bbs_node* __restrict__ pending,
                                                           const uint32_t* __restrict__ d_n,
                                                           uint32_t chunks_per_run,
                                                           int32_t* __restrict__ scores) {
-  extern __shared__ uint32_t s_win[];  // staged level's padded column window
+  extern __shared__ __align__(16) uint32_t s_win[];  // staged level's padded column window
+  __shared__ __align__(8) unsigned long long s_mbar;
+  // the window is search-constant: one bulk copy per CTA (before pdl_wait:
+  // it does not depend on the previous kernel)
+  if (c.stg_level >= 0)
+    bulk_load_to_smem(s_win, c.stg_win, ((c.stg_pitch * c.stg_rows * 4u) + 15u) & ~15u, &s_mbar);
   pdl_wait();
-  if (c.stg_level >= 0) {
-    const LevelView& SL = map.level[c.stg_level];
-    for (uint32_t i = threadIdx.x; i < c.stg_pitch * c.stg_rows; i += blockDim.x) {
-      const int32_t x = c.stg_sx0 + static_cast<int32_t>(i % c.stg_pitch);
-      const int32_t y = c.stg_sy0 + static_cast<int32_t>(i / c.stg_pitch);
-      s_win[i] = (x >= 0 && y >= 0 && x < static_cast<int32_t>(SL.dim[0]) && y < static_cast<int32_t>(SL.dim[1]))
-                     ? __ldg(&SL.words[static_cast<uint32_t>(y) * SL.dim[0] + static_cast<uint32_t>(x)]) << 8
-                     : 0u;
-    }
-    __syncthreads();
-  }
 
   const uint32_t n_runs = *d_n / 8;
   const uint64_t n_items = static_cast<uint64_t>(n_runs) * chunks_per_run;
@@ -366,7 +360,9 @@ __global__ void __launch_bounds__(256) cache_probe_kernel(RotCache c, MapView ma
         const int32_t base = (by - L.box_min[1] - c.stg_sy0) * pitch + (bx - L.box_min[0] - c.stg_sx0);
         const int32_t oz8 = bz - L.box_min[2] + 8;
         uint32_t a8[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-        for (uint32_t g = (e0 >> 2) + lane; g < ((e1 + 3) >> 2); g += 32) {
+        const uint32_t g_end = (e1 + 3) >> 2;
+#pragma unroll 2
+        for (uint32_t g = (e0 >> 2) + lane; g < g_end; g += 32) {
           const int4 o = __ldg(ent + 2 * g);
           const int4 q = __ldg(ent + 2 * g + 1);
           const int32_t eo[4] = {o.x, o.y, o.z, o.w};
@@ -430,7 +426,28 @@ __global__ void __launch_bounds__(256) cache_probe_kernel(RotCache c, MapView ma
   }
 }
 
+// The staged probe window: zero-padded, words shifted up by 8 bits; the
+// tail up to a multiple of 4 words (16 bytes for the bulk copy) is zero.
+__global__ void stage_window_kernel(LevelView SL, int32_t sx0, int32_t sy0, uint32_t pitch, uint32_t n,
+                                    uint32_t n16, uint32_t* __restrict__ win) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n16; i += gridDim.x * blockDim.x) {
+    const int32_t x = sx0 + static_cast<int32_t>(i % pitch);
+    const int32_t y = sy0 + static_cast<int32_t>(i / pitch);
+    win[i] = i < n && x >= 0 && y >= 0 && x < static_cast<int32_t>(SL.dim[0]) && y < static_cast<int32_t>(SL.dim[1])
+                 ? SL.words[static_cast<uint32_t>(y) * SL.dim[0] + static_cast<uint32_t>(x)] << 8
+                 : 0u;
+  }
+}
+
 }  // namespace
+
+void build_stage_window(const MapView& map, const RotCache& cache, uint32_t* win, cudaStream_t s) {
+  const uint32_t n = cache.stg_pitch * cache.stg_rows;
+  const uint32_t n16 = (n + 3u) & ~3u;  // bulk copies move multiples of 16 bytes
+  stage_window_kernel<<<std::min<uint32_t>((n16 + 255) / 256, 148 * 8), 256, 0, s>>>(
+      map.level[cache.stg_level], cache.stg_sx0, cache.stg_sy0, cache.stg_pitch, n, n16, win);
+  BBS_CUDA(cudaGetLastError());
+}
 
 void launch_epoch_score(const MapView& map, const GridView& grid, const ScanView& scan,
                         const bbs_node* pending, const uint32_t* d_n, uint32_t n_max,
@@ -456,7 +473,7 @@ void launch_epoch_score(const MapView& map, const GridView& grid, const ScanView
   const uint32_t chunks = (scan.k + kProbeChunk - 1) / kProbeChunk;
   const uint64_t warp_items = static_cast<uint64_t>(max_runs) * chunks;
   const unsigned g = static_cast<unsigned>(std::min<uint64_t>((warp_items + 7) / 8 + 1, 148ull * 16));
-  const int win_smem = cache.stg_level >= 0 ? static_cast<int>(cache.stg_pitch * cache.stg_rows * 4u) : 0;
+  const int win_smem = cache.stg_level >= 0 ? static_cast<int>(((cache.stg_pitch * cache.stg_rows * 4u) + 15u) & ~15u) : 0;
   static bool probe_attr = false;
   if (!probe_attr) {
     BBS_CUDA(cudaFuncSetAttribute(cache_probe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,

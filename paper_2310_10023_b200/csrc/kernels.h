@@ -133,6 +133,7 @@ struct RotCache {
   int stg_level;
   int32_t stg_sx0, stg_sy0;
   uint32_t stg_pitch, stg_rows;
+  const uint32_t* stg_win;     // the window, built once per search (bytes rounded to 16)
   int4* builds;                // [max runs] (slot, level, iroll, ipitch)
   int32_t* builds_w;           // [max runs] iyaw
   uint64_t pool_cap, amb_cap;
@@ -159,6 +160,9 @@ void score_nodes_general(const MapView& map, const GridView& grid, const ScanVie
 
 // Choose the point-tile split for `runs` runs so the grid fills the chip.
 uint32_t choose_ptiles(uint64_t runs, uint32_t k);
+
+// Builds the staged probe window (zero-padded, words << 8) in global memory.
+void build_stage_window(const MapView& map, const RotCache& cache, uint32_t* win, cudaStream_t s);
 
 // Launch with programmatic stream serialization (PDL) so the kernel's launch
 // overlaps the tail of the previous kernel in the stream; the kernel must

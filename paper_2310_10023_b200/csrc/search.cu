@@ -713,7 +713,7 @@ struct Workspace {
   Buf<uint32_t> perm0, perm1, sk0, sk1, exp_parent, exp_off;
   Buf<int32_t> pscores, trace, hist_n;
   Buf<int4> hist_ent, cache_info, cache_pool, cache_builds;
-  Buf<uint32_t> cache_u32, cache_amb, cache_fb;
+  Buf<uint32_t> cache_u32, cache_amb, cache_fb, stage_win;
   Buf<int32_t> cache_builds_w;
   Buf<uint32_t> hist_amb;
   Buf<EpochState> st;
@@ -744,6 +744,7 @@ struct Workspace {
     cache_u32.release();
     cache_amb.release();
     cache_fb.release();
+    stage_win.release();
     cache_builds_w.release();
     st.release();
     if (h_st) cudaFreeHost(h_st);
@@ -1112,6 +1113,11 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
       cache.builds = W.cache_builds.get(mr, s);
       cache.builds_w = W.cache_builds_w.get(mr, s);
       cache.fb_runs = W.cache_fb.get(mr, s);
+      if (cache.stg_level >= 0) {
+        uint32_t* win = W.stage_win.get(((static_cast<size_t>(cache.stg_pitch) * cache.stg_rows + 3) & ~size_t(3)), s);
+        build_stage_window(m->view, cache, win, s);
+        cache.stg_win = win;
+      }
       BBS_CUDA(cudaMemsetAsync(cache.info, 0xFF, slots * sizeof(int4), s));  // all kCacheEmpty
       BBS_CUDA(cudaMemsetAsync(cache.ctl, 0, kCacheCtl * sizeof(uint32_t), s));
     }
