@@ -231,7 +231,10 @@ def run_b200_arm(args, cfgd):
     import torch
     world, rank, local = dist_env()
     torch.cuda.set_device(local)
-    if world > 1:
+    # BBS_BENCH_SHARDED=1 takes the sharded path at world 1 too (torchrun
+    # --nproc-per-node 1): a one-GPU check of the NCCL glue
+    sharded = world > 1 or os.environ.get("BBS_BENCH_SHARDED") == "1"
+    if sharded:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     import paper_2310_10023_b200 as B
@@ -249,23 +252,23 @@ def run_b200_arm(args, cfgd):
     dscan = B.DeviceScan(vmap, scan)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")  # > 126 MB L2
 
-    if world > 1:
+    if sharded:
         import torch.distributed as dist
-        red = torch.zeros(8, dtype=torch.int64, device="cuda")
+        # the search's own NCCL communicator: incumbent / score exchanges are
+        # ncclAllReduce(MAX) calls on the search stream (no host round-trip)
+        uid = [B.Comm.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        comm = B.Comm(local, rank, world, uid[0])
 
-        def allreduce_max(vals):
-            red[: len(vals)].copy_(torch.tensor(vals, dtype=torch.int64))
-            dist.all_reduce(red[: len(vals)], op=dist.ReduceOp.MAX)
-            return red[: len(vals)].tolist()
-
-        def one_search():
-            return B.search_sharded(vmap, dscan, cfg, rank, world, allreduce_max)
+        def one_search(ds=None):
+            return B.search_sharded(vmap, ds or dscan, cfg, rank, world, comm=comm,
+                                    mode=args.shard_mode)
     else:
         def one_search():
             return B.search_scan(vmap, dscan, cfg)
 
     def barrier():
-        if world > 1:
+        if sharded:
             torch.distributed.barrier()
         torch.cuda.synchronize()
 
@@ -289,12 +292,15 @@ def run_b200_arm(args, cfgd):
     clk = clocks.stop()
     t_local = sum(step_ms)
     evals_local = sum(r.stats.nodes_generated for r in results)
-    if world > 1:
+    # roots mode: ranks search disjoint subtrees (sum); exact mode: every rank
+    # reports the whole search's Stats (count them once)
+    ev_op = "MAX" if args.shard_mode == "exact" else "SUM"
+    if sharded:
         import torch.distributed as dist
         tt = torch.tensor([t_local], dtype=torch.float64, device="cuda")
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ev = torch.tensor([evals_local], dtype=torch.int64, device="cuda")
-        dist.all_reduce(ev, op=dist.ReduceOp.SUM)
+        dist.all_reduce(ev, op=getattr(dist.ReduceOp, ev_op))
         t_max, evals = float(tt.item()), int(ev.item())
     else:
         t_max, evals = t_local, evals_local
@@ -307,7 +313,7 @@ def run_b200_arm(args, cfgd):
     pinned.copy_(torch.from_numpy(scan))
     host_scan = pinned.numpy()
     e2e_t, e2e_evals, h2d, d2h = 0.0, 0, 0, 0
-    if world == 1:
+    if not sharded:
         B.search(vmap, host_scan, cfg)  # warm
         for _ in range(args.steps):
             flush.fill_(1)
@@ -327,7 +333,7 @@ def run_b200_arm(args, cfgd):
             barrier()
             t = time.perf_counter()
             ds = B.DeviceScan(vmap, host_scan)
-            re = B.search_sharded(vmap, ds, cfg, rank, world, allreduce_max)
+            re = one_search(ds)
             barrier()
             e2e_t += time.perf_counter() - t
             e2e_evals += re.stats.nodes_generated
@@ -336,7 +342,7 @@ def run_b200_arm(args, cfgd):
         tt = torch.tensor([e2e_t], dtype=torch.float64, device="cuda")
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ev = torch.tensor([e2e_evals], dtype=torch.int64, device="cuda")
-        dist.all_reduce(ev, op=dist.ReduceOp.SUM)
+        dist.all_reduce(ev, op=getattr(dist.ReduceOp, ev_op))
         e2e = {"value": int(ev.item()) / float(tt.item()), "unit": "evals/s",
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                "ms_per_step": 1e3 * float(tt.item()) / args.steps,
@@ -386,7 +392,8 @@ def run_b200_arm(args, cfgd):
         "scaling": "strong" if world > 1 else "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (gen_scene restatement, bit-identical to the reference's)",
         "config": {"workload": cfgd["workload"], "K": K, "map_points": int(map_pts.shape[0]),
-                   "parallelism": f"root-shard x{world}" if world > 1 else "single GPU",
+                   "parallelism": (f"{args.shard_mode}-shard x{world}, NCCL incumbent/score "
+                                   "all-reduce on the search stream") if sharded else "single GPU",
                    "l2": "flushed (256 MiB write) before every timed step",
                    "layouts": layouts},
         "latency_ms": {"localization_total": statistics.mean(r.stats.localization_total_ms()
@@ -417,7 +424,9 @@ def run_b200_arm(args, cfgd):
                                     "kind": "reference", "sample": f"unavailable: {exc}"}
     if rank == 0:
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if sharded:
+        torch.cuda.synchronize()
+        comm.close()
         torch.distributed.destroy_process_group()
 
 
@@ -540,6 +549,9 @@ def main():
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
     ap.add_argument("--config", choices=sorted(CONFIGS), default="c2")
     ap.add_argument("--layout", choices=["auto", "bitmap", "hash"], default="auto")
+    ap.add_argument("--shard-mode", choices=["roots", "exact"], default="roots",
+                    help="N>1: roots = own BnB per rank over its root share + incumbent "
+                         "all-reduce; exact = batch-split replay of the single-queue schedule")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-gather-bench", action="store_true")

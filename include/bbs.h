@@ -33,7 +33,7 @@
 extern "C" {
 #endif
 
-#define BBS_ABI_VERSION 2
+#define BBS_ABI_VERSION 3
 
 /* Status codes, 1:1 with the exception classes of errors.hpp:11-98. */
 typedef enum bbs_status {
@@ -266,19 +266,55 @@ int bbs_stream_destroy(void* stream);
 int bbs_batch_evaluate_device(bbs_map_t map, bbs_scan_t scan, const bbs_search_config* cfg,
                               double d_max, bbs_node* d_nodes, uint64_t n, void* stream);
 
-/* ---- multi-GPU (root sharding) ---------------------------- */
+/* ---- multi-GPU ------------------------------------------ */
 /* Element-wise MAX all-reduce of `count` int64 values in place across all
  * ranks; returns 0 on success.  Supplied by the caller (NCCL / gloo). */
 typedef int (*bbs_allreduce_max_fn)(int64_t* values, int32_t count, void* user);
+
+/* NCCL communicator for the device-side exchanges of a sharded search
+ * (ncclAllReduce MAX on the search stream over NVLink / NVSwitch; no host
+ * round-trip per epoch).  NCCL is loaded at run time (libnccl.so.2; inside
+ * a torch process, the NCCL torch already loaded).  Rank 0 calls
+ * bbs_comm_unique_id and ships the 128 bytes to every rank out of band
+ * (e.g. torch.distributed.broadcast_object_list); every rank then calls
+ * bbs_comm_init collectively.  One sharded search per comm at a time. */
+typedef struct bbs_comm* bbs_comm_t;
+int bbs_comm_unique_id(uint8_t id[128]);
+int bbs_comm_init(int32_t device, int32_t rank, int32_t world_size, const uint8_t id[128],
+                  bbs_comm_t* out);
+int bbs_comm_free(bbs_comm_t comm);
+/* Version of the loaded NCCL (e.g. 22809), 0 when NCCL cannot be loaded. */
+int bbs_nccl_version(void);
+
+/* Sharding modes. */
+enum {
+  /* Each rank runs its own best-first BnB over its share of the root set and
+   * adopts the max-all-reduced incumbent after every epoch; the winner is
+   * elected at the end.  RotoTrans results may differ from the
+   * single-queue schedule (SURVEY §8e caveat); TransOnly best scores equal
+   * the unsharded search (admissible bound). */
+  BBS_SHARD_ROOTS = 0,
+  /* Batch-split exact mode: every rank replays the single-queue schedule;
+   * the root batch and every flush batch are split across the ranks (root
+   * units as above, flush runs of 8 children by run % world_size) and the
+   * int32 scores max-all-reduced, so every rank returns the unsharded
+   * search() result exactly (score, pose, Stats, trace). */
+  BBS_SHARD_EXACT = 1
+};
+
 typedef struct bbs_shard {
   int32_t rank;
   int32_t world_size;
-  bbs_allreduce_max_fn allreduce_max;
+  bbs_allreduce_max_fn allreduce_max; /* host exchange; used when comm is NULL */
   void* user;
+  int32_t mode;                       /* BBS_SHARD_ROOTS / BBS_SHARD_EXACT */
+  int32_t reserved;
+  bbs_comm_t comm;                    /* device exchange (NCCL); NULL = allreduce_max */
 } bbs_shard;
-/* search() over the roots with index % world_size == rank; the incumbent is
- * max-all-reduced after every epoch and the winner elected at the end, so
- * every rank returns the same best pose/score.  Stats are this rank's. */
+/* search() sharded across ranks (see the modes above).  Root (ix, iy, iz,
+ * rot) of initial_nodes belongs to rank ((ix - ix_min) * n_rot + rot) %
+ * world_size.  Every rank returns the same best pose/score.  ROOTS: Stats
+ * are this rank's; EXACT: Stats are the whole search's. */
 int bbs_search_sharded(bbs_map_t map, bbs_scan_t scan, const bbs_search_config* cfg,
                        const bbs_shard* shard, bbs_search_result* result);
 

@@ -450,6 +450,23 @@ static uint64_t branch(const bbs_node* c, const bbs_axis_grid* g, int32_t L, bbs
   return w;
 }
 
+/* Exact mode: element-wise MAX of the nodes' scores over the ranks. */
+static int exchange_scores(const bbs_shard* shard, bbs_node* nodes, uint64_t n) {
+  const uint64_t chunk = 1u << 20;
+  int64_t* v = (int64_t*)malloc(sizeof(int64_t) * (n < chunk ? (n ? n : 1) : chunk));
+  for (uint64_t o = 0; o < n; o += chunk) {
+    const uint64_t c = n - o < chunk ? n - o : chunk;
+    for (uint64_t i = 0; i < c; ++i) v[i] = nodes[o + i].score;
+    if (shard->allreduce_max(v, (int32_t)c, shard->user)) {
+      free(v);
+      return 1;
+    }
+    for (uint64_t i = 0; i < c; ++i) nodes[o + i].score = (int32_t)v[i];
+  }
+  free(v);
+  return 0;
+}
+
 /* Reference loop with an optional incumbent exchange after each batch. */
 static int search_impl(const orc_map* m, const bbs_aabb* map_bbox, const double* scan,
                        uint64_t k, const bbs_search_config* cfg, const bbs_shard* shard,
@@ -473,6 +490,10 @@ static int search_impl(const orc_map* m, const bbs_aabb* map_bbox, const double*
   const bbs_aabb* tr = cfg->has_translation_range ? &cfg->translation_range : map_bbox;
   const int rank = shard ? shard->rank : 0;
   const int world = shard ? shard->world_size : 1;
+  /* batch-split exact mode: every rank replays the single-queue
+   * schedule; root and flush scores are split over the ranks and
+   * max-all-reduced (unscored entries are -1) */
+  const int exact = shard && shard->mode == BBS_SHARD_EXACT && shard->allreduce_max;
 
   memset(&out->stats, 0, sizeof(out->stats));
   out->scan_points = k;
@@ -499,7 +520,30 @@ static int search_impl(const orc_map* m, const bbs_aabb* map_bbox, const double*
    * ((ix - ix_min) * nrot + rot) % world — whole (x-slab, rotation) units,
    * the rule of the device root kernel (csrc/kernels.h owned_slabs). */
   uint64_t nmine = 0;
-  {
+  if (exact) {
+    const int64_t np_ = max_index(axis_at(g, L, 1, L)) + 1;
+    const int64_t nw_ = max_index(axis_at(g, L, 2, L)) + 1;
+    const int64_t nrot = (max_index(axis_at(g, L, 0, L)) + 1) * np_ * nw_;
+    const int32_t ix_min = nroots ? roots[0].ix : 0;
+    for (uint64_t i = 0; i < nroots; ++i) {
+      const int64_t rot = ((int64_t)roots[i].iroll * np_ + roots[i].ipitch) * nw_ + roots[i].iyaw;
+      const int64_t unit = ((int64_t)roots[i].ix - ix_min) * nrot + rot;
+      if ((int)(unit % world) == rank) {
+        score_node(m, g, L, scan, k, &roots[i]);
+        ++nmine;
+      } else {
+        roots[i].score = -1;
+      }
+    }
+    if (exchange_scores(shard, roots, nroots)) {
+      free(roots);
+      free(g);
+      return BBS_ERR_GENERIC;
+    }
+    stats->nodes_generated += nroots;
+    out->root_nodes = nmine;
+    nmine = nroots; /* every root is in play below, in initial_nodes order */
+  } else {
     const int64_t np_ = max_index(axis_at(g, L, 1, L)) + 1;
     const int64_t nw_ = max_index(axis_at(g, L, 2, L)) + 1;
     const int64_t nrot = (max_index(axis_at(g, L, 0, L)) + 1) * np_ * nw_;
@@ -510,9 +554,11 @@ static int search_impl(const orc_map* m, const bbs_aabb* map_bbox, const double*
       if ((int)(unit % world) == rank) roots[nmine++] = roots[i];
     }
   }
-  stats->nodes_generated += nmine;
-  out->root_nodes = nmine;
-  for (uint64_t i = 0; i < nmine; ++i) score_node(m, g, L, scan, k, &roots[i]);
+  if (!exact) {
+    stats->nodes_generated += nmine;
+    out->root_nodes = nmine;
+    for (uint64_t i = 0; i < nmine; ++i) score_node(m, g, L, scan, k, &roots[i]);
+  }
   stats->batches_flushed++;
   for (uint64_t i = 0; i < nmine; ++i) {
     if (roots[i].score < threshold)
@@ -540,7 +586,7 @@ static int search_impl(const orc_map* m, const bbs_aabb* map_bbox, const double*
   int active = 1;
 #define EXCHANGE()                                                      \
   do {                                                                  \
-    if (shard && shard->allreduce_max) {                                \
+    if (shard && shard->allreduce_max && !exact) {                      \
       int64_t v[2] = {best, active};                                    \
       if (shard->allreduce_max(v, 2, shard->user)) {                    \
         st = BBS_ERR_GENERIC;                                           \
@@ -582,7 +628,21 @@ static int search_impl(const orc_map* m, const bbs_aabb* map_bbox, const double*
     }
     if (flushed) {
       /* flush, search.hpp:132-143 */
-      for (uint64_t i = 0; i < np; ++i) score_node(m, g, L, scan, k, &pending[i]);
+      if (exact) {
+        /* runs of 8 children dealt round-robin (csrc/search.cu RunSplit) */
+        for (uint64_t i = 0; i < np; ++i) {
+          if ((int)((i / 8) % (uint64_t)world) == rank)
+            score_node(m, g, L, scan, k, &pending[i]);
+          else
+            pending[i].score = -1;
+        }
+        if (exchange_scores(shard, pending, np)) {
+          st = BBS_ERR_GENERIC;
+          goto done;
+        }
+      } else {
+        for (uint64_t i = 0; i < np; ++i) score_node(m, g, L, scan, k, &pending[i]);
+      }
       stats->batches_flushed++;
       for (uint64_t i = 0; i < np; ++i) {
         if (pending[i].score < best)
@@ -596,7 +656,7 @@ static int search_impl(const orc_map* m, const bbs_aabb* map_bbox, const double*
   }
   /* this rank is done; keep answering exchanges until every rank is */
   active = 0;
-  if (shard && shard->allreduce_max) {
+  if (shard && shard->allreduce_max && !exact) {
     do {
       EXCHANGE();
     } while (others_active);
@@ -614,7 +674,7 @@ static int search_impl(const orc_map* m, const bbs_aabb* map_bbox, const double*
   }
 
   /* winner election (sharded): max of (score, world-1-rank) among matched */
-  if (shard && shard->allreduce_max && world > 1) {
+  if (shard && shard->allreduce_max && world > 1 && !exact) {
     int64_t key[1] = {matched ? ((int64_t)best << 32) | (int64_t)(world - 1 - rank) : -1};
     if (shard->allreduce_max(key, 1, shard->user)) {
       st = BBS_ERR_GENERIC;

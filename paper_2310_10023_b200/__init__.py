@@ -31,7 +31,7 @@ __all__ = [
     "InfeasiblePoseError", "ConfigError", "CudaError", "InvalidArgumentError",
     "Strategy", "BranchMode", "Layout", "SearchConfig", "Stats", "SearchResult", "Pose6",
     "AxisGrid", "AngularGrid", "LevelMap", "MultiResVoxelMap", "DeviceScan", "NODE_DTYPE",
-    "batch_evaluate", "search", "search_sharded", "localize_scan", "prepare_source",
+    "batch_evaluate", "search", "search_sharded", "Comm", "nccl_version", "localize_scan", "prepare_source",
     "max_range", "bounding_box", "pose_to_transform", "node_pose", "initial_node_count",
     "gen_scene", "gen_scans", "cut_scan", "SceneSpec", "device_count",
 ]
@@ -628,22 +628,71 @@ def search_scan(vmap: MultiResVoxelMap, dscan: DeviceScan, cfg: SearchConfig,
     return _result_from_c(res, buf)
 
 
-def search_sharded(vmap: MultiResVoxelMap, dscan: DeviceScan, cfg: SearchConfig, rank, world,
-                   allreduce_max, trace_capacity=1 << 16):
-    """Root-sharded search.  allreduce_max(list_of_int64) ->
-    element-wise max over ranks (e.g. torch.distributed all_reduce MAX)."""
-    def _cb(values, count, _user):
-        try:
-            vals = [values[i] for i in range(count)]
-            out = allreduce_max(vals)
-            for i in range(count):
-                values[i] = int(out[i])
-            return 0
-        except Exception:  # noqa: BLE001 - reported through the status code
-            return 1
+class Comm:
+    """NCCL communicator for the device-side exchanges of a sharded search
+    (bbs_comm_t).  Rank 0 draws ``Comm.unique_id()``; every rank builds
+    ``Comm(device, rank, world, uid)`` collectively."""
 
-    cb = _abi.ALLREDUCE_MAX_FN(_cb)
-    shard = Shard(int(rank), int(world), cb, None)
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = (C.c_uint8 * 128)()
+        _check(lib.bbs_comm_unique_id(buf))
+        return bytes(buf)
+
+    def __init__(self, device: int, rank: int, world: int, uid: bytes):
+        if len(uid) != 128:
+            raise ValueError("NCCL unique id must be 128 bytes")
+        self._h = C.c_void_p()
+        buf = (C.c_uint8 * 128).from_buffer_copy(uid)
+        _check(lib.bbs_comm_init(int(device), int(rank), int(world), buf, C.byref(self._h)))
+        self.rank, self.world = int(rank), int(world)
+
+    def close(self):
+        if self._h:
+            lib.bbs_comm_free(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001
+            pass
+
+
+def nccl_version() -> int:
+    """Version of the NCCL the library loads (0 when none can be loaded)."""
+    return int(lib.bbs_nccl_version())
+
+
+def search_sharded(vmap: MultiResVoxelMap, dscan: DeviceScan, cfg: SearchConfig, rank, world,
+                   allreduce_max=None, trace_capacity=1 << 16, mode="roots",
+                   comm: Optional[Comm] = None):
+    """Sharded search (include/bbs.h bbs_search_sharded).
+
+    mode "roots": each rank runs its own BnB over its root share, the
+    incumbent is max-all-reduced every epoch and the winner elected.
+    mode "exact": batch-split replay of the single-queue schedule; every rank
+    returns the unsharded search() result.
+    Exchanges go through ``comm`` (NCCL on the device) when given, else
+    through ``allreduce_max(list_of_int64) -> element-wise max over ranks``
+    (e.g. torch.distributed all_reduce MAX on the host)."""
+    if mode not in ("roots", "exact"):
+        raise ValueError(f"unknown shard mode {mode!r}")
+    cb = _abi.ALLREDUCE_MAX_FN()
+    if allreduce_max is not None:
+        def _cb(values, count, _user):
+            try:
+                vals = [values[i] for i in range(count)]
+                out = allreduce_max(vals)
+                for i in range(count):
+                    values[i] = int(out[i])
+                return 0
+            except Exception:  # noqa: BLE001 - reported through the status code
+                return 1
+        cb = _abi.ALLREDUCE_MAX_FN(_cb)
+    shard = Shard(int(rank), int(world), cb, None,
+                  _abi.SHARD_EXACT if mode == "exact" else _abi.SHARD_ROOTS, 0,
+                  comm._h if comm is not None else None)
     res, buf = _new_result(trace_capacity if cfg.collect_trace else 0)
     c = cfg.to_c()
     _check(lib.bbs_search_sharded(vmap._h, dscan._h, C.byref(c), C.byref(shard), C.byref(res)))

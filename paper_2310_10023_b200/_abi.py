@@ -135,7 +135,14 @@ class Shard(C.Structure):
         ("world_size", C.c_int32),
         ("allreduce_max", ALLREDUCE_MAX_FN),
         ("user", C.c_void_p),
+        ("mode", C.c_int32),
+        ("reserved", C.c_int32),
+        ("comm", C.c_void_p),
     ]
+
+
+SHARD_ROOTS = 0  # BBS_SHARD_ROOTS: own BnB per rank over its root share
+SHARD_EXACT = 1  # BBS_SHARD_EXACT: batch-split replay of the single-queue schedule
 
 
 NODE_DTYPE_FIELDS = ("ix", "iy", "iz", "iroll", "ipitch", "iyaw", "level", "score")

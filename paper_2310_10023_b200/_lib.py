@@ -72,6 +72,10 @@ SIGNATURES = {
     "bbs_stream_destroy": (C.c_int, [_vp]),
     "bbs_search_sharded": (C.c_int, [_vp, _vp, C.POINTER(SearchConfigC), C.POINTER(Shard),
                                      C.POINTER(SearchResultC)]),
+    "bbs_comm_unique_id": (C.c_int, [C.POINTER(C.c_uint8)]),
+    "bbs_comm_init": (C.c_int, [_i32, _i32, _i32, C.POINTER(C.c_uint8), C.POINTER(_vp)]),
+    "bbs_comm_free": (C.c_int, [_vp]),
+    "bbs_nccl_version": (C.c_int, []),
     "bbs_scene_spec_default": (None, [_vp]),
     "bbs_gen_scene": (C.c_int, [_vp, _u64, C.POINTER(_dp), C.POINTER(_u64), C.POINTER(_dp),
                                 C.POINTER(_u64), _dp]),
@@ -87,7 +91,7 @@ for _name, (_res, _args) in SIGNATURES.items():
     _f.restype = _res
     _f.argtypes = _args
 
-ABI_VERSION = 2  # include/bbs.h BBS_ABI_VERSION this mirror was written for
+ABI_VERSION = 3  # include/bbs.h BBS_ABI_VERSION this mirror was written for
 if lib.bbs_abi_version() != ABI_VERSION:
     raise ImportError(f"{LIB_PATH} has ABI version {lib.bbs_abi_version()}, "
                       f"the Python mirror expects {ABI_VERSION}: rebuild the library")

@@ -12,6 +12,7 @@
 #include <new>
 #include <string>
 
+#include "bbs_comm.h"
 #include "bbs_map_impl.h"
 
 namespace bbs {
@@ -341,11 +342,39 @@ int bbs_stream_destroy(void* stream) {
   });
 }
 
+int bbs_comm_unique_id(uint8_t id[128]) {
+  return guard([&] {
+    REQUIRE(id, "null argument");
+    bbs::comm_unique_id(id);
+  });
+}
+
+int bbs_comm_init(int32_t device, int32_t rank, int32_t world_size, const uint8_t id[128],
+                  bbs_comm_t* out) {
+  return guard([&] {
+    REQUIRE(id && out, "null argument");
+    *out = reinterpret_cast<bbs_comm_t>(bbs::comm_create(device, rank, world_size, id));
+  });
+}
+
+int bbs_comm_free(bbs_comm_t comm) {
+  return guard([&] { bbs::comm_destroy(reinterpret_cast<bbs::Comm*>(comm)); });
+}
+
+int bbs_nccl_version(void) { return bbs::comm_nccl_version(); }
+
 int bbs_search_sharded(bbs_map_t map, bbs_scan_t scan, const bbs_search_config* cfg,
                        const bbs_shard* shard, bbs_search_result* result) {
   return guard([&] {
     REQUIRE(map && scan && cfg && result && shard, "null argument");
     REQUIRE(scan->map == map, "scan was uploaded for a different map");
+    REQUIRE(shard->mode == BBS_SHARD_ROOTS || shard->mode == BBS_SHARD_EXACT, "unknown shard mode");
+    if (shard->comm) {
+      const bbs::Comm* c = reinterpret_cast<const bbs::Comm*>(shard->comm);
+      REQUIRE(c->rank == shard->rank && c->world == shard->world_size,
+              "shard rank/world_size differ from the communicator's");
+      REQUIRE(c->device == map->device, "communicator is on a different device than the map");
+    }
     bbs::run_search(map, scan, *cfg, shard, result);
   });
 }

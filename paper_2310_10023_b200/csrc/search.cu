@@ -27,6 +27,7 @@
 #include <limits>
 #include <vector>
 
+#include "bbs_comm.h"
 #include "bbs_map_impl.h"
 #include "device_common.cuh"
 #include "kernels.h"
@@ -57,14 +58,22 @@ struct EpochState {
   uint32_t n_keep;         // queue remainder kept after the incumbent trim
   uint32_t surv_ticket;    // survivors tile tickets (reset by the frontier)
   uint32_t merge_done;     // merge CTAs finished (the last one finalizes the epoch)
+  uint32_t n_own;          // batch-split exact mode: children of this rank's runs
+  int32_t any_active;      // sharded (device exchange): any rank still active
   unsigned long long level_evals[kMaxLevels];  // flush evaluations per level
   // kept ranges of the remainder: one per key segment (BFS: 1, DFS: level)
   uint32_t seg_lo[kMaxLevels], seg_len[kMaxLevels], seg_pre[kMaxLevels + 1];
 };
 
+// The queue is a sorted array of 64-bit keys (double-buffered); a key embeds
+// its entry's insertion seq, and the entry's node lives at pool[seq] (an
+// append-only pool written once per push), so re-ordering moves 8 B keys.
 struct Queue {
   unsigned long long* key[2];
-  bbs_node* node[2];
+  bbs_node* pool;
+  // select, not index: a runtime index into a by-value kernel parameter
+  // array makes the compiler copy the struct to local memory
+  __device__ __forceinline__ unsigned long long* keys(uint32_t b) const { return b ? key[1] : key[0]; }
 };
 
 __device__ __forceinline__ unsigned long long queue_key(int strategy, int32_t score, int32_t level,
@@ -73,6 +82,11 @@ __device__ __forceinline__ unsigned long long queue_key(int strategy, int32_t sc
   if (strategy == BBS_STRATEGY_BFS)
     return (s << 44) | (static_cast<unsigned long long>(15 - level) << 40) | seq;
   return (static_cast<unsigned long long>(level) << 60) | (s << 40) | (kSeqMax - seq);
+}
+
+__device__ __forceinline__ uint32_t key_seq(int strategy, unsigned long long key) {
+  const unsigned long long low = key & kSeqMax;
+  return static_cast<uint32_t>(strategy == BBS_STRATEGY_BFS ? low : kSeqMax - low);
 }
 
 // Per-axis in-range rotational children of branch(), nodes.hpp:99-111.
@@ -130,7 +144,8 @@ __global__ void __launch_bounds__(kFT) frontier_kernel(EpochState* st, Queue q, 
     return;
   }
   const uint32_t qlen = st->q_len;
-  const bbs_node* __restrict__ nodes = q.node[st->cur];
+  const unsigned long long* __restrict__ qk = q.keys(st->cur);
+  const bbs_node* __restrict__ pool = q.pool;
   int carry_best = st->best;
   unsigned long long carry_sum = 0, carry_trace = st->trace_len;
   uint32_t carry_exp = 0;
@@ -147,7 +162,7 @@ __global__ void __launch_bounds__(kFT) frontier_kernel(EpochState* st, Queue q, 
       const uint32_t i = base + tid * kFIPT + k;
       valid[k] = i < qlen;
       if (valid[k]) {
-        nd[k] = nodes[i];
+        nd[k] = pool[key_seq(strategy, qk[i])];
         if (nd[k].level == 0) lm = max(lm, nd[k].score);
       }
     }
@@ -215,7 +230,7 @@ __global__ void __launch_bounds__(kFT) frontier_kernel(EpochState* st, Queue q, 
       const long long i = base + tid * kFIPT + k;
       if (!valid[k] || i > limit) continue;
       if (c[k]) {
-        exp_parent[carry_exp + epos] = static_cast<uint32_t>(i);
+        exp_parent[carry_exp + epos] = key_seq(strategy, qk[i]);  // the parent's pool slot
         exp_off[carry_exp + epos] = static_cast<uint32_t>(sbefore[k]);
         ++epos;
       }
@@ -230,7 +245,7 @@ __global__ void __launch_bounds__(kFT) frontier_kernel(EpochState* st, Queue q, 
     __syncthreads();
     if (s_lastlu >= 0) {
       best_i = s_lastlu;
-      carry_best = nodes[best_i].score;  // leaf updates are non-decreasing
+      carry_best = pool[key_seq(strategy, qk[best_i])].score;  // leaf updates are non-decreasing
     }
     carry_exp += static_cast<uint32_t>(etot);
     carry_trace += static_cast<unsigned long long>(ttot);
@@ -271,7 +286,7 @@ __global__ void __launch_bounds__(kFT) frontier_kernel(EpochState* st, Queue q, 
     st->n_expand = carry_exp;
     st->n_children = static_cast<uint32_t>(carry_sum);
     if (best_i >= 0) {
-      st->best_node = nodes[best_i];
+      st->best_node = pool[key_seq(strategy, qk[best_i])];
       st->matched = 1;
       st->last_best_epoch = static_cast<int32_t>(st->pass);
     }
@@ -290,16 +305,31 @@ __global__ void __launch_bounds__(kFT) frontier_kernel(EpochState* st, Queue q, 
 
 // E2: branch() (nodes.hpp:91-121) for every expanding parent, children in
 // pop order, each parent's children in (jr, jp, jw, jx, jy, jz) order.
-__global__ void branch_kernel(const EpochState* st, Queue q, GridView G,
+// Batch-split exact mode: the flush's runs of 8 children are
+// dealt round-robin over the ranks; this rank scores its runs from a compact
+// copy (pending_own) and the scores are scattered back and max-all-reduced.
+struct RunSplit {
+  bbs_node* pending_own;
+  int32_t* pscores_own;
+  uint32_t rank, world;  // world == 0: no split
+};
+
+__device__ __forceinline__ uint32_t own_children(uint32_t n, uint32_t rank, uint32_t world) {
+  const uint32_t runs = n >> 3;
+  return runs > rank ? ((runs - rank + world - 1) / world) * 8u : 0u;
+}
+
+__global__ void branch_kernel(EpochState* st, Queue q, GridView G,
                               const uint32_t* __restrict__ exp_parent,
                               const uint32_t* __restrict__ exp_off, bbs_node* __restrict__ pending,
-                              int32_t* __restrict__ pscores, RotCache cache) {
+                              int32_t* __restrict__ pscores, RotCache cache, RunSplit split) {
   pdl_wait();
 
   const uint32_t n = st->n_children;
+  if (split.world && blockIdx.x == 0 && threadIdx.x == 0) st->n_own = own_children(n, split.rank, split.world);
   if (n == 0) return;
   const uint32_t ne = st->n_expand;
-  const bbs_node* __restrict__ nodes = q.node[st->cur];
+  const bbs_node* __restrict__ pool = q.pool;
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     uint32_t lo = 0, hi = ne - 1;  // largest m with exp_off[m] <= i
     while (lo < hi) {
@@ -309,7 +339,7 @@ __global__ void branch_kernel(const EpochState* st, Queue q, GridView G,
       else
         hi = mid - 1;
     }
-    const bbs_node p = nodes[exp_parent[lo]];
+    const bbs_node p = pool[exp_parent[lo]];
     const uint32_t local = i - exp_off[lo];
     int32_t a[3], c[3];
     child_counts(G, p, a, c);
@@ -327,10 +357,22 @@ __global__ void branch_kernel(const EpochState* st, Queue q, GridView G,
     ch.level = p.level - 1;
     ch.score = -1;
     pending[i] = ch;
-    pscores[i] = 0;  // the flush kernels accumulate into it
+    bool own = true;
+    if (split.world) {
+      const uint32_t run = i >> 3;
+      own = run % split.world == split.rank;
+      pscores[i] = -1;  // other ranks' runs: filled by the max-all-reduce
+      if (own) {
+        const uint32_t j = (run / split.world) * 8u + t;
+        split.pending_own[j] = ch;
+        split.pscores_own[j] = 0;
+      }
+    } else {
+      pscores[i] = 0;  // the flush kernels accumulate into it
+    }
     // first child of a run (8 translation siblings): claim its rotation's
     // histogram slot (epoch_cache.cu)
-    if (cache.enabled && t == 0)
+    if (cache.enabled && t == 0 && own)
       cache_claim_run(cache, G, make_int4(ch.ix, ch.iy, ch.iz, ch.iroll),
                       make_int4(ch.ipitch, ch.iyaw, ch.level, ch.score));
   }
@@ -363,7 +405,7 @@ __device__ void trim_remainder(EpochState* st, const Queue& q, int strategy, int
   const int lane = threadIdx.x & 31;
   const uint32_t n_cons = st->n_cons;
   const uint32_t n_rem = st->q_len - n_cons;
-  const unsigned long long* qk = q.key[st->cur] + n_cons;
+  const unsigned long long* qk = q.keys(st->cur) + n_cons;
   const int nseg = strategy == BBS_STRATEGY_BFS ? 1 : kMaxLevels;
   uint32_t lo = 0, hi = 0;
   if (lane < nseg) {
@@ -411,7 +453,6 @@ __global__ void __launch_bounds__(kST) survivors_kernel(EpochState* st, Queue q,
                                                         const bbs_node* __restrict__ pending,
                                                         const int32_t* __restrict__ scores,
                                                         unsigned long long* __restrict__ s_key,
-                                                        bbs_node* __restrict__ s_node,
                                                         unsigned long long* __restrict__ tiles) {
   pdl_wait();
 
@@ -493,7 +534,7 @@ __global__ void __launch_bounds__(kST) survivors_kernel(EpochState* st, Queue q,
       const uint32_t i = base + threadIdx.x * kSIPT + k;
       bbs_node nd = pending[i];
       nd.score = sc[k];
-      s_node[o] = nd;
+      q.pool[seq0 + o] = nd;  // push: the node's permanent slot
       s_key[o] = queue_key(strategy, nd.score, nd.level, seq0 + o);
       ++o;
     }
@@ -505,9 +546,7 @@ __global__ void __launch_bounds__(kST) survivors_kernel(EpochState* st, Queue q,
 constexpr int kRT = 256;
 __global__ void __launch_bounds__(kRT) rank_sort_kernel(const EpochState* st,
                                                         const unsigned long long* __restrict__ key,
-                                                        const bbs_node* __restrict__ node,
-                                                        unsigned long long* __restrict__ out_key,
-                                                        bbs_node* __restrict__ out_node) {
+                                                        unsigned long long* __restrict__ out_key) {
   pdl_wait();
 
   __shared__ unsigned long long tile[kRT];
@@ -525,18 +564,19 @@ __global__ void __launch_bounds__(kRT) rank_sort_kernel(const EpochState* st,
 #pragma unroll 8
       for (uint32_t i = 0; i < lim; ++i) rank += tile[i] < kj ? 1u : 0u;
     }
-    if (j < n) {
-      out_key[rank] = kj;
-      out_node[rank] = node[j];
-    }
+    if (j < n) out_key[rank] = kj;
   }
 }
 
 // E6: merge the sorted survivors into the trimmed queue remainder (push,
 // search.hpp:139).  The remainder is read through the kept segment ranges.
+// Keys only (nodes stay in the pool).  A thread moves kMIPT consecutive
+// remainder keys: one binary search into the survivors for the first, then a
+// forward walk (both sides are sorted); each survivor finds its place in its
+// remainder segment by binary search.
+constexpr uint32_t kMIPT = 8;
 __global__ void merge_kernel(EpochState* st, Queue q, int strategy,
-                             const unsigned long long* __restrict__ skey,
-                             const bbs_node* __restrict__ snode) {
+                             const unsigned long long* __restrict__ skey) {
   pdl_wait();
 
   __shared__ uint32_t s_lo[kMaxLevels], s_len[kMaxLevels], s_pre[kMaxLevels + 1];
@@ -551,29 +591,35 @@ __global__ void merge_kernel(EpochState* st, Queue q, int strategy,
   const uint32_t cur = st->cur;
   const uint32_t n_keep = st->n_keep;
   const uint32_t n_s = st->n_surv;
-  const unsigned long long* __restrict__ qk = q.key[cur] + st->n_cons;
-  const bbs_node* __restrict__ qn = q.node[cur] + st->n_cons;
-  unsigned long long* __restrict__ ok = q.key[cur ^ 1];
-  bbs_node* __restrict__ on = q.node[cur ^ 1];
-  const uint32_t total = n_keep + n_s;
+  const unsigned long long* __restrict__ qk = q.keys(cur) + st->n_cons;
+  unsigned long long* __restrict__ ok = q.keys(cur ^ 1u);
   const bool bfs = strategy == BBS_STRATEGY_BFS;
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
-    if (i < n_keep) {
+  const uint32_t n_kitems = (n_keep + kMIPT - 1) / kMIPT;
+  const uint32_t items = n_kitems + n_s;
+  for (uint32_t it = blockIdx.x * blockDim.x + threadIdx.x; it < items; it += gridDim.x * blockDim.x) {
+    if (it < n_kitems) {
+      uint32_t i = it * kMIPT;
+      const uint32_t iend = min(i + kMIPT, n_keep);
       int sg = 0;
-      if (!bfs)
-        while (s_pre[sg + 1] <= i) ++sg;
-      const uint32_t src = s_lo[sg] + (i - s_pre[sg]);
-      const unsigned long long k = qk[src];
-      const uint32_t pos = i + lower_bound_u64(skey, n_s, k);
-      ok[pos] = k;
-      on[pos] = qn[src];
+      uint32_t p = 0;
+      bool first = true;
+      for (; i < iend; ++i) {
+        if (!bfs)
+          while (s_pre[sg + 1] <= i) ++sg;
+        const unsigned long long k = qk[s_lo[sg] + (i - s_pre[sg])];
+        if (first) {
+          p = lower_bound_u64(skey, n_s, k);
+          first = false;
+        } else {
+          while (p < n_s && skey[p] < k) ++p;
+        }
+        ok[i + p] = k;
+      }
     } else {
-      const uint32_t j = i - n_keep;
+      const uint32_t j = it - n_kitems;
       const unsigned long long k = skey[j];
       const int sg = bfs ? 0 : static_cast<int>(k >> 60);
-      const uint32_t pos = j + s_pre[sg] + lower_bound_u64(qk + s_lo[sg], s_len[sg], k);
-      ok[pos] = k;
-      on[pos] = snode[j];
+      ok[j + s_pre[sg] + lower_bound_u64(qk + s_lo[sg], s_len[sg], k)] = k;
     }
   }
   // E7 (last CTA): swap queue buffers; the loop ends when queue and pending
@@ -594,6 +640,24 @@ __global__ void merge_kernel(EpochState* st, Queue q, int strategy,
 }
 
 
+
+// Exact mode: this rank's run scores back to their pending positions.
+__global__ void scatter_own_kernel(const EpochState* st, RunSplit split, int32_t* __restrict__ pscores) {
+  pdl_wait();
+  const uint32_t n = st->n_own;
+  for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x)
+    pscores[((j >> 3) * split.world + split.rank) * 8u + (j & 7u)] = split.pscores_own[j];
+}
+
+// Roots mode, device exchange: {incumbent, active} out, max-reduced back in.
+__global__ void xchg_pack_kernel(const EpochState* st, int32_t* x) {
+  x[0] = st->best;
+  x[1] = st->active;
+}
+__global__ void xchg_unpack_kernel(EpochState* st, const int32_t* x) {
+  if (x[0] > st->best) st->best = x[0];
+  st->any_active = x[1];
+}
 
 // Root survivors -> queue entries (seq = rank in initial_nodes order).  All
 // roots share one level, so the queue order is (score desc, seq asc) for BFS
@@ -623,13 +687,11 @@ __global__ void roots_to_queue_kernel(const unsigned long long* __restrict__ ref
   }
 }
 
-__global__ void gather_nodes_kernel(const uint32_t* __restrict__ perm, const bbs_node* __restrict__ in,
-                                    int strategy, bbs_node* __restrict__ out,
-                                    unsigned long long* __restrict__ key, uint32_t n) {
+__global__ void queue_keys_kernel(const uint32_t* __restrict__ perm, const bbs_node* __restrict__ pool,
+                                  int strategy, unsigned long long* __restrict__ key, uint32_t n) {
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     const uint32_t seq = perm[i];
-    const bbs_node nd = in[seq];
-    out[i] = nd;
+    const bbs_node nd = pool[seq];
     key[i] = queue_key(strategy, nd.score, nd.level, seq);
   }
 }
@@ -709,9 +771,9 @@ struct Workspace {
   Buf<unsigned long long> probes, surv_idx, qk0, qk1, s_key, s_key2, surv_tiles;
   Buf<int> nsel;
   Buf<unsigned char> temp;
-  Buf<bbs_node> n0, qn0, qn1, pending, s_node, s_node2;
+  Buf<bbs_node> pool, pending, pending_own;
   Buf<uint32_t> perm0, perm1, sk0, sk1, exp_parent, exp_off;
-  Buf<int32_t> pscores, trace, hist_n;
+  Buf<int32_t> pscores, trace, hist_n, pscores_own, xchg;
   Buf<int4> hist_ent, cache_info, cache_pool, cache_builds;
   Buf<uint32_t> cache_u32, cache_amb, cache_fb, stage_win;
   Buf<int32_t> cache_builds_w;
@@ -730,9 +792,9 @@ struct Workspace {
     return ev[ev_used++];
   }
   void release_all() {
-    for (auto* b : {&root_scores, &pscores, &trace, &hist_n}) b->release();
+    for (auto* b : {&root_scores, &pscores, &trace, &hist_n, &pscores_own, &xchg}) b->release();
     for (auto* b : {&probes, &surv_idx, &qk0, &qk1, &s_key, &s_key2, &surv_tiles}) b->release();
-    for (auto* b : {&n0, &qn0, &qn1, &pending, &s_node, &s_node2}) b->release();
+    for (auto* b : {&pool, &pending, &pending_own}) b->release();
     for (auto* b : {&perm0, &perm1, &sk0, &sk1, &exp_parent, &exp_off, &hist_amb}) b->release();
     lut.release();
     nsel.release();
@@ -843,6 +905,15 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
   const int rank = shard ? shard->rank : 0;
   const int world = shard ? std::max(1, shard->world_size) : 1;
   if (rank < 0 || rank >= world) throw Error(BBS_ERR_CONFIG, "search: shard rank out of range");
+  // exchanges: on the device through NCCL when a communicator is
+  // given, else through the caller's host all-reduce
+  const bool exact = shard && shard->mode == BBS_SHARD_EXACT;
+  Comm* comm = shard ? reinterpret_cast<Comm*>(shard->comm) : nullptr;
+  const bool host_x = shard && !comm && shard->allreduce_max;
+  if (exact && world > 1 && !comm && !host_x)
+    throw Error(BBS_ERR_CONFIG, "search: the exact shard mode needs an all-reduce");
+  const bool roots_dev_x = comm && !exact;    // incumbent exchange every epoch, on the device
+  const bool roots_host_x = host_x && !exact; // ... on the host
 
   DeviceGuard dg(m->device);
   Lease lease(m);
@@ -852,6 +923,35 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
   const int32_t threshold =
       static_cast<int32_t>(std::floor(cfg.score_threshold_fraction * static_cast<double>(K)));
   const int L = cfg.max_level;
+  uint64_t h2d = 0, d2h = 0;
+
+  // in-place element-wise MAX of n int32 over the ranks (same call count on
+  // every rank: the sizes below are identical across ranks)
+  std::vector<int32_t> xh;
+  std::vector<int64_t> xw;
+  auto xmax = [&](int32_t* d, size_t n) {
+    if (n == 0) return;
+    if (comm) {
+      comm_allreduce_max_i32(comm, d, n, s);
+      return;
+    }
+    if (!host_x) return;
+    xh.resize(n);
+    BBS_CUDA(cudaMemcpyAsync(xh.data(), d, n * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    BBS_CUDA(cudaStreamSynchronize(s));
+    d2h += n * sizeof(int32_t);
+    constexpr size_t kChunk = size_t(1) << 24;
+    for (size_t o = 0; o < n; o += kChunk) {
+      const size_t c = std::min(kChunk, n - o);
+      xw.assign(xh.begin() + o, xh.begin() + o + c);
+      if (shard->allreduce_max(xw.data(), static_cast<int32_t>(c), shard->user) != 0)
+        throw Error(BBS_ERR_GENERIC, "search: score all-reduce failed");
+      for (size_t i = 0; i < c; ++i) xh[o + i] = static_cast<int32_t>(xw[i]);
+    }
+    BBS_CUDA(cudaMemcpyAsync(d, xh.data(), n * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+    BBS_CUDA(cudaStreamSynchronize(s));
+    h2d += n * sizeof(int32_t);
+  };
 
   // root set, initial_nodes (nodes.hpp:60-85)
   const double cell = std::ldexp(cfg.min_resolution, L);
@@ -883,7 +983,7 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
   const uint64_t maxc = max_children(grid);
   const uint64_t pend_cap = cfg.batch_size + maxc;
   const int strategy = cfg.strategy;
-  uint64_t h2d = lut.size() * sizeof(double), d2h = 0;
+  h2d += lut.size() * sizeof(double);
   uint64_t launches = 0;
 
   cudaEvent_t ev_start = W.next_event(), ev_roots0 = W.next_event(), ev_roots1 = W.next_event(),
@@ -939,9 +1039,12 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
     launches += 3 * ((nrot + kRotBatch - 1) / kRotBatch);
   }
   BBS_CUDA(cudaEventRecord(ev_roots1, s));
+  // exact mode: every rank gets every root score (unowned roots are -1)
+  if (exact) xmax(root_scores, static_cast<size_t>(std::max<int64_t>(total, 0)));
+  const uint64_t n_scored_roots = exact ? static_cast<uint64_t>(std::max<int64_t>(total, 0)) : n_own;
 
   // survivors >= threshold among own roots, in initial_nodes order
-  unsigned long long* surv_idx = W.surv_idx.get(static_cast<size_t>(std::max<uint64_t>(n_own, 1)), s);
+  unsigned long long* surv_idx = W.surv_idx.get(static_cast<size_t>(std::max<uint64_t>(n_scored_roots, 1)), s);
   int n_root_surv = 0;
   if (total > 0) {
     cub::CountingInputIterator<unsigned long long> cnt(0);
@@ -962,14 +1065,16 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
   const unsigned long long root_probes = W.h_small[0];
 
   // queue buffers
-  const int E = (shard && shard->allreduce_max) ? 1 : 8;  // epochs per host check
+  const int E = host_x ? 1 : 8;  // epochs per host check
   uint64_t qcap = static_cast<uint64_t>(n_root_surv) + static_cast<uint64_t>(E + 1) * pend_cap;
   Queue q{};
   q.key[0] = W.qk0.get(qcap, s);
   q.key[1] = W.qk1.get(qcap, s);
-  q.node[0] = W.qn0.get(qcap, s);
-  q.node[1] = W.qn1.get(qcap, s);
-  qcap = std::min({W.qk0.cap, W.qk1.cap, W.qn0.cap, W.qn1.cap});
+  qcap = std::min(W.qk0.cap, W.qk1.cap);
+  // node pool: one slot per push (seq), roots first in initial_nodes order
+  uint64_t pool_cap = static_cast<uint64_t>(n_root_surv) + static_cast<uint64_t>(E + 1) * pend_cap;
+  q.pool = W.pool.get(pool_cap, s);
+  pool_cap = W.pool.cap;
   if (n_root_surv > 0) {
     // nodes in initial_nodes order (seq = position), stable sort on the
     // score key over only the bits it spans, then gather nodes + queue keys
@@ -979,7 +1084,7 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
     while (end_bit < 32 && (span >> end_bit) != 0) ++end_bit;
     uint32_t* sk0 = W.sk0.get(n_root_surv, s);
     uint32_t* sk1 = W.sk1.get(n_root_surv, s);
-    bbs_node* n0 = W.n0.get(n_root_surv, s);
+    bbs_node* n0 = q.pool;  // pool[seq] = root with rank seq among the survivors
     uint32_t* perm0 = W.perm0.get(n_root_surv, s);
     uint32_t* perm1 = W.perm1.get(n_root_surv, s);
     roots_to_queue_kernel<<<grid1(n_root_surv), 256, 0, s>>>(surv_idx, n_root_surv, root_scores, bp,
@@ -991,8 +1096,7 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
     BBS_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, dk, dv, n_root_surv, 0, end_bit, s));
     void* temp = W.temp.get(tb, s);
     BBS_CUDA(cub::DeviceRadixSort::SortPairs(temp, tb, dk, dv, n_root_surv, 0, end_bit, s));
-    gather_nodes_kernel<<<grid1(n_root_surv), 256, 0, s>>>(dv.Current(), n0, strategy, q.node[0], q.key[0],
-                                                           n_root_surv);
+    queue_keys_kernel<<<grid1(n_root_surv), 256, 0, s>>>(dv.Current(), n0, strategy, q.key[0], n_root_surv);
     BBS_CUDA(cudaGetLastError());
     launches += 2;  // roots_to_queue, gather
   }
@@ -1002,11 +1106,12 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
   h0.q_len = static_cast<uint32_t>(n_root_surv);
   h0.cur = 0;
   h0.seq = static_cast<unsigned long long>(n_root_surv);
-  h0.nodes_generated = n_own;
-  h0.nodes_pruned = n_own - static_cast<uint64_t>(n_root_surv);
+  h0.nodes_generated = n_scored_roots;
+  h0.nodes_pruned = n_scored_roots - static_cast<uint64_t>(n_root_surv);
   h0.batches_flushed = 1;
   h0.last_best_epoch = -1;
   h0.active = n_root_surv > 0 ? 1 : 0;
+  h0.any_active = h0.active;
   h0.q_peak = h0.q_len;
   EpochState* d_st = W.st.get(1, s);
   *W.h_st = h0;
@@ -1016,6 +1121,16 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
 
   bbs_node* pending = W.pending.get(pend_cap, s);
   int32_t* pscores = W.pscores.get(pend_cap, s);
+  // exact mode: this rank's runs are scored from a compact copy
+  RunSplit split{};
+  if (exact) {
+    const uint64_t own_cap = ((pend_cap / 8) / world + 2) * 8;
+    split.pending_own = W.pending_own.get(own_cap, s);
+    split.pscores_own = W.pscores_own.get(own_cap, s);
+    split.rank = static_cast<uint32_t>(rank);
+    split.world = static_cast<uint32_t>(world);
+  }
+  int32_t* d_x = W.xchg.get(2, s);
   const uint64_t n_surv_tiles = (pend_cap + kSTile - 1) / kSTile;
   unsigned long long* surv_tiles = W.surv_tiles.get(n_surv_tiles, s);
   BBS_CUDA(cudaMemsetAsync(surv_tiles, 0, n_surv_tiles * sizeof(unsigned long long), s));
@@ -1024,9 +1139,7 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
   uint32_t* exp_parent = W.exp_parent.get(exp_cap, s);
   uint32_t* exp_off = W.exp_off.get(exp_cap, s);
   unsigned long long* s_key = W.s_key.get(pend_cap, s);
-  bbs_node* s_node = W.s_node.get(pend_cap, s);
   unsigned long long* s_key2 = W.s_key2.get(pend_cap, s);
-  bbs_node* s_node2 = W.s_node2.get(pend_cap, s);
   const uint64_t trace_cap = cfg.collect_trace ? std::max<uint64_t>(out->trace_capacity, 1) : 0;
   int32_t* d_trace = W.trace.get(std::max<uint64_t>(trace_cap, 1), s);
   const uint32_t ptiles = choose_ptiles((pend_cap + 7) / 8, static_cast<uint32_t>(K));
@@ -1132,8 +1245,8 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
   }
   std::vector<float> pass_ms;  // loop start -> end of each frontier pass
   double esm = 0.0;            // device time in the flush score kernels
-  const uint32_t* d_nchild = reinterpret_cast<const uint32_t*>(reinterpret_cast<char*>(d_st) +
-                                                               offsetof(EpochState, n_children));
+  const uint32_t* d_nchild = reinterpret_cast<const uint32_t*>(
+      reinterpret_cast<char*>(d_st) + (exact ? offsetof(EpochState, n_own) : offsetof(EpochState, n_children)));
   const size_t graph_after = [] {
     const char* v = std::getenv("BBS_GRAPH_AFTER");  // epochs before batches run as graphs
     return v ? static_cast<size_t>(std::atoi(v)) : static_cast<size_t>(24);
@@ -1151,25 +1264,44 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
     BBS_CUDA(cudaGetLastError());
     record(ev_pass[e]);
     launch_pdl(branch_kernel, grid1(pend_cap), 256, 0, s, d_st, q, gv, exp_parent, exp_off, pending, pscores,
-               cache);
+               cache, split);
     BBS_CUDA(cudaGetLastError());
     record(ev_s0[e]);
-    launch_epoch_score(m->view, gv, sv, pending, d_nchild, static_cast<uint32_t>(pend_cap), ptiles,
-                       pscores, cache, s);
-    record(ev_s1[e]);
-    launch_pdl(survivors_kernel, surv_grid, kST, 0, s, d_st, q, strategy, pending, pscores, s_key, s_node,
+    if (exact) {
+      launch_epoch_score(m->view, gv, sv, split.pending_own, d_nchild, static_cast<uint32_t>(pend_cap), ptiles,
+                         split.pscores_own, cache, s);
+      record(ev_s1[e]);
+      launch_pdl(scatter_own_kernel, grid1(pend_cap), 256, 0, s, d_st, split, pscores);
+      BBS_CUDA(cudaGetLastError());
+      ++launches;
+      xmax(pscores, pend_cap);  // every rank: every score of the flush
+    } else {
+      launch_epoch_score(m->view, gv, sv, pending, d_nchild, static_cast<uint32_t>(pend_cap), ptiles,
+                         pscores, cache, s);
+      record(ev_s1[e]);
+    }
+    launch_pdl(survivors_kernel, surv_grid, kST, 0, s, d_st, q, strategy, pending, pscores, s_key,
                surv_tiles);
     BBS_CUDA(cudaGetLastError());
-    launch_pdl(rank_sort_kernel, grid1(pend_cap, kRT), kRT, 0, s, d_st, s_key, s_node, s_key2, s_node2);
+    launch_pdl(rank_sort_kernel, grid1(pend_cap, kRT), kRT, 0, s, d_st, s_key, s_key2);
     BBS_CUDA(cudaGetLastError());
-    launch_pdl(merge_kernel, grid1(qcap), 256, 0, s, d_st, q, strategy, s_key2, s_node2);
+    launch_pdl(merge_kernel, grid1((qcap + kMIPT - 1) / kMIPT), 256, 0, s, d_st, q, strategy, s_key2);
     BBS_CUDA(cudaGetLastError());
     launches += 6;  // frontier, branch, score, survivors, rank_sort, merge (+ finalize)
+    if (roots_dev_x) {  // incumbent + activity over NCCL, no host round-trip
+      xchg_pack_kernel<<<1, 1, 0, s>>>(d_st, d_x);
+      BBS_CUDA(cudaGetLastError());
+      comm_allreduce_max_i32(comm, d_x, 2, s);
+      xchg_unpack_kernel<<<1, 1, 0, s>>>(d_st, d_x);
+      BBS_CUDA(cudaGetLastError());
+      launches += 2;
+    }
   };
   // E epochs as one CUDA graph (all sizes live in EpochState, so the graph is
   // valid until the queue buffers are re-allocated)
   cudaGraphExec_t batch_exec = nullptr;
   uint64_t batch_qcap = 0;
+  const bbs_node* batch_pool = nullptr;
   struct ExecGuard {
     cudaGraphExec_t* e;
     ~ExecGuard() {
@@ -1180,7 +1312,7 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
   bool self_active = h0.active != 0;
   bool others_active = false;
   auto exchange = [&]() {
-    if (!(shard && shard->allreduce_max)) return;
+    if (!roots_host_x) return;
     int64_t v[2] = {hs.best, self_active ? 1 : 0};
     if (shard->allreduce_max(v, 2, shard->user) != 0)
       throw Error(BBS_ERR_GENERIC, "search: incumbent all-reduce failed");
@@ -1195,6 +1327,19 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
     }
   };
   exchange();  // after the root batch
+  if (roots_dev_x) {
+    xchg_pack_kernel<<<1, 1, 0, s>>>(d_st, d_x);
+    BBS_CUDA(cudaGetLastError());
+    comm_allreduce_max_i32(comm, d_x, 2, s);
+    xchg_unpack_kernel<<<1, 1, 0, s>>>(d_st, d_x);
+    BBS_CUDA(cudaGetLastError());
+    BBS_CUDA(cudaMemcpyAsync(W.h_st, d_st, sizeof(EpochState), cudaMemcpyDeviceToHost, s));
+    BBS_CUDA(cudaStreamSynchronize(s));
+    d2h += sizeof(EpochState);
+    hs = *W.h_st;
+    others_active = hs.any_active != 0;
+    launches += 2;
+  }
 
   while (self_active || others_active) {
     // capacity: the queue grows by at most pend_cap per epoch
@@ -1203,14 +1348,21 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
       // the live queue sits in buffer hs.cur; keep its contents
       q.key[0] = W.qk0.get(need, s, true, hs.cur == 0 ? hs.q_len : 0);
       q.key[1] = W.qk1.get(need, s, true, hs.cur == 1 ? hs.q_len : 0);
-      q.node[0] = W.qn0.get(need, s, true, hs.cur == 0 ? hs.q_len : 0);
-      q.node[1] = W.qn1.get(need, s, true, hs.cur == 1 ? hs.q_len : 0);
-      qcap = std::min({W.qk0.cap, W.qk1.cap, W.qn0.cap, W.qn1.cap});
+      qcap = std::min(W.qk0.cap, W.qk1.cap);
     }
-    const int n_ep = self_active ? E : 1;
+    // the pool gains at most pend_cap nodes per epoch; slots [0, seq) are live
+    if (hs.seq + static_cast<uint64_t>(E + 1) * pend_cap > pool_cap) {
+      const uint64_t need = 2 * (hs.seq + static_cast<uint64_t>(E + 1) * pend_cap);
+      if (need >= (1ull << 32)) throw Error(BBS_ERR_TOO_LARGE, "search: more than 2^32 queue pushes");
+      q.pool = W.pool.get(need, s, true, hs.seq);
+      pool_cap = W.pool.cap;
+    }
+    // device exchange: every rank runs the same number of epochs (and so
+    // of collectives) per batch; the stop decision uses the reduced flag
+    const int n_ep = (self_active || roots_dev_x) ? E : 1;
     // graphs pay off for long searches (capture + instantiate ~0.2 ms)
     if (n_ep == E && E > 1 && pass_ms.size() >= graph_after) {
-      if (!batch_exec || batch_qcap != qcap) {
+      if (!batch_exec || batch_qcap != qcap || batch_pool != q.pool) {
         if (batch_exec) BBS_CUDA(cudaGraphExecDestroy(batch_exec));
         batch_exec = nullptr;
         cudaGraph_t graph;
@@ -1224,6 +1376,7 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
         BBS_CUDA(cudaGraphInstantiate(&batch_exec, graph, 0));
         BBS_CUDA(cudaGraphDestroy(graph));
         batch_qcap = qcap;
+        batch_pool = q.pool;
       }
       BBS_CUDA(cudaGraphLaunch(batch_exec, s));
       launches += 6ull * E;
@@ -1239,10 +1392,10 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
     }
     hs = *W.h_st;
     self_active = hs.active != 0;
-    if (shard && shard->allreduce_max)
+    if (roots_host_x)
       exchange();
     else
-      others_active = false;
+      others_active = roots_dev_x && hs.any_active != 0;
   }
   cudaEvent_t ev_end = W.next_event();
   BBS_CUDA(cudaEventRecord(ev_end, s));
@@ -1272,7 +1425,7 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
   out->root_score_ms = elapsed(ev_roots0, ev_roots1);
   out->epoch_score_ms = esm;
   out->epochs = hs.epochs;
-  out->root_nodes = n_own;
+  out->root_nodes = n_own;  // roots this rank scored
   out->lookups = hs.nodes_generated * K;
   out->queue_peak = hs.q_peak;
   if (cache.enabled && std::getenv("BBS_DEBUG_CACHE")) {
@@ -1314,12 +1467,41 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
   out->d2h_bytes = d2h;
   out->kernel_launches = launches;
   for (int l = 0; l < kMaxLevels; ++l) out->evals_per_level[l] = hs.level_evals[l];
-  out->evals_per_level[L] += n_own;  // the root batch
+  out->evals_per_level[L] += n_scored_roots;  // the root batch
   int32_t best = hs.best;
   bbs_node best_node = hs.best_node;
   int matched = hs.matched;
   // winner election across ranks: max of (score, world-1-rank) among matched
-  if (shard && shard->allreduce_max && world > 1) {
+  // (exact mode: every rank already holds the single-queue result)
+  if (!exact && roots_dev_x && world > 1) {
+    // over NCCL in int32 steps: top score, then the lowest rank holding it,
+    // then that rank's node (same winner as the host protocol below)
+    int32_t* d = W.xchg.get(8, s);
+    int32_t* h = reinterpret_cast<int32_t*>(W.h_small);  // pinned, >= 32 B
+    auto reduce = [&](int n) {
+      BBS_CUDA(cudaMemcpyAsync(d, h, n * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+      comm_allreduce_max_i32(comm, d, n, s);
+      BBS_CUDA(cudaMemcpyAsync(h, d, n * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+      BBS_CUDA(cudaStreamSynchronize(s));
+    };
+    h[0] = matched ? best : -1;
+    reduce(1);
+    const int32_t top = h[0];
+    h[0] = (matched && best == top) ? world - 1 - rank : -1;
+    reduce(1);
+    const int winner = top < 0 ? -1 : world - 1 - h[0];
+    const int32_t* f = reinterpret_cast<const int32_t*>(&best_node);
+    for (int i = 0; i < 8; ++i) h[i] = rank == winner ? f[i] : INT32_MIN;
+    reduce(8);
+    if (winner >= 0) {
+      std::memcpy(&best_node, h, sizeof(best_node));
+      best = top;
+      matched = 1;
+    } else {
+      matched = 0;
+    }
+  }
+  if (!exact && roots_host_x && world > 1) {
     int64_t key[1] = {matched ? (static_cast<int64_t>(best) << 32) | static_cast<int64_t>(world - 1 - rank) : -1};
     if (shard->allreduce_max(key, 1, shard->user) != 0)
       throw Error(BBS_ERR_GENERIC, "search: winner election failed");

@@ -185,3 +185,118 @@ def test_device_sharded_equals_restated_protocol(B, orc, world, mode):
         assert d.best_score_trace == wt
     assert sum(dev[r].root_nodes for r in range(world)) == \
         B.search(vm, s, cfg).root_nodes
+
+
+# ---- batch-split exact mode (SURVEY §8e "parity caveat" mitigation) --------
+
+def _gloo_exact_worker(rank, world, port, mode, out_q):
+    import sys
+    sys.path.insert(0, ROOT)
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import torch
+    from pyoracle import Restated
+    from paper_2310_10023_b200._abi import ALLREDUCE_MAX_FN, SHARD_EXACT, Shard
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    orc = Restated()
+    m, s, _ = _scene()
+    om = orc.map_build(m, 0.5, 3)
+    calls = [0]
+
+    def allreduce(values, count, _user):
+        calls[0] += 1
+        t = torch.tensor([values[i] for i in range(count)], dtype=torch.int64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        for i in range(count):
+            values[i] = int(t[i])
+        return 0
+
+    cb = ALLREDUCE_MAX_FN(allreduce)
+    res, trace = om.search(s, _cfg(mode), shard=Shard(rank, world, cb, None, SHARD_EXACT, 0, None))
+    out_q.put((rank, res.best_score, bool(res.matched), res.best_pose.as_tuple(), res.root_nodes,
+               res.stats.nodes_generated, res.stats.nodes_pruned, res.stats.batches_flushed,
+               tuple(trace), calls[0]))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("mode", [0, 1])
+def test_gloo_world2_exact_equals_unsharded(mode, orc):
+    """Exact mode over gloo: each rank scores half of every batch, yet both
+    return the single-queue search() result, RotoTrans included."""
+    import random
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = random.randint(20000, 40000)
+    procs = [ctx.Process(target=_gloo_exact_worker, args=(r, 2, port, mode, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=300)
+        assert p.exitcode == 0
+    got = dict((r[0], r[1:]) for r in (q.get(timeout=10) for _ in range(2)))
+    m, s, _ = _scene()
+    om = orc.map_build(m, 0.5, 3)
+    single, strace = om.search(s, _cfg(mode))
+    want = (single.best_score, bool(single.matched), single.best_pose.as_tuple())
+    for r in (0, 1):
+        assert got[r][:3] == want, r
+        assert got[r][4:7] == (single.stats.nodes_generated, single.stats.nodes_pruned,
+                               single.stats.batches_flushed), r
+        assert list(got[r][7]) == list(strace), r
+        assert got[r][8] == single.stats.batches_flushed  # one score exchange per batch
+    assert got[0][3] + got[1][3] == single.root_nodes and min(got[0][3], got[1][3]) > 0
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("mode", [0, 1])
+def test_device_exact_threads_equal_unsharded(B, world, mode):
+    """Exact mode on the device (host exchange, one host thread per rank):
+    every rank equals the unsharded device search exactly."""
+    m, s, _ = _scene()
+    vm = B.MultiResVoxelMap.build(m, 0.5, 3)
+    ds = B.DeviceScan(vm, s)
+    cfg = B.SearchConfig(min_resolution=0.5, max_level=3, branch_mode=mode, batch_size=400,
+                         roll_pitch_half_range=0.0 if mode == 0 else 0.02, collect_trace=True)
+    single = B.search_scan(vm, ds, cfg)
+    with pytest.raises(B.ConfigError):  # exact mode with world > 1 needs an exchange
+        B.search_sharded(vm, ds, cfg, 0, world, mode="exact")
+    ar = ThreadAllReduce(world)
+    dev = _run_threads(world, lambda r: B.search_sharded(vm, ds, cfg, r, world,
+                                                         lambda v: ar(r, v), mode="exact"))
+    for r in range(world):
+        d = dev[r]
+        assert (d.best_score, d.matched, d.best_pose.as_tuple()) == \
+            (single.best_score, single.matched, single.best_pose.as_tuple()), r
+        assert (d.stats.nodes_generated, d.stats.nodes_pruned, d.stats.batches_flushed) == \
+            (single.stats.nodes_generated, single.stats.nodes_pruned, single.stats.batches_flushed), r
+        assert d.best_score_trace == single.best_score_trace, r
+        assert d.epochs == single.epochs
+    assert sum(dev[r].root_nodes for r in range(world)) == single.root_nodes
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("mode", [0, 1])
+def test_nccl_world1_equals_unsharded(B, mode):
+    """The device-side NCCL exchange path (bbs_comm_t, world 1): roots and
+    exact modes reproduce the unsharded search, Stats and trace included."""
+    m, s, _ = _scene()
+    vm = B.MultiResVoxelMap.build(m, 0.5, 3)
+    ds = B.DeviceScan(vm, s)
+    cfg = B.SearchConfig(min_resolution=0.5, max_level=3, branch_mode=mode, batch_size=400,
+                         roll_pitch_half_range=0.0 if mode == 0 else 0.02, collect_trace=True)
+    single = B.search_scan(vm, ds, cfg)
+    comm = B.Comm(0, 0, 1, B.Comm.unique_id())
+    try:
+        for smode in ("roots", "exact"):
+            d = B.search_sharded(vm, ds, cfg, 0, 1, comm=comm, mode=smode)
+            assert (d.best_score, d.matched, d.best_pose.as_tuple()) == \
+                (single.best_score, single.matched, single.best_pose.as_tuple()), smode
+            assert (d.stats.nodes_generated, d.stats.nodes_pruned, d.stats.batches_flushed) == \
+                (single.stats.nodes_generated, single.stats.nodes_pruned,
+                 single.stats.batches_flushed), smode
+            assert d.best_score_trace == single.best_score_trace, smode
+    finally:
+        comm.close()
