@@ -449,6 +449,36 @@ void build_stage_window(const MapView& map, const RotCache& cache, uint32_t* win
   BBS_CUDA(cudaGetLastError());
 }
 
+// Prebuild: every rotation of one level listed as a build (all slots of the
+// level are claimed up front).  The level-(L-1) histograms are needed by
+// nearly every rotation of that level during the search (C2: 466 of 472,
+// C3: 1264 of 1264), so building them in one launch replaces one serial
+// CTA-per-build tail in each of the first flushes.
+__global__ void cache_prebuild_list_kernel(RotCache c, GridView G, int l, uint32_t n_rot) {
+  const uint32_t np = static_cast<uint32_t>(G.max_index[l * 3 + 1]) + 1;
+  const uint32_t nw = static_cast<uint32_t>(G.max_index[l * 3 + 2]) + 1;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n_rot; i += gridDim.x * blockDim.x) {
+    const uint32_t slot = c.base[l] + i;
+    c.info[slot].x = kCacheBuilding;
+    c.builds[i] = make_int4(static_cast<int32_t>(slot), l, static_cast<int32_t>(i / (nw * np)),
+                            static_cast<int32_t>((i / nw) % np));
+    c.builds_w[i] = static_cast<int32_t>(i % nw);
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) c.ctl[2] = n_rot;
+}
+
+void launch_cache_prebuild(const MapView& map, const GridView& grid, const ScanView& scan,
+                           const RotCache& cache, int level, uint32_t n_rot, cudaStream_t s) {
+  if (n_rot == 0) return;
+  const int build_smem = kCacheHashSlots * 12 + kCacheAmbCap * 4;
+  BBS_CUDA(cudaFuncSetAttribute(cache_build_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, build_smem));
+  cache_prebuild_list_kernel<<<(n_rot + 255) / 256, 256, 0, s>>>(cache, grid, level, n_rot);
+  BBS_CUDA(cudaGetLastError());
+  cache_build_kernel<<<std::min<uint32_t>(n_rot, 148 * 2), kBuildThreads, build_smem, s>>>(cache, map, grid,
+                                                                                          scan);
+  BBS_CUDA(cudaGetLastError());
+}
+
 void launch_epoch_score(const MapView& map, const GridView& grid, const ScanView& scan,
                         const bbs_node* pending, const uint32_t* d_n, uint32_t n_max,
                         uint32_t n_ptiles, int32_t* scores, const RotCache& cache, cudaStream_t s) {

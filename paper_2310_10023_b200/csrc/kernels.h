@@ -153,6 +153,11 @@ void launch_epoch_score(const MapView& map, const GridView& grid, const ScanView
                         const bbs_node* pending, const uint32_t* d_n, uint32_t n_max,
                         uint32_t n_ptiles, int32_t* scores, const RotCache& cache, cudaStream_t s);
 
+// Build the histograms of every rotation of `level` (n_rot slots from
+// cache.base[level]) in one launch; cache.builds must hold n_rot entries.
+void launch_cache_prebuild(const MapView& map, const GridView& grid, const ScanView& scan,
+                           const RotCache& cache, int level, uint32_t n_rot, cudaStream_t s);
+
 // Score arbitrary nodes in place (node.score), grouping equal rotations on
 // the device.  Host-synchronous.
 void score_nodes_general(const MapView& map, const GridView& grid, const ScanView& scan,

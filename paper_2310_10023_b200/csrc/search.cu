@@ -1222,7 +1222,17 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
       cache.ctl = cache.amb_off + slots;
       cache.pool = W.cache_pool.get(cache.pool_cap, s);
       cache.amb_pool = W.cache_amb.get(cache.amb_cap, s);
-      const uint64_t mr = (pend_cap + 7) / 8;
+      // level L-1 is prebuilt in one launch when its rotation count is modest
+      const int pl = L - 1;
+      const uint64_t pre_rot = (pl >= 0 && cache.base[pl] != 0xFFFFFFFFu)
+                                   ? static_cast<uint64_t>(grid.axis(0, pl).index_count()) *
+                                         grid.axis(1, pl).index_count() * grid.axis(2, pl).index_count()
+                                   : 0;
+      const bool prebuild = pre_rot > 0 && pre_rot <= 16384 && [] {
+        const char* v = std::getenv("BBS_PREBUILD");  // "0" disables (A/B timing)
+        return !(v && v[0] == '0');
+      }();
+      const uint64_t mr = std::max<uint64_t>((pend_cap + 7) / 8, prebuild ? pre_rot : 0);
       cache.builds = W.cache_builds.get(mr, s);
       cache.builds_w = W.cache_builds_w.get(mr, s);
       cache.fb_runs = W.cache_fb.get(mr, s);
@@ -1233,6 +1243,10 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
       }
       BBS_CUDA(cudaMemsetAsync(cache.info, 0xFF, slots * sizeof(int4), s));  // all kCacheEmpty
       BBS_CUDA(cudaMemsetAsync(cache.ctl, 0, kCacheCtl * sizeof(uint32_t), s));
+      if (prebuild) {
+        launch_cache_prebuild(m->view, gv, sv, cache, pl, static_cast<uint32_t>(pre_rot), s);
+        launches += 2;
+      }
     }
   }
 
