@@ -219,11 +219,14 @@ def measured_peaks():
         return {"hbm_gbs": 6650.0}, "fallback"
 
 
-def profile_traffic(kernel):
+def profile_traffic(config, group):
+    """DRAM bytes per launch of a kernel group (read + write), from the ncu
+    launch list committed under profiles/ (scripts/traffic.py)."""
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
-            return json.load(f).get(kernel)
-    except (OSError, ValueError):
+            g = json.load(f).get(config, {}).get(group)
+        return None if g is None else g["dram_bytes_per_launch"]
+    except (OSError, ValueError, KeyError):
         return None
 
 
@@ -355,10 +358,13 @@ def run_b200_arm(args, cfgd):
     root_probes = statistics.mean(r.root_probes for r in results)
     epoch_lookups = statistics.mean((r.stats.nodes_generated - r.root_nodes) * K for r in results)
     if root_ms >= epoch_ms:
-        kern, ms, probes = "root_col_kernel (+ root_hist_kernel)", root_ms, root_probes
+        group, ms, probes = "root", root_ms, root_probes
+        kern = "root batch: root_hist_kernel + root_colpad_kernel (batch_evaluate on initial_nodes)"
         launches_per_step = 1
     else:
-        kern, ms, probes = "score_cube8_kernel", epoch_ms, epoch_lookups
+        group, ms, probes = "flush", epoch_ms, epoch_lookups
+        kern = ("flush scoring, per epoch: cache_build_kernel + cache_probe_kernel + "
+                "score_cube8_kernel (batch_evaluate on each flushed batch)")
         launches_per_step = max(1, statistics.mean(r.epochs for r in results))
     bytes_per_launch = probes * 32.0 / launches_per_step
     achieved = bytes_per_launch / (ms / launches_per_step * 1e-3) / 1e9
@@ -372,17 +378,22 @@ def run_b200_arm(args, cfgd):
                 gather[label] = round(out.value, 1)
     roofline = {
         "bound": "hbm", "kernel": kern, "achieved": achieved, "peak": peak, "unit": "GB/s",
-        "frac": achieved / peak, "traffic": profile_traffic(kern),
+        "frac": achieved / peak, "traffic": profile_traffic(args.config, group),
+        "traffic_source": "profiles/ncu_traffic.json: dram__bytes_read.sum + dram__bytes_write.sum "
+                          "per launch of the group, ncu launch list (scripts/traffic.py)",
         "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
         "algorithmic_bytes_per_launch": bytes_per_launch,
         "unit_of_work": "one membership probe = one random 32 B sector (SURVEY §8d)",
         "kernel_ms_per_step": ms, "gather_peaks_gbs": gather,
         "frac_of_l2_gather": (achieved / gather["l2_64MiB"]) if gather.get("l2_64MiB") else None,
-        "note": ("achieved counts SURVEY §8d's model (one random 32 B sector per (node, point) "
-                 "lookup, or per de-duplicated root probe); the kernels answer a 2x2x2 child "
-                 "cube with 4 column-word loads and a root z-column with one, from L1/L2-resident "
-                 "z-column bitmaps, so frac > 1 means the structure beats the per-lookup gather "
-                 "model; the kernel's true limiter is SM issue (see DESIGN.md / profiles/)"),
+        "note": ("achieved counts SURVEY §8d's unit: one random 32 B sector per (node, scan point) "
+                 "lookup in the flush batches, per de-duplicated (root, voxel offset) probe in the "
+                 "root batch.  The kernels issue far fewer memory operations than that model: per "
+                 "(level, rotation) histograms de-duplicate the scan's voxel offsets (C2: 10k points "
+                 "-> ~2k entries), a 2x2x2 child cube is answered with 4 z-column words and a root "
+                 "z-column with one, from shared-memory windows of the z-column bitmap; frac > 1 means "
+                 "the algorithm beats the per-lookup gather roofline.  The measured limiter is SM "
+                 "issue / latency (profiles/)"),
     }
 
     line = {
