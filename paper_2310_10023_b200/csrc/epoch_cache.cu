@@ -89,7 +89,43 @@ __global__ void __launch_bounds__(kBuildThreads) cache_build_kernel(RotCache c, 
     __syncthreads();
     // all lanes stay in the loop together (warp-aggregated inserts below)
     bool aborted = false;
-    for (uint32_t p0 = 0; p0 < scan.k; p0 += 2 * blockDim.x) {
+    if (dense) {
+      // Dense box, tight loop: one constant eps per level (dn_eps bounds the
+      // per-point eps of fast_floor for every in-box offset; an out-of-box
+      // point gives the build up, so the bound is only ever used in-box) and
+      // an unsigned box test on the saturated int conversion.
+      const double eps = c.dn_eps[l], eps1 = c.dn_eps1[l], inv = L.inv_cell;
+      const uint32_t udxy = static_cast<uint32_t>(dxy), unz = static_cast<uint32_t>(c.dn_nz[l]);
+      for (uint32_t p0 = 0; p0 < scan.k; p0 += blockDim.x) {
+        const uint32_t p = p0 + threadIdx.x;
+        int idx = -1;
+        if (p < scan.k) {
+          const double px = scan.x[p], py = scan.y[p], pz = scan.z[p];
+          const double wx = __dmul_rn(rot_row(R[0], R[1], R[2], px, py, pz), inv);
+          const double wy = __dmul_rn(rot_row(R[3], R[4], R[5], px, py, pz), inv);
+          const double wz = __dmul_rn(rot_row(R[6], R[7], R[8], px, py, pz), inv);
+          const double flx = floor(wx), fly = floor(wy), flz = floor(wz);
+          const double frx = __dsub_rn(wx, flx), fry = __dsub_rn(wy, fly), frz = __dsub_rn(wz, flz);
+          const bool ok = frx > eps && frx < eps1 && fry > eps && fry < eps1 && frz > eps && frz < eps1;
+          if (!ok) {
+            const int a = atomicAdd(&s_namb, 1);
+            if (a < kCacheAmbCap) s_amb[a] = p;
+          } else {
+            const uint32_t ux = static_cast<uint32_t>(__double2int_rz(flx)) + static_cast<uint32_t>(dr);
+            const uint32_t uy = static_cast<uint32_t>(__double2int_rz(fly)) + static_cast<uint32_t>(dr);
+            const uint32_t uz = static_cast<uint32_t>(__double2int_rz(flz)) - static_cast<uint32_t>(dzlo);
+            if (ux < udxy && uy < udxy && uz < unz)
+              idx = static_cast<int>((uz * udxy + uy) * udxy + ux);
+            else
+              s_oob = 1;  // outside the box: this build gives up (cube kernel scores its runs)
+          }
+        }
+        const unsigned same = __match_any_sync(0xffffffffu, idx);
+        if (idx >= 0 && (__ffs(same) - 1) == lane)
+          atomicAdd(&s_w[idx >> 1], static_cast<uint32_t>(__popc(same)) << ((idx & 1) << 4));
+      }
+    }
+    for (uint32_t p0 = 0; !dense && p0 < scan.k; p0 += 2 * blockDim.x) {
       uint32_t p[2];
       double px[2], py[2], pz[2];
 #pragma unroll

@@ -125,6 +125,9 @@ struct RotCache {
   // dense-histogram box per level (dn_r = 0: hash build): offsets in
   // [-r, r]^2 x [zlo, zlo + nz), two 16-bit counts per shared word
   int32_t dn_r[kMaxLevels], dn_zlo[kMaxLevels], dn_nz[kMaxLevels];
+  // fast-path eps of the dense box: (W + tmax) * 2^-48 with W >= |w| + 1 for
+  // every in-box offset, so it bounds fast_floor's per-point eps (and 1 - eps)
+  double dn_eps[kMaxLevels], dn_eps1[kMaxLevels];
   // staged level (-1: none): its histograms are stored as groups of 4
   // entries (column offset in the padded window, z bytes, count bytes) and
   // the probe reads the level's z-column words from a zero-padded shared

@@ -1186,6 +1186,9 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
           cache.dn_r[l] = static_cast<int32_t>(r);
           cache.dn_zlo[l] = static_cast<int32_t>(zlo);
           cache.dn_nz[l] = static_cast<int32_t>(zhi - zlo + 1.0);
+          const double W = std::max({r, std::fabs(zlo), std::fabs(zhi + 1.0)}) + 1.0;
+          cache.dn_eps[l] = (W + cache.tmax[l]) * 0x1p-48;
+          cache.dn_eps1[l] = 1.0 - cache.dn_eps[l];
         }
       }
     }
@@ -1244,8 +1247,16 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
       BBS_CUDA(cudaMemsetAsync(cache.info, 0xFF, slots * sizeof(int4), s));  // all kCacheEmpty
       BBS_CUDA(cudaMemsetAsync(cache.ctl, 0, kCacheCtl * sizeof(uint32_t), s));
       if (prebuild) {
+        cudaEvent_t e0 = W.next_event(), e1 = W.next_event();
+        BBS_CUDA(cudaEventRecord(e0, s));
         launch_cache_prebuild(m->view, gv, sv, cache, pl, static_cast<uint32_t>(pre_rot), s);
+        BBS_CUDA(cudaEventRecord(e1, s));
         launches += 2;
+        if (std::getenv("BBS_DEBUG_CACHE")) {
+          BBS_CUDA(cudaEventSynchronize(e1));
+          std::fprintf(stderr, "[cache] prebuild level %d: %llu rotations in %.3f ms\n", pl,
+                       static_cast<unsigned long long>(pre_rot), elapsed(e0, e1));
+        }
       }
     }
   }
