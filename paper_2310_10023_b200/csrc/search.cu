@@ -395,6 +395,25 @@ __device__ __forceinline__ uint32_t lower_bound_u64(const unsigned long long* a,
   return lo;
 }
 
+// First index i in [0, n) with a[i] >= v (n if none), searched by the whole
+// warp (uniform arguments): each round the 32 lanes probe 32 evenly spaced
+// positions, so a queue of ~500k keys takes 4 dependent rounds instead of 19.
+__device__ __forceinline__ uint32_t warp_lower_bound_u64(const unsigned long long* __restrict__ a, uint32_t n,
+                                                         unsigned long long v) {
+  const uint32_t lane = threadIdx.x & 31u;
+  uint32_t lo = 0, hi = n;  // a[i] < v for i < lo, a[i] >= v for i >= hi
+  while (lo < hi) {
+    const uint32_t step = (hi - lo + 31u) >> 5;
+    const uint32_t pos = lo + (lane + 1u) * step - 1u;
+    const bool less = pos < hi && a[pos] < v;
+    const uint32_t c = static_cast<uint32_t>(__popc(__ballot_sync(0xffffffffu, less)));
+    const uint32_t nhi = lo + (c + 1u) * step - 1u;
+    lo += c * step;
+    if (nhi < hi) hi = nhi;
+  }
+  return lo;
+}
+
 // Incumbent trim (one warp).  B never decreases, so a queued entry with
 // score < B is pruned whenever it is popped (search.hpp:150-153) and never
 // branches or updates the incumbent: dropping it now and counting it as
@@ -408,7 +427,12 @@ __device__ void trim_remainder(EpochState* st, const Queue& q, int strategy, int
   const unsigned long long* qk = q.keys(st->cur) + n_cons;
   const int nseg = strategy == BBS_STRATEGY_BFS ? 1 : kMaxLevels;
   uint32_t lo = 0, hi = 0;
-  if (lane < nseg) {
+  if (strategy == BBS_STRATEGY_BFS) {
+    // one segment: the whole warp searches it (log32 rounds of L2 latency)
+    const unsigned long long sb = kSMax - static_cast<unsigned long long>(B < 0 ? 0 : B) + 1;
+    const uint32_t h = B > 0 ? warp_lower_bound_u64(qk, n_rem, sb << 44) : n_rem;
+    hi = lane == 0 ? h : 0;
+  } else if (lane < nseg) {
     unsigned long long seg_base = 0, seg_end_key = ~0ull, cut_key;
     const unsigned long long sb = kSMax - static_cast<unsigned long long>(B < 0 ? 0 : B) + 1;
     if (strategy == BBS_STRATEGY_BFS) {
@@ -569,21 +593,55 @@ __global__ void __launch_bounds__(kRT) rank_sort_kernel(const EpochState* st,
 }
 
 // E6: merge the sorted survivors into the trimmed queue remainder (push,
-// search.hpp:139).  The remainder is read through the kept segment ranges.
-// Keys only (nodes stay in the pool).  A thread moves kMIPT consecutive
-// remainder keys: one binary search into the survivors for the first, then a
-// forward walk (both sides are sorted); each survivor finds its place in its
-// remainder segment by binary search.
-constexpr uint32_t kMIPT = 8;
-__global__ void merge_kernel(EpochState* st, Queue q, int strategy,
-                             const unsigned long long* __restrict__ skey) {
+// search.hpp:139).  The remainder A is read through the kept segment ranges
+// (one per key segment); the survivors B are sorted; keys are unique.  Keys
+// only (nodes stay in the pool).  Merge path: each CTA owns kMTile outputs,
+// two warps find the tile's diagonal splits with 32-ary searches, the tile's
+// A and B ranges are staged in shared memory and each thread merges 8
+// outputs from its own in-tile split.
+constexpr uint32_t kMT = 256, kMItems = 8, kMTile = kMT * kMItems;
+
+struct RemView {
+  const unsigned long long* qk;
+  const uint32_t* lo;   // smem: segment start in qk
+  const uint32_t* pre;  // smem: segment start in the kept order (kMaxLevels + 1)
+  bool bfs;
+  __device__ __forceinline__ unsigned long long operator[](uint32_t i) const {
+    int sg = 0;
+    if (!bfs)
+      while (pre[sg + 1] <= i) ++sg;
+    return qk[lo[sg] + (i - pre[sg])];
+  }
+};
+
+// #A elements among the first d merged outputs (warp-uniform arguments).
+__device__ __forceinline__ uint32_t warp_merge_split(const RemView& A, uint32_t na,
+                                                     const unsigned long long* __restrict__ B, uint32_t nb,
+                                                     uint32_t d) {
+  const uint32_t lane = threadIdx.x & 31u;
+  uint32_t lo = d > nb ? d - nb : 0u, hi = min(d, na);  // P(a) = A[a] < B[d-1-a], true below the answer
+  while (lo < hi) {
+    const uint32_t step = (hi - lo + 31u) >> 5;
+    const uint32_t a = lo + (lane + 1u) * step - 1u;
+    const bool p = a < hi && A[a] < B[d - 1u - a];
+    const uint32_t c = static_cast<uint32_t>(__popc(__ballot_sync(0xffffffffu, p)));
+    const uint32_t nhi = lo + (c + 1u) * step - 1u;
+    lo += c * step;
+    if (nhi < hi) hi = nhi;
+  }
+  return lo;
+}
+
+__global__ void __launch_bounds__(kMT) merge_kernel(EpochState* st, Queue q, int strategy,
+                                                    const unsigned long long* __restrict__ skey) {
   pdl_wait();
 
-  __shared__ uint32_t s_lo[kMaxLevels], s_len[kMaxLevels], s_pre[kMaxLevels + 1];
+  __shared__ uint32_t s_lo[kMaxLevels], s_pre[kMaxLevels + 1];
+  __shared__ uint32_t s_split[2];
+  __shared__ unsigned long long s_ab[kMTile];
   if (st->n_children == 0) return;
   if (threadIdx.x < kMaxLevels) {
     s_lo[threadIdx.x] = st->seg_lo[threadIdx.x];
-    s_len[threadIdx.x] = st->seg_len[threadIdx.x];
     s_pre[threadIdx.x] = st->seg_pre[threadIdx.x];
   }
   if (threadIdx.x == 0) s_pre[kMaxLevels] = st->seg_pre[kMaxLevels];
@@ -591,36 +649,42 @@ __global__ void merge_kernel(EpochState* st, Queue q, int strategy,
   const uint32_t cur = st->cur;
   const uint32_t n_keep = st->n_keep;
   const uint32_t n_s = st->n_surv;
-  const unsigned long long* __restrict__ qk = q.keys(cur) + st->n_cons;
+  const RemView A{q.keys(cur) + st->n_cons, s_lo, s_pre, strategy == BBS_STRATEGY_BFS};
   unsigned long long* __restrict__ ok = q.keys(cur ^ 1u);
-  const bool bfs = strategy == BBS_STRATEGY_BFS;
-  const uint32_t n_kitems = (n_keep + kMIPT - 1) / kMIPT;
-  const uint32_t items = n_kitems + n_s;
-  for (uint32_t it = blockIdx.x * blockDim.x + threadIdx.x; it < items; it += gridDim.x * blockDim.x) {
-    if (it < n_kitems) {
-      uint32_t i = it * kMIPT;
-      const uint32_t iend = min(i + kMIPT, n_keep);
-      int sg = 0;
-      uint32_t p = 0;
-      bool first = true;
-      for (; i < iend; ++i) {
-        if (!bfs)
-          while (s_pre[sg + 1] <= i) ++sg;
-        const unsigned long long k = qk[s_lo[sg] + (i - s_pre[sg])];
-        if (first) {
-          p = lower_bound_u64(skey, n_s, k);
-          first = false;
-        } else {
-          while (p < n_s && skey[p] < k) ++p;
-        }
-        ok[i + p] = k;
-      }
-    } else {
-      const uint32_t j = it - n_kitems;
-      const unsigned long long k = skey[j];
-      const int sg = bfs ? 0 : static_cast<int>(k >> 60);
-      ok[j + s_pre[sg] + lower_bound_u64(qk + s_lo[sg], s_len[sg], k)] = k;
+  const uint32_t total = n_keep + n_s;
+  const uint32_t warp = threadIdx.x >> 5;
+  for (uint32_t d0 = blockIdx.x * kMTile; d0 < total; d0 += gridDim.x * kMTile) {
+    const uint32_t d1 = min(total, d0 + kMTile);
+    if (warp < 2) {
+      const uint32_t sp = warp_merge_split(A, n_keep, skey, n_s, warp ? d1 : d0);
+      if ((threadIdx.x & 31u) == 0) s_split[warp] = sp;
     }
+    __syncthreads();
+    const uint32_t a0 = s_split[0], a1 = s_split[1];
+    const uint32_t na = a1 - a0, nb = (d1 - d0) - na, b0 = d0 - a0;
+    for (uint32_t i = threadIdx.x; i < na + nb; i += kMT)
+      s_ab[i] = i < na ? A[a0 + i] : skey[b0 + (i - na)];
+    __syncthreads();
+    const unsigned long long* sa = s_ab;
+    const unsigned long long* sb = s_ab + na;
+    const uint32_t dt = threadIdx.x * kMItems;
+    if (dt < na + nb) {
+      uint32_t lo = dt > nb ? dt - nb : 0u, hi = min(dt, na);
+      while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (sa[mid] < sb[dt - 1u - mid])
+          lo = mid + 1u;
+        else
+          hi = mid;
+      }
+      uint32_t i = lo, j = dt - lo;
+      const uint32_t end = min(dt + kMItems, na + nb);
+      for (uint32_t o = dt; o < end; ++o) {
+        const bool take_a = j >= nb || (i < na && sa[i] < sb[j]);
+        ok[d0 + o] = take_a ? sa[i++] : sb[j++];
+      }
+    }
+    __syncthreads();
   }
   // E7 (last CTA): swap queue buffers; the loop ends when queue and pending
   // are empty
@@ -1310,7 +1374,8 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
     BBS_CUDA(cudaGetLastError());
     launch_pdl(rank_sort_kernel, grid1(pend_cap, kRT), kRT, 0, s, d_st, s_key, s_key2);
     BBS_CUDA(cudaGetLastError());
-    launch_pdl(merge_kernel, grid1((qcap + kMIPT - 1) / kMIPT), 256, 0, s, d_st, q, strategy, s_key2);
+    launch_pdl(merge_kernel, static_cast<unsigned>(std::min<uint64_t>((qcap + kMTile - 1) / kMTile, 148ull * 8)),
+               kMT, 0, s, d_st, q, strategy, s_key2);
     BBS_CUDA(cudaGetLastError());
     launches += 6;  // frontier, branch, score, survivors, rank_sort, merge (+ finalize)
     if (roots_dev_x) {  // incumbent + activity over NCCL, no host round-trip
