@@ -32,7 +32,7 @@ namespace {
 constexpr int kCacheHashSlots = 8192;
 constexpr int kCacheHashCap = 4096;   // distinct offsets kept in shared memory
 constexpr int kCacheAmbCap = 2048;    // ambiguous points buffered per build
-constexpr int kProbeChunk = 1024;     // histogram entries per warp item
+constexpr int kProbeChunk = 512;      // histogram entries per warp item
 constexpr unsigned long long kEmptyKey = ~0ull;
 
 __device__ __forceinline__ uint32_t cache_hash(unsigned long long key) {
@@ -291,6 +291,7 @@ __global__ void __launch_bounds__(kBuildThreads) cache_build_kernel(RotCache c, 
       // publish: entries first, then the state (readers run in later kernels)
       c.info[slot] = fits ? make_int4(kCacheReady, static_cast<int32_t>(off), static_cast<int32_t>(n_ent), namb)
                           : make_int4(kCacheNone, 0, 0, 0);
+      if (fits) atomicMax(&c.ctl[kCtlMaxEnt], n_ent);  // sizes the probe's chunk grid
     }
     __syncthreads();
   }
@@ -321,7 +322,12 @@ __device__ __forceinline__ void probe_ambiguous(const RotCache& c, const LevelVi
 // first fetch the headers (run node, cache info) of 32 items in parallel and
 // the warp then walks only the items that have entries, so empty chunks and
 // uncached runs cost no serial load latency.
-__global__ void __launch_bounds__(256, 3) cache_probe_kernel(RotCache c, MapView map, GridView G,
+#ifndef BBS_PROBE_T
+#define BBS_PROBE_T 256
+#define BBS_PROBE_B 3
+#endif
+constexpr int kProbeThreads = BBS_PROBE_T;
+__global__ void __launch_bounds__(BBS_PROBE_T, BBS_PROBE_B) cache_probe_kernel(RotCache c, MapView map, GridView G,
                                                           ScanView scan,
                                                           const bbs_node* __restrict__ pending,
                                                           const uint32_t* __restrict__ d_n,
@@ -336,6 +342,8 @@ __global__ void __launch_bounds__(256, 3) cache_probe_kernel(RotCache c, MapView
   pdl_wait();
 
   const uint32_t n_runs = *d_n / 8;
+  // chunks per run: the largest histogram built so far (not the scan size)
+  chunks_per_run = min(chunks_per_run, max(1u, (c.ctl[kCtlMaxEnt] + kProbeChunk - 1) / kProbeChunk));
   const uint64_t n_items = static_cast<uint64_t>(n_runs) * chunks_per_run;
   const int lane = threadIdx.x & 31;
   const uint64_t n_warps = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
@@ -538,7 +546,8 @@ void launch_epoch_score(const MapView& map, const GridView& grid, const ScanView
   BBS_CUDA(cudaGetLastError());
   const uint32_t chunks = (scan.k + kProbeChunk - 1) / kProbeChunk;
   const uint64_t warp_items = static_cast<uint64_t>(max_runs) * chunks;
-  const unsigned g = static_cast<unsigned>(std::min<uint64_t>((warp_items + 7) / 8 + 1, 148ull * 16));
+  const uint64_t wpc = kProbeThreads / 32;  // warps per CTA
+  const unsigned g = static_cast<unsigned>(std::min<uint64_t>((warp_items + wpc - 1) / wpc + 1, 148ull * 16));
   const int win_smem = cache.stg_level >= 0 ? static_cast<int>(((cache.stg_pitch * cache.stg_rows * 4u) + 15u) & ~15u) : 0;
   static bool probe_attr = false;
   if (!probe_attr) {
@@ -550,10 +559,10 @@ void launch_epoch_score(const MapView& map, const GridView& grid, const ScanView
   if (win_smem > 0) {
     // persistent: each CTA stages the window once
     int per_sm = 1;
-    BBS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cache_probe_kernel, 256, win_smem));
+    BBS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cache_probe_kernel, kProbeThreads, win_smem));
     gp = std::min<unsigned>(g, 148u * static_cast<unsigned>(std::max(per_sm, 1)));
   }
-  launch_pdl(cache_probe_kernel, gp, 256, win_smem, s, cache, map, grid, scan, pending, d_n, chunks, scores);
+  launch_pdl(cache_probe_kernel, gp, kProbeThreads, win_smem, s, cache, map, grid, scan, pending, d_n, chunks, scores);
   BBS_CUDA(cudaGetLastError());
   launch_score_cube8(map, grid, scan, pending, d_n, n_max, n_ptiles, scores, &cache, s);
 }

@@ -108,7 +108,8 @@ void launch_score_runs8(const MapView& map, const GridView& grid, const ScanView
 // for the flush batches (epoch_cache.cu).  info[slot] = {state, pool offset,
 // entries, ambiguous points}; slot = base[level] + dense rotation id.
 constexpr int32_t kCacheEmpty = -1, kCacheBuilding = -2, kCacheNone = -3, kCacheReady = 0;
-constexpr int kCacheCtl = 4 + kMaxLevels;
+constexpr int kCacheCtl = 4 + kMaxLevels + 1;  // ... + [20] largest histogram (entries)
+constexpr int kCtlMaxEnt = 4 + kMaxLevels;
 constexpr int kCacheDenseCells = 48 * 1024;  // 96 KB of 16-bit counters
 constexpr int kStageWindowMax = 96 * 1024;   // bytes of the probe's staged column window
 struct RotCache {
