@@ -211,6 +211,19 @@ int bbs_map_from_levels(const int32_t* const* level_voxels, const uint64_t* coun
                         int32_t n_levels, double min_resolution, const bbs_aabb* bbox,
                         double collision_target, uint64_t memory_cap_bytes,
                         const bbs_map_options* opts, bbs_map_t* out);
+/* load_map, map_io.hpp:67-115: the reference's map file (layout
+ * map_io.hpp:17-21) read in chunks straight into device levels.  Errors in
+ * the reference's order: FILE_NOT_FOUND ("file not found: <path>"), IO
+ * ("cannot open: <path>"), FORMAT (bad magic, unsupported version, invalid
+ * header values, level blocks out of order, truncated map file) — all
+ * checked before any device work.  opts may be NULL. */
+int bbs_map_load(const char* path, double collision_target, uint64_t memory_cap_bytes,
+                 const bbs_map_options* opts, bbs_map_t* out);
+/* save_map, map_io.hpp:44-65: byte-identical to the reference's file for the
+ * same occupied sets (levels written in occupied_voxels order). */
+int bbs_map_save(bbs_map_t map, const char* path);
+/* is_map_file, map_io.hpp:119-126: 1 when the file starts with the magic. */
+int bbs_is_map_file(const char* path);
 int bbs_map_free(bbs_map_t map);
 int bbs_map_min_resolution(bbs_map_t map, double* out);   /* voxel_map.hpp:263 */
 int bbs_map_max_level(bbs_map_t map, int32_t* out);       /* voxel_map.hpp:264 */

@@ -564,6 +564,16 @@ class MultiResVoxelMap {
                                       min_resolution, &b, collision_target, memory_cap_bytes, &o, &h->h));
     return MultiResVoxelMap(h);
   }
+  // load_map (map_io.hpp:67-115) into device levels
+  static MultiResVoxelMap load(const std::string& path, double collision_target = kDefaultCollisionTarget,
+                               std::size_t memory_cap_bytes = LevelMap::kDefaultMemoryCapBytes,
+                               int device = 0) {
+    detail::check_abi();
+    auto h = std::make_shared<detail::MapHandle>();
+    const bbs_map_options o{device, BBS_LAYOUT_AUTO};
+    detail::check(bbs_map_load(path.c_str(), collision_target, memory_cap_bytes, &o, &h->h));
+    return MultiResVoxelMap(h);
+  }
   double min_resolution() const { return r_; }
   int max_level() const { return max_level_; }
   const Aabb& bbox() const { return bbox_; }
@@ -588,6 +598,18 @@ class MultiResVoxelMap {
   Aabb bbox_;
   std::vector<LevelMap> levels_;
 };
+
+// ---- map_io.hpp (load_map / save_map / is_map_file), device-backed ---------
+inline void save_map(const MultiResVoxelMap& map, const std::string& path) {
+  detail::check(bbs_map_save(map.handle(), path.c_str()));
+}
+inline MultiResVoxelMap load_map(const std::string& path,
+                                 double collision_target = MultiResVoxelMap::kDefaultCollisionTarget,
+                                 std::size_t memory_cap_bytes = LevelMap::kDefaultMemoryCapBytes,
+                                 int device = 0) {
+  return MultiResVoxelMap::load(path, collision_target, memory_cap_bytes, device);
+}
+inline bool is_map_file(const std::string& path) { return bbs_is_map_file(path.c_str()) != 0; }
 
 // build_level (voxel_map.hpp:209-216): a map of levels 0..max(level, 1),
 // returned as the requested level (the view keeps the device map alive).

@@ -33,6 +33,7 @@ class OracleError(RuntimeError):
     def __init__(self, code, msg=""):
         super().__init__(f"{STATUS_NAMES.get(code, code)}: {msg}")
         self.code = code
+        self.message = msg
         self.kind = STATUS_NAMES.get(code, str(code))
 
 
@@ -80,6 +81,10 @@ class Reference:
         L.ref_map_free.restype = None
         L.ref_free.argtypes = [C.c_void_p]
         L.ref_free.restype = None
+        L.ref_save_map.argtypes = [C.c_void_p, C.c_char_p]
+        L.ref_load_map.argtypes = [C.c_char_p, C.c_double, C.c_uint64, C.POINTER(C.c_void_p)]
+        L.ref_is_map_file.argtypes = [C.c_char_p]
+        L.ref_map_max_level.argtypes = [C.c_void_p, C.POINTER(C.c_int32)]
 
     def _check(self, st):
         if st != 0:
@@ -108,6 +113,18 @@ class Reference:
         self._check(self.lib.ref_map_build(_dptr(pts), pts.shape[0], r, max_level,
                                            collision_target, cap, C.byref(h)))
         return RefMap(self, h, max_level)
+
+    def load_map(self, path, collision_target=0.001, cap=2 << 30):
+        """load_map, map_io.hpp:67-115 (raises OracleError(status, message))."""
+        h = C.c_void_p()
+        self._check(self.lib.ref_load_map(os.fsencode(path), C.c_double(collision_target),
+                                          C.c_uint64(cap), C.byref(h)))
+        m = RefMap(self, h, 0)
+        m.max_level = m.max_level_from_levels()
+        return m
+
+    def is_map_file(self, path):
+        return bool(self.lib.ref_is_map_file(os.fsencode(path)))
 
     def map_from_levels(self, levels, r, bbox, collision_target=0.001, cap=2 << 30):
         arrs = [np.ascontiguousarray(np.asarray(v, dtype=np.int32).reshape(-1, 3)) for v in levels]
@@ -189,6 +206,15 @@ class Reference:
 class RefMap:
     def __init__(self, ref, handle, max_level):
         self.ref, self.h, self.max_level = ref, handle, max_level
+
+    def save(self, path):
+        """save_map, map_io.hpp:44-65."""
+        self.ref._check(self.ref.lib.ref_save_map(self.h, os.fsencode(path)))
+
+    def max_level_from_levels(self):
+        lvl = C.c_int32()
+        self.ref._check(self.ref.lib.ref_map_max_level(self.h, C.byref(lvl)))
+        return lvl.value
 
     def __del__(self):
         try:

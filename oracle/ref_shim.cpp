@@ -21,6 +21,7 @@
 #include <vector>
 
 #include "bbs.h"
+#include "bnbloc/map_io.hpp"
 #include "bnbloc/oracle.hpp"
 #include "bnbloc/pipeline.hpp"
 #include "bnbloc/scene.hpp"
@@ -196,6 +197,24 @@ int ref_map_from_levels(const int32_t* const* lv, const uint64_t* counts, int32_
         bnbloc::MultiResVoxelMap::from_levels(std::move(per), r, b, ct, cap));
   });
 }
+
+// save_map, map_io.hpp:44-65.
+int ref_save_map(void* m, const char* path) {
+  return guard([&] { bnbloc::save_map(*static_cast<bnbloc::MultiResVoxelMap*>(m), path); });
+}
+
+// load_map, map_io.hpp:67-115.
+int ref_load_map(const char* path, double ct, uint64_t cap, void** out) {
+  return guard([&] { *out = new bnbloc::MultiResVoxelMap(bnbloc::load_map(path, ct, cap)); });
+}
+
+int ref_map_max_level(void* m, int32_t* out) {
+  *out = static_cast<bnbloc::MultiResVoxelMap*>(m)->max_level();
+  return BBS_OK;
+}
+
+// is_map_file, map_io.hpp:119-126.
+int ref_is_map_file(const char* path) { return bnbloc::is_map_file(path) ? 1 : 0; }
 
 void ref_map_free(void* m) { delete static_cast<bnbloc::MultiResVoxelMap*>(m); }
 

@@ -16,6 +16,7 @@ libbbs_b200.so; there is no CPU fallback.
 import ctypes as C
 import enum
 import math
+import os
 from dataclasses import dataclass, field
 from typing import List, Optional
 
@@ -31,7 +32,8 @@ __all__ = [
     "InfeasiblePoseError", "ConfigError", "CudaError", "InvalidArgumentError",
     "Strategy", "BranchMode", "Layout", "SearchConfig", "Stats", "SearchResult", "Pose6",
     "AxisGrid", "AngularGrid", "LevelMap", "MultiResVoxelMap", "DeviceScan", "NODE_DTYPE",
-    "batch_evaluate", "search", "search_sharded", "Comm", "nccl_version", "localize_scan", "prepare_source",
+    "batch_evaluate", "search", "search_sharded", "Comm", "nccl_version",
+    "save_map", "load_map", "is_map_file", "localize_scan", "prepare_source",
     "max_range", "bounding_box", "pose_to_transform", "node_pose", "initial_node_count",
     "gen_scene", "gen_scans", "cut_scan", "SceneSpec", "device_count",
 ]
@@ -530,6 +532,10 @@ class MultiResVoxelMap:
                                        C.byref(opts), C.byref(h)))
         return MultiResVoxelMap(h)
 
+    def save(self, path):
+        """save_map, map_io.hpp:44-65."""
+        _check(lib.bbs_map_save(self._h, os.fsencode(path)))
+
     def min_resolution(self):
         return self._r
 
@@ -555,6 +561,26 @@ class MultiResVoxelMap:
         out = C.c_double()
         _check(lib.bbs_map_build_ms(self._h, C.byref(out)))
         return out.value
+
+
+def save_map(vmap: MultiResVoxelMap, path):
+    """save_map, map_io.hpp:44-65 (byte-identical to the reference's file)."""
+    vmap.save(path)
+
+
+def load_map(path, collision_target=0.001, memory_cap_bytes=2 << 30, layout=Layout.AUTO, device=0):
+    """load_map, map_io.hpp:67-115: the reference's map file straight into
+    device levels (format errors are raised before any device work)."""
+    h = C.c_void_p()
+    opts = MapOptions(int(device), int(layout))
+    _check(lib.bbs_map_load(os.fsencode(path), float(collision_target), int(memory_cap_bytes),
+                            C.byref(opts), C.byref(h)))
+    return MultiResVoxelMap(h)
+
+
+def is_map_file(path) -> bool:
+    """is_map_file, map_io.hpp:119-126."""
+    return bool(lib.bbs_is_map_file(os.fsencode(path)))
 
 
 class DeviceScan:

@@ -47,6 +47,9 @@ SIGNATURES = {
     "bbs_map_from_levels": (C.c_int, [C.POINTER(_ip), C.POINTER(_u64), _i32, _d, C.POINTER(Aabb),
                                       _d, _u64, C.POINTER(MapOptions), C.POINTER(_vp)]),
     "bbs_map_free": (C.c_int, [_vp]),
+    "bbs_map_load": (C.c_int, [C.c_char_p, _d, _u64, C.POINTER(MapOptions), C.POINTER(_vp)]),
+    "bbs_map_save": (C.c_int, [_vp, C.c_char_p]),
+    "bbs_is_map_file": (C.c_int, [C.c_char_p]),
     "bbs_map_min_resolution": (C.c_int, [_vp, _dp]),
     "bbs_map_max_level": (C.c_int, [_vp, _ip]),
     "bbs_map_bbox": (C.c_int, [_vp, C.POINTER(Aabb)]),

@@ -14,6 +14,7 @@
 
 #include "bbs_comm.h"
 #include "bbs_map_impl.h"
+#include "bbs_map_io.h"
 
 namespace bbs {
 void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const bbs_shard* shard,
@@ -225,6 +226,33 @@ int bbs_map_from_levels(const int32_t* const* level_voxels, const uint64_t* coun
     *out = m.release();
   });
 }
+
+int bbs_map_load(const char* path, double collision_target, uint64_t memory_cap_bytes,
+                 const bbs_map_options* opts, bbs_map_t* out) {
+  return guard([&] {
+    REQUIRE(path && out, "bbs_map_load: null argument");
+    *out = nullptr;
+    bbs::MapFile mf;
+    bbs::map_file_open(path, &mf);
+    bbs::map_file_check_levels(&mf);
+    if (mf.max_level + 1 > static_cast<uint32_t>(bbs::kMaxLevels))
+      throw bbs::Error(BBS_ERR_CONFIG, "map: more than 16 levels are not supported");
+    std::unique_ptr<bbs_map> m(new_map(opts, mf.r, memory_cap_bytes, collision_target));
+    m->max_level = static_cast<int>(mf.max_level);
+    m->bbox = mf.bbox;
+    bbs::map_file_read_levels(&mf, m.get());
+    *out = m.release();
+  });
+}
+
+int bbs_map_save(bbs_map_t map, const char* path) {
+  return guard([&] {
+    REQUIRE(map && path, "bbs_map_save: null argument");
+    bbs::map_file_save(map, path);
+  });
+}
+
+int bbs_is_map_file(const char* path) { return path && bbs::map_file_is_map(path) ? 1 : 0; }
 
 int bbs_map_free(bbs_map_t map) {
   return guard([&] { delete map; });

@@ -96,6 +96,36 @@ __global__ void voxelize_kernel(const double* __restrict__ xyz, uint64_t n, doub
   }
 }
 
+// Box of AoS int32 voxel triples (min, max per axis).
+__global__ void voxel_box_kernel(const int32_t* __restrict__ vox, uint64_t n, int32_t* __restrict__ minmax) {
+  int32_t mn[3] = {INT32_MAX, INT32_MAX, INT32_MAX};
+  int32_t mx[3] = {INT32_MIN, INT32_MIN, INT32_MIN};
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
+       i += uint64_t(gridDim.x) * blockDim.x) {
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      const int32_t v = vox[3 * i + a];
+      mn[a] = min(mn[a], v);
+      mx[a] = max(mx[a], v);
+    }
+  }
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      mn[a] = min(mn[a], __shfl_xor_sync(0xffffffffu, mn[a], o));
+      mx[a] = max(mx[a], __shfl_xor_sync(0xffffffffu, mx[a], o));
+    }
+  }
+  if ((threadIdx.x & 31) == 0) {
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      atomicMin(&minmax[a], mn[a]);
+      atomicMax(&minmax[3 + a], mx[a]);
+    }
+  }
+}
+
 // Voxel triples (AoS int32) -> packed keys relative to box_min.
 __global__ void pack_kernel(const int32_t* __restrict__ vox, uint64_t n, int3 box_min,
                             uint32_t by, uint32_t bz, unsigned long long* __restrict__ keys) {
@@ -417,41 +447,55 @@ void build_map_from_points(bbs_map* m, const double* xyz, uint64_t n) {
   cudaEventDestroy(e1);
 }
 
+// One level from n voxel triples already in device memory (LevelMap::from_voxels,
+// voxel_map.hpp:72-116: duplicates collapse, membership is the set).
+void build_level_from_device_voxels(bbs_map* m, int l, const int32_t* d_vox, uint64_t n) {
+  cudaStream_t s = m->stream;
+  int64_t lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
+  uint64_t dims[3] = {1, 1, 1};
+  uint32_t bits[3] = {1, 1, 1};
+  unsigned long long* keys = nullptr;
+  uint64_t nu = 0;
+  if (n) {
+    DevBuf<int32_t> d_mm(6, s);
+    const int32_t init[6] = {INT32_MAX, INT32_MAX, INT32_MAX, INT32_MIN, INT32_MIN, INT32_MIN};
+    BBS_CUDA(cudaMemcpyAsync(d_mm.p, init, sizeof(init), cudaMemcpyHostToDevice, s));
+    voxel_box_kernel<<<grid_for(n), kThreads, 0, s>>>(d_vox, n, d_mm.p);
+    BBS_CUDA(cudaGetLastError());
+    int32_t mm[6];
+    BBS_CUDA(cudaMemcpyAsync(mm, d_mm.p, sizeof(mm), cudaMemcpyDeviceToHost, s));
+    BBS_CUDA(cudaStreamSynchronize(s));
+    for (int a = 0; a < 3; ++a) {
+      lo[a] = mm[a];
+      hi[a] = mm[3 + a];
+    }
+    check_box(l, lo, hi, dims, bits);
+    BBS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&keys), n * sizeof(unsigned long long), s));
+    const int3 bmin = make_int3(static_cast<int32_t>(lo[0]), static_cast<int32_t>(lo[1]),
+                                static_cast<int32_t>(lo[2]));
+    pack_kernel<<<grid_for(n), kThreads, 0, s>>>(d_vox, n, bmin, bits[1], bits[2], keys);
+    BBS_CUDA(cudaGetLastError());
+    nu = sort_unique(keys, n, static_cast<int>(bits[0] + bits[1] + bits[2]), s);
+  }
+  finish_level(m, l, keys, nu, lo, dims, bits, m->layout_pref);
+}
+
+void begin_levels(bbs_map* m, int n_levels) {
+  m->levels.assign(static_cast<size_t>(n_levels), bbs_map::Level{});
+  m->view.n_levels = n_levels;
+  m->view.r = m->r;
+}
+
 void build_map_from_levels(bbs_map* m, const int32_t* const* lv, const uint64_t* counts,
                            int n_levels) {
   DeviceGuard g(m->device);
   cudaStream_t s = m->stream;
-  m->levels.assign(static_cast<size_t>(n_levels), bbs_map::Level{});
-  m->view.n_levels = n_levels;
-  m->view.r = m->r;
+  begin_levels(m, n_levels);
   for (int l = 0; l < n_levels; ++l) {
     const uint64_t n = counts[l];
-    int64_t lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
-    uint64_t dims[3] = {1, 1, 1};
-    uint32_t bits[3] = {1, 1, 1};
-    unsigned long long* keys = nullptr;
-    uint64_t nu = 0;
-    if (n) {
-      for (int a = 0; a < 3; ++a) {
-        lo[a] = INT64_MAX;
-        hi[a] = INT64_MIN;
-      }
-      for (uint64_t i = 0; i < n; ++i)
-        for (int a = 0; a < 3; ++a) {
-          lo[a] = std::min<int64_t>(lo[a], lv[l][3 * i + a]);
-          hi[a] = std::max<int64_t>(hi[a], lv[l][3 * i + a]);
-        }
-      check_box(l, lo, hi, dims, bits);
-      DevBuf<int32_t> d_vox(3 * n, s);
-      BBS_CUDA(cudaMemcpyAsync(d_vox.p, lv[l], 3 * n * sizeof(int32_t), cudaMemcpyHostToDevice, s));
-      BBS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&keys), n * sizeof(unsigned long long), s));
-      const int3 bmin = make_int3(static_cast<int32_t>(lo[0]), static_cast<int32_t>(lo[1]),
-                                  static_cast<int32_t>(lo[2]));
-      pack_kernel<<<grid_for(n), kThreads, 0, s>>>(d_vox.p, n, bmin, bits[1], bits[2], keys);
-      BBS_CUDA(cudaGetLastError());
-      nu = sort_unique(keys, n, static_cast<int>(bits[0] + bits[1] + bits[2]), s);
-    }
-    finish_level(m, l, keys, nu, lo, dims, bits, m->layout_pref);
+    DevBuf<int32_t> d_vox(3 * std::max<uint64_t>(n, 1), s);
+    if (n) BBS_CUDA(cudaMemcpyAsync(d_vox.p, lv[l], 3 * n * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+    build_level_from_device_voxels(m, l, d_vox.p, n);
   }
   BBS_CUDA(cudaStreamSynchronize(s));
 }

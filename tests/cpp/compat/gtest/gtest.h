@@ -1,7 +1,7 @@
 // Minimal GoogleTest-compatible shim (GTest is not installed in this image).
 // Supports what the reference's proj/tests sources use: TEST, EXPECT_* /
 // ASSERT_* (EQ NE LT LE GT GE TRUE FALSE NEAR DOUBLE_EQ THROW) with `<<`
-// messages, and RecordProperty.  main() lives in gtest_main.cpp.
+// messages, TEST_F fixtures (SetUp/TearDown) and RecordProperty.  main() lives in gtest_main.cpp.
 #pragma once
 
 #include <cmath>
@@ -88,7 +88,32 @@ inline void RecordProperty(const std::string& k, const std::string& v) {
   std::cerr << "  [property] " << k << " = " << v << std::endl;
 }
 
+namespace testing {
+// Fixture base (TEST_F): SetUp before and TearDown after each test body.
+class Test {
+ public:
+  virtual ~Test() = default;
+  virtual void SetUp() {}
+  virtual void TearDown() {}
+};
+}  // namespace testing
+
 #define GTSHIM_CAT(a, b) a##b
+#define TEST_F(fixture, name)                                                          \
+  struct GTSHIM_CAT(fixture##_, name) : public fixture {                               \
+    void Body();                                                                       \
+    void Run() {                                                                       \
+      this->SetUp();                                                                   \
+      Body();                                                                          \
+      this->TearDown();                                                                \
+    }                                                                                  \
+  };                                                                                   \
+  static ::gtshim::Registrar GTSHIM_CAT(gtshim_reg_##fixture##_, name)(                \
+      #fixture, #name, [] {                                                            \
+        GTSHIM_CAT(fixture##_, name) t;                                                \
+        t.Run();                                                                       \
+      });                                                                              \
+  void GTSHIM_CAT(fixture##_, name)::Body()
 #define TEST(suite, name)                                                              \
   static void GTSHIM_CAT(gtshim_##suite##_, name)();                                   \
   static ::gtshim::Registrar GTSHIM_CAT(gtshim_reg_##suite##_, name)(                  \

@@ -1,4 +1,4 @@
-"""The reference's OWN unit tests (proj/tests/voxel_map_test.cpp,
+"""The reference's OWN unit tests (proj/tests/voxel_map_test.cpp, map_io_test.cpp,
 search_test.cpp, angular_grid_test.cpp), compiled unmodified against the
 B200 facade (include/bnbloc_b200.hpp) by tests/cpp/Makefile, run on the GPU.
 Every map build, membership probe, score, batch_evaluate and search they
@@ -14,7 +14,8 @@ BIN = os.path.join(ROOT, "tests", "cpp", "bin")
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("suite", ["voxel_map_test", "search_test", "angular_grid_test"])
+@pytest.mark.parametrize("suite", ["voxel_map_test", "search_test", "angular_grid_test",
+                                   "map_io_test"])
 def test_reference_suite_passes_on_device(suite):
     exe = os.path.join(BIN, suite)
     if not os.path.exists(exe):
