@@ -192,6 +192,16 @@ int bbs_bounding_box(const double* xyz, uint64_t n, bbs_aabb* out);
 int bbs_prepare_source(const double* xyz, uint64_t n, uint64_t target_points, double* out_xyz,
                        uint64_t capacity, uint64_t* count, double* leaf, int32_t* converged,
                        double* d_max);
+/* prepare_source on the device (csrc/source_prep.cu): auto_leaf's bisection
+ * with device voxel counts and voxel_grid_downsample's sort + centroids on
+ * `device`.  Leaf, convergence flag, voxel set and output order equal the
+ * reference's; a voxel's centroid sums its points in input order (the
+ * reference in std::sort's unstable order), so centroids of voxels with >= 3
+ * points may differ from bbs_prepare_source in the last bits.  Used by
+ * bbs_localize_scan. */
+int bbs_prepare_source_device(int32_t device, const double* xyz, uint64_t n, uint64_t target_points,
+                              double* out_xyz, uint64_t capacity, uint64_t* count, double* leaf,
+                              int32_t* converged, double* d_max);
 /* Root node count of initial_nodes, nodes.hpp:60-85. */
 int bbs_initial_node_count(const bbs_search_config* cfg, double d_max, const bbs_aabb* range,
                            uint64_t* count);
@@ -255,7 +265,8 @@ int bbs_batch_evaluate(bbs_map_t map, const double* scan_xyz, uint64_t k,
 /* search, search.hpp:72-186. */
 int bbs_search(bbs_map_t map, const double* scan_xyz, uint64_t k, const bbs_search_config* cfg,
                bbs_search_result* result);
-/* localize_scan, pipeline.hpp:45-51. */
+/* localize_scan, pipeline.hpp:45-51 (prepare_source on the device, see
+ * bbs_prepare_source_device). */
 int bbs_localize_scan(bbs_map_t map, const double* raw_xyz, uint64_t n,
                       const bbs_search_config* cfg, uint64_t downsample_target,
                       bbs_search_result* result);

@@ -33,7 +33,7 @@ __all__ = [
     "Strategy", "BranchMode", "Layout", "SearchConfig", "Stats", "SearchResult", "Pose6",
     "AxisGrid", "AngularGrid", "LevelMap", "MultiResVoxelMap", "DeviceScan", "NODE_DTYPE",
     "batch_evaluate", "search", "search_sharded", "Comm", "nccl_version",
-    "save_map", "load_map", "is_map_file", "localize_scan", "prepare_source",
+    "save_map", "load_map", "is_map_file", "localize_scan", "prepare_source", "prepare_source_device",
     "max_range", "bounding_box", "pose_to_transform", "node_pose", "initial_node_count",
     "gen_scene", "gen_scans", "cut_scan", "SceneSpec", "device_count",
 ]
@@ -332,6 +332,20 @@ def prepare_source(raw_scan, target_points):
     _check(lib.bbs_prepare_source(_dptr(a), a.shape[0], int(target_points), _dptr(out), cnt.value,
                                   C.byref(cnt), C.byref(leaf), C.byref(conv), C.byref(dm)))
     return SourcePrep(out, leaf.value, bool(conv.value), dm.value)
+
+
+def prepare_source_device(raw_scan, target_points, device=0):
+    """pipeline.hpp:25-41 on the device (bbs_prepare_source_device): exact
+    leaf / convergence / voxel set; centroid sums in input order."""
+    a = _xyz(raw_scan)
+    cnt = C.c_uint64()
+    leaf, dm = C.c_double(), C.c_double()
+    conv = C.c_int32()
+    out = np.zeros((max(a.shape[0], 1), 3))
+    _check(lib.bbs_prepare_source_device(int(device), _dptr(a), a.shape[0], int(target_points), _dptr(out),
+                                         out.shape[0], C.byref(cnt), C.byref(leaf), C.byref(conv),
+                                         C.byref(dm)))
+    return SourcePrep(out[: cnt.value].copy(), leaf.value, bool(conv.value), dm.value)
 
 
 # ---- angular grid (angular_grid.hpp) ----------------------------------------

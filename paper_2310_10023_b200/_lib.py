@@ -40,6 +40,8 @@ SIGNATURES = {
     "bbs_max_range": (C.c_int, [_dp, _u64, _dp]),
     "bbs_bounding_box": (C.c_int, [_dp, _u64, C.POINTER(Aabb)]),
     "bbs_prepare_source": (C.c_int, [_dp, _u64, _u64, _dp, _u64, C.POINTER(_u64), _dp, _ip, _dp]),
+    "bbs_prepare_source_device": (C.c_int, [_i32, _dp, _u64, _u64, _dp, _u64, C.POINTER(_u64), _dp, _ip,
+                                            _dp]),
     "bbs_initial_node_count": (C.c_int, [C.POINTER(SearchConfigC), _d, C.POINTER(Aabb),
                                          C.POINTER(_u64)]),
     "bbs_map_build": (C.c_int, [_dp, _u64, _d, _i32, _d, _u64, C.POINTER(MapOptions),

@@ -110,5 +110,8 @@ struct SourcePrep {
   double d_max = 0.0;
 };
 SourcePrep host_prepare_source(const double* xyz, uint64_t n, uint64_t target);
+// The same on the device (source_prep.cu): exact leaf, convergence, voxel set
+// and order; centroid sums in input order within a voxel.
+SourcePrep device_prepare_source(int device, const double* xyz, uint64_t n, uint64_t target);
 
 }  // namespace bbs

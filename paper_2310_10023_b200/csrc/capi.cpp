@@ -167,6 +167,22 @@ int bbs_prepare_source(const double* xyz, uint64_t n, uint64_t target, double* o
   });
 }
 
+int bbs_prepare_source_device(int32_t device, const double* xyz, uint64_t n, uint64_t target,
+                              double* out_xyz, uint64_t capacity, uint64_t* count, double* leaf,
+                              int32_t* converged, double* d_max) {
+  return guard([&] {
+    REQUIRE(count && (xyz || n == 0), "bbs_prepare_source_device: null argument");
+    require_device(device);
+    const bbs::SourcePrep p = bbs::device_prepare_source(device, xyz, n, target);
+    const uint64_t m = p.xyz.size() / 3;
+    *count = m;
+    if (out_xyz) std::memcpy(out_xyz, p.xyz.data(), 3 * std::min(m, capacity) * sizeof(double));
+    if (leaf) *leaf = p.leaf;
+    if (converged) *converged = p.converged ? 1 : 0;
+    if (d_max) *d_max = p.d_max;
+  });
+}
+
 int bbs_initial_node_count(const bbs_search_config* cfg, double d_max, const bbs_aabb* range,
                            uint64_t* count) {
   return guard([&] {
@@ -422,9 +438,10 @@ int bbs_localize_scan(bbs_map_t map, const double* raw_xyz, uint64_t n, const bb
                       uint64_t downsample_target, bbs_search_result* result) {
   return guard([&] {
     REQUIRE(map && cfg && result && (raw_xyz || n == 0), "null argument");
-    // prepare_source, pipeline.hpp:25-41 (host), then search (pipeline.hpp:48)
+    // prepare_source, pipeline.hpp:25-41 (device voxel counts and centroids),
+    // then search (pipeline.hpp:48)
     const auto t0 = std::chrono::steady_clock::now();
-    const bbs::SourcePrep prep = bbs::host_prepare_source(raw_xyz, n, downsample_target);
+    const bbs::SourcePrep prep = bbs::device_prepare_source(map->device, raw_xyz, n, downsample_target);
     const double prep_ms =
         std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     const uint64_t k = prep.xyz.size() / 3;

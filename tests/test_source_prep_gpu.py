@@ -1,0 +1,78 @@
+"""prepare_source on the device (csrc/source_prep.cu)
+against the reference's prepare_source (pipeline.hpp:25-41, oracle/_ref).
+
+Exact: leaf (auto_leaf's bisection, point_cloud.hpp:137-182), convergence
+flag, number of voxels and their order (ascending voxel triple).  Centroids:
+the reference sums a voxel's points in std::sort's (unstable) order and the
+device in input order, so they agree to a few ulps (tolerance below: 64 ulps
+of the coordinate magnitude, rtol 1e-14 relative to the scan extent)."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _raw(B, seed, spacing=0.2, rng=14.0):
+    spec = B.SceneSpec.default(size_x=24.0, size_y=24.0, size_z=10.0, num_boxes=4,
+                               min_box_side=2.5, max_box_side=6.0, min_box_height=3.0,
+                               map_spacing=0.3, scan_spacing=spacing, scan_range=rng,
+                               min_scan_points=300)
+    return B.gen_scene(spec, seed)
+
+
+def _check(got, want_xyz, want_leaf, want_conv, want_dmax):
+    assert got.leaf == want_leaf and got.leaf_converged == want_conv
+    assert got.scan.shape == want_xyz.shape
+    scale = max(1.0, float(np.abs(want_xyz).max()))
+    np.testing.assert_allclose(got.scan, want_xyz, rtol=0, atol=1e-14 * scale)
+    assert abs(got.d_max - want_dmax) <= 1e-14 * scale
+    return float(np.mean(np.all(got.scan == want_xyz, axis=1)))
+
+
+@pytest.mark.parametrize("seed", [3, 9, 21])
+@pytest.mark.parametrize("target", [1, 50, 400, 1000, 5000])
+def test_device_prepare_source_matches_reference(B, ref, seed, target):
+    _, raw, _ = _raw(B, seed)
+    got = B.prepare_source_device(raw, target)
+    want_xyz, leaf, conv, dmax = ref.prepare_source(raw, target)
+    _check(got, want_xyz, leaf, conv, dmax)
+
+
+def test_device_prepare_source_passthrough(B, ref):
+    _, raw, _ = _raw(B, 5)
+    for target in (0, raw.shape[0], raw.shape[0] + 7):
+        got = B.prepare_source_device(raw, target)
+        assert np.array_equal(got.scan, raw) and got.leaf == 0.0
+        assert got.d_max == ref.prepare_source(raw, target)[3]
+
+
+def test_device_prepare_source_campus_raw_scan(B, ref):
+    """C2's raw scan (~236k points, extents need > 64 key bits at auto_leaf's
+    first probe: the three-pass LSD sort) down to ~10k points."""
+    spec = B.SceneSpec.default(size_x=300.0, size_y=300.0, size_z=30.0, num_boxes=60,
+                               min_box_side=6.0, max_box_side=30.0, min_box_height=8.0,
+                               map_spacing=0.19, scan_spacing=0.3, scan_range=60.0,
+                               min_scan_points=400)
+    _, raw, _ = B.gen_scene(spec, 1)
+    for target in (10000, 2000):
+        got = B.prepare_source_device(raw, target)
+        want = ref.prepare_source(raw, target)
+        # voxels of <= 2 points are bit-identical (a + b == b + a); C2's ~24-100
+        # points per voxel make most sums order-dependent in the last bits
+        # (measured: 10% / 4% bit-identical, max |diff| 7e-14 m)
+        _check(got, *want)
+
+
+def test_device_prepare_source_degenerate_clouds(B, ref):
+    """Coincident points (one voxel at every leaf: bisection cannot converge),
+    a line, negative coordinates and points on voxel boundaries."""
+    clouds = [
+        np.tile([[1.5, -2.0, 0.25]], (100, 1)),
+        np.column_stack([np.linspace(-10, 10, 999), np.zeros(999), np.zeros(999)]),
+        np.array([[i * 0.5, -j * 0.25, (i + j) * 0.125] for i in range(-20, 20) for j in range(30)]),
+    ]
+    for raw in clouds:
+        for target in (1, 10, 100):
+            got = B.prepare_source_device(raw, target)
+            want = ref.prepare_source(raw, target)
+            _check(got, *want)
