@@ -52,11 +52,11 @@ CONFIGS = {
                          scan_spacing=0.3, scan_range=80.0, min_scan_points=400),
                seed=1, r=0.2, max_level=6, rp=0.0873, K=30000),
     "c4": dict(workload="C4 throughput: 64 independent 10k-pt scans against the C2 campus map "
-                        "(~5M pts), 8 concurrent streams, BFS RotoTrans b=10000",
+                        "(~5M pts), 16 concurrent streams, BFS RotoTrans b=10000",
                spec=dict(size_x=300.0, size_y=300.0, size_z=30.0, num_boxes=60, min_box_side=6.0,
                          max_box_side=30.0, min_box_height=8.0, map_spacing=0.19, scan_spacing=0.3,
                          scan_range=60.0, min_scan_points=400),
-               seed=1, r=0.2, max_level=5, rp=0.02, K=10000, n_scans=64, streams=8),
+               seed=1, r=0.2, max_level=5, rp=0.02, K=10000, n_scans=64, streams=16),
     "c1": dict(workload="C1 room: 20x20x4 m (~200k map pts), 2k-pt scan, r=0.1 m, 6 levels, "
                         "360 deg yaw, +-5 deg roll/pitch, BFS RotoTrans b=10000",
                spec=dict(size_x=20.0, size_y=20.0, size_z=4.0, num_boxes=8, min_box_side=1.0,
@@ -464,7 +464,7 @@ def run_b200_throughput(args, cfgd):
     cfg = search_config(B, cfgd)
     vmap = B.MultiResVoxelMap.build(map_pts, cfgd["r"], cfgd["max_level"], device=local)
     dscans = {j: B.DeviceScan(vmap, scans[j]) for j in mine}
-    T = cfgd["streams"]
+    T = int(os.environ.get("BBS_BENCH_STREAMS", cfgd["streams"]))
     streams = [B.DeviceStream(local) for _ in range(T)]
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 
