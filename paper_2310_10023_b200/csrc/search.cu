@@ -1346,6 +1346,14 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
     BBS_CUDA(capturing ? cudaEventRecordWithFlags(ev, s, cudaEventRecordExternal)
                        : cudaEventRecord(ev, s));
   };
+  // BBS_DEBUG_PHASES: per-phase in-stream times of every epoch (no graphs;
+  // each event breaks the PDL overlap, so phases read ~2 us long)
+  const bool dbg_phases = std::getenv("BBS_DEBUG_PHASES") != nullptr;
+  std::vector<cudaEvent_t> ev_dbg(dbg_phases ? 3 * E : 0);
+  for (auto& ev : ev_dbg) ev = W.next_event();
+  double dbg_sum[6] = {0, 0, 0, 0, 0, 0};
+  uint64_t dbg_n = 0;
+  cudaEvent_t dbg_prev = ev_loop;
   // one flush epoch (frontier -> branch -> score -> survivors -> sort -> merge)
   auto enqueue_epoch = [&](int e) {
     launch_pdl(frontier_kernel, 1, kFT, 0, s, d_st, q, gv, cfg.batch_size, exp_parent, exp_off, d_trace,
@@ -1372,11 +1380,14 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
     launch_pdl(survivors_kernel, surv_grid, kST, 0, s, d_st, q, strategy, pending, pscores, s_key,
                surv_tiles);
     BBS_CUDA(cudaGetLastError());
+    if (dbg_phases) record(ev_dbg[3 * e]);
     launch_pdl(rank_sort_kernel, grid1(pend_cap, kRT), kRT, 0, s, d_st, s_key, s_key2);
     BBS_CUDA(cudaGetLastError());
+    if (dbg_phases) record(ev_dbg[3 * e + 1]);
     launch_pdl(merge_kernel, static_cast<unsigned>(std::min<uint64_t>((qcap + kMTile - 1) / kMTile, 148ull * 8)),
                kMT, 0, s, d_st, q, strategy, s_key2);
     BBS_CUDA(cudaGetLastError());
+    if (dbg_phases) record(ev_dbg[3 * e + 2]);
     launches += 6;  // frontier, branch, score, survivors, rank_sort, merge (+ finalize)
     if (roots_dev_x) {  // incumbent + activity over NCCL, no host round-trip
       xchg_pack_kernel<<<1, 1, 0, s>>>(d_st, d_x);
@@ -1451,7 +1462,7 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
     // of collectives) per batch; the stop decision uses the reduced flag
     const int n_ep = (self_active || roots_dev_x) ? E : 1;
     // graphs pay off for long searches (capture + instantiate ~0.2 ms)
-    if (n_ep == E && E > 1 && pass_ms.size() >= graph_after) {
+    if (n_ep == E && E > 1 && pass_ms.size() >= graph_after && !dbg_phases) {
       if (!batch_exec || batch_qcap != qcap || batch_pool != q.pool) {
         if (batch_exec) BBS_CUDA(cudaGraphExecDestroy(batch_exec));
         batch_exec = nullptr;
@@ -1479,6 +1490,19 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
     for (int e = 0; e < n_ep; ++e) {
       pass_ms.push_back(elapsed(ev_loop, ev_pass[e]));
       esm += elapsed(ev_s0[e], ev_s1[e]);
+      if (dbg_phases) {
+        const cudaEvent_t pts[7] = {dbg_prev, ev_pass[e], ev_s0[e], ev_s1[e], ev_dbg[3 * e], ev_dbg[3 * e + 1],
+                                    ev_dbg[3 * e + 2]};
+        for (int k = 0; k < 6; ++k) dbg_sum[k] += elapsed(pts[k], pts[k + 1]);
+        ++dbg_n;
+        dbg_prev = ev_dbg[3 * e + 2];
+      }
+    }
+    if (dbg_phases && n_ep > 0) {
+      // the next batch reuses the events: keep the last end time in its own event
+      cudaEvent_t keep = W.next_event();
+      BBS_CUDA(cudaEventRecord(keep, s));
+      dbg_prev = keep;
     }
     hs = *W.h_st;
     self_active = hs.active != 0;
@@ -1489,6 +1513,12 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
   }
   cudaEvent_t ev_end = W.next_event();
   BBS_CUDA(cudaEventRecord(ev_end, s));
+  if (dbg_phases && dbg_n) {
+    static const char* names[6] = {"frontier", "branch", "score", "survivors", "rank_sort", "merge"};
+    std::fprintf(stderr, "[phases] %llu epochs, us/epoch:", static_cast<unsigned long long>(dbg_n));
+    for (int k = 0; k < 6; ++k) std::fprintf(stderr, " %s %.2f", names[k], 1e3 * dbg_sum[k] / dbg_n);
+    std::fprintf(stderr, "\n");
+  }
   BBS_CUDA(cudaMemcpyAsync(W.h_st, d_st, sizeof(EpochState), cudaMemcpyDeviceToHost, s));
   d2h += sizeof(EpochState);
   BBS_CUDA(cudaStreamSynchronize(s));
