@@ -40,6 +40,7 @@ __device__ __forceinline__ uint32_t cache_hash(unsigned long long key) {
 }
 
 constexpr int kBuildThreads = 512;
+constexpr uint32_t kEarlyAbortPoints = 2048;  // sample before judging a build's de-duplication
 
 // One CTA per claimed (level, rotation): rotate + floor every scan point
 // (fast path), de-duplicate the voxel offsets in a shared-memory hash, and
@@ -136,7 +137,10 @@ __global__ void __launch_bounds__(kBuildThreads) cache_build_kernel(RotCache c, 
         py[h] = live ? scan.y[p[h]] : 0.0;
         pz[h] = live ? scan.z[p[h]] : 0.0;
       }
-      if (!dense && s_distinct >= kCacheHashCap) {  // uniform: read after the step barrier
+      // uniform (read after the step barrier): give up when the table is full,
+      // or early when the offsets seen so far do not even halve the points
+      // (fine levels: the histogram would cost more than the runs it serves)
+      if (!dense && (s_distinct >= kCacheHashCap || (p0 >= kEarlyAbortPoints && 2u * s_distinct > p0))) {
         aborted = true;
         break;
       }
@@ -292,6 +296,12 @@ __global__ void __launch_bounds__(kBuildThreads) cache_build_kernel(RotCache c, 
       c.info[slot] = fits ? make_int4(kCacheReady, static_cast<int32_t>(off), static_cast<int32_t>(n_ent), namb)
                           : make_int4(kCacheNone, 0, 0, 0);
       if (fits) atomicMax(&c.ctl[kCtlMaxEnt], n_ent);  // sizes the probe's chunk grid
+      // the prebuilt level predicts the finer ones: a scan of surfaces has
+      // ~4x the distinct offsets per halving of the cell, so when that would
+      // not halve the points (or not fit a build) the finer levels are
+      // scored directly instead of each paying a failed build first
+      if (fits && l == c.pre_level && 4u * n_ent > min(scan.k / 2u, static_cast<uint32_t>(kCacheHashCap)))
+        for (int l2 = 0; l2 < l; ++l2) c.ctl[4 + l2] = 1u;
     }
     __syncthreads();
   }

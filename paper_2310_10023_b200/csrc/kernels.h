@@ -134,6 +134,7 @@ struct RotCache {
   // the probe reads the level's z-column words from a zero-padded shared
   // window [sx0, sx0 + pitch) x [sy0, sy0 + rows) (relative to box_min),
   // pre-shifted up by 8 bits
+  int pre_level;                // level prebuilt for all rotations (-1: none)
   int stg_level;
   int32_t stg_sx0, stg_sy0;
   uint32_t stg_pitch, stg_rows;

@@ -1214,6 +1214,7 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
   }();
   RotCache cache{};
   cache.stg_level = -1;
+  cache.pre_level = -1;
   // a histogram build costs about one direct run; small scans (C1: K = 2000)
   // rarely amortize it, large ones (C2/C3) reuse rotations across flushes
   if (cache_on && K >= 4096) {
@@ -1311,6 +1312,7 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
       BBS_CUDA(cudaMemsetAsync(cache.info, 0xFF, slots * sizeof(int4), s));  // all kCacheEmpty
       BBS_CUDA(cudaMemsetAsync(cache.ctl, 0, kCacheCtl * sizeof(uint32_t), s));
       if (prebuild) {
+        cache.pre_level = pl;
         cudaEvent_t e0 = W.next_event(), e1 = W.next_event();
         BBS_CUDA(cudaEventRecord(e0, s));
         launch_cache_prebuild(m->view, gv, sv, cache, pl, static_cast<uint32_t>(pre_rot), s);
@@ -1493,7 +1495,12 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
       if (dbg_phases) {
         const cudaEvent_t pts[7] = {dbg_prev, ev_pass[e], ev_s0[e], ev_s1[e], ev_dbg[3 * e], ev_dbg[3 * e + 1],
                                     ev_dbg[3 * e + 2]};
-        for (int k = 0; k < 6; ++k) dbg_sum[k] += elapsed(pts[k], pts[k + 1]);
+        float ph[6];
+        for (int k = 0; k < 6; ++k) dbg_sum[k] += (ph[k] = elapsed(pts[k], pts[k + 1]));
+        if (dbg_n < 16)
+          std::fprintf(stderr, "[phases] epoch %llu: %.1f %.1f %.1f %.1f %.1f %.1f us\n",
+                       static_cast<unsigned long long>(dbg_n), 1e3 * ph[0], 1e3 * ph[1], 1e3 * ph[2],
+                       1e3 * ph[3], 1e3 * ph[4], 1e3 * ph[5]);
         ++dbg_n;
         dbg_prev = ev_dbg[3 * e + 2];
       }
