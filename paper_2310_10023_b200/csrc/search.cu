@@ -1051,7 +1051,7 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
   uint64_t launches = 0;
 
   cudaEvent_t ev_start = W.next_event(), ev_roots0 = W.next_event(), ev_roots1 = W.next_event(),
-              ev_loop = W.next_event();
+              ev_loop = W.next_event(), ev_sel = W.next_event(), ev_q0 = W.next_event();
   BBS_CUDA(cudaEventRecord(ev_start, s));
 
   // ---- root batch (search.hpp:111-124) ----
@@ -1121,6 +1121,7 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
     BBS_CUDA(cudaMemcpyAsync(&W.h_small[0], d_probes, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
     BBS_CUDA(cudaMemcpyAsync(&W.h_small[1], d_nsel, sizeof(int), cudaMemcpyDeviceToHost, s));
     d2h += sizeof(unsigned long long) + sizeof(int);
+    BBS_CUDA(cudaEventRecord(ev_sel, s));
     BBS_CUDA(cudaStreamSynchronize(s));
     n_root_surv = *reinterpret_cast<int*>(&W.h_small[1]);
   } else {
@@ -1139,6 +1140,7 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
   uint64_t pool_cap = static_cast<uint64_t>(n_root_surv) + static_cast<uint64_t>(E + 1) * pend_cap;
   q.pool = W.pool.get(pool_cap, s);
   pool_cap = W.pool.cap;
+  BBS_CUDA(cudaEventRecord(ev_q0, s));
   if (n_root_surv > 0) {
     // nodes in initial_nodes order (seq = position), stable sort on the
     // score key over only the bits it spans, then gather nodes + queue keys
@@ -1520,6 +1522,11 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
   }
   cudaEvent_t ev_end = W.next_event();
   BBS_CUDA(cudaEventRecord(ev_end, s));
+  if (dbg_phases && total > 0) {
+    std::fprintf(stderr, "[phases] init: roots %.1f us, select %.1f us, host sync gap %.1f us, queue %.1f us\n",
+                 1e3 * elapsed(ev_roots0, ev_roots1), 1e3 * elapsed(ev_roots1, ev_sel), 1e3 * elapsed(ev_sel, ev_q0),
+                 1e3 * elapsed(ev_q0, ev_loop));
+  }
   if (dbg_phases && dbg_n) {
     static const char* names[6] = {"frontier", "branch", "score", "survivors", "rank_sort", "merge"};
     std::fprintf(stderr, "[phases] %llu epochs, us/epoch:", static_cast<unsigned long long>(dbg_n));
