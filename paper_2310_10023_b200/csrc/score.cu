@@ -31,6 +31,46 @@ namespace bbs {
 namespace {
 
 // ---- runs kernel ------------------------------------------------------------
+// Per point of [p0, p1) (strided by the CTA): rotate once, probe the run's
+// M translations, reduce the counts into s_cnt.
+template <int M, int NT>
+__device__ __forceinline__ void runs_points(const LevelView& L, const double R[9], double tmax,
+                                            const ScanView& scan, const int32_t (*s_t)[3], int count,
+                                            uint32_t p0, uint32_t p1, int lane, int32_t* s_cnt) {
+  int32_t tx[M], ty[M], tz[M];
+  int cnt[M];
+#pragma unroll
+  for (int j = 0; j < M; ++j) {
+    tx[j] = s_t[j][0];
+    ty[j] = s_t[j][1];
+    tz[j] = s_t[j][2];
+    cnt[j] = 0;
+  }
+  for (uint32_t p = p0 + threadIdx.x; p < p1; p += blockDim.x) {
+    const double px = scan.x[p], py = scan.y[p], pz = scan.z[p];
+    const double rx = rot_row(R[0], R[1], R[2], px, py, pz);
+    const double ry = rot_row(R[3], R[4], R[5], px, py, pz);
+    const double rz = rot_row(R[6], R[7], R[8], px, py, pz);
+    int32_t fx, fy, fz;
+    const bool ok = fast_floor(rx, L.inv_cell, tmax, &fx) & fast_floor(ry, L.inv_cell, tmax, &fy) &
+                    fast_floor(rz, L.inv_cell, tmax, &fz);
+    if (ok) {
+#pragma unroll
+      for (int j = 0; j < M; ++j)
+        if (j < count) cnt[j] += level_contains(L, fx + tx[j], fy + ty[j], fz + tz[j]) ? 1 : 0;
+    } else {
+#pragma unroll
+      for (int j = 0; j < M; ++j)
+        if (j < count) cnt[j] += exact_hit(L, rx, ry, rz, tx[j], ty[j], tz[j]);
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < M; ++j) {
+    const int v = __reduce_add_sync(0xffffffffu, cnt[j]);
+    if (lane == 0 && j < count && v) atomicAdd(&s_cnt[j], v);
+  }
+}
+
 // One work item = (run of <= NT same-rotation nodes, tile of scan points).
 // Each thread walks its points; per point the rotation work is shared by the
 // run's NT translations.  Counts are reduced warp -> block -> global.
@@ -101,42 +141,14 @@ __global__ void __launch_bounds__(256) score_runs_kernel(
     double R[9];
 #pragma unroll
     for (int i = 0; i < 9; ++i) R[i] = s_R[i];
-    int32_t tx[NT], ty[NT], tz[NT];
-#pragma unroll
-    for (int j = 0; j < NT; ++j) {
-      tx[j] = s_t[j][0];
-      ty[j] = s_t[j][1];
-      tz[j] = s_t[j][2];
-    }
-    int cnt[NT];
-#pragma unroll
-    for (int j = 0; j < NT; ++j) cnt[j] = 0;
-
     const uint32_t p0 = pt * tile;
     const uint32_t p1 = min(k, p0 + tile);
-    for (uint32_t p = p0 + threadIdx.x; p < p1; p += blockDim.x) {
-      const double px = scan.x[p], py = scan.y[p], pz = scan.z[p];
-      const double rx = rot_row(R[0], R[1], R[2], px, py, pz);
-      const double ry = rot_row(R[3], R[4], R[5], px, py, pz);
-      const double rz = rot_row(R[6], R[7], R[8], px, py, pz);
-      int32_t fx, fy, fz;
-      const bool ok = fast_floor(rx, L.inv_cell, tmax, &fx) & fast_floor(ry, L.inv_cell, tmax, &fy) &
-                      fast_floor(rz, L.inv_cell, tmax, &fz);
-      if (ok) {
-#pragma unroll
-        for (int j = 0; j < NT; ++j)
-          if (j < count) cnt[j] += level_contains(L, fx + tx[j], fy + ty[j], fz + tz[j]) ? 1 : 0;
-      } else {
-#pragma unroll
-        for (int j = 0; j < NT; ++j)
-          if (j < count) cnt[j] += exact_hit(L, rx, ry, rz, tx[j], ty[j], tz[j]);
-      }
-    }
-#pragma unroll
-    for (int j = 0; j < NT; ++j) {
-      const int v = __reduce_add_sync(0xffffffffu, cnt[j]);
-      if (lane == 0 && j < count && v) atomicAdd(&s_cnt[j], v);
-    }
+    // short runs (random candidates: ~3 per rotation) take a 4-wide body so
+    // the predicated-off lanes of the NT-wide one cost no issue slots
+    if (count <= 4)
+      runs_points<4, NT>(L, R, tmax, scan, s_t, count, p0, p1, lane, s_cnt);
+    else
+      runs_points<NT, NT>(L, R, tmax, scan, s_t, count, p0, p1, lane, s_cnt);
     __syncthreads();
     if (threadIdx.x < static_cast<unsigned>(count)) {
       if (n_ptiles == 1)
