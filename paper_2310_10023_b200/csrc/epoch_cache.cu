@@ -39,6 +39,23 @@ __device__ __forceinline__ uint32_t cache_hash(unsigned long long key) {
   return static_cast<uint32_t>((key * 0x9E3779B97F4A7C15ull) >> 51);  // 13 bits
 }
 
+// Cell i of a dense box with rows of n cells: (x, y, z) = (i % n, i / n % n,
+// i / n^2), divided once and then stepped cell by cell.
+struct CellWalk {
+  int i, x, y, z, n;
+  __device__ CellWalk(int i0, int n_) : i(i0), x(i0 % n_), y(i0 / n_ % n_), z(i0 / (n_ * n_)), n(n_) {}
+  __device__ void next() {
+    ++i;
+    if (++x == n) {
+      x = 0;
+      if (++y == n) {
+        y = 0;
+        ++z;
+      }
+    }
+  }
+};
+
 constexpr int kBuildThreads = 512;
 constexpr uint32_t kEarlyAbortPoints = 2048;  // sample before judging a build's de-duplication
 
@@ -243,10 +260,10 @@ __global__ void __launch_bounds__(kBuildThreads) cache_build_kernel(RotCache c, 
     if (fits && staged) {
       int32_t* gw = reinterpret_cast<int32_t*>(c.pool + off);
       unsigned char* gb = reinterpret_cast<unsigned char*>(c.pool + off);
-      for (int i = dc0; i < dc1; ++i) {
-        uint32_t v = dcount(i);
+      for (CellWalk w(dc0, dxy); w.i < dc1; w.next()) {
+        uint32_t v = dcount(w.i);
         if (!v) continue;
-        const int fx = i % dxy - dr, fy = (i / dxy) % dxy - dr, fz = i / (dxy * dxy) + dzlo;
+        const int fx = w.x - dr, fy = w.y - dr, fz = w.z + dzlo;
         const int32_t eoff = fy * static_cast<int32_t>(c.stg_pitch) + fx;
         for (; v; ++epos) {
           const uint32_t w = min(v, 255u);
@@ -266,11 +283,10 @@ __global__ void __launch_bounds__(kBuildThreads) cache_build_kernel(RotCache c, 
         gb[(g * 8 + 5) * 4 + k] = 0;
       }
     } else if (fits && dense) {
-      for (int i = dc0; i < dc1; ++i) {
-        const uint32_t v = dcount(i);
+      for (CellWalk w(dc0, dxy); w.i < dc1; w.next()) {
+        const uint32_t v = dcount(w.i);
         if (v) {
-          const int fx = i % dxy - dr, fy = (i / dxy) % dxy - dr, fz = i / (dxy * dxy) + dzlo;
-          c.pool[off + epos] = make_int4(fx, fy, fz, static_cast<int32_t>(v));
+          c.pool[off + epos] = make_int4(w.x - dr, w.y - dr, w.z + dzlo, static_cast<int32_t>(v));
           ++epos;
         }
       }
