@@ -556,14 +556,14 @@ void launch_epoch_score(const MapView& map, const GridView& grid, const ScanView
     launch_score_cube8(map, grid, scan, pending, d_n, n_max, n_ptiles, scores, nullptr, s);
     return;
   }
-  static bool attr_done = false;
+  static std::atomic<uint64_t> attr_done{0};
+  static std::mutex attr_mu;
   const int build_smem = kCacheHashSlots * 12 + kCacheAmbCap * 4;
   static_assert(kCacheHashSlots % kBuildThreads == 0, "slot rows per thread");
-  if (!attr_done) {
-    BBS_CUDA(cudaFuncSetAttribute(cache_build_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  build_smem));
-    attr_done = true;
-  }
+  once_per_device(attr_done, attr_mu, [&] {
+    BBS_CUDA(cudaFuncSetAttribute(cache_build_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, build_smem));
+    BBS_CUDA(cudaFuncSetAttribute(cache_probe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kStageWindowMax));
+  });
   const uint32_t max_runs = (n_max + 7) / 8;
   // the epoch's branch kernel already claimed the slots (cache_claim_run)
   // after its frontier reset ctl[2..3]
@@ -575,12 +575,7 @@ void launch_epoch_score(const MapView& map, const GridView& grid, const ScanView
   const uint64_t wpc = kProbeThreads / 32;  // warps per CTA
   const unsigned g = static_cast<unsigned>(std::min<uint64_t>((warp_items + wpc - 1) / wpc + 1, 148ull * 16));
   const int win_smem = cache.stg_level >= 0 ? static_cast<int>(((cache.stg_pitch * cache.stg_rows * 4u) + 15u) & ~15u) : 0;
-  static bool probe_attr = false;
-  if (!probe_attr) {
-    BBS_CUDA(cudaFuncSetAttribute(cache_probe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  kStageWindowMax));
-    probe_attr = true;
-  }
+
   unsigned gp = g;
   if (win_smem > 0) {
     // persistent: each CTA stages the window once

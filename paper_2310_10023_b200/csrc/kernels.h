@@ -1,6 +1,9 @@
 // kernels.h — host launchers of the device kernels (score.cu, search.cu).
 #pragma once
 
+#include <atomic>
+#include <mutex>
+
 #include <cuda_runtime.h>
 
 #include <utility>
@@ -26,6 +29,9 @@ struct BoxParams {
   uint32_t n_tchunks;         // translation chunks per rotation (grid = nrot * n_tchunks)
   int32_t fpad;               // bound on |voxel offset| of a rotated scan point (d_max / cell + 2)
   double tmax;                // max |translation index| in the box (fast-path guard)
+  // dense histogram box of the root level (dn_r = 0: hash), see RotCache
+  int32_t dn_r, dn_zlo, dn_nz;
+  double dn_eps, dn_eps1;
 };
 
 // Padded shared-memory copy of the root level's z-column words for the
@@ -179,6 +185,21 @@ void build_stage_window(const MapView& map, const RotCache& cache, uint32_t* win
 // call pdl_wait() before reading what its predecessor wrote.  BBS_PDL=0
 // turns it off (plain launches).
 bool pdl_enabled();
+
+// Runs f once per (call site, CUDA device): kernel attributes such as the
+// dynamic shared-memory limit are per device, and several host threads may
+// launch concurrently.
+template <typename F>
+void once_per_device(std::atomic<uint64_t>& done, std::mutex& mu, F&& f) {
+  int d = 0;
+  BBS_CUDA(cudaGetDevice(&d));
+  const uint64_t bit = 1ull << (d & 63);
+  if (done.load(std::memory_order_acquire) & bit) return;
+  std::lock_guard<std::mutex> lk(mu);
+  if (done.load(std::memory_order_relaxed) & bit) return;
+  f();
+  done.fetch_or(bit, std::memory_order_release);
+}
 template <typename... KArgs, typename... Args>
 void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
                 Args&&... args) {

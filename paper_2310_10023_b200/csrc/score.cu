@@ -449,6 +449,50 @@ __device__ __forceinline__ uint32_t hist_slot(unsigned long long key) {
   return static_cast<uint32_t>((key * 0x9E3779B97F4A7C15ull) >> 51);  // 13 bits
 }
 
+// One histogram entry (f, cnt) of root_hist_kernel, appended warp-cooperatively
+// (every lane calls; has = false for lanes without an entry).  Staged mode
+// (root_colpad_kernel): (padded column offset << 8 | z shift + 8) words in
+// groups of 4 with their counts packed as bytes (counts > 255 split),
+// dropping entries whose z never meets a translation's column; otherwise plain
+// (fx, fy, fz, count).
+__device__ __forceinline__ void root_emit(bool has, int32_t fx, int32_t fy, int32_t fz, int32_t cnt,
+                                          const BoxParams& bp, const RootStage& st, int4* ent4,
+                                          int* s_nent, int* s_badpad) {
+  const int lane = threadIdx.x & 31;
+  int parts = has ? 1 : 0;
+  int32_t sh = 0;
+  if (has && st.enabled) {
+    if (abs(fx) > bp.fpad || abs(fy) > bp.fpad) *s_badpad = 1;
+    sh = fz + st.zoff;
+    parts = (sh < static_cast<int32_t>(st.dimz) && sh > -static_cast<int32_t>(bp.nz)) ? (cnt + 254) / 255 : 0;
+  }
+  int incl = parts;  // warp inclusive scan of the parts
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, incl, d);
+    if (lane >= d) incl += v;
+  }
+  const int wtot = __shfl_sync(0xffffffffu, incl, 31);
+  int at = 0;
+  if (lane == 0 && wtot) at = atomicAdd(s_nent, wtot);
+  at = __shfl_sync(0xffffffffu, at, 0) + incl - parts;
+  if (!parts) return;
+  if (st.enabled) {
+    const uint32_t word = (static_cast<uint32_t>(fy * static_cast<int32_t>(st.pitch) + fx) << 8) |
+                          static_cast<uint32_t>(sh + 8);
+    int32_t* g = reinterpret_cast<int32_t*>(ent4);
+    unsigned char* wb = reinterpret_cast<unsigned char*>(ent4);
+    for (int q = 0; q < parts; ++q) {
+      const int e = at + q;
+      if (e >= 4 * kColGroupCap) break;
+      g[(e >> 2) * 8 + (e & 3)] = static_cast<int32_t>(word);
+      wb[((e >> 2) * 8 + 4) * 4 + (e & 3)] = static_cast<unsigned char>(min(255, cnt - 255 * q));
+    }
+  } else if (at < kHistCap) {  // more is an overflow (the rotation falls back)
+    ent4[at] = make_int4(fx, fy, fz, cnt);
+  }
+}
+
 __global__ void __launch_bounds__(512) root_hist_kernel(GridView grid, ScanView scan, BoxParams bp,
                                                         LevelView L, uint32_t rot_begin,
                                                         uint32_t rot_end, RootHist h, RootStage st,
@@ -456,8 +500,14 @@ __global__ void __launch_bounds__(512) root_hist_kernel(GridView grid, ScanView 
   extern __shared__ __align__(16) unsigned char smem[];
   unsigned long long* s_key = reinterpret_cast<unsigned long long*>(smem);  // 64 KB
   int32_t* s_cnt = reinterpret_cast<int32_t*>(s_key + kHistSlots);          // 32 KB
+  uint32_t* s_w = reinterpret_cast<uint32_t*>(smem);  // dense box: 16-bit counters (overlays the hash)
   __shared__ int s_distinct, s_namb, s_nent, s_skip, s_badpad;
   const uint32_t nrot = bp.nr * bp.np * bp.nw;
+  const int lane = threadIdx.x & 31;
+  // dense box (coarse root levels): direct-mapped counters, no probing
+  const int dr = bp.dn_r, dxy = 2 * dr + 1, dzlo = bp.dn_zlo;
+  const bool dense = dr > 0;
+  const int ncells = dense ? dxy * dxy * bp.dn_nz : 0;
   for (uint32_t rot = rot_begin + blockIdx.x; rot < rot_end; rot += gridDim.x) {
     const uint32_t slot = rot - rot_begin;
     uint32_t P, x0r;
@@ -469,9 +519,13 @@ __global__ void __launch_bounds__(512) root_hist_kernel(GridView grid, ScanView 
       }
       continue;
     }
-    for (int i = threadIdx.x; i < kHistSlots; i += blockDim.x) {
-      s_key[i] = kSlotEmpty;
-      s_cnt[i] = 0;
+    if (dense) {
+      for (int i = threadIdx.x; i < (ncells + 1) >> 1; i += blockDim.x) s_w[i] = 0u;
+    } else {
+      for (int i = threadIdx.x; i < kHistSlots; i += blockDim.x) {
+        s_key[i] = kSlotEmpty;
+        s_cnt[i] = 0;
+      }
     }
     if (threadIdx.x == 0) {
       s_distinct = 0;
@@ -484,101 +538,116 @@ __global__ void __launch_bounds__(512) root_hist_kernel(GridView grid, ScanView 
     const uint32_t ir = rot / (bp.np * bp.nw), ip = (rot / bp.nw) % bp.np, iw = rot % bp.nw;
     double R[9];
     rotation_of(grid, bp.level, static_cast<int>(ir), static_cast<int>(ip), static_cast<int>(iw), R);
-    for (uint32_t p0 = 0; p0 < scan.k; p0 += blockDim.x) {
-      const uint32_t p = p0 + threadIdx.x;
-      const bool live = p < scan.k;
-      bool ok = false;
-      int32_t fx = 0, fy = 0, fz = 0;
-      if (live) {
-        const double px = scan.x[p], py = scan.y[p], pz = scan.z[p];
-        ok = fast_floor(rot_row(R[0], R[1], R[2], px, py, pz), L.inv_cell, bp.tmax, &fx) &
-             fast_floor(rot_row(R[3], R[4], R[5], px, py, pz), L.inv_cell, bp.tmax, &fy) &
-             fast_floor(rot_row(R[6], R[7], R[8], px, py, pz), L.inv_cell, bp.tmax, &fz);
-        ok = ok && fx > -(1 << 20) && fx < (1 << 20) && fy > -(1 << 20) && fy < (1 << 20) &&
-             fz > -(1 << 20) && fz < (1 << 20);
-        if (!ok) {
-          const int a = atomicAdd(&s_namb, 1);
-          if (a < kAmbCap) h.amb[static_cast<uint64_t>(slot) * kAmbCap + a] = p;
-        }
-      }
-      const bool ins = live && ok && s_distinct < kHistCap;
-      if (live && ok && !ins) s_skip = 1;  // table saturated: this rotation falls back
-      const unsigned long long key = ins ? (static_cast<unsigned long long>(fx + (1 << 20)) << 42) |
-                                               (static_cast<unsigned long long>(fy + (1 << 20)) << 21) |
-                                               static_cast<unsigned long long>(fz + (1 << 20))
-                                         : kSlotEmpty;
-      // neighbouring scan points often share a voxel: one insert per distinct key per warp
-      const unsigned same = __match_any_sync(0xffffffffu, key);
-      if (ins && (__ffs(same) - 1) == (threadIdx.x & 31)) {
-        const int mult = __popc(same);
-        uint32_t hs = hist_slot(key);
-        for (;;) {
-          const unsigned long long prev = atomicCAS(&s_key[hs], kSlotEmpty, key);
-          if (prev == kSlotEmpty) atomicAdd(&s_distinct, 1);
-          if (prev == kSlotEmpty || prev == key) {
-            atomicAdd(&s_cnt[hs], mult);
-            break;
+    if (dense) {
+      // constant eps (bounds every in-box point's fast_floor eps; an
+      // out-of-box point sends the rotation to the chunked kernel)
+      const double eps = bp.dn_eps, eps1 = bp.dn_eps1, inv = L.inv_cell;
+      const uint32_t udxy = static_cast<uint32_t>(dxy), unz = static_cast<uint32_t>(bp.dn_nz);
+      for (uint32_t p0 = 0; p0 < scan.k; p0 += blockDim.x) {
+        const uint32_t p = p0 + threadIdx.x;
+        int idx = -1;
+        if (p < scan.k) {
+          const double px = scan.x[p], py = scan.y[p], pz = scan.z[p];
+          const double wx = __dmul_rn(rot_row(R[0], R[1], R[2], px, py, pz), inv);
+          const double wy = __dmul_rn(rot_row(R[3], R[4], R[5], px, py, pz), inv);
+          const double wz = __dmul_rn(rot_row(R[6], R[7], R[8], px, py, pz), inv);
+          const double flx = floor(wx), fly = floor(wy), flz = floor(wz);
+          const double frx = __dsub_rn(wx, flx), fry = __dsub_rn(wy, fly), frz = __dsub_rn(wz, flz);
+          if (frx > eps && frx < eps1 && fry > eps && fry < eps1 && frz > eps && frz < eps1) {
+            const uint32_t ux = static_cast<uint32_t>(__double2int_rz(flx)) + static_cast<uint32_t>(dr);
+            const uint32_t uy = static_cast<uint32_t>(__double2int_rz(fly)) + static_cast<uint32_t>(dr);
+            const uint32_t uz = static_cast<uint32_t>(__double2int_rz(flz)) - static_cast<uint32_t>(dzlo);
+            if (ux < udxy && uy < udxy && uz < unz)
+              idx = static_cast<int>((uz * udxy + uy) * udxy + ux);
+            else
+              s_skip = 1;
+          } else {
+            const int a = atomicAdd(&s_namb, 1);
+            if (a < kAmbCap) h.amb[static_cast<uint64_t>(slot) * kAmbCap + a] = p;
           }
-          hs = (hs + 1) & (kHistSlots - 1);
+        }
+        const unsigned same = __match_any_sync(0xffffffffu, idx);
+        if (idx >= 0 && (__ffs(same) - 1) == lane)
+          atomicAdd(&s_w[idx >> 1], static_cast<uint32_t>(__popc(same)) << ((idx & 1) << 4));
+      }
+    } else {
+      for (uint32_t p0 = 0; p0 < scan.k; p0 += blockDim.x) {
+        const uint32_t p = p0 + threadIdx.x;
+        const bool live = p < scan.k;
+        bool ok = false;
+        int32_t fx = 0, fy = 0, fz = 0;
+        if (live) {
+          const double px = scan.x[p], py = scan.y[p], pz = scan.z[p];
+          ok = fast_floor(rot_row(R[0], R[1], R[2], px, py, pz), L.inv_cell, bp.tmax, &fx) &
+               fast_floor(rot_row(R[3], R[4], R[5], px, py, pz), L.inv_cell, bp.tmax, &fy) &
+               fast_floor(rot_row(R[6], R[7], R[8], px, py, pz), L.inv_cell, bp.tmax, &fz);
+          ok = ok && fx > -(1 << 20) && fx < (1 << 20) && fy > -(1 << 20) && fy < (1 << 20) &&
+               fz > -(1 << 20) && fz < (1 << 20);
+          if (!ok) {
+            const int a = atomicAdd(&s_namb, 1);
+            if (a < kAmbCap) h.amb[static_cast<uint64_t>(slot) * kAmbCap + a] = p;
+          }
+        }
+        const bool ins = live && ok && s_distinct < kHistCap;
+        if (live && ok && !ins) s_skip = 1;  // table saturated: this rotation falls back
+        const unsigned long long key = ins ? (static_cast<unsigned long long>(fx + (1 << 20)) << 42) |
+                                                 (static_cast<unsigned long long>(fy + (1 << 20)) << 21) |
+                                                 static_cast<unsigned long long>(fz + (1 << 20))
+                                           : kSlotEmpty;
+        // neighbouring scan points often share a voxel: one insert per distinct key per warp
+        const unsigned same = __match_any_sync(0xffffffffu, key);
+        if (ins && (__ffs(same) - 1) == lane) {
+          const int mult = __popc(same);
+          uint32_t hs = hist_slot(key);
+          for (;;) {
+            const unsigned long long prev = atomicCAS(&s_key[hs], kSlotEmpty, key);
+            if (prev == kSlotEmpty) atomicAdd(&s_distinct, 1);
+            if (prev == kSlotEmpty || prev == key) {
+              atomicAdd(&s_cnt[hs], mult);
+              break;
+            }
+            hs = (hs + 1) & (kHistSlots - 1);
+          }
         }
       }
     }
     __syncthreads();
     bool over = s_skip || s_distinct > kHistCap || s_namb > kAmbCap;
     if (!over) {
-      // staged mode (root_colpad_kernel): entries (padded column offset << 8
-      // | z shift + 8) in groups of 4 with their counts packed as bytes
-      // (counts > 255 split), dropping those whose z never meets a
-      // translation's column; otherwise plain (fx, fy, fz, count)
       int4* ent4 = h.entries + static_cast<uint64_t>(slot) * kHistCap;
-      const int lane = threadIdx.x & 31;
-      for (int i0 = 0; i0 < kHistSlots; i0 += blockDim.x) {
-        const int i = i0 + threadIdx.x;
-        const unsigned long long key = s_key[i];
-        int parts = key != kSlotEmpty ? 1 : 0;
-        int32_t fx = 0, fy = 0, fz = 0, sh = 0, cnt = 0;
-        if (parts) {
-          fx = static_cast<int32_t>((key >> 42) & 0x1FFFFF) - (1 << 20);
-          fy = static_cast<int32_t>((key >> 21) & 0x1FFFFF) - (1 << 20);
-          fz = static_cast<int32_t>(key & 0x1FFFFF) - (1 << 20);
-          cnt = s_cnt[i];
-          if (st.enabled) {
-            if (abs(fx) > bp.fpad || abs(fy) > bp.fpad) s_badpad = 1;
-            sh = fz + st.zoff;
-            parts = (sh < static_cast<int32_t>(st.dimz) && sh > -static_cast<int32_t>(bp.nz)) ? (cnt + 254) / 255 : 0;
-          }
-        }
-        int incl = parts;  // warp inclusive scan of the parts
-#pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-          const int v = __shfl_up_sync(0xffffffffu, incl, d);
-          if (lane >= d) incl += v;
-        }
-        const int wtot = __shfl_sync(0xffffffffu, incl, 31);
-        int at = 0;
-        if (lane == 0 && wtot) at = atomicAdd(&s_nent, wtot);
-        at = __shfl_sync(0xffffffffu, at, 0) + incl - parts;
-        if (parts) {
-          if (st.enabled) {
-            const uint32_t word = (static_cast<uint32_t>(fy * static_cast<int32_t>(st.pitch) + fx) << 8) |
-                                  static_cast<uint32_t>(sh + 8);
-            int32_t* g = reinterpret_cast<int32_t*>(ent4);
-            unsigned char* wb = reinterpret_cast<unsigned char*>(ent4);
-            for (int q = 0; q < parts; ++q) {
-              const int e = at + q;
-              if (e >= 4 * kColGroupCap) break;
-              g[(e >> 2) * 8 + (e & 3)] = static_cast<int32_t>(word);
-              wb[((e >> 2) * 8 + 4) * 4 + (e & 3)] = static_cast<unsigned char>(min(255, cnt - 255 * q));
+      if (dense) {
+        // each thread walks a contiguous cell range; the warp emits in lockstep
+        const int dper = (ncells + static_cast<int>(blockDim.x) - 1) / static_cast<int>(blockDim.x);
+        const int dc0 = min(ncells, static_cast<int>(threadIdx.x) * dper), dc1 = min(ncells, dc0 + dper);
+        int cx = dc0 % dxy, cy = dc0 / dxy % dxy, cz = dc0 / (dxy * dxy);
+        for (int step = 0; step < dper; ++step) {
+          const int i = dc0 + step;
+          const uint32_t v = i < dc1 ? (s_w[i >> 1] >> ((i & 1) << 4)) & 0xFFFFu : 0u;
+          root_emit(v != 0u, cx - dr, cy - dr, cz + dzlo, static_cast<int32_t>(v), bp, st, ent4, &s_nent,
+                    &s_badpad);
+          if (++cx == dxy) {
+            cx = 0;
+            if (++cy == dxy) {
+              cy = 0;
+              ++cz;
             }
-          } else {
-            ent4[at] = make_int4(fx, fy, fz, cnt);
           }
+        }
+      } else {
+        for (int i0 = 0; i0 < kHistSlots; i0 += blockDim.x) {
+          const int i = i0 + threadIdx.x;
+          const unsigned long long key = s_key[i];
+          const bool has = key != kSlotEmpty;
+          root_emit(has, has ? static_cast<int32_t>((key >> 42) & 0x1FFFFF) - (1 << 20) : 0,
+                    has ? static_cast<int32_t>((key >> 21) & 0x1FFFFF) - (1 << 20) : 0,
+                    has ? static_cast<int32_t>(key & 0x1FFFFF) - (1 << 20) : 0, has ? s_cnt[i] : 0, bp, st,
+                    ent4, &s_nent, &s_badpad);
         }
       }
     }
     __syncthreads();
     // an offset beyond the padding or too many split entries: chunked fallback
-    over = over || s_badpad || (st.enabled && s_nent > 4 * kColGroupCap);
+    over = over || s_badpad || (st.enabled && s_nent > 4 * kColGroupCap) || (!st.enabled && s_nent > kHistCap);
     if (!over && st.enabled && (s_nent & 3)) {
       // zero-weight padding of the last group
       const int e = s_nent + static_cast<int>(threadIdx.x);
@@ -858,13 +927,12 @@ void launch_score_box_chunked(const MapView& map, const GridView& grid, const Sc
                               const BoxParams& bp, uint32_t rot_begin, uint32_t rot_end,
                               const int32_t* only, int32_t* scores, unsigned long long* probes,
                               cudaStream_t s) {
-  static bool attr_done = false;
+  static std::atomic<uint64_t> attr_done{0};
+  static std::mutex attr_mu;
   const int smem = kHashSlots * 8 + kHashSlots * 4 + kChunk * 16 + kChunk * 4;
-  if (!attr_done) {
-    BBS_CUDA(cudaFuncSetAttribute(score_box_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  smem));
-    attr_done = true;
-  }
+  once_per_device(attr_done, attr_mu, [&] {
+    BBS_CUDA(cudaFuncSetAttribute(score_box_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  });
   const uint64_t items = static_cast<uint64_t>(rot_end - rot_begin) * bp.n_tchunks;
   const unsigned grid_sz = static_cast<unsigned>(std::min<uint64_t>(std::max<uint64_t>(items, 1), 148ull * 2 * 64));
   score_box_kernel<<<grid_sz, kBoxThreads, smem, s>>>(map, grid, scan, bp, rot_begin, rot_end, only,
@@ -896,10 +964,11 @@ void launch_score_roots(const MapView& map, const GridView& grid, const ScanView
     launch_score_box_chunked(map, grid, scan, bp, 0, nrot, nullptr, scores, probes, s);
     return;
   }
-  static bool attr_done = false;
+  static std::atomic<uint64_t> attr_done{0};
+  static std::mutex attr_mu;
   const int hist_smem = kHistSlots * 12;
   const int col_stage_max = 64 << 10;
-  if (!attr_done) {
+  once_per_device(attr_done, attr_mu, [&] {
     BBS_CUDA(cudaFuncSetAttribute(root_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   hist_smem));
     BBS_CUDA(cudaFuncSetAttribute(root_col_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -914,8 +983,7 @@ void launch_score_roots(const MapView& map, const GridView& grid, const ScanView
     BBS_COLPAD_ATTR(1) BBS_COLPAD_ATTR(2) BBS_COLPAD_ATTR(3) BBS_COLPAD_ATTR(4) BBS_COLPAD_ATTR(5)
     BBS_COLPAD_ATTR(6) BBS_COLPAD_ATTR(7) BBS_COLPAD_ATTR(8)
 #undef BBS_COLPAD_ATTR
-    attr_done = true;
-  }
+  });
   const uint64_t col_bytes = static_cast<uint64_t>(L.dim[0]) * L.dim[1] * 4ull;
   const int stage = col_bytes <= static_cast<uint64_t>(col_stage_max) ? 1 : 0;
   const int col_smem = kEntTile * 16 + (stage ? static_cast<int>(col_bytes) : 0);

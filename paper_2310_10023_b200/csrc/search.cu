@@ -1085,6 +1085,33 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
                                   std::fabs(static_cast<double>(z0)), std::fabs(static_cast<double>(z1))});
     bp.tmax = tmax + 2.0;
   }
+  // dense histogram box of a rotated scan at a level's cell (root batch and
+  // the flush cache): |fx|, |fy| <= d_max / cell + 2; the rotated z of a
+  // point moves by at most sin(t)(|x| + |y|) + (1 - cos^2 t)|z| for
+  // roll/pitch within t (the third row of Rz Ry Rx is yaw-free).  A point
+  // outside the box makes that histogram fall back (never wrong).  eps bounds
+  // fast_floor's per-point eps for every in-box offset.
+  auto dense_box = [&](double cell, double tmax_l, int32_t* dr, int32_t* dzlo, int32_t* dnz, double* eps,
+                       double* eps1) {
+    *dr = 0;
+    const double t = std::fabs(cfg.roll_pitch_half_range) + 1e-6;
+    const double zabs = std::max(std::fabs(scan->z_min), std::fabs(scan->z_max));
+    const double dz = std::sin(t) * scan->l1xy_max + (1.0 - std::cos(t) * std::cos(t)) * zabs + 1e-6 * (1.0 + d_max);
+    const double r = std::floor(scan->d_max / cell) + 2.0;
+    const double zlo = std::floor((scan->z_min - dz) / cell) - 1.0;
+    const double zhi = std::floor((scan->z_max + dz) / cell) + 1.0;
+    const double cells = (2.0 * r + 1.0) * (2.0 * r + 1.0) * (zhi - zlo + 1.0);
+    if (cells <= static_cast<double>(kCacheDenseCells) && K < 65536 && t < 0.5 &&
+        std::getenv("BBS_DENSE_HIST") == nullptr) {
+      *dr = static_cast<int32_t>(r);
+      *dzlo = static_cast<int32_t>(zlo);
+      *dnz = static_cast<int32_t>(zhi - zlo + 1.0);
+      const double W = std::max({r, std::fabs(zlo), std::fabs(zhi + 1.0)}) + 1.0;
+      *eps = (W + tmax_l) * 0x1p-48;
+      *eps1 = 1.0 - *eps;
+    }
+  };
+  dense_box(m->view.level[L].cell, bp.tmax, &bp.dn_r, &bp.dn_zlo, &bp.dn_nz, &bp.dn_eps, &bp.dn_eps1);
   int32_t* root_scores = W.root_scores.get(static_cast<size_t>(std::max<int64_t>(total, 1)), s);
   unsigned long long* d_probes = W.probes.get(1, s);
   int* d_nsel = W.nsel.get(1, s);
@@ -1236,27 +1263,8 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
       if (n_rot <= (1ull << 20) && slots + n_rot <= (1ull << 23) && cache.tmax[l] < 0x1p28) {
         cache.base[l] = static_cast<uint32_t>(slots);
         slots += n_rot;
-        // dense histogram box: |fx|, |fy| <= d_max / cell + 2; the rotated z
-        // of a point moves by at most sin(t)(|x| + |y|) + (1 - cos^2 t)|z|
-        // for roll/pitch within t (third row of Rz Ry Rx is yaw-free).  A
-        // point outside the box makes that build fall back (never wrong).
-        const double cell = m->view.level[l].cell;
-        const double t = std::fabs(cfg.roll_pitch_half_range) + 1e-6;
-        const double zabs = std::max(std::fabs(scan->z_min), std::fabs(scan->z_max));
-        const double dz = std::sin(t) * scan->l1xy_max + (1.0 - std::cos(t) * std::cos(t)) * zabs + 1e-6 * (1.0 + d_max);
-        const double r = std::floor(scan->d_max / cell) + 2.0;
-        const double zlo = std::floor((scan->z_min - dz) / cell) - 1.0;
-        const double zhi = std::floor((scan->z_max + dz) / cell) + 1.0;
-        const double cells = (2.0 * r + 1.0) * (2.0 * r + 1.0) * (zhi - zlo + 1.0);
-        if (cells <= static_cast<double>(kCacheDenseCells) && K < 65536 && t < 0.5 &&
-            std::getenv("BBS_DENSE_HIST") == nullptr) {
-          cache.dn_r[l] = static_cast<int32_t>(r);
-          cache.dn_zlo[l] = static_cast<int32_t>(zlo);
-          cache.dn_nz[l] = static_cast<int32_t>(zhi - zlo + 1.0);
-          const double W = std::max({r, std::fabs(zlo), std::fabs(zhi + 1.0)}) + 1.0;
-          cache.dn_eps[l] = (W + cache.tmax[l]) * 0x1p-48;
-          cache.dn_eps1[l] = 1.0 - cache.dn_eps[l];
-        }
+        dense_box(m->view.level[l].cell, cache.tmax[l], &cache.dn_r[l], &cache.dn_zlo[l], &cache.dn_nz[l],
+                  &cache.dn_eps[l], &cache.dn_eps1[l]);
       }
     }
     cache.stg_level = -1;

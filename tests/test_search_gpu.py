@@ -246,3 +246,22 @@ def test_rotation_cache_is_transparent(B, golden_scenes, monkeypatch):
     for strat in ("BFS", "DFS"):
         assert out[("1", strat)] == out[("0", strat)], strat
     assert out[("1", "BFS")][6][0] > 0  # the search reached the uncached level 0
+
+
+def test_dense_histograms_are_transparent(B, golden_scenes, monkeypatch):
+    """Dense-box histograms (root batch and flush cache, constant eps per
+    level) and the shared-memory hash they replace give identical searches."""
+    m, s, _, sc = load_case(B, golden_scenes, "campus")
+    vm = B.MultiResVoxelMap.build(m, sc["r"], sc["max_level"])
+    ds = B.DeviceScan(vm, s)
+    out = {}
+    for flag in (None, "1"):
+        if flag is None:
+            monkeypatch.delenv("BBS_DENSE_HIST", raising=False)
+        else:
+            monkeypatch.setenv("BBS_DENSE_HIST", flag)
+        cfg = B.SearchConfig(min_resolution=sc["r"], max_level=sc["max_level"], collect_trace=True)
+        r = B.search_scan(vm, ds, cfg)
+        out[flag] = (r.best_score, r.best_pose.as_tuple(), r.stats.nodes_generated, r.stats.nodes_pruned,
+                     r.stats.batches_flushed, tuple(r.best_score_trace), r.root_probes)
+    assert out[None][:6] == out["1"][:6]
