@@ -844,6 +844,7 @@ struct Workspace {
   Buf<uint32_t> hist_amb;
   Buf<EpochState> st;
   EpochState* h_st = nullptr;
+  cudaStream_t side = nullptr;            // prebuild stream (forked per search)
   unsigned long long* h_small = nullptr;  // pinned: probes, n_root_surv
   std::vector<cudaEvent_t> ev;
   size_t ev_used = 0;
@@ -876,6 +877,7 @@ struct Workspace {
     if (h_st) cudaFreeHost(h_st);
     if (h_small) cudaFreeHost(h_small);
     for (auto e : ev) cudaEventDestroy(e);
+    if (side) cudaStreamDestroy(side);
   }
 };
 
@@ -1130,6 +1132,116 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
     launches += 3 * ((nrot + kRotBatch - 1) / kRotBatch);
   }
   BBS_CUDA(cudaEventRecord(ev_roots1, s));
+  cudaEvent_t ev_fork = W.next_event(), ev_prebuilt = W.next_event();
+  bool prebuild_pending = false;
+  // per-search (level, rotation) histogram cache for the flushes (epoch_cache.cu)
+  const bool cache_on = [] {
+    const char* v = std::getenv("BBS_ROT_CACHE");  // "0" disables (A/B timing, tests)
+    return !(v && v[0] == '0');
+  }();
+  RotCache cache{};
+  cache.stg_level = -1;
+  cache.pre_level = -1;
+  // a histogram build costs about one direct run; small scans (C1: K = 2000)
+  // rarely amortize it, large ones (C2/C3) reuse rotations across flushes
+  if (cache_on && K >= 4096) {
+    uint64_t slots = 0;
+    const double M = std::max({std::fabs(static_cast<double>(x0)), std::fabs(static_cast<double>(x1)),
+                               std::fabs(static_cast<double>(y0)), std::fabs(static_cast<double>(y1)),
+                               std::fabs(static_cast<double>(z0)), std::fabs(static_cast<double>(z1))});
+    for (int l = 0; l < kMaxLevels; ++l) {
+      cache.base[l] = 0xFFFFFFFFu;
+      cache.tmax[l] = 0.0;
+    }
+    for (int l = 0; l < L; ++l) {
+      const uint64_t n_rot = static_cast<uint64_t>(grid.axis(0, l).index_count()) *
+                             grid.axis(1, l).index_count() * grid.axis(2, l).index_count();
+      // nodes at level l have |index| <= (M + 1) * 2^(L - l) (children 2c + j)
+      cache.tmax[l] = (M + 1.0) * std::ldexp(1.0, L - l) + 2.0;
+      if (n_rot <= (1ull << 20) && slots + n_rot <= (1ull << 23) && cache.tmax[l] < 0x1p28) {
+        cache.base[l] = static_cast<uint32_t>(slots);
+        slots += n_rot;
+        dense_box(m->view.level[l].cell, cache.tmax[l], &cache.dn_r[l], &cache.dn_zlo[l], &cache.dn_nz[l],
+                  &cache.dn_eps[l], &cache.dn_eps1[l]);
+      }
+    }
+    cache.stg_level = -1;
+    {
+      // stage level L-1 (it carries almost all cached flush work): needs a
+      // dense box, a single z word per column with 8 bits of headroom, and a
+      // padded window that fits shared memory
+      const int l = L - 1;
+      const LevelView& LV = m->view.level[l];
+      if (l >= 0 && cache.base[l] != 0xFFFFFFFFu && cache.dn_r[l] > 0 && LV.layout == BBS_LAYOUT_BITMAP &&
+          LV.nwz == 1 && LV.dim[2] <= 24 && cache.dn_zlo[l] >= -128 && cache.dn_zlo[l] + cache.dn_nz[l] <= 128 &&
+          std::getenv("BBS_STAGE_PROBE") == nullptr) {
+        // child translations at level L-1 span [2 x0, 2 x1 + 1] (+1 for the cube)
+        const int64_t R = cache.dn_r[l];
+        const int64_t x_lo = 2ll * x0 - LV.box_min[0] - R, x_hi = 2ll * x1 + 2 - LV.box_min[0] + R + 1;
+        const int64_t y_lo = 2ll * y0 - LV.box_min[1] - R, y_hi = 2ll * y1 + 2 - LV.box_min[1] + R + 1;
+        const int64_t words = (x_hi - x_lo) * (y_hi - y_lo);
+        if (words > 0 && words * 4 <= kStageWindowMax) {
+          cache.stg_level = l;
+          cache.stg_sx0 = static_cast<int32_t>(x_lo);
+          cache.stg_sy0 = static_cast<int32_t>(y_lo);
+          cache.stg_pitch = static_cast<uint32_t>(x_hi - x_lo);
+          cache.stg_rows = static_cast<uint32_t>(y_hi - y_lo);
+        }
+      }
+    }
+    if (slots > 0) {
+      cache.enabled = 1;
+      cache.pool_cap = 64ull << 20;  // entries (16 B each)
+      cache.amb_cap = 8ull << 20;
+      cache.info = W.cache_info.get(slots, s);
+      cache.amb_off = W.cache_u32.get(slots + kCacheCtl, s);
+      cache.ctl = cache.amb_off + slots;
+      cache.pool = W.cache_pool.get(cache.pool_cap, s);
+      cache.amb_pool = W.cache_amb.get(cache.amb_cap, s);
+      // level L-1 is prebuilt in one launch when its rotation count is modest
+      const int pl = L - 1;
+      const uint64_t pre_rot = (pl >= 0 && cache.base[pl] != 0xFFFFFFFFu)
+                                   ? static_cast<uint64_t>(grid.axis(0, pl).index_count()) *
+                                         grid.axis(1, pl).index_count() * grid.axis(2, pl).index_count()
+                                   : 0;
+      const bool prebuild = pre_rot > 0 && pre_rot <= 16384 && [] {
+        const char* v = std::getenv("BBS_PREBUILD");  // "0" disables (A/B timing)
+        return !(v && v[0] == '0');
+      }();
+      const uint64_t mr = std::max<uint64_t>((pend_cap + 7) / 8, prebuild ? pre_rot : 0);
+      cache.builds = W.cache_builds.get(mr, s);
+      cache.builds_w = W.cache_builds_w.get(mr, s);
+      cache.fb_runs = W.cache_fb.get(mr, s);
+      if (cache.stg_level >= 0) {
+        uint32_t* win = W.stage_win.get(((static_cast<size_t>(cache.stg_pitch) * cache.stg_rows + 3) & ~size_t(3)), s);
+        build_stage_window(m->view, cache, win, s);
+        cache.stg_win = win;
+      }
+      BBS_CUDA(cudaMemsetAsync(cache.info, 0xFF, slots * sizeof(int4), s));  // all kCacheEmpty
+      BBS_CUDA(cudaMemsetAsync(cache.ctl, 0, kCacheCtl * sizeof(uint32_t), s));
+      if (prebuild) {
+        // fork: the histograms need only the scan, the map and the LUT, so
+        // they build on a side stream while this stream selects and sorts
+        // the root survivors (a host sync and small kernels: idle SMs)
+        cache.pre_level = pl;
+        if (!W.side) BBS_CUDA(cudaStreamCreateWithFlags(&W.side, cudaStreamNonBlocking));
+        cudaEvent_t e0 = W.next_event();
+        BBS_CUDA(cudaEventRecord(ev_fork, s));
+        BBS_CUDA(cudaStreamWaitEvent(W.side, ev_fork, 0));
+        BBS_CUDA(cudaEventRecord(e0, W.side));
+        launch_cache_prebuild(m->view, gv, sv, cache, pl, static_cast<uint32_t>(pre_rot), W.side);
+        BBS_CUDA(cudaEventRecord(ev_prebuilt, W.side));
+        prebuild_pending = true;
+        launches += 2;
+        if (std::getenv("BBS_DEBUG_CACHE")) {
+          BBS_CUDA(cudaEventSynchronize(ev_prebuilt));
+          std::fprintf(stderr, "[cache] prebuild level %d: %llu rotations in %.3f ms\n", pl,
+                       static_cast<unsigned long long>(pre_rot), elapsed(e0, ev_prebuilt));
+        }
+      }
+    }
+  }
+
   // exact mode: every rank gets every root score (unowned roots are -1)
   if (exact) xmax(root_scores, static_cast<size_t>(std::max<int64_t>(total, 0)));
   const uint64_t n_scored_roots = exact ? static_cast<uint64_t>(std::max<int64_t>(total, 0)) : n_own;
@@ -1236,106 +1348,9 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
   const uint64_t trace_cap = cfg.collect_trace ? std::max<uint64_t>(out->trace_capacity, 1) : 0;
   int32_t* d_trace = W.trace.get(std::max<uint64_t>(trace_cap, 1), s);
   const uint32_t ptiles = choose_ptiles((pend_cap + 7) / 8, static_cast<uint32_t>(K));
-  // per-search (level, rotation) histogram cache for the flushes (epoch_cache.cu)
-  const bool cache_on = [] {
-    const char* v = std::getenv("BBS_ROT_CACHE");  // "0" disables (A/B timing, tests)
-    return !(v && v[0] == '0');
-  }();
-  RotCache cache{};
-  cache.stg_level = -1;
-  cache.pre_level = -1;
-  // a histogram build costs about one direct run; small scans (C1: K = 2000)
-  // rarely amortize it, large ones (C2/C3) reuse rotations across flushes
-  if (cache_on && K >= 4096) {
-    uint64_t slots = 0;
-    const double M = std::max({std::fabs(static_cast<double>(x0)), std::fabs(static_cast<double>(x1)),
-                               std::fabs(static_cast<double>(y0)), std::fabs(static_cast<double>(y1)),
-                               std::fabs(static_cast<double>(z0)), std::fabs(static_cast<double>(z1))});
-    for (int l = 0; l < kMaxLevels; ++l) {
-      cache.base[l] = 0xFFFFFFFFu;
-      cache.tmax[l] = 0.0;
-    }
-    for (int l = 0; l < L; ++l) {
-      const uint64_t n_rot = static_cast<uint64_t>(grid.axis(0, l).index_count()) *
-                             grid.axis(1, l).index_count() * grid.axis(2, l).index_count();
-      // nodes at level l have |index| <= (M + 1) * 2^(L - l) (children 2c + j)
-      cache.tmax[l] = (M + 1.0) * std::ldexp(1.0, L - l) + 2.0;
-      if (n_rot <= (1ull << 20) && slots + n_rot <= (1ull << 23) && cache.tmax[l] < 0x1p28) {
-        cache.base[l] = static_cast<uint32_t>(slots);
-        slots += n_rot;
-        dense_box(m->view.level[l].cell, cache.tmax[l], &cache.dn_r[l], &cache.dn_zlo[l], &cache.dn_nz[l],
-                  &cache.dn_eps[l], &cache.dn_eps1[l]);
-      }
-    }
-    cache.stg_level = -1;
-    {
-      // stage level L-1 (it carries almost all cached flush work): needs a
-      // dense box, a single z word per column with 8 bits of headroom, and a
-      // padded window that fits shared memory
-      const int l = L - 1;
-      const LevelView& LV = m->view.level[l];
-      if (l >= 0 && cache.base[l] != 0xFFFFFFFFu && cache.dn_r[l] > 0 && LV.layout == BBS_LAYOUT_BITMAP &&
-          LV.nwz == 1 && LV.dim[2] <= 24 && cache.dn_zlo[l] >= -128 && cache.dn_zlo[l] + cache.dn_nz[l] <= 128 &&
-          std::getenv("BBS_STAGE_PROBE") == nullptr) {
-        // child translations at level L-1 span [2 x0, 2 x1 + 1] (+1 for the cube)
-        const int64_t R = cache.dn_r[l];
-        const int64_t x_lo = 2ll * x0 - LV.box_min[0] - R, x_hi = 2ll * x1 + 2 - LV.box_min[0] + R + 1;
-        const int64_t y_lo = 2ll * y0 - LV.box_min[1] - R, y_hi = 2ll * y1 + 2 - LV.box_min[1] + R + 1;
-        const int64_t words = (x_hi - x_lo) * (y_hi - y_lo);
-        if (words > 0 && words * 4 <= kStageWindowMax) {
-          cache.stg_level = l;
-          cache.stg_sx0 = static_cast<int32_t>(x_lo);
-          cache.stg_sy0 = static_cast<int32_t>(y_lo);
-          cache.stg_pitch = static_cast<uint32_t>(x_hi - x_lo);
-          cache.stg_rows = static_cast<uint32_t>(y_hi - y_lo);
-        }
-      }
-    }
-    if (slots > 0) {
-      cache.enabled = 1;
-      cache.pool_cap = 64ull << 20;  // entries (16 B each)
-      cache.amb_cap = 8ull << 20;
-      cache.info = W.cache_info.get(slots, s);
-      cache.amb_off = W.cache_u32.get(slots + kCacheCtl, s);
-      cache.ctl = cache.amb_off + slots;
-      cache.pool = W.cache_pool.get(cache.pool_cap, s);
-      cache.amb_pool = W.cache_amb.get(cache.amb_cap, s);
-      // level L-1 is prebuilt in one launch when its rotation count is modest
-      const int pl = L - 1;
-      const uint64_t pre_rot = (pl >= 0 && cache.base[pl] != 0xFFFFFFFFu)
-                                   ? static_cast<uint64_t>(grid.axis(0, pl).index_count()) *
-                                         grid.axis(1, pl).index_count() * grid.axis(2, pl).index_count()
-                                   : 0;
-      const bool prebuild = pre_rot > 0 && pre_rot <= 16384 && [] {
-        const char* v = std::getenv("BBS_PREBUILD");  // "0" disables (A/B timing)
-        return !(v && v[0] == '0');
-      }();
-      const uint64_t mr = std::max<uint64_t>((pend_cap + 7) / 8, prebuild ? pre_rot : 0);
-      cache.builds = W.cache_builds.get(mr, s);
-      cache.builds_w = W.cache_builds_w.get(mr, s);
-      cache.fb_runs = W.cache_fb.get(mr, s);
-      if (cache.stg_level >= 0) {
-        uint32_t* win = W.stage_win.get(((static_cast<size_t>(cache.stg_pitch) * cache.stg_rows + 3) & ~size_t(3)), s);
-        build_stage_window(m->view, cache, win, s);
-        cache.stg_win = win;
-      }
-      BBS_CUDA(cudaMemsetAsync(cache.info, 0xFF, slots * sizeof(int4), s));  // all kCacheEmpty
-      BBS_CUDA(cudaMemsetAsync(cache.ctl, 0, kCacheCtl * sizeof(uint32_t), s));
-      if (prebuild) {
-        cache.pre_level = pl;
-        cudaEvent_t e0 = W.next_event(), e1 = W.next_event();
-        BBS_CUDA(cudaEventRecord(e0, s));
-        launch_cache_prebuild(m->view, gv, sv, cache, pl, static_cast<uint32_t>(pre_rot), s);
-        BBS_CUDA(cudaEventRecord(e1, s));
-        launches += 2;
-        if (std::getenv("BBS_DEBUG_CACHE")) {
-          BBS_CUDA(cudaEventSynchronize(e1));
-          std::fprintf(stderr, "[cache] prebuild level %d: %llu rotations in %.3f ms\n", pl,
-                       static_cast<unsigned long long>(pre_rot), elapsed(e0, e1));
-        }
-      }
-    }
-  }
+  // the level L-1 prebuild ran on the side stream during the root survivor
+  // selection and queue build
+  if (prebuild_pending) BBS_CUDA(cudaStreamWaitEvent(s, ev_prebuilt, 0));
 
   // per-epoch-slot events of one batch; timings are harvested after each batch
   std::vector<cudaEvent_t> ev_pass(E), ev_s0(E), ev_s1(E);
