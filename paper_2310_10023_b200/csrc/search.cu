@@ -1191,7 +1191,7 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
     }
     if (slots > 0) {
       cache.enabled = 1;
-      cache.pool_cap = 64ull << 20;  // entries (16 B each)
+      cache.pool_cap = 16ull << 20;  // entries (16 B each): C3's level-5 histograms use ~1/8 of it
       cache.amb_cap = 8ull << 20;
       cache.info = W.cache_info.get(slots, s);
       cache.amb_off = W.cache_u32.get(slots + kCacheCtl, s);
