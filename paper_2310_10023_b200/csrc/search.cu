@@ -768,6 +768,16 @@ __global__ void soa_kernel(const double* __restrict__ aos, uint64_t k, double* _
     soa[2 * k + i] = aos[3 * i + 2];
   }
 }
+// Survivors of the root batch (score >= threshold), counted.
+__global__ void count_survivors_kernel(const int32_t* __restrict__ scores, uint64_t n, int32_t threshold,
+                                       unsigned long long* __restrict__ out) {
+  unsigned long long c = 0;
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x)
+    c += scores[i] >= threshold ? 1u : 0u;
+  c = cub::BlockReduce<unsigned long long, 256>().Sum(c);
+  if (threadIdx.x == 0 && c) atomicAdd(out, c);
+}
+
 // Root ownership predicate over initial_nodes() order: the root scores buffer
 // is pre-filled with -1, so only owned roots can reach the threshold (>= 0).
 struct RootSurvives {
@@ -1115,7 +1125,7 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
   };
   dense_box(m->view.level[L].cell, bp.tmax, &bp.dn_r, &bp.dn_zlo, &bp.dn_nz, &bp.dn_eps, &bp.dn_eps1);
   int32_t* root_scores = W.root_scores.get(static_cast<size_t>(std::max<int64_t>(total, 1)), s);
-  unsigned long long* d_probes = W.probes.get(1, s);
+  unsigned long long* d_probes = W.probes.get(2, s);  // [0] root probes, [1] survivor count
   int* d_nsel = W.nsel.get(1, s);
   RootHist hist{};
   hist.entries = W.hist_ent.get(static_cast<size_t>(kRotBatch) * kHistCap, s);
@@ -1124,7 +1134,9 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
   hist.n_ent = hn;
   hist.n_amb = hn + kRotBatch;
   hist.overflow = hn + 2 * kRotBatch;  // kRotBatch flags + 1 overflow counter
-  BBS_CUDA(cudaMemsetAsync(root_scores, 0xFF, static_cast<size_t>(std::max<int64_t>(total, 1)) * 4, s));
+  // unowned roots must read -1 (below any threshold); a single rank scores
+  // and writes every root
+  if (world > 1) BBS_CUDA(cudaMemsetAsync(root_scores, 0xFF, static_cast<size_t>(std::max<int64_t>(total, 1)) * 4, s));
   BBS_CUDA(cudaMemsetAsync(d_probes, 0, sizeof(unsigned long long), s));
   BBS_CUDA(cudaEventRecord(ev_roots0, s));
   if (total > 0) {
@@ -1247,7 +1259,22 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
   const uint64_t n_scored_roots = exact ? static_cast<uint64_t>(std::max<int64_t>(total, 0)) : n_own;
 
   // survivors >= threshold among own roots, in initial_nodes order
-  unsigned long long* surv_idx = W.surv_idx.get(static_cast<size_t>(std::max<uint64_t>(n_scored_roots, 1)), s);
+  // survivor index buffer: the root count bounds it; huge root sets (TransOnly
+  // searches: billions of roots) count the survivors first instead
+  uint64_t surv_cap = std::max<uint64_t>(n_scored_roots, 1);
+  if (total > 0 && n_scored_roots > (64ull << 20)) {
+    unsigned long long* d_cnt = d_probes + 1;
+    BBS_CUDA(cudaMemsetAsync(d_cnt, 0, sizeof(unsigned long long), s));
+    count_survivors_kernel<<<grid1(static_cast<uint64_t>(total)), 256, 0, s>>>(root_scores, static_cast<uint64_t>(total),
+                                                                               threshold, d_cnt);
+    BBS_CUDA(cudaGetLastError());
+    BBS_CUDA(cudaMemcpyAsync(&W.h_small[2], d_cnt, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+    BBS_CUDA(cudaStreamSynchronize(s));
+    d2h += sizeof(unsigned long long);
+    surv_cap = std::max<uint64_t>(W.h_small[2], 1);
+    ++launches;
+  }
+  unsigned long long* surv_idx = W.surv_idx.get(static_cast<size_t>(surv_cap), s);
   int n_root_surv = 0;
   if (total > 0) {
     cub::CountingInputIterator<unsigned long long> cnt(0);
