@@ -61,7 +61,8 @@ void level_score_transform(bbs_map* m, int level, const double* R, const double*
                            const double* scan, uint64_t k, int32_t* score);
 
 // Scans (search.cu).
-bbs_scan* upload_scan(bbs_map* m, const double* xyz, uint64_t k);
+// sync = false: the caller uses the scan on the map's stream only.
+bbs_scan* upload_scan(bbs_map* m, const double* xyz, uint64_t k, bool sync = true);
 
 struct DeviceGuard {
   int prev = 0;

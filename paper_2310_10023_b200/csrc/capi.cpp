@@ -428,7 +428,7 @@ int bbs_search(bbs_map_t map, const double* scan_xyz, uint64_t k, const bbs_sear
   return guard([&] {
     REQUIRE(map && cfg && result && (scan_xyz || k == 0), "null argument");
     if (k == 0) throw bbs::Error(BBS_ERR_DEGENERATE_SCAN, "search: empty scan");
-    std::unique_ptr<bbs_scan> sc(bbs::upload_scan(map, scan_xyz, k));
+    std::unique_ptr<bbs_scan> sc(bbs::upload_scan(map, scan_xyz, k, false));  // same stream as the search
     bbs::run_search(map, sc.get(), *cfg, nullptr, result);
     result->h2d_bytes += 3 * k * sizeof(double);
   });
@@ -445,7 +445,7 @@ int bbs_localize_scan(bbs_map_t map, const double* raw_xyz, uint64_t n, const bb
     const double prep_ms =
         std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     const uint64_t k = prep.xyz.size() / 3;
-    std::unique_ptr<bbs_scan> sc(bbs::upload_scan(map, prep.xyz.data(), k));
+    std::unique_ptr<bbs_scan> sc(bbs::upload_scan(map, prep.xyz.data(), k, false));
     bbs::run_search(map, sc.get(), *cfg, nullptr, result);
     result->stats.set_source_ms = prep_ms;
   });

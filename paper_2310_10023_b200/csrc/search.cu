@@ -932,7 +932,7 @@ void set_pool_retention(int device) {
   }
 }
 
-bbs_scan* upload_scan(bbs_map* m, const double* xyz, uint64_t k) {
+bbs_scan* upload_scan(bbs_map* m, const double* xyz, uint64_t k, bool sync) {
   DeviceGuard g(m->device);
   auto* sc = new bbs_scan();
   sc->map = m;
@@ -954,7 +954,7 @@ bbs_scan* upload_scan(bbs_map* m, const double* xyz, uint64_t k) {
     BBS_CUDA(cudaGetLastError());
     BBS_CUDA(cudaFreeAsync(aos, s));
   }
-  BBS_CUDA(cudaStreamSynchronize(s));
+  if (sync) BBS_CUDA(cudaStreamSynchronize(s));  // callers on other streams see a complete scan
   return sc;
 }
 
@@ -1748,7 +1748,7 @@ bbs_scan::~bbs_scan() {
     int prev = 0;
     cudaGetDevice(&prev);
     cudaSetDevice(map->device);
-    cudaFree(soa);
+    cudaFreeAsync(soa, map->stream);  // stream-ordered (searches using it have returned)
     cudaSetDevice(prev);
   }
 }
