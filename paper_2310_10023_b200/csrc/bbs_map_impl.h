@@ -45,7 +45,6 @@ struct bbs_scan {
   double d_max = 0.0;          // max_range of the scan (host libm)
   double z_min = 0.0, z_max = 0.0, l1xy_max = 0.0;  // bounds for the dense histogram boxes
   double* soa = nullptr;       // device: x[k], y[k], z[k]
-  std::vector<double> host;    // the scan as given (AoS)
   ~bbs_scan();
 };
 

@@ -937,7 +937,6 @@ bbs_scan* upload_scan(bbs_map* m, const double* xyz, uint64_t k, bool sync) {
   auto* sc = new bbs_scan();
   sc->map = m;
   sc->k = k;
-  sc->host.assign(xyz, xyz + 3 * k);
   sc->d_max = k ? host_max_range(xyz, k) : 0.0;
   for (uint64_t i = 0; i < k; ++i) {
     const double x = xyz[3 * i], y = xyz[3 * i + 1], z = xyz[3 * i + 2];
