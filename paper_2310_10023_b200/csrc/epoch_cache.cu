@@ -551,7 +551,8 @@ void launch_cache_prebuild(const MapView& map, const GridView& grid, const ScanV
 
 void launch_epoch_score(const MapView& map, const GridView& grid, const ScanView& scan,
                         const bbs_node* pending, const uint32_t* d_n, uint32_t n_max,
-                        uint32_t n_ptiles, int32_t* scores, const RotCache& cache, cudaStream_t s) {
+                        uint32_t n_ptiles, int32_t* scores, const RotCache& cache, cudaStream_t s,
+                        bool builds) {
   if (!cache.enabled) {
     launch_score_cube8(map, grid, scan, pending, d_n, n_max, n_ptiles, scores, nullptr, s);
     return;
@@ -567,9 +568,11 @@ void launch_epoch_score(const MapView& map, const GridView& grid, const ScanView
   const uint32_t max_runs = (n_max + 7) / 8;
   // the epoch's branch kernel already claimed the slots (cache_claim_run)
   // after its frontier reset ctl[2..3]
-  launch_pdl(cache_build_kernel, std::min<uint32_t>(std::max<uint32_t>(max_runs, 1), 148 * 2), kBuildThreads,
-             build_smem, s, cache, map, grid, scan);
-  BBS_CUDA(cudaGetLastError());
+  if (builds) {  // false once no level can claim a build any more (host-known)
+    launch_pdl(cache_build_kernel, std::min<uint32_t>(std::max<uint32_t>(max_runs, 1), 148 * 2), kBuildThreads,
+               build_smem, s, cache, map, grid, scan);
+    BBS_CUDA(cudaGetLastError());
+  }
   const uint32_t chunks = (scan.k + kProbeChunk - 1) / kProbeChunk;
   const uint64_t warp_items = static_cast<uint64_t>(max_runs) * chunks;
   const uint64_t wpc = kProbeThreads / 32;  // warps per CTA

@@ -162,7 +162,8 @@ void launch_score_cube8(const MapView& map, const GridView& grid, const ScanView
 // scores must be zeroed first.
 void launch_epoch_score(const MapView& map, const GridView& grid, const ScanView& scan,
                         const bbs_node* pending, const uint32_t* d_n, uint32_t n_max,
-                        uint32_t n_ptiles, int32_t* scores, const RotCache& cache, cudaStream_t s);
+                        uint32_t n_ptiles, int32_t* scores, const RotCache& cache, cudaStream_t s,
+                        bool builds = true);
 
 // Build the histograms of every rotation of `level` (n_rot slots from
 // cache.base[level]) in one launch; cache.builds must hold n_rot entries.

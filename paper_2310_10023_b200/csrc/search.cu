@@ -58,6 +58,7 @@ struct EpochState {
   uint32_t n_keep;         // queue remainder kept after the incumbent trim
   uint32_t surv_ticket;    // survivors tile tickets (reset by the frontier)
   uint32_t merge_done;     // merge CTAs finished (the last one finalizes the epoch)
+  uint32_t cache_raw;      // levels whose histogram builds gave up (flush cache, per frontier pass)
   uint32_t n_own;          // batch-split exact mode: children of this rank's runs
   int32_t any_active;      // sharded (device exchange): any rank still active
   unsigned long long level_evals[kMaxLevels];  // flush evaluations per level
@@ -275,6 +276,9 @@ __global__ void __launch_bounds__(kFT) frontier_kernel(EpochState* st, Queue q, 
   if (tid == 0 && cache_ctl) {
     cache_ctl[2] = 0;  // builds claimed this flush
     cache_ctl[3] = 0;  // runs listed for the cube kernel
+    uint32_t raw = 0;
+    for (int l = 0; l < kMaxLevels; ++l) raw |= cache_ctl[4 + l] ? 1u << l : 0u;
+    st->cache_raw = raw;  // lets the host stop launching empty build kernels
   }
   if (tid == 0) {
     st->surv_ticket = 0;
@@ -1407,6 +1411,13 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
   double dbg_sum[6] = {0, 0, 0, 0, 0, 0};
   uint64_t dbg_n = 0;
   cudaEvent_t dbg_prev = ev_loop;
+  // cached levels that can still claim a build (the prebuilt level cannot);
+  // once the host sees all of them given up, the build launch is dropped
+  uint32_t claimable = 0;
+  if (cache.enabled)
+    for (int l = 0; l < kMaxLevels; ++l)
+      if (cache.base[l] != 0xFFFFFFFFu && l != cache.pre_level) claimable |= 1u << l;
+  bool builds_live = claimable != 0;
   // one flush epoch (frontier -> branch -> score -> survivors -> sort -> merge)
   auto enqueue_epoch = [&](int e) {
     launch_pdl(frontier_kernel, 1, kFT, 0, s, d_st, q, gv, cfg.batch_size, exp_parent, exp_off, d_trace,
@@ -1419,7 +1430,7 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
     record(ev_s0[e]);
     if (exact) {
       launch_epoch_score(m->view, gv, sv, split.pending_own, d_nchild, static_cast<uint32_t>(pend_cap), ptiles,
-                         split.pscores_own, cache, s);
+                         split.pscores_own, cache, s, builds_live);
       record(ev_s1[e]);
       launch_pdl(scatter_own_kernel, grid1(pend_cap), 256, 0, s, d_st, split, pscores);
       BBS_CUDA(cudaGetLastError());
@@ -1427,7 +1438,7 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
       xmax(pscores, pend_cap);  // every rank: every score of the flush
     } else {
       launch_epoch_score(m->view, gv, sv, pending, d_nchild, static_cast<uint32_t>(pend_cap), ptiles,
-                         pscores, cache, s);
+                         pscores, cache, s, builds_live);
       record(ev_s1[e]);
     }
     launch_pdl(survivors_kernel, surv_grid, kST, 0, s, d_st, q, strategy, pending, pscores, s_key,
@@ -1456,6 +1467,7 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
   cudaGraphExec_t batch_exec = nullptr;
   uint64_t batch_qcap = 0;
   const bbs_node* batch_pool = nullptr;
+  bool batch_builds = true;
   struct ExecGuard {
     cudaGraphExec_t* e;
     ~ExecGuard() {
@@ -1516,7 +1528,7 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
     const int n_ep = (self_active || roots_dev_x) ? E : 1;
     // graphs pay off for long searches (capture + instantiate ~0.2 ms)
     if (n_ep == E && E > 1 && pass_ms.size() >= graph_after && !dbg_phases) {
-      if (!batch_exec || batch_qcap != qcap || batch_pool != q.pool) {
+      if (!batch_exec || batch_qcap != qcap || batch_pool != q.pool || batch_builds != builds_live) {
         if (batch_exec) BBS_CUDA(cudaGraphExecDestroy(batch_exec));
         batch_exec = nullptr;
         cudaGraph_t graph;
@@ -1531,6 +1543,7 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
         BBS_CUDA(cudaGraphDestroy(graph));
         batch_qcap = qcap;
         batch_pool = q.pool;
+        batch_builds = builds_live;
       }
       BBS_CUDA(cudaGraphLaunch(batch_exec, s));
       launches += 6ull * E;
@@ -1564,6 +1577,7 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
     }
     hs = *W.h_st;
     self_active = hs.active != 0;
+    builds_live = (claimable & ~hs.cache_raw) != 0;  // raw flags only ever get set
     if (roots_host_x)
       exchange();
     else
