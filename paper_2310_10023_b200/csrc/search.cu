@@ -1159,7 +1159,11 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
   cache.pre_level = -1;
   // a histogram build costs about one direct run; small scans (C1: K = 2000)
   // rarely amortize it, large ones (C2/C3) reuse rotations across flushes
-  if (cache_on && K >= 4096) {
+  const uint64_t cache_min_k = [] {
+    const char* v = std::getenv("BBS_CACHE_MIN_K");  // A/B timing
+    return v ? static_cast<uint64_t>(std::atoll(v)) : uint64_t(4096);
+  }();
+  if (cache_on && K >= cache_min_k) {
     uint64_t slots = 0;
     const double M = std::max({std::fabs(static_cast<double>(x0)), std::fabs(static_cast<double>(x1)),
                                std::fabs(static_cast<double>(y0)), std::fabs(static_cast<double>(y1)),
