@@ -424,9 +424,15 @@ def run_b200_arm(args, cfgd):
             out = C.c_double()
             if B.lib.bbs_gather_bench(local, nbytes, C.byref(out)) == 0:
                 gather[label] = round(out.value, 1)
+    traffic = profile_traffic(args.config, group)
+    launch_ms = ms / launches_per_step
+    dram_gbs = (traffic / (launch_ms * 1e-3) / 1e9) if traffic else None
     roofline = {
         "bound": "hbm", "kernel": kern, "achieved": achieved, "peak": peak, "unit": "GB/s",
-        "frac": achieved / peak, "traffic": profile_traffic(args.config, group),
+        "frac": achieved / peak, "traffic": traffic,
+        # what the kernels actually pull from DRAM per second (ncu bytes per
+        # launch / in-run launch time): the tables live in L2 / shared memory
+        "dram_gbs": dram_gbs, "dram_frac": (dram_gbs / peak) if dram_gbs else None,
         "traffic_source": "profiles/ncu_traffic.json: dram__bytes_read.sum + dram__bytes_write.sum "
                           "per launch of the group, ncu launch list (scripts/traffic.py)",
         "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
