@@ -31,6 +31,7 @@ struct BoxParams {
   double tmax;                // max |translation index| in the box (fast-path guard)
   // dense histogram box of the root level (dn_r = 0: hash), see RotCache
   int32_t dn_r, dn_zlo, dn_nz;
+  int32_t threshold;          // survivor score (search.hpp:97-100): roots below it only count as pruned
   double dn_eps, dn_eps1;
 };
 
@@ -61,6 +62,7 @@ struct RootHist {
   int32_t* n_ent;     // [kRotBatch]
   int32_t* n_amb;     // [kRotBatch]
   int32_t* overflow;  // [kRotBatch] 1: rotation falls back to the chunked kernel
+  int32_t* total;     // [kRotBatch] sum of the emitted entries' counts
 };
 
 // Owned x-slabs of rotation `rot`: slab ix_rel is owned iff

@@ -449,6 +449,16 @@ __device__ __forceinline__ uint32_t hist_slot(unsigned long long key) {
   return static_cast<uint32_t>((key * 0x9E3779B97F4A7C15ull) >> 51);  // 13 bits
 }
 
+// Entries are emitted heaviest first by count bucket (2 buckets: counts >= 2
+// first; more buckets cost emission passes and did not pay off on C2/C3).
+#ifndef BBS_ROOT_BUCKETS
+#define BBS_ROOT_BUCKETS 2
+#endif
+constexpr int kRootCountBuckets = BBS_ROOT_BUCKETS;
+__device__ __forceinline__ int count_bucket(uint32_t v) {
+  return kRootCountBuckets == 1 ? 0 : min(kRootCountBuckets - 1, 31 - __clz(max(v, 1u)));
+}
+
 // One histogram entry (f, cnt) of root_hist_kernel, appended warp-cooperatively
 // (every lane calls; has = false for lanes without an entry).  Staged mode
 // (root_colpad_kernel): (padded column offset << 8 | z shift + 8) words in
@@ -457,7 +467,7 @@ __device__ __forceinline__ uint32_t hist_slot(unsigned long long key) {
 // (fx, fy, fz, count).
 __device__ __forceinline__ void root_emit(bool has, int32_t fx, int32_t fy, int32_t fz, int32_t cnt,
                                           const BoxParams& bp, const RootStage& st, int4* ent4,
-                                          int* s_nent, int* s_badpad) {
+                                          int* s_nent, int* s_badpad, int* s_total) {
   const int lane = threadIdx.x & 31;
   int parts = has ? 1 : 0;
   int32_t sh = 0;
@@ -473,8 +483,10 @@ __device__ __forceinline__ void root_emit(bool has, int32_t fx, int32_t fy, int3
     if (lane >= d) incl += v;
   }
   const int wtot = __shfl_sync(0xffffffffu, incl, 31);
+  const int wcnt = __reduce_add_sync(0xffffffffu, parts ? cnt : 0);  // counts the entries carry
   int at = 0;
   if (lane == 0 && wtot) at = atomicAdd(s_nent, wtot);
+  if (lane == 0 && wcnt) atomicAdd(s_total, wcnt);
   at = __shfl_sync(0xffffffffu, at, 0) + incl - parts;
   if (!parts) return;
   if (st.enabled) {
@@ -501,7 +513,7 @@ __global__ void __launch_bounds__(512) root_hist_kernel(GridView grid, ScanView 
   unsigned long long* s_key = reinterpret_cast<unsigned long long*>(smem);  // 64 KB
   int32_t* s_cnt = reinterpret_cast<int32_t*>(s_key + kHistSlots);          // 32 KB
   uint32_t* s_w = reinterpret_cast<uint32_t*>(smem);  // dense box: 16-bit counters (overlays the hash)
-  __shared__ int s_distinct, s_namb, s_nent, s_skip, s_badpad;
+  __shared__ int s_distinct, s_namb, s_nent, s_skip, s_badpad, s_total;
   const uint32_t nrot = bp.nr * bp.np * bp.nw;
   const int lane = threadIdx.x & 31;
   // dense box (coarse root levels): direct-mapped counters, no probing
@@ -533,6 +545,7 @@ __global__ void __launch_bounds__(512) root_hist_kernel(GridView grid, ScanView 
       s_nent = 0;
       s_skip = 0;
       s_badpad = 0;
+      s_total = 0;
     }
     __syncthreads();
     const uint32_t ir = rot / (bp.np * bp.nw), ip = (rot / bp.nw) % bp.np, iw = rot % bp.nw;
@@ -616,33 +629,38 @@ __global__ void __launch_bounds__(512) root_hist_kernel(GridView grid, ScanView 
     if (!over) {
       int4* ent4 = h.entries + static_cast<uint64_t>(slot) * kHistCap;
       if (dense) {
-        // each thread walks a contiguous cell range; the warp emits in lockstep
+        // each thread walks a contiguous cell range; the warp emits in
+        // lockstep, heaviest counts first (log2 buckets) so the column
+        // kernel's survivor bound tightens early
         const int dper = (ncells + static_cast<int>(blockDim.x) - 1) / static_cast<int>(blockDim.x);
         const int dc0 = min(ncells, static_cast<int>(threadIdx.x) * dper), dc1 = min(ncells, dc0 + dper);
-        int cx = dc0 % dxy, cy = dc0 / dxy % dxy, cz = dc0 / (dxy * dxy);
-        for (int step = 0; step < dper; ++step) {
-          const int i = dc0 + step;
-          const uint32_t v = i < dc1 ? (s_w[i >> 1] >> ((i & 1) << 4)) & 0xFFFFu : 0u;
-          root_emit(v != 0u, cx - dr, cy - dr, cz + dzlo, static_cast<int32_t>(v), bp, st, ent4, &s_nent,
-                    &s_badpad);
-          if (++cx == dxy) {
-            cx = 0;
-            if (++cy == dxy) {
-              cy = 0;
-              ++cz;
+        for (int bk = kRootCountBuckets - 1; bk >= 0; --bk) {
+          int cx = dc0 % dxy, cy = dc0 / dxy % dxy, cz = dc0 / (dxy * dxy);
+          for (int step = 0; step < dper; ++step) {
+            const int i = dc0 + step;
+            const uint32_t v = i < dc1 ? (s_w[i >> 1] >> ((i & 1) << 4)) & 0xFFFFu : 0u;
+            root_emit(v != 0u && count_bucket(v) == bk, cx - dr, cy - dr, cz + dzlo, static_cast<int32_t>(v), bp,
+                      st, ent4, &s_nent, &s_badpad, &s_total);
+            if (++cx == dxy) {
+              cx = 0;
+              if (++cy == dxy) {
+                cy = 0;
+                ++cz;
+              }
             }
           }
         }
       } else {
-        for (int i0 = 0; i0 < kHistSlots; i0 += blockDim.x) {
-          const int i = i0 + threadIdx.x;
-          const unsigned long long key = s_key[i];
-          const bool has = key != kSlotEmpty;
-          root_emit(has, has ? static_cast<int32_t>((key >> 42) & 0x1FFFFF) - (1 << 20) : 0,
-                    has ? static_cast<int32_t>((key >> 21) & 0x1FFFFF) - (1 << 20) : 0,
-                    has ? static_cast<int32_t>(key & 0x1FFFFF) - (1 << 20) : 0, has ? s_cnt[i] : 0, bp, st,
-                    ent4, &s_nent, &s_badpad);
-        }
+        for (int bk = kRootCountBuckets - 1; bk >= 0; --bk)
+          for (int i0 = 0; i0 < kHistSlots; i0 += blockDim.x) {
+            const int i = i0 + threadIdx.x;
+            const unsigned long long key = s_key[i];
+            const bool has = key != kSlotEmpty && count_bucket(static_cast<uint32_t>(s_cnt[i])) == bk;
+            root_emit(has, has ? static_cast<int32_t>((key >> 42) & 0x1FFFFF) - (1 << 20) : 0,
+                      has ? static_cast<int32_t>((key >> 21) & 0x1FFFFF) - (1 << 20) : 0,
+                      has ? static_cast<int32_t>(key & 0x1FFFFF) - (1 << 20) : 0, has ? s_cnt[i] : 0, bp, st,
+                      ent4, &s_nent, &s_badpad, &s_total);
+          }
       }
     }
     __syncthreads();
@@ -660,6 +678,7 @@ __global__ void __launch_bounds__(512) root_hist_kernel(GridView grid, ScanView 
     if (threadIdx.x == 0) {
       h.n_ent[slot] = over ? 0 : s_nent;
       h.n_amb[slot] = over ? 0 : s_namb;
+      h.total[slot] = over ? 0 : s_total;
       h.overflow[slot] = over ? 1 : 0;
       if (over) atomicAdd(n_overflow, 1);
     }
@@ -812,7 +831,15 @@ __global__ void __launch_bounds__(256) root_colpad_kernel(GridView grid, ScanVie
 #pragma unroll
     for (int j = 0; j < NZ; ++j) acc[j] = 0;
     const int n_grp = (h.n_ent[slot] + 3) >> 2;
+    const int n_amb = h.n_amb[slot];
     const int4* __restrict__ grp = h.entries + static_cast<uint64_t>(slot) * kHistCap;
+    // Survivor bound: a root's score can still grow by at most the counts of
+    // the entries not yet probed plus its ambiguous points.  Once even the
+    // best of this column's z-translations cannot reach the threshold, its
+    // exact value is unobservable (search.hpp:117-123 only counts the root
+    // as pruned) and the column stops early; entries come heaviest first.
+    int rem = h.total[slot] + n_amb;
+    bool done = !valid;
     for (int t0 = 0; t0 < n_grp; t0 += kGrpTile) {
       const int tn = min(kGrpTile, n_grp - t0);
       __syncthreads();
@@ -822,9 +849,19 @@ __global__ void __launch_bounds__(256) root_colpad_kernel(GridView grid, ScanVie
       }
       __syncthreads();
 #pragma unroll 2
-      for (int g = 0; g < tn; ++g) {
+      for (int g = 0; g < tn && !done; ++g) {
+        if ((g & 7) == 0 && g) {
+          uint32_t best = 0;
+#pragma unroll
+          for (int j = 0; j < NZ; ++j) best = max(best, acc[j] >> j);
+          if (static_cast<int>(best) + rem < bp.threshold) {
+            done = true;
+            break;
+          }
+        }
         const int4 o = s_go[g];
         const uint32_t w4 = s_gw[g];
+        rem -= static_cast<int>(__dp4a(w4, 0x01010101u, 0u));  // this group's counts
         // shift amounts ride in the low 5 bits (wrap funnel shift)
         const uint32_t b0 = __funnelshift_r(s_col[base + (o.x >> 8)], 0u, static_cast<uint32_t>(o.x));
         const uint32_t b1 = __funnelshift_r(s_col[base + (o.y >> 8)], 0u, static_cast<uint32_t>(o.y));
@@ -838,8 +875,7 @@ __global__ void __launch_bounds__(256) root_colpad_kernel(GridView grid, ScanVie
     int res[NZ];
 #pragma unroll
     for (int j = 0; j < NZ; ++j) res[j] = static_cast<int>(acc[j] >> j);
-    const int n_amb = h.n_amb[slot];
-    if (valid && n_amb) {
+    if (valid && n_amb && !done) {
       const uint32_t ir = rot / (bp.np * bp.nw), ip = (rot / bp.nw) % bp.np, iw = rot % bp.nw;
       double R[9];
       rotation_of(grid, bp.level, static_cast<int>(ir), static_cast<int>(ip), static_cast<int>(iw), R);

@@ -1081,6 +1081,7 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
   bp.nr = static_cast<uint32_t>(nr);
   bp.np = static_cast<uint32_t>(np);
   bp.nw = static_cast<uint32_t>(nw);
+  bp.threshold = threshold;
   bp.rank = static_cast<uint32_t>(rank);
   bp.world = static_cast<uint32_t>(world);
   bp.fpad = static_cast<int32_t>(std::min(std::ceil(scan->d_max / m->view.level[L].cell) + 2.0, 1e6));
@@ -1133,10 +1134,11 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
   RootHist hist{};
   hist.entries = W.hist_ent.get(static_cast<size_t>(kRotBatch) * kHistCap, s);
   hist.amb = W.hist_amb.get(static_cast<size_t>(kRotBatch) * kAmbCap, s);
-  int32_t* hn = W.hist_n.get(3 * kRotBatch + 1, s);
+  int32_t* hn = W.hist_n.get(4 * kRotBatch + 1, s);
   hist.n_ent = hn;
   hist.n_amb = hn + kRotBatch;
   hist.overflow = hn + 2 * kRotBatch;  // kRotBatch flags + 1 overflow counter
+  hist.total = hn + 3 * kRotBatch + 1;
   // unowned roots must read -1 (below any threshold); a single rank scores
   // and writes every root
   if (world > 1) BBS_CUDA(cudaMemsetAsync(root_scores, 0xFF, static_cast<size_t>(std::max<int64_t>(total, 1)) * 4, s));
