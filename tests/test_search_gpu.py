@@ -265,3 +265,24 @@ def test_dense_histograms_are_transparent(B, golden_scenes, monkeypatch):
         out[flag] = (r.best_score, r.best_pose.as_tuple(), r.stats.nodes_generated, r.stats.nodes_pruned,
                      r.stats.batches_flushed, tuple(r.best_score_trace), r.root_probes)
     assert out[None][:6] == out["1"][:6]
+
+
+def test_large_scan_paths_are_transparent(B, golden_scenes, monkeypatch):
+    """K = 70,000 (> 65535: no 16-bit dense histograms, hash builds; the
+    root batch's early column exit, prebuild and probe chunks at a size the
+    C2 bench never uses): cache on/off give identical searches."""
+    m, raw, _ = B.gen_scene(B.SceneSpec.default(**golden_scenes["campus"]["spec"]),
+                            golden_scenes["campus"]["seed"])
+    s = B.cut_scan(raw, min(70000, raw.shape[0]), 3)
+    sc = golden_scenes["campus"]
+    vm = B.MultiResVoxelMap.build(m, sc["r"], sc["max_level"])
+    ds = B.DeviceScan(vm, s)
+    out = {}
+    for flag in ("1", "0"):
+        monkeypatch.setenv("BBS_ROT_CACHE", flag)
+        cfg = B.SearchConfig(min_resolution=sc["r"], max_level=sc["max_level"], collect_trace=True)
+        r = B.search_scan(vm, ds, cfg)
+        out[flag] = (r.best_score, r.best_pose.as_tuple(), r.stats.nodes_generated, r.stats.nodes_pruned,
+                     r.stats.batches_flushed, tuple(r.best_score_trace))
+    assert out["1"] == out["0"]
+    assert s.shape[0] > 65535
