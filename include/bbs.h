@@ -282,6 +282,13 @@ int bbs_search_scan(bbs_map_t map, bbs_scan_t scan, const bbs_search_config* cfg
  * (each call leases its own workspace; the map is shared read-only). */
 int bbs_search_scan_on(bbs_map_t map, bbs_scan_t scan, const bbs_search_config* cfg, void* stream,
                        bbs_search_result* result);
+/* Throughput mode (C4: many scans, one map): search() for each of n
+ * device-resident scans, `concurrency` searches in flight at a time (native
+ * worker threads, one stream each; every search leases its own workspace).
+ * results[i] receives scan i's result (its trace buffer as set by the
+ * caller).  The first failure is returned after all workers stop. */
+int bbs_search_scans(bbs_map_t map, const bbs_scan_t* scans, uint64_t n, const bbs_search_config* cfg,
+                     int32_t concurrency, bbs_search_result* results);
 /* Non-blocking stream on `device` for bbs_search_scan_on. */
 int bbs_stream_create(int32_t device, void** out);
 int bbs_stream_destroy(void* stream);

@@ -32,7 +32,7 @@ __all__ = [
     "InfeasiblePoseError", "ConfigError", "CudaError", "InvalidArgumentError",
     "Strategy", "BranchMode", "Layout", "SearchConfig", "Stats", "SearchResult", "Pose6",
     "AxisGrid", "AngularGrid", "LevelMap", "MultiResVoxelMap", "DeviceScan", "NODE_DTYPE",
-    "batch_evaluate", "search", "search_sharded", "Comm", "nccl_version",
+    "batch_evaluate", "search", "search_sharded", "search_scans", "Comm", "nccl_version",
     "save_map", "load_map", "is_map_file", "localize_scan", "prepare_source", "prepare_source_device",
     "max_range", "bounding_box", "pose_to_transform", "node_pose", "initial_node_count",
     "gen_scene", "gen_scans", "cut_scan", "SceneSpec", "device_count",
@@ -666,6 +666,26 @@ def search_scan(vmap: MultiResVoxelMap, dscan: DeviceScan, cfg: SearchConfig,
         sp = stream._h if isinstance(stream, DeviceStream) else C.c_void_p(int(stream))
         _check(lib.bbs_search_scan_on(vmap._h, dscan._h, C.byref(c), sp, C.byref(res)))
     return _result_from_c(res, buf)
+
+
+def search_scans(vmap: MultiResVoxelMap, dscans, cfg: SearchConfig, concurrency=16, trace_capacity=0):
+    """Throughput mode (bbs_search_scans): search() for every device scan,
+    `concurrency` searches in flight on native threads / streams."""
+    n = len(dscans)
+    arr = (SearchResultC * max(n, 1))()
+    bufs = []
+    for i in range(n):
+        if cfg.collect_trace and trace_capacity:
+            b = (C.c_int32 * trace_capacity)()
+            arr[i].best_score_trace = C.cast(b, C.POINTER(C.c_int32))
+            arr[i].trace_capacity = trace_capacity
+            bufs.append(b)
+        else:
+            bufs.append(None)
+    handles = (C.c_void_p * max(n, 1))(*[d._h for d in dscans])
+    c = cfg.to_c()
+    _check(lib.bbs_search_scans(vmap._h, handles, n, C.byref(c), int(concurrency), arr))
+    return [_result_from_c(arr[i], bufs[i]) for i in range(n)]
 
 
 class Comm:

@@ -73,6 +73,8 @@ SIGNATURES = {
                                             _vp]),
     "bbs_search_scan_on": (C.c_int, [_vp, _vp, C.POINTER(SearchConfigC), _vp,
                                      C.POINTER(SearchResultC)]),
+    "bbs_search_scans": (C.c_int, [_vp, C.POINTER(_vp), _u64, C.POINTER(SearchConfigC), _i32,
+                                   C.POINTER(SearchResultC)]),
     "bbs_stream_create": (C.c_int, [_i32, C.POINTER(_vp)]),
     "bbs_stream_destroy": (C.c_int, [_vp]),
     "bbs_search_sharded": (C.c_int, [_vp, _vp, C.POINTER(SearchConfigC), C.POINTER(Shard),

@@ -4,13 +4,18 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cmath>
 #include <cstring>
+#include <exception>
 #include <limits>
 #include <memory>
+#include <mutex>
 #include <new>
 #include <string>
+#include <thread>
+#include <vector>
 
 #include "bbs_comm.h"
 #include "bbs_map_impl.h"
@@ -366,6 +371,39 @@ int bbs_search_scan_on(bbs_map_t map, bbs_scan_t scan, const bbs_search_config* 
     REQUIRE(map && scan && cfg && result, "null argument");
     REQUIRE(scan->map == map, "scan was uploaded for a different map");
     bbs::run_search(map, scan, *cfg, nullptr, result, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int bbs_search_scans(bbs_map_t map, const bbs_scan_t* scans, uint64_t n, const bbs_search_config* cfg,
+                     int32_t concurrency, bbs_search_result* results) {
+  return guard([&] {
+    REQUIRE(map && cfg && (results || n == 0) && (scans || n == 0), "null argument");
+    for (uint64_t i = 0; i < n; ++i)
+      REQUIRE(scans[i] && scans[i]->map == map, "scan was uploaded for a different map");
+    if (n == 0) return;
+    const int T = static_cast<int>(std::min<uint64_t>(n, static_cast<uint64_t>(std::max(1, std::min(concurrency, 128)))));
+    bbs::DeviceGuard g(map->device);
+    std::vector<cudaStream_t> streams(static_cast<size_t>(T));
+    for (auto& st : streams) BBS_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    std::atomic<uint64_t> next{0};
+    std::mutex err_mu;
+    std::exception_ptr first_err;
+    std::vector<std::thread> workers;
+    for (int t = 0; t < T; ++t)
+      workers.emplace_back([&, t] {
+        try {
+          bbs::DeviceGuard wg(map->device);
+          for (uint64_t j = next++; j < n; j = next++)
+            bbs::run_search(map, scans[j], *cfg, nullptr, &results[j], streams[static_cast<size_t>(t)]);
+        } catch (...) {
+          std::lock_guard<std::mutex> lk(err_mu);
+          if (!first_err) first_err = std::current_exception();
+          next = n;
+        }
+      });
+    for (auto& w : workers) w.join();
+    for (auto& st : streams) cudaStreamDestroy(st);
+    if (first_err) std::rethrow_exception(first_err);
   });
 }
 
