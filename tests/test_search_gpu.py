@@ -286,3 +286,22 @@ def test_large_scan_paths_are_transparent(B, golden_scenes, monkeypatch):
                      r.stats.batches_flushed, tuple(r.best_score_trace))
     assert out["1"] == out["0"]
     assert s.shape[0] > 65535
+
+
+def test_search_scans_throughput_mode_matches_single_searches(B):
+    """bbs_search_scans (native workers, one stream each, workspaces leased
+    concurrently) returns each scan's search() result."""
+    spec = B.SceneSpec.default(size_x=24.0, size_y=24.0, size_z=10.0, num_boxes=4, min_box_side=2.5,
+                               max_box_side=6.0, min_box_height=3.0, map_spacing=0.3,
+                               scan_spacing=0.45, scan_range=14.0, min_scan_points=300)
+    m, _, _ = B.gen_scene(spec, 42)
+    scans, _ = B.gen_scans(spec, 42, 1000, 6)
+    vm = B.MultiResVoxelMap.build(m, 0.5, 3)
+    ds = [B.DeviceScan(vm, s) for s in scans]
+    cfg = B.SearchConfig(min_resolution=0.5, max_level=3, batch_size=400, collect_trace=True)
+    many = B.search_scans(vm, ds, cfg, concurrency=4, trace_capacity=1 << 12)
+    for d, r in zip(ds, many):
+        one = B.search_scan(vm, d, cfg)
+        assert (r.best_score, r.best_pose.as_tuple(), r.stats.nodes_generated, r.stats.nodes_pruned,
+                r.best_score_trace) == (one.best_score, one.best_pose.as_tuple(), one.stats.nodes_generated,
+                                        one.stats.nodes_pruned, one.best_score_trace)
