@@ -7,6 +7,7 @@ timeout 900 python -m pytest tests -m gpu -q > $O/pytest_gpu.log 2>&1; echo "pyt
 python bench.py > $O/bench_c2.json 2> $O/bench_c2.err
 python bench.py --config c3 --steps 3 --no-cpu-baseline > $O/bench_c3.json 2> $O/bench_c3.err
 python bench.py --config c4 --steps 3 --no-cpu-baseline > $O/bench_c4.json 2> $O/bench_c4.err
+python bench.py --config c1 --steps 5 --no-cpu-baseline > $O/bench_c1.json 2> $O/bench_c1.err
 python bench.py --impl reference --steps 3 --warmup 1 > $O/bench_reference.json 2> $O/bench_reference.err
 timeout 900 python scripts/sweep_c5.py > $O/sweep_c5.json 2> $O/sweep_c5.err
 M=gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum
