@@ -110,7 +110,9 @@ void map_file_read_levels(MapFile* mf, bbs_map* m) {
   cudaStream_t s = m->stream;
   const int n_levels = static_cast<int>(mf->max_level) + 1;
   begin_levels(m, n_levels);
-  Pinned stage(2 * kChunk);
+  // staging: two chunks, no larger than the file's voxel payload needs
+  const size_t chunk = static_cast<size_t>(std::min<uint64_t>(kChunk, std::max<uint64_t>(12, mf->size - mf->pos)));
+  Pinned stage(2 * chunk);
   cudaEvent_t done[2];
   BBS_CUDA(cudaEventCreateWithFlags(&done[0], cudaEventDisableTiming));
   BBS_CUDA(cudaEventCreateWithFlags(&done[1], cudaEventDisableTiming));
@@ -137,9 +139,9 @@ void map_file_read_levels(MapFile* mf, bbs_map* m) {
     uint64_t bytes = count * 12, off = 0;
     int b = 0;
     while (bytes > 0) {
-      const size_t n = static_cast<size_t>(std::min<uint64_t>(bytes, kChunk));
+      const size_t n = static_cast<size_t>(std::min<uint64_t>(bytes, chunk));
       if (used[b]) BBS_CUDA(cudaEventSynchronize(done[b]));  // its previous copy finished
-      char* h = static_cast<char*>(stage.p) + b * kChunk;
+      char* h = static_cast<char*>(stage.p) + b * chunk;
       mf->read(h, n);
       BBS_CUDA(cudaMemcpyAsync(reinterpret_cast<char*>(d_vox) + off, h, n, cudaMemcpyHostToDevice, s));
       BBS_CUDA(cudaEventRecord(done[b], s));
