@@ -1,7 +1,7 @@
 """Extra reference searches on the C2 campus workload (DFS, small batch,
 +-5 deg roll/pitch), appended to campus_search.json.  Runs the UNMODIFIED
 reference (oracle/_ref) — several CPU minutes each; the device replays them in
-tests/test_search_gpu.py::test_campus_extra_searches_match_reference."""
+tests/test_search_gpu.py::test_search_matches_reference_golden (every label)."""
 import json
 import os
 import sys
