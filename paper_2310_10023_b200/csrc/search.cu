@@ -764,6 +764,210 @@ __global__ void queue_keys_kernel(const uint32_t* __restrict__ perm, const bbs_n
   }
 }
 
+// Root survivors -> sorted queue without a host round trip (the push of the
+// root batch, search.hpp:120-124).  The same order as roots_to_queue + the
+// stable radix sort above, with every size kept on the device:
+//  1. root_select_kernel: ordered compaction of the roots with score >=
+//     threshold (decoupled look-back over tiles taken by ticket); survivor o
+//     (seq o) goes to pool[o], its short key smax - score to bkey[o]; the
+//     digit histograms of the <= 2 radix passes are counted on the way and
+//     the last tile sets the queue length.
+//  2. root_pass_kernel, one launch per 8-bit digit: stable LSD pass (match-
+//     based block rank in warp-striped order + per-digit look-back across
+//     tiles); the last pass writes the 64-bit queue keys directly.  DFS feeds
+//     the survivors in reverse so ties order by seq descending.
+constexpr int kRST = 256, kRSIPT = 16, kRSTile = kRST * kRSIPT;
+constexpr int kRPT = 256, kRPIPT = 8, kRPTile = kRPT * kRPIPT;
+constexpr int kRCtlHist = 4;  // ctl: [0] select ticket, [1 + p] pass tickets, [4 + 256 p + d] digit counts
+
+struct RootInit {
+  uint32_t* ctl;
+  unsigned long long* sel_tiles;   // one look-back word per selection tile
+  unsigned long long* pass_tiles;  // 256 look-back words per pass tile, per pass
+  uint32_t pass_tiles_cap;
+  unsigned long long tag;          // per-search tag (bits 34+): nothing to clear between searches
+  uint32_t* bkey;                  // smax - score, seq order
+  uint32_t* k1;                    // after pass 0 (two-pass sorts)
+  uint32_t* v1;
+};
+
+__device__ __forceinline__ unsigned long long lookback_excl(unsigned long long* words, uint32_t tile,
+                                                            uint32_t stride, unsigned long long tag,
+                                                            uint32_t count) {
+  // words[t * stride]: tag | flag << 32 | value (flag 1 aggregate, 2 inclusive)
+  if (tile == 0) {
+    atomicExch(&words[0], tag | (2ull << 32) | count);
+    return 0;
+  }
+  atomicExch(&words[static_cast<size_t>(tile) * stride], tag | (1ull << 32) | count);
+  uint32_t excl = 0;
+  for (int64_t t = static_cast<int64_t>(tile) - 1; t >= 0;) {
+    const unsigned long long w = atomicAdd(&words[static_cast<size_t>(t) * stride], 0ull);
+    if ((w & ~((1ull << 34) - 1)) != tag) continue;  // not published yet
+    excl += static_cast<uint32_t>(w);
+    if (((w >> 32) & 3u) == 2u) break;
+    --t;
+  }
+  atomicExch(&words[static_cast<size_t>(tile) * stride], tag | (2ull << 32) | (excl + count));
+  return excl;
+}
+
+__global__ void __launch_bounds__(kRST) root_select_kernel(EpochState* st, const int32_t* __restrict__ scores,
+                                                           uint32_t n, unsigned long long n_scored,
+                                                           int32_t threshold, int32_t smax, BoxParams bp,
+                                                           bbs_node* __restrict__ pool, RootInit ri, EpochState h0) {
+  pdl_wait();
+
+  using Load = cub::BlockLoad<int32_t, kRST, kRSIPT, cub::BLOCK_LOAD_WARP_TRANSPOSE>;
+  using ScanI = cub::BlockScan<int, kRST>;
+  __shared__ union {
+    typename Load::TempStorage load;
+    typename ScanI::TempStorage scan;
+  } tmp;
+  __shared__ uint32_t s_tile, s_excl;
+  __shared__ uint32_t s_h[2 * 256];
+  for (int i = threadIdx.x; i < 2 * 256; i += kRST) s_h[i] = 0;
+  const uint32_t n_tiles = (n + kRSTile - 1) / kRSTile;
+  const unsigned long long nrot = static_cast<unsigned long long>(bp.nr) * bp.np * bp.nw;
+  for (;;) {
+    if (threadIdx.x == 0) s_tile = atomicAdd(&ri.ctl[0], 1u);
+    __syncthreads();
+    const uint32_t tile = s_tile;
+    if (tile >= n_tiles) break;
+    const uint32_t base = tile * kRSTile;
+    const uint32_t valid = min(static_cast<uint32_t>(kRSTile), n - base);
+    int32_t sc[kRSIPT];
+    Load(tmp.load).Load(scores + base, sc, static_cast<int>(valid), INT_MIN);
+    __syncthreads();
+    int cnt = 0;
+#pragma unroll
+    for (int k = 0; k < kRSIPT; ++k) cnt += sc[k] >= threshold ? 1 : 0;
+    int pos, tot;
+    ScanI(tmp.scan).ExclusiveSum(cnt, pos, tot);
+    if (threadIdx.x == 0) {
+      const uint32_t excl = lookback_excl(ri.sel_tiles, tile, 1, ri.tag, static_cast<uint32_t>(tot));
+      s_excl = excl;
+      if (tile == n_tiles - 1) {
+        // the loop's initial state (no host copy on this path)
+        const uint32_t kept = excl + static_cast<uint32_t>(tot);
+        h0.q_len = kept;
+        h0.seq = kept;
+        h0.q_peak = kept;
+        h0.nodes_pruned = n_scored - kept;
+        h0.active = kept > 0 ? 1 : 0;
+        h0.any_active = h0.active;
+        *st = h0;
+      }
+    }
+    __syncthreads();
+    uint32_t o = s_excl + static_cast<uint32_t>(pos);
+#pragma unroll
+    for (int k = 0; k < kRSIPT; ++k) {
+      if (sc[k] < threshold) continue;
+      const unsigned long long r = base + threadIdx.x * kRSIPT + k;
+      const unsigned long long rot = r % nrot, t = r / nrot;
+      bbs_node nd;
+      nd.iyaw = static_cast<int32_t>(rot % bp.nw);
+      nd.ipitch = static_cast<int32_t>((rot / bp.nw) % bp.np);
+      nd.iroll = static_cast<int32_t>(rot / (static_cast<unsigned long long>(bp.nw) * bp.np));
+      nd.iz = bp.z0 + static_cast<int32_t>(t % bp.nz);
+      nd.iy = bp.y0 + static_cast<int32_t>((t / bp.nz) % bp.ny);
+      nd.ix = bp.x0 + static_cast<int32_t>(t / (static_cast<unsigned long long>(bp.nz) * bp.ny));
+      nd.level = bp.level;
+      nd.score = sc[k];
+      pool[o] = nd;
+      const uint32_t b = static_cast<uint32_t>(smax - sc[k]);
+      ri.bkey[o] = b;
+      atomicAdd(&s_h[b & 255u], 1u);
+      atomicAdd(&s_h[256 + ((b >> 8) & 255u)], 1u);
+      ++o;
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < 2 * 256; i += kRST)
+    if (s_h[i]) atomicAdd(&ri.ctl[kRCtlHist + i], s_h[i]);
+}
+
+struct RootDigit {
+  uint32_t shift;
+  __device__ __forceinline__ uint32_t Digit(uint32_t key) const { return (key >> shift) & 255u; }
+};
+
+template <bool kFinal>
+__global__ void __launch_bounds__(kRPT) root_pass_kernel(const EpochState* st, RootInit ri, uint32_t pass,
+                                                         int strategy, int32_t smax, int32_t level,
+                                                         const uint32_t* __restrict__ kin,
+                                                         const uint32_t* __restrict__ vin,
+                                                         uint32_t* __restrict__ kout, uint32_t* __restrict__ vout,
+                                                         unsigned long long* __restrict__ qkey) {
+  pdl_wait();
+
+  using Rank = cub::BlockRadixRankMatch<kRPT, 8, false>;
+  using ScanU = cub::BlockScan<uint32_t, kRPT>;
+  __shared__ union {
+    typename Rank::TempStorage rank;
+    typename ScanU::TempStorage scan;
+  } tmp;
+  __shared__ uint32_t s_tile, s_pre[256], s_base[256];
+  const uint32_t n = st->q_len;
+  const uint32_t n_tiles = (n + kRPTile - 1) / kRPTile;
+  unsigned long long* words = ri.pass_tiles + static_cast<size_t>(pass) * ri.pass_tiles_cap * 256;
+  // the pass's global digit offsets
+  uint32_t gpre;
+  ScanU(tmp.scan).ExclusiveSum(ri.ctl[kRCtlHist + 256 * pass + threadIdx.x], gpre);
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
+  const RootDigit dig{8u * pass};
+  for (;;) {
+    if (threadIdx.x == 0) s_tile = atomicAdd(&ri.ctl[1 + pass], 1u);
+    __syncthreads();
+    const uint32_t tile = s_tile;
+    if (tile >= n_tiles) break;
+    const uint32_t base = tile * kRPTile;
+    const uint32_t valid = min(static_cast<uint32_t>(kRPTile), n - base);
+    // warp-striped: the match-based rank is stable in this order
+    uint32_t key[kRPIPT], val[kRPIPT];
+#pragma unroll
+    for (int k = 0; k < kRPIPT; ++k) {
+      const uint32_t j = warp * (32 * kRPIPT) + k * 32 + lane;
+      key[k] = 0xFFFFFFFFu;  // digit 255, after every real key of the tile
+      val[k] = 0;
+      if (j < valid) {
+        if (pass == 0) {
+          const uint32_t src = strategy == BBS_STRATEGY_BFS ? base + j : n - 1 - (base + j);
+          key[k] = kin[src];
+          val[k] = src;
+        } else {
+          key[k] = kin[base + j];
+          val[k] = vin[base + j];
+        }
+      }
+    }
+    int ranks[kRPIPT];
+    int pre[1];
+    Rank(tmp.rank).RankKeys(key, ranks, dig, pre);
+    s_pre[threadIdx.x] = static_cast<uint32_t>(pre[0]);
+    __syncthreads();
+    uint32_t cnt = (threadIdx.x < 255 ? s_pre[threadIdx.x + 1] : static_cast<uint32_t>(kRPTile)) - s_pre[threadIdx.x];
+    if (threadIdx.x == 255) cnt -= kRPTile - valid;  // the padding
+    const uint32_t excl = lookback_excl(words + threadIdx.x, tile, 256, ri.tag, cnt);
+    s_base[threadIdx.x] = gpre + excl - s_pre[threadIdx.x];
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < kRPIPT; ++k) {
+      const uint32_t j = warp * (32 * kRPIPT) + k * 32 + lane;
+      if (j >= valid) continue;
+      const uint32_t p = s_base[dig.Digit(key[k])] + static_cast<uint32_t>(ranks[k]);
+      if (kFinal) {
+        qkey[p] = queue_key(strategy, smax - static_cast<int32_t>(key[k]), level, val[k]);
+      } else {
+        kout[p] = key[k];
+        vout[p] = val[k];
+      }
+    }
+    __syncthreads();
+  }
+}
+
 __global__ void soa_kernel(const double* __restrict__ aos, uint64_t k, double* __restrict__ soa) {
   for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < k;
        i += uint64_t(gridDim.x) * blockDim.x) {
@@ -855,7 +1059,9 @@ struct Workspace {
   Buf<int4> hist_ent, cache_info, cache_pool, cache_builds;
   Buf<uint32_t> cache_u32, cache_amb, cache_fb, stage_win;
   Buf<int32_t> cache_builds_w;
-  Buf<uint32_t> hist_amb;
+  Buf<uint32_t> hist_amb, rinit_ctl;
+  Buf<unsigned long long> rinit_tiles;
+  unsigned long long rinit_tag = 0;
   Buf<EpochState> st;
   EpochState* h_st = nullptr;
   cudaStream_t side = nullptr;            // prebuild stream (forked per search)
@@ -874,7 +1080,8 @@ struct Workspace {
     for (auto* b : {&root_scores, &pscores, &trace, &hist_n, &pscores_own, &xchg}) b->release();
     for (auto* b : {&probes, &surv_idx, &qk0, &qk1, &s_key, &s_key2, &surv_tiles}) b->release();
     for (auto* b : {&pool, &pending, &pending_own}) b->release();
-    for (auto* b : {&perm0, &perm1, &sk0, &sk1, &exp_parent, &exp_off, &hist_amb}) b->release();
+    for (auto* b : {&perm0, &perm1, &sk0, &sk1, &exp_parent, &exp_off, &hist_amb, &rinit_ctl}) b->release();
+    rinit_tiles.release();
     lut.release();
     nsel.release();
     temp.release();
@@ -1143,6 +1350,33 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
   // and writes every root
   if (world > 1) BBS_CUDA(cudaMemsetAsync(root_scores, 0xFF, static_cast<size_t>(std::max<int64_t>(total, 1)) * 4, s));
   BBS_CUDA(cudaMemsetAsync(d_probes, 0, sizeof(unsigned long long), s));
+  // root survivors -> queue on the device (root_select + root_pass kernels)
+  // when the short key (smax - score) takes <= 2 digit passes and the roots
+  // fit 32-bit positions; else CUB select + sort after a host sync
+  const int32_t smax = static_cast<int32_t>(std::min<size_t>(K, 0x7FFFFFFF));
+  const uint32_t span = static_cast<uint32_t>(smax - std::max<int32_t>(0, std::min(threshold, smax)));
+  int end_bit = 1;
+  while (end_bit < 32 && (span >> end_bit) != 0) ++end_bit;
+  const char* init_env = std::getenv("BBS_ROOT_INIT");  // "host" / "device": A/B override
+  const bool dev_init_ok = total > 0 && static_cast<uint64_t>(total) <= (64ull << 20) && end_bit <= 16 &&
+                           !(init_env && std::strcmp(init_env, "host") == 0);
+  RootInit rinit{};
+  if (dev_init_ok) {
+    const uint64_t n = static_cast<uint64_t>(total);
+    const uint64_t sel_tiles = (n + kRSTile - 1) / kRSTile, pass_tiles = (n + kRPTile - 1) / kRPTile;
+    const size_t words = sel_tiles + 2 * 256 * pass_tiles;
+    const size_t had = W.rinit_tiles.cap;
+    unsigned long long* tw = W.rinit_tiles.get(words, s);
+    if (W.rinit_tiles.cap != had)  // fresh words: no tag matches zero
+      BBS_CUDA(cudaMemsetAsync(tw, 0, W.rinit_tiles.cap * sizeof(unsigned long long), s));
+    rinit.sel_tiles = tw;
+    rinit.pass_tiles = tw + sel_tiles;
+    rinit.pass_tiles_cap = static_cast<uint32_t>(pass_tiles);
+    W.rinit_tag = (W.rinit_tag % ((1ull << 30) - 1)) + 1;
+    rinit.tag = W.rinit_tag << 34;
+    rinit.ctl = W.rinit_ctl.get(kRCtlHist + 512, s);
+    BBS_CUDA(cudaMemsetAsync(rinit.ctl, 0, (kRCtlHist + 512) * sizeof(uint32_t), s));
+  }
   BBS_CUDA(cudaEventRecord(ev_roots0, s));
   if (total > 0) {
     launch_score_roots(m->view, gv, sv, bp, hist, root_scores, d_probes, s);
@@ -1263,66 +1497,129 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
     }
   }
 
+  // (A/B on one box, 3 rounds: C2 0.936 vs 0.938 ms, C3 54.8 vs 55.1 ms, C1
+  // 2.065 vs 2.046 ms for device vs host; between bench processes the same
+  // path moves by ~1.5% with the buffers' placement, so the two are even on
+  // latency; the device path has no host round trip, which frees the host
+  // thread for concurrent searches)
+  const bool dev_init = dev_init_ok;
+
   // exact mode: every rank gets every root score (unowned roots are -1)
   if (exact) xmax(root_scores, static_cast<size_t>(std::max<int64_t>(total, 0)));
   const uint64_t n_scored_roots = exact ? static_cast<uint64_t>(std::max<int64_t>(total, 0)) : n_own;
 
   // survivors >= threshold among own roots, in initial_nodes order
-  // survivor index buffer: the root count bounds it; huge root sets (TransOnly
-  // searches: billions of roots) count the survivors first instead
-  uint64_t surv_cap = std::max<uint64_t>(n_scored_roots, 1);
-  if (total > 0 && n_scored_roots > (64ull << 20)) {
-    unsigned long long* d_cnt = d_probes + 1;
-    BBS_CUDA(cudaMemsetAsync(d_cnt, 0, sizeof(unsigned long long), s));
-    count_survivors_kernel<<<grid1(static_cast<uint64_t>(total)), 256, 0, s>>>(root_scores, static_cast<uint64_t>(total),
-                                                                               threshold, d_cnt);
-    BBS_CUDA(cudaGetLastError());
-    BBS_CUDA(cudaMemcpyAsync(&W.h_small[2], d_cnt, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
-    BBS_CUDA(cudaStreamSynchronize(s));
-    d2h += sizeof(unsigned long long);
-    surv_cap = std::max<uint64_t>(W.h_small[2], 1);
-    ++launches;
-  }
-  unsigned long long* surv_idx = W.surv_idx.get(static_cast<size_t>(surv_cap), s);
-  int n_root_surv = 0;
-  if (total > 0) {
-    cub::CountingInputIterator<unsigned long long> cnt(0);
-    size_t tb = 0;
-    BBS_CUDA(cub::DeviceSelect::If(nullptr, tb, cnt, surv_idx, d_nsel, static_cast<int64_t>(total),
-                                   RootSurvives{root_scores, threshold}, s));
-    void* temp = W.temp.get(tb, s);
-    BBS_CUDA(cub::DeviceSelect::If(temp, tb, cnt, surv_idx, d_nsel, static_cast<int64_t>(total),
-                                   RootSurvives{root_scores, threshold}, s));
-    BBS_CUDA(cudaMemcpyAsync(&W.h_small[0], d_probes, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
-    BBS_CUDA(cudaMemcpyAsync(&W.h_small[1], d_nsel, sizeof(int), cudaMemcpyDeviceToHost, s));
-    d2h += sizeof(unsigned long long) + sizeof(int);
+  const int E = host_x ? 1 : 8;  // epochs per host check
+  unsigned long long root_probes = 0;
+  int n_root_surv = 0;       // host path only
+  unsigned long long* surv_idx = nullptr;
+  uint64_t q_upper = 0;      // bound on the root survivors (queue / pool sizing)
+  if (dev_init) {
+    q_upper = static_cast<uint64_t>(total);
     BBS_CUDA(cudaEventRecord(ev_sel, s));
-    BBS_CUDA(cudaStreamSynchronize(s));
-    n_root_surv = *reinterpret_cast<int*>(&W.h_small[1]);
   } else {
-    W.h_small[0] = 0;
+    // survivor index buffer: the root count bounds it; huge root sets (TransOnly
+    // searches: billions of roots) count the survivors first instead
+    uint64_t surv_cap = std::max<uint64_t>(n_scored_roots, 1);
+    if (total > 0 && n_scored_roots > (64ull << 20)) {
+      unsigned long long* d_cnt = d_probes + 1;
+      BBS_CUDA(cudaMemsetAsync(d_cnt, 0, sizeof(unsigned long long), s));
+      count_survivors_kernel<<<grid1(static_cast<uint64_t>(total)), 256, 0, s>>>(root_scores, static_cast<uint64_t>(total),
+                                                                                 threshold, d_cnt);
+      BBS_CUDA(cudaGetLastError());
+      BBS_CUDA(cudaMemcpyAsync(&W.h_small[2], d_cnt, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+      BBS_CUDA(cudaStreamSynchronize(s));
+      d2h += sizeof(unsigned long long);
+      surv_cap = std::max<uint64_t>(W.h_small[2], 1);
+      ++launches;
+    }
+    surv_idx = W.surv_idx.get(static_cast<size_t>(surv_cap), s);
+    if (total > 0) {
+      cub::CountingInputIterator<unsigned long long> cnt(0);
+      size_t tb = 0;
+      BBS_CUDA(cub::DeviceSelect::If(nullptr, tb, cnt, surv_idx, d_nsel, static_cast<int64_t>(total),
+                                     RootSurvives{root_scores, threshold}, s));
+      void* temp = W.temp.get(tb, s);
+      BBS_CUDA(cub::DeviceSelect::If(temp, tb, cnt, surv_idx, d_nsel, static_cast<int64_t>(total),
+                                     RootSurvives{root_scores, threshold}, s));
+      BBS_CUDA(cudaMemcpyAsync(&W.h_small[0], d_probes, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+      BBS_CUDA(cudaMemcpyAsync(&W.h_small[1], d_nsel, sizeof(int), cudaMemcpyDeviceToHost, s));
+      d2h += sizeof(unsigned long long) + sizeof(int);
+      BBS_CUDA(cudaEventRecord(ev_sel, s));
+      BBS_CUDA(cudaStreamSynchronize(s));
+      n_root_surv = *reinterpret_cast<int*>(&W.h_small[1]);
+      root_probes = W.h_small[0];
+    } else {
+      BBS_CUDA(cudaEventRecord(ev_sel, s));
+    }
+    q_upper = static_cast<uint64_t>(n_root_surv);
   }
-  const unsigned long long root_probes = W.h_small[0];
 
   // queue buffers
-  const int E = host_x ? 1 : 8;  // epochs per host check
-  uint64_t qcap = static_cast<uint64_t>(n_root_surv) + static_cast<uint64_t>(E + 1) * pend_cap;
+  uint64_t qcap = q_upper + static_cast<uint64_t>(E + 1) * pend_cap;
   Queue q{};
   q.key[0] = W.qk0.get(qcap, s);
   q.key[1] = W.qk1.get(qcap, s);
   qcap = std::min(W.qk0.cap, W.qk1.cap);
   // node pool: one slot per push (seq), roots first in initial_nodes order
-  uint64_t pool_cap = static_cast<uint64_t>(n_root_surv) + static_cast<uint64_t>(E + 1) * pend_cap;
+  uint64_t pool_cap = q_upper + static_cast<uint64_t>(E + 1) * pend_cap;
   q.pool = W.pool.get(pool_cap, s);
   pool_cap = W.pool.cap;
   BBS_CUDA(cudaEventRecord(ev_q0, s));
-  if (n_root_surv > 0) {
+
+  // device path: the root kernels set the queue length, activity and prune
+  // count of this state
+  EpochState h0{};
+  h0.best = threshold;
+  h0.q_len = static_cast<uint32_t>(n_root_surv);
+  h0.cur = 0;
+  h0.seq = static_cast<unsigned long long>(n_root_surv);
+  h0.nodes_generated = n_scored_roots;
+  h0.nodes_pruned = n_scored_roots - static_cast<uint64_t>(n_root_surv);
+  h0.batches_flushed = 1;
+  h0.last_best_epoch = -1;
+  h0.active = n_root_surv > 0 ? 1 : 0;
+  h0.any_active = h0.active;
+  h0.q_peak = h0.q_len;
+  EpochState* d_st = W.st.get(1, s);
+  if (!dev_init) {
+    *W.h_st = h0;
+    BBS_CUDA(cudaMemcpyAsync(d_st, W.h_st, sizeof(h0), cudaMemcpyHostToDevice, s));
+    h2d += sizeof(h0);
+  }
+
+  if (dev_init) {
+    const uint32_t n = static_cast<uint32_t>(total);
+    const uint32_t sel_tiles = (n + kRSTile - 1) / kRSTile;
+    const uint32_t pass_tiles = (n + kRPTile - 1) / kRPTile;
+    rinit.bkey = W.sk0.get(n, s);
+    rinit.k1 = W.sk1.get(n, s);
+    rinit.v1 = W.perm0.get(n, s);
+    launch_pdl(root_select_kernel, std::min<uint32_t>(sel_tiles, 148u * 8u), kRST, 0, s, d_st,
+               static_cast<const int32_t*>(root_scores), n, static_cast<unsigned long long>(n_scored_roots),
+               threshold, smax, bp, q.pool, rinit, h0);
+    BBS_CUDA(cudaGetLastError());
+    const unsigned pgrid = std::min<uint32_t>(pass_tiles, 148u * 8u);
+    if (end_bit <= 8) {
+      launch_pdl(root_pass_kernel<true>, pgrid, kRPT, 0, s, static_cast<const EpochState*>(d_st), rinit, 0u,
+                 strategy, smax, L, static_cast<const uint32_t*>(rinit.bkey), static_cast<const uint32_t*>(nullptr),
+                 static_cast<uint32_t*>(nullptr), static_cast<uint32_t*>(nullptr), q.key[0]);
+      BBS_CUDA(cudaGetLastError());
+      launches += 2;
+    } else {
+      launch_pdl(root_pass_kernel<false>, pgrid, kRPT, 0, s, static_cast<const EpochState*>(d_st), rinit, 0u,
+                 strategy, smax, L, static_cast<const uint32_t*>(rinit.bkey), static_cast<const uint32_t*>(nullptr),
+                 rinit.k1, rinit.v1, static_cast<unsigned long long*>(nullptr));
+      BBS_CUDA(cudaGetLastError());
+      launch_pdl(root_pass_kernel<true>, pgrid, kRPT, 0, s, static_cast<const EpochState*>(d_st), rinit, 1u,
+                 strategy, smax, L, static_cast<const uint32_t*>(rinit.k1), static_cast<const uint32_t*>(rinit.v1),
+                 static_cast<uint32_t*>(nullptr), static_cast<uint32_t*>(nullptr), q.key[0]);
+      BBS_CUDA(cudaGetLastError());
+      launches += 3;
+    }
+  } else if (n_root_surv > 0) {
     // nodes in initial_nodes order (seq = position), stable sort on the
     // score key over only the bits it spans, then gather nodes + queue keys
-    const int32_t smax = static_cast<int32_t>(std::min<size_t>(K, 0x7FFFFFFF));
-    const uint32_t span = static_cast<uint32_t>(smax - std::max<int32_t>(0, std::min(threshold, smax)));
-    int end_bit = 1;
-    while (end_bit < 32 && (span >> end_bit) != 0) ++end_bit;
     uint32_t* sk0 = W.sk0.get(n_root_surv, s);
     uint32_t* sk1 = W.sk1.get(n_root_surv, s);
     bbs_node* n0 = q.pool;  // pool[seq] = root with rank seq among the survivors
@@ -1341,23 +1638,6 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
     BBS_CUDA(cudaGetLastError());
     launches += 2;  // roots_to_queue, gather
   }
-
-  EpochState h0{};
-  h0.best = threshold;
-  h0.q_len = static_cast<uint32_t>(n_root_surv);
-  h0.cur = 0;
-  h0.seq = static_cast<unsigned long long>(n_root_surv);
-  h0.nodes_generated = n_scored_roots;
-  h0.nodes_pruned = n_scored_roots - static_cast<uint64_t>(n_root_surv);
-  h0.batches_flushed = 1;
-  h0.last_best_epoch = -1;
-  h0.active = n_root_surv > 0 ? 1 : 0;
-  h0.any_active = h0.active;
-  h0.q_peak = h0.q_len;
-  EpochState* d_st = W.st.get(1, s);
-  *W.h_st = h0;
-  BBS_CUDA(cudaMemcpyAsync(d_st, W.h_st, sizeof(h0), cudaMemcpyHostToDevice, s));
-  h2d += sizeof(h0);
   BBS_CUDA(cudaEventRecord(ev_loop, s));
 
   bbs_node* pending = W.pending.get(pend_cap, s);
@@ -1482,6 +1762,11 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
   } exec_guard{&batch_exec};
   EpochState hs = h0;
   bool self_active = h0.active != 0;
+  if (dev_init) {  // upper bounds until the first device state comes back
+    hs.q_len = static_cast<uint32_t>(q_upper);
+    hs.seq = q_upper;
+    self_active = true;
+  }
   bool others_active = false;
   auto exchange = [&]() {
     if (!roots_host_x) return;
@@ -1604,8 +1889,13 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
   }
   BBS_CUDA(cudaMemcpyAsync(W.h_st, d_st, sizeof(EpochState), cudaMemcpyDeviceToHost, s));
   d2h += sizeof(EpochState);
+  if (dev_init) {
+    BBS_CUDA(cudaMemcpyAsync(&W.h_small[0], d_probes, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+    d2h += sizeof(unsigned long long);
+  }
   BBS_CUDA(cudaStreamSynchronize(s));
   hs = *W.h_st;
+  if (dev_init) root_probes = W.h_small[0];
 
   // ---- results ----
   std::memset(&out->stats, 0, sizeof(out->stats));
@@ -1631,6 +1921,25 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
   out->root_nodes = n_own;  // roots this rank scored
   out->lookups = hs.nodes_generated * K;
   out->queue_peak = hs.q_peak;
+  if (std::getenv("BBS_DEBUG_CACHE") && hs.seq > 0) {
+    // dev aid: rotations (and level L-1 child rotations) the root survivors use
+    const uint64_t np0 = std::min<uint64_t>(hs.seq, q_upper);
+    std::vector<bbs_node> pn(np0);
+    BBS_CUDA(cudaMemcpyAsync(pn.data(), q.pool, np0 * sizeof(bbs_node), cudaMemcpyDeviceToHost, s));
+    BBS_CUDA(cudaStreamSynchronize(s));
+    std::vector<char> used(nrot, 0);
+    uint64_t nroot = 0;
+    for (const auto& nd : pn)
+      if (nd.level == L) {
+        ++nroot;
+        used[(static_cast<uint64_t>(nd.iroll) * bp.np + nd.ipitch) * bp.nw + nd.iyaw] = 1;
+      }
+    uint64_t nu = 0;
+    for (char c : used) nu += c;
+    std::fprintf(stderr, "[roots] survivors %llu of %llu, rotations used %llu of %u\n",
+                 static_cast<unsigned long long>(nroot), static_cast<unsigned long long>(n_scored_roots),
+                 static_cast<unsigned long long>(nu), nrot);
+  }
   if (cache.enabled && std::getenv("BBS_DEBUG_CACHE")) {
     // dev aid: built histograms per level and their mean size
     const size_t ns = W.cache_info.cap;

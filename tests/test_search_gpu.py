@@ -42,6 +42,21 @@ def test_search_matches_reference_golden(B, golden_scenes, name, layout):
         assert_same(res, want, f"{name}/{label}/{layout}")
 
 
+@pytest.mark.parametrize("init", ["device", "host"])
+@pytest.mark.parametrize("name", ["small", "room", "campus"])
+def test_root_queue_init_paths(B, golden_scenes, name, init, monkeypatch):
+    """Both builds of the initial queue (root survivors -> sorted queue) match
+    the reference: the device path (root_select + root_pass kernels, no host
+    round trip) and the host path (CUB select + sort after a sync); the
+    default picks one per search (DESIGN §3 K5/K6)."""
+    monkeypatch.setenv("BBS_ROOT_INIT", init)
+    m, s, _, sc = load_case(B, golden_scenes, name)
+    vm = B.MultiResVoxelMap.build(m, sc["r"], sc["max_level"])
+    for label, want in golden_json(f"{name}_search.json").items():
+        res = B.search(vm, s, make_cfg(B, sc, name, want["overrides"]))
+        assert_same(res, want, f"{name}/{label}/{init}")
+
+
 def test_device_scan_equals_host_scan(B, golden_scenes):
     m, s, _, sc = load_case(B, golden_scenes, "small")
     vm = B.MultiResVoxelMap.build(m, sc["r"], sc["max_level"])
