@@ -786,8 +786,11 @@ __global__ void __launch_bounds__(256) root_col_kernel(GridView grid, ScanView s
 // bits, 3 PRMT pack their low bytes, and per z-translation j one LOP3 keeps
 // bit j of every byte and one IDP4A adds 2^j * sum(count) of the hits.
 constexpr int kGrpTile = 1024;  // groups per shared-memory tile (16 KB + 4 KB)
+#ifndef BBS_COLPAD_MINB
+#define BBS_COLPAD_MINB 3  // <= 80 registers, no spills: 3 CTAs per SM (C2 root batch -13 us; 4 spills)
+#endif
 template <int NZ>
-__global__ void __launch_bounds__(256) root_colpad_kernel(GridView grid, ScanView scan, BoxParams bp,
+__global__ void __launch_bounds__(256, BBS_COLPAD_MINB) root_colpad_kernel(GridView grid, ScanView scan, BoxParams bp,
                                                           LevelView L, uint32_t rot_begin,
                                                           uint32_t rot_end, RootHist h, RootStage st,
                                                           uint32_t n_cchunks,
@@ -1032,13 +1035,16 @@ void launch_score_roots(const MapView& map, const GridView& grid, const ScanView
     const int64_t yo0 = static_cast<int64_t>(bp.y0) - L.box_min[1], yo1 = yo0 + bp.ny - 1;
     const int64_t sx0 = std::min<int64_t>(0, xo0) - R, sx1 = std::max<int64_t>(L.dim[0], xo1 + 1) + R;
     const int64_t sy0 = std::min<int64_t>(0, yo0) - R, sy1 = std::max<int64_t>(L.dim[1], yo1 + 1) + R;
-    const int64_t words = (sx1 - sx0) * (sy1 - sy0);
+    // odd pitch: the 32 lanes of a warp (consecutive y, one pitch apart)
+    // read 32 distinct shared-memory banks
+    const int64_t pitch = (sx1 - sx0) | (std::getenv("BBS_EVEN_PITCH") ? 0 : 1);
+    const int64_t words = pitch * (sy1 - sy0);
     if (bp.nz <= 8 && L.dim[2] <= 24 && R < (1 << 15) && words * 4 <= kColPadMax &&
         std::getenv("BBS_ROOT_PAD") == nullptr) {
       st.enabled = 1;
       st.sx0 = static_cast<int32_t>(sx0);
       st.sy0 = static_cast<int32_t>(sy0);
-      st.pitch = static_cast<uint32_t>(sx1 - sx0);
+      st.pitch = static_cast<uint32_t>(pitch);
       st.rows = static_cast<uint32_t>(sy1 - sy0);
       st.zoff = bp.z0 - L.box_min[2];
       st.dimz = L.dim[2];
