@@ -466,9 +466,19 @@ int bbs_search(bbs_map_t map, const double* scan_xyz, uint64_t k, const bbs_sear
   return guard([&] {
     REQUIRE(map && cfg && result && (scan_xyz || k == 0), "null argument");
     if (k == 0) throw bbs::Error(BBS_ERR_DEGENERATE_SCAN, "search: empty scan");
+    const auto t0 = std::chrono::steady_clock::now();
     std::unique_ptr<bbs_scan> sc(bbs::upload_scan(map, scan_xyz, k, false));  // same stream as the search
+    const auto t1 = std::chrono::steady_clock::now();
     bbs::run_search(map, sc.get(), *cfg, nullptr, result);
     result->h2d_bytes += 3 * k * sizeof(double);
+    if (std::getenv("BBS_DEBUG_HOST")) {
+      sc.reset();
+      const auto t2 = std::chrono::steady_clock::now();
+      std::fprintf(stderr, "[host] bbs_search: upload %.1f us, search %.1f us, total (with scan free) %.1f us\n",
+                   std::chrono::duration<double, std::micro>(t1 - t0).count(),
+                   std::chrono::duration<double, std::micro>(t2 - t1).count(),
+                   std::chrono::duration<double, std::micro>(t2 - t0).count());
+    }
   });
 }
 

@@ -21,6 +21,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -1062,6 +1063,9 @@ struct Workspace {
   Buf<uint32_t> hist_amb, rinit_ctl;
   Buf<unsigned long long> rinit_tiles;
   unsigned long long rinit_tag = 0;
+  GridView lut_view;  // the rotation LUT in `lut`, built for lut_key
+  double lut_key[7] = {};
+  bool lut_valid = false;
   Buf<EpochState> st;
   EpochState* h_st = nullptr;
   cudaStream_t side = nullptr;            // prebuild stream (forked per search)
@@ -1083,6 +1087,7 @@ struct Workspace {
     for (auto* b : {&perm0, &perm1, &sk0, &sk1, &exp_parent, &exp_off, &hist_amb, &rinit_ctl}) b->release();
     rinit_tiles.release();
     lut.release();
+    lut_valid = false;
     nsel.release();
     temp.release();
     hist_ent.release();
@@ -1148,13 +1153,18 @@ bbs_scan* upload_scan(bbs_map* m, const double* xyz, uint64_t k, bool sync) {
   auto* sc = new bbs_scan();
   sc->map = m;
   sc->k = k;
-  sc->d_max = k ? host_max_range(xyz, k) : 0.0;
+  // one pass: max_range (point_cloud.hpp:58-63) as sqrt of the largest
+  // x*x + y*y + z*z (sqrt is correctly rounded and monotonic, so this is the
+  // max of the per-point ranges bit for bit), the z range and max |x| + |y|
+  double r2 = 0.0;
   for (uint64_t i = 0; i < k; ++i) {
     const double x = xyz[3 * i], y = xyz[3 * i + 1], z = xyz[3 * i + 2];
+    r2 = std::max(r2, x * x + y * y + z * z);
     sc->z_min = i ? std::min(sc->z_min, z) : z;
     sc->z_max = i ? std::max(sc->z_max, z) : z;
     sc->l1xy_max = std::max(sc->l1xy_max, std::fabs(x) + std::fabs(y));
   }
+  sc->d_max = std::sqrt(r2);
   cudaStream_t s = m->stream;
   sc->soa = dalloc<double>(3 * std::max<uint64_t>(k, 1), s);
   if (k) {
@@ -1261,15 +1271,37 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
     throw Error(BBS_ERR_TOO_LARGE, "search: root set too large");
 
   GridView gv;
-  const std::vector<double> lut = build_lut(grid, &gv);
-  double2* d_lut = W.lut.get(lut.size() / 2, s);
-  BBS_CUDA(cudaMemcpyAsync(d_lut, lut.data(), lut.size() * sizeof(double), cudaMemcpyHostToDevice, s));
-  gv.lut = d_lut;
+  // BBS_DEBUG_HOST: host-side timestamps of one search (stderr)
+  const bool dbg_host = std::getenv("BBS_DEBUG_HOST") != nullptr;
+  const auto th0 = std::chrono::steady_clock::now();
+  std::vector<std::pair<const char*, double>> th;
+  auto tmark = [&](const char* what) {
+    if (dbg_host)
+      th.emplace_back(what, std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - th0).count());
+  };
+  // the rotation LUT depends on make_grid's inputs only: a workspace keeps
+  // the last one on the device (sequential searches with one config skip the
+  // host libm pass and the copy)
+  const double lut_key[7] = {cfg.min_resolution, static_cast<double>(cfg.max_level), cfg.roll_pitch_half_range,
+                             cfg.yaw_min, cfg.yaw_max, static_cast<double>(cfg.branch_mode), d_max};
+  if (W.lut_valid && std::memcmp(W.lut_key, lut_key, sizeof(lut_key)) == 0) {
+    gv = W.lut_view;
+  } else {
+    W.lut_valid = false;
+    const std::vector<double> lut = build_lut(grid, &gv);
+    double2* d_lut = W.lut.get(lut.size() / 2, s);
+    BBS_CUDA(cudaMemcpyAsync(d_lut, lut.data(), lut.size() * sizeof(double), cudaMemcpyHostToDevice, s));
+    h2d += lut.size() * sizeof(double);
+    gv.lut = d_lut;
+    std::memcpy(W.lut_key, lut_key, sizeof(lut_key));
+    W.lut_view = gv;
+    W.lut_valid = true;
+  }
+  tmark("lut");
   const ScanView sv{scan->soa, scan->soa + K, scan->soa + 2 * K, static_cast<uint32_t>(K)};
   const uint64_t maxc = max_children(grid);
   const uint64_t pend_cap = cfg.batch_size + maxc;
   const int strategy = cfg.strategy;
-  h2d += lut.size() * sizeof(double);
   uint64_t launches = 0;
 
   cudaEvent_t ev_start = W.next_event(), ev_roots0 = W.next_event(), ev_roots1 = W.next_event(),
@@ -1383,6 +1415,7 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
     launches += 3 * ((nrot + kRotBatch - 1) / kRotBatch);
   }
   BBS_CUDA(cudaEventRecord(ev_roots1, s));
+  tmark("roots enqueued");
   cudaEvent_t ev_fork = W.next_event(), ev_prebuilt = W.next_event();
   bool prebuild_pending = false;
   // per-search (level, rotation) histogram cache for the flushes (epoch_cache.cu)
@@ -1798,6 +1831,7 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
     launches += 2;
   }
 
+  tmark("loop");
   while (self_active || others_active) {
     // capacity: the queue grows by at most pend_cap per epoch
     if (static_cast<uint64_t>(hs.q_len) + static_cast<uint64_t>(E + 1) * pend_cap > qcap) {
@@ -1897,6 +1931,7 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
   hs = *W.h_st;
   if (dev_init) root_probes = W.h_small[0];
 
+  tmark("state read");
   // ---- results ----
   std::memset(&out->stats, 0, sizeof(out->stats));
   out->scan_points = K;
@@ -1977,6 +2012,12 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
   }
   out->h2d_bytes = h2d;
   out->d2h_bytes = d2h;
+  if (dbg_host) {
+    tmark("results");
+    std::fprintf(stderr, "[host]");
+    for (const auto& m : th) std::fprintf(stderr, " %s %.1f", m.first, m.second);
+    std::fprintf(stderr, " us (device %.1f us)\n", 1e3 * out->device_ms);
+  }
   out->kernel_launches = launches;
   for (int l = 0; l < kMaxLevels; ++l) out->evals_per_level[l] = hs.level_evals[l];
   out->evals_per_level[L] += n_scored_roots;  // the root batch
