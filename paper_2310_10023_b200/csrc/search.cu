@@ -1153,6 +1153,17 @@ bbs_scan* upload_scan(bbs_map* m, const double* xyz, uint64_t k, bool sync) {
   auto* sc = new bbs_scan();
   sc->map = m;
   sc->k = k;
+  // the copy and the SoA transform go first: they run while the host scans
+  // the points below
+  cudaStream_t s = m->stream;
+  sc->soa = dalloc<double>(3 * std::max<uint64_t>(k, 1), s);
+  if (k) {
+    double* aos = dalloc<double>(3 * k, s);
+    BBS_CUDA(cudaMemcpyAsync(aos, xyz, 3 * k * sizeof(double), cudaMemcpyHostToDevice, s));
+    soa_kernel<<<grid1(k), 256, 0, s>>>(aos, k, sc->soa);
+    BBS_CUDA(cudaGetLastError());
+    BBS_CUDA(cudaFreeAsync(aos, s));
+  }
   // one pass: max_range (point_cloud.hpp:58-63) as sqrt of the largest
   // x*x + y*y + z*z (sqrt is correctly rounded and monotonic, so this is the
   // max of the per-point ranges bit for bit), the z range and max |x| + |y|
@@ -1165,15 +1176,6 @@ bbs_scan* upload_scan(bbs_map* m, const double* xyz, uint64_t k, bool sync) {
     sc->l1xy_max = std::max(sc->l1xy_max, std::fabs(x) + std::fabs(y));
   }
   sc->d_max = std::sqrt(r2);
-  cudaStream_t s = m->stream;
-  sc->soa = dalloc<double>(3 * std::max<uint64_t>(k, 1), s);
-  if (k) {
-    double* aos = dalloc<double>(3 * k, s);
-    BBS_CUDA(cudaMemcpyAsync(aos, xyz, 3 * k * sizeof(double), cudaMemcpyHostToDevice, s));
-    soa_kernel<<<grid1(k), 256, 0, s>>>(aos, k, sc->soa);
-    BBS_CUDA(cudaGetLastError());
-    BBS_CUDA(cudaFreeAsync(aos, s));
-  }
   if (sync) BBS_CUDA(cudaStreamSynchronize(s));  // callers on other streams see a complete scan
   return sc;
 }
