@@ -297,6 +297,18 @@ int bbs_stream_destroy(void* stream);
 int bbs_batch_evaluate_device(bbs_map_t map, bbs_scan_t scan, const bbs_search_config* cfg,
                               double d_max, bbs_node* d_nodes, uint64_t n, void* stream);
 
+/* oracle_search, oracle.hpp:29-95: every level-0 leaf under the root index
+ * ranges x the level-0 rotation grid, enumerated and scored on the device.
+ * best_score = the maximum (the reference's OracleResult::best_score);
+ * argmax receives the first argmax_capacity leaves attaining it, in the
+ * reference's enumeration order (their poses are node_pose(.).normalized(),
+ * see the facade); argmax_count is the full count; leaf_count the grid size.
+ * Errors as the reference: DEGENERATE_SCAN, CONFIG (r mismatch),
+ * EMPTY_SEARCH_SPACE, TOO_LARGE (> 1e8 leaves). */
+int bbs_oracle_search(bbs_map_t map, const double* scan_xyz, uint64_t k, const bbs_search_config* cfg,
+                      int32_t* best_score, bbs_node* argmax, uint64_t argmax_capacity,
+                      uint64_t* argmax_count, uint64_t* leaf_count);
+
 /* ---- multi-GPU ------------------------------------------ */
 /* Element-wise MAX all-reduce of `count` int64 values in place across all
  * ranks; returns 0 on success.  Supplied by the caller (NCCL / gloo). */

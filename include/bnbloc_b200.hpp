@@ -679,6 +679,41 @@ inline SearchResult localize_scan(const MultiResVoxelMap& map, const PointCloud&
   return detail::to_result(r, trace);
 }
 
+// ---- oracle.hpp:17-95, device-backed (bbs_oracle_search) ---------------------
+struct OracleResult {
+  int best_score = 0;
+  std::vector<Pose6> argmax_poses;  ///< every leaf attaining best_score
+  std::uint64_t leaf_count = 0;
+};
+
+inline constexpr std::uint64_t kOracleMaxLeaves = 100000000;  // 1e8 guard
+
+inline OracleResult oracle_search(const MultiResVoxelMap& map, const PointCloud& scan,
+                                  const SearchConfig& cfg) {
+  const bbs_search_config c = detail::to_c(cfg);
+  std::int32_t best = 0;
+  std::uint64_t count = 0, leaves = 0;
+  std::vector<bbs_node> nodes(1024);
+  detail::check(bbs_oracle_search(map.handle(), xyz(scan), scan.size(), &c, &best, nodes.data(),
+                                  nodes.size(), &count, &leaves));
+  if (count > nodes.size()) {  // retry with the full count
+    nodes.resize(count);
+    detail::check(bbs_oracle_search(map.handle(), xyz(scan), scan.size(), &c, &best, nodes.data(),
+                                    nodes.size(), &count, &leaves));
+  }
+  OracleResult out;
+  out.best_score = best;
+  out.leaf_count = leaves;
+  const AngularGrid grids(cfg, cfg.d_max ? *cfg.d_max : max_range(scan));
+  out.argmax_poses.reserve(count);
+  for (std::uint64_t i = 0; i < count; ++i) {
+    const bbs_node& b = nodes[i];
+    const Node n{b.ix, b.iy, b.iz, b.iroll, b.ipitch, b.iyaw, b.level, b.score};
+    out.argmax_poses.push_back(node_pose(n, grids, cfg.min_resolution).normalized());
+  }
+  return out;
+}
+
 }  // namespace bnbloc_b200
 
 #ifdef BNBLOC_B200_AS_BNBLOC

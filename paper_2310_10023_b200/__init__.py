@@ -639,6 +639,40 @@ def search(vmap: MultiResVoxelMap, scan, cfg: SearchConfig, trace_capacity=1 << 
     return _result_from_c(res, buf)
 
 
+ORACLE_MAX_LEAVES = 100_000_000  # kOracleMaxLeaves, oracle.hpp:25
+
+
+@dataclass
+class OracleResult:
+    """oracle.hpp:17-21 (plus the argmax leaves as (n, 8) int32 nodes)."""
+    best_score: int
+    argmax_poses: list
+    leaf_count: int
+    argmax_nodes: np.ndarray
+
+
+def oracle_search(vmap: MultiResVoxelMap, scan, cfg: SearchConfig, argmax_capacity=1024):
+    """oracle.hpp:29-95: every level-0 leaf under the root index ranges x the
+    level-0 rotation grid, enumerated and scored on the device (no pruning)."""
+    s = _xyz(scan)
+    c = cfg.to_c()
+    best, cnt, leaves = C.c_int32(), C.c_uint64(), C.c_uint64()
+    cap = max(int(argmax_capacity), 1)
+    while True:
+        buf = np.zeros((cap, 8), np.int32)
+        _check(lib.bbs_oracle_search(vmap._h, _dptr(s), s.shape[0], C.byref(c), C.byref(best),
+                                     buf.ctypes.data_as(C.POINTER(Node)), cap, C.byref(cnt),
+                                     C.byref(leaves)))
+        if cnt.value <= cap:
+            break
+        cap = cnt.value
+    nodes = buf[:cnt.value].copy()
+    d_max = cfg.d_max if cfg.d_max is not None else max_range(s)
+    grids = AngularGrid(cfg, d_max)
+    poses = [node_pose(n, grids, cfg.min_resolution).normalized() for n in nodes]
+    return OracleResult(int(best.value), poses, int(leaves.value), nodes)
+
+
 class DeviceStream:
     """A non-blocking CUDA stream owned by the library (concurrent searches)."""
 

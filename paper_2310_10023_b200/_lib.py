@@ -64,6 +64,8 @@ SIGNATURES = {
     "bbs_batch_evaluate": (C.c_int, [_vp, _dp, _u64, C.POINTER(SearchConfigC), _d,
                                      C.POINTER(Node), _u64]),
     "bbs_search": (C.c_int, [_vp, _dp, _u64, C.POINTER(SearchConfigC), C.POINTER(SearchResultC)]),
+    "bbs_oracle_search": (C.c_int, [_vp, _dp, _u64, C.POINTER(SearchConfigC), _ip,
+                                    C.POINTER(Node), _u64, C.POINTER(_u64), C.POINTER(_u64)]),
     "bbs_localize_scan": (C.c_int, [_vp, _dp, _u64, C.POINTER(SearchConfigC), _u64,
                                     C.POINTER(SearchResultC)]),
     "bbs_scan_upload": (C.c_int, [_vp, _dp, _u64, C.POINTER(_vp)]),

@@ -63,6 +63,20 @@ void level_score_transform(bbs_map* m, int level, const double* R, const double*
 // sync = false: the caller uses the scan on the map's stream only.
 bbs_scan* upload_scan(bbs_map* m, const double* xyz, uint64_t k, bool sync = true);
 
+// oracle_search's level-0 leaf grid (oracle.hpp:39-54): translation index
+// ranges [lo, lo + n) at level 0 and the level-0 rotation index counts.
+struct LeafGridSpec {
+  int64_t x_lo = 0, y_lo = 0, z_lo = 0;
+  uint64_t nx = 0, ny = 0, nz = 0, nr = 0, np = 0, nw = 0;
+  uint64_t total() const { return nx * ny * nz * (nr * np * nw); }
+};
+// leaf_grid.cu: score every leaf in blocks of `block`; best score (-1 if
+// none), the nodes attaining it in enumeration order (first `capacity`) and
+// their full count.
+void leaf_grid_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, double d_max,
+                      const LeafGridSpec& g, uint64_t block, int32_t* best_score, bbs_node* argmax,
+                      uint64_t capacity, uint64_t* count);
+
 struct DeviceGuard {
   int prev = 0;
   explicit DeviceGuard(int dev);

@@ -7,6 +7,7 @@
 #include <atomic>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <exception>
 #include <limits>
@@ -554,6 +555,53 @@ int bbs_batch_evaluate_device(bbs_map_t map, bbs_scan_t scan, const bbs_search_c
     bbs::DeviceGuard g(map->device);
     cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : map->stream;
     bbs::batch_evaluate_device(map, scan, *cfg, d_max, d_nodes, n, s, nullptr, nullptr);
+  });
+}
+
+int bbs_oracle_search(bbs_map_t map, const double* scan_xyz, uint64_t k, const bbs_search_config* cfg,
+                      int32_t* best_score, bbs_node* argmax, uint64_t argmax_capacity,
+                      uint64_t* argmax_count, uint64_t* leaf_count) {
+  return guard([&] {
+    REQUIRE(map && cfg && best_score && argmax_count && leaf_count && (scan_xyz || k == 0) &&
+                (argmax || argmax_capacity == 0),
+            "null argument");
+    // oracle.hpp:31-35, same order and messages
+    if (k == 0) throw bbs::Error(BBS_ERR_DEGENERATE_SCAN, "oracle_search: empty scan");
+    if (map->r != cfg->min_resolution)
+      throw bbs::Error(BBS_ERR_CONFIG, "oracle_search: config r does not match the map");
+    std::unique_ptr<bbs_scan> sc(bbs::upload_scan(map, scan_xyz, k, false));
+    const double d_max = cfg->has_d_max ? cfg->d_max : sc->d_max;
+    if (!(d_max > 0.0)) throw bbs::Error(BBS_ERR_DEGENERATE_SCAN, "oracle_search: zero scan range");
+    const bbs::HostGrid grids = bbs::make_grid(*cfg, d_max);  // AngularGrid(cfg, d_max), :37
+    const bbs_aabb range = cfg->has_translation_range ? cfg->translation_range : map->bbox;
+    const double root_cell = std::ldexp(cfg->min_resolution, cfg->max_level);
+    const int64_t scale = int64_t{1} << cfg->max_level;
+    // trans_index_range (nodes.hpp:53-56): int32 floor / ceil of w / cell
+    auto tir = [&](double lo, double hi, int64_t* a, int64_t* b) {
+      *a = static_cast<int32_t>(std::floor(lo / root_cell)) * scale;
+      *b = (static_cast<int64_t>(static_cast<int32_t>(std::ceil(hi / root_cell))) + 1) * scale;
+    };
+    bbs::LeafGridSpec g;
+    int64_t xh, yh, zh;
+    tir(range.min.x, range.max.x, &g.x_lo, &xh);
+    tir(range.min.y, range.max.y, &g.y_lo, &yh);
+    tir(range.min.z, range.max.z, &g.z_lo, &zh);
+    g.nx = static_cast<uint64_t>(xh - g.x_lo);
+    g.ny = static_cast<uint64_t>(yh - g.y_lo);
+    g.nz = static_cast<uint64_t>(zh - g.z_lo);
+    g.nr = static_cast<uint64_t>(grids.axis(0, 0).index_count());
+    g.np = static_cast<uint64_t>(grids.axis(1, 0).index_count());
+    g.nw = static_cast<uint64_t>(grids.axis(2, 0).index_count());
+    const uint64_t total = g.total();
+    if (total == 0) throw bbs::Error(BBS_ERR_EMPTY_SEARCH_SPACE, "oracle_search: empty leaf grid");
+    if (total > 100000000ull)  // kOracleMaxLeaves, oracle.hpp:25
+      throw bbs::Error(BBS_ERR_TOO_LARGE, "oracle_search: leaf grid of " + std::to_string(total) +
+                                              " nodes exceeds the 1e8 guard");
+    *leaf_count = total;
+    const char* eb = std::getenv("BBS_LEAF_BLOCK");
+    const uint64_t block = eb ? std::strtoull(eb, nullptr, 10) : (uint64_t{1} << 20);
+    bbs::leaf_grid_search(map, sc.get(), *cfg, d_max, g, block, best_score, argmax, argmax_capacity,
+                          argmax_count);
   });
 }
 

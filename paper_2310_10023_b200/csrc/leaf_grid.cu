@@ -1,0 +1,140 @@
+// leaf_grid.cu — exhaustive leaf-grid scoring on the device: the reference's
+// `oracle_search` (oracle.hpp:29-95), SURVEY §8f row 4.  Every level-0 node
+// under the root translation index ranges times the level-0 rotation grid is
+// enumerated ON THE DEVICE in the reference's loop order (ix, iy, iz, ir, ip,
+// iw; oracle.hpp:80-92), scored by the same batch_evaluate kernels the search
+// uses (bit-exact per node), and reduced per block: block max, then an
+// order-preserving select of the nodes attaining the running best (the
+// reference's drain lambda, oracle.hpp:66-77).  Only the block max (4 B) and
+// the argmax nodes cross PCIe.  Host validation lives in capi.cpp
+// (bbs_oracle_search), in the reference's order.
+#include <cuda_runtime.h>
+
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cstdint>
+#include <cstring>
+
+#include "bbs_map_impl.h"
+
+namespace bbs {
+
+void batch_evaluate_device(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, double d_max,
+                           bbs_node* d_nodes, uint64_t n, cudaStream_t s, const int32_t* lo,
+                           const int32_t* hi);
+
+namespace {
+
+// leaf index q -> node, iw fastest (oracle.hpp:80-92)
+__global__ void leaf_nodes_kernel(LeafGridSpec g, uint64_t first, uint64_t n,
+                                  bbs_node* __restrict__ out) {
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
+       i += uint64_t(gridDim.x) * blockDim.x) {
+    uint64_t q = first + i;
+    const uint64_t iw = q % g.nw;
+    q /= g.nw;
+    const uint64_t ip = q % g.np;
+    q /= g.np;
+    const uint64_t ir = q % g.nr;
+    q /= g.nr;
+    const uint64_t iz = q % g.nz;
+    q /= g.nz;
+    const uint64_t iy = q % g.ny;
+    q /= g.ny;
+    bbs_node nd;
+    nd.ix = static_cast<int32_t>(g.x_lo + static_cast<int64_t>(q));
+    nd.iy = static_cast<int32_t>(g.y_lo + static_cast<int64_t>(iy));
+    nd.iz = static_cast<int32_t>(g.z_lo + static_cast<int64_t>(iz));
+    nd.iroll = static_cast<int32_t>(ir);
+    nd.ipitch = static_cast<int32_t>(ip);
+    nd.iyaw = static_cast<int32_t>(iw);
+    nd.level = 0;
+    nd.score = -1;
+    out[i] = nd;
+  }
+}
+
+__global__ void block_max_kernel(const bbs_node* __restrict__ nodes, uint64_t n,
+                                 int32_t* __restrict__ out) {
+  int32_t m = -1;
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
+       i += uint64_t(gridDim.x) * blockDim.x)
+    m = max(m, nodes[i].score);
+  m = __reduce_max_sync(0xffffffffu, m);
+  if ((threadIdx.x & 31) == 0) atomicMax(out, m);
+}
+
+struct ScoreIs {
+  int32_t v;
+  __device__ __forceinline__ bool operator()(const bbs_node& a) const { return a.score == v; }
+};
+
+unsigned grid_for(uint64_t n) {
+  return static_cast<unsigned>(std::min<uint64_t>(std::max<uint64_t>((n + 255) / 256, 1), 148ull * 16));
+}
+
+}  // namespace
+
+void leaf_grid_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, double d_max,
+                      const LeafGridSpec& g, uint64_t block, int32_t* best_score, bbs_node* argmax,
+                      uint64_t capacity, uint64_t* count) {
+  DeviceGuard dg(m->device);
+  cudaStream_t s = m->stream;
+  const uint64_t total = g.total();
+  block = std::max<uint64_t>(1, std::min(block, total));
+  bbs_node *d_nodes = nullptr, *d_sel = nullptr;
+  int32_t* d_small = nullptr;  // [0] block max, [1..2] selected count (int64 via two words)
+  void* d_tmp = nullptr;
+  size_t tmp_bytes = 0;
+  BBS_CUDA(cub::DeviceSelect::If(nullptr, tmp_bytes, d_nodes, d_sel,
+                                 reinterpret_cast<unsigned long long*>(d_small), block, ScoreIs{0}, s));
+  BBS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_nodes), block * sizeof(bbs_node), s));
+  BBS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_sel), block * sizeof(bbs_node), s));
+  BBS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_small), 16, s));
+  BBS_CUDA(cudaMallocAsync(&d_tmp, std::max<size_t>(tmp_bytes, 16), s));
+  int32_t* h_small = nullptr;
+  BBS_CUDA(cudaMallocHost(reinterpret_cast<void**>(&h_small), 16));
+  unsigned long long* d_nsel = reinterpret_cast<unsigned long long*>(d_small + 2);
+  int32_t best = -1;
+  uint64_t cnt = 0;
+  for (uint64_t first = 0; first < total; first += block) {
+    const uint64_t n = std::min(block, total - first);
+    leaf_nodes_kernel<<<grid_for(n), 256, 0, s>>>(g, first, n, d_nodes);
+    BBS_CUDA(cudaGetLastError());
+    batch_evaluate_device(m, scan, cfg, d_max, d_nodes, n, s, nullptr, nullptr);
+    BBS_CUDA(cudaMemsetAsync(d_small, 0xff, 4, s));  // -1: the reference's initial best
+    block_max_kernel<<<grid_for(n), 256, 0, s>>>(d_nodes, n, d_small);
+    BBS_CUDA(cudaGetLastError());
+    BBS_CUDA(cudaMemcpyAsync(h_small, d_small, 4, cudaMemcpyDeviceToHost, s));
+    BBS_CUDA(cudaStreamSynchronize(s));
+    const int32_t bm = h_small[0];
+    if (bm > best) {  // oracle.hpp:70-73
+      best = bm;
+      cnt = 0;
+    }
+    if (bm != best) continue;
+    size_t tb = tmp_bytes;
+    BBS_CUDA(cub::DeviceSelect::If(d_tmp, tb, d_nodes, d_sel, d_nsel, n, ScoreIs{best}, s));
+    BBS_CUDA(cudaMemcpyAsync(h_small + 2, d_nsel, 8, cudaMemcpyDeviceToHost, s));
+    BBS_CUDA(cudaStreamSynchronize(s));
+    uint64_t nsel = 0;
+    std::memcpy(&nsel, h_small + 2, 8);
+    if (cnt < capacity && nsel) {
+      const uint64_t take = std::min(nsel, capacity - cnt);
+      BBS_CUDA(cudaMemcpyAsync(argmax + cnt, d_sel, take * sizeof(bbs_node), cudaMemcpyDeviceToHost, s));
+      BBS_CUDA(cudaStreamSynchronize(s));
+    }
+    cnt += nsel;
+  }
+  BBS_CUDA(cudaFreeAsync(d_nodes, s));
+  BBS_CUDA(cudaFreeAsync(d_sel, s));
+  BBS_CUDA(cudaFreeAsync(d_small, s));
+  BBS_CUDA(cudaFreeAsync(d_tmp, s));
+  BBS_CUDA(cudaStreamSynchronize(s));
+  BBS_CUDA(cudaFreeHost(h_small));
+  *best_score = best;
+  *count = cnt;
+}
+
+}  // namespace bbs
