@@ -2,7 +2,9 @@
 search_test.cpp, angular_grid_test.cpp), compiled unmodified against the
 B200 facade (include/bnbloc_b200.hpp) by tests/cpp/Makefile, run on the GPU.
 Every map build, membership probe, score, batch_evaluate and search they
-perform goes through libbbs_b200.so."""
+perform goes through libbbs_b200.so.  oracle_facade_test is our own
+(tests/cpp/oracle_facade_test.cpp): harness_test.cpp's Oracle cases through
+the facade's device-backed oracle_search."""
 import os
 import subprocess
 
@@ -15,7 +17,7 @@ BIN = os.path.join(ROOT, "tests", "cpp", "bin")
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("suite", ["voxel_map_test", "search_test", "angular_grid_test",
-                                   "map_io_test"])
+                                   "map_io_test", "oracle_facade_test"])
 def test_reference_suite_passes_on_device(suite):
     exe = os.path.join(BIN, suite)
     if not os.path.exists(exe):
