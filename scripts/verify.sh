@@ -1,5 +1,6 @@
-mkdir -p gpurun_out/r1c
-O=gpurun_out/r1c
+TAG=${TAG:-r1c}
+mkdir -p gpurun_out/$TAG
+O=gpurun_out/$TAG
 timeout 900 python -m pytest tests -m gpu -q -x > $O/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $O/pytest_gpu.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > $O/smoke.log 2>&1; echo "smoke rc=$?" >> $O/smoke.log
 timeout 600 python bench.py > $O/bench_c2.json 2> $O/bench_c2.err
