@@ -83,18 +83,33 @@ void leaf_grid_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, 
   cudaStream_t s = m->stream;
   const uint64_t total = g.total();
   block = std::max<uint64_t>(1, std::min(block, total));
-  bbs_node *d_nodes = nullptr, *d_sel = nullptr;
-  int32_t* d_small = nullptr;  // [0] block max, [1..2] selected count (int64 via two words)
-  void* d_tmp = nullptr;
+  // buffers released on every exit path (BBS_CUDA throws)
+  struct Bufs {
+    cudaStream_t s;
+    bbs_node *nodes = nullptr, *sel = nullptr;
+    int32_t* small = nullptr;  // [0] block max, [2..3] selected count (u64)
+    void* tmp = nullptr;
+    int32_t* host = nullptr;
+    ~Bufs() {
+      for (void* p : {static_cast<void*>(nodes), static_cast<void*>(sel), static_cast<void*>(small), tmp})
+        if (p) cudaFreeAsync(p, s);
+      cudaStreamSynchronize(s);
+      if (host) cudaFreeHost(host);
+    }
+  } bufs{s};
   size_t tmp_bytes = 0;
-  BBS_CUDA(cub::DeviceSelect::If(nullptr, tmp_bytes, d_nodes, d_sel,
-                                 reinterpret_cast<unsigned long long*>(d_small), block, ScoreIs{0}, s));
-  BBS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_nodes), block * sizeof(bbs_node), s));
-  BBS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_sel), block * sizeof(bbs_node), s));
-  BBS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_small), 16, s));
-  BBS_CUDA(cudaMallocAsync(&d_tmp, std::max<size_t>(tmp_bytes, 16), s));
-  int32_t* h_small = nullptr;
-  BBS_CUDA(cudaMallocHost(reinterpret_cast<void**>(&h_small), 16));
+  BBS_CUDA(cub::DeviceSelect::If(nullptr, tmp_bytes, bufs.nodes, bufs.sel,
+                                 reinterpret_cast<unsigned long long*>(bufs.small), block, ScoreIs{0}, s));
+  BBS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&bufs.nodes), block * sizeof(bbs_node), s));
+  BBS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&bufs.sel), block * sizeof(bbs_node), s));
+  BBS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&bufs.small), 16, s));
+  BBS_CUDA(cudaMallocAsync(&bufs.tmp, std::max<size_t>(tmp_bytes, 16), s));
+  BBS_CUDA(cudaMallocHost(reinterpret_cast<void**>(&bufs.host), 16));
+  bbs_node* const d_nodes = bufs.nodes;
+  bbs_node* const d_sel = bufs.sel;
+  int32_t* const d_small = bufs.small;
+  void* const d_tmp = bufs.tmp;
+  int32_t* const h_small = bufs.host;
   unsigned long long* d_nsel = reinterpret_cast<unsigned long long*>(d_small + 2);
   int32_t best = -1;
   uint64_t cnt = 0;
@@ -127,12 +142,6 @@ void leaf_grid_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, 
     }
     cnt += nsel;
   }
-  BBS_CUDA(cudaFreeAsync(d_nodes, s));
-  BBS_CUDA(cudaFreeAsync(d_sel, s));
-  BBS_CUDA(cudaFreeAsync(d_small, s));
-  BBS_CUDA(cudaFreeAsync(d_tmp, s));
-  BBS_CUDA(cudaStreamSynchronize(s));
-  BBS_CUDA(cudaFreeHost(h_small));
   *best_score = best;
   *count = cnt;
 }
