@@ -36,6 +36,7 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+import harness as H  # noqa: E402  (synthetic inputs)
 
 CONFIGS = {
     # name: scene spec, seed, search params, K
@@ -183,10 +184,10 @@ class ClockSampler:
 
 
 def build_inputs(B, cfgd):
-    spec = B.SceneSpec.default(**cfgd["spec"])
+    spec = H.SceneSpec.default(**cfgd["spec"])
     t = time.time()
-    map_pts, raw_scan, gt = B.gen_scene(spec, cfgd["seed"])
-    scan = B.cut_scan(raw_scan, min(cfgd["K"], raw_scan.shape[0]), 7)
+    map_pts, raw_scan, gt = H.gen_scene(spec, cfgd["seed"])
+    scan = H.cut_scan(raw_scan, min(cfgd["K"], raw_scan.shape[0]), 7)
     log(f"scene: {map_pts.shape[0]} map pts, raw scan {raw_scan.shape[0]}, K={scan.shape[0]} "
         f"({time.time() - t:.1f}s)")
     return map_pts, scan, gt
@@ -508,11 +509,11 @@ def run_b200_throughput(args, cfgd):
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     import paper_2310_10023_b200 as B
-    spec = B.SceneSpec.default(**cfgd["spec"])
+    spec = H.SceneSpec.default(**cfgd["spec"])
     t = time.time()
-    map_pts, _, _ = B.gen_scene(spec, cfgd["seed"])
-    scans, poses = B.gen_scans(spec, cfgd["seed"], 1000, cfgd["n_scans"])
-    scans = [B.cut_scan(s, min(cfgd["K"], s.shape[0]), 7) for s in scans]
+    map_pts, _, _ = H.gen_scene(spec, cfgd["seed"])
+    scans, poses = H.gen_scans(spec, cfgd["seed"], 1000, cfgd["n_scans"])
+    scans = [H.cut_scan(s, min(cfgd["K"], s.shape[0]), 7) for s in scans]
     log(f"scene + {len(scans)} scans: {time.time() - t:.1f}s")
     mine = [j for j in range(len(scans)) if j % world == rank]
     cfg = search_config(B, cfgd)

@@ -1,9 +1,9 @@
-// scene.cpp — synthetic-input harness (NOT part of the matcher path).
+// harness/scene.cpp — synthetic-input harness (NOT the product library).
 //
 // Restates the reference's box-world generator gen_scene (scene.hpp:156-220)
 // and its splitmix64 Rng (rng.hpp:11-38) so the benchmark and the GPU tests
 // can build the SAME doubles the reference consumes without shipping the
-// reference (tests/test_scene.py checks bit-identity against oracle/_ref).
+// reference (tests/test_host.py checks bit-identity against oracle/_ref).
 // Also: a seeded Fisher-Yates prefix to cut a scan to exactly K points
 // and the C4 helper that renders extra scans of one map.
 #include <algorithm>
@@ -16,7 +16,7 @@
 #include <unordered_map>
 #include <vector>
 
-#include "bbs_internal.h"
+#include "scene.h"
 
 namespace {
 
@@ -166,7 +166,7 @@ struct Layout {
 };
 
 // layout part of gen_scene, scene.hpp:161-180.
-Layout make_layout(const bbs_scene_spec& s, Rng& rng) {
+Layout make_layout(const hs_scene_spec& s, Rng& rng) {
   Layout L;
   L.surfaces.push_back({{0, 0, 0}, {s.size_x, 0, 0}, {0, s.size_y, 0}});
   const double max_h = 0.9 * s.size_z;
@@ -184,7 +184,7 @@ Layout make_layout(const bbs_scene_spec& s, Rng& rng) {
 }
 
 // pose attempts, scene.hpp:192-216.  Returns false when infeasible.
-bool place_scan(const bbs_scene_spec& s, const Layout& L, const std::vector<P3>& map_cloud,
+bool place_scan(const hs_scene_spec& s, const Layout& L, const std::vector<P3>& map_cloud,
                 const std::vector<P3>& world_scan, Rng& rng, const NeighborGrid* grid_in,
                 std::vector<P3>& scan, double* gt6) {
   std::unique_ptr<NeighborGrid> own;
@@ -242,7 +242,7 @@ double* to_buf(const std::vector<P3>& v) {
 
 extern "C" {
 
-void bbs_scene_spec_default(bbs_scene_spec* s) {  // SceneSpec defaults, scene.hpp:21-38
+void hs_scene_spec_default(hs_scene_spec* s) {  // SceneSpec defaults, scene.hpp:21-38
   s->size_x = 64.0;
   s->size_y = 64.0;
   s->size_z = 16.0;
@@ -261,15 +261,15 @@ void bbs_scene_spec_default(bbs_scene_spec* s) {  // SceneSpec defaults, scene.h
   s->feasibility_resolution = 1.0;
 }
 
-void bbs_free(void* p) { std::free(p); }
+void hs_free(void* p) { std::free(p); }
 
 // gen_scene, scene.hpp:156-220.
-int bbs_gen_scene(const bbs_scene_spec* s, uint64_t seed, double** map_xyz, uint64_t* n_map,
+int hs_gen_scene(const hs_scene_spec* s, uint64_t seed, double** map_xyz, uint64_t* n_map,
                   double** scan_xyz, uint64_t* n_scan, double* gt6) {
-  if (!s || !map_xyz || !n_map || !scan_xyz || !n_scan || !gt6) return BBS_ERR_INVALID_ARGUMENT;
+  if (!s || !map_xyz || !n_map || !scan_xyz || !n_scan || !gt6) return 14;
   if (!(s->size_x > 0 && s->size_y > 0 && s->size_z > 0)) {
     g_scene_err = "gen_scene: dimensions must be positive";
-    return BBS_ERR_CONFIG;
+    return 12;
   }
   Rng rng(seed * 0x9E3779B97F4A7C15ULL + 1);
   const Layout L = make_layout(*s, rng);
@@ -278,22 +278,22 @@ int bbs_gen_scene(const bbs_scene_spec* s, uint64_t seed, double** map_xyz, uint
   for (const auto& r : L.surfaces) sample_rect(r, s->scan_spacing, s->point_jitter, rng, world_scan);
   if (!place_scan(*s, L, map_cloud, world_scan, rng, nullptr, scan, gt6)) {
     g_scene_err = "gen_scene: no feasible pose found in 64 attempts (seed " + std::to_string(seed) + ")";
-    return BBS_ERR_INFEASIBLE_POSE;
+    return 11;
   }
   *map_xyz = to_buf(map_cloud);
   *n_map = map_cloud.size();
   *scan_xyz = to_buf(scan);
   *n_scan = scan.size();
-  return BBS_OK;
+  return 0;
 }
 
 // C4 helper: replay seed's layout and map, then render
 // n_scans scans with poses drawn from Rng(pose_seed_base + j) under the same
 // feasibility rules.  Scans are concatenated; offsets[j] is scan j's first
 // point (n_scans + 1 entries); gt is 6 * n_scans doubles.
-int bbs_gen_scans(const bbs_scene_spec* s, uint64_t seed, uint64_t pose_seed_base, int32_t n_scans,
+int hs_gen_scans(const hs_scene_spec* s, uint64_t seed, uint64_t pose_seed_base, int32_t n_scans,
                   double** scan_xyz, uint64_t* offsets, double* gt) {
-  if (!s || !scan_xyz || !offsets || !gt || n_scans < 0) return BBS_ERR_INVALID_ARGUMENT;
+  if (!s || !scan_xyz || !offsets || !gt || n_scans < 0) return 14;
   Rng rng(seed * 0x9E3779B97F4A7C15ULL + 1);
   const Layout L = make_layout(*s, rng);
   std::vector<P3> map_cloud, world_scan, scan, all;
@@ -305,19 +305,19 @@ int bbs_gen_scans(const bbs_scene_spec* s, uint64_t seed, uint64_t pose_seed_bas
     Rng prng(pose_seed_base + static_cast<uint64_t>(j));
     if (!place_scan(*s, L, map_cloud, world_scan, prng, &grid, scan, gt + 6 * j)) {
       g_scene_err = "gen_scans: no feasible pose for scan " + std::to_string(j);
-      return BBS_ERR_INFEASIBLE_POSE;
+      return 11;
     }
     all.insert(all.end(), scan.begin(), scan.end());
     offsets[j + 1] = all.size();
   }
   *scan_xyz = to_buf(all);
-  return BBS_OK;
+  return 0;
 }
 
 // Seeded Fisher-Yates prefix: the first k points of a uniform shuffle
 // driven by Rng(seed) (SURVEY §8d "cut to exactly K points").
-int bbs_cut_scan(const double* xyz, uint64_t n, uint64_t k, uint64_t seed, double* out) {
-  if (!xyz || !out || k > n) return BBS_ERR_INVALID_ARGUMENT;
+int hs_cut_scan(const double* xyz, uint64_t n, uint64_t k, uint64_t seed, double* out) {
+  if (!xyz || !out || k > n) return 14;
   std::vector<uint64_t> idx(n);
   for (uint64_t i = 0; i < n; ++i) idx[i] = i;
   Rng rng(seed);
@@ -328,9 +328,9 @@ int bbs_cut_scan(const double* xyz, uint64_t n, uint64_t k, uint64_t seed, doubl
     out[3 * i + 1] = xyz[3 * idx[i] + 1];
     out[3 * i + 2] = xyz[3 * idx[i] + 2];
   }
-  return BBS_OK;
+  return 0;
 }
 
-const char* bbs_scene_last_error(void) { return g_scene_err.c_str(); }
+const char* hs_last_error(void) { return g_scene_err.c_str(); }
 
 }  // extern "C"

@@ -33,7 +33,7 @@
 extern "C" {
 #endif
 
-#define BBS_ABI_VERSION 3
+#define BBS_ABI_VERSION 4
 
 /* Status codes, 1:1 with the exception classes of errors.hpp:11-98. */
 typedef enum bbs_status {
@@ -361,30 +361,37 @@ typedef struct bbs_shard {
 int bbs_search_sharded(bbs_map_t map, bbs_scan_t scan, const bbs_search_config* cfg,
                        const bbs_shard* shard, bbs_search_result* result);
 
-/* ---- synthetic-input harness (not part of the matcher path) ----------- */
-/* SceneSpec, scene.hpp:21-38. */
-typedef struct bbs_scene_spec {
-  double size_x, size_y, size_z;
-  int32_t num_boxes;
-  double min_box_side, max_box_side, min_box_height;
-  double map_spacing, scan_spacing, scan_range, point_jitter;
-  int32_t tilt_noise;
-  double gt_yaw_min, gt_yaw_max;
-  uint64_t min_scan_points;
-  double feasibility_resolution;
-} bbs_scene_spec;
-void bbs_scene_spec_default(bbs_scene_spec* spec);
-/* gen_scene, scene.hpp:156-220 (bit-identical restatement).  Buffers are
- * malloc'ed; release with bbs_free.  gt6 = x, y, z, roll, pitch, yaw. */
-int bbs_gen_scene(const bbs_scene_spec* spec, uint64_t seed, double** map_xyz, uint64_t* n_map,
-                  double** scan_xyz, uint64_t* n_scan, double* gt6);
-/* Extra scans of seed's map (poses from Rng(pose_seed_base + j)). */
-int bbs_gen_scans(const bbs_scene_spec* spec, uint64_t seed, uint64_t pose_seed_base,
-                  int32_t n_scans, double** scan_xyz, uint64_t* offsets, double* gt);
-/* First k points of a Fisher-Yates shuffle driven by Rng(seed). */
-int bbs_cut_scan(const double* xyz, uint64_t n, uint64_t k, uint64_t seed, double* out);
-const char* bbs_scene_last_error(void);
-void bbs_free(void* p);
+/* ---- parity instrumentation ------------------------------------------ */
+/* What the device scored inside one search(), for per-candidate parity
+ * against the reference's batch_evaluate (search.hpp:23-34): the root batch
+ * (search.hpp:111-124) and the flushed batches (search.hpp:132-143).
+ * Buffers are caller-owned host memory; *_count receive the full counts even
+ * when they exceed the capacities (only the first capacity entries are
+ * written). */
+typedef struct bbs_search_dump {
+  /* 1: the root kernel runs without its survivor-bound early exit, so every
+   * root score is the full hit count (default 0: roots that provably cannot
+   * reach the threshold stop early and keep a partial count below it). */
+  int32_t exact_roots;
+  /* dump the flush batches of epochs e with e % epoch_stride == 0 (0 = 1) */
+  uint32_t epoch_stride;
+  int32_t* root_scores;        /* initial_nodes() order (nodes.hpp:77-83) */
+  uint64_t root_capacity;
+  uint64_t root_count;
+  bbs_node* flush_nodes;       /* pending batches in the reference's order */
+  int32_t* flush_scores;       /* their device scores */
+  uint64_t flush_capacity;
+  uint64_t flush_count;
+  uint64_t* epoch_offsets;     /* batch i = [epoch_offsets[i], epoch_offsets[i+1]) */
+  uint32_t* epoch_ids;         /* flush index (0-based, roots excluded) of batch i */
+  uint64_t epoch_capacity;     /* entries of epoch_ids; epoch_offsets holds +1 */
+  uint64_t epoch_count;
+} bbs_search_dump;
+/* search_scan with the dump above: one epoch per host check, no CUDA graphs,
+ * the flush batches copied out after each epoch.  Results (score, pose,
+ * Stats, trace) are the same as bbs_search_scan's. */
+int bbs_search_scan_dump(bbs_map_t map, bbs_scan_t scan, const bbs_search_config* cfg,
+                         bbs_search_dump* dump, bbs_search_result* result);
 
 /* ---- measurement ------------------------------------------------------ */
 /* Random independent 32-byte gather ceiling over a `bytes` buffer on

@@ -107,6 +107,21 @@ class Reference:
         self.lib.ref_free(sp)
         return m, s, tuple(gt)
 
+    def gen_scans(self, spec, seed, pose_seed_base, n_scans):
+        """C4 harness helper (ref_gen_scans): seed's map layout, n_scans scans
+        with poses from Rng(pose_seed_base + j).  Returns (list of (n,3)
+        scans, list of gt 6-tuples)."""
+        sp = _dp()
+        offs = (C.c_uint64 * (n_scans + 1))()
+        gt = (C.c_double * (6 * max(n_scans, 1)))()
+        self._check(self.lib.ref_gen_scans(C.byref(spec), C.c_uint64(seed),
+                                           C.c_uint64(pose_seed_base), C.c_int32(n_scans),
+                                           C.byref(sp), offs, gt))
+        allp = np.ctypeslib.as_array(sp, shape=(max(offs[n_scans], 1), 3)).copy()
+        self.lib.ref_free(sp)
+        scans = [allp[offs[j]:offs[j + 1]].copy() for j in range(n_scans)]
+        return scans, [tuple(gt[6 * j:6 * j + 6]) for j in range(n_scans)]
+
     def map_build(self, pts, r, max_level, collision_target=0.001, cap=2 << 30):
         pts = _xyz(pts)
         h = C.c_void_p()

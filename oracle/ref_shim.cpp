@@ -173,6 +173,88 @@ int ref_gen_scene(const ref_scene_spec* s, uint64_t seed, double** map_xyz, uint
   });
 }
 
+// C4 harness helper (SURVEY §8d "C4 throughput"): the reference cannot render
+// several scans of one map (layout, map, scan samples and gt share one Rng
+// stream, scene.hpp:159-216).  This replays gen_scene's layout and surface
+// sampling for `seed` with the reference's OWN detail:: functions
+// (scene.hpp:50-97), then places n_scans sensors with poses drawn from
+// Rng(pose_seed_base + j) under gen_scene's feasibility rules
+// (scene.hpp:192-216; the overlap test is scene_overlap_fraction,
+// scene.hpp:143-150, over one NeighborGrid built once).  Scans are
+// concatenated (offsets[j] = first point of scan j, n_scans + 1 entries);
+// gt is 6 * n_scans doubles.  Buffer malloc'ed; free with ref_free.
+int ref_gen_scans(const ref_scene_spec* s, uint64_t seed, uint64_t pose_seed_base, int32_t n_scans,
+                  double** scan_xyz, uint64_t* offsets, double* gt) {
+  return guard([&] {
+    namespace D = bnbloc::detail;
+    bnbloc::Rng rng(seed * 0x9E3779B97F4A7C15ULL + 1);
+    std::vector<D::Rect> surfaces;
+    surfaces.push_back({{0, 0, 0}, {s->size_x, 0, 0}, {0, s->size_y, 0}});
+    std::vector<D::Box> boxes;
+    const double max_h = 0.9 * s->size_z;
+    for (int i = 0; i < s->num_boxes; ++i) {
+      const double w = std::min(rng.uniform(s->min_box_side, s->max_box_side), s->size_x - 2.5);
+      const double d = std::min(rng.uniform(s->min_box_side, s->max_box_side), s->size_y - 2.5);
+      const double h = rng.uniform(std::min(s->min_box_height, max_h), max_h);
+      const double x0 = rng.uniform(1.0, std::max(1.0 + 1e-6, s->size_x - w - 1.0));
+      const double y0 = rng.uniform(1.0, std::max(1.0 + 1e-6, s->size_y - d - 1.0));
+      const D::Box b{x0, y0, x0 + w, y0 + d, h};
+      boxes.push_back(b);
+      for (const auto& f : D::box_faces(b)) surfaces.push_back(f);
+    }
+    bnbloc::PointCloud map_cloud, world_scan;
+    for (const auto& r : surfaces) D::sample_rect(r, s->map_spacing, s->point_jitter, rng, map_cloud);
+    for (const auto& r : surfaces) D::sample_rect(r, s->scan_spacing, s->point_jitter, rng, world_scan);
+    const D::NeighborGrid grid(map_cloud, s->feasibility_resolution);
+    std::vector<bnbloc::Point3> all;
+    offsets[0] = 0;
+    for (int32_t j = 0; j < n_scans; ++j) {
+      bnbloc::Rng prng(pose_seed_base + static_cast<uint64_t>(j));
+      bool ok = false;
+      std::vector<bnbloc::Point3> scan;
+      for (int attempt = 0; attempt < 64 && !ok; ++attempt) {
+        bnbloc::Pose6 g;
+        g.x = prng.uniform(0.12 * s->size_x, 0.88 * s->size_x);
+        g.y = prng.uniform(0.12 * s->size_y, 0.88 * s->size_y);
+        g.z = prng.uniform(1.2, 2.2);
+        g.yaw = bnbloc::normalize_angle(prng.uniform(s->gt_yaw_min, s->gt_yaw_max));
+        if (s->tilt_noise) {
+          g.roll = prng.uniform(-0.01, 0.01);
+          g.pitch = prng.uniform(-0.01, 0.01);
+        }
+        bool inside = false;
+        for (const auto& b : boxes)
+          if (b.contains_xy(g.x, g.y, 1.0)) inside = true;
+        if (inside) continue;
+        scan.clear();
+        const bnbloc::Transform to_sensor = bnbloc::pose_to_transform(g).inverse();
+        const bnbloc::Point3 sensor{g.x, g.y, g.z};
+        for (const bnbloc::Point3& w : world_scan.points) {
+          if ((w - sensor).norm() > s->scan_range) continue;
+          scan.push_back(bnbloc::transform_point(to_sensor, w));
+        }
+        if (scan.size() < s->min_scan_points) continue;
+        const bnbloc::Transform t = bnbloc::pose_to_transform(g);
+        std::size_t hits = 0;
+        for (const bnbloc::Point3& p : scan)
+          if (grid.has_neighbor_within(bnbloc::transform_point(t, p), s->feasibility_resolution)) ++hits;
+        if (static_cast<double>(hits) / static_cast<double>(scan.size()) >= 0.95) {
+          const double v[6] = {g.x, g.y, g.z, g.roll, g.pitch, g.yaw};
+          std::memcpy(gt + 6 * j, v, sizeof(v));
+          ok = true;
+        }
+      }
+      if (!ok)
+        throw bnbloc::InfeasiblePoseError("gen_scans: no feasible pose for scan " + std::to_string(j));
+      all.insert(all.end(), scan.begin(), scan.end());
+      offsets[j + 1] = all.size();
+    }
+    bnbloc::PointCloud c;
+    c.points = std::move(all);
+    *scan_xyz = to_buffer(c);
+  });
+}
+
 // MultiResVoxelMap::build, voxel_map.hpp:226-244.
 int ref_map_build(const double* xyz, uint64_t n, double r, int32_t max_level, double ct,
                   uint64_t cap, void** out) {

@@ -32,10 +32,10 @@ __all__ = [
     "InfeasiblePoseError", "ConfigError", "CudaError", "InvalidArgumentError",
     "Strategy", "BranchMode", "Layout", "SearchConfig", "Stats", "SearchResult", "Pose6",
     "AxisGrid", "AngularGrid", "LevelMap", "MultiResVoxelMap", "DeviceScan", "NODE_DTYPE",
-    "batch_evaluate", "search", "search_sharded", "search_scans", "Comm", "nccl_version",
+    "batch_evaluate", "search", "search_scan_dump", "search_sharded", "search_scans", "Comm", "nccl_version",
     "save_map", "load_map", "is_map_file", "localize_scan", "prepare_source", "prepare_source_device",
     "max_range", "bounding_box", "pose_to_transform", "node_pose", "initial_node_count",
-    "gen_scene", "gen_scans", "cut_scan", "SceneSpec", "device_count",
+    "device_count",
 ]
 
 KTWO_PI = _abi.TWO_PI
@@ -702,6 +702,50 @@ def search_scan(vmap: MultiResVoxelMap, dscan: DeviceScan, cfg: SearchConfig,
     return _result_from_c(res, buf)
 
 
+@dataclass
+class SearchDumpResult:
+    """What the device scored inside one search (bbs_search_scan_dump)."""
+    result: "SearchResult"
+    root_scores: np.ndarray       # int32, initial_nodes() order
+    flush_nodes: np.ndarray       # (n, 8) int32, every dumped flush batch
+    flush_scores: np.ndarray      # int32 device scores of flush_nodes
+    epoch_offsets: np.ndarray     # batch i = [off[i], off[i+1])
+    epoch_ids: np.ndarray         # flush index of batch i
+
+
+def search_scan_dump(vmap: MultiResVoxelMap, dscan: DeviceScan, cfg: SearchConfig, exact_roots=False,
+                     epoch_stride=1, root_capacity=1 << 24, flush_capacity=1 << 22,
+                     epoch_capacity=1 << 16, trace_capacity=1 << 16) -> SearchDumpResult:
+    """search() with the root batch and flushed batches copied out
+    (parity instrumentation; one epoch per host check, no graphs)."""
+    res, buf = _new_result(trace_capacity if cfg.collect_trace else 0)
+    c = cfg.to_c()
+    roots = np.zeros(root_capacity, np.int32)
+    fn = np.zeros((flush_capacity, 8), np.int32)
+    fs = np.zeros(flush_capacity, np.int32)
+    off = np.zeros(epoch_capacity + 1, np.uint64)
+    ids = np.zeros(epoch_capacity, np.uint32)
+    d = _abi.SearchDump()
+    d.exact_roots = 1 if exact_roots else 0
+    d.epoch_stride = int(epoch_stride)
+    d.root_scores = roots.ctypes.data_as(C.POINTER(C.c_int32))
+    d.root_capacity = root_capacity
+    d.flush_nodes = fn.ctypes.data_as(C.POINTER(Node))
+    d.flush_scores = fs.ctypes.data_as(C.POINTER(C.c_int32))
+    d.flush_capacity = flush_capacity
+    d.epoch_offsets = off.ctypes.data_as(C.POINTER(C.c_uint64))
+    d.epoch_ids = ids.ctypes.data_as(C.POINTER(C.c_uint32))
+    d.epoch_capacity = epoch_capacity
+    _check(lib.bbs_search_scan_dump(vmap._h, dscan._h, C.byref(c), C.byref(d), C.byref(res)))
+    if d.root_count > root_capacity or d.flush_count > flush_capacity or d.epoch_count > epoch_capacity:
+        raise InvalidArgumentError(f"search_scan_dump: capacity exceeded (roots {d.root_count}, "
+                                   f"flush {d.flush_count}, epochs {d.epoch_count})")
+    ne = int(d.epoch_count)
+    return SearchDumpResult(_result_from_c(res, buf), roots[:d.root_count].copy(),
+                            fn[:d.flush_count].copy(), fs[:d.flush_count].copy(),
+                            off[:ne + 1].astype(np.int64), ids[:ne].copy())
+
+
 def search_scans(vmap: MultiResVoxelMap, dscans, cfg: SearchConfig, concurrency=16, trace_capacity=0):
     """Throughput mode (bbs_search_scans): search() for every device scan,
     `concurrency` searches in flight on native threads / streams."""
@@ -804,63 +848,3 @@ def localize_scan(vmap: MultiResVoxelMap, raw_scan, cfg: SearchConfig, downsampl
     return _result_from_c(res, buf)
 
 
-# ---- synthetic inputs (scene.hpp restatement; harness, not the path) -------
-class SceneSpec(C.Structure):
-    """SceneSpec, scene.hpp:21-38 (defaults from bbs_scene_spec_default)."""
-    _fields_ = [
-        ("size_x", C.c_double), ("size_y", C.c_double), ("size_z", C.c_double),
-        ("num_boxes", C.c_int32),
-        ("min_box_side", C.c_double), ("max_box_side", C.c_double),
-        ("min_box_height", C.c_double),
-        ("map_spacing", C.c_double), ("scan_spacing", C.c_double),
-        ("scan_range", C.c_double), ("point_jitter", C.c_double),
-        ("tilt_noise", C.c_int32),
-        ("gt_yaw_min", C.c_double), ("gt_yaw_max", C.c_double),
-        ("min_scan_points", C.c_uint64),
-        ("feasibility_resolution", C.c_double),
-    ]
-
-    @staticmethod
-    def default(**kw):
-        s = SceneSpec()
-        lib.bbs_scene_spec_default(C.byref(s))
-        for k, v in kw.items():
-            setattr(s, k, v)
-        return s
-
-
-def gen_scene(spec: SceneSpec, seed):
-    """scene.hpp:156-220 -> (map (n,3), scan (k,3), gt Pose6)."""
-    mp, sp = C.POINTER(C.c_double)(), C.POINTER(C.c_double)()
-    nm, ns = C.c_uint64(), C.c_uint64()
-    gt = (C.c_double * 6)()
-    _check(lib.bbs_gen_scene(C.byref(spec), int(seed), C.byref(mp), C.byref(nm), C.byref(sp),
-                             C.byref(ns), gt), lib.bbs_scene_last_error)
-    m = np.ctypeslib.as_array(mp, shape=(nm.value, 3)).copy()
-    s = np.ctypeslib.as_array(sp, shape=(ns.value, 3)).copy()
-    lib.bbs_free(C.cast(mp, C.c_void_p))
-    lib.bbs_free(C.cast(sp, C.c_void_p))
-    return m, s, Pose6(*gt)
-
-
-def gen_scans(spec: SceneSpec, seed, pose_seed_base, n_scans):
-    """Extra scans of seed's map (C4 helper) -> (list of (k,3), list of Pose6)."""
-    sp = C.POINTER(C.c_double)()
-    offs = (C.c_uint64 * (n_scans + 1))()
-    gt = (C.c_double * (6 * max(n_scans, 1)))()
-    _check(lib.bbs_gen_scans(C.byref(spec), int(seed), int(pose_seed_base), int(n_scans),
-                             C.byref(sp), offs, gt), lib.bbs_scene_last_error)
-    allp = np.ctypeslib.as_array(sp, shape=(max(offs[n_scans], 1), 3)).copy()
-    lib.bbs_free(C.cast(sp, C.c_void_p))
-    scans = [allp[offs[j]:offs[j + 1]].copy() for j in range(n_scans)]
-    poses = [Pose6(*gt[6 * j:6 * j + 6]) for j in range(n_scans)]
-    return scans, poses
-
-
-def cut_scan(scan, k, seed):
-    """First k points of a Fisher-Yates shuffle driven by Rng(seed)."""
-    a = _xyz(scan)
-    k = int(k)
-    out = np.zeros((k, 3))
-    _check(lib.bbs_cut_scan(_dptr(a), a.shape[0], k, int(seed), _dptr(out)))
-    return out

@@ -141,6 +141,25 @@ class Shard(C.Structure):
     ]
 
 
+class SearchDump(C.Structure):
+    """bbs_search_dump (parity instrumentation)."""
+    _fields_ = [
+        ("exact_roots", C.c_int32),
+        ("epoch_stride", C.c_uint32),
+        ("root_scores", C.POINTER(C.c_int32)),
+        ("root_capacity", C.c_uint64),
+        ("root_count", C.c_uint64),
+        ("flush_nodes", C.POINTER(Node)),
+        ("flush_scores", C.POINTER(C.c_int32)),
+        ("flush_capacity", C.c_uint64),
+        ("flush_count", C.c_uint64),
+        ("epoch_offsets", C.POINTER(C.c_uint64)),
+        ("epoch_ids", C.POINTER(C.c_uint32)),
+        ("epoch_capacity", C.c_uint64),
+        ("epoch_count", C.c_uint64),
+    ]
+
+
 SHARD_ROOTS = 0  # BBS_SHARD_ROOTS: own BnB per rank over its root share
 SHARD_EXACT = 1  # BBS_SHARD_EXACT: batch-split replay of the single-queue schedule
 

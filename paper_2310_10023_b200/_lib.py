@@ -9,7 +9,8 @@ import ctypes as C
 import os
 
 from ._abi import (
-    Aabb, AxisGridC, LevelInfo, MapOptions, Node, SearchConfigC, SearchResultC, Shard,
+    Aabb, AxisGridC, LevelInfo, MapOptions, Node, SearchConfigC, SearchDump, SearchResultC,
+    Shard,
 )
 
 HERE = os.path.dirname(os.path.abspath(__file__))
@@ -71,6 +72,8 @@ SIGNATURES = {
     "bbs_scan_upload": (C.c_int, [_vp, _dp, _u64, C.POINTER(_vp)]),
     "bbs_scan_free": (C.c_int, [_vp]),
     "bbs_search_scan": (C.c_int, [_vp, _vp, C.POINTER(SearchConfigC), C.POINTER(SearchResultC)]),
+    "bbs_search_scan_dump": (C.c_int, [_vp, _vp, C.POINTER(SearchConfigC), C.POINTER(SearchDump),
+                                       C.POINTER(SearchResultC)]),
     "bbs_batch_evaluate_device": (C.c_int, [_vp, _vp, C.POINTER(SearchConfigC), _d, _vp, _u64,
                                             _vp]),
     "bbs_search_scan_on": (C.c_int, [_vp, _vp, C.POINTER(SearchConfigC), _vp,
@@ -85,13 +88,6 @@ SIGNATURES = {
     "bbs_comm_init": (C.c_int, [_i32, _i32, _i32, C.POINTER(C.c_uint8), C.POINTER(_vp)]),
     "bbs_comm_free": (C.c_int, [_vp]),
     "bbs_nccl_version": (C.c_int, []),
-    "bbs_scene_spec_default": (None, [_vp]),
-    "bbs_gen_scene": (C.c_int, [_vp, _u64, C.POINTER(_dp), C.POINTER(_u64), C.POINTER(_dp),
-                                C.POINTER(_u64), _dp]),
-    "bbs_gen_scans": (C.c_int, [_vp, _u64, _u64, _i32, C.POINTER(_dp), C.POINTER(_u64), _dp]),
-    "bbs_cut_scan": (C.c_int, [_dp, _u64, _u64, _u64, _dp]),
-    "bbs_scene_last_error": (C.c_char_p, []),
-    "bbs_free": (None, [_vp]),
     "bbs_gather_bench": (C.c_int, [_i32, _u64, _dp]),
 }
 
@@ -100,7 +96,7 @@ for _name, (_res, _args) in SIGNATURES.items():
     _f.restype = _res
     _f.argtypes = _args
 
-ABI_VERSION = 3  # include/bbs.h BBS_ABI_VERSION this mirror was written for
+ABI_VERSION = 4  # include/bbs.h BBS_ABI_VERSION this mirror was written for
 if lib.bbs_abi_version() != ABI_VERSION:
     raise ImportError(f"{LIB_PATH} has ABI version {lib.bbs_abi_version()}, "
                       f"the Python mirror expects {ABI_VERSION}: rebuild the library")

@@ -24,7 +24,7 @@
 
 namespace bbs {
 void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const bbs_shard* shard,
-                bbs_search_result* out, cudaStream_t stream = nullptr);
+                bbs_search_result* out, cudaStream_t stream = nullptr, bbs_search_dump* dump = nullptr);
 void batch_evaluate_device(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, double d_max,
                            bbs_node* d_nodes, uint64_t n, cudaStream_t s, const int32_t* lo,
                            const int32_t* hi);
@@ -372,6 +372,15 @@ int bbs_search_scan_on(bbs_map_t map, bbs_scan_t scan, const bbs_search_config* 
     REQUIRE(map && scan && cfg && result, "null argument");
     REQUIRE(scan->map == map, "scan was uploaded for a different map");
     bbs::run_search(map, scan, *cfg, nullptr, result, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int bbs_search_scan_dump(bbs_map_t map, bbs_scan_t scan, const bbs_search_config* cfg,
+                         bbs_search_dump* dump, bbs_search_result* result) {
+  return guard([&] {
+    REQUIRE(map && scan && cfg && dump && result, "null argument");
+    REQUIRE(scan->map == map, "scan was uploaded for a different map");
+    bbs::run_search(map, scan, *cfg, nullptr, result, nullptr, dump);
   });
 }
 

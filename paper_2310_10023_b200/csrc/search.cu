@@ -1183,7 +1183,7 @@ bbs_scan* upload_scan(bbs_map* m, const double* xyz, uint64_t k, bool sync) {
 // search(), search.hpp:72-186, on the device.  `shard` may be null;
 // `stream` null = the map's stream (concurrent searches use their own).
 void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const bbs_shard* shard,
-                bbs_search_result* out, cudaStream_t stream) {
+                bbs_search_result* out, cudaStream_t stream, bbs_search_dump* dump) {
   // validation, search.hpp:79-89, same order and messages
   if (scan->k == 0) throw Error(BBS_ERR_DEGENERATE_SCAN, "search: empty scan");
   if (m->r != cfg.min_resolution) throw Error(BBS_ERR_CONFIG, "search: config r does not match the map");
@@ -1369,6 +1369,8 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
     }
   };
   dense_box(m->view.level[L].cell, bp.tmax, &bp.dn_r, &bp.dn_zlo, &bp.dn_nz, &bp.dn_eps, &bp.dn_eps1);
+  // parity dump: no survivor-bound early exit in the root column kernel
+  if (dump && dump->exact_roots) bp.threshold = INT32_MIN;
   int32_t* root_scores = W.root_scores.get(static_cast<size_t>(std::max<int64_t>(total, 1)), s);
   unsigned long long* d_probes = W.probes.get(2, s);  // [0] root probes, [1] survivor count
   int* d_nsel = W.nsel.get(1, s);
@@ -1418,6 +1420,18 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
   }
   BBS_CUDA(cudaEventRecord(ev_roots1, s));
   tmark("roots enqueued");
+  if (dump) {
+    dump->root_count = static_cast<uint64_t>(std::max<int64_t>(total, 0));
+    const uint64_t nr_out = std::min(dump->root_count, dump->root_scores ? dump->root_capacity : 0);
+    if (nr_out) {
+      BBS_CUDA(cudaMemcpyAsync(dump->root_scores, root_scores, nr_out * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+      BBS_CUDA(cudaStreamSynchronize(s));
+    }
+    dump->flush_count = 0;
+    dump->epoch_count = 0;
+    if (dump->epoch_offsets) dump->epoch_offsets[0] = 0;
+  }
+  uint64_t dump_epoch = 0;  // flushes seen so far (dump mode)
   cudaEvent_t ev_fork = W.next_event(), ev_prebuilt = W.next_event();
   bool prebuild_pending = false;
   // per-search (level, rotation) histogram cache for the flushes (epoch_cache.cu)
@@ -1544,7 +1558,7 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
   const uint64_t n_scored_roots = exact ? static_cast<uint64_t>(std::max<int64_t>(total, 0)) : n_own;
 
   // survivors >= threshold among own roots, in initial_nodes order
-  const int E = host_x ? 1 : 8;  // epochs per host check
+  const int E = (host_x || dump) ? 1 : 8;  // epochs per host check
   unsigned long long root_probes = 0;
   int n_root_surv = 0;       // host path only
   unsigned long long* surv_idx = nullptr;
@@ -1903,6 +1917,28 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
       dbg_prev = keep;
     }
     hs = *W.h_st;
+    if (dump && hs.n_children > 0) {
+      // this epoch's flushed batch: pending[0, n) and its scores (still in
+      // place: the next epoch's branch kernel has not run)
+      const uint32_t stride = std::max<uint32_t>(dump->epoch_stride, 1);
+      if (dump_epoch % stride == 0) {
+        const uint64_t n = hs.n_children, o = dump->flush_count;
+        const uint64_t fit = o < dump->flush_capacity ? std::min<uint64_t>(n, dump->flush_capacity - o) : 0;
+        if (fit && dump->flush_nodes)
+          BBS_CUDA(cudaMemcpyAsync(dump->flush_nodes + o, pending, fit * sizeof(bbs_node), cudaMemcpyDeviceToHost, s));
+        if (fit && dump->flush_scores)
+          BBS_CUDA(cudaMemcpyAsync(dump->flush_scores + o, pscores, fit * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+        BBS_CUDA(cudaStreamSynchronize(s));
+        const uint64_t e = dump->epoch_count;
+        if (e < dump->epoch_capacity) {
+          if (dump->epoch_ids) dump->epoch_ids[e] = static_cast<uint32_t>(dump_epoch);
+          if (dump->epoch_offsets) dump->epoch_offsets[e + 1] = o + n;
+        }
+        dump->flush_count = o + n;
+        dump->epoch_count = e + 1;
+      }
+      ++dump_epoch;
+    }
     self_active = hs.active != 0;
     builds_live = (claimable & ~hs.cache_raw) != 0;  // raw flags only ever get set
     if (roots_host_x)

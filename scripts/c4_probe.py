@@ -2,13 +2,14 @@
 import os, sys, time
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
+import harness as H  # noqa: E402  (synthetic inputs)
 import bench
 import paper_2310_10023_b200 as B
 cfgd = bench.CONFIGS["c4"]
-spec = B.SceneSpec.default(**cfgd["spec"])
-m, _, _ = B.gen_scene(spec, cfgd["seed"])
-scans, poses = B.gen_scans(spec, cfgd["seed"], 1000, 32)
-scans = [B.cut_scan(s, min(cfgd["K"], s.shape[0]), 7) for s in scans]
+spec = H.SceneSpec.default(**cfgd["spec"])
+m, _, _ = H.gen_scene(spec, cfgd["seed"])
+scans, poses = H.gen_scans(spec, cfgd["seed"], 1000, 32)
+scans = [H.cut_scan(s, min(cfgd["K"], s.shape[0]), 7) for s in scans]
 vm = B.MultiResVoxelMap.build(m, cfgd["r"], cfgd["max_level"])
 ds = [B.DeviceScan(vm, s) for s in scans]
 cfg = bench.search_config(B, cfgd)

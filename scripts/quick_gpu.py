@@ -4,14 +4,15 @@ import sys, time, os
 import numpy as np
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT); sys.path.insert(0, os.path.join(ROOT, 'oracle'))
+import harness as H  # noqa: E402  (synthetic inputs)
 import paper_2310_10023_b200 as B
 from pyoracle import Reference, Restated, default_config
 
 ref = Reference(); orc = Restated()
-spec = B.SceneSpec.default(size_x=24, size_y=24, size_z=10, num_boxes=4, min_box_side=2.5,
+spec = H.SceneSpec.default(size_x=24, size_y=24, size_z=10, num_boxes=4, min_box_side=2.5,
                            max_box_side=6.0, min_box_height=3.0, map_spacing=0.3,
                            scan_spacing=0.45, scan_range=14.0, min_scan_points=300)
-m, s, gt = B.gen_scene(spec, 42)
+m, s, gt = H.gen_scene(spec, 42)
 r, L = 0.25, 4
 for layout in (B.Layout.BITMAP, B.Layout.HASH):
     t = time.time(); dm = B.MultiResVoxelMap.build(m, r, L, layout=layout); bt = time.time() - t

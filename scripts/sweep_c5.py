@@ -23,6 +23,7 @@ import torch
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
+import harness as H  # noqa: E402  (synthetic inputs)
 import bench  # noqa: E402
 import paper_2310_10023_b200 as B  # noqa: E402
 
@@ -34,10 +35,10 @@ def main():
     ap.add_argument("--ks", default="1000,2000,5000,10000,20000,50000,100000")
     args = ap.parse_args()
     cfgd = bench.CONFIGS["c2"]
-    spec = B.SceneSpec.default(**cfgd["spec"])
-    m, raw, _ = B.gen_scene(spec, cfgd["seed"])
+    spec = H.SceneSpec.default(**cfgd["spec"])
+    m, raw, _ = H.gen_scene(spec, cfgd["seed"])
     kmax = min(max(int(k) for k in args.ks.split(",")), raw.shape[0])
-    full = B.cut_scan(raw, kmax, 7)
+    full = H.cut_scan(raw, kmax, 7)
     vm = B.MultiResVoxelMap.build(m, cfgd["r"], cfgd["max_level"])
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)

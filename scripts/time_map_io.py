@@ -3,12 +3,13 @@ reference's load_map (oracle/_ref, collision_target 0.3)."""
 import os, sys, tempfile, time
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT); sys.path.insert(0, os.path.join(ROOT, "oracle"))
+import harness as H  # noqa: E402  (synthetic inputs)
 import numpy as np
 import bench
 import paper_2310_10023_b200 as B
 from pyoracle import Reference
 cfgd = bench.CONFIGS["c2"]
-m, _, _ = B.gen_scene(B.SceneSpec.default(**cfgd["spec"]), cfgd["seed"])
+m, _, _ = H.gen_scene(H.SceneSpec.default(**cfgd["spec"]), cfgd["seed"])
 vm = B.MultiResVoxelMap.build(m, cfgd["r"], cfgd["max_level"])
 d = tempfile.mkdtemp()
 path = os.path.join(d, "c2.vxm")

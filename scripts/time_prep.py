@@ -2,13 +2,14 @@
 import os, sys, time
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT); sys.path.insert(0, os.path.join(ROOT, "oracle"))
+import harness as H  # noqa: E402  (synthetic inputs)
 import numpy as np
 import bench
 import paper_2310_10023_b200 as B
 from pyoracle import Reference
 cfgd = bench.CONFIGS["c2"]
-spec = B.SceneSpec.default(**cfgd["spec"])
-_, raw, _ = B.gen_scene(spec, 1)
+spec = H.SceneSpec.default(**cfgd["spec"])
+_, raw, _ = H.gen_scene(spec, 1)
 ref = Reference()
 for target in (10000, 2000):
     B.prepare_source_device(raw, target)  # warm

@@ -18,6 +18,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 GOLDEN = os.path.join(ROOT, "tests", "golden")
 sys.path.insert(0, ROOT)
 sys.path.insert(0, os.path.join(ROOT, "oracle"))
+import harness as H  # noqa: E402  (synthetic inputs)
 
 
 def pytest_configure(config):
@@ -54,10 +55,10 @@ def load_case(B, scenes, name):
     """Regenerate a golden case's inputs with the product's scene restatement
     (bit-identity against the reference's gen_scene is tested separately)."""
     sc = scenes[name]
-    spec = B.SceneSpec.default(**sc["spec"])
-    m, s, gt = B.gen_scene(spec, sc["seed"])
+    spec = H.SceneSpec.default(**sc["spec"])
+    m, s, gt = H.gen_scene(spec, sc["seed"])
     if sc["K"] is not None:
-        s = B.cut_scan(s, min(sc["K"], s.shape[0]), sc["cut_seed"])
+        s = H.cut_scan(s, min(sc["K"], s.shape[0]), sc["cut_seed"])
     return m, s, gt, sc
 
 

@@ -6,6 +6,7 @@ import math
 
 import numpy as np
 import pytest
+import harness as H  # noqa: E402  (synthetic inputs)
 
 PI = 3.14159265358979323846
 
@@ -102,7 +103,7 @@ def test_gen_scene_bit_identical(B, ref, seed):
     kw = dict(size_x=24.0, size_y=24.0, size_z=10.0, num_boxes=4, min_box_side=2.5,
               max_box_side=6.0, min_box_height=3.0, map_spacing=0.3, scan_spacing=0.45,
               scan_range=14.0, min_scan_points=300)
-    m1, s1, gt1 = B.gen_scene(B.SceneSpec.default(**kw), seed)
+    m1, s1, gt1 = H.gen_scene(H.SceneSpec.default(**kw), seed)
     spec = ref.default_spec()
     for k, v in kw.items():
         setattr(spec, k, v)
@@ -114,12 +115,12 @@ def test_gen_scene_bit_identical(B, ref, seed):
 
 def test_gen_scene_deterministic_and_feasible(B):
     # harness_test.cpp:31-62
-    spec = B.SceneSpec.default(size_x=24.0, size_y=24.0, size_z=10.0, num_boxes=4,
+    spec = H.SceneSpec.default(size_x=24.0, size_y=24.0, size_z=10.0, num_boxes=4,
                                min_box_side=2.5, max_box_side=6.0, min_box_height=3.0,
                                map_spacing=0.3, scan_spacing=0.45, scan_range=14.0,
                                min_scan_points=300)
-    a = B.gen_scene(spec, 42)
-    b = B.gen_scene(spec, 42)
+    a = H.gen_scene(spec, 42)
+    b = H.gen_scene(spec, 42)
     np.testing.assert_array_equal(a[0], b[0])
     assert a[2].as_tuple() == b[2].as_tuple()
     assert a[1].shape[0] >= 300
@@ -127,19 +128,19 @@ def test_gen_scene_deterministic_and_feasible(B):
 
 
 def test_gen_scans_match_gen_scene_layout(B):
-    spec = B.SceneSpec.default(size_x=24.0, size_y=24.0, size_z=10.0, num_boxes=4,
+    spec = H.SceneSpec.default(size_x=24.0, size_y=24.0, size_z=10.0, num_boxes=4,
                                min_box_side=2.5, max_box_side=6.0, min_box_height=3.0,
                                map_spacing=0.3, scan_spacing=0.45, scan_range=14.0,
                                min_scan_points=300)
-    scans, poses = B.gen_scans(spec, 42, 1000, 3)
+    scans, poses = H.gen_scans(spec, 42, 1000, 3)
     assert len(scans) == 3 and all(s.shape[0] >= 300 for s in scans)
     assert len({p.as_tuple() for p in poses}) == 3
 
 
 def test_cut_scan_is_a_seeded_prefix(B):
     pts = np.arange(300, dtype=np.float64).reshape(100, 3)
-    a = B.cut_scan(pts, 40, 7)
-    b = B.cut_scan(pts, 40, 7)
+    a = H.cut_scan(pts, 40, 7)
+    b = H.cut_scan(pts, 40, 7)
     np.testing.assert_array_equal(a, b)
     rows = {tuple(r) for r in pts}
     assert all(tuple(r) in rows for r in a) and len({tuple(r) for r in a}) == 40
@@ -150,11 +151,11 @@ def test_cut_scan_is_a_seeded_prefix(B):
 
 @pytest.mark.parametrize("target", [0, 300, 1000, 5000])
 def test_prepare_source_bit_identical(B, ref, target):
-    spec = B.SceneSpec.default(size_x=24.0, size_y=24.0, size_z=10.0, num_boxes=4,
+    spec = H.SceneSpec.default(size_x=24.0, size_y=24.0, size_z=10.0, num_boxes=4,
                                min_box_side=2.5, max_box_side=6.0, min_box_height=3.0,
                                map_spacing=0.3, scan_spacing=0.2, scan_range=14.0,
                                min_scan_points=300)
-    _, raw, _ = B.gen_scene(spec, 9)
+    _, raw, _ = H.gen_scene(spec, 9)
     ours = B.prepare_source(raw, target)
     scan, leaf, conv, dmax = ref.prepare_source(raw, target)
     np.testing.assert_array_equal(ours.scan, scan)
@@ -167,3 +168,26 @@ def test_max_range_and_bbox_bit_identical(B, ref):
     assert B.max_range(pts) == ref.max_range(pts)
     (lo, hi) = B.bounding_box(pts)
     assert lo == tuple(pts.min(axis=0)) and hi == tuple(pts.max(axis=0))
+
+
+def test_gen_scans_bit_identical(ref):
+    """C4 harness helper: harness/libbbs_scene.so's gen_scans equals
+    oracle/_ref's ref_gen_scans (the reference's own scene internals)."""
+    kw = dict(size_x=40.0, size_y=40.0, size_z=10.0, num_boxes=5, min_box_side=3.0,
+              max_box_side=8.0, min_box_height=3.0, map_spacing=0.3, scan_spacing=0.45,
+              scan_range=20.0, min_scan_points=300)
+    a, pa = H.gen_scans(H.SceneSpec.default(**kw), 3, 1000, 4)
+    spec = ref.default_spec()
+    for k, v in kw.items():
+        setattr(spec, k, v)
+    b, pb = ref.gen_scans(spec, 3, 1000, 4)
+    for x, y in zip(a, b):
+        np.testing.assert_array_equal(x, y)
+    assert [p.as_tuple() for p in pa] == pb
+
+
+def test_cut_scan_python_equals_native():
+    rng = np.random.default_rng(3)
+    pts = rng.normal(size=(5000, 3))
+    for k in (0, 1, 777, 5000):
+        np.testing.assert_array_equal(H.cut_scan(pts, k, 7), H.cut_scan_py(pts, k, 7))

@@ -12,6 +12,7 @@ import struct
 
 import numpy as np
 import pytest
+import harness as H  # noqa: E402  (synthetic inputs)
 
 MAGIC = b"3DBBS\x01"
 
@@ -91,10 +92,10 @@ def test_missing_file_and_is_map_file(B, ref, tmp_path):
 
 
 def _scene(B):
-    spec = B.SceneSpec.default(size_x=24, size_y=24, size_z=10, num_boxes=4, min_box_side=2.5,
+    spec = H.SceneSpec.default(size_x=24, size_y=24, size_z=10, num_boxes=4, min_box_side=2.5,
                                max_box_side=6.0, min_box_height=3.0, map_spacing=0.3,
                                scan_spacing=0.45, scan_range=14.0, min_scan_points=300)
-    return B.gen_scene(spec, 42)
+    return H.gen_scene(spec, 42)
 
 
 @pytest.mark.gpu

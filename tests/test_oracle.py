@@ -6,6 +6,7 @@ import hashlib
 
 import numpy as np
 import pytest
+import harness as H  # noqa: E402  (synthetic inputs)
 
 from conftest import golden_json, golden_npz, load_case
 
@@ -58,12 +59,12 @@ def test_restated_search_matches_golden(B, orc, golden_scenes, name):
 
 def test_restatement_vs_reference_live(B, ref, orc):
     """Fresh seeds: map sets, scores and full searches agree exactly."""
-    spec = B.SceneSpec.default(size_x=16, size_y=16, size_z=8, num_boxes=3, min_box_side=2.0,
+    spec = H.SceneSpec.default(size_x=16, size_y=16, size_z=8, num_boxes=3, min_box_side=2.0,
                                max_box_side=5.0, min_box_height=2.0, map_spacing=0.3,
                                scan_spacing=0.5, scan_range=10.0, min_scan_points=200)
     from pyoracle import default_config
     for seed in (3, 5):
-        m, s, _ = B.gen_scene(spec, seed)
+        m, s, _ = H.gen_scene(spec, seed)
         rm = ref.map_build(m, 0.5, 3, 0.05)
         om = orc.map_build(m, 0.5, 3)
         for lv in range(4):

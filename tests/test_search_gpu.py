@@ -7,6 +7,7 @@ import math
 
 import numpy as np
 import pytest
+import harness as H  # noqa: E402  (synthetic inputs)
 
 from conftest import golden_json, load_case
 
@@ -221,11 +222,11 @@ def test_yaw_result_is_normalized(B):
 
 
 def test_localize_scan_matches_reference(B, ref):
-    spec = B.SceneSpec.default(size_x=24.0, size_y=24.0, size_z=10.0, num_boxes=4,
+    spec = H.SceneSpec.default(size_x=24.0, size_y=24.0, size_z=10.0, num_boxes=4,
                                min_box_side=2.5, max_box_side=6.0, min_box_height=3.0,
                                map_spacing=0.3, scan_spacing=0.2, scan_range=14.0,
                                min_scan_points=300)
-    m, raw, _ = B.gen_scene(spec, 9)
+    m, raw, _ = H.gen_scene(spec, 9)
     vm = B.MultiResVoxelMap.build(m, 0.5, 3)
     rm = ref.map_build(m, 0.5, 3, 0.05)
     cfg = B.SearchConfig(min_resolution=0.5, max_level=3, batch_size=1000)
@@ -286,9 +287,9 @@ def test_large_scan_paths_are_transparent(B, golden_scenes, monkeypatch):
     """K = 70,000 (> 65535: no 16-bit dense histograms, hash builds; the
     root batch's early column exit, prebuild and probe chunks at a size the
     C2 bench never uses): cache on/off give identical searches."""
-    m, raw, _ = B.gen_scene(B.SceneSpec.default(**golden_scenes["campus"]["spec"]),
+    m, raw, _ = H.gen_scene(H.SceneSpec.default(**golden_scenes["campus"]["spec"]),
                             golden_scenes["campus"]["seed"])
-    s = B.cut_scan(raw, min(70000, raw.shape[0]), 3)
+    s = H.cut_scan(raw, min(70000, raw.shape[0]), 3)
     sc = golden_scenes["campus"]
     vm = B.MultiResVoxelMap.build(m, sc["r"], sc["max_level"])
     ds = B.DeviceScan(vm, s)
@@ -306,11 +307,11 @@ def test_large_scan_paths_are_transparent(B, golden_scenes, monkeypatch):
 def test_search_scans_throughput_mode_matches_single_searches(B):
     """bbs_search_scans (native workers, one stream each, workspaces leased
     concurrently) returns each scan's search() result."""
-    spec = B.SceneSpec.default(size_x=24.0, size_y=24.0, size_z=10.0, num_boxes=4, min_box_side=2.5,
+    spec = H.SceneSpec.default(size_x=24.0, size_y=24.0, size_z=10.0, num_boxes=4, min_box_side=2.5,
                                max_box_side=6.0, min_box_height=3.0, map_spacing=0.3,
                                scan_spacing=0.45, scan_range=14.0, min_scan_points=300)
-    m, _, _ = B.gen_scene(spec, 42)
-    scans, _ = B.gen_scans(spec, 42, 1000, 6)
+    m, _, _ = H.gen_scene(spec, 42)
+    scans, _ = H.gen_scans(spec, 42, 1000, 6)
     vm = B.MultiResVoxelMap.build(m, 0.5, 3)
     ds = [B.DeviceScan(vm, s) for s in scans]
     cfg = B.SearchConfig(min_resolution=0.5, max_level=3, batch_size=400, collect_trace=True)

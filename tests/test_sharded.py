@@ -17,6 +17,7 @@ import threading
 
 import numpy as np
 import pytest
+import harness as H  # noqa: E402  (synthetic inputs)
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
@@ -29,7 +30,7 @@ SPEC = dict(size_x=24.0, size_y=24.0, size_z=10.0, num_boxes=4, min_box_side=2.5
 
 def _scene():
     import paper_2310_10023_b200 as B
-    m, s, gt = B.gen_scene(B.SceneSpec.default(**SPEC), 42)
+    m, s, gt = H.gen_scene(H.SceneSpec.default(**SPEC), 42)
     return m, s, gt
 
 

@@ -8,16 +8,17 @@ device in input order, so they agree to a few ulps (tolerance below: 64 ulps
 of the coordinate magnitude, rtol 1e-14 relative to the scan extent)."""
 import numpy as np
 import pytest
+import harness as H  # noqa: E402  (synthetic inputs)
 
 pytestmark = pytest.mark.gpu
 
 
 def _raw(B, seed, spacing=0.2, rng=14.0):
-    spec = B.SceneSpec.default(size_x=24.0, size_y=24.0, size_z=10.0, num_boxes=4,
+    spec = H.SceneSpec.default(size_x=24.0, size_y=24.0, size_z=10.0, num_boxes=4,
                                min_box_side=2.5, max_box_side=6.0, min_box_height=3.0,
                                map_spacing=0.3, scan_spacing=spacing, scan_range=rng,
                                min_scan_points=300)
-    return B.gen_scene(spec, seed)
+    return H.gen_scene(spec, seed)
 
 
 def _check(got, want_xyz, want_leaf, want_conv, want_dmax):
@@ -49,11 +50,11 @@ def test_device_prepare_source_passthrough(B, ref):
 def test_device_prepare_source_campus_raw_scan(B, ref):
     """C2's raw scan (~236k points, extents need > 64 key bits at auto_leaf's
     first probe: the three-pass LSD sort) down to ~10k points."""
-    spec = B.SceneSpec.default(size_x=300.0, size_y=300.0, size_z=30.0, num_boxes=60,
+    spec = H.SceneSpec.default(size_x=300.0, size_y=300.0, size_z=30.0, num_boxes=60,
                                min_box_side=6.0, max_box_side=30.0, min_box_height=8.0,
                                map_spacing=0.19, scan_spacing=0.3, scan_range=60.0,
                                min_scan_points=400)
-    _, raw, _ = B.gen_scene(spec, 1)
+    _, raw, _ = H.gen_scene(spec, 1)
     for target in (10000, 2000):
         got = B.prepare_source_device(raw, target)
         want = ref.prepare_source(raw, target)
