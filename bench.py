@@ -7,20 +7,25 @@ localization of a K=10,000-point scan against a ~5M-point synthetic campus map
 roll/pitch +-0.02 rad, BFS, RotoTrans, b = 10,000, threshold 0.95).  A "step"
 is one search() (root batch + every flush epoch until the queue drains).
 
-  value   candidate score evals/s = nodes_generated (all ranks) / max-rank
-          device time of the K timed steps (CUDA events on the search stream,
-          scan and map resident in HBM; L2 flushed before every step)
+  value   candidate score evals/s = W / max-rank device time of the K timed
+          steps (CUDA events on the search stream, scan and map resident in
+          HBM; L2 flushed before every step).  W = the single-queue search's
+          nodes_generated (= the reference's, checked against the golden), so
+          at N > 1 the work is held at the N = 1 amount (strong scaling)
   e2e     same metric through the public host API bbs_search(): the scan is
           copied from pinned host memory and the result read back every step
           (host wall clock around each call)
+  parity  the result against the reference's search() golden
+          (tests/golden): exact at N = 1 and in the exact shard mode; the
+          best score plus the pose within one finest voxel / angular step in
+          the roots shard mode (north_star's tolerance)
   cpu_baseline / --impl reference
-          the UNMODIFIED reference (oracle/_ref, bnbloc::batch_evaluate with
-          workers = all host threads) on a bounded sample of the same root
-          batch: evals/s
+          the UNMODIFIED reference (oracle/_ref, bnbloc::batch_evaluate) on a
+          bounded uniform sample of the same root batch, all host threads and
+          one thread: evals/s; a full search's time is extrapolated from it
 
-N > 1 (torchrun, NCCL): the root set is sharded (root i -> rank i % N) and the
-incumbent is max-all-reduced after every epoch; total work per
-search is fixed, so scaling is "strong".
+--gpus N without torchrun re-launches itself under torch.distributed.run
+(one process per GPU, NCCL); the root set is sharded.
 """
 import argparse
 import json
@@ -36,7 +41,9 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
-import harness as H  # noqa: E402  (synthetic inputs)
+import harness as H  # noqa: E402  (synthetic inputs; not the product)
+
+GOLDENS = {"c1": "room_search.json", "c2": "campus_search.json", "c3": "c3_search.json"}
 
 CONFIGS = {
     # name: scene spec, seed, search params, K
@@ -183,7 +190,9 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm), "source": "nvidia-smi"}
 
 
-def build_inputs(B, cfgd):
+def build_inputs(cfgd):
+    """The workload's map and K-point scan from the harness's gen_scene
+    restatement (bit-identical to the reference's, tests/test_host.py)."""
     spec = H.SceneSpec.default(**cfgd["spec"])
     t = time.time()
     map_pts, raw_scan, gt = H.gen_scene(spec, cfgd["seed"])
@@ -193,69 +202,154 @@ def build_inputs(B, cfgd):
     return map_pts, scan, gt
 
 
+def config_dict(cfgd, K, map_points):
+    """The `config` object of BOTH arms (identical keys and values)."""
+    return {"workload": cfgd["workload"], "K": int(K), "map_points": int(map_points),
+            "r": cfgd["r"], "levels": cfgd["max_level"] + 1, "roll_pitch_half_range": cfgd["rp"],
+            "strategy": "BFS", "branch_mode": "RotoTrans", "batch_size": 10000,
+            "l2": "flushed (256 MiB write) before every timed step; the reference arm runs on "
+                  "host cores"}
+
+
 def search_config(B, cfgd):
     return B.SearchConfig(min_resolution=cfgd["r"], max_level=cfgd["max_level"],
                           roll_pitch_half_range=cfgd["rp"], strategy=B.Strategy.BFS,
                           branch_mode=B.BranchMode.ROTO_TRANS, batch_size=10000)
 
 
-def reference_sample(map_pts, scan, cfgd, target_s, log_prefix=""):
-    """Time the UNMODIFIED reference (oracle/_ref) batch_evaluate on a bounded
-    sample of the root batch.  Returns (evals/s, sample description, cores)."""
-    sys.path.insert(0, os.path.join(ROOT, "oracle"))
-    from pyoracle import Reference, default_config  # noqa: E402  (cpu_baseline leg only)
-    ref = Reference()
-    t = time.time()
-    rmap = ref.map_build(map_pts, cfgd["r"], cfgd["max_level"], 0.3, 8 << 30)
-    log(f"{log_prefix}reference map build (collision_target 0.3): {time.time() - t:.1f}s")
-    cfg = default_config(min_resolution=cfgd["r"], max_level=cfgd["max_level"],
-                         roll_pitch_half_range=cfgd["rp"])
-    d_max = ref.max_range(scan)
-    roots = ref.initial_nodes(cfg, d_max, rmap.bbox())
-    rng = np.random.default_rng(11)
-    cores = os.cpu_count() or 1
-    n = 512
-    while True:
-        sample = roots[rng.choice(roots.shape[0], size=min(n, roots.shape[0]), replace=False)]
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def golden_search(config):
+    """The reference's search() result for this workload (tests/golden, made
+    by running oracle/_ref: tests/golden/make_golden.py, make_scale_goldens.py)."""
+    name = GOLDENS.get(config)
+    if not name:
+        return None
+    try:
+        with open(os.path.join(ROOT, "tests", "golden", name)) as f:
+            return json.load(f)["bfs_roto_b10000"]
+    except (OSError, KeyError, ValueError):
+        return None
+
+
+class RefSampler:
+    """The UNMODIFIED reference (oracle/_ref) on bounded uniform samples of
+    the workload's root batch (search.hpp:111-124 scores every root with
+    batch_evaluate; ~98% of a C2 search's evaluations are roots)."""
+
+    def __init__(self, map_pts, scan, cfgd, log_prefix=""):
+        sys.path.insert(0, os.path.join(ROOT, "oracle"))
+        from pyoracle import Reference, default_config  # noqa: E402  (reference / cpu_baseline legs only)
+        self.ref = Reference()
         t = time.time()
-        rmap.batch_evaluate(scan, cfg, sample, d_max=d_max, workers=cores)
-        dt = time.time() - t
-        if dt >= 0.25 * target_s or n >= roots.shape[0]:
-            break
-        n = int(min(roots.shape[0], n * max(2.0, 0.3 * target_s / max(dt, 1e-3))))
-    return ref, rmap, cfg, d_max, roots, sample.shape[0] / dt, sample.shape[0], cores
+        self.rmap = self.ref.map_build(map_pts, cfgd["r"], cfgd["max_level"], 0.3, 16 << 30)
+        log(f"{log_prefix}reference map build (collision_target 0.3): {time.time() - t:.1f}s")
+        self.cfg = default_config(min_resolution=cfgd["r"], max_level=cfgd["max_level"],
+                                  roll_pitch_half_range=cfgd["rp"])
+        self.scan = scan
+        self.d_max = self.ref.max_range(scan)
+        self.roots = self.ref.initial_nodes(self.cfg, self.d_max, self.rmap.bbox(), cap=1 << 25)
+        self.rng = np.random.default_rng(11)
+
+    def time_sample(self, n, workers):
+        sample = self.roots[self.rng.choice(self.roots.shape[0], size=min(n, self.roots.shape[0]),
+                                            replace=False)]
+        t = time.time()
+        self.rmap.batch_evaluate(self.scan, self.cfg, sample, d_max=self.d_max, workers=workers)
+        return sample.shape[0], time.time() - t
+
+    def size_for(self, target_s, workers):
+        """Sample size whose batch_evaluate takes ~target_s seconds."""
+        n = 256
+        while True:
+            m, dt = self.time_sample(n, workers)
+            if dt >= 0.25 * target_s or m >= self.roots.shape[0]:
+                return max(1, min(self.roots.shape[0], int(m * target_s / max(dt, 1e-6))))
+            n = int(min(self.roots.shape[0], n * max(2.0, 0.3 * target_s / max(dt, 1e-3))))
+
+    def baseline(self, target_s, work_evals):
+        """cpu_baseline: all host threads and one thread, with the full
+        search's time extrapolated from the measured rate."""
+        cores = os.cpu_count() or 1
+        n = self.size_for(target_s, cores)
+        m, dt = self.time_sample(n, cores)
+        v_all = m / dt
+        n1 = self.size_for(max(1.0, target_s / 4), 1)
+        m1, dt1 = self.time_sample(n1, 1)
+        v_one = m1 / dt1
+        return {
+            "value": v_all, "unit": "evals/s", "cores": cores, "kind": "reference",
+            "cpu_model": cpu_model(),
+            "sample": (f"{m} root nodes drawn uniformly from initial_nodes() of the workload "
+                       f"(level {self.cfg.max_level}, K={self.scan.shape[0]}), bnbloc::batch_evaluate "
+                       f"with workers={cores} (oracle/_ref); {dt:.1f} s"),
+            "workers_1": {"value": v_one, "unit": "evals/s", "cores": 1,
+                          "sample": f"{m1} root nodes, workers=1; {dt1:.1f} s"},
+            "extrapolated_search_s": {
+                "all_threads": work_evals / v_all if work_evals else None,
+                "one_thread": work_evals / v_one if work_evals else None,
+                "note": "EXTRAPOLATION: the search's nodes_generated divided by the sampled "
+                        "root-batch rate (roots are ~98% of a C2 search's evaluations); not a "
+                        "timed full search"},
+        }
 
 
 def run_reference_arm(args, cfgd):
+    """--impl reference: the reference's own CPU implementation (oracle/_ref,
+    compiled from /root/reference by oracle/Makefile) on the box's host
+    cores.  Loads NO library of this repo's product: inputs come from the
+    reference's own gen_scene (oracle/_ref) and a pure-Python cut."""
     world, rank, _ = dist_env()
     if rank != 0:
         return
-    import paper_2310_10023_b200 as B  # scene generator only (no GPU work)
-    map_pts, scan, _ = build_inputs(B, cfgd)
-    ref, rmap, cfg, d_max, roots, _, n, cores = reference_sample(map_pts, scan, cfgd, 6.0)
-    rng = np.random.default_rng(5)
-    vals = []
-    t_all = 0.0
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    from pyoracle import Reference  # noqa: E402
+    ref = Reference()
+    spec = ref.default_spec()
+    for k, v in cfgd["spec"].items():
+        setattr(spec, k, v)
+    t = time.time()
+    map_pts, raw, _ = ref.gen_scene(spec, cfgd["seed"])
+    scan = H.cut_scan_py(raw, min(cfgd["K"], raw.shape[0]), 7)
+    log(f"reference scene: {map_pts.shape[0]} map pts, K={scan.shape[0]} ({time.time() - t:.1f}s)")
+    rs = RefSampler(map_pts, scan, cfgd)
+    cores = os.cpu_count() or 1
+    n = rs.size_for(args.ref_step_seconds, cores)
+    vals, t_all, n_all = [], 0.0, 0
     for step in range(args.warmup + args.steps):
-        sample = roots[rng.choice(roots.shape[0], size=n, replace=False)]
-        t = time.time()
-        rmap.batch_evaluate(scan, cfg, sample, d_max=d_max, workers=cores)
-        dt = time.time() - t
+        m, dt = rs.time_sample(n, cores)
         if step >= args.warmup:
-            vals.append(n / dt)
+            vals.append(m / dt)
             t_all += dt
-    value = args.steps * n / t_all
+            n_all += m
+    value = n_all / t_all
+    g = golden_search(args.config)
+    work = g["nodes_generated"] if g else None
     sample_desc = (f"{n} root nodes per step drawn uniformly from initial_nodes() of the workload "
                    f"(level {cfgd['max_level']}), bnbloc::batch_evaluate with workers={cores}")
     line = {
         "impl": "reference", "metric": "candidate score evals/sec", "value": value,
         "unit": "evals/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * t_all / args.steps, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": cfgd["workload"], "K": int(scan.shape[0])},
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (the reference's own gen_scene, oracle/_ref)",
+        "config": config_dict(cfgd, scan.shape[0], map_pts.shape[0]),
+        "parallelism": f"host threads x{cores} (parallel_chunks, parallel.hpp:16-42)",
         "cpu_baseline": {"value": value, "unit": "evals/s", "cores": cores, "kind": "reference",
-                         "sample": sample_desc},
+                         "cpu_model": cpu_model(), "sample": sample_desc},
         "e2e": {"value": value, "unit": "evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "extrapolated_search_s": (work / value) if work else None,
+        "extrapolation": "a full search() = the golden's nodes_generated / this rate (EXTRAPOLATION, "
+                         "not a timed search)",
     }
     print(json.dumps(line), flush=True)
 
@@ -268,15 +362,41 @@ def measured_peaks():
         return {"hbm_gbs": 6650.0}, "fallback"
 
 
-def profile_traffic(config, group):
-    """DRAM bytes per launch of a kernel group (read + write), from the ncu
-    launch list committed under profiles/ (scripts/traffic.py)."""
+def profile_summary(config):
+    """ncu evidence committed under profiles/ (scripts/traffic.py): DRAM
+    bytes per launch and speed-of-light percentages per kernel."""
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
-            g = json.load(f).get(config, {}).get(group)
-        return None if g is None else g["dram_bytes_per_launch"]
-    except (OSError, ValueError, KeyError):
-        return None
+            return json.load(f).get(config, {})
+    except (OSError, ValueError):
+        return {}
+
+
+def pose_parity(res, want, grids, r, exact):
+    """north_star: best score equal; pose equal, or (roots shard mode, where
+    the RotoTrans schedule legitimately differs) within one finest-level
+    voxel and one finest angular step."""
+    got = list(res.best_pose.as_tuple())
+    out = {"best_score": res.best_score, "golden_best_score": want["best_score"],
+           "score_ok": res.best_score == want["best_score"]}
+    if got == want["best_pose"]:
+        out["pose"] = "exact"
+    elif exact:
+        out["pose"] = "DIFFERS"
+    else:
+        d = [abs(a - b) for a, b in zip(got, want["best_pose"])]
+        d[5] = min(d[5], 2 * math.pi - d[5])
+        steps = [grids.axis(a, 0).step for a in range(3)]
+        ok = all(x <= r * (1 + 1e-9) for x in d[:3]) and all(
+            d[3 + a] <= steps[a] * (1 + 1e-9) for a in range(3))
+        out["pose"] = "within one finest voxel / angular step" if ok else "OUT OF TOLERANCE"
+    if exact:
+        out["stats_ok"] = (res.stats.nodes_generated, res.stats.nodes_pruned,
+                           res.stats.batches_flushed) == (want["nodes_generated"], want["nodes_pruned"],
+                                                          want["batches_flushed"])
+    out["ok"] = out["score_ok"] and out["pose"] != "DIFFERS" and out["pose"] != "OUT OF TOLERANCE" \
+        and out.get("stats_ok", True)
+    return out
 
 
 def run_b200_arm(args, cfgd):
@@ -291,7 +411,7 @@ def run_b200_arm(args, cfgd):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     import paper_2310_10023_b200 as B
 
-    map_pts, scan, gt = build_inputs(B, cfgd)
+    map_pts, scan, gt = build_inputs(cfgd)
     cfg = search_config(B, cfgd)
     stream = torch.cuda.current_stream()
     vmap = B.MultiResVoxelMap.build(map_pts, cfgd["r"], cfgd["max_level"],
@@ -303,6 +423,12 @@ def run_b200_arm(args, cfgd):
     log(f"rank {rank}: map build {build_ms:.1f} ms device, layouts {layouts}, bytes {level_bytes}")
     dscan = B.DeviceScan(vmap, scan)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")  # > 126 MB L2
+    K = int(scan.shape[0])
+
+    # the single-queue search (= the reference's schedule): its
+    # nodes_generated is the work W of one step at every N
+    single = B.search_scan(vmap, dscan, cfg)
+    work = int(single.stats.nodes_generated)
 
     if sharded:
         import torch.distributed as dist
@@ -343,28 +469,38 @@ def run_b200_arm(args, cfgd):
     barrier()
     clk = clocks.stop()
     t_local = sum(step_ms)
-    evals_local = sum(r.stats.nodes_generated for r in results)
-    # roots mode: ranks search disjoint subtrees (sum); exact mode: every rank
-    # reports the whole search's Stats (count them once)
-    ev_op = "MAX" if args.shard_mode == "exact" else "SUM"
+    executed_local = sum(r.stats.nodes_generated for r in results)
     if sharded:
         import torch.distributed as dist
         tt = torch.tensor([t_local], dtype=torch.float64, device="cuda")
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        ev = torch.tensor([evals_local], dtype=torch.int64, device="cuda")
-        dist.all_reduce(ev, op=getattr(dist.ReduceOp, ev_op))
-        t_max, evals = float(tt.item()), int(ev.item())
+        ev = torch.tensor([executed_local], dtype=torch.int64, device="cuda")
+        # exact mode: every rank reports the whole search's Stats
+        dist.all_reduce(ev, op=dist.ReduceOp.MAX if args.shard_mode == "exact" else dist.ReduceOp.SUM)
+        t_max, executed = float(tt.item()), int(ev.item())
     else:
-        t_max, evals = t_local, evals_local
-    value = evals / (t_max * 1e-3)
+        t_max, executed = t_local, executed_local
+    value = work * args.steps / (t_max * 1e-3)
     r0 = results[-1]
-    K = int(scan.shape[0])
+
+    # ---- parity against the reference's golden search()
+    want = golden_search(args.config)
+    grids = B.AngularGrid(cfg, B.max_range(scan))
+    exact = (not sharded) or args.shard_mode == "exact"
+    if want is not None:
+        parity = pose_parity(r0, want, grids, cfgd["r"], exact)
+        parity["golden"] = f"tests/golden/{GOLDENS[args.config]} (reference search(), oracle/_ref)"
+        parity["work_matches_golden"] = work == want["nodes_generated"]
+    else:
+        parity = {"golden": None, "note": "no reference golden for this config"}
+    if rank == 0 and want is not None and not parity["ok"]:
+        log(f"PARITY FAILURE: {parity}")
 
     # ---- e2e through the public host API (pinned host scan, result read back)
     pinned = torch.empty((K, 3), dtype=torch.float64, pin_memory=True)
     pinned.copy_(torch.from_numpy(scan))
     host_scan = pinned.numpy()
-    e2e_t, e2e_evals, h2d, d2h = 0.0, 0, 0, 0
+    e2e_t, h2d, d2h = 0.0, 0, 0
     if not sharded:
         B.search(vmap, host_scan, cfg)  # warm
         for _ in range(args.steps):
@@ -373,11 +509,10 @@ def run_b200_arm(args, cfgd):
             t = time.perf_counter()
             re = B.search(vmap, host_scan, cfg)
             e2e_t += time.perf_counter() - t
-            e2e_evals += re.stats.nodes_generated
             h2d, d2h = re.h2d_bytes, re.d2h_bytes
-        e2e = {"value": e2e_evals / e2e_t, "unit": "evals/s", "h2d_bytes_per_step": int(h2d),
+        e2e = {"value": work * args.steps / e2e_t, "unit": "evals/s", "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h), "ms_per_step": 1e3 * e2e_t / args.steps,
-               "timing": "host wall clock around bbs_search()"}
+               "timing": "host wall clock around bbs_search() (scan copied in, result read back)"}
     else:
         # sharded e2e: the scan is re-uploaded from pinned memory every step
         for _ in range(args.steps):
@@ -388,103 +523,97 @@ def run_b200_arm(args, cfgd):
             re = one_search(ds)
             barrier()
             e2e_t += time.perf_counter() - t
-            e2e_evals += re.stats.nodes_generated
             h2d, d2h = re.h2d_bytes + 24 * K, re.d2h_bytes
         import torch.distributed as dist
         tt = torch.tensor([e2e_t], dtype=torch.float64, device="cuda")
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        ev = torch.tensor([e2e_evals], dtype=torch.int64, device="cuda")
-        dist.all_reduce(ev, op=getattr(dist.ReduceOp, ev_op))
-        e2e = {"value": int(ev.item()) / float(tt.item()), "unit": "evals/s",
+        e2e = {"value": work * args.steps / float(tt.item()), "unit": "evals/s",
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                "ms_per_step": 1e3 * float(tt.item()) / args.steps,
-               "timing": "host wall clock, max over ranks"}
+               "timing": "host wall clock (scan upload + sharded search), max over ranks"}
 
-    # ---- roofline of the dominant kernel
+    # ---- roofline of the dominant kernel: the root column kernel
+    # (root_colpad_kernel, the largest single launch of a step, profiles/).
+    # Algorithmic bytes = the z-column words it actually gathers from its
+    # staged shared-memory window (4 B each, counted on the device): one word
+    # per (translation column, de-duplicated histogram entry), which answers
+    # all nz z-translations of that column at once.  Peak = the measured
+    # conflict-free shared-memory read ceiling of this GPU (bbs_smem_bench).
     peaks, peak_kind = measured_peaks()
-    root_ms = statistics.mean(r.root_score_ms for r in results)
-    epoch_ms = statistics.mean(r.epoch_score_ms for r in results)
-    root_probes = statistics.mean(r.root_probes for r in results)
-    epoch_lookups = statistics.mean((r.stats.nodes_generated - r.root_nodes) * K for r in results)
-    if root_ms >= epoch_ms:
-        group, ms, probes = "root", root_ms, root_probes
-        kern = "root batch: root_hist_kernel + root_colpad_kernel (batch_evaluate on initial_nodes)"
-        launches_per_step = 1
-    else:
-        group, ms, probes = "flush", epoch_ms, epoch_lookups
-        kern = ("flush scoring, per epoch: cache_build_kernel + cache_probe_kernel + "
-                "score_cube8_kernel (batch_evaluate on each flushed batch)")
-        launches_per_step = max(1, statistics.mean(r.epochs for r in results))
-    bytes_per_launch = probes * 32.0 / launches_per_step
-    achieved = bytes_per_launch / (ms / launches_per_step * 1e-3) / 1e9
-    peak = float(peaks.get("hbm_gbs", 6650.0))
-    gather = {}
+    col_ms = statistics.mean(r.root_col_ms for r in results)
+    words = statistics.mean(r.root_words for r in results)
+    smem_gbs = gather_l2 = gather_hbm = None
     if rank == 0 and not args.no_gather_bench:
         import ctypes as C
-        for label, nbytes in (("l2_64MiB", 64 << 20), ("hbm_4GiB", 4 << 30)):
-            out = C.c_double()
+        out = C.c_double()
+        if B.lib.bbs_smem_bench(local, C.byref(out)) == 0:
+            smem_gbs = round(out.value, 1)
+        for label, nbytes in (("l2", 64 << 20), ("hbm", 4 << 30)):
             if B.lib.bbs_gather_bench(local, nbytes, C.byref(out)) == 0:
-                gather[label] = round(out.value, 1)
-    traffic = profile_traffic(args.config, group)
-    launch_ms = ms / launches_per_step
-    dram_gbs = (traffic / (launch_ms * 1e-3) / 1e9) if traffic else None
+                if label == "l2":
+                    gather_l2 = round(out.value, 1)
+                else:
+                    gather_hbm = round(out.value, 1)
+    achieved = (words * 4.0 / (col_ms * 1e-3) / 1e9) if col_ms > 0 else None
+    prof = profile_summary(args.config)
+    col_prof = prof.get("root_colpad_kernel", {})
+    traffic = col_prof.get("dram_bytes_per_launch")
     roofline = {
-        "bound": "hbm", "kernel": kern, "achieved": achieved, "peak": peak, "unit": "GB/s",
-        "frac": achieved / peak, "traffic": traffic,
-        # what the kernels actually pull from DRAM per second (ncu bytes per
-        # launch / in-run launch time): the tables live in L2 / shared memory
-        "dram_gbs": dram_gbs, "dram_frac": (dram_gbs / peak) if dram_gbs else None,
-        "traffic_source": "profiles/ncu_traffic.json: dram__bytes_read.sum + dram__bytes_write.sum "
-                          "per launch of the group, ncu launch list (scripts/traffic.py)",
-        "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
-        "algorithmic_bytes_per_launch": bytes_per_launch,
-        "unit_of_work": "one membership probe = one random 32 B sector (SURVEY §8d)",
-        "kernel_ms_per_step": ms, "gather_peaks_gbs": gather,
-        "frac_of_l2_gather": (achieved / gather["l2_64MiB"]) if gather.get("l2_64MiB") else None,
-        "note": ("achieved counts SURVEY §8d's unit: one random 32 B sector per (node, scan point) "
-                 "lookup in the flush batches, per de-duplicated (root, voxel offset) probe in the "
-                 "root batch.  The kernels issue far fewer memory operations than that model: per "
-                 "(level, rotation) histograms de-duplicate the scan's voxel offsets (C2: 10k points "
-                 "-> ~2k entries), a 2x2x2 child cube is answered with 4 z-column words and a root "
-                 "z-column with one, from shared-memory windows of the z-column bitmap; frac > 1 means "
-                 "the algorithm beats the per-lookup gather roofline.  The measured limiter is SM "
-                 "issue / latency (profiles/)"),
+        "bound": "smem", "kernel": "root_colpad_kernel (root batch: batch_evaluate on initial_nodes)",
+        "achieved": achieved, "peak": smem_gbs, "unit": "GB/s",
+        "frac": (achieved / smem_gbs) if (achieved and smem_gbs) else None,
+        "traffic": traffic,
+        "algorithmic_bytes_per_launch": words * 4.0,
+        "kernel_ms_per_step": col_ms,
+        "unit_of_work": "one 4 B z-column word gathered from the staged shared-memory window per "
+                        "(translation column, de-duplicated scan-voxel offset); one word answers every "
+                        "z-translation of the column",
+        "peak_source": "measured in this run: bbs_smem_bench, conflict-free LDS.32 over all 148 SMs "
+                       "(MEASURED_PEAKS.json has no shared-memory figure)",
+        "ncu": {k: col_prof.get(k) for k in ("sm_throughput_pct", "memory_throughput_pct",
+                                             "l1tex_throughput_pct", "ipc_active", "achieved_occupancy_pct",
+                                             "source")},
+        "traffic_source": "profiles/ncu_traffic.json (dram__bytes_read.sum + dram__bytes_write.sum per launch)",
+        "context": {"hbm_copy_gbs": peaks.get("hbm_gbs"), "hbm_peak_source": f"MEASURED_PEAKS.json ({peak_kind})",
+                    "l2_random_sector_gather_gbs": gather_l2, "hbm_random_sector_gather_gbs": gather_hbm,
+                    "survey_lookup_model": {
+                        "lookups_per_s": r0.lookups / (statistics.mean(step_ms) * 1e-3),
+                        "note": "SURVEY §8d's per-(node, scan point) lookup count (nodes_generated x K): "
+                                "an effective rate, not a traffic figure; histogram de-duplication and "
+                                "column words make the kernels issue far fewer loads"}},
     }
 
     line = {
         "metric": "candidate score evals/sec", "value": value, "unit": "evals/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": t_max / args.steps, "higher_is_better": True,
-        "scaling": "strong" if world > 1 else "strong", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (gen_scene restatement, bit-identical to the reference's)",
-        "config": {"workload": cfgd["workload"], "K": K, "map_points": int(map_pts.shape[0]),
-                   "parallelism": (f"{args.shard_mode}-shard x{world}, NCCL incumbent/score "
-                                   "all-reduce on the search stream") if sharded else "single GPU",
-                   "l2": "flushed (256 MiB write) before every timed step",
-                   "layouts": layouts},
-        "latency_ms": {"localization_total": statistics.mean(r.stats.localization_total_ms()
-                                                              for r in results),
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (harness gen_scene restatement, bit-identical to the reference's)",
+        "config": config_dict(cfgd, K, map_pts.shape[0]),
+        "parallelism": (f"{args.shard_mode}-shard x{world}, NCCL incumbent/score all-reduce on the "
+                        "search stream") if sharded else "single GPU",
+        "work_evals_per_step": work,
+        "executed_evals_per_step": executed / args.steps,
+        "latency_ms": {"localization_total": t_max / args.steps,
                        "initial_nodes": statistics.mean(r.stats.initial_nodes_ms for r in results),
                        "find_best_score": statistics.mean(r.stats.find_best_score_ms for r in results),
                        "pop_remaining_queue": statistics.mean(r.stats.pop_remaining_queue_ms
                                                               for r in results),
-                       "create_voxel_maps": build_ms},
+                       "create_voxel_maps": build_ms,
+                       "note": "localization_total = max-rank device time per step (CUDA events)"},
         "search": {"best_score": r0.best_score, "matched": r0.matched,
                    "nodes_generated": r0.stats.nodes_generated, "epochs": r0.epochs,
                    "root_nodes": r0.root_nodes, "root_probes": r0.root_probes,
-                   "lookups_per_s": r0.lookups / (statistics.mean(step_ms) * 1e-3),
+                   "root_words": r0.root_words, "layouts": layouts,
                    "trans_err_m": math.dist(r0.best_pose.as_tuple()[:3], gt.as_tuple()[:3])},
+        "parity": parity,
         "e2e": e2e, "roofline": roofline, "clocks": clk,
         "gpu_launches": int(sum(r.kernel_launches for r in results)),
     }
     if world == 1 and rank == 0 and not args.no_cpu_baseline:
         try:
-            _, _, _, _, _, cpu_val, n, cores = reference_sample(map_pts, scan, cfgd,
-                                                               args.cpu_seconds, "cpu_baseline: ")
-            line["cpu_baseline"] = {
-                "value": cpu_val, "unit": "evals/s", "cores": cores, "kind": "reference",
-                "sample": f"{n} root nodes drawn uniformly from initial_nodes() of the workload, "
-                          f"bnbloc::batch_evaluate with workers={cores} (oracle/_ref)"}
+            rs = RefSampler(map_pts, scan, cfgd, "cpu_baseline: ")
+            line["cpu_baseline"] = rs.baseline(args.cpu_seconds, work)
         except Exception as exc:  # noqa: BLE001
             line["cpu_baseline"] = {"value": None, "unit": "evals/s", "cores": os.cpu_count(),
                                     "kind": "reference", "sample": f"unavailable: {exc}"}
@@ -494,6 +623,8 @@ def run_b200_arm(args, cfgd):
         torch.cuda.synchronize()
         comm.close()
         torch.distributed.destroy_process_group()
+    if want is not None and exact and not parity["ok"]:
+        sys.exit(3)  # the single-queue schedule must equal the reference exactly
 
 
 def run_b200_throughput(args, cfgd):
@@ -580,7 +711,7 @@ def run_b200_throughput(args, cfgd):
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": t_max / args.steps, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (gen_scene restatement, bit-identical to the reference's)",
+        "data": "synthetic (harness gen_scene restatement, bit-identical to the reference's)",
         "config": {"workload": cfgd["workload"], "scans": len(scans), "K": cfgd["K"],
                    "parallelism": f"replicas x{world}, {T} concurrent searches per GPU (bbs_search_scans)",
                    "l2": "flushed (256 MiB write) before every timed step"},
@@ -598,6 +729,20 @@ def run_b200_throughput(args, cfgd):
         torch.distributed.destroy_process_group()
 
 
+def spawn_ranks(args):
+    """--gpus N outside torchrun: re-launch this script as N ranks, one per
+    GPU, under torch.distributed.run (rendezvous on 127.0.0.1)."""
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1", f"--master-port={port}",
+           os.path.abspath(__file__)] + sys.argv[1:]
+    log("launching: " + " ".join(cmd))
+    return subprocess.call(cmd)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -609,7 +754,10 @@ def main():
     ap.add_argument("--shard-mode", choices=["roots", "exact"], default="roots",
                     help="N>1: roots = own BnB per rank over its root share + incumbent "
                          "all-reduce; exact = batch-split replay of the single-queue schedule")
-    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--cpu-seconds", type=float, default=8.0,
+                    help="cpu_baseline: seconds of reference work per leg")
+    ap.add_argument("--ref-step-seconds", type=float, default=6.0,
+                    help="--impl reference: seconds of reference work per step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-gather-bench", action="store_true")
     args = ap.parse_args()
@@ -617,6 +765,8 @@ def main():
         log("warmup raised to 3 (contract minimum)")
         args.warmup = 3
     cfgd = CONFIGS[args.config]
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl == "b200":
+        sys.exit(spawn_ranks(args))
     if args.impl == "reference":
         run_reference_arm(args, cfgd)
     elif "n_scans" in cfgd:

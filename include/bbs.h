@@ -136,6 +136,8 @@ typedef struct bbs_search_result {
   uint64_t d2h_bytes;     /* device->host bytes copied by this call */
   uint64_t kernel_launches; /* launches of this library's own kernels (CUB launches excluded) */
   uint64_t evals_per_level[16]; /* nodes scored per tree level (roots included) */
+  uint64_t root_words;    /* z-column words the root column kernel read (its actual gathers) */
+  double root_col_ms;     /* device time of the root column kernel launches, CUDA events */
 } bbs_search_result;
 
 /* AxisGrid, angular_grid.hpp:45-58. */
@@ -197,8 +199,8 @@ int bbs_prepare_source(const double* xyz, uint64_t n, uint64_t target_points, do
  * `device`.  Leaf, convergence flag, voxel set and output order equal the
  * reference's; a voxel's centroid sums its points in input order (the
  * reference in std::sort's unstable order), so centroids of voxels with >= 3
- * points may differ from bbs_prepare_source in the last bits.  Used by
- * bbs_localize_scan. */
+ * points may differ from bbs_prepare_source in the last bits.  The fast
+ * path of bbs_localize_scan_ex(..., BBS_PREPARE_DEVICE). */
 int bbs_prepare_source_device(int32_t device, const double* xyz, uint64_t n, uint64_t target_points,
                               double* out_xyz, uint64_t capacity, uint64_t* count, double* leaf,
                               int32_t* converged, double* d_max);
@@ -265,11 +267,22 @@ int bbs_batch_evaluate(bbs_map_t map, const double* scan_xyz, uint64_t k,
 /* search, search.hpp:72-186. */
 int bbs_search(bbs_map_t map, const double* scan_xyz, uint64_t k, const bbs_search_config* cfg,
                bbs_search_result* result);
-/* localize_scan, pipeline.hpp:45-51 (prepare_source on the device, see
- * bbs_prepare_source_device). */
+/* localize_scan, pipeline.hpp:45-51: prepare_source, then search.
+ * prepare_source runs auto_leaf's voxel counts on the device; the
+ * centroids are summed in the reference's order (bit-identical to the
+ * reference's localize_scan).  = bbs_localize_scan_ex(..., BBS_PREPARE_EXACT). */
 int bbs_localize_scan(bbs_map_t map, const double* raw_xyz, uint64_t n,
                       const bbs_search_config* cfg, uint64_t downsample_target,
                       bbs_search_result* result);
+enum {
+  BBS_PREPARE_EXACT = 0,  /* centroids in the reference's std::sort order (host replay) */
+  BBS_PREPARE_DEVICE = 1  /* centroids summed on the device in input order (faster; a voxel of
+                             >= 3 points may differ in the last bits, see
+                             bbs_prepare_source_device) */
+};
+int bbs_localize_scan_ex(bbs_map_t map, const double* raw_xyz, uint64_t n,
+                         const bbs_search_config* cfg, uint64_t downsample_target, int32_t prepare,
+                         bbs_search_result* result);
 
 /* Device-resident scan: upload once, search many times with no host copy
  * of the scan inside the call. */
@@ -397,6 +410,9 @@ int bbs_search_scan_dump(bbs_map_t map, bbs_scan_t scan, const bbs_search_config
 /* Random independent 32-byte gather ceiling over a `bytes` buffer on
  * `device` (SURVEY §8d tier ceilings): sector GB/s. */
 int bbs_gather_bench(int32_t device, uint64_t bytes, double* out_gbs);
+/* Conflict-free random 4-byte shared-memory read ceiling of the whole GPU
+ * (GB/s): the tier the root column kernel gathers from. */
+int bbs_smem_bench(int32_t device, double* out_gbs);
 
 #ifdef __cplusplus
 }  /* extern "C" */

@@ -12,15 +12,29 @@ cpu_baseline legs may import this module, and only as the checker or the
 timed CPU baseline — never as the product path.
 """
 import ctypes as C
+import importlib.util
 import os
 
 import numpy as np
 
-from paper_2310_10023_b200._abi import (
-    Aabb, AxisGridC, Node, SearchConfigC, SearchResultC, Shard, STATUS_NAMES,
-)
-
 HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+def _load_abi_structs():
+    """The C-ABI struct layouts (paper_2310_10023_b200/_abi.py: ctypes only),
+    loaded by file path so that importing the checker never imports the
+    product package (which would load libbbs_b200.so into the process)."""
+    path = os.path.join(os.path.dirname(HERE), "paper_2310_10023_b200", "_abi.py")
+    spec = importlib.util.spec_from_file_location("bbs_abi_structs", path)
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    return mod
+
+
+_abi = _load_abi_structs()
+Aabb, AxisGridC, Node, SearchConfigC = _abi.Aabb, _abi.AxisGridC, _abi.Node, _abi.SearchConfigC
+SearchResultC, Shard, STATUS_NAMES = _abi.SearchResultC, _abi.Shard, _abi.STATUS_NAMES
+
 RESTATED_SO = os.path.join(HERE, "liboracle.so")
 REFERENCE_SO = os.path.join(HERE, "_ref", "libbnbloc_ref.so")
 

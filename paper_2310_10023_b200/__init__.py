@@ -234,6 +234,8 @@ class SearchResult:
     d2h_bytes: int = 0
     kernel_launches: int = 0
     evals_per_level: tuple = ()
+    root_words: int = 0
+    root_col_ms: float = 0.0
 
 
 def _result_from_c(r: SearchResultC, trace_buf=None) -> SearchResult:
@@ -248,7 +250,8 @@ def _result_from_c(r: SearchResultC, trace_buf=None) -> SearchResult:
         epochs=r.epochs, lookups=r.lookups, device_ms=r.device_ms, root_score_ms=r.root_score_ms,
         epoch_score_ms=r.epoch_score_ms, root_nodes=r.root_nodes, queue_peak=r.queue_peak,
         root_probes=r.root_probes, h2d_bytes=r.h2d_bytes, d2h_bytes=r.d2h_bytes,
-        kernel_launches=r.kernel_launches, evals_per_level=tuple(r.evals_per_level))
+        kernel_launches=r.kernel_launches, evals_per_level=tuple(r.evals_per_level),
+        root_words=r.root_words, root_col_ms=r.root_col_ms)
     if trace_buf is not None:
         out.best_score_trace = list(trace_buf[: min(r.trace_length, len(trace_buf))])
     return out
@@ -838,13 +841,18 @@ def search_sharded(vmap: MultiResVoxelMap, dscan: DeviceScan, cfg: SearchConfig,
 
 
 def localize_scan(vmap: MultiResVoxelMap, raw_scan, cfg: SearchConfig, downsample_target,
-                  trace_capacity=1 << 16):
-    """pipeline.hpp:45-51."""
+                  trace_capacity=1 << 16, prepare="exact"):
+    """pipeline.hpp:45-51.  prepare="exact" (default): centroids in the
+    reference's summation order, bit-identical to the reference;
+    "device": centroids summed on the device (faster, last-bit differences
+    possible for voxels of >= 3 points)."""
+    if prepare not in ("exact", "device"):
+        raise ValueError(f"unknown prepare mode {prepare!r}")
     s = _xyz(raw_scan)
     res, buf = _new_result(trace_capacity if cfg.collect_trace else 0)
     c = cfg.to_c()
-    _check(lib.bbs_localize_scan(vmap._h, _dptr(s), s.shape[0], C.byref(c), int(downsample_target),
-                                 C.byref(res)))
+    _check(lib.bbs_localize_scan_ex(vmap._h, _dptr(s), s.shape[0], C.byref(c), int(downsample_target),
+                                    0 if prepare == "exact" else 1, C.byref(res)))
     return _result_from_c(res, buf)
 
 

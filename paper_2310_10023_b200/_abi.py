@@ -97,6 +97,8 @@ class SearchResultC(C.Structure):
         ("d2h_bytes", C.c_uint64),
         ("kernel_launches", C.c_uint64),
         ("evals_per_level", C.c_uint64 * 16),
+        ("root_words", C.c_uint64),
+        ("root_col_ms", C.c_double),
     ]
 
 

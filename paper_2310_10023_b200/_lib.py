@@ -67,6 +67,8 @@ SIGNATURES = {
     "bbs_search": (C.c_int, [_vp, _dp, _u64, C.POINTER(SearchConfigC), C.POINTER(SearchResultC)]),
     "bbs_oracle_search": (C.c_int, [_vp, _dp, _u64, C.POINTER(SearchConfigC), _ip,
                                     C.POINTER(Node), _u64, C.POINTER(_u64), C.POINTER(_u64)]),
+    "bbs_localize_scan_ex": (C.c_int, [_vp, _dp, _u64, C.POINTER(SearchConfigC), _u64, _i32,
+                                       C.POINTER(SearchResultC)]),
     "bbs_localize_scan": (C.c_int, [_vp, _dp, _u64, C.POINTER(SearchConfigC), _u64,
                                     C.POINTER(SearchResultC)]),
     "bbs_scan_upload": (C.c_int, [_vp, _dp, _u64, C.POINTER(_vp)]),
@@ -89,6 +91,7 @@ SIGNATURES = {
     "bbs_comm_free": (C.c_int, [_vp]),
     "bbs_nccl_version": (C.c_int, []),
     "bbs_gather_bench": (C.c_int, [_i32, _u64, _dp]),
+    "bbs_smem_bench": (C.c_int, [_i32, _dp]),
 }
 
 for _name, (_res, _args) in SIGNATURES.items():

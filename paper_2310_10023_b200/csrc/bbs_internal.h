@@ -110,8 +110,16 @@ struct SourcePrep {
   double d_max = 0.0;
 };
 SourcePrep host_prepare_source(const double* xyz, uint64_t n, uint64_t target);
-// The same on the device (source_prep.cu): exact leaf, convergence, voxel set
-// and order; centroid sums in input order within a voxel.
-SourcePrep device_prepare_source(int device, const double* xyz, uint64_t n, uint64_t target);
+// voxel_grid_downsample, point_cloud.hpp:78-111 (host, the reference's
+// summation order).
+std::vector<double> host_voxel_grid_downsample(const double* xyz, uint64_t n, double leaf);
+// The same on the device (source_prep.cu): auto_leaf's voxel counts on the
+// device (exact leaf, convergence, voxel set and order).  Centroids:
+// exact_centroids = true sums each voxel in the reference's std::sort order
+// (host_voxel_grid_downsample at the device-found leaf: bit-identical to the
+// reference); false sums on the device in input order (fast path; voxels of
+// >= 3 points may differ in the last bits).
+SourcePrep device_prepare_source(int device, const double* xyz, uint64_t n, uint64_t target,
+                                 bool exact_centroids = true);
 
 }  // namespace bbs

@@ -179,7 +179,7 @@ int bbs_prepare_source_device(int32_t device, const double* xyz, uint64_t n, uin
   return guard([&] {
     REQUIRE(count && (xyz || n == 0), "bbs_prepare_source_device: null argument");
     require_device(device);
-    const bbs::SourcePrep p = bbs::device_prepare_source(device, xyz, n, target);
+    const bbs::SourcePrep p = bbs::device_prepare_source(device, xyz, n, target, false);
     const uint64_t m = p.xyz.size() / 3;
     *count = m;
     if (out_xyz) std::memcpy(out_xyz, p.xyz.data(), 3 * std::min(m, capacity) * sizeof(double));
@@ -494,12 +494,19 @@ int bbs_search(bbs_map_t map, const double* scan_xyz, uint64_t k, const bbs_sear
 
 int bbs_localize_scan(bbs_map_t map, const double* raw_xyz, uint64_t n, const bbs_search_config* cfg,
                       uint64_t downsample_target, bbs_search_result* result) {
+  return bbs_localize_scan_ex(map, raw_xyz, n, cfg, downsample_target, BBS_PREPARE_EXACT, result);
+}
+
+int bbs_localize_scan_ex(bbs_map_t map, const double* raw_xyz, uint64_t n, const bbs_search_config* cfg,
+                         uint64_t downsample_target, int32_t prepare, bbs_search_result* result) {
   return guard([&] {
     REQUIRE(map && cfg && result && (raw_xyz || n == 0), "null argument");
-    // prepare_source, pipeline.hpp:25-41 (device voxel counts and centroids),
-    // then search (pipeline.hpp:48)
+    REQUIRE(prepare == BBS_PREPARE_EXACT || prepare == BBS_PREPARE_DEVICE, "unknown prepare mode");
+    // prepare_source, pipeline.hpp:25-41 (device voxel counts; centroids in
+    // the reference's order, or on the device), then search (pipeline.hpp:48)
     const auto t0 = std::chrono::steady_clock::now();
-    const bbs::SourcePrep prep = bbs::device_prepare_source(map->device, raw_xyz, n, downsample_target);
+    const bbs::SourcePrep prep =
+        bbs::device_prepare_source(map->device, raw_xyz, n, downsample_target, prepare == BBS_PREPARE_EXACT);
     const double prep_ms =
         std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     const uint64_t k = prep.xyz.size() / 3;

@@ -163,40 +163,81 @@ struct VoxelAccum {  // point_cloud.hpp:66-70
   uint32_t count;
 };
 
-// voxel_grid_downsample, point_cloud.hpp:78-111.  std::sort with the same
-// comparator over the same input order reproduces the reference's
-// permutation, and so its summation order.
+// voxel_grid_downsample, point_cloud.hpp:78-111.  The reference std::sorts
+// 40-byte VoxelAccum records by (vx, vy, vz) and sums each voxel's points in
+// the sorted order.  libstdc++'s introsort takes every decision from the
+// comparator alone, so ANY element type whose comparisons come out the same
+// yields the same permutation: when the voxel box packs into 64 bits, a
+// monotone packed key + point index (16 B) is sorted instead (same
+// permutation, ~2.5x less data moved); otherwise the reference's own record
+// layout is sorted.  Either way the sums run in the reference's order.
 std::vector<double> voxel_grid_downsample(const double* xyz, uint64_t n, double leaf) {
   if (n == 0) throw Error(BBS_ERR_EMPTY_CLOUD, "voxel_grid_downsample: empty cloud");
   if (!(leaf > 0.0)) throw Error(BBS_ERR_CONFIG, "voxel_grid_downsample: leaf must be > 0");
+  std::vector<int64_t> v(3 * n);
+  int64_t mn[3] = {INT64_MAX, INT64_MAX, INT64_MAX}, mx[3] = {INT64_MIN, INT64_MIN, INT64_MIN};
+  for (uint64_t i = 0; i < n; ++i)
+    for (int a = 0; a < 3; ++a) {
+      const int64_t c = to_i64(std::floor(xyz[3 * i + a] / leaf));
+      v[3 * i + a] = c;
+      mn[a] = std::min(mn[a], c);
+      mx[a] = std::max(mx[a], c);
+    }
+  int bits[3];
+  for (int a = 0; a < 3; ++a) {
+    const uint64_t span = static_cast<uint64_t>(mx[a]) - static_cast<uint64_t>(mn[a]);
+    bits[a] = 0;
+    while (bits[a] < 64 && (span >> bits[a]) != 0) ++bits[a];
+  }
+  std::vector<double> out;
+  auto emit = [&](auto&& point_of, std::size_t m, auto&& same) {
+    std::size_t i = 0;
+    while (i < m) {
+      std::size_t j = i + 1;
+      const double* p0 = point_of(i);
+      double sx = p0[0], sy = p0[1], sz = p0[2];
+      while (j < m && same(i, j)) {
+        const double* p = point_of(j);
+        sx += p[0];
+        sy += p[1];
+        sz += p[2];
+        ++j;
+      }
+      const double cnt = static_cast<double>(j - i);
+      out.push_back(sx / cnt);
+      out.push_back(sy / cnt);
+      out.push_back(sz / cnt);
+      i = j;
+    }
+  };
+  if (bits[0] + bits[1] + bits[2] <= 64) {
+    struct KeyIdx {
+      uint64_t key;
+      uint64_t idx;
+    };
+    std::vector<KeyIdx> cells(n);
+    for (uint64_t i = 0; i < n; ++i) {
+      const uint64_t kx = static_cast<uint64_t>(v[3 * i]) - static_cast<uint64_t>(mn[0]);
+      const uint64_t ky = static_cast<uint64_t>(v[3 * i + 1]) - static_cast<uint64_t>(mn[1]);
+      const uint64_t kz = static_cast<uint64_t>(v[3 * i + 2]) - static_cast<uint64_t>(mn[2]);
+      auto shl = [](uint64_t x, int b) { return b >= 64 ? uint64_t(0) : x << b; };
+      cells[i] = {shl(shl(kx, bits[1]) | ky, bits[2]) | kz, i};  // monotone in (vx, vy, vz)
+    }
+    std::sort(cells.begin(), cells.end(), [](const KeyIdx& a, const KeyIdx& b) { return a.key < b.key; });
+    emit([&](std::size_t i) { return xyz + 3 * cells[i].idx; }, cells.size(),
+         [&](std::size_t i, std::size_t j) { return cells[j].key == cells[i].key; });
+    return out;
+  }
   std::vector<VoxelAccum> cells;
   cells.reserve(n);
-  for (uint64_t i = 0; i < n; ++i) {
-    const double x = xyz[3 * i], y = xyz[3 * i + 1], z = xyz[3 * i + 2];
-    cells.push_back({to_i64(std::floor(x / leaf)), to_i64(std::floor(y / leaf)),
-                     to_i64(std::floor(z / leaf)), x, y, z, 1});
-  }
+  for (uint64_t i = 0; i < n; ++i)
+    cells.push_back({v[3 * i], v[3 * i + 1], v[3 * i + 2], xyz[3 * i], xyz[3 * i + 1], xyz[3 * i + 2], 1});
   std::sort(cells.begin(), cells.end(), [](const VoxelAccum& a, const VoxelAccum& b) {
     return std::tie(a.vx, a.vy, a.vz) < std::tie(b.vx, b.vy, b.vz);
   });
-  std::vector<double> out;
-  std::size_t i = 0;
-  while (i < cells.size()) {
-    std::size_t j = i + 1;
-    double sx = cells[i].sx, sy = cells[i].sy, sz = cells[i].sz;
-    while (j < cells.size() && cells[j].vx == cells[i].vx && cells[j].vy == cells[i].vy &&
-           cells[j].vz == cells[i].vz) {
-      sx += cells[j].sx;
-      sy += cells[j].sy;
-      sz += cells[j].sz;
-      ++j;
-    }
-    const double cnt = static_cast<double>(j - i);
-    out.push_back(sx / cnt);
-    out.push_back(sy / cnt);
-    out.push_back(sz / cnt);
-    i = j;
-  }
+  emit([&](std::size_t i) { return &cells[i].sx; }, cells.size(), [&](std::size_t i, std::size_t j) {
+    return cells[j].vx == cells[i].vx && cells[j].vy == cells[i].vy && cells[j].vz == cells[i].vz;
+  });
   return out;
 }
 
@@ -256,6 +297,10 @@ AutoLeaf auto_leaf(const double* xyz, uint64_t n, std::size_t target) {
 }
 
 }  // namespace
+
+std::vector<double> host_voxel_grid_downsample(const double* xyz, uint64_t n, double leaf) {
+  return voxel_grid_downsample(xyz, n, leaf);
+}
 
 // prepare_source, pipeline.hpp:25-41.
 SourcePrep host_prepare_source(const double* xyz, uint64_t n, uint64_t target) {

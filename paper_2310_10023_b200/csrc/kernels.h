@@ -99,10 +99,14 @@ void launch_score_box_chunked(const MapView& map, const GridView& grid, const Sc
 
 // Score every root owned by (rank, world) into scores[ref index], where
 // ref index = position in initial_nodes() order (nodes.hpp:77-83).
-// `hist` is scratch for kRotBatch rotations.
+// `hist` is scratch for kRotBatch rotations.  probes[0] += de-duplicated
+// (root, voxel offset) probes; probes[2] += z-column words the column kernel
+// read from its shared-memory window (the actual gathers, bench roofline).
+// ev_col0/ev_col1 (optional) bracket the column-kernel launches.
 void launch_score_roots(const MapView& map, const GridView& grid, const ScanView& scan,
                         const BoxParams& bp, const RootHist& hist, int32_t* scores,
-                        unsigned long long* probes, cudaStream_t s);
+                        unsigned long long* probes, cudaStream_t s, cudaEvent_t ev_col0 = nullptr,
+                        cudaEvent_t ev_col1 = nullptr);
 
 // Score n nodes that come in contiguous same-rotation runs of 8 (the output
 // order of branch(), nodes.hpp:103-116).  n is read from *d_n when non-null

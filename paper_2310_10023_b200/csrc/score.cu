@@ -810,6 +810,7 @@ __global__ void __launch_bounds__(256, BBS_COLPAD_MINB) root_colpad_kernel(GridV
                    : 0u;
   }
   __syncthreads();
+  uint32_t n_words = 0;  // z-column words this thread read from the window (4 per group)
   const uint64_t n_items = static_cast<uint64_t>(rot_end - rot_begin) * n_cchunks;
   for (uint64_t item = blockIdx.x; item < n_items; item += gridDim.x) {
     const uint32_t slot = static_cast<uint32_t>(item / n_cchunks);
@@ -864,6 +865,7 @@ __global__ void __launch_bounds__(256, BBS_COLPAD_MINB) root_colpad_kernel(GridV
         }
         const int4 o = s_go[g];
         const uint32_t w4 = s_gw[g];
+        n_words += 4;
         rem -= static_cast<int>(__dp4a(w4, 0x01010101u, 0u));  // this group's counts
         // shift amounts ride in the low 5 bits (wrap funnel shift)
         const uint32_t b0 = __funnelshift_r(s_col[base + (o.x >> 8)], 0u, static_cast<uint32_t>(o.x));
@@ -903,6 +905,12 @@ __global__ void __launch_bounds__(256, BBS_COLPAD_MINB) root_colpad_kernel(GridV
       const uint64_t nc = min(static_cast<uint64_t>(blockDim.x), ncols - col0);
       atomicAdd(probes, static_cast<unsigned long long>(nc) * (h.n_ent[slot] + n_amb) * bp.nz);
     }
+  }
+  if (probes) {
+    unsigned long long w = n_words;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) w += __shfl_xor_sync(0xffffffffu, w, o);
+    if ((threadIdx.x & 31) == 0 && w) atomicAdd(probes + 2, w);
   }
 }
 
@@ -994,7 +1002,8 @@ int colpad_ctas_per_sm(uint32_t nz, int smem) {
 
 void launch_score_roots(const MapView& map, const GridView& grid, const ScanView& scan,
                         const BoxParams& bp, const RootHist& hist, int32_t* scores,
-                        unsigned long long* probes, cudaStream_t s) {
+                        unsigned long long* probes, cudaStream_t s, cudaEvent_t ev_col0,
+                        cudaEvent_t ev_col1) {
   const LevelView& L = map.level[bp.level];
   const uint32_t nrot = bp.nr * bp.np * bp.nw;
   const bool col_ok = L.layout == BBS_LAYOUT_BITMAP && L.nwz == 1 && L.words != nullptr &&
@@ -1066,6 +1075,7 @@ void launch_score_roots(const MapView& map, const GridView& grid, const ScanView
     BBS_CUDA(cudaGetLastError());
     const uint64_t items = static_cast<uint64_t>(re - rb) * n_cchunks;
     const unsigned g = static_cast<unsigned>(std::min<uint64_t>(std::max<uint64_t>(items, 1), 148ull * 16));
+    if (ev_col0 && rb == 0) BBS_CUDA(cudaEventRecord(ev_col0, s));
     if (st.enabled) {
       // persistent grid: every CTA stages the padded window once
       const unsigned gp = std::min<unsigned>(g, 148u * static_cast<unsigned>(colpad_ctas_per_sm(bp.nz, pad_smem)));
@@ -1089,6 +1099,7 @@ void launch_score_roots(const MapView& map, const GridView& grid, const ScanView
       root_col_kernel<32><<<g, 256, col_smem, s>>>(grid, scan, bp, L, rb, re, hist, n_cchunks, stage,
                                                    scores, probes);
     BBS_CUDA(cudaGetLastError());
+    if (ev_col1 && re == nrot) BBS_CUDA(cudaEventRecord(ev_col1, s));
     // rotations whose histogram overflowed: chunked kernel (exits at once when none)
     launch_score_box_chunked(map, grid, scan, bp, rb, re, hist.overflow, scores, probes, s);
   }

@@ -1372,7 +1372,8 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
   // parity dump: no survivor-bound early exit in the root column kernel
   if (dump && dump->exact_roots) bp.threshold = INT32_MIN;
   int32_t* root_scores = W.root_scores.get(static_cast<size_t>(std::max<int64_t>(total, 1)), s);
-  unsigned long long* d_probes = W.probes.get(2, s);  // [0] root probes, [1] survivor count
+  // [0] root probes, [1] survivor count, [2] column words read by the root kernel
+  unsigned long long* d_probes = W.probes.get(4, s);
   int* d_nsel = W.nsel.get(1, s);
   RootHist hist{};
   hist.entries = W.hist_ent.get(static_cast<size_t>(kRotBatch) * kHistCap, s);
@@ -1385,7 +1386,7 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
   // unowned roots must read -1 (below any threshold); a single rank scores
   // and writes every root
   if (world > 1) BBS_CUDA(cudaMemsetAsync(root_scores, 0xFF, static_cast<size_t>(std::max<int64_t>(total, 1)) * 4, s));
-  BBS_CUDA(cudaMemsetAsync(d_probes, 0, sizeof(unsigned long long), s));
+  BBS_CUDA(cudaMemsetAsync(d_probes, 0, 3 * sizeof(unsigned long long), s));
   // root survivors -> queue on the device (root_select + root_pass kernels)
   // when the short key (smax - score) takes <= 2 digit passes and the roots
   // fit 32-bit positions; else CUB select + sort after a host sync
@@ -1413,9 +1414,14 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
     rinit.ctl = W.rinit_ctl.get(kRCtlHist + 512, s);
     BBS_CUDA(cudaMemsetAsync(rinit.ctl, 0, (kRCtlHist + 512) * sizeof(uint32_t), s));
   }
+  cudaEvent_t ev_col0 = W.next_event(), ev_col1 = W.next_event();
+  bool col_timed = false;
   BBS_CUDA(cudaEventRecord(ev_roots0, s));
+  BBS_CUDA(cudaEventRecord(ev_col0, s));  // re-recorded around the column kernels when they run
+  BBS_CUDA(cudaEventRecord(ev_col1, s));
   if (total > 0) {
-    launch_score_roots(m->view, gv, sv, bp, hist, root_scores, d_probes, s);
+    col_timed = true;
+    launch_score_roots(m->view, gv, sv, bp, hist, root_scores, d_probes, s, ev_col0, ev_col1);
     launches += 3 * ((nrot + kRotBatch - 1) / kRotBatch);
   }
   BBS_CUDA(cudaEventRecord(ev_roots1, s));
@@ -1965,9 +1971,13 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
     BBS_CUDA(cudaMemcpyAsync(&W.h_small[0], d_probes, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
     d2h += sizeof(unsigned long long);
   }
+  BBS_CUDA(cudaMemcpyAsync(&W.h_small[3], d_probes + 2, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+  d2h += sizeof(unsigned long long);
   BBS_CUDA(cudaStreamSynchronize(s));
   hs = *W.h_st;
   if (dev_init) root_probes = W.h_small[0];
+  out->root_words = W.h_small[3];
+  out->root_col_ms = col_timed ? elapsed(ev_col0, ev_col1) : 0.0;
 
   tmark("state read");
   // ---- results ----

@@ -245,7 +245,8 @@ struct VoxelSorter {
 
 // prepare_source, pipeline.hpp:25-41, with auto_leaf (point_cloud.hpp:137-182)
 // driving device voxel counts and voxel_grid_downsample on the device.
-SourcePrep device_prepare_source(int device, const double* xyz, uint64_t n, uint64_t target) {
+SourcePrep device_prepare_source(int device, const double* xyz, uint64_t n, uint64_t target,
+                                 bool exact_centroids) {
   SourcePrep p;
   if (target > 0 && n > target) {
     if (n >= (1ull << 32)) throw Error(BBS_ERR_TOO_LARGE, "prepare_source: more than 2^32 points");
@@ -306,8 +307,14 @@ SourcePrep device_prepare_source(int device, const double* xyz, uint64_t n, uint
     }
     // voxel_grid_downsample, point_cloud.hpp:78-111
     if (!(leaf > 0.0)) throw Error(BBS_ERR_CONFIG, "voxel_grid_downsample: leaf must be > 0");
-    const uint64_t count = vs.sort(leaf);
-    p.xyz = vs.centroids(count);
+    if (exact_centroids) {
+      // the reference's per-voxel summation order is its introsort's
+      // permutation: replayed on the host at the device-found leaf
+      p.xyz = host_voxel_grid_downsample(xyz, n, leaf);
+    } else {
+      const uint64_t count = vs.sort(leaf);
+      p.xyz = vs.centroids(count);
+    }
     p.leaf = leaf;
     p.converged = converged;
   } else {

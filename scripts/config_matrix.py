@@ -7,7 +7,7 @@ sys.path.insert(0, ROOT)
 import bench
 import paper_2310_10023_b200 as B
 cfgd = bench.CONFIGS[sys.argv[1] if len(sys.argv) > 1 else "c2"]
-m, s, gt = bench.build_inputs(B, cfgd)
+m, s, gt = bench.build_inputs(cfgd)
 vm = B.MultiResVoxelMap.build(m, cfgd["r"], cfgd["max_level"])
 ds = B.DeviceScan(vm, s)
 for strat in ("BFS", "DFS"):

@@ -10,7 +10,7 @@ ap.add_argument("--config", default="c2")
 ap.add_argument("--layout", default="auto")
 a = ap.parse_args()
 cfgd = bench.CONFIGS[a.config]
-m, s, gt = bench.build_inputs(B, cfgd)
+m, s, gt = bench.build_inputs(cfgd)
 vm = B.MultiResVoxelMap.build(m, cfgd["r"], cfgd["max_level"], layout=B.Layout[a.layout.upper()])
 ds = B.DeviceScan(vm, s)
 cfg = bench.search_config(B, cfgd)

@@ -10,7 +10,7 @@ import paper_2310_10023_b200 as B
 from pyoracle import Reference
 
 cfgd = bench.CONFIGS["c1"]
-m, scan, gt = bench.build_inputs(B, cfgd)
+m, scan, gt = bench.build_inputs(cfgd)
 vm = B.MultiResVoxelMap.build(m, cfgd["r"], cfgd["max_level"])
 gx, gy, gz = gt.x, gt.y, gt.z
 half = float(os.environ.get("ORACLE_HALF", "1.0"))

@@ -6,7 +6,7 @@ sys.path.insert(0, ROOT)
 import bench
 import paper_2310_10023_b200 as B
 cfgd = bench.CONFIGS["c2"]
-m, scan, gt = bench.build_inputs(B, cfgd)
+m, scan, gt = bench.build_inputs(cfgd)
 cfg = bench.search_config(B, cfgd)
 vm = B.MultiResVoxelMap.build(m, cfgd["r"], cfgd["max_level"])
 ds = B.DeviceScan(vm, scan)

@@ -1,7 +1,10 @@
 """Per-kernel DRAM traffic and duration from an ncu CSV launch list taken with
   --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum
 Usage: traffic.py launches.csv [--last N] [--json out.json --config c2]
-Groups the bench's roofline kernels and prints bytes per launch."""
+                  [--sol kernel=report.ncu-rep ...]
+Groups the bench's roofline kernels, prints bytes per launch, and (--json)
+writes per-kernel and per-group entries; --sol adds the speed-of-light
+percentages of a kernel from a `ncu --set full` report."""
 import collections
 import csv
 import json
@@ -13,6 +16,14 @@ GROUPS = {
     "root": ("root_hist_kernel", "root_colpad_kernel", "root_col_kernel"),
     "flush": ("cache_probe_kernel", "score_cube8_kernel", "cache_build_kernel"),
 }
+
+
+# the search's own kernels (map build and CUB launches excluded from shares)
+SEARCH_KERNELS = {"root_hist_kernel", "root_colpad_kernel", "root_col_kernel", "score_box_kernel",
+                  "root_select_kernel", "root_pass_kernel", "stage_window_kernel",
+                  "cache_prebuild_list_kernel", "cache_build_kernel", "cache_probe_kernel",
+                  "score_cube8_kernel", "frontier_kernel", "branch_kernel", "survivors_kernel",
+                  "rank_sort_kernel", "merge_kernel", "soa_kernel", "score_runs_kernel"}
 
 
 def load(path, last=0):
@@ -30,6 +41,30 @@ def load(path, last=0):
         launches.setdefault(k, {})[d["Metric Name"]] = v
     items = list(launches.items())
     return items[-last:] if last else items
+
+
+def sol(rep):
+    """Speed-of-light numbers of the first kernel in an ncu --set full report."""
+    import io
+    import subprocess
+    txt = subprocess.run(["ncu", "-i", rep, "--page", "details", "--csv"], capture_output=True,
+                         text=True).stdout
+    rows = list(csv.reader(io.StringIO(txt)))
+    want = {"Compute (SM) Throughput": "sm_throughput_pct", "Memory Throughput": "memory_throughput_pct",
+            "L1/TEX Cache Throughput": "l1tex_throughput_pct", "L2 Cache Throughput": "l2_throughput_pct",
+            "Issued Ipc Active": "ipc_active", "Achieved Occupancy": "achieved_occupancy_pct",
+            "Duration": "ncu_duration", "Registers Per Thread": "registers"}
+    out = {"source": rep}
+    hdr = rows[0]
+    for r in rows[1:]:
+        d = dict(zip(hdr, r))
+        k = want.get(d.get("Metric Name"))
+        if k and k not in out and (d.get("Metric Unit") != "Gbyte/s"):
+            try:
+                out[k] = float(d["Metric Value"].replace(",", ""))
+            except ValueError:
+                pass
+    return out
 
 
 def main():
@@ -57,6 +92,16 @@ def main():
             allj = json.load(open(js))
         except (OSError, ValueError):
             allj = {}
+        search_us = sum(v[1] for k, v in agg.items() if k in SEARCH_KERNELS)
+        for name, (n, us, by) in agg.items():
+            if n == 0:
+                continue
+            out[name] = {"dram_bytes_per_launch": by / n, "us_per_launch": us / n, "launches": n}
+            if name in SEARCH_KERNELS:
+                out[name]["share_of_search_device_time"] = us / max(search_us, 1e-9)
+        for spec in [a for i, a in enumerate(sys.argv) if i and sys.argv[i - 1] == "--sol"]:
+            kname, rep = spec.split("=", 1)
+            out.setdefault(kname, {}).update(sol(rep))
         allj[cfg] = out
         json.dump(allj, open(js, "w"), indent=1)
         print(json.dumps(out, indent=1))

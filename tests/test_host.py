@@ -162,6 +162,34 @@ def test_prepare_source_bit_identical(B, ref, target):
     assert (ours.leaf, ours.leaf_converged, ours.d_max) == (leaf, conv, dmax)
 
 
+def test_prepare_source_campus_raw_scan_bit_identical(B, ref):
+    """C2 raw scan (~236k points -> target 10k): the packed-key replay of the
+    reference's introsort gives its per-voxel summation order exactly."""
+    spec = H.SceneSpec.default(size_x=300.0, size_y=300.0, size_z=30.0, num_boxes=60,
+                               min_box_side=6.0, max_box_side=30.0, min_box_height=8.0,
+                               map_spacing=0.19, scan_spacing=0.3, scan_range=60.0,
+                               min_scan_points=400)
+    _, raw, _ = H.gen_scene(spec, 1)
+    ours = B.prepare_source(raw, 10000)
+    scan, leaf, conv, dmax = ref.prepare_source(raw, 10000)
+    np.testing.assert_array_equal(ours.scan, scan)
+    assert (ours.leaf, ours.leaf_converged, ours.d_max) == (leaf, conv, dmax)
+
+
+def test_prepare_source_unpackable_voxels_bit_identical(B, ref):
+    """Voxel indices spanning more than 64 packed bits take the reference's
+    own record layout; NaN coordinates map to INT64_MIN voxels as on x86."""
+    rng = np.random.default_rng(8)
+    raw = rng.normal(size=(3000, 3))
+    raw[:40] *= 1e17  # ~2^57 voxels apart on every axis at the chosen leaf
+    raw[40:43, 1] = np.nan
+    ours = B.prepare_source(raw, 500)
+    scan, leaf, conv, dmax = ref.prepare_source(raw, 500)
+    np.testing.assert_array_equal(ours.scan, scan)
+    assert (ours.leaf, ours.leaf_converged) == (leaf, conv)
+    assert (ours.d_max == dmax) or (np.isnan(ours.d_max) and np.isnan(dmax))
+
+
 def test_max_range_and_bbox_bit_identical(B, ref):
     rng = np.random.default_rng(5)
     pts = rng.normal(size=(5000, 3)) * 17.0

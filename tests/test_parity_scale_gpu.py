@@ -231,3 +231,25 @@ def test_c3_batches_match_reference(B, c3):
     grids = B.AngularGrid(cfg, B.max_range(s))
     got = B.batch_evaluate(g["nodes"], vm, s, grids)[:, 7]
     np.testing.assert_array_equal(got, g["scores"])
+
+
+def test_c2_localize_scan_raw_scan_matches_reference(B):
+    """localize_scan (pipeline.hpp:45-51), the public entry point, on the RAW
+    C2 scan (~236k points, downsample target 10k): the default exact prepare
+    (device auto_leaf counts + the reference's centroid summation order) and
+    the search equal the reference's localize_scan: score, pose, Stats."""
+    if not has("c2_localize.json"):
+        pytest.skip("c2 localize golden not generated")
+    want = golden_json("c2_localize.json")
+    m, raw, _ = H.gen_scene(H.SceneSpec.default(**C2["spec"]), C2["seed"])
+    assert digest(raw) == want["raw_digest"]
+    prep = B.prepare_source(raw, want["target"])  # host restatement, same order
+    assert digest(prep.scan) == want["prepared_digest"]
+    vm = _c2_map(B, m)
+    cfg = search_cfg(B, C2, collect_trace=False)
+    res = B.localize_scan(vm, raw, cfg, want["target"])
+    assert res.scan_points == want["scan_points"]
+    assert res.best_score == want["best_score"]
+    assert list(res.best_pose.as_tuple()) == want["best_pose"]
+    assert (res.stats.nodes_generated, res.stats.nodes_pruned, res.stats.batches_flushed) == \
+        (want["nodes_generated"], want["nodes_pruned"], want["batches_flushed"])
