@@ -322,6 +322,15 @@ int bbs_oracle_search(bbs_map_t map, const double* scan_xyz, uint64_t k, const b
                       int32_t* best_score, bbs_node* argmax, uint64_t argmax_capacity,
                       uint64_t* argmax_count, uint64_t* leaf_count);
 
+/* oracle_search returning EVERY argmax leaf in one pass: *argmax is a
+ * malloc'ed array of *argmax_count nodes (release with bbs_free; non-NULL
+ * on success even when the count is 0). */
+int bbs_oracle_search_all(bbs_map_t map, const double* scan_xyz, uint64_t k, const bbs_search_config* cfg,
+                          int32_t* best_score, bbs_node** argmax, uint64_t* argmax_count,
+                          uint64_t* leaf_count);
+/* Releases memory the library malloc'ed for the caller. */
+void bbs_free(void* p);
+
 /* ---- multi-GPU ------------------------------------------ */
 /* Element-wise MAX all-reduce of `count` int64 values in place across all
  * ranks; returns 0 on success.  Supplied by the caller (NCCL / gloo). */

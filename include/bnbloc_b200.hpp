@@ -693,14 +693,11 @@ inline OracleResult oracle_search(const MultiResVoxelMap& map, const PointCloud&
   const bbs_search_config c = detail::to_c(cfg);
   std::int32_t best = 0;
   std::uint64_t count = 0, leaves = 0;
-  std::vector<bbs_node> nodes(1024);
-  detail::check(bbs_oracle_search(map.handle(), xyz(scan), scan.size(), &c, &best, nodes.data(),
-                                  nodes.size(), &count, &leaves));
-  if (count > nodes.size()) {  // retry with the full count
-    nodes.resize(count);
-    detail::check(bbs_oracle_search(map.handle(), xyz(scan), scan.size(), &c, &best, nodes.data(),
-                                    nodes.size(), &count, &leaves));
-  }
+  bbs_node* raw = nullptr;  // every argmax leaf, one pass
+  detail::check(bbs_oracle_search_all(map.handle(), xyz(scan), scan.size(), &c, &best, &raw, &count,
+                                      &leaves));
+  const std::unique_ptr<bbs_node, void (*)(void*)> own(raw, bbs_free);
+  const bbs_node* nodes = raw;
   OracleResult out;
   out.best_score = best;
   out.leaf_count = leaves;

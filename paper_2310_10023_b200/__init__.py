@@ -654,22 +654,30 @@ class OracleResult:
     argmax_nodes: np.ndarray
 
 
-def oracle_search(vmap: MultiResVoxelMap, scan, cfg: SearchConfig, argmax_capacity=1024):
+def oracle_search(vmap: MultiResVoxelMap, scan, cfg: SearchConfig, argmax_capacity=None):
     """oracle.hpp:29-95: every level-0 leaf under the root index ranges x the
-    level-0 rotation grid, enumerated and scored on the device (no pruning)."""
+    level-0 rotation grid, enumerated and scored on the device (no pruning),
+    in one pass (bbs_oracle_search_all); argmax_capacity (optional) takes the
+    capped bbs_oracle_search entry point instead."""
     s = _xyz(scan)
     c = cfg.to_c()
     best, cnt, leaves = C.c_int32(), C.c_uint64(), C.c_uint64()
-    cap = max(int(argmax_capacity), 1)
-    while True:
+    if argmax_capacity is not None:
+        cap = max(int(argmax_capacity), 1)
         buf = np.zeros((cap, 8), np.int32)
         _check(lib.bbs_oracle_search(vmap._h, _dptr(s), s.shape[0], C.byref(c), C.byref(best),
                                      buf.ctypes.data_as(C.POINTER(Node)), cap, C.byref(cnt),
                                      C.byref(leaves)))
-        if cnt.value <= cap:
-            break
-        cap = cnt.value
-    nodes = buf[:cnt.value].copy()
+        nodes = buf[:min(cnt.value, cap)].copy()
+    else:
+        p = C.POINTER(Node)()
+        _check(lib.bbs_oracle_search_all(vmap._h, _dptr(s), s.shape[0], C.byref(c), C.byref(best),
+                                         C.byref(p), C.byref(cnt), C.byref(leaves)))
+        try:
+            nodes = np.ctypeslib.as_array(C.cast(p, C.POINTER(C.c_int32)),
+                                          shape=(max(cnt.value, 1), 8))[:cnt.value].copy()
+        finally:
+            lib.bbs_free(C.cast(p, C.c_void_p))
     d_max = cfg.d_max if cfg.d_max is not None else max_range(s)
     grids = AngularGrid(cfg, d_max)
     poses = [node_pose(n, grids, cfg.min_resolution).normalized() for n in nodes]

@@ -67,6 +67,9 @@ SIGNATURES = {
     "bbs_search": (C.c_int, [_vp, _dp, _u64, C.POINTER(SearchConfigC), C.POINTER(SearchResultC)]),
     "bbs_oracle_search": (C.c_int, [_vp, _dp, _u64, C.POINTER(SearchConfigC), _ip,
                                     C.POINTER(Node), _u64, C.POINTER(_u64), C.POINTER(_u64)]),
+    "bbs_oracle_search_all": (C.c_int, [_vp, _dp, _u64, C.POINTER(SearchConfigC), _ip,
+                                        C.POINTER(C.POINTER(Node)), C.POINTER(_u64), C.POINTER(_u64)]),
+    "bbs_free": (None, [_vp]),
     "bbs_localize_scan_ex": (C.c_int, [_vp, _dp, _u64, C.POINTER(SearchConfigC), _u64, _i32,
                                        C.POINTER(SearchResultC)]),
     "bbs_localize_scan": (C.c_int, [_vp, _dp, _u64, C.POINTER(SearchConfigC), _u64,

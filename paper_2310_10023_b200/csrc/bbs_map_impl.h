@@ -70,12 +70,18 @@ struct LeafGridSpec {
   uint64_t nx = 0, ny = 0, nz = 0, nr = 0, np = 0, nw = 0;
   uint64_t total() const { return nx * ny * nz * (nr * np * nw); }
 };
+// batch_evaluate on device nodes (search.hpp:23-34), search.cu: the LUT
+// built here (lo/hi widen the per-(level, axis) index range), or prebuilt.
+void batch_evaluate_device(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, double d_max,
+                           bbs_node* d_nodes, uint64_t n, cudaStream_t s, const int32_t* lo,
+                           const int32_t* hi);
+void batch_evaluate_device(bbs_map* m, bbs_scan* scan, const GridView& gv, bbs_node* d_nodes, uint64_t n,
+                           cudaStream_t s);
 // leaf_grid.cu: score every leaf in blocks of `block`; best score (-1 if
-// none), the nodes attaining it in enumeration order (first `capacity`) and
-// their full count.
+// none) and every node attaining it, in enumeration order.
 void leaf_grid_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, double d_max,
-                      const LeafGridSpec& g, uint64_t block, int32_t* best_score, bbs_node* argmax,
-                      uint64_t capacity, uint64_t* count);
+                      const LeafGridSpec& g, uint64_t block, int32_t* best_score,
+                      std::vector<bbs_node>* argmax);
 
 struct DeviceGuard {
   int prev = 0;

@@ -25,9 +25,6 @@
 namespace bbs {
 void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const bbs_shard* shard,
                 bbs_search_result* out, cudaStream_t stream = nullptr, bbs_search_dump* dump = nullptr);
-void batch_evaluate_device(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, double d_max,
-                           bbs_node* d_nodes, uint64_t n, cudaStream_t s, const int32_t* lo,
-                           const int32_t* hi);
 void set_pool_retention(int device);
 }  // namespace bbs
 
@@ -574,13 +571,12 @@ int bbs_batch_evaluate_device(bbs_map_t map, bbs_scan_t scan, const bbs_search_c
   });
 }
 
-int bbs_oracle_search(bbs_map_t map, const double* scan_xyz, uint64_t k, const bbs_search_config* cfg,
-                      int32_t* best_score, bbs_node* argmax, uint64_t argmax_capacity,
-                      uint64_t* argmax_count, uint64_t* leaf_count) {
-  return guard([&] {
-    REQUIRE(map && cfg && best_score && argmax_count && leaf_count && (scan_xyz || k == 0) &&
-                (argmax || argmax_capacity == 0),
-            "null argument");
+namespace {
+// oracle_search, oracle.hpp:29-95 (validation in the reference's order and
+// messages, then the device leaf grid); every argmax leaf into `all`.
+void oracle_search_impl(bbs_map_t map, const double* scan_xyz, uint64_t k, const bbs_search_config* cfg,
+                        int32_t* best_score, std::vector<bbs_node>* all, uint64_t* leaf_count) {
+  {
     // oracle.hpp:31-35, same order and messages
     if (k == 0) throw bbs::Error(BBS_ERR_DEGENERATE_SCAN, "oracle_search: empty scan");
     if (map->r != cfg->min_resolution)
@@ -593,32 +589,82 @@ int bbs_oracle_search(bbs_map_t map, const double* scan_xyz, uint64_t k, const b
     const double root_cell = std::ldexp(cfg->min_resolution, cfg->max_level);
     const int64_t scale = int64_t{1} << cfg->max_level;
     // trans_index_range (nodes.hpp:53-56): int32 floor / ceil of w / cell
+    // with the x86 conversion (out of range / NaN -> INT32_MIN)
+    auto to_i32 = [](double f) {
+      return (f >= -2147483648.0 && f < 2147483648.0) ? static_cast<int32_t>(f) : INT32_MIN;
+    };
     auto tir = [&](double lo, double hi, int64_t* a, int64_t* b) {
-      *a = static_cast<int32_t>(std::floor(lo / root_cell)) * scale;
-      *b = (static_cast<int64_t>(static_cast<int32_t>(std::ceil(hi / root_cell))) + 1) * scale;
+      *a = static_cast<int64_t>(to_i32(std::floor(lo / root_cell))) * scale;
+      *b = (static_cast<int64_t>(to_i32(std::ceil(hi / root_cell))) + 1) * scale;
     };
     bbs::LeafGridSpec g;
     int64_t xh, yh, zh;
     tir(range.min.x, range.max.x, &g.x_lo, &xh);
     tir(range.min.y, range.max.y, &g.y_lo, &yh);
     tir(range.min.z, range.max.z, &g.z_lo, &zh);
+    const int64_t nrot = static_cast<int64_t>(grids.axis(0, 0).index_count()) *
+                         grids.axis(1, 0).index_count() * grids.axis(2, 0).index_count();
+    // the reference's count, oracle.hpp:50-53: unsigned products that wrap
+    // when an extent is negative
+    const uint64_t total = static_cast<uint64_t>(xh - g.x_lo) * static_cast<uint64_t>(yh - g.y_lo) *
+                           static_cast<uint64_t>(zh - g.z_lo) * static_cast<uint64_t>(nrot);
+    if (total == 0) throw bbs::Error(BBS_ERR_EMPTY_SEARCH_SPACE, "oracle_search: empty leaf grid");
+    if (total > 100000000ull)  // kOracleMaxLeaves, oracle.hpp:25
+      throw bbs::Error(BBS_ERR_TOO_LARGE, "oracle_search: leaf grid of " + std::to_string(total) +
+                                              " nodes exceeds the 1e8 guard");
+    if (xh <= g.x_lo || yh <= g.y_lo || zh <= g.z_lo) {
+      // an inverted range: the reference's loops (oracle.hpp:79-81) score no
+      // leaf, so best_score stays -1 and the argmax list is empty
+      *leaf_count = total;
+      *best_score = -1;
+      all->clear();
+      return;
+    }
     g.nx = static_cast<uint64_t>(xh - g.x_lo);
     g.ny = static_cast<uint64_t>(yh - g.y_lo);
     g.nz = static_cast<uint64_t>(zh - g.z_lo);
     g.nr = static_cast<uint64_t>(grids.axis(0, 0).index_count());
     g.np = static_cast<uint64_t>(grids.axis(1, 0).index_count());
     g.nw = static_cast<uint64_t>(grids.axis(2, 0).index_count());
-    const uint64_t total = g.total();
-    if (total == 0) throw bbs::Error(BBS_ERR_EMPTY_SEARCH_SPACE, "oracle_search: empty leaf grid");
-    if (total > 100000000ull)  // kOracleMaxLeaves, oracle.hpp:25
-      throw bbs::Error(BBS_ERR_TOO_LARGE, "oracle_search: leaf grid of " + std::to_string(total) +
-                                              " nodes exceeds the 1e8 guard");
     *leaf_count = total;
     const char* eb = std::getenv("BBS_LEAF_BLOCK");
     const uint64_t block = eb ? std::strtoull(eb, nullptr, 10) : (uint64_t{1} << 20);
-    bbs::leaf_grid_search(map, sc.get(), *cfg, d_max, g, block, best_score, argmax, argmax_capacity,
-                          argmax_count);
+    bbs::leaf_grid_search(map, sc.get(), *cfg, d_max, g, block, best_score, all);
+  }
+}
+}  // namespace
+
+int bbs_oracle_search(bbs_map_t map, const double* scan_xyz, uint64_t k, const bbs_search_config* cfg,
+                      int32_t* best_score, bbs_node* argmax, uint64_t argmax_capacity,
+                      uint64_t* argmax_count, uint64_t* leaf_count) {
+  return guard([&] {
+    REQUIRE(map && cfg && best_score && argmax_count && leaf_count && (scan_xyz || k == 0) &&
+                (argmax || argmax_capacity == 0),
+            "null argument");
+    std::vector<bbs_node> all;
+    oracle_search_impl(map, scan_xyz, k, cfg, best_score, &all, leaf_count);
+    *argmax_count = all.size();
+    if (argmax_capacity) std::memcpy(argmax, all.data(), std::min<uint64_t>(all.size(), argmax_capacity) * sizeof(bbs_node));
   });
 }
+
+int bbs_oracle_search_all(bbs_map_t map, const double* scan_xyz, uint64_t k, const bbs_search_config* cfg,
+                          int32_t* best_score, bbs_node** argmax, uint64_t* argmax_count,
+                          uint64_t* leaf_count) {
+  return guard([&] {
+    REQUIRE(map && cfg && best_score && argmax && argmax_count && leaf_count && (scan_xyz || k == 0),
+            "null argument");
+    *argmax = nullptr;
+    std::vector<bbs_node> all;
+    oracle_search_impl(map, scan_xyz, k, cfg, best_score, &all, leaf_count);
+    auto* out = static_cast<bbs_node*>(std::malloc(std::max<size_t>(all.size(), 1) * sizeof(bbs_node)));
+    if (!out) throw bbs::Error(BBS_ERR_GENERIC, "oracle_search: out of host memory");
+    std::memcpy(out, all.data(), all.size() * sizeof(bbs_node));
+    *argmax = out;
+    *argmax_count = all.size();
+  });
+}
+
+void bbs_free(void* p) { std::free(p); }
 
 }  // extern "C"

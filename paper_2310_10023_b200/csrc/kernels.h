@@ -12,6 +12,28 @@
 
 namespace bbs {
 
+// Stream-ordered device allocations released on scope exit, so a BBS_CUDA
+// throw between the allocation and the normal end leaks nothing.
+struct StreamAllocs {
+  cudaStream_t s;
+  std::vector<void*> p;
+  explicit StreamAllocs(cudaStream_t st) : s(st) {}
+  StreamAllocs(const StreamAllocs&) = delete;
+  StreamAllocs& operator=(const StreamAllocs&) = delete;
+  template <typename T>
+  T* get(size_t n) {
+    void* x = nullptr;
+    if (cudaMallocAsync(&x, n ? n * sizeof(T) : 1, s) != cudaSuccess)
+      throw Error(BBS_ERR_CUDA, "CUDA: cudaMallocAsync failed");
+    p.push_back(x);
+    return static_cast<T*>(x);
+  }
+  ~StreamAllocs() {
+    for (void* x : p) cudaFreeAsync(x, s);
+  }
+};
+
+
 struct ScanView {
   const double* x;
   const double* y;
@@ -178,6 +200,10 @@ void launch_cache_prebuild(const MapView& map, const GridView& grid, const ScanV
 
 // Score arbitrary nodes in place (node.score), grouping equal rotations on
 // the device.  Host-synchronous.
+// The rotation LUT of (cfg, d_max) uploaded into `al` (search.cu).
+GridView upload_grid(const bbs_search_config& cfg, double d_max, const int32_t* lo, const int32_t* hi,
+                     cudaStream_t s, StreamAllocs& al);
+
 void score_nodes_general(const MapView& map, const GridView& grid, const ScanView& scan,
                          bbs_node* d_nodes, uint64_t n, cudaStream_t s);
 

@@ -17,12 +17,9 @@
 #include <cstring>
 
 #include "bbs_map_impl.h"
+#include "kernels.h"
 
 namespace bbs {
-
-void batch_evaluate_device(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, double d_max,
-                           bbs_node* d_nodes, uint64_t n, cudaStream_t s, const int32_t* lo,
-                           const int32_t* hi);
 
 namespace {
 
@@ -77,8 +74,8 @@ unsigned grid_for(uint64_t n) {
 }  // namespace
 
 void leaf_grid_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, double d_max,
-                      const LeafGridSpec& g, uint64_t block, int32_t* best_score, bbs_node* argmax,
-                      uint64_t capacity, uint64_t* count) {
+                      const LeafGridSpec& g, uint64_t block, int32_t* best_score,
+                      std::vector<bbs_node>* argmax) {
   DeviceGuard dg(m->device);
   cudaStream_t s = m->stream;
   const uint64_t total = g.total();
@@ -112,12 +109,15 @@ void leaf_grid_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, 
   int32_t* const h_small = bufs.host;
   unsigned long long* d_nsel = reinterpret_cast<unsigned long long*>(d_small + 2);
   int32_t best = -1;
-  uint64_t cnt = 0;
+  argmax->clear();
+  // the rotation LUT once for every block (level-0 indices in [0, max_index])
+  StreamAllocs al(s);
+  const GridView gv = upload_grid(cfg, d_max, nullptr, nullptr, s, al);
   for (uint64_t first = 0; first < total; first += block) {
     const uint64_t n = std::min(block, total - first);
     leaf_nodes_kernel<<<grid_for(n), 256, 0, s>>>(g, first, n, d_nodes);
     BBS_CUDA(cudaGetLastError());
-    batch_evaluate_device(m, scan, cfg, d_max, d_nodes, n, s, nullptr, nullptr);
+    batch_evaluate_device(m, scan, gv, d_nodes, n, s);
     BBS_CUDA(cudaMemsetAsync(d_small, 0xff, 4, s));  // -1: the reference's initial best
     block_max_kernel<<<grid_for(n), 256, 0, s>>>(d_nodes, n, d_small);
     BBS_CUDA(cudaGetLastError());
@@ -126,7 +126,7 @@ void leaf_grid_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, 
     const int32_t bm = h_small[0];
     if (bm > best) {  // oracle.hpp:70-73
       best = bm;
-      cnt = 0;
+      argmax->clear();
     }
     if (bm != best) continue;
     size_t tb = tmp_bytes;
@@ -135,15 +135,14 @@ void leaf_grid_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, 
     BBS_CUDA(cudaStreamSynchronize(s));
     uint64_t nsel = 0;
     std::memcpy(&nsel, h_small + 2, 8);
-    if (cnt < capacity && nsel) {
-      const uint64_t take = std::min(nsel, capacity - cnt);
-      BBS_CUDA(cudaMemcpyAsync(argmax + cnt, d_sel, take * sizeof(bbs_node), cudaMemcpyDeviceToHost, s));
+    if (nsel) {
+      const size_t o = argmax->size();
+      argmax->resize(o + nsel);
+      BBS_CUDA(cudaMemcpyAsync(argmax->data() + o, d_sel, nsel * sizeof(bbs_node), cudaMemcpyDeviceToHost, s));
       BBS_CUDA(cudaStreamSynchronize(s));
     }
-    cnt += nsel;
   }
   *best_score = best;
-  *count = cnt;
 }
 
 }  // namespace bbs

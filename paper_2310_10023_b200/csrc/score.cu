@@ -1139,31 +1139,27 @@ void score_nodes_general(const MapView& map, const GridView& grid, const ScanVie
   if (n == 0) return;
   if (n >= (1ull << 31)) throw Error(BBS_ERR_TOO_LARGE, "batch_evaluate: more than 2^31 nodes");
   const int ni = static_cast<int>(n);
-  unsigned long long *keys, *keys_alt;
-  uint32_t *idx, *idx_alt;
-  BBS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&keys), n * 8, s));
-  BBS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&keys_alt), n * 8, s));
-  BBS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&idx), n * 4, s));
-  BBS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&idx_alt), n * 4, s));
+  StreamAllocs al(s);
+  unsigned long long* keys = al.get<unsigned long long>(n);
+  unsigned long long* keys_alt = al.get<unsigned long long>(n);
+  uint32_t* idx = al.get<uint32_t>(n);
+  uint32_t* idx_alt = al.get<uint32_t>(n);
   rotation_key_kernel<<<grid_1d(n), 256, 0, s>>>(d_nodes, n, grid, keys, idx);
   BBS_CUDA(cudaGetLastError());
   cub::DoubleBuffer<unsigned long long> dk(keys, keys_alt);
   cub::DoubleBuffer<uint32_t> dv(idx, idx_alt);
   size_t t_sort = 0, t_rle = 0, t_scan = 0;
   BBS_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, t_sort, dk, dv, ni, 0, 64, s));
-  int32_t *counts, *starts, *nch, *choff, *d_nruns;
-  unsigned long long* uniq;
-  BBS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&counts), (n + 1) * 4, s));
-  BBS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&starts), (n + 1) * 4, s));
-  BBS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&nch), (n + 1) * 4, s));
-  BBS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&choff), (n + 1) * 4, s));
-  BBS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_nruns), 4, s));
-  BBS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&uniq), n * 8, s));
+  int32_t* counts = al.get<int32_t>(n + 1);
+  int32_t* starts = al.get<int32_t>(n + 1);
+  int32_t* nch = al.get<int32_t>(n + 1);
+  int32_t* choff = al.get<int32_t>(n + 1);
+  int32_t* d_nruns = al.get<int32_t>(1);
+  unsigned long long* uniq = al.get<unsigned long long>(n);
   BBS_CUDA(cub::DeviceRunLengthEncode::Encode(nullptr, t_rle, keys, uniq, counts, d_nruns, ni, s));
   BBS_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, t_scan, counts, starts, ni, s));
-  void* temp;
   const size_t t_all = std::max(t_sort, std::max(t_rle, t_scan));
-  BBS_CUDA(cudaMallocAsync(&temp, t_all, s));
+  void* temp = al.get<unsigned char>(t_all);
   BBS_CUDA(cub::DeviceRadixSort::SortPairs(temp, t_sort, dk, dv, ni, 0, 64, s));
   BBS_CUDA(cub::DeviceRunLengthEncode::Encode(temp, t_rle, dk.Current(), uniq, counts, d_nruns, ni, s));
   int32_t nruns = 0;
@@ -1177,10 +1173,8 @@ void score_nodes_general(const MapView& map, const GridView& grid, const ScanVie
   BBS_CUDA(cudaMemcpyAsync(&last_n, nch + nruns - 1, 4, cudaMemcpyDeviceToHost, s));
   BBS_CUDA(cudaStreamSynchronize(s));
   const uint32_t nchunks = static_cast<uint32_t>(last_off + last_n);
-  uint2* runs;
-  int32_t* sc;
-  BBS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&runs), static_cast<size_t>(nchunks) * 8, s));
-  BBS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&sc), n * 4, s));
+  uint2* runs = al.get<uint2>(nchunks);
+  int32_t* sc = al.get<int32_t>(n);
   expand_runs_kernel<<<grid_1d(nruns), 256, 0, s>>>(counts, starts, choff, nruns, runs);
   BBS_CUDA(cudaGetLastError());
   const uint32_t pt = choose_ptiles(nchunks, scan.k);
@@ -1192,12 +1186,6 @@ void score_nodes_general(const MapView& map, const GridView& grid, const ScanVie
   BBS_CUDA(cudaGetLastError());
   write_scores_kernel<<<grid_1d(n), 256, 0, s>>>(d_nodes, sc, n);
   BBS_CUDA(cudaGetLastError());
-  for (void* p : {static_cast<void*>(keys), static_cast<void*>(keys_alt), static_cast<void*>(idx),
-                  static_cast<void*>(idx_alt), static_cast<void*>(counts),
-                  static_cast<void*>(starts), static_cast<void*>(nch), static_cast<void*>(choff),
-                  static_cast<void*>(d_nruns), static_cast<void*>(uniq), temp,
-                  static_cast<void*>(runs), static_cast<void*>(sc)})
-    BBS_CUDA(cudaFreeAsync(p, s));
 }
 
 }  // namespace bbs

@@ -18,6 +18,7 @@
 // its sizes from the device-resident EpochState, so epochs are enqueued back
 // to back with no host round-trip; the host reads the 100-byte state every
 // few epochs (or every epoch when an incumbent exchange is configured).
+#include <nvtx3/nvToolsExt.h>
 #include <cub/cub.cuh>
 
 #include <algorithm>
@@ -597,6 +598,17 @@ __global__ void __launch_bounds__(kRT) rank_sort_kernel(const EpochState* st,
   }
 }
 
+// E4b': large flushes (batch_size above kRankSortMax): the unused tail of
+// the survivor keys is set to the largest key and the whole buffer goes
+// through a CUB radix sort (O(n) instead of rank_sort's O(n^2)).
+constexpr uint64_t kRankSortMax = 16384;
+__global__ void pad_keys_kernel(const EpochState* st, unsigned long long* __restrict__ key, uint64_t cap) {
+  pdl_wait();
+  const uint64_t n = st->n_children ? st->n_surv : 0;
+  for (uint64_t i = n + blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < cap; i += uint64_t(gridDim.x) * blockDim.x)
+    key[i] = ~0ull;
+}
+
 // E6: merge the sorted survivors into the trimmed queue remainder (push,
 // search.hpp:139).  The remainder A is read through the kept segment ranges
 // (one per key segment); the survivors B are sorted; keys are unique.  Keys
@@ -1053,7 +1065,7 @@ struct Workspace {
   Buf<int32_t> root_scores;
   Buf<unsigned long long> probes, surv_idx, qk0, qk1, s_key, s_key2, surv_tiles;
   Buf<int> nsel;
-  Buf<unsigned char> temp;
+  Buf<unsigned char> temp, sort_temp;
   Buf<bbs_node> pool, pending, pending_own;
   Buf<uint32_t> perm0, perm1, sk0, sk1, exp_parent, exp_off;
   Buf<int32_t> pscores, trace, hist_n, pscores_own, xchg;
@@ -1090,6 +1102,7 @@ struct Workspace {
     lut_valid = false;
     nsel.release();
     temp.release();
+    sort_temp.release();
     hist_ent.release();
     cache_info.release();
     cache_pool.release();
@@ -1150,7 +1163,7 @@ void set_pool_retention(int device) {
 
 bbs_scan* upload_scan(bbs_map* m, const double* xyz, uint64_t k, bool sync) {
   DeviceGuard g(m->device);
-  auto* sc = new bbs_scan();
+  std::unique_ptr<bbs_scan> sc(new bbs_scan());  // released to the caller on success
   sc->map = m;
   sc->k = k;
   // the copy and the SoA transform go first: they run while the host scans
@@ -1158,11 +1171,11 @@ bbs_scan* upload_scan(bbs_map* m, const double* xyz, uint64_t k, bool sync) {
   cudaStream_t s = m->stream;
   sc->soa = dalloc<double>(3 * std::max<uint64_t>(k, 1), s);
   if (k) {
-    double* aos = dalloc<double>(3 * k, s);
+    StreamAllocs al(s);
+    double* aos = al.get<double>(3 * k);
     BBS_CUDA(cudaMemcpyAsync(aos, xyz, 3 * k * sizeof(double), cudaMemcpyHostToDevice, s));
     soa_kernel<<<grid1(k), 256, 0, s>>>(aos, k, sc->soa);
     BBS_CUDA(cudaGetLastError());
-    BBS_CUDA(cudaFreeAsync(aos, s));
   }
   // one pass: max_range (point_cloud.hpp:58-63) as sqrt of the largest
   // x*x + y*y + z*z (sqrt is correctly rounded and monotonic, so this is the
@@ -1177,13 +1190,22 @@ bbs_scan* upload_scan(bbs_map* m, const double* xyz, uint64_t k, bool sync) {
   }
   sc->d_max = std::sqrt(r2);
   if (sync) BBS_CUDA(cudaStreamSynchronize(s));  // callers on other streams see a complete scan
-  return sc;
+  return sc.release();
 }
 
 // search(), search.hpp:72-186, on the device.  `shard` may be null;
 // `stream` null = the map's stream (concurrent searches use their own).
+// NVTX range for profilers (nsys / ncu --nvtx); free when no tool is attached.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+
 void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const bbs_shard* shard,
                 bbs_search_result* out, cudaStream_t stream, bbs_search_dump* dump) {
+  NvtxRange nv_search("bbs::search");  // search.hpp:72-186
   // validation, search.hpp:79-89, same order and messages
   if (scan->k == 0) throw Error(BBS_ERR_DEGENERATE_SCAN, "search: empty scan");
   if (m->r != cfg.min_resolution) throw Error(BBS_ERR_CONFIG, "search: config r does not match the map");
@@ -1420,6 +1442,7 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
   BBS_CUDA(cudaEventRecord(ev_col0, s));  // re-recorded around the column kernels when they run
   BBS_CUDA(cudaEventRecord(ev_col1, s));
   if (total > 0) {
+    NvtxRange nv_roots("bbs::root batch");  // search.hpp:111-124
     col_timed = true;
     launch_score_roots(m->view, gv, sv, bp, hist, root_scores, d_probes, s, ev_col0, ev_col1);
     launches += 3 * ((nrot + kRotBatch - 1) / kRotBatch);
@@ -1716,6 +1739,13 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
   uint32_t* exp_off = W.exp_off.get(exp_cap, s);
   unsigned long long* s_key = W.s_key.get(pend_cap, s);
   unsigned long long* s_key2 = W.s_key2.get(pend_cap, s);
+  size_t sort_temp_bytes = 0;
+  void* sort_temp = nullptr;
+  if (pend_cap > kRankSortMax) {
+    BBS_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, sort_temp_bytes, s_key, s_key2, static_cast<int64_t>(pend_cap),
+                                            0, 64, s));
+    sort_temp = W.sort_temp.get(sort_temp_bytes, s);
+  }
   const uint64_t trace_cap = cfg.collect_trace ? std::max<uint64_t>(out->trace_capacity, 1) : 0;
   int32_t* d_trace = W.trace.get(std::max<uint64_t>(trace_cap, 1), s);
   const uint32_t ptiles = choose_ptiles((pend_cap + 7) / 8, static_cast<uint32_t>(K));
@@ -1786,8 +1816,16 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
                surv_tiles);
     BBS_CUDA(cudaGetLastError());
     if (dbg_phases) record(ev_dbg[3 * e]);
-    launch_pdl(rank_sort_kernel, grid1(pend_cap, kRT), kRT, 0, s, d_st, s_key, s_key2);
-    BBS_CUDA(cudaGetLastError());
+    if (pend_cap <= kRankSortMax) {
+      launch_pdl(rank_sort_kernel, grid1(pend_cap, kRT), kRT, 0, s, d_st, s_key, s_key2);
+      BBS_CUDA(cudaGetLastError());
+    } else {
+      launch_pdl(pad_keys_kernel, grid1(pend_cap), 256, 0, s, static_cast<const EpochState*>(d_st), s_key,
+                 static_cast<uint64_t>(pend_cap));
+      BBS_CUDA(cudaGetLastError());
+      size_t tb = sort_temp_bytes;
+      BBS_CUDA(cub::DeviceRadixSort::SortKeys(sort_temp, tb, s_key, s_key2, static_cast<int64_t>(pend_cap), 0, 64, s));
+    }
     if (dbg_phases) record(ev_dbg[3 * e + 1]);
     launch_pdl(merge_kernel, static_cast<unsigned>(std::min<uint64_t>((qcap + kMTile - 1) / kMTile, 148ull * 8)),
                kMT, 0, s, d_st, q, strategy, s_key2);
@@ -1873,6 +1911,7 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
     // device exchange: every rank runs the same number of epochs (and so
     // of collectives) per batch; the stop decision uses the reduced flag
     const int n_ep = (self_active || roots_dev_x) ? E : 1;
+    NvtxRange nv_epochs("bbs::flush epochs");  // search.hpp:145-169, n_ep flushes per host check
     // graphs pay off for long searches (capture + instantiate ~0.2 ms)
     if (n_ep == E && E > 1 && pass_ms.size() >= graph_after && !dbg_phases) {
       if (!batch_exec || batch_qcap != qcap || batch_pool != q.pool || batch_builds != builds_live) {
@@ -2145,17 +2184,30 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
 void batch_evaluate_device(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, double d_max,
                            bbs_node* d_nodes, uint64_t n, cudaStream_t s, const int32_t* lo,
                            const int32_t* hi) {
-  const double dm = d_max > 0 ? d_max : scan->d_max;
-  const HostGrid grid = make_grid(cfg, dm);
+  StreamAllocs al(s);
+  const GridView gv = upload_grid(cfg, d_max > 0 ? d_max : scan->d_max, lo, hi, s, al);
+  batch_evaluate_device(m, scan, gv, d_nodes, n, s);
+}
+
+// The rotation LUT of (cfg, d_max) on the device (host libm, build_lut),
+// allocated in `al` (freed with it).
+GridView upload_grid(const bbs_search_config& cfg, double d_max, const int32_t* lo, const int32_t* hi,
+                     cudaStream_t s, StreamAllocs& al) {
+  const HostGrid grid = make_grid(cfg, d_max);
   GridView gv;
   const std::vector<double> lut = build_lut(grid, &gv, lo, hi);
-  double2* d_lut = dalloc<double2>(lut.size() / 2, s);
+  double2* d_lut = al.get<double2>(lut.size() / 2);
   BBS_CUDA(cudaMemcpyAsync(d_lut, lut.data(), lut.size() * sizeof(double), cudaMemcpyHostToDevice, s));
   gv.lut = d_lut;
+  return gv;
+}
+
+// batch_evaluate with a prebuilt device LUT (callers scoring many blocks).
+void batch_evaluate_device(bbs_map* m, bbs_scan* scan, const GridView& gv, bbs_node* d_nodes, uint64_t n,
+                           cudaStream_t s) {
   const uint64_t K = scan->k;
   const ScanView sv{scan->soa, scan->soa + K, scan->soa + 2 * K, static_cast<uint32_t>(K)};
   score_nodes_general(m->view, gv, sv, d_nodes, n, s);
-  BBS_CUDA(cudaFreeAsync(d_lut, s));
 }
 
 }  // namespace bbs

@@ -55,9 +55,12 @@ def test_oracle_search_block_size_invariant(B, monkeypatch):
     a = B.oracle_search(vm, s, cfg)
     for blk in ("97", "4096"):
         monkeypatch.setenv("BBS_LEAF_BLOCK", blk)
-        b = B.oracle_search(vm, s, cfg, argmax_capacity=1)  # also exercises the retry
+        b = B.oracle_search(vm, s, cfg)  # one pass, every argmax leaf
         assert (b.best_score, b.leaf_count) == (a.best_score, a.leaf_count), blk
         assert np.array_equal(b.argmax_nodes, a.argmax_nodes), blk
+        c = B.oracle_search(vm, s, cfg, argmax_capacity=1)  # the capped entry point
+        assert (c.best_score, c.leaf_count) == (a.best_score, a.leaf_count), blk
+        assert np.array_equal(c.argmax_nodes, a.argmax_nodes[:1]), blk
     # argmax nodes are level-0 leaves carrying the best score
     assert (a.argmax_nodes[:, 6] == 0).all() and (a.argmax_nodes[:, 7] == a.best_score).all()
 
@@ -93,3 +96,19 @@ def test_oracle_search_errors(B):
     with pytest.raises(B.EmptySearchSpaceError, match="empty leaf grid"):
         B.oracle_search(vm, s, small_cfg(B, B.BranchMode.TRANS_ONLY,
                                          translation_range=((4, 5, 5), (-1, 5, 5))))
+
+
+def test_oracle_search_inverted_range_matches_reference(B, ref):
+    """Two inverted translation axes: the reference's unsigned leaf count
+    wraps to a small positive number that passes its guards (oracle.hpp:50-57)
+    and its loops score nothing -> best_score -1, no argmax."""
+    gt = B.Pose6(6.0, 5.0, 0.4, 0, 0, 0.7)
+    m, s = mini_scene(B, 44, gt)
+    vm = B.MultiResVoxelMap.build(m, 1.0, 2, 0.01)
+    rm = ref.map_build(m, 1.0, 2, 0.01)
+    cfg = small_cfg(B, B.BranchMode.TRANS_ONLY, yaw_min=0.4, yaw_max=0.6,
+                    translation_range=((7, 6, 0), (5, 4, 0.5)))
+    got = B.oracle_search(vm, s, cfg)
+    want = rm.oracle_search(s, cfg.to_c())
+    assert want[0] == -1 and want[2].shape[0] == 0
+    _same(got, want, "inverted")

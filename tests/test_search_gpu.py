@@ -321,3 +321,20 @@ def test_search_scans_throughput_mode_matches_single_searches(B):
         assert (r.best_score, r.best_pose.as_tuple(), r.stats.nodes_generated, r.stats.nodes_pruned,
                 r.best_score_trace) == (one.best_score, one.best_pose.as_tuple(), one.stats.nodes_generated,
                                         one.stats.nodes_pruned, one.best_score_trace)
+
+
+@pytest.mark.parametrize("strategy", ["BFS", "DFS"])
+def test_large_batch_uses_radix_sorted_survivors(B, ref, golden_scenes, strategy):
+    """batch_size above 16384 sorts each flush's survivors with a radix sort
+    (not the O(n^2) rank sort): results equal the reference's search()."""
+    m, s, _, sc = load_case(B, golden_scenes, "small")
+    vm = B.MultiResVoxelMap.build(m, sc["r"], sc["max_level"])
+    cfg = make_cfg(B, sc, "small", dict(batch_size=40000, strategy=getattr(B.Strategy, strategy)))
+    got = B.search(vm, s, cfg)
+    rm = ref.map_build(m, sc["r"], sc["max_level"], 0.01)
+    want, trace = rm.search(s, cfg.to_c(), trace_cap=1 << 16)
+    assert got.best_score == want.best_score
+    assert got.best_pose.as_tuple() == want.best_pose.as_tuple()
+    assert (got.stats.nodes_generated, got.stats.nodes_pruned, got.stats.batches_flushed) == \
+        (want.stats.nodes_generated, want.stats.nodes_pruned, want.stats.batches_flushed)
+    assert got.best_score_trace == trace
