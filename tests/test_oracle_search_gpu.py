@@ -106,8 +106,9 @@ def test_oracle_search_inverted_range_matches_reference(B, ref):
     m, s = mini_scene(B, 44, gt)
     vm = B.MultiResVoxelMap.build(m, 1.0, 2, 0.01)
     rm = ref.map_build(m, 1.0, 2, 0.01)
+    # root cell 4 m: x and y index ranges [5, 2] -> leaf ranges [20, 12)
     cfg = small_cfg(B, B.BranchMode.TRANS_ONLY, yaw_min=0.4, yaw_max=0.6,
-                    translation_range=((7, 6, 0), (5, 4, 0.5)))
+                    translation_range=((20, 20, 0), (5, 5, 0.5)))
     got = B.oracle_search(vm, s, cfg)
     want = rm.oracle_search(s, cfg.to_c())
     assert want[0] == -1 and want[2].shape[0] == 0
