@@ -63,6 +63,10 @@ struct EpochState {
   uint32_t cache_raw;      // levels whose histogram builds gave up (flush cache, per frontier pass)
   uint32_t n_own;          // batch-split exact mode: children of this rank's runs
   int32_t any_active;      // sharded (device exchange): any rank still active
+  uint32_t spec_n;         // speculative round: epochs the frontier formed
+  uint32_t spec_acc;       // ... of which the validation accepted (a prefix)
+  uint32_t spec_k;         // epochs the next round may form (adaptive, 1..spec_kmax)
+  uint32_t spec_kmax;
   unsigned long long level_evals[kMaxLevels];  // flush evaluations per level
   // kept ranges of the remainder: one per key segment (BFS: 1, DFS: level)
   uint32_t seg_lo[kMaxLevels], seg_len[kMaxLevels], seg_pre[kMaxLevels + 1];
@@ -309,6 +313,326 @@ __global__ void __launch_bounds__(kFT) frontier_kernel(EpochState* st, Queue q, 
   }
 }
 
+// ---- speculative rounds (BFS) ----------------------------------------------
+// Between two flushes nothing is pushed, and in BFS a flush's survivors only
+// change later pops when their key precedes an entry those pops take.  A
+// round therefore forms up to k consecutive epochs from the current queue as
+// if no flush had survivors (frontier_spec_kernel; the incumbent B is carried
+// through leaf pops exactly as in the sequential loop, so every prune is
+// exact), branches and scores ALL their children with one launch of each
+// kernel, and validates (survivors_spec_kernel): epoch j is kept only when no
+// survivor of the kept epochs < j has a key below the last entry epoch j
+// popped (a drain epoch: when those epochs had no survivors at all).  The
+// kept epochs are a prefix; their Stats, trace and survivors are committed
+// exactly as the sequential schedule makes them (search.hpp:132-169), the
+// rest is discarded and re-formed by the next round from the true queue.
+constexpr int kSpecMax = 16;
+struct SpecRec {
+  unsigned long long lastkey;    // key of the epoch's last pop (its cut entry)
+  unsigned long long pruned;     // pops pruned, cumulative over the round
+  unsigned long long trace_end;  // trace length after the epoch
+  unsigned long long minkey;     // smallest survivor key, seq taken as newest (survivors_spec_kernel; ~0 none)
+  uint32_t child_end;            // children of epochs <= this one (pending offset end)
+  uint32_t cons_end;             // queue entries consumed through this epoch
+  uint32_t exp_end;              // expanding parents through this epoch
+  uint32_t n_surv;               // survivors of the epoch (survivors_spec_kernel)
+  int32_t B;                     // incumbent after the epoch's pops: its flush threshold
+  int32_t best_i;                // queue index of the round's last leaf update through this epoch (-1)
+  int32_t drained;               // 1: the queue ran out (drain flush, search.hpp:146-148)
+  int32_t pad;
+  uint32_t lv[kMaxLevels];       // the epoch's children per level (survivors_spec_kernel)
+};
+
+// per-pop counts packed for one block scan: pruned | leaf updates | expanding
+__device__ __forceinline__ unsigned long long pack3(uint32_t pr, uint32_t lu, uint32_t ex) {
+  return (static_cast<unsigned long long>(pr) << 42) | (static_cast<unsigned long long>(lu) << 21) | ex;
+}
+
+__global__ void __launch_bounds__(kFT) frontier_spec_kernel(EpochState* st, Queue q, GridView G,
+                                                            unsigned long long b, int k_max,
+                                                            uint32_t* __restrict__ exp_parent,
+                                                            uint32_t* __restrict__ exp_off,
+                                                            int32_t* __restrict__ trace,
+                                                            unsigned long long trace_cap,
+                                                            uint32_t* __restrict__ cache_ctl,
+                                                            SpecRec* __restrict__ rec) {
+  pdl_wait();
+
+  using ScanI = cub::BlockScan<int, kFT>;
+  using ScanU = cub::BlockScan<unsigned long long, kFT>;
+  using RedI = cub::BlockReduce<int, kFT>;
+  __shared__ union {
+    typename ScanI::TempStorage si;
+    typename ScanU::TempStorage su;
+    typename RedI::TempStorage ri;
+  } tmp;
+  __shared__ int s_i;
+  __shared__ int s_active;
+  __shared__ struct {
+    unsigned long long S[kFChunk];  // inclusive children sums (round-global); ~0 past the queue
+    unsigned long long C[kFChunk];  // inclusive packed counts (chunk)
+    int L[kFChunk];                 // last leaf update through the pop
+    int Bk[kFChunk];                // incumbent after the pop
+    int ep, limit;
+    unsigned long long cut_base;
+  } sh;
+
+  const int tid = threadIdx.x;
+  if (tid == 0) s_active = st->active;
+  __syncthreads();
+  if (!s_active) {
+    if (tid == 0) {
+      st->n_children = 0;
+      st->spec_n = 0;
+    }
+    return;
+  }
+  const uint32_t qlen = st->q_len;
+  const unsigned long long* __restrict__ qk = q.keys(st->cur);
+  const bbs_node* __restrict__ pool = q.pool;
+  k_max = max(1, min(k_max, static_cast<int>(st->spec_k)));  // adaptive depth of this round
+  int carry_best = st->best;
+  unsigned long long carry_sum = 0, carry_trace = st->trace_len, carry_pruned = 0;
+  unsigned long long cut_base = 0;  // children of the epochs formed so far
+  uint32_t carry_exp = 0;
+  int carry_lu = -1;                // queue index of the round's last leaf update
+  int ep = 0;
+
+  for (uint32_t base = 0; base < qlen && ep < k_max; base += kFChunk) {
+    bbs_node nd[kFIPT];
+    bool valid[kFIPT];
+    int lm = INT_MIN;
+#pragma unroll
+    for (int k = 0; k < kFIPT; ++k) {
+      const uint32_t i = base + tid * kFIPT + k;
+      valid[k] = i < qlen;
+      if (valid[k]) {
+        nd[k] = pool[key_seq(BBS_STRATEGY_BFS, qk[i])];
+        if (nd[k].level == 0) lm = max(lm, nd[k].score);
+      }
+    }
+    int excl;
+    ScanI(tmp.si).ExclusiveScan(lm, excl, INT_MIN, cub::Max());
+    __syncthreads();
+    int B = max(carry_best, excl);
+    uint32_t c[kFIPT];
+    bool pr[kFIPT], lu[kFIPT];
+    int Bk[kFIPT];
+    unsigned long long csum = 0, cnt = 0;
+    int mylu = -1;
+#pragma unroll
+    for (int k = 0; k < kFIPT; ++k) {
+      c[k] = 0;
+      pr[k] = lu[k] = false;
+      if (valid[k]) {
+        const int sc = nd[k].score;
+        pr[k] = sc < B;  // search.hpp:150-153
+        const bool leaf = nd[k].level == 0;
+        lu[k] = !pr[k] && leaf;  // search.hpp:154-160
+        if (lu[k]) {
+          B = sc;
+          mylu = static_cast<int>(base + tid * kFIPT + k);
+        }
+        if (!pr[k] && !leaf) c[k] = n_children_of(G, nd[k]);
+      }
+      Bk[k] = B;  // the incumbent after this pop
+      csum += c[k];
+      cnt += pack3(pr[k] ? 1u : 0u, lu[k] ? 1u : 0u, c[k] ? 1u : 0u);
+    }
+    unsigned long long sexcl, stotal;
+    ScanU(tmp.su).ExclusiveSum(csum, sexcl, stotal);
+    __syncthreads();
+    unsigned long long cexcl, ctotal;
+    ScanU(tmp.su).ExclusiveSum(cnt, cexcl, ctotal);
+    __syncthreads();
+    int luexcl;
+    ScanI(tmp.si).ExclusiveScan(mylu, luexcl, -1, cub::Max());
+    __syncthreads();
+    // inclusive per pop: children sum (round-global), packed counts, last leaf update
+    unsigned long long Sin[kFIPT], Cin[kFIPT];
+    int Lin[kFIPT];
+    {
+      unsigned long long S = carry_sum + sexcl, Cc = cexcl;
+      int Lc = max(carry_lu, luexcl);
+#pragma unroll
+      for (int k = 0; k < kFIPT; ++k) {
+        S += c[k];
+        Cc += pack3(pr[k] ? 1u : 0u, lu[k] ? 1u : 0u, c[k] ? 1u : 0u);
+        if (lu[k]) Lc = static_cast<int>(base + tid * kFIPT + k);
+        Sin[k] = S;
+        Cin[k] = Cc;
+        Lin[k] = Lc;
+      }
+    }
+    // successive cuts in this chunk: the first pop whose inclusive children
+    // sum exceeds the previous cut's by more than b (search.hpp:166).  The
+    // sums are non-decreasing, so warp 0 finds each cut with a 32-ary search
+    // over the chunk's sums in shared memory (the first index past a sum is
+    // a pop with children) and writes the epoch records.
+#pragma unroll
+    for (int k = 0; k < kFIPT; ++k) {
+      const int li = tid * kFIPT + k;
+      sh.S[li] = valid[k] ? Sin[k] : ~0ull;
+      sh.C[li] = Cin[k];
+      sh.L[li] = Lin[k];
+      sh.Bk[li] = Bk[k];
+    }
+    __syncthreads();
+    if (tid < 32) {
+      const uint32_t lane = tid;
+      const uint32_t nv = min(static_cast<uint32_t>(kFChunk), qlen - base);
+      uint32_t lo = 0;
+      int e = ep;
+      unsigned long long cb = cut_base;
+      int lim = kFChunk - 1;
+      while (e < k_max && lo < nv) {
+        // first li in [lo, nv) with S[li] > cb + b
+        const unsigned long long x = cb + b;
+        uint32_t l = lo, h = nv;
+        while (l < h) {
+          const uint32_t step = (h - l + 31u) >> 5;
+          const uint32_t pos = l + (lane + 1u) * step - 1u;
+          const bool le = pos < h && sh.S[pos] <= x;
+          const uint32_t c = static_cast<uint32_t>(__popc(__ballot_sync(0xffffffffu, le)));
+          const uint32_t nh = l + (c + 1u) * step - 1u;
+          l += c * step;
+          if (nh < h) h = nh;
+        }
+        if (l >= nv) break;
+        if (lane == 0) {
+          const unsigned long long Cc = sh.C[l];
+          SpecRec r;
+          r.lastkey = qk[base + l];
+          r.pruned = carry_pruned + (Cc >> 42);
+          r.trace_end = carry_trace + ((Cc >> 21) & 0x1FFFFFull);
+          r.minkey = ~0ull;
+          r.child_end = static_cast<uint32_t>(sh.S[l]);
+          r.cons_end = base + l + 1u;
+          r.exp_end = carry_exp + static_cast<uint32_t>(Cc & 0x1FFFFFull);
+          r.n_surv = 0;
+          r.B = sh.Bk[l];
+          r.best_i = sh.L[l];
+          r.drained = 0;
+          r.pad = 0;
+          for (int lv = 0; lv < kMaxLevels; ++lv) r.lv[lv] = 0;
+          rec[e] = r;
+        }
+        cb = sh.S[l];
+        lo = l + 1;
+        ++e;
+        if (e == k_max) lim = static_cast<int>(l);
+      }
+      if (lane == 0) {
+        sh.ep = e;
+        sh.cut_base = cb;
+        sh.limit = lim;
+      }
+    }
+    __syncthreads();
+    ep = sh.ep;
+    cut_base = sh.cut_base;
+    const long long limit = static_cast<long long>(base) + sh.limit;  // pops this round emits
+    __syncthreads();
+    // expanding parents (branch inputs) and leaf updates (trace) of the pops
+    // up to `limit`, at their round-global positions
+#pragma unroll
+    for (int k = 0; k < kFIPT; ++k) {
+      const long long i = base + tid * kFIPT + k;
+      if (!valid[k] || i > limit) continue;
+      if (c[k]) {
+        const uint32_t e = carry_exp + static_cast<uint32_t>(Cin[k] & 0x1FFFFFull) - 1u;
+        exp_parent[e] = key_seq(BBS_STRATEGY_BFS, qk[i]);  // the parent's pool slot
+        exp_off[e] = static_cast<uint32_t>(Sin[k] - c[k]);
+      }
+      if (lu[k]) {
+        const unsigned long long t = carry_trace + ((Cin[k] >> 21) & 0x1FFFFFull) - 1u;
+        if (t < trace_cap) trace[t] = nd[k].score;
+      }
+    }
+    if (ep == k_max) break;
+    // the whole chunk belongs to the round: carry it
+    carry_sum += stotal;
+    carry_pruned += ctotal >> 42;
+    carry_trace += (ctotal >> 21) & 0x1FFFFFull;
+    carry_exp += static_cast<uint32_t>(ctotal & 0x1FFFFFull);
+    {
+      const int lmax = RedI(tmp.ri).Reduce(Lin[kFIPT - 1], cub::Max());
+      if (tid == 0) s_i = lmax;
+      __syncthreads();
+      carry_lu = s_i;
+      __syncthreads();
+    }
+    // the incumbent after the chunk: the last pop's B (non-decreasing)
+    if (tid == kFT - 1) s_i = Bk[kFIPT - 1];
+    __syncthreads();
+    carry_best = s_i;
+    __syncthreads();
+    // BFS: the first pruned pop ends the queue (scores non-increasing, B never
+    // decreases): all later pops are pruned, with no children
+    bool has_pr = false;
+#pragma unroll
+    for (int k = 0; k < kFIPT; ++k) has_pr |= valid[k] && pr[k];
+    if (__syncthreads_or(has_pr)) {
+      const uint32_t end = base + kFChunk;
+      if (qlen > end) carry_pruned += qlen - end;
+      break;
+    }
+  }
+  if (tid != 0) return;
+  if (ep < k_max) {
+    // the queue ran out (or only pruned pops remain) with the open epoch
+    if (carry_sum > cut_base) {
+      // its children are flushed on the drain (search.hpp:146-148)
+      SpecRec r;
+      r.lastkey = ~0ull;
+      r.pruned = carry_pruned;
+      r.trace_end = carry_trace;
+      r.minkey = ~0ull;
+      r.child_end = static_cast<uint32_t>(carry_sum);
+      r.cons_end = qlen;
+      r.exp_end = carry_exp;
+      r.n_surv = 0;
+      r.B = carry_best;
+      r.best_i = carry_lu;
+      r.drained = 1;
+      r.pad = 0;
+      for (int l = 0; l < kMaxLevels; ++l) r.lv[l] = 0;
+      rec[ep] = r;
+      ++ep;
+    } else if (ep == 0) {
+      // queue drained with nothing pending: the loop ends (search.hpp:145);
+      // commit the last pops (prunes, leaf updates) here
+      st->nodes_pruned += carry_pruned;
+      st->best = carry_best;
+      st->flush_best = carry_best;
+      st->trace_len = carry_trace;
+      if (carry_lu >= 0) {
+        st->best_node = pool[key_seq(BBS_STRATEGY_BFS, qk[carry_lu])];
+        st->matched = 1;
+        st->last_best_epoch = static_cast<int32_t>(st->pass);
+      }
+      st->pass += 1;
+      st->active = 0;
+      st->q_len = 0;
+      st->n_children = 0;
+      st->spec_n = 0;
+      return;
+    }
+    // else: the trailing pops (no children) are left to the next round
+  }
+  if (cache_ctl) {
+    cache_ctl[2] = 0;  // builds claimed this flush
+    cache_ctl[3] = 0;  // runs listed for the cube kernel
+    uint32_t raw = 0;
+    for (int l = 0; l < kMaxLevels; ++l) raw |= cache_ctl[4 + l] ? 1u << l : 0u;
+    st->cache_raw = raw;
+  }
+  st->surv_ticket = 0;
+  st->spec_n = static_cast<uint32_t>(ep);
+  st->n_children = rec[ep - 1].child_end;  // every formed epoch's children are scored
+  st->n_expand = rec[ep - 1].exp_end;
+}
+
 // E2: branch() (nodes.hpp:91-121) for every expanding parent, children in
 // pop order, each parent's children in (jr, jp, jw, jx, jy, jz) order.
 // Batch-split exact mode: the flush's runs of 8 children are
@@ -336,15 +660,28 @@ __global__ void branch_kernel(EpochState* st, Queue q, GridView G,
   if (n == 0) return;
   const uint32_t ne = st->n_expand;
   const bbs_node* __restrict__ pool = q.pool;
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    uint32_t lo = 0, hi = ne - 1;  // largest m with exp_off[m] <= i
-    while (lo < hi) {
-      const uint32_t mid = (lo + hi + 1) >> 1;
-      if (exp_off[mid] <= i)
-        lo = mid;
-      else
-        hi = mid - 1;
+  const uint32_t lane = threadIdx.x & 31u;
+  // warps take 32 consecutive children: lane 0 binary-searches the first
+  // one's parent, the lanes step forward from it (a parent has >= 8
+  // children, so a warp spans at most 5 parents)
+  for (uint32_t w0 = blockIdx.x * blockDim.x + (threadIdx.x & ~31u); w0 < n; w0 += gridDim.x * blockDim.x) {
+    uint32_t m0 = 0;
+    if (lane == 0) {
+      uint32_t lo = 0, hi = ne - 1;  // largest m with exp_off[m] <= w0
+      while (lo < hi) {
+        const uint32_t mid = (lo + hi + 1) >> 1;
+        if (exp_off[mid] <= w0)
+          lo = mid;
+        else
+          hi = mid - 1;
+      }
+      m0 = lo;
     }
+    m0 = __shfl_sync(0xffffffffu, m0, 0);
+    const uint32_t i = w0 + lane;
+    if (i >= n) continue;
+    uint32_t lo = m0;
+    while (lo + 1 < ne && exp_off[lo + 1] <= i) ++lo;
     const bbs_node p = pool[exp_parent[lo]];
     const uint32_t local = i - exp_off[lo];
     int32_t a[3], c[3];
@@ -474,6 +811,47 @@ __device__ void trim_remainder(EpochState* st, const Queue& q, int strategy, int
   }
 }
 
+// Decoupled look-back by one whole warp (ordered compaction across tiles):
+// tile `tile` publishes its aggregate `tot`, then the 32 lanes read 32
+// predecessor words at a time, stop at the nearest inclusive prefix and sum
+// the aggregates after it; returns the exclusive prefix of `tile` and
+// publishes the inclusive one.  Words: tag | status << 32 | value (status 1
+// aggregate, 2 inclusive); tile 0 is inclusive at once, so the walk ends.
+__device__ uint32_t warp_lookback(unsigned long long* tiles, uint32_t tile, uint32_t tot,
+                                  unsigned long long tag) {
+  const uint32_t lane = threadIdx.x & 31u;
+  constexpr unsigned long long kTagMask = ~((1ull << 34) - 1);
+  if (tile == 0) {
+    if (lane == 0) atomicExch(&tiles[0], tag | (2ull << 32) | tot);
+    return 0;
+  }
+  if (lane == 0) atomicExch(&tiles[tile], tag | (1ull << 32) | tot);
+  uint32_t excl = 0;
+  int64_t t = static_cast<int64_t>(tile) - 1;  // the window is tiles t, t-1, ..., t-31
+  for (;;) {
+    const int64_t j = t - static_cast<int64_t>(lane);
+    unsigned long long w = 0;
+    bool pub = true;
+    if (j >= 0) {
+      w = atomicAdd(&tiles[j], 0ull);
+      pub = (w & kTagMask) == tag;
+    }
+    const unsigned incl = __ballot_sync(0xffffffffu, j >= 0 && pub && ((w >> 32) & 3u) == 2u);
+    const unsigned unpub = __ballot_sync(0xffffffffu, j >= 0 && !pub);
+    const int stop = incl ? __ffs(incl) - 1 : 31;  // lanes 0..stop are needed
+    const unsigned need = stop == 31 ? 0xffffffffu : ((2u << stop) - 1u);
+    if (unpub & need) continue;  // a needed predecessor has not published yet
+    uint32_t v = (j >= 0 && static_cast<int>(lane) <= stop) ? static_cast<uint32_t>(w) : 0u;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    excl += v;
+    if (incl) break;
+    t -= 32;
+  }
+  if (lane == 0) atomicExch(&tiles[tile], tag | (2ull << 32) | (excl + tot));
+  return excl;
+}
+
 // E4a: flush pruning (search.hpp:134-140): keep score >= B in pending order
 // and give them consecutive seq numbers.  Single-pass ordered compaction:
 // tiles take tickets in order and chain their prefix through `tiles`
@@ -533,23 +911,10 @@ __global__ void __launch_bounds__(kST) survivors_kernel(EpochState* st, Queue q,
     }
     int pos, tot;
     ScanI(tmp.scan).ExclusiveSum(cnt, pos, tot);
-    if (threadIdx.x == 0) {
-      uint32_t excl = 0;
-      if (tile == 0) {
-        atomicExch(&tiles[0], tag | (2ull << 32) | static_cast<uint32_t>(tot));
-      } else {
-        atomicExch(&tiles[tile], tag | (1ull << 32) | static_cast<uint32_t>(tot));
-        for (int64_t t = static_cast<int64_t>(tile) - 1; t >= 0;) {
-          const unsigned long long w = atomicAdd(&tiles[t], 0ull);
-          if ((w & ~((1ull << 34) - 1)) != tag) continue;  // not published yet
-          excl += static_cast<uint32_t>(w);
-          if (((w >> 32) & 3u) == 2u) break;                // inclusive prefix
-          --t;
-        }
-        atomicExch(&tiles[tile], tag | (2ull << 32) | (excl + static_cast<uint32_t>(tot)));
-      }
-      s_excl = excl;
-      if (tile == n_tiles - 1) {
+    if (threadIdx.x < 32) {
+      const uint32_t excl = warp_lookback(tiles, tile, static_cast<uint32_t>(tot), tag);
+      if (threadIdx.x == 0) s_excl = excl;
+      if (threadIdx.x == 0 && tile == n_tiles - 1) {
         const uint32_t kept = excl + static_cast<uint32_t>(tot);
         st->n_surv = kept;
         st->seq = seq0 + kept;
@@ -571,15 +936,207 @@ __global__ void __launch_bounds__(kST) survivors_kernel(EpochState* st, Queue q,
   }
 }
 
+
+// E4a, speculative round: survivors of EVERY formed epoch (each against its
+// own B) compacted in pending order -- the kept epochs' survivors are a
+// prefix of them -- while each tile adds its per-epoch survivor count, its
+// smallest survivor key and its per-(epoch, level) evaluations to the round
+// records BEFORE publishing its look-back aggregate; the last tile then
+// holds every tile's contribution, validates the round (epoch j kept while
+// no kept survivor precedes its last pop; a drain epoch only without
+// earlier survivors) and commits the kept epochs into EpochState exactly as
+// the sequential loop would have (search.hpp:132-169).  The queue trim runs
+// in the next kernel (it needs the committed B and consumed count).
+__global__ void __launch_bounds__(kST) survivors_spec_kernel(EpochState* st, Queue q,
+                                                             const bbs_node* __restrict__ pending,
+                                                             const int32_t* __restrict__ scores,
+                                                             unsigned long long* __restrict__ s_key,
+                                                             unsigned long long* __restrict__ tiles,
+                                                             SpecRec* __restrict__ rec) {
+  pdl_wait();
+
+  using Load = cub::BlockLoad<int32_t, kST, kSIPT, cub::BLOCK_LOAD_WARP_TRANSPOSE>;
+  using ScanI = cub::BlockScan<int, kST>;
+  __shared__ union {
+    typename Load::TempStorage load;
+    typename ScanI::TempStorage scan;
+  } tmp;
+  __shared__ uint32_t s_tile, s_excl;
+  __shared__ uint32_t s_end[kSpecMax];
+  __shared__ int32_t s_B[kSpecMax];
+  __shared__ unsigned long long s_min[kSpecMax];
+  __shared__ uint32_t s_cnt[kSpecMax];
+  __shared__ uint32_t s_lv[kSpecMax * kMaxLevels];
+  const uint32_t ne = st->spec_n;
+  if (ne == 0) return;  // nothing formed: the search ended in the frontier
+  if (threadIdx.x < ne) {
+    s_end[threadIdx.x] = rec[threadIdx.x].child_end;
+    s_B[threadIdx.x] = rec[threadIdx.x].B;
+  }
+  const uint32_t n = st->n_children;  // every formed epoch's children
+  const unsigned long long seq0 = st->seq;
+  // look-back tag of this round: never 0 (the zeroed tile words), and the
+  // round's pass is only incremented by the commit below
+  const unsigned long long tag = static_cast<unsigned long long>(st->pass % 0x3FFFFFFFu + 1u) << 34;
+  const uint32_t n_tiles = (n + kSTile - 1) / kSTile;
+  for (;;) {
+    __syncthreads();
+    if (threadIdx.x == 0) s_tile = atomicAdd(&st->surv_ticket, 1u);
+    if (threadIdx.x < kSpecMax) {
+      s_min[threadIdx.x] = ~0ull;
+      s_cnt[threadIdx.x] = 0;
+    }
+    for (int t = threadIdx.x; t < kSpecMax * kMaxLevels; t += kST) s_lv[t] = 0;
+    __syncthreads();
+    const uint32_t tile = s_tile;
+    if (tile >= n_tiles) break;
+    const uint32_t base = tile * kSTile;
+    const uint32_t valid = min(static_cast<uint32_t>(kSTile), n - base);
+    int32_t sc[kSIPT];
+    Load(tmp.load).Load(scores + base, sc, static_cast<int>(valid), INT_MIN);
+    __syncthreads();
+    // each thread's kSIPT items lie in at most a few epochs (boundaries are
+    // multiples of 8, the runs of one parent's translation cube)
+    uint32_t ek[kSIPT];
+    int cnt = 0;
+    {
+      uint32_t e = 0;
+#pragma unroll
+      for (int k = 0; k < kSIPT; ++k) {
+        const uint32_t i = base + threadIdx.x * kSIPT + k;
+        if (threadIdx.x * kSIPT + k >= valid) sc[k] = INT_MIN;
+        while (e + 1 < ne && s_end[e] <= i) ++e;
+        ek[k] = e;
+        cnt += sc[k] >= s_B[e] ? 1 : 0;
+      }
+    }
+    static_assert(kSIPT % 8 == 0, "tile rows must hold whole runs");
+#pragma unroll
+    for (int rr = 0; rr < kSIPT / 8; ++rr) {
+      const uint32_t li = threadIdx.x * kSIPT + rr * 8;
+      const int lvl = li < valid ? static_cast<int>(ek[rr * 8] * kMaxLevels) + (pending[base + li].level & (kMaxLevels - 1)) : -1;
+      const unsigned same = __match_any_sync(0xffffffffu, lvl);
+      if (lvl >= 0 && (__ffs(same) - 1) == (threadIdx.x & 31)) atomicAdd(&s_lv[lvl], 8u * __popc(same));
+    }
+#pragma unroll
+    for (int k = 0; k < kSIPT; ++k) {
+      if (threadIdx.x * kSIPT + k >= valid || sc[k] < s_B[ek[k]]) continue;
+      const uint32_t i = base + threadIdx.x * kSIPT + k;
+      // a survivor's seq is newer than every queued entry's
+      atomicMin(&s_min[ek[k]], queue_key(BBS_STRATEGY_BFS, sc[k], pending[i].level, kSeqMax));
+      atomicAdd(&s_cnt[ek[k]], 1u);
+    }
+    __syncthreads();
+    // this tile's contributions to the round records, then its aggregate
+    {
+      bool wrote = false;
+      if (threadIdx.x < ne && s_cnt[threadIdx.x]) {
+        atomicMin(&rec[threadIdx.x].minkey, s_min[threadIdx.x]);
+        atomicAdd(&rec[threadIdx.x].n_surv, s_cnt[threadIdx.x]);
+        wrote = true;
+      }
+      for (int t = threadIdx.x; t < static_cast<int>(ne) * kMaxLevels; t += kST)
+        if (s_lv[t]) {
+          atomicAdd(&rec[t / kMaxLevels].lv[t % kMaxLevels], s_lv[t]);
+          wrote = true;
+        }
+      if (wrote) __threadfence();  // before this tile's aggregate is published
+    }
+    __syncthreads();
+    int pos, tot;
+    ScanI(tmp.scan).ExclusiveSum(cnt, pos, tot);
+    if (threadIdx.x < 32) {
+      const uint32_t excl = warp_lookback(tiles, tile, static_cast<uint32_t>(tot), tag);
+      if (threadIdx.x == 0) s_excl = excl;
+      if (tile == n_tiles - 1) {
+        // every tile published after adding to the records: validate and
+        // commit, warp-parallel (lane e reads epoch e's record)
+        __threadfence();
+        const uint32_t lane = threadIdx.x;
+        const bool has = lane < ne;
+        const uint32_t ns = has ? __ldcg(&rec[lane].n_surv) : 0u;
+        const unsigned long long mk = has ? __ldcg(&rec[lane].minkey) : ~0ull;
+        const unsigned long long lk = has ? __ldcg(&rec[lane].lastkey) : 0ull;
+        const int dr = has ? __ldcg(&rec[lane].drained) : 0;
+        // epoch j > 0 is overtaken when a survivor of an earlier epoch
+        // precedes its last pop (drain epoch: any earlier survivor)
+        unsigned long long pm = mk;  // inclusive prefix min of the survivor keys
+        uint32_t ps = ns;            // inclusive prefix sum of the survivor counts
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+          const unsigned long long om = __shfl_up_sync(0xffffffffu, pm, d);
+          const uint32_t os = __shfl_up_sync(0xffffffffu, ps, d);
+          if (static_cast<int>(lane) >= d) {
+            pm = min(pm, om);
+            ps += os;
+          }
+        }
+        const unsigned long long pm_before = __shfl_up_sync(0xffffffffu, pm, 1);
+        const uint32_t ps_before = __shfl_up_sync(0xffffffffu, ps, 1);
+        const bool bad = has && lane > 0 && (dr ? ps_before != 0 : !(pm_before > lk));
+        const unsigned badm = __ballot_sync(0xffffffffu, bad);
+        const uint32_t A = badm ? static_cast<uint32_t>(__ffs(badm) - 1) : ne;
+        const uint32_t S_acc = __shfl_sync(0xffffffffu, ps, A - 1);
+        // per-level evaluations of the kept epochs: lane l sums level l
+        if (lane < kMaxLevels) {
+          unsigned long long v = 0;
+          for (uint32_t e = 0; e < A; ++e) v += __ldcg(&rec[e].lv[lane]);
+          if (v) st->level_evals[lane] += v;
+        }
+        if (lane == 0) {
+          const SpecRec& r = rec[A - 1];
+          const uint32_t child_acc = r.child_end;
+          st->spec_acc = A;
+          st->n_surv = S_acc;
+          st->seq = seq0 + S_acc;
+          st->n_children = child_acc;
+          st->n_cons = r.cons_end;
+          st->n_expand = r.exp_end;
+          st->nodes_pruned += r.pruned + (child_acc - S_acc);
+          st->best = r.B;
+          st->flush_best = r.B;
+          st->trace_len = r.trace_end;
+          if (r.best_i >= 0) {
+            st->best_node = q.pool[key_seq(BBS_STRATEGY_BFS, q.keys(st->cur)[r.best_i])];
+            st->matched = 1;
+            st->last_best_epoch = static_cast<int32_t>(st->pass);
+          }
+          st->pass += 1;
+          st->nodes_generated += child_acc;
+          st->batches_flushed += A;
+          st->epochs += A;
+        }
+      }
+    }
+    __syncthreads();
+    uint32_t o = s_excl + static_cast<uint32_t>(pos);
+#pragma unroll
+    for (int k = 0; k < kSIPT; ++k) {
+      if (sc[k] < s_B[ek[k]] || threadIdx.x * kSIPT + k >= valid) continue;
+      const uint32_t i = base + threadIdx.x * kSIPT + k;
+      bbs_node c = pending[i];
+      c.score = sc[k];
+      q.pool[seq0 + o] = c;  // push: the node's permanent slot (kept prefix only survives)
+      s_key[o] = queue_key(BBS_STRATEGY_BFS, c.score, c.level, seq0 + o);
+      ++o;
+    }
+  }
+}
+
 // E4b: order the survivors by key.  Keys are unique (they embed seq), so a
 // survivor's rank = #keys below it; ranks are computed against smem tiles.
 constexpr int kRT = 256;
-__global__ void __launch_bounds__(kRT) rank_sort_kernel(const EpochState* st,
+__global__ void __launch_bounds__(kRT) rank_sort_kernel(EpochState* st,
                                                         const unsigned long long* __restrict__ key,
-                                                        unsigned long long* __restrict__ out_key) {
+                                                        unsigned long long* __restrict__ out_key,
+                                                        Queue q, int trim_strategy) {
   pdl_wait();
 
   __shared__ unsigned long long tile[kRT];
+  // speculative rounds: the incumbent trim of the queue remainder runs here,
+  // after survivors_spec_kernel committed the round (trim_strategy >= 0)
+  if (trim_strategy >= 0 && blockIdx.x == 0 && threadIdx.x < 32 && st->n_children)
+    trim_remainder(st, q, trim_strategy, st->flush_best);
   const uint32_t n = st->n_children ? st->n_surv : 0;
   if (n == 0) return;
   for (uint32_t base = blockIdx.x * kRT; base < n; base += gridDim.x * kRT) {
@@ -602,8 +1159,11 @@ __global__ void __launch_bounds__(kRT) rank_sort_kernel(const EpochState* st,
 // the survivor keys is set to the largest key and the whole buffer goes
 // through a CUB radix sort (O(n) instead of rank_sort's O(n^2)).
 constexpr uint64_t kRankSortMax = 16384;
-__global__ void pad_keys_kernel(const EpochState* st, unsigned long long* __restrict__ key, uint64_t cap) {
+__global__ void pad_keys_kernel(EpochState* st, unsigned long long* __restrict__ key, uint64_t cap, Queue q,
+                                int trim_strategy) {
   pdl_wait();
+  if (trim_strategy >= 0 && blockIdx.x == 0 && threadIdx.x < 32 && st->n_children)
+    trim_remainder(st, q, trim_strategy, st->flush_best);
   const uint64_t n = st->n_children ? st->n_surv : 0;
   for (uint64_t i = n + blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < cap; i += uint64_t(gridDim.x) * blockDim.x)
     key[i] = ~0ull;
@@ -1065,7 +1625,7 @@ struct Workspace {
   Buf<int32_t> root_scores;
   Buf<unsigned long long> probes, surv_idx, qk0, qk1, s_key, s_key2, surv_tiles;
   Buf<int> nsel;
-  Buf<unsigned char> temp, sort_temp;
+  Buf<unsigned char> temp, sort_temp, spec;
   Buf<bbs_node> pool, pending, pending_own;
   Buf<uint32_t> perm0, perm1, sk0, sk1, exp_parent, exp_off;
   Buf<int32_t> pscores, trace, hist_n, pscores_own, xchg;
@@ -1103,6 +1663,7 @@ struct Workspace {
     nsel.release();
     temp.release();
     sort_temp.release();
+    spec.release();
     hist_ent.release();
     cache_info.release();
     cache_pool.release();
@@ -1324,8 +1885,19 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
   tmark("lut");
   const ScanView sv{scan->soa, scan->soa + K, scan->soa + 2 * K, static_cast<uint32_t>(K)};
   const uint64_t maxc = max_children(grid);
-  const uint64_t pend_cap = cfg.batch_size + maxc;
   const int strategy = cfg.strategy;
+  const uint64_t pend_epoch = cfg.batch_size + maxc;  // children of one flush, at most
+  // speculative rounds (BFS, unsharded, no dump): up to spec_k epochs per
+  // round (frontier_spec_kernel); BBS_SPEC=n overrides (1 = one epoch per round)
+  const int spec_k = [&] {
+    if (dump || shard || strategy != BBS_STRATEGY_BFS) return 1;
+    const char* v = std::getenv("BBS_SPEC");
+    int k = v ? std::atoi(v) : 16;
+    k = std::max(1, std::min(k, kSpecMax));
+    while (k > 1 && pend_epoch * static_cast<uint64_t>(k) > (1ull << 21)) --k;
+    return k;
+  }();
+  const uint64_t pend_cap = pend_epoch * static_cast<uint64_t>(spec_k);  // children of one round
   uint64_t launches = 0;
 
   cudaEvent_t ev_start = W.next_event(), ev_roots0 = W.next_event(), ev_roots1 = W.next_event(),
@@ -1587,7 +2159,8 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
   const uint64_t n_scored_roots = exact ? static_cast<uint64_t>(std::max<int64_t>(total, 0)) : n_own;
 
   // survivors >= threshold among own roots, in initial_nodes order
-  const int E = (host_x || dump) ? 1 : 8;  // epochs per host check
+  const bool dbg_spec = std::getenv("BBS_DEBUG_SPEC") != nullptr;  // per-round state (stderr)
+  const int E = (host_x || dump || dbg_spec) ? 1 : 8;  // epochs per host check
   unsigned long long root_probes = 0;
   int n_root_surv = 0;       // host path only
   unsigned long long* surv_idx = nullptr;
@@ -1659,6 +2232,8 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
   h0.active = n_root_surv > 0 ? 1 : 0;
   h0.any_active = h0.active;
   h0.q_peak = h0.q_len;
+  h0.spec_k = static_cast<uint32_t>(spec_k);
+  h0.spec_kmax = static_cast<uint32_t>(spec_k);
   EpochState* d_st = W.st.get(1, s);
   if (!dev_init) {
     *W.h_st = h0;
@@ -1741,14 +2316,20 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
   unsigned long long* s_key2 = W.s_key2.get(pend_cap, s);
   size_t sort_temp_bytes = 0;
   void* sort_temp = nullptr;
-  if (pend_cap > kRankSortMax) {
+  // survivors of one flush are at most pend_epoch: the rank sort up to
+  // kRankSortMax of them (a speculative round keeps few), else a radix sort
+  const bool rank_sorted = pend_epoch <= kRankSortMax;
+  SpecRec* d_rec = spec_k > 1 ? reinterpret_cast<SpecRec*>(W.spec.get(kSpecMax * sizeof(SpecRec), s)) : nullptr;
+  if (!rank_sorted) {
     BBS_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, sort_temp_bytes, s_key, s_key2, static_cast<int64_t>(pend_cap),
                                             0, 64, s));
     sort_temp = W.sort_temp.get(sort_temp_bytes, s);
   }
   const uint64_t trace_cap = cfg.collect_trace ? std::max<uint64_t>(out->trace_capacity, 1) : 0;
   int32_t* d_trace = W.trace.get(std::max<uint64_t>(trace_cap, 1), s);
-  const uint32_t ptiles = choose_ptiles((pend_cap + 7) / 8, static_cast<uint32_t>(K));
+  // point tiles per run: one epoch's children, or a whole speculative round's
+  const uint32_t ptiles_epoch = choose_ptiles((pend_epoch + 7) / 8, static_cast<uint32_t>(K));
+  const uint32_t ptiles_round = choose_ptiles((pend_cap + 7) / 8, static_cast<uint32_t>(K));
   // the level L-1 prebuild ran on the side stream during the root survivor
   // selection and queue build
   if (prebuild_pending) BBS_CUDA(cudaStreamWaitEvent(s, ev_prebuilt, 0));
@@ -1790,9 +2371,17 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
       if (cache.base[l] != 0xFFFFFFFFu && l != cache.pre_level) claimable |= 1u << l;
   bool builds_live = claimable != 0;
   // one flush epoch (frontier -> branch -> score -> survivors -> sort -> merge)
+  // speculative rounds start once the search outlives its first host check
+  // (E single epochs): short searches (C2: 7 flushes, survivors that overtake
+  // the next prefix every flush) keep the plain epoch chain
+  bool spec_on = false;
   auto enqueue_epoch = [&](int e) {
-    launch_pdl(frontier_kernel, 1, kFT, 0, s, d_st, q, gv, cfg.batch_size, exp_parent, exp_off, d_trace,
-               trace_cap, strategy, cache.enabled ? cache.ctl : nullptr);
+    if (spec_on)
+      launch_pdl(frontier_spec_kernel, 1, kFT, 0, s, d_st, q, gv, cfg.batch_size, spec_k, exp_parent, exp_off,
+                 d_trace, trace_cap, cache.enabled ? cache.ctl : nullptr, d_rec);
+    else
+      launch_pdl(frontier_kernel, 1, kFT, 0, s, d_st, q, gv, cfg.batch_size, exp_parent, exp_off, d_trace,
+                 trace_cap, strategy, cache.enabled ? cache.ctl : nullptr);
     BBS_CUDA(cudaGetLastError());
     record(ev_pass[e]);
     launch_pdl(branch_kernel, grid1(pend_cap), 256, 0, s, d_st, q, gv, exp_parent, exp_off, pending, pscores,
@@ -1800,28 +2389,33 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
     BBS_CUDA(cudaGetLastError());
     record(ev_s0[e]);
     if (exact) {
-      launch_epoch_score(m->view, gv, sv, split.pending_own, d_nchild, static_cast<uint32_t>(pend_cap), ptiles,
-                         split.pscores_own, cache, s, builds_live);
+      launch_epoch_score(m->view, gv, sv, split.pending_own, d_nchild, static_cast<uint32_t>(pend_epoch),
+                         ptiles_epoch, split.pscores_own, cache, s, builds_live);
       record(ev_s1[e]);
       launch_pdl(scatter_own_kernel, grid1(pend_cap), 256, 0, s, d_st, split, pscores);
       BBS_CUDA(cudaGetLastError());
       ++launches;
       xmax(pscores, pend_cap);  // every rank: every score of the flush
     } else {
-      launch_epoch_score(m->view, gv, sv, pending, d_nchild, static_cast<uint32_t>(pend_cap), ptiles,
-                         pscores, cache, s, builds_live);
+      launch_epoch_score(m->view, gv, sv, pending, d_nchild, static_cast<uint32_t>(spec_on ? pend_cap : pend_epoch),
+                         spec_on ? ptiles_round : ptiles_epoch, pscores, cache, s, builds_live);
       record(ev_s1[e]);
     }
-    launch_pdl(survivors_kernel, surv_grid, kST, 0, s, d_st, q, strategy, pending, pscores, s_key,
-               surv_tiles);
+    if (spec_on)  // survivors of the round + validation + commit of the kept epochs
+      launch_pdl(survivors_spec_kernel, surv_grid, kST, 0, s, d_st, q, static_cast<const bbs_node*>(pending),
+                 static_cast<const int32_t*>(pscores), s_key, surv_tiles, d_rec);
+    else
+      launch_pdl(survivors_kernel, surv_grid, kST, 0, s, d_st, q, strategy, pending, pscores, s_key,
+                 surv_tiles);
     BBS_CUDA(cudaGetLastError());
     if (dbg_phases) record(ev_dbg[3 * e]);
-    if (pend_cap <= kRankSortMax) {
-      launch_pdl(rank_sort_kernel, grid1(pend_cap, kRT), kRT, 0, s, d_st, s_key, s_key2);
+    if (rank_sorted) {
+      launch_pdl(rank_sort_kernel, grid1(pend_cap, kRT), kRT, 0, s, d_st, s_key, s_key2, q,
+                 spec_on ? strategy : -1);
       BBS_CUDA(cudaGetLastError());
     } else {
-      launch_pdl(pad_keys_kernel, grid1(pend_cap), 256, 0, s, static_cast<const EpochState*>(d_st), s_key,
-                 static_cast<uint64_t>(pend_cap));
+      launch_pdl(pad_keys_kernel, grid1(pend_cap), 256, 0, s, d_st, s_key, static_cast<uint64_t>(pend_cap), q,
+                 spec_on ? strategy : -1);
       BBS_CUDA(cudaGetLastError());
       size_t tb = sort_temp_bytes;
       BBS_CUDA(cub::DeviceRadixSort::SortKeys(sort_temp, tb, s_key, s_key2, static_cast<int64_t>(pend_cap), 0, 64, s));
@@ -1846,7 +2440,7 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
   cudaGraphExec_t batch_exec = nullptr;
   uint64_t batch_qcap = 0;
   const bbs_node* batch_pool = nullptr;
-  bool batch_builds = true;
+  bool batch_builds = true, batch_spec = false;
   struct ExecGuard {
     cudaGraphExec_t* e;
     ~ExecGuard() {
@@ -1914,7 +2508,8 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
     NvtxRange nv_epochs("bbs::flush epochs");  // search.hpp:145-169, n_ep flushes per host check
     // graphs pay off for long searches (capture + instantiate ~0.2 ms)
     if (n_ep == E && E > 1 && pass_ms.size() >= graph_after && !dbg_phases) {
-      if (!batch_exec || batch_qcap != qcap || batch_pool != q.pool || batch_builds != builds_live) {
+      if (!batch_exec || batch_qcap != qcap || batch_pool != q.pool || batch_builds != builds_live ||
+          batch_spec != spec_on) {
         if (batch_exec) BBS_CUDA(cudaGraphExecDestroy(batch_exec));
         batch_exec = nullptr;
         cudaGraph_t graph;
@@ -1930,6 +2525,7 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
         batch_qcap = qcap;
         batch_pool = q.pool;
         batch_builds = builds_live;
+        batch_spec = spec_on;
       }
       BBS_CUDA(cudaGraphLaunch(batch_exec, s));
       launches += 6ull * E;
@@ -1962,6 +2558,10 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
       dbg_prev = keep;
     }
     hs = *W.h_st;
+    if (dbg_spec)
+      std::fprintf(stderr, "[spec] pass %u q_len %u best %d n_cons %u n_children %u n_surv %u spec_n %u acc %u k %u gen %llu pruned %llu flushed %llu trace %llu matched %d\n",
+                   hs.pass, hs.q_len, hs.best, hs.n_cons, hs.n_children, hs.n_surv, hs.spec_n, hs.spec_acc, hs.spec_k,
+                   hs.nodes_generated, hs.nodes_pruned, hs.batches_flushed, hs.trace_len, hs.matched);
     if (dump && hs.n_children > 0) {
       // this epoch's flushed batch: pending[0, n) and its scores (still in
       // place: the next epoch's branch kernel has not run)
@@ -1986,6 +2586,7 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
     }
     self_active = hs.active != 0;
     builds_live = (claimable & ~hs.cache_raw) != 0;  // raw flags only ever get set
+    spec_on = spec_k > 1;  // from the second host check on
     if (roots_host_x)
       exchange();
     else

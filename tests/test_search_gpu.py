@@ -338,3 +338,18 @@ def test_large_batch_uses_radix_sorted_survivors(B, ref, golden_scenes, strategy
     assert (got.stats.nodes_generated, got.stats.nodes_pruned, got.stats.batches_flushed) == \
         (want.stats.nodes_generated, want.stats.nodes_pruned, want.stats.batches_flushed)
     assert got.best_score_trace == trace
+
+
+@pytest.mark.parametrize("spec", ["1", "2", "5", "16"])
+@pytest.mark.parametrize("name", ["small", "room"])
+def test_speculative_rounds_match_reference(B, golden_scenes, name, spec, monkeypatch):
+    """Speculative flush rounds (BFS; frontier_spec_kernel + survivors_spec_
+    kernel, from the second host check on): any round depth gives the
+    reference's search() exactly -- score, pose, Stats, incumbent trace --
+    on searches with many flushes (small b=7: ~1.9k flushes; room: 73)."""
+    monkeypatch.setenv("BBS_SPEC", spec)
+    m, s, _, sc = load_case(B, golden_scenes, name)
+    vm = B.MultiResVoxelMap.build(m, sc["r"], sc["max_level"])
+    for label, want in golden_json(f"{name}_search.json").items():
+        res = B.search(vm, s, make_cfg(B, sc, name, want["overrides"]))
+        assert_same(res, want, f"{name}/{label}/spec{spec}")
