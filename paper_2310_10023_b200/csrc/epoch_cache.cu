@@ -32,7 +32,7 @@ namespace {
 constexpr int kCacheHashSlots = 8192;
 constexpr int kCacheHashCap = 4096;   // distinct offsets kept in shared memory
 constexpr int kCacheAmbCap = 2048;    // ambiguous points buffered per build
-constexpr int kProbeChunk = 512;      // histogram entries per warp item
+constexpr int kProbeChunk = 128;      // granule of the histogram entries per warp item (32 lanes x 4)
 constexpr unsigned long long kEmptyKey = ~0ull;
 
 __device__ __forceinline__ uint32_t cache_hash(unsigned long long key) {
@@ -368,11 +368,22 @@ __global__ void __launch_bounds__(BBS_PROBE_T, BBS_PROBE_B) cache_probe_kernel(R
   pdl_wait();
 
   const uint32_t n_runs = *d_n / 8;
-  // chunks per run: the largest histogram built so far (not the scan size)
-  chunks_per_run = min(chunks_per_run, max(1u, (c.ctl[kCtlMaxEnt] + kProbeChunk - 1) / kProbeChunk));
-  const uint64_t n_items = static_cast<uint64_t>(n_runs) * chunks_per_run;
   const int lane = threadIdx.x & 31;
   const uint64_t n_warps = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
+  // warp items = (run, chunk of the run's histogram): as few chunks per run
+  // as keep ~2 items per warp (each item ends in 8 warp reductions and
+  // atomics), sized by the largest histogram built so far
+  const uint32_t max_ent = max(1u, c.ctl[kCtlMaxEnt]);
+  const uint32_t granules = (max_ent + kProbeChunk - 1) / kProbeChunk;
+  const uint64_t want = (2 * n_warps + max(n_runs, 1u) - 1) / max(n_runs, 1u);
+  {
+    uint64_t cpr = want < granules ? want : granules;
+    if (cpr > chunks_per_run) cpr = chunks_per_run;
+    chunks_per_run = static_cast<uint32_t>(cpr);
+  }
+  chunks_per_run = max(chunks_per_run, 1u);
+  const uint32_t chunk_len = ((granules + chunks_per_run - 1) / chunks_per_run) * kProbeChunk;
+  const uint64_t n_items = static_cast<uint64_t>(n_runs) * chunks_per_run;
   const uint64_t gw = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   for (uint64_t k0 = 0; gw + k0 * n_warps < n_items; k0 += 32) {
     const uint64_t item = gw + (k0 + lane) * n_warps;
@@ -388,7 +399,7 @@ __global__ void __launch_bounds__(BBS_PROBE_T, BBS_PROBE_B) cache_probe_kernel(R
       if (run_slot(c, G, a, b, &slot)) {
         inf = c.info[slot];
         has = inf.x == kCacheReady &&
-              (chunk * kProbeChunk < static_cast<uint32_t>(inf.z) || (chunk == 0 && inf.w > 0));
+              (chunk * chunk_len < static_cast<uint32_t>(inf.z) || (chunk == 0 && inf.w > 0));
       }
     }
     // runs without a READY histogram go to the cube kernel's list (chunk 0 items)
@@ -419,8 +430,8 @@ __global__ void __launch_bounds__(BBS_PROBE_T, BBS_PROBE_B) cache_probe_kernel(R
       const uint32_t oy = static_cast<uint32_t>(by) - static_cast<uint32_t>(L.box_min[1]);
       const uint32_t oz = static_cast<uint32_t>(bz) - static_cast<uint32_t>(L.box_min[2]);
       int acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-      const uint32_t e0 = ch * kProbeChunk;
-      const uint32_t e1 = min(n_ent, e0 + kProbeChunk);
+      const uint32_t e0 = ch * chunk_len;
+      const uint32_t e1 = min(n_ent, e0 + chunk_len);
       const int4* __restrict__ ent = c.pool + off;
       if (l == c.stg_level) {
         // staged: 4 LDS + 4 clamped funnel shifts give an entry's 2x2x2 child
