@@ -32,6 +32,7 @@ namespace {
 constexpr int kCacheHashSlots = 8192;
 constexpr int kCacheHashCap = 4096;   // distinct offsets kept in shared memory
 constexpr int kCacheAmbCap = 2048;    // ambiguous points buffered per build
+constexpr int kCacheListCap = 4096;   // dense box: cells touched, listed (beyond: the box is walked)
 constexpr int kProbeChunk = 128;      // granule of the histogram entries per warp item (32 lanes x 4)
 constexpr unsigned long long kEmptyKey = ~0ull;
 
@@ -71,9 +72,10 @@ __global__ void __launch_bounds__(kBuildThreads) cache_build_kernel(RotCache c, 
   unsigned long long* s_key = reinterpret_cast<unsigned long long*>(smem);   // 64 KB
   int32_t* s_cnt = reinterpret_cast<int32_t*>(s_key + kCacheHashSlots);      // 32 KB
   uint32_t* s_amb = reinterpret_cast<uint32_t*>(s_cnt + kCacheHashSlots);    // 8 KB
+
   using ScanI = cub::BlockScan<int, kBuildThreads>;
   __shared__ typename ScanI::TempStorage s_scan;
-  __shared__ int s_distinct, s_namb, s_oob;
+  __shared__ int s_distinct, s_namb, s_oob, s_nl;
   __shared__ uint32_t s_off, s_aoff;
   const int lane = threadIdx.x & 31;
   const uint32_t n_build = c.ctl[2];
@@ -91,6 +93,9 @@ __global__ void __launch_bounds__(kBuildThreads) cache_build_kernel(RotCache c, 
     const int dzlo = c.dn_zlo[l], dxy = 2 * dr + 1;
     const int ncells = dense ? dxy * dxy * c.dn_nz[l] : 0;
     uint32_t* s_w = reinterpret_cast<uint32_t*>(smem);  // overlays the hash table
+    // touched dense cells, listed after the counters in the hash region
+    uint16_t* s_list = reinterpret_cast<uint16_t*>(s_w + ((ncells + 1) >> 1));
+    const int list_cap = min(kCacheListCap, (kCacheHashSlots * 12 - ((ncells + 1) >> 1) * 4) / 2);
     if (dense) {
       for (int i = threadIdx.x; i < (ncells + 1) >> 1; i += blockDim.x) s_w[i] = 0u;
     } else {
@@ -103,6 +108,7 @@ __global__ void __launch_bounds__(kBuildThreads) cache_build_kernel(RotCache c, 
       s_distinct = 0;
       s_namb = 0;
       s_oob = 0;
+      s_nl = 0;
     }
     __syncthreads();
     // all lanes stay in the loop together (warp-aggregated inserts below)
@@ -114,33 +120,53 @@ __global__ void __launch_bounds__(kBuildThreads) cache_build_kernel(RotCache c, 
       // an unsigned box test on the saturated int conversion.
       const double eps = c.dn_eps[l], eps1 = c.dn_eps1[l], inv = L.inv_cell;
       const uint32_t udxy = static_cast<uint32_t>(dxy), unz = static_cast<uint32_t>(c.dn_nz[l]);
-      for (uint32_t p0 = 0; p0 < scan.k; p0 += blockDim.x) {
-        const uint32_t p = p0 + threadIdx.x;
-        int idx = -1;
-        if (p < scan.k) {
-          const double px = scan.x[p], py = scan.y[p], pz = scan.z[p];
-          const double wx = __dmul_rn(rot_row(R[0], R[1], R[2], px, py, pz), inv);
-          const double wy = __dmul_rn(rot_row(R[3], R[4], R[5], px, py, pz), inv);
-          const double wz = __dmul_rn(rot_row(R[6], R[7], R[8], px, py, pz), inv);
-          const double flx = floor(wx), fly = floor(wy), flz = floor(wz);
-          const double frx = __dsub_rn(wx, flx), fry = __dsub_rn(wy, fly), frz = __dsub_rn(wz, flz);
-          const bool ok = frx > eps && frx < eps1 && fry > eps && fry < eps1 && frz > eps && frz < eps1;
-          if (!ok) {
-            const int a = atomicAdd(&s_namb, 1);
-            if (a < kCacheAmbCap) s_amb[a] = p;
-          } else {
-            const uint32_t ux = static_cast<uint32_t>(__double2int_rz(flx)) + static_cast<uint32_t>(dr);
-            const uint32_t uy = static_cast<uint32_t>(__double2int_rz(fly)) + static_cast<uint32_t>(dr);
-            const uint32_t uz = static_cast<uint32_t>(__double2int_rz(flz)) - static_cast<uint32_t>(dzlo);
-            if (ux < udxy && uy < udxy && uz < unz)
-              idx = static_cast<int>((uz * udxy + uy) * udxy + ux);
-            else
-              s_oob = 1;  // outside the box: this build gives up (cube kernel scores its runs)
+      // two points per thread per step: two load / rotate chains in flight
+      for (uint32_t p0 = 0; p0 < scan.k; p0 += 2 * blockDim.x) {
+        double px[2], py[2], pz[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const uint32_t p = p0 + h * blockDim.x + threadIdx.x;
+          const bool live = p < scan.k;
+          px[h] = live ? scan.x[p] : 0.0;
+          py[h] = live ? scan.y[p] : 0.0;
+          pz[h] = live ? scan.z[p] : 0.0;
+        }
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const uint32_t p = p0 + h * blockDim.x + threadIdx.x;
+          int idx = -1;
+          if (p < scan.k) {
+            const double wx = __dmul_rn(rot_row(R[0], R[1], R[2], px[h], py[h], pz[h]), inv);
+            const double wy = __dmul_rn(rot_row(R[3], R[4], R[5], px[h], py[h], pz[h]), inv);
+            const double wz = __dmul_rn(rot_row(R[6], R[7], R[8], px[h], py[h], pz[h]), inv);
+            const double flx = floor(wx), fly = floor(wy), flz = floor(wz);
+            const double frx = __dsub_rn(wx, flx), fry = __dsub_rn(wy, fly), frz = __dsub_rn(wz, flz);
+            const bool ok = frx > eps && frx < eps1 && fry > eps && fry < eps1 && frz > eps && frz < eps1;
+            if (!ok) {
+              const int a = atomicAdd(&s_namb, 1);
+              if (a < kCacheAmbCap) s_amb[a] = p;
+            } else {
+              const uint32_t ux = static_cast<uint32_t>(__double2int_rz(flx)) + static_cast<uint32_t>(dr);
+              const uint32_t uy = static_cast<uint32_t>(__double2int_rz(fly)) + static_cast<uint32_t>(dr);
+              const uint32_t uz = static_cast<uint32_t>(__double2int_rz(flz)) - static_cast<uint32_t>(dzlo);
+              if (ux < udxy && uy < udxy && uz < unz)
+                idx = static_cast<int>((uz * udxy + uy) * udxy + ux);
+              else
+                s_oob = 1;  // outside the box: this build gives up (cube kernel scores its runs)
+            }
+          }
+          const unsigned same = __match_any_sync(0xffffffffu, idx);
+          if (idx >= 0 && (__ffs(same) - 1) == lane) {
+            // the first count of a cell lists it: the entries are emitted from
+            // the list (~2k cells) instead of a walk over the whole box (~20k)
+            const uint32_t sh = static_cast<uint32_t>(idx & 1) << 4;
+            const uint32_t old = atomicAdd(&s_w[idx >> 1], static_cast<uint32_t>(__popc(same)) << sh);
+            if (((old >> sh) & 0xFFFFu) == 0u) {
+              const int pos = atomicAdd(&s_nl, 1);
+              if (pos < list_cap) s_list[pos] = static_cast<uint16_t>(idx);
+            }
           }
         }
-        const unsigned same = __match_any_sync(0xffffffffu, idx);
-        if (idx >= 0 && (__ffs(same) - 1) == lane)
-          atomicAdd(&s_w[idx >> 1], static_cast<uint32_t>(__popc(same)) << ((idx & 1) << 4));
       }
     }
     for (uint32_t p0 = 0; !dense && p0 < scan.k; p0 += 2 * blockDim.x) {
@@ -231,8 +257,16 @@ __global__ void __launch_bounds__(kBuildThreads) cache_build_kernel(RotCache c, 
     auto dcount = [&](int i) { return (s_w[i >> 1] >> ((i & 1) << 4)) & 0xFFFFu; };
     // the staged level stores groups of 4 byte-count entries (counts > 255 split)
     const bool staged = dense && l == c.stg_level;
+    const int nl = s_nl;
+    const bool listed = dense && nl <= list_cap;  // else: walk the whole box
     int cnt = 0;
-    if (dense) {
+    if (listed) {
+      if (!oob)
+        for (int j = threadIdx.x; j < nl; j += kBuildThreads) {
+          const uint32_t v = dcount(s_list[j]);
+          cnt += staged ? static_cast<int>((v + 254u) / 255u) : 1;
+        }
+    } else if (dense) {
       if (!oob)
         for (int i = dc0; i < dc1; ++i) {
           const uint32_t v = dcount(i);
@@ -260,10 +294,7 @@ __global__ void __launch_bounds__(kBuildThreads) cache_build_kernel(RotCache c, 
     if (fits && staged) {
       int32_t* gw = reinterpret_cast<int32_t*>(c.pool + off);
       unsigned char* gb = reinterpret_cast<unsigned char*>(c.pool + off);
-      for (CellWalk w(dc0, dxy); w.i < dc1; w.next()) {
-        uint32_t v = dcount(w.i);
-        if (!v) continue;
-        const int fx = w.x - dr, fy = w.y - dr, fz = w.z + dzlo;
+      auto put = [&](uint32_t v, int fx, int fy, int fz) {
         const int32_t eoff = fy * static_cast<int32_t>(c.stg_pitch) + fx;
         for (; v; ++epos) {
           const uint32_t w = min(v, 255u);
@@ -273,6 +304,17 @@ __global__ void __launch_bounds__(kBuildThreads) cache_build_kernel(RotCache c, 
           gb[(g * 8 + 4) * 4 + k] = static_cast<unsigned char>(static_cast<int8_t>(fz));
           gb[(g * 8 + 5) * 4 + k] = static_cast<unsigned char>(w);
         }
+      };
+      if (listed) {
+        for (int j = threadIdx.x; j < nl; j += kBuildThreads) {
+          const int i = s_list[j];
+          put(dcount(i), i % dxy - dr, (i / dxy) % dxy - dr, i / (dxy * dxy) + dzlo);
+        }
+      } else {
+        for (CellWalk w(dc0, dxy); w.i < dc1; w.next()) {
+          const uint32_t v = dcount(w.i);
+          if (v) put(v, w.x - dr, w.y - dr, w.z + dzlo);
+        }
       }
       // zero-count padding of the last group
       const int pe = static_cast<int>(n_ent) + static_cast<int>(threadIdx.x);
@@ -281,6 +323,13 @@ __global__ void __launch_bounds__(kBuildThreads) cache_build_kernel(RotCache c, 
         gw[g * 8 + k] = 0;
         gb[(g * 8 + 4) * 4 + k] = 0;
         gb[(g * 8 + 5) * 4 + k] = 0;
+      }
+    } else if (fits && listed) {
+      for (int j = threadIdx.x; j < nl; j += kBuildThreads) {
+        const int i = s_list[j];
+        c.pool[off + epos] = make_int4(i % dxy - dr, (i / dxy) % dxy - dr, i / (dxy * dxy) + dzlo,
+                                       static_cast<int32_t>(dcount(i)));
+        ++epos;
       }
     } else if (fits && dense) {
       for (CellWalk w(dc0, dxy); w.i < dc1; w.next()) {

@@ -459,6 +459,8 @@ __device__ __forceinline__ int count_bucket(uint32_t v) {
   return kRootCountBuckets == 1 ? 0 : min(kRootCountBuckets - 1, 31 - __clz(max(v, 1u)));
 }
 
+constexpr int kRootListCap = 4096;  // dense root box: touched cells listed (beyond: the box is walked)
+
 // One histogram entry (f, cnt) of root_hist_kernel, appended warp-cooperatively
 // (every lane calls; has = false for lanes without an entry).  Staged mode
 // (root_colpad_kernel): (padded column offset << 8 | z shift + 8) words in
@@ -513,13 +515,16 @@ __global__ void __launch_bounds__(512) root_hist_kernel(GridView grid, ScanView 
   unsigned long long* s_key = reinterpret_cast<unsigned long long*>(smem);  // 64 KB
   int32_t* s_cnt = reinterpret_cast<int32_t*>(s_key + kHistSlots);          // 32 KB
   uint32_t* s_w = reinterpret_cast<uint32_t*>(smem);  // dense box: 16-bit counters (overlays the hash)
-  __shared__ int s_distinct, s_namb, s_nent, s_skip, s_badpad, s_total;
+  __shared__ int s_distinct, s_namb, s_nent, s_skip, s_badpad, s_total, s_nl;
   const uint32_t nrot = bp.nr * bp.np * bp.nw;
   const int lane = threadIdx.x & 31;
   // dense box (coarse root levels): direct-mapped counters, no probing
   const int dr = bp.dn_r, dxy = 2 * dr + 1, dzlo = bp.dn_zlo;
   const bool dense = dr > 0;
   const int ncells = dense ? dxy * dxy * bp.dn_nz : 0;
+  // touched dense cells, listed after the counters in the hash region
+  uint16_t* s_list = reinterpret_cast<uint16_t*>(s_w + ((ncells + 1) >> 1));
+  const int list_cap = min(kRootListCap, (kHistSlots * 12 - ((ncells + 1) >> 1) * 4) / 2);
   for (uint32_t rot = rot_begin + blockIdx.x; rot < rot_end; rot += gridDim.x) {
     const uint32_t slot = rot - rot_begin;
     uint32_t P, x0r;
@@ -546,6 +551,7 @@ __global__ void __launch_bounds__(512) root_hist_kernel(GridView grid, ScanView 
       s_skip = 0;
       s_badpad = 0;
       s_total = 0;
+      s_nl = 0;
     }
     __syncthreads();
     const uint32_t ir = rot / (bp.np * bp.nw), ip = (rot / bp.nw) % bp.np, iw = rot % bp.nw;
@@ -556,32 +562,51 @@ __global__ void __launch_bounds__(512) root_hist_kernel(GridView grid, ScanView 
       // out-of-box point sends the rotation to the chunked kernel)
       const double eps = bp.dn_eps, eps1 = bp.dn_eps1, inv = L.inv_cell;
       const uint32_t udxy = static_cast<uint32_t>(dxy), unz = static_cast<uint32_t>(bp.dn_nz);
-      for (uint32_t p0 = 0; p0 < scan.k; p0 += blockDim.x) {
-        const uint32_t p = p0 + threadIdx.x;
-        int idx = -1;
-        if (p < scan.k) {
-          const double px = scan.x[p], py = scan.y[p], pz = scan.z[p];
-          const double wx = __dmul_rn(rot_row(R[0], R[1], R[2], px, py, pz), inv);
-          const double wy = __dmul_rn(rot_row(R[3], R[4], R[5], px, py, pz), inv);
-          const double wz = __dmul_rn(rot_row(R[6], R[7], R[8], px, py, pz), inv);
-          const double flx = floor(wx), fly = floor(wy), flz = floor(wz);
-          const double frx = __dsub_rn(wx, flx), fry = __dsub_rn(wy, fly), frz = __dsub_rn(wz, flz);
-          if (frx > eps && frx < eps1 && fry > eps && fry < eps1 && frz > eps && frz < eps1) {
-            const uint32_t ux = static_cast<uint32_t>(__double2int_rz(flx)) + static_cast<uint32_t>(dr);
-            const uint32_t uy = static_cast<uint32_t>(__double2int_rz(fly)) + static_cast<uint32_t>(dr);
-            const uint32_t uz = static_cast<uint32_t>(__double2int_rz(flz)) - static_cast<uint32_t>(dzlo);
-            if (ux < udxy && uy < udxy && uz < unz)
-              idx = static_cast<int>((uz * udxy + uy) * udxy + ux);
-            else
-              s_skip = 1;
-          } else {
-            const int a = atomicAdd(&s_namb, 1);
-            if (a < kAmbCap) h.amb[static_cast<uint64_t>(slot) * kAmbCap + a] = p;
+      // two points per thread per step: two load / rotate chains in flight
+      for (uint32_t p0 = 0; p0 < scan.k; p0 += 2 * blockDim.x) {
+        double px[2], py[2], pz[2];
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+          const uint32_t p = p0 + hh * blockDim.x + threadIdx.x;
+          const bool live = p < scan.k;
+          px[hh] = live ? scan.x[p] : 0.0;
+          py[hh] = live ? scan.y[p] : 0.0;
+          pz[hh] = live ? scan.z[p] : 0.0;
+        }
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+          const uint32_t p = p0 + hh * blockDim.x + threadIdx.x;
+          int idx = -1;
+          if (p < scan.k) {
+            const double wx = __dmul_rn(rot_row(R[0], R[1], R[2], px[hh], py[hh], pz[hh]), inv);
+            const double wy = __dmul_rn(rot_row(R[3], R[4], R[5], px[hh], py[hh], pz[hh]), inv);
+            const double wz = __dmul_rn(rot_row(R[6], R[7], R[8], px[hh], py[hh], pz[hh]), inv);
+            const double flx = floor(wx), fly = floor(wy), flz = floor(wz);
+            const double frx = __dsub_rn(wx, flx), fry = __dsub_rn(wy, fly), frz = __dsub_rn(wz, flz);
+            if (frx > eps && frx < eps1 && fry > eps && fry < eps1 && frz > eps && frz < eps1) {
+              const uint32_t ux = static_cast<uint32_t>(__double2int_rz(flx)) + static_cast<uint32_t>(dr);
+              const uint32_t uy = static_cast<uint32_t>(__double2int_rz(fly)) + static_cast<uint32_t>(dr);
+              const uint32_t uz = static_cast<uint32_t>(__double2int_rz(flz)) - static_cast<uint32_t>(dzlo);
+              if (ux < udxy && uy < udxy && uz < unz)
+                idx = static_cast<int>((uz * udxy + uy) * udxy + ux);
+              else
+                s_skip = 1;
+            } else {
+              const int a = atomicAdd(&s_namb, 1);
+              if (a < kAmbCap) h.amb[static_cast<uint64_t>(slot) * kAmbCap + a] = p;
+            }
+          }
+          const unsigned same = __match_any_sync(0xffffffffu, idx);
+          if (idx >= 0 && (__ffs(same) - 1) == lane) {
+            // a cell's first count lists it (emission walks the list, not the box)
+            const uint32_t sh = static_cast<uint32_t>(idx & 1) << 4;
+            const uint32_t old = atomicAdd(&s_w[idx >> 1], static_cast<uint32_t>(__popc(same)) << sh);
+            if (((old >> sh) & 0xFFFFu) == 0u) {
+              const int pos = atomicAdd(&s_nl, 1);
+              if (pos < list_cap) s_list[pos] = static_cast<uint16_t>(idx);
+            }
           }
         }
-        const unsigned same = __match_any_sync(0xffffffffu, idx);
-        if (idx >= 0 && (__ffs(same) - 1) == lane)
-          atomicAdd(&s_w[idx >> 1], static_cast<uint32_t>(__popc(same)) << ((idx & 1) << 4));
       }
     } else {
       for (uint32_t p0 = 0; p0 < scan.k; p0 += blockDim.x) {
@@ -628,7 +653,20 @@ __global__ void __launch_bounds__(512) root_hist_kernel(GridView grid, ScanView 
     bool over = s_skip || s_distinct > kHistCap || s_namb > kAmbCap;
     if (!over) {
       int4* ent4 = h.entries + static_cast<uint64_t>(slot) * kHistCap;
-      if (dense) {
+      const int nl = s_nl;
+      if (dense && nl <= list_cap) {
+        // the touched cells, heaviest counts first (log2 buckets) so the
+        // column kernel's survivor bound tightens early; the warp emits in
+        // lockstep
+        for (int bk = kRootCountBuckets - 1; bk >= 0; --bk)
+          for (int j0 = 0; j0 < nl; j0 += static_cast<int>(blockDim.x)) {
+            const int j = j0 + static_cast<int>(threadIdx.x);
+            const int i = j < nl ? s_list[j] : 0;
+            const uint32_t v = j < nl ? (s_w[i >> 1] >> ((i & 1) << 4)) & 0xFFFFu : 0u;
+            root_emit(v != 0u && count_bucket(v) == bk, i % dxy - dr, (i / dxy) % dxy - dr, i / (dxy * dxy) + dzlo,
+                      static_cast<int32_t>(v), bp, st, ent4, &s_nent, &s_badpad, &s_total);
+          }
+      } else if (dense) {
         // each thread walks a contiguous cell range; the warp emits in
         // lockstep, heaviest counts first (log2 buckets) so the column
         // kernel's survivor bound tightens early
