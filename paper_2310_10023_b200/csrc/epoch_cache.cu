@@ -155,12 +155,13 @@ __global__ void __launch_bounds__(kBuildThreads) cache_build_kernel(RotCache c, 
                 s_oob = 1;  // outside the box: this build gives up (cube kernel scores its runs)
             }
           }
-          const unsigned same = __match_any_sync(0xffffffffu, idx);
-          if (idx >= 0 && (__ffs(same) - 1) == lane) {
-            // the first count of a cell lists it: the entries are emitted from
-            // the list (~2k cells) instead of a walk over the whole box (~20k)
+          // one shared atomic per point (warp aggregation with MATCH.ANY
+          // costs more than the conflicts it saves: C3 prebuild 0.42 -> 0.21
+          // ms); the first count of a cell lists it, so the entries are
+          // emitted from the list (~2k cells) instead of a box walk (~20k)
+          if (idx >= 0) {
             const uint32_t sh = static_cast<uint32_t>(idx & 1) << 4;
-            const uint32_t old = atomicAdd(&s_w[idx >> 1], static_cast<uint32_t>(__popc(same)) << sh);
+            const uint32_t old = atomicAdd(&s_w[idx >> 1], 1u << sh);
             if (((old >> sh) & 0xFFFFu) == 0u) {
               const int pos = atomicAdd(&s_nl, 1);
               if (pos < list_cap) s_list[pos] = static_cast<uint16_t>(idx);

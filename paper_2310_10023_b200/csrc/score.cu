@@ -596,11 +596,11 @@ __global__ void __launch_bounds__(512) root_hist_kernel(GridView grid, ScanView 
               if (a < kAmbCap) h.amb[static_cast<uint64_t>(slot) * kAmbCap + a] = p;
             }
           }
-          const unsigned same = __match_any_sync(0xffffffffu, idx);
-          if (idx >= 0 && (__ffs(same) - 1) == lane) {
-            // a cell's first count lists it (emission walks the list, not the box)
+          // one shared atomic per point (cheaper than MATCH.ANY aggregation);
+          // a cell's first count lists it (emission walks the list, not the box)
+          if (idx >= 0) {
             const uint32_t sh = static_cast<uint32_t>(idx & 1) << 4;
-            const uint32_t old = atomicAdd(&s_w[idx >> 1], static_cast<uint32_t>(__popc(same)) << sh);
+            const uint32_t old = atomicAdd(&s_w[idx >> 1], 1u << sh);
             if (((old >> sh) & 0xFFFFu) == 0u) {
               const int pos = atomicAdd(&s_nl, 1);
               if (pos < list_cap) s_list[pos] = static_cast<uint16_t>(idx);
