@@ -1105,6 +1105,10 @@ __global__ void __launch_bounds__(kST) survivors_spec_kernel(EpochState* st, Que
           st->nodes_generated += child_acc;
           st->batches_flushed += A;
           st->epochs += A;
+          // depth of the next round: double after a fully kept round, else
+          // one more than this round kept (a discarded epoch costs its
+          // scoring; a kept one saves a whole kernel chain)
+          st->spec_k = A == ne ? min(2u * st->spec_k, st->spec_kmax) : min(A + 1u, st->spec_kmax);
         }
       }
     }
@@ -2232,7 +2236,7 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
   h0.active = n_root_surv > 0 ? 1 : 0;
   h0.any_active = h0.active;
   h0.q_peak = h0.q_len;
-  h0.spec_k = static_cast<uint32_t>(spec_k);
+  h0.spec_k = std::min(2, spec_k);  // the first round's depth; adapted per round
   h0.spec_kmax = static_cast<uint32_t>(spec_k);
   EpochState* d_st = W.st.get(1, s);
   if (!dev_init) {
