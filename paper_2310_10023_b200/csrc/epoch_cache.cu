@@ -366,8 +366,17 @@ __global__ void __launch_bounds__(kBuildThreads) cache_build_kernel(RotCache c, 
       // ~4x the distinct offsets per halving of the cell, so when that would
       // not halve the points (or not fit a build) the finer levels are
       // scored directly instead of each paying a failed build first
-      if (fits && l == c.pre_level && 4u * n_ent > min(scan.k / 2u, static_cast<uint32_t>(kCacheHashCap)))
-        for (int l2 = 0; l2 < l; ++l2) c.ctl[4 + l2] = 1u;
+      // (a dense-box level holds up to kCacheDenseCells offsets, a hashed
+      // one kCacheHashCap)
+      if (fits && l == c.pre_level) {
+        uint64_t pred = n_ent;
+        for (int l2 = l - 1; l2 >= 0; --l2) {
+          pred *= 4u;
+          const uint64_t cap2 = c.dn_r[l2] > 0 ? static_cast<uint64_t>(kCacheDenseCells)
+                                               : static_cast<uint64_t>(kCacheHashCap);
+          if (pred > min(static_cast<uint64_t>(scan.k / 2u), cap2)) c.ctl[4 + l2] = 1u;
+        }
+      }
     }
     __syncthreads();
   }
