@@ -301,3 +301,63 @@ def test_nccl_world1_equals_unsharded(B, mode):
             assert d.best_score_trace == single.best_score_trace, smode
     finally:
         comm.close()
+
+
+def _nccl_worker(rank, world, port, mode, out_q):
+    import sys
+    sys.path.insert(0, ROOT)
+    import torch
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(rank)
+    dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", rank))
+    import paper_2310_10023_b200 as B
+    m, s, _ = _scene()
+    vm = B.MultiResVoxelMap.build(m, 0.5, 3, device=rank)
+    ds = B.DeviceScan(vm, s)
+    cfg = B.SearchConfig(min_resolution=0.5, max_level=3, branch_mode=1, batch_size=400,
+                         roll_pitch_half_range=0.02, collect_trace=True)
+    uid = [B.Comm.unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(uid, src=0)
+    comm = B.Comm(rank, rank, world, uid[0])
+    try:
+        d = B.search_sharded(vm, ds, cfg, rank, world, comm=comm, mode=mode)
+        single = B.search_scan(vm, ds, cfg)
+        out_q.put((rank, d.best_score, d.best_pose.as_tuple(),
+                   (d.stats.nodes_generated, d.stats.nodes_pruned, d.stats.batches_flushed),
+                   d.best_score_trace, single.best_score, single.best_pose.as_tuple(),
+                   (single.stats.nodes_generated, single.stats.nodes_pruned, single.stats.batches_flushed),
+                   single.best_score_trace))
+    finally:
+        comm.close()
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("mode", ["exact", "roots"])
+def test_nccl_world2_processes(mode):
+    """Two processes, one GPU each, NCCL communicator (the bench's --gpus 2
+    path): EXACT equals the unsharded search on every rank (Stats and trace
+    included); ROOTS gives every rank the same winner.  Needs >= 2 GPUs
+    (ranks that wait on one another must not share a GPU)."""
+    import torch
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    ps = [ctx.Process(target=_nccl_worker, args=(r, 2, port, mode, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    res = sorted(q.get(timeout=600) for _ in ps)
+    for p in ps:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    winners = {(r[1], r[2]) for r in res}
+    assert len(winners) == 1
+    if mode == "exact":
+        for r in res:
+            assert (r[1], r[2], r[3], r[4]) == (r[5], r[6], r[7], r[8])
