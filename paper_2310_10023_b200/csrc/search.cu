@@ -1645,6 +1645,7 @@ struct Workspace {
   Buf<EpochState> st;
   EpochState* h_st = nullptr;
   cudaStream_t side = nullptr;            // prebuild stream (forked per search)
+  cudaGraphExec_t graph_exec = nullptr;   // epoch-batch graph, updated in place per search
   unsigned long long* h_small = nullptr;  // pinned: probes, n_root_surv
   std::vector<cudaEvent_t> ev;
   size_t ev_used = 0;
@@ -1682,6 +1683,7 @@ struct Workspace {
     if (h_small) cudaFreeHost(h_small);
     for (auto e : ev) cudaEventDestroy(e);
     if (side) cudaStreamDestroy(side);
+    if (graph_exec) cudaGraphExecDestroy(graph_exec);
   }
 };
 
@@ -2351,7 +2353,7 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
       reinterpret_cast<char*>(d_st) + (exact ? offsetof(EpochState, n_own) : offsetof(EpochState, n_children)));
   const size_t graph_after = [] {
     const char* v = std::getenv("BBS_GRAPH_AFTER");  // epochs before batches run as graphs
-    return v ? static_cast<size_t>(std::atoi(v)) : static_cast<size_t>(24);
+    return v ? static_cast<size_t>(std::atoi(v)) : static_cast<size_t>(0);
   }();
   bool capturing = false;
   auto record = [&](cudaEvent_t ev) {
@@ -2440,17 +2442,14 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
     }
   };
   // E epochs as one CUDA graph (all sizes live in EpochState, so the graph is
-  // valid until the queue buffers are re-allocated)
-  cudaGraphExec_t batch_exec = nullptr;
+  // valid until the queue buffers are re-allocated).  The executable graph
+  // lives in the workspace and is UPDATED in place (cudaGraphExecUpdate) for
+  // every new capture -- across searches too -- so a search pays a capture
+  // (host-side recording, overlapped with its root batch) but no instantiate.
+  bool batch_ok = false;  // W.graph_exec holds this search's current capture
   uint64_t batch_qcap = 0;
   const bbs_node* batch_pool = nullptr;
   bool batch_builds = true, batch_spec = false;
-  struct ExecGuard {
-    cudaGraphExec_t* e;
-    ~ExecGuard() {
-      if (*e) cudaGraphExecDestroy(*e);
-    }
-  } exec_guard{&batch_exec};
   EpochState hs = h0;
   bool self_active = h0.active != 0;
   if (dev_init) {  // upper bounds until the first device state comes back
@@ -2512,10 +2511,8 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
     NvtxRange nv_epochs("bbs::flush epochs");  // search.hpp:145-169, n_ep flushes per host check
     // graphs pay off for long searches (capture + instantiate ~0.2 ms)
     if (n_ep == E && E > 1 && pass_ms.size() >= graph_after && !dbg_phases) {
-      if (!batch_exec || batch_qcap != qcap || batch_pool != q.pool || batch_builds != builds_live ||
+      if (!batch_ok || batch_qcap != qcap || batch_pool != q.pool || batch_builds != builds_live ||
           batch_spec != spec_on) {
-        if (batch_exec) BBS_CUDA(cudaGraphExecDestroy(batch_exec));
-        batch_exec = nullptr;
         cudaGraph_t graph;
         BBS_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeRelaxed));
         capturing = true;
@@ -2524,14 +2521,28 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
         launches = l0;
         capturing = false;
         BBS_CUDA(cudaStreamEndCapture(s, &graph));
-        BBS_CUDA(cudaGraphInstantiate(&batch_exec, graph, 0));
-        BBS_CUDA(cudaGraphDestroy(graph));
+        struct GraphGuard {
+          cudaGraph_t g;
+          ~GraphGuard() { cudaGraphDestroy(g); }
+        } gg{graph};
+        bool updated = false;
+        if (W.graph_exec) {
+          cudaGraphExecUpdateResultInfo info{};
+          updated = cudaGraphExecUpdate(W.graph_exec, graph, &info) == cudaSuccess;
+          if (!updated) {
+            (void)cudaGetLastError();  // a topology change: re-instantiate
+            cudaGraphExecDestroy(W.graph_exec);
+            W.graph_exec = nullptr;
+          }
+        }
+        if (!updated) BBS_CUDA(cudaGraphInstantiate(&W.graph_exec, graph, 0));
+        batch_ok = true;
         batch_qcap = qcap;
         batch_pool = q.pool;
         batch_builds = builds_live;
         batch_spec = spec_on;
       }
-      BBS_CUDA(cudaGraphLaunch(batch_exec, s));
+      BBS_CUDA(cudaGraphLaunch(W.graph_exec, s));
       launches += 6ull * E;
     } else {
       for (int e = 0; e < n_ep; ++e) enqueue_epoch(e);
