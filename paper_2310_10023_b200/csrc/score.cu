@@ -377,39 +377,77 @@ __global__ void __launch_bounds__(256, 4) score_cube8_kernel(MapView map, GridVi
 #pragma unroll
     for (int t = 0; t < 8; ++t) cnt[t] = 0;
     const uint32_t p0 = pt * tile, p1 = min(k, p0 + tile);
-    for (uint32_t p = p0 + threadIdx.x; p < p1; p += blockDim.x) {
-      const double px = scan.x[p], py = scan.y[p], pz = scan.z[p];
-      const double rx = rot_row(R[0], R[1], R[2], px, py, pz);
-      const double ry = rot_row(R[3], R[4], R[5], px, py, pz);
-      const double rz = rot_row(R[6], R[7], R[8], px, py, pz);
-      int32_t fx, fy, fz;
-      const bool ok = fast_floor(rx, L.inv_cell, tmax, &fx) & fast_floor(ry, L.inv_cell, tmax, &fy) &
-                      fast_floor(rz, L.inv_cell, tmax, &fz);
-      if (ok && bitmap) {
-        const uint32_t ux = static_cast<uint32_t>(fx) + ox;
-        const uint32_t uy = static_cast<uint32_t>(fy) + oy;
-        const uint32_t z0 = static_cast<uint32_t>(fz) + oz, z1 = z0 + 1;
-        const bool in0 = z0 < dimz, in1 = z1 < dimz;
-        const bool same = (z0 >> 5) == (z1 >> 5);
+    // two points per thread per step: both points' coordinates, then both
+    // rotations, then all their column-word loads in flight together
+    for (uint32_t pb = p0 + threadIdx.x; pb < p1; pb += 2 * blockDim.x) {
+      double px[2], py[2], pz[2];
+      bool live[2];
 #pragma unroll
-        for (int d = 0; d < 4; ++d) {
-          const uint32_t x = ux + (d >> 1), y = uy + (d & 1);
-          if (x < dimx && y < dimy) {
+      for (int h = 0; h < 2; ++h) {
+        const uint32_t p = pb + h * blockDim.x;
+        live[h] = p < p1;
+        px[h] = live[h] ? scan.x[p] : 0.0;
+        py[h] = live[h] ? scan.y[p] : 0.0;
+        pz[h] = live[h] ? scan.z[p] : 0.0;
+      }
+      double rx[2], ry[2], rz[2];
+      int32_t fx[2], fy[2], fz[2];
+      bool fast[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        rx[h] = rot_row(R[0], R[1], R[2], px[h], py[h], pz[h]);
+        ry[h] = rot_row(R[3], R[4], R[5], px[h], py[h], pz[h]);
+        rz[h] = rot_row(R[6], R[7], R[8], px[h], py[h], pz[h]);
+        fast[h] = fast_floor(rx[h], L.inv_cell, tmax, &fx[h]) & fast_floor(ry[h], L.inv_cell, tmax, &fy[h]) &
+                  fast_floor(rz[h], L.inv_cell, tmax, &fz[h]);
+      }
+      if (bitmap) {
+        uint32_t w[2][8];
+        uint32_t zz[2][2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const bool use = live[h] && fast[h];
+          const uint32_t ux = static_cast<uint32_t>(fx[h]) + ox;
+          const uint32_t uy = static_cast<uint32_t>(fy[h]) + oy;
+          const uint32_t z0 = static_cast<uint32_t>(fz[h]) + oz, z1 = z0 + 1;
+          zz[h][0] = z0;
+          zz[h][1] = z1;
+          const bool in0 = use && z0 < dimz, in1 = use && z1 < dimz;
+          const bool same = (z0 >> 5) == (z1 >> 5);
+#pragma unroll
+          for (int d = 0; d < 4; ++d) {
+            const uint32_t x = ux + (d >> 1), y = uy + (d & 1);
+            const bool inxy = x < dimx && y < dimy;
             const uint64_t col = static_cast<uint64_t>(y) * dimx + x;
-            const uint32_t w0 = in0 ? __ldg(&L.words[(z0 >> 5) * plane + col]) : 0u;
-            const uint32_t w1 = in1 ? (same ? w0 : __ldg(&L.words[(z1 >> 5) * plane + col])) : 0u;
-            cnt[2 * d] += (w0 >> (z0 & 31)) & 1u;
-            cnt[2 * d + 1] += (w1 >> (z1 & 31)) & 1u;
+            w[h][2 * d] = (in0 && inxy) ? __ldg(&L.words[(z0 >> 5) * plane + col]) : 0u;
+            w[h][2 * d + 1] = (in1 && inxy && !same) ? __ldg(&L.words[(z1 >> 5) * plane + col]) : 0u;
           }
+          // same z word: reuse the first load
+#pragma unroll
+          for (int d = 0; d < 4; ++d)
+            if (same) w[h][2 * d + 1] = in1 ? w[h][2 * d] : 0u;
         }
-      } else if (ok) {
 #pragma unroll
-        for (int t = 0; t < 8; ++t)
-          cnt[t] += level_contains(L, fx + bx + (t >> 2), fy + by + ((t >> 1) & 1), fz + bz + (t & 1)) ? 1 : 0;
-      } else {
+        for (int h = 0; h < 2; ++h)
 #pragma unroll
-        for (int t = 0; t < 8; ++t)
-          cnt[t] += exact_hit(L, rx, ry, rz, bx + (t >> 2), by + ((t >> 1) & 1), bz + (t & 1));
+          for (int d = 0; d < 4; ++d) {
+            cnt[2 * d] += (w[h][2 * d] >> (zz[h][0] & 31)) & 1u;
+            cnt[2 * d + 1] += (w[h][2 * d + 1] >> (zz[h][1] & 31)) & 1u;
+          }
+      }
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        if (!live[h] || (bitmap && fast[h])) continue;
+        if (fast[h]) {
+#pragma unroll
+          for (int t = 0; t < 8; ++t)
+            cnt[t] += level_contains(L, fx[h] + bx + (t >> 2), fy[h] + by + ((t >> 1) & 1), fz[h] + bz + (t & 1)) ? 1
+                                                                                                                : 0;
+        } else {
+#pragma unroll
+          for (int t = 0; t < 8; ++t)
+            cnt[t] += exact_hit(L, rx[h], ry[h], rz[h], bx + (t >> 2), by + ((t >> 1) & 1), bz + (t & 1));
+        }
       }
     }
 #pragma unroll
