@@ -402,6 +402,9 @@ def pose_parity(res, want, grids, r, exact):
 def run_b200_arm(args, cfgd):
     import torch
     world, rank, local = dist_env()
+    if torch.cuda.device_count() <= local:
+        raise SystemExit(f"bench.py: rank {rank} needs GPU {local}, only {torch.cuda.device_count()} visible "
+                         f"(--gpus N needs N GPUs on this node)")
     torch.cuda.set_device(local)
     # BBS_BENCH_SHARDED=1 takes the sharded path at world 1 too (torchrun
     # --nproc-per-node 1): a one-GPU check of the NCCL glue
