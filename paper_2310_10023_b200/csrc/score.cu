@@ -317,6 +317,7 @@ __global__ void __launch_bounds__(kBoxThreads, 2) score_box_kernel(MapView map, 
 // probes form a 2x2x2 voxel cube = 4 (x, y) columns x 2 z-bits of the
 // z-column bitmap: 4 word loads answer all 8 children.  One work item =
 // (run, tile of scan points); counts reduce warp -> CTA -> scores.
+template <bool kILP>
 __global__ void __launch_bounds__(256, 4) score_cube8_kernel(MapView map, GridView grid, ScanView scan,
                                                              const bbs_node* __restrict__ nodes,
                                                              const uint32_t* __restrict__ d_n,
@@ -377,9 +378,47 @@ __global__ void __launch_bounds__(256, 4) score_cube8_kernel(MapView map, GridVi
 #pragma unroll
     for (int t = 0; t < 8; ++t) cnt[t] = 0;
     const uint32_t p0 = pt * tile, p1 = min(k, p0 + tile);
-    // two points per thread per step: both points' coordinates, then both
-    // rotations, then all their column-word loads in flight together
-    for (uint32_t pb = p0 + threadIdx.x; pb < p1; pb += 2 * blockDim.x) {
+    // long tiles: two points per thread per step (both points' coordinates,
+    // then both rotations, then all their column-word loads in flight);
+    // short tiles (small scans, many point tiles): one point per step
+    if (!kILP || p1 - p0 < 2 * blockDim.x) {
+      for (uint32_t p = p0 + threadIdx.x; p < p1; p += blockDim.x) {
+        const double px = scan.x[p], py = scan.y[p], pz = scan.z[p];
+        const double rx = rot_row(R[0], R[1], R[2], px, py, pz);
+        const double ry = rot_row(R[3], R[4], R[5], px, py, pz);
+        const double rz = rot_row(R[6], R[7], R[8], px, py, pz);
+        int32_t fx, fy, fz;
+        const bool ok = fast_floor(rx, L.inv_cell, tmax, &fx) & fast_floor(ry, L.inv_cell, tmax, &fy) &
+                        fast_floor(rz, L.inv_cell, tmax, &fz);
+        if (ok && bitmap) {
+          const uint32_t ux = static_cast<uint32_t>(fx) + ox;
+          const uint32_t uy = static_cast<uint32_t>(fy) + oy;
+          const uint32_t z0 = static_cast<uint32_t>(fz) + oz, z1 = z0 + 1;
+          const bool in0 = z0 < dimz, in1 = z1 < dimz;
+          const bool same = (z0 >> 5) == (z1 >> 5);
+#pragma unroll
+          for (int d = 0; d < 4; ++d) {
+            const uint32_t x = ux + (d >> 1), y = uy + (d & 1);
+            if (x < dimx && y < dimy) {
+              const uint64_t col = static_cast<uint64_t>(y) * dimx + x;
+              const uint32_t w0 = in0 ? __ldg(&L.words[(z0 >> 5) * plane + col]) : 0u;
+              const uint32_t w1 = in1 ? (same ? w0 : __ldg(&L.words[(z1 >> 5) * plane + col])) : 0u;
+              cnt[2 * d] += (w0 >> (z0 & 31)) & 1u;
+              cnt[2 * d + 1] += (w1 >> (z1 & 31)) & 1u;
+            }
+          }
+        } else if (ok) {
+#pragma unroll
+          for (int t = 0; t < 8; ++t)
+            cnt[t] += level_contains(L, fx + bx + (t >> 2), fy + by + ((t >> 1) & 1), fz + bz + (t & 1)) ? 1 : 0;
+        } else {
+#pragma unroll
+          for (int t = 0; t < 8; ++t)
+            cnt[t] += exact_hit(L, rx, ry, rz, bx + (t >> 2), by + ((t >> 1) & 1), bz + (t & 1));
+        }
+      }
+    } else
+    for (uint32_t pb = p0 + threadIdx.x; kILP && pb < p1; pb += 2 * blockDim.x) {
       double px[2], py[2], pz[2];
       bool live[2];
 #pragma unroll
@@ -1195,8 +1234,12 @@ void launch_score_cube8(const MapView& map, const GridView& grid, const ScanView
   // one resident wave (4 CTAs per SM), grid-strided
   const unsigned g = cache ? 148u * 4u
                            : static_cast<unsigned>(std::min<uint64_t>(std::max<uint64_t>(items, 1), 148ull * 4 * 8));
-  launch_pdl(score_cube8_kernel, g, 256, 0, s, map, grid, scan, nodes, d_n, n_ptiles, scores,
-             cache ? *cache : RotCache{}, cache ? 1 : 0);
+  // the flush cache's direct runs (large scans) keep two points in flight;
+  // without the cache (small scans, short point tiles) one point per step
+  if (cache)
+    launch_pdl(score_cube8_kernel<true>, g, 256, 0, s, map, grid, scan, nodes, d_n, n_ptiles, scores, *cache, 1);
+  else
+    launch_pdl(score_cube8_kernel<false>, g, 256, 0, s, map, grid, scan, nodes, d_n, n_ptiles, scores, RotCache{}, 0);
   BBS_CUDA(cudaGetLastError());
 }
 
