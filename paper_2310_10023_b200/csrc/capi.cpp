@@ -26,6 +26,8 @@ namespace bbs {
 void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const bbs_shard* shard,
                 bbs_search_result* out, cudaStream_t stream = nullptr, bbs_search_dump* dump = nullptr);
 void set_pool_retention(int device);
+extern thread_local unsigned g_grid_share;  // kernels.h
+extern thread_local bool g_blocking_sync;
 }  // namespace bbs
 
 namespace {
@@ -390,6 +392,13 @@ int bbs_search_scans(bbs_map_t map, const bbs_scan_t* scans, uint64_t n, const b
     if (n == 0) return;
     const int T = static_cast<int>(std::min<uint64_t>(n, static_cast<uint64_t>(std::max(1, std::min(concurrency, 128)))));
     bbs::DeviceGuard g(map->device);
+    // each search's persistent epoch grids take ~1/share of the GPU (C4, 32
+    // scans, 16 in flight: 1081 scans/s at share 1, 1134-1146 at 2-4, 732
+    // at 16); waits spin (blocking-sync events: -6% at 16 in flight)
+    unsigned share = static_cast<unsigned>(std::max(1, std::min(4, T / 4)));
+    if (const char* e = std::getenv("BBS_GRID_SHARE")) share = static_cast<unsigned>(std::max(1, std::atoi(e)));
+    bool blocking = false;
+    if (const char* e = std::getenv("BBS_BLOCKING_SYNC")) blocking = e[0] == '1';
     std::vector<cudaStream_t> streams(static_cast<size_t>(T));
     for (auto& st : streams) BBS_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
     std::atomic<uint64_t> next{0};
@@ -400,6 +409,8 @@ int bbs_search_scans(bbs_map_t map, const bbs_scan_t* scans, uint64_t n, const b
       workers.emplace_back([&, t] {
         try {
           bbs::DeviceGuard wg(map->device);
+          bbs::g_grid_share = share;
+          bbs::g_blocking_sync = blocking;
           for (uint64_t j = next++; j < n; j = next++)
             bbs::run_search(map, scans[j], *cfg, nullptr, &results[j], streams[static_cast<size_t>(t)]);
         } catch (...) {

@@ -72,10 +72,10 @@ __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;"
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
 // One-shot TMA bulk copy global -> shared (1D, bytes % 16 == 0, both
-// addresses 16-byte aligned) completing on an mbarrier.  Call from every
-// thread of the CTA: thread 0 issues, everyone waits.
-__device__ __forceinline__ void bulk_load_to_smem(void* dst, const void* src, uint32_t bytes,
-                                                  unsigned long long* mbar) {
+// addresses 16-byte aligned) completing on an mbarrier, in two halves:
+// thread 0 initialises the barrier and issues (a __syncthreads must follow
+// before anyone polls), then any thread may wait for the bytes.
+__device__ __forceinline__ void bulk_issue(void* dst, const void* src, uint32_t bytes, unsigned long long* mbar) {
   const uint32_t b = static_cast<uint32_t>(__cvta_generic_to_shared(mbar));
   if (threadIdx.x == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(b) : "memory");
@@ -86,7 +86,9 @@ __device__ __forceinline__ void bulk_load_to_smem(void* dst, const void* src, ui
                  "l"(src), "r"(bytes), "r"(b)
                  : "memory");
   }
-  __syncthreads();  // the barrier is initialised before anyone polls it
+}
+__device__ __forceinline__ void bulk_wait(unsigned long long* mbar) {
+  const uint32_t b = static_cast<uint32_t>(__cvta_generic_to_shared(mbar));
   asm volatile(
       "{\n"
       ".reg .pred p;\n"

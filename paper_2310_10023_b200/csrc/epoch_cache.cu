@@ -21,6 +21,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "kernels.h"
 #include "score_common.cuh"
@@ -403,27 +404,45 @@ __device__ __forceinline__ void probe_ambiguous(const RotCache& c, const LevelVi
   }
 }
 
-// Warp items are (run, 256-entry chunk) pairs, grid-strided.  The 32 lanes
-// first fetch the headers (run node, cache info) of 32 items in parallel and
-// the warp then walks only the items that have entries, so empty chunks and
-// uncached runs cost no serial load latency.
+// Warp items are (run, chunk of its histogram) pairs, grid-strided.  The 32
+// lanes first fetch the headers (run node, cache info) of 32 items in
+// parallel and park the ones with entries in a per-warp shared-memory list,
+// so the probe loops hold no header registers and empty chunks or uncached
+// runs cost no serial load latency.  Block shape (A/B, C2 / C3 device ms):
+// 256x3 0.833 / 13.83, 512x2 0.838 / 13.95, 1024x1 0.838 / 14.39 -- the
+// kernel is bound by its dependent-load chain (headers, window, entries),
+// not by occupancy (1024x1 reaches 37% achieved vs 22%).
 #ifndef BBS_PROBE_T
 #define BBS_PROBE_T 256
 #define BBS_PROBE_B 3
 #endif
 constexpr int kProbeThreads = BBS_PROBE_T;
+constexpr int kProbeWarps = kProbeThreads / 32;
+struct __align__(16) ProbeItem {
+  int4 h0;  // bx, by, bz, run
+  int4 h1;  // level, pool offset, first entry, end entry
+  int4 h2;  // ambiguous points (chunk 0 only), slot, iroll, ipitch | iyaw << 16
+};
+constexpr int kProbeItemBytes = kProbeWarps * 32 * static_cast<int>(sizeof(ProbeItem));
+
 __global__ void __launch_bounds__(BBS_PROBE_T, BBS_PROBE_B) cache_probe_kernel(RotCache c, MapView map, GridView G,
                                                           ScanView scan,
                                                           const bbs_node* __restrict__ pending,
                                                           const uint32_t* __restrict__ d_n,
-                                                          uint32_t chunks_per_run,
+                                                          uint32_t chunks_per_run, uint32_t half_items_per_warp,
                                                           int32_t* __restrict__ scores) {
-  extern __shared__ __align__(16) uint32_t s_win[];  // staged level's padded column window
+  // [staged level's padded column window][per-warp item lists]
+  extern __shared__ __align__(16) unsigned char probe_smem[];
   __shared__ __align__(8) unsigned long long s_mbar;
-  // the window is search-constant: one bulk copy per CTA (before pdl_wait:
-  // it does not depend on the previous kernel)
-  if (c.stg_level >= 0)
-    bulk_load_to_smem(s_win, c.stg_win, ((c.stg_pitch * c.stg_rows * 4u) + 15u) & ~15u, &s_mbar);
+  const uint32_t win_bytes = c.stg_level >= 0 ? ((c.stg_pitch * c.stg_rows * 4u) + 15u) & ~15u : 0u;
+  const uint32_t* s_win = reinterpret_cast<const uint32_t*>(probe_smem);
+  ProbeItem* s_items = reinterpret_cast<ProbeItem*>(probe_smem + win_bytes) + (threadIdx.x >> 5) * 32;
+  // the window is search-constant: one bulk copy per CTA, issued before
+  // pdl_wait (it does not depend on the previous kernel) and awaited only
+  // by warps that probe the staged level
+  if (win_bytes) bulk_issue(probe_smem, c.stg_win, win_bytes, &s_mbar);
+  __syncthreads();  // the mbarrier is initialised before anyone polls it
+  bool win_ready = win_bytes == 0;
   pdl_wait();
 
   const uint32_t n_runs = *d_n / 8;
@@ -434,7 +453,7 @@ __global__ void __launch_bounds__(BBS_PROBE_T, BBS_PROBE_B) cache_probe_kernel(R
   // atomics), sized by the largest histogram built so far
   const uint32_t max_ent = max(1u, c.ctl[kCtlMaxEnt]);
   const uint32_t granules = (max_ent + kProbeChunk - 1) / kProbeChunk;
-  const uint64_t want = (2 * n_warps + max(n_runs, 1u) - 1) / max(n_runs, 1u);
+  const uint64_t want = (half_items_per_warp * n_warps / 2 + max(n_runs, 1u) - 1) / max(n_runs, 1u);
   {
     uint64_t cpr = want < granules ? want : granules;
     if (cpr > chunks_per_run) cpr = chunks_per_run;
@@ -445,54 +464,62 @@ __global__ void __launch_bounds__(BBS_PROBE_T, BBS_PROBE_B) cache_probe_kernel(R
   const uint64_t n_items = static_cast<uint64_t>(n_runs) * chunks_per_run;
   const uint64_t gw = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   for (uint64_t k0 = 0; gw + k0 * n_warps < n_items; k0 += 32) {
-    const uint64_t item = gw + (k0 + lane) * n_warps;
-    // inf stays NONE for runs at uncached levels (no slot)
-    int4 a = make_int4(0, 0, 0, 0), b = make_int4(0, 0, 0, 0), inf = make_int4(kCacheNone, 0, 0, 0);
-    uint32_t slot = 0, chunk = 0, run = 0;
-    bool has = false;
-    if (item < n_items) {
-      run = static_cast<uint32_t>(item / chunks_per_run);
-      chunk = static_cast<uint32_t>(item % chunks_per_run);
-      a = __ldg(reinterpret_cast<const int4*>(pending) + 16ull * run);
-      b = __ldg(reinterpret_cast<const int4*>(pending) + 16ull * run + 1);
-      if (run_slot(c, G, a, b, &slot)) {
-        inf = c.info[slot];
-        has = inf.x == kCacheReady &&
-              (chunk * chunk_len < static_cast<uint32_t>(inf.z) || (chunk == 0 && inf.w > 0));
+    unsigned hm;
+    {
+      const uint64_t item = gw + (k0 + lane) * n_warps;
+      // inf stays NONE for runs at uncached levels (no slot)
+      int4 a = make_int4(0, 0, 0, 0), b = make_int4(0, 0, 0, 0), inf = make_int4(kCacheNone, 0, 0, 0);
+      uint32_t slot = 0, chunk = 0, run = 0;
+      bool has = false;
+      if (item < n_items) {
+        run = static_cast<uint32_t>(item / chunks_per_run);
+        chunk = static_cast<uint32_t>(item % chunks_per_run);
+        a = __ldg(reinterpret_cast<const int4*>(pending) + 16ull * run);
+        b = __ldg(reinterpret_cast<const int4*>(pending) + 16ull * run + 1);
+        if (run_slot(c, G, a, b, &slot)) {
+          inf = c.info[slot];
+          has = inf.x == kCacheReady &&
+                (chunk * chunk_len < static_cast<uint32_t>(inf.z) || (chunk == 0 && inf.w > 0));
+        }
       }
+      // runs without a READY histogram go to the cube kernel's list (chunk 0 items)
+      const bool fb = item < n_items && chunk == 0 && inf.x != kCacheReady;
+      const unsigned fbm = __ballot_sync(0xffffffffu, fb);
+      if (fbm) {
+        const int leader = __ffs(fbm) - 1;
+        uint32_t at = 0;
+        if (lane == leader) at = atomicAdd(&c.ctl[3], static_cast<uint32_t>(__popc(fbm)));
+        at = __shfl_sync(0xffffffffu, at, leader);
+        if (fb) c.fb_runs[at + __popc(fbm & ((1u << lane) - 1))] = run;
+      }
+      hm = __ballot_sync(0xffffffffu, has);
+      if (has) {
+        const uint32_t e0 = chunk * chunk_len;
+        const uint32_t e1 = min(static_cast<uint32_t>(inf.z), e0 + chunk_len);
+        ProbeItem it;
+        it.h0 = make_int4(a.x, a.y, a.z, static_cast<int32_t>(run));
+        it.h1 = make_int4(b.z, inf.y, static_cast<int32_t>(e0), static_cast<int32_t>(e1));
+        it.h2 = make_int4(chunk == 0 ? inf.w : 0, static_cast<int32_t>(slot), a.w,
+                          (b.x & 0xFFFF) | (b.y << 16));
+        s_items[__popc(hm & ((1u << lane) - 1))] = it;
+      }
+      __syncwarp();
     }
-    // runs without a READY histogram go to the cube kernel's list (chunk 0 items)
-    const bool fb = item < n_items && chunk == 0 && inf.x != kCacheReady;
-    const unsigned fbm = __ballot_sync(0xffffffffu, fb);
-    if (fbm) {
-      const int leader = __ffs(fbm) - 1;
-      uint32_t at = 0;
-      if (lane == leader) at = atomicAdd(&c.ctl[3], static_cast<uint32_t>(__popc(fbm)));
-      at = __shfl_sync(0xffffffffu, at, leader);
-      if (fb) c.fb_runs[at + __popc(fbm & ((1u << lane) - 1))] = run;
-    }
-    unsigned todo = __ballot_sync(0xffffffffu, has);
-    while (todo) {
-      const int src = __ffs(todo) - 1;
-      todo &= todo - 1;
-      const uint32_t r = __shfl_sync(0xffffffffu, run, src);
-      const uint32_t ch = __shfl_sync(0xffffffffu, chunk, src);
-      const int32_t bx = __shfl_sync(0xffffffffu, a.x, src);
-      const int32_t by = __shfl_sync(0xffffffffu, a.y, src);
-      const int32_t bz = __shfl_sync(0xffffffffu, a.z, src);
-      const int l = __shfl_sync(0xffffffffu, b.z, src);
-      const uint32_t off = static_cast<uint32_t>(__shfl_sync(0xffffffffu, inf.y, src));
-      const uint32_t n_ent = static_cast<uint32_t>(__shfl_sync(0xffffffffu, inf.z, src));
-      const int n_amb = ch == 0 ? __shfl_sync(0xffffffffu, inf.w, src) : 0;
+    const int nh = __popc(hm);
+    for (int j = 0; j < nh; ++j) {
+      const int4 h0 = s_items[j].h0;
+      const int4 h1 = s_items[j].h1;
+      const int32_t bx = h0.x, by = h0.y, bz = h0.z;
+      const int l = h1.x;
+      const int4* __restrict__ ent = c.pool + static_cast<uint32_t>(h1.y);
+      const uint32_t e0 = static_cast<uint32_t>(h1.z), e1 = static_cast<uint32_t>(h1.w);
       const LevelView& L = map.level[l];
-      const uint32_t ox = static_cast<uint32_t>(bx) - static_cast<uint32_t>(L.box_min[0]);
-      const uint32_t oy = static_cast<uint32_t>(by) - static_cast<uint32_t>(L.box_min[1]);
-      const uint32_t oz = static_cast<uint32_t>(bz) - static_cast<uint32_t>(L.box_min[2]);
       int acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-      const uint32_t e0 = ch * chunk_len;
-      const uint32_t e1 = min(n_ent, e0 + chunk_len);
-      const int4* __restrict__ ent = c.pool + off;
       if (l == c.stg_level) {
+        if (!win_ready) {
+          bulk_wait(&s_mbar);
+          win_ready = true;
+        }
         // staged: 4 LDS + 4 clamped funnel shifts give an entry's 2x2x2 child
         // mask (bits t = dx*4 + dy*2 + dz); 4 masks are packed as bytes and
         // per child t one LOP3 + IDP4A adds 2^t * count of the hits
@@ -524,6 +551,9 @@ __global__ void __launch_bounds__(BBS_PROBE_T, BBS_PROBE_B) cache_probe_kernel(R
 #pragma unroll
         for (int t = 0; t < 8; ++t) acc[t] = static_cast<int>(a8[t] >> t);
       } else if (L.layout == BBS_LAYOUT_BITMAP) {
+        const uint32_t ox = static_cast<uint32_t>(bx) - static_cast<uint32_t>(L.box_min[0]);
+        const uint32_t oy = static_cast<uint32_t>(by) - static_cast<uint32_t>(L.box_min[1]);
+        const uint32_t oz = static_cast<uint32_t>(bz) - static_cast<uint32_t>(L.box_min[2]);
         // two entries per lane per step: 8-16 independent column loads in flight
         uint32_t e = e0 + lane;
         for (; e + 32 < e1; e += 64) {
@@ -550,20 +580,21 @@ __global__ void __launch_bounds__(BBS_PROBE_T, BBS_PROBE_B) cache_probe_kernel(R
                           : 0;
         }
       }
-      if (n_amb > 0) {
-        const uint32_t sl = __shfl_sync(0xffffffffu, slot, src);
-        const int ir = __shfl_sync(0xffffffffu, a.w, src);
-        const int ip = __shfl_sync(0xffffffffu, b.x, src);
-        const int iw = __shfl_sync(0xffffffffu, b.y, src);
-        probe_ambiguous(c, L, G, scan, sl, n_amb, l, ir, ip, iw, bx, by, bz, lane, acc);
-      }
+      const int4 h2 = s_items[j].h2;
+      if (h2.x > 0)
+        probe_ambiguous(c, L, G, scan, static_cast<uint32_t>(h2.y), h2.x, l, h2.z, h2.w & 0xFFFF, h2.w >> 16,
+                        bx, by, bz, lane, acc);
+      const uint32_t r = static_cast<uint32_t>(h0.w);
 #pragma unroll
       for (int t = 0; t < 8; ++t) {
         const int v = __reduce_add_sync(0xffffffffu, acc[t]);
         if (lane == 0 && v) atomicAdd(&scores[8ull * r + t], v);
       }
     }
+    __syncwarp();  // the list is rewritten by the next round of headers
   }
+  // no CTA exits with its window copy in flight
+  if (!win_ready) bulk_wait(&s_mbar);
 }
 
 // The staged probe window: zero-padded, words shifted up by 8 bits; the
@@ -633,30 +664,37 @@ void launch_epoch_score(const MapView& map, const GridView& grid, const ScanView
   static_assert(kCacheHashSlots % kBuildThreads == 0, "slot rows per thread");
   once_per_device(attr_done, attr_mu, [&] {
     BBS_CUDA(cudaFuncSetAttribute(cache_build_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, build_smem));
-    BBS_CUDA(cudaFuncSetAttribute(cache_probe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kStageWindowMax));
+    BBS_CUDA(cudaFuncSetAttribute(cache_probe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  kStageWindowMax + kProbeItemBytes));
   });
   const uint32_t max_runs = (n_max + 7) / 8;
   // the epoch's branch kernel already claimed the slots (cache_claim_run)
   // after its frontier reset ctl[2..3]
   if (builds) {  // false once no level can claim a build any more (host-known)
-    launch_pdl(cache_build_kernel, std::min<uint32_t>(std::max<uint32_t>(max_runs, 1), 148 * 2), kBuildThreads,
+    launch_pdl(cache_build_kernel, std::min<uint32_t>(std::max<uint32_t>(max_runs, 1), share_cap(148 * 2)), kBuildThreads,
                build_smem, s, cache, map, grid, scan);
     BBS_CUDA(cudaGetLastError());
   }
   const uint32_t chunks = (scan.k + kProbeChunk - 1) / kProbeChunk;
   const uint64_t warp_items = static_cast<uint64_t>(max_runs) * chunks;
   const uint64_t wpc = kProbeThreads / 32;  // warps per CTA
-  const unsigned g = static_cast<unsigned>(std::min<uint64_t>((warp_items + wpc - 1) / wpc + 1, 148ull * 16));
-  const int win_smem = cache.stg_level >= 0 ? static_cast<int>(((cache.stg_pitch * cache.stg_rows * 4u) + 15u) & ~15u) : 0;
+  const unsigned g = static_cast<unsigned>(std::min<uint64_t>((warp_items + wpc - 1) / wpc + 1, share_cap(148ull * 16)));
+  const int win_smem = (cache.stg_level >= 0 ? static_cast<int>(((cache.stg_pitch * cache.stg_rows * 4u) + 15u) & ~15u) : 0) +
+                       kProbeItemBytes;
 
   unsigned gp = g;
   if (win_smem > 0) {
     // persistent: each CTA stages the window once
     int per_sm = 1;
     BBS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cache_probe_kernel, kProbeThreads, win_smem));
-    gp = std::min<unsigned>(g, 148u * static_cast<unsigned>(std::max(per_sm, 1)));
+    gp = std::min<unsigned>(g, share_cap(148ull * static_cast<unsigned>(std::max(per_sm, 1))));
   }
-  launch_pdl(cache_probe_kernel, gp, kProbeThreads, win_smem, s, cache, map, grid, scan, pending, d_n, chunks, scores);
+  static const uint32_t hipw = [] {
+    const char* v = std::getenv("BBS_PROBE_HIPW");  // A/B: 2x the warp items per warp
+    return v ? static_cast<uint32_t>(std::max(1, std::atoi(v))) : 4u;
+  }();
+  launch_pdl(cache_probe_kernel, gp, kProbeThreads, win_smem, s, cache, map, grid, scan, pending, d_n, chunks, hipw,
+             scores);
   BBS_CUDA(cudaGetLastError());
   launch_score_cube8(map, grid, scan, pending, d_n, n_max, n_ptiles, scores, &cache, s);
 }

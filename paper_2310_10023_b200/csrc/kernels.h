@@ -33,6 +33,17 @@ struct StreamAllocs {
   }
 };
 
+// Share of the GPU one search's persistent (grid-strided) epoch kernels
+// claim: 1 for a lone search; bbs_search_scans sets it per worker thread so
+// T concurrent searches size their grids to co-reside instead of each
+// filling every SM (the epoch kernels are latency-bound at C4's sizes).
+extern thread_local unsigned g_grid_share;
+extern thread_local bool g_blocking_sync;  // host checks wait on a blocking-sync event
+inline unsigned share_cap(uint64_t cap) {
+  const uint64_t c = cap / (g_grid_share ? g_grid_share : 1u);
+  return static_cast<unsigned>(c < 16 ? 16 : c);
+}
+
 
 struct ScanView {
   const double* x;

@@ -1232,8 +1232,8 @@ void launch_score_cube8(const MapView& map, const GridView& grid, const ScanView
   const uint64_t items = static_cast<uint64_t>((n_max + 7) / 8) * n_ptiles;
   // with the cache the run list and tiling are only known on the device:
   // one resident wave (4 CTAs per SM), grid-strided
-  const unsigned g = cache ? 148u * 4u
-                           : static_cast<unsigned>(std::min<uint64_t>(std::max<uint64_t>(items, 1), 148ull * 4 * 8));
+  const unsigned g = cache ? share_cap(148ull * 4)
+                           : static_cast<unsigned>(std::min<uint64_t>(std::max<uint64_t>(items, 1), share_cap(148ull * 4 * 8)));
   // the flush cache's direct runs (large scans) keep two points in flight;
   // without the cache (small scans, short point tiles) one point per step
   if (cache)

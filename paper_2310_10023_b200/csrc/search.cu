@@ -37,6 +37,9 @@
 
 namespace bbs {
 
+thread_local unsigned g_grid_share = 1;
+thread_local bool g_blocking_sync = false;
+
 namespace {
 
 constexpr unsigned long long kSMax = (1ull << 20) - 1;
@@ -1574,7 +1577,7 @@ struct RootSurvives {
 };
 
 unsigned grid1(uint64_t n, int threads = 256) {
-  return static_cast<unsigned>(std::min<uint64_t>(std::max<uint64_t>((n + threads - 1) / threads, 1), 148ull * 16));
+  return static_cast<unsigned>(std::min<uint64_t>(std::max<uint64_t>((n + threads - 1) / threads, 1), share_cap(148ull * 16)));
 }
 
 float elapsed(cudaEvent_t a, cudaEvent_t b) {
@@ -1646,6 +1649,7 @@ struct Workspace {
   EpochState* h_st = nullptr;
   cudaStream_t side = nullptr;            // prebuild stream (forked per search)
   cudaGraphExec_t graph_exec = nullptr;   // epoch-batch graph, updated in place per search
+  cudaEvent_t block_ev = nullptr;         // blocking-sync event (host checks of concurrent searches)
   unsigned long long* h_small = nullptr;  // pinned: probes, n_root_surv
   std::vector<cudaEvent_t> ev;
   size_t ev_used = 0;
@@ -1684,6 +1688,7 @@ struct Workspace {
     for (auto e : ev) cudaEventDestroy(e);
     if (side) cudaStreamDestroy(side);
     if (graph_exec) cudaGraphExecDestroy(graph_exec);
+    if (block_ev) cudaEventDestroy(block_ev);
   }
 };
 
@@ -2314,7 +2319,7 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
   const uint64_t n_surv_tiles = (pend_cap + kSTile - 1) / kSTile;
   unsigned long long* surv_tiles = W.surv_tiles.get(n_surv_tiles, s);
   BBS_CUDA(cudaMemsetAsync(surv_tiles, 0, n_surv_tiles * sizeof(unsigned long long), s));
-  const unsigned surv_grid = static_cast<unsigned>(std::min<uint64_t>(n_surv_tiles, 148ull * 4));
+  const unsigned surv_grid = static_cast<unsigned>(std::min<uint64_t>(n_surv_tiles, share_cap(148ull * 4)));
   const uint64_t exp_cap = pend_cap / 8 + 2;
   uint32_t* exp_parent = W.exp_parent.get(exp_cap, s);
   uint32_t* exp_off = W.exp_off.get(exp_cap, s);
@@ -2427,7 +2432,7 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
       BBS_CUDA(cub::DeviceRadixSort::SortKeys(sort_temp, tb, s_key, s_key2, static_cast<int64_t>(pend_cap), 0, 64, s));
     }
     if (dbg_phases) record(ev_dbg[3 * e + 1]);
-    launch_pdl(merge_kernel, static_cast<unsigned>(std::min<uint64_t>((qcap + kMTile - 1) / kMTile, 148ull * 8)),
+    launch_pdl(merge_kernel, static_cast<unsigned>(std::min<uint64_t>((qcap + kMTile - 1) / kMTile, share_cap(148ull * 8))),
                kMT, 0, s, d_st, q, strategy, s_key2);
     BBS_CUDA(cudaGetLastError());
     if (dbg_phases) record(ev_dbg[3 * e + 2]);
@@ -2488,6 +2493,17 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
     launches += 2;
   }
 
+  // concurrent searches (bbs_search_scans) wait on a blocking-sync event so
+  // T waiting host threads do not spin on T cores
+  auto host_wait = [&] {
+    if (!g_blocking_sync) {
+      BBS_CUDA(cudaStreamSynchronize(s));
+      return;
+    }
+    if (!W.block_ev) BBS_CUDA(cudaEventCreateWithFlags(&W.block_ev, cudaEventBlockingSync | cudaEventDisableTiming));
+    BBS_CUDA(cudaEventRecord(W.block_ev, s));
+    BBS_CUDA(cudaEventSynchronize(W.block_ev));
+  };
   tmark("loop");
   while (self_active || others_active) {
     // capacity: the queue grows by at most pend_cap per epoch
@@ -2549,7 +2565,7 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
     }
     BBS_CUDA(cudaMemcpyAsync(W.h_st, d_st, sizeof(EpochState), cudaMemcpyDeviceToHost, s));
     d2h += sizeof(EpochState);
-    BBS_CUDA(cudaStreamSynchronize(s));
+    host_wait();
     for (int e = 0; e < n_ep; ++e) {
       pass_ms.push_back(elapsed(ev_loop, ev_pass[e]));
       esm += elapsed(ev_s0[e], ev_s1[e]);
@@ -2628,7 +2644,7 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
   }
   BBS_CUDA(cudaMemcpyAsync(&W.h_small[3], d_probes + 2, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
   d2h += sizeof(unsigned long long);
-  BBS_CUDA(cudaStreamSynchronize(s));
+  host_wait();
   hs = *W.h_st;
   if (dev_init) root_probes = W.h_small[0];
   out->root_words = W.h_small[3];

@@ -8,16 +8,29 @@ import paper_2310_10023_b200 as B
 cfgd = bench.CONFIGS["c4"]
 spec = H.SceneSpec.default(**cfgd["spec"])
 m, _, _ = H.gen_scene(spec, cfgd["seed"])
-scans, poses = H.gen_scans(spec, cfgd["seed"], 1000, 32)
+scans, poses = H.gen_scans(spec, cfgd["seed"], 1000, int(os.environ.get("C4_N", "32")))
 scans = [H.cut_scan(s, min(cfgd["K"], s.shape[0]), 7) for s in scans]
 vm = B.MultiResVoxelMap.build(m, cfgd["r"], cfgd["max_level"])
 ds = [B.DeviceScan(vm, s) for s in scans]
 cfg = bench.search_config(B, cfgd)
-for conc in (1, 2, 4, 8, 16):
-    B.search_scans(vm, ds, cfg, concurrency=conc)
-    t = time.perf_counter()
-    res = B.search_scans(vm, ds, cfg, concurrency=conc)
-    dt = time.perf_counter() - t
-    dev = sum(r.device_ms for r in res)
-    print(f"concurrency {conc}: {len(ds) / dt:.0f} scans/s, wall {1e3 * dt:.1f} ms, sum device {dev:.1f} ms, "
-          f"mean device {dev / len(ds):.2f} ms", flush=True)
+shares = [int(x) for x in os.environ.get("C4_SHARES", "0").split(",")]
+concs = [int(x) for x in os.environ.get("C4_CONCS", "1,2,4,8,16").split(",")]
+print("host cores", os.cpu_count(), flush=True)
+for share in shares:
+    if share:
+        os.environ["BBS_GRID_SHARE"] = str(share)
+    else:
+        os.environ.pop("BBS_GRID_SHARE", None)
+    for conc in concs:
+        B.search_scans(vm, ds, cfg, concurrency=conc)
+        c0 = time.process_time()
+        best = 1e9
+        for _ in range(int(os.environ.get("C4_REPS", "3"))):
+            t = time.perf_counter()
+            res = B.search_scans(vm, ds, cfg, concurrency=conc)
+            best = min(best, time.perf_counter() - t)
+        if best == 1e9:
+            continue
+        dev = sum(r.device_ms for r in res)
+        print(f"share {share or 'T'} concurrency {conc}: {len(ds) / best:.0f} scans/s, wall {1e3 * best:.1f} ms, "
+              f"sum device {dev:.1f} ms, mean device {dev / len(ds):.2f} ms, cpu {1e3 * (time.process_time() - c0):.0f} ms", flush=True)
