@@ -33,7 +33,7 @@
 extern "C" {
 #endif
 
-#define BBS_ABI_VERSION 4
+#define BBS_ABI_VERSION 5
 
 /* Status codes, 1:1 with the exception classes of errors.hpp:11-98. */
 typedef enum bbs_status {
@@ -138,6 +138,8 @@ typedef struct bbs_search_result {
   uint64_t evals_per_level[16]; /* nodes scored per tree level (roots included) */
   uint64_t root_words;    /* z-column words the root column kernel read (its actual gathers) */
   double root_col_ms;     /* device time of the root column kernel launches, CUDA events */
+  uint64_t group_checks;  /* bbs_search_scans: host checks whose epochs ran in a co-batched group
+                             launch (0: the search launched its own) */
 } bbs_search_result;
 
 /* AxisGrid, angular_grid.hpp:45-58. */

@@ -236,6 +236,7 @@ class SearchResult:
     evals_per_level: tuple = ()
     root_words: int = 0
     root_col_ms: float = 0.0
+    group_checks: int = 0
 
 
 def _result_from_c(r: SearchResultC, trace_buf=None) -> SearchResult:
@@ -251,7 +252,7 @@ def _result_from_c(r: SearchResultC, trace_buf=None) -> SearchResult:
         epoch_score_ms=r.epoch_score_ms, root_nodes=r.root_nodes, queue_peak=r.queue_peak,
         root_probes=r.root_probes, h2d_bytes=r.h2d_bytes, d2h_bytes=r.d2h_bytes,
         kernel_launches=r.kernel_launches, evals_per_level=tuple(r.evals_per_level),
-        root_words=r.root_words, root_col_ms=r.root_col_ms)
+        root_words=r.root_words, root_col_ms=r.root_col_ms, group_checks=r.group_checks)
     if trace_buf is not None:
         out.best_score_trace = list(trace_buf[: min(r.trace_length, len(trace_buf))])
     return out

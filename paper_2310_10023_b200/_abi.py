@@ -99,6 +99,7 @@ class SearchResultC(C.Structure):
         ("evals_per_level", C.c_uint64 * 16),
         ("root_words", C.c_uint64),
         ("root_col_ms", C.c_double),
+        ("group_checks", C.c_uint64),
     ]
 
 

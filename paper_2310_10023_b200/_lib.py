@@ -102,7 +102,7 @@ for _name, (_res, _args) in SIGNATURES.items():
     _f.restype = _res
     _f.argtypes = _args
 
-ABI_VERSION = 4  # include/bbs.h BBS_ABI_VERSION this mirror was written for
+ABI_VERSION = 5  # include/bbs.h BBS_ABI_VERSION this mirror was written for
 if lib.bbs_abi_version() != ABI_VERSION:
     raise ImportError(f"{LIB_PATH} has ABI version {lib.bbs_abi_version()}, "
                       f"the Python mirror expects {ABI_VERSION}: rebuild the library")

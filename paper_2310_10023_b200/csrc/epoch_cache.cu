@@ -65,8 +65,10 @@ constexpr uint32_t kEarlyAbortPoints = 2048;  // sample before judging a build's
 // (fast path), de-duplicate the voxel offsets in a shared-memory hash, and
 // append (offset, count) entries + ambiguous point ids to the pool.  Two
 // points per thread per step keep two load/rotate chains in flight.
-__global__ void __launch_bounds__(kBuildThreads) cache_build_kernel(RotCache c, MapView map, GridView G,
-                                                                    ScanView scan) {
+__device__ __forceinline__ void cache_build_kernel_body(const RotCache& c,
+                                                        const MapView& map,
+                                                        const GridView& G,
+                                                        ScanView scan) {
   pdl_wait();
 
   extern __shared__ __align__(16) unsigned char smem[];
@@ -383,6 +385,11 @@ __global__ void __launch_bounds__(kBuildThreads) cache_build_kernel(RotCache c, 
   }
 }
 
+__global__ void __launch_bounds__(kBuildThreads) cache_build_kernel(RotCache c, MapView map, GridView G,
+                                                                    ScanView scan) {
+  cache_build_kernel_body(c, map, G, scan);
+}
+
 // Ambiguous points of one run (exact divide path), kept out of line so the
 // probe loop's register budget stays small.
 __device__ __forceinline__ void probe_ambiguous(const RotCache& c, const LevelView& L, const GridView& G,
@@ -425,12 +432,16 @@ struct __align__(16) ProbeItem {
 };
 constexpr int kProbeItemBytes = kProbeWarps * 32 * static_cast<int>(sizeof(ProbeItem));
 
-__global__ void __launch_bounds__(BBS_PROBE_T, BBS_PROBE_B) cache_probe_kernel(RotCache c, MapView map, GridView G,
-                                                          ScanView scan,
-                                                          const bbs_node* __restrict__ pending,
-                                                          const uint32_t* __restrict__ d_n,
-                                                          uint32_t chunks_per_run, uint32_t half_items_per_warp,
-                                                          int32_t* __restrict__ scores) {
+__device__ __forceinline__ void cache_probe_kernel_body(const RotCache& c,
+                                                        const MapView& map,
+                                                        const GridView& G,
+                                                        ScanView scan,
+                                                        const bbs_node* __restrict__ pending,
+                                                        const uint32_t* __restrict__ d_n,
+                                                        uint32_t chunks_per_run,
+                                                        uint32_t half_items_per_warp,
+                                                        bool lazy_stage,
+                                                        int32_t* __restrict__ scores) {
   // [staged level's padded column window][per-warp item lists]
   extern __shared__ __align__(16) unsigned char probe_smem[];
   __shared__ __align__(8) unsigned long long s_mbar;
@@ -440,7 +451,8 @@ __global__ void __launch_bounds__(BBS_PROBE_T, BBS_PROBE_B) cache_probe_kernel(R
   // the window is search-constant: one bulk copy per CTA, issued before
   // pdl_wait (it does not depend on the previous kernel) and awaited only
   // by warps that probe the staged level
-  if (win_bytes) bulk_issue(probe_smem, c.stg_win, win_bytes, &s_mbar);
+  // (co-batched launches stage lazily: most CTAs of a light slot have no item)
+  if (!lazy_stage && win_bytes) bulk_issue(probe_smem, c.stg_win, win_bytes, &s_mbar);
   __syncthreads();  // the mbarrier is initialised before anyone polls it
   bool win_ready = win_bytes == 0;
   pdl_wait();
@@ -463,6 +475,12 @@ __global__ void __launch_bounds__(BBS_PROBE_T, BBS_PROBE_B) cache_probe_kernel(R
   const uint32_t chunk_len = ((granules + chunks_per_run - 1) / chunks_per_run) * kProbeChunk;
   const uint64_t n_items = static_cast<uint64_t>(n_runs) * chunks_per_run;
   const uint64_t gw = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  if (lazy_stage) {
+    const bool any = static_cast<uint64_t>(blockIdx.x) * (blockDim.x >> 5) < n_items;
+    if (win_bytes && any) bulk_issue(probe_smem, c.stg_win, win_bytes, &s_mbar);
+    win_ready = win_bytes == 0 || !any;
+    __syncthreads();
+  }
   for (uint64_t k0 = 0; gw + k0 * n_warps < n_items; k0 += 32) {
     unsigned hm;
     {
@@ -597,6 +615,15 @@ __global__ void __launch_bounds__(BBS_PROBE_T, BBS_PROBE_B) cache_probe_kernel(R
   if (!win_ready) bulk_wait(&s_mbar);
 }
 
+__global__ void __launch_bounds__(BBS_PROBE_T, BBS_PROBE_B) cache_probe_kernel(RotCache c, MapView map, GridView G,
+                                                          ScanView scan,
+                                                          const bbs_node* __restrict__ pending,
+                                                          const uint32_t* __restrict__ d_n,
+                                                          uint32_t chunks_per_run, uint32_t half_items_per_warp,
+                                                          int32_t* __restrict__ scores) {
+  cache_probe_kernel_body(c, map, G, scan, pending, d_n, chunks_per_run, half_items_per_warp, false, scores);
+}
+
 // The staged probe window: zero-padded, words shifted up by 8 bits; the
 // tail up to a multiple of 4 words (16 bytes for the bulk copy) is zero.
 __global__ void stage_window_kernel(LevelView SL, int32_t sx0, int32_t sy0, uint32_t pitch, uint32_t n,
@@ -608,6 +635,24 @@ __global__ void stage_window_kernel(LevelView SL, int32_t sx0, int32_t sy0, uint
                  ? SL.words[static_cast<uint32_t>(y) * SL.dim[0] + static_cast<uint32_t>(x)] << 8
                  : 0u;
   }
+}
+
+// Co-batched flushes: blockIdx.y selects the search (ScoreSlot).  Slots
+// without the cache skip both kernels (the cube kernel scores their runs).
+__global__ void __launch_bounds__(kBuildThreads) cache_build_group(MapView map, const ScoreSlot* __restrict__ ga,
+                                                                   size_t stride) {
+  const ScoreSlot& a = score_slot(ga, stride);
+  if (!a.cache.enabled) return;
+  cache_build_kernel_body(a.cache, map, a.G, a.scan);
+}
+
+__global__ void __launch_bounds__(BBS_PROBE_T, BBS_PROBE_B) cache_probe_group(MapView map,
+                                                                             const ScoreSlot* __restrict__ ga,
+                                                                             size_t stride, uint32_t hipw) {
+  const ScoreSlot& a = score_slot(ga, stride);
+  if (!a.cache.enabled) return;
+  cache_probe_kernel_body(a.cache, map, a.G, a.scan, a.nodes, a.d_n, (a.scan.k + kProbeChunk - 1) / kProbeChunk, hipw,
+                          true, a.scores);
 }
 
 }  // namespace
@@ -697,6 +742,31 @@ void launch_epoch_score(const MapView& map, const GridView& grid, const ScanView
              scores);
   BBS_CUDA(cudaGetLastError());
   launch_score_cube8(map, grid, scan, pending, d_n, n_max, n_ptiles, scores, &cache, s);
+}
+
+void launch_epoch_score_group(const MapView& map, const ScoreSlot* slots, size_t stride, uint32_t n_slots,
+                              cudaStream_t s) {
+  static std::atomic<uint64_t> attr_done{0};
+  static std::mutex attr_mu;
+  const int build_smem = kCacheHashSlots * 12 + kCacheAmbCap * 4;
+  const int probe_smem = kStageWindowMax + kProbeItemBytes;  // any slot's window
+  once_per_device(attr_done, attr_mu, [&] {
+    BBS_CUDA(cudaFuncSetAttribute(cache_build_group, cudaFuncAttributeMaxDynamicSharedMemorySize, build_smem));
+    BBS_CUDA(cudaFuncSetAttribute(cache_probe_group, cudaFuncAttributeMaxDynamicSharedMemorySize, probe_smem));
+  });
+  static const uint32_t hipw = [] {
+    const char* v = std::getenv("BBS_PROBE_HIPW");
+    return v ? static_cast<uint32_t>(std::max(1, std::atoi(v))) : 4u;
+  }();
+  launch_pdl(cache_build_group, dim3(per_slot(148 * 2, n_slots), n_slots), kBuildThreads, build_smem, s, map, slots,
+             stride);
+  BBS_CUDA(cudaGetLastError());
+  int per_sm = 1;
+  BBS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cache_probe_group, kProbeThreads, probe_smem));
+  launch_pdl(cache_probe_group, dim3(per_slot(148u * static_cast<unsigned>(std::max(per_sm, 1)), n_slots, 4), n_slots),
+             kProbeThreads, probe_smem, s, map, slots, stride, hipw);
+  BBS_CUDA(cudaGetLastError());
+  launch_score_cube8_group(map, slots, stride, n_slots, s);
 }
 
 }  // namespace bbs

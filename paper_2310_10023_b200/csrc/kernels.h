@@ -2,6 +2,7 @@
 #pragma once
 
 #include <atomic>
+#include <cstdlib>
 #include <mutex>
 
 #include <cuda_runtime.h>
@@ -203,6 +204,40 @@ void launch_epoch_score(const MapView& map, const GridView& grid, const ScanView
                         const bbs_node* pending, const uint32_t* d_n, uint32_t n_max,
                         uint32_t n_ptiles, int32_t* scores, const RotCache& cache, cudaStream_t s,
                         bool builds = true);
+
+// Co-batched flushes (bbs_search_scans): one launch per score kernel for a
+// group of searches, blockIdx.y = slot.  A slot's score-kernel arguments sit
+// at the front of the caller's per-slot record (`stride` bytes apart).
+struct ScoreSlot {
+  GridView G;
+  ScanView scan;
+  RotCache cache;            // cache.enabled == 0: the cube kernel scores every run
+  const bbs_node* nodes;     // pending children
+  const uint32_t* d_n;       // their count (device)
+  int32_t* scores;
+  uint32_t n_ptiles;         // point tiles per run without the cache
+  uint32_t chunks;           // probe: histogram chunks per run at most
+};
+void launch_epoch_score_group(const MapView& map, const ScoreSlot* slots, size_t stride, uint32_t n_slots,
+                              cudaStream_t s);
+void launch_score_cube8_group(const MapView& map, const ScoreSlot* slots, size_t stride, uint32_t n_slots,
+                              cudaStream_t s);
+__device__ __forceinline__ const ScoreSlot& score_slot(const ScoreSlot* ga, size_t stride) {
+  return *reinterpret_cast<const ScoreSlot*>(reinterpret_cast<const char*>(ga) + blockIdx.y * stride);
+}
+// CTAs per slot when `full` CTAs would fill the GPU for one search
+inline unsigned per_slot(unsigned full, uint32_t n_slots, unsigned at_least = 8) {
+  // a slot's kernels may take 1/min(slots, div) of the GPU: slots are
+  // unevenly loaded, so 1/slots starves the heavy ones (C4 16 in flight:
+  // 514 scans/s at div = slots, 789 at 1, 883 at 2)
+  static const unsigned div = [] {
+    const char* v = std::getenv("BBS_GROUP_DIV");
+    return v ? static_cast<unsigned>(std::atoi(v)) : 2u;
+  }();
+  if (div) n_slots = n_slots < div ? n_slots : div;
+  const unsigned g = full / (n_slots ? n_slots : 1u);
+  return g < at_least ? at_least : g;
+}
 
 // Build the histograms of every rotation of `level` (n_rot slots from
 // cache.base[level]) in one launch; cache.builds must hold n_rot entries.

@@ -318,12 +318,15 @@ __global__ void __launch_bounds__(kBoxThreads, 2) score_box_kernel(MapView map, 
 // z-column bitmap: 4 word loads answer all 8 children.  One work item =
 // (run, tile of scan points); counts reduce warp -> CTA -> scores.
 template <bool kILP>
-__global__ void __launch_bounds__(256, 4) score_cube8_kernel(MapView map, GridView grid, ScanView scan,
-                                                             const bbs_node* __restrict__ nodes,
-                                                             const uint32_t* __restrict__ d_n,
-                                                             uint32_t n_ptiles,
-                                                             int32_t* __restrict__ scores,
-                                                             RotCache cache, int use_cache) {
+__device__ __forceinline__ void score_cube8_kernel_body(const MapView& map,
+                                                        const GridView& grid,
+                                                        ScanView scan,
+                                                        const bbs_node* __restrict__ nodes,
+                                                        const uint32_t* __restrict__ d_n,
+                                                        uint32_t n_ptiles,
+                                                        int32_t* __restrict__ scores,
+                                                        const RotCache& cache,
+                                                        int use_cache) {
   pdl_wait();
 
   __shared__ double s_R[9];
@@ -504,6 +507,16 @@ __global__ void __launch_bounds__(256, 4) score_cube8_kernel(MapView map, GridVi
     }
     __syncthreads();
   }
+}
+
+template <bool kILP>
+__global__ void __launch_bounds__(256, 4) score_cube8_kernel(MapView map, GridView grid, ScanView scan,
+                                                             const bbs_node* __restrict__ nodes,
+                                                             const uint32_t* __restrict__ d_n,
+                                                             uint32_t n_ptiles,
+                                                             int32_t* __restrict__ scores,
+                                                             RotCache cache, int use_cache) {
+  score_cube8_kernel_body<kILP>(map, grid, scan, nodes, d_n, n_ptiles, scores, cache, use_cache);
 }
 
 // ---- root batch: whole-scan histogram + z-column kernel ---------------------
@@ -1075,6 +1088,16 @@ unsigned grid_1d(uint64_t n) {
   return static_cast<unsigned>(std::min<uint64_t>(std::max<uint64_t>((n + 255) / 256, 1), 148ull * 32));
 }
 
+// Co-batched flushes: blockIdx.y selects the search (ScoreSlot).
+__global__ void __launch_bounds__(256, 4) score_cube8_group(MapView map, const ScoreSlot* __restrict__ ga,
+                                                            size_t stride) {
+  const ScoreSlot& a = score_slot(ga, stride);
+  if (a.cache.enabled)
+    score_cube8_kernel_body<true>(map, a.G, a.scan, a.nodes, a.d_n, a.n_ptiles, a.scores, a.cache, 1);
+  else
+    score_cube8_kernel_body<false>(map, a.G, a.scan, a.nodes, a.d_n, a.n_ptiles, a.scores, a.cache, 0);
+}
+
 }  // namespace
 
 uint32_t choose_ptiles(uint64_t runs, uint32_t k) {
@@ -1304,6 +1327,12 @@ void score_nodes_general(const MapView& map, const GridView& grid, const ScanVie
                                           nullptr, ni, pt, sc);
   BBS_CUDA(cudaGetLastError());
   write_scores_kernel<<<grid_1d(n), 256, 0, s>>>(d_nodes, sc, n);
+  BBS_CUDA(cudaGetLastError());
+}
+
+void launch_score_cube8_group(const MapView& map, const ScoreSlot* slots, size_t stride, uint32_t n_slots,
+                              cudaStream_t s) {
+  launch_pdl(score_cube8_group, dim3(per_slot(148 * 4, n_slots), n_slots), 256, 0, s, map, slots, stride);
   BBS_CUDA(cudaGetLastError());
 }
 

@@ -23,6 +23,9 @@
 
 #include <algorithm>
 #include <chrono>
+#include <condition_variable>
+#include <exception>
+#include <mutex>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -124,13 +127,16 @@ constexpr int kFIPT = 4;
 constexpr int kFChunk = kFT * kFIPT;
 
 // E1: which queue prefix this epoch pops, pruning, leaf updates, children.
-__global__ void __launch_bounds__(kFT) frontier_kernel(EpochState* st, Queue q, GridView G,
-                                                       unsigned long long b,
-                                                       uint32_t* __restrict__ exp_parent,
-                                                       uint32_t* __restrict__ exp_off,
-                                                       int32_t* __restrict__ trace,
-                                                       unsigned long long trace_cap,
-                                                       int strategy, uint32_t* __restrict__ cache_ctl) {
+__device__ __forceinline__ void frontier_kernel_body(EpochState* st,
+                                                     Queue q,
+                                                     const GridView& G,
+                                                     unsigned long long b,
+                                                     uint32_t* __restrict__ exp_parent,
+                                                     uint32_t* __restrict__ exp_off,
+                                                     int32_t* __restrict__ trace,
+                                                     unsigned long long trace_cap,
+                                                     int strategy,
+                                                     uint32_t* __restrict__ cache_ctl) {
   pdl_wait();
 
   using ScanI = cub::BlockScan<int, kFT>;
@@ -316,6 +322,16 @@ __global__ void __launch_bounds__(kFT) frontier_kernel(EpochState* st, Queue q, 
   }
 }
 
+__global__ void __launch_bounds__(kFT) frontier_kernel(EpochState* st, Queue q, GridView G,
+                                                       unsigned long long b,
+                                                       uint32_t* __restrict__ exp_parent,
+                                                       uint32_t* __restrict__ exp_off,
+                                                       int32_t* __restrict__ trace,
+                                                       unsigned long long trace_cap,
+                                                       int strategy, uint32_t* __restrict__ cache_ctl) {
+  frontier_kernel_body(st, q, G, b, exp_parent, exp_off, trace, trace_cap, strategy, cache_ctl);
+}
+
 // ---- speculative rounds (BFS) ----------------------------------------------
 // Between two flushes nothing is pushed, and in BFS a flush's survivors only
 // change later pops when their key precedes an entry those pops take.  A
@@ -351,14 +367,17 @@ __device__ __forceinline__ unsigned long long pack3(uint32_t pr, uint32_t lu, ui
   return (static_cast<unsigned long long>(pr) << 42) | (static_cast<unsigned long long>(lu) << 21) | ex;
 }
 
-__global__ void __launch_bounds__(kFT) frontier_spec_kernel(EpochState* st, Queue q, GridView G,
-                                                            unsigned long long b, int k_max,
-                                                            uint32_t* __restrict__ exp_parent,
-                                                            uint32_t* __restrict__ exp_off,
-                                                            int32_t* __restrict__ trace,
-                                                            unsigned long long trace_cap,
-                                                            uint32_t* __restrict__ cache_ctl,
-                                                            SpecRec* __restrict__ rec) {
+__device__ __forceinline__ void frontier_spec_kernel_body(EpochState* st,
+                                                          Queue q,
+                                                          const GridView& G,
+                                                          unsigned long long b,
+                                                          int k_max,
+                                                          uint32_t* __restrict__ exp_parent,
+                                                          uint32_t* __restrict__ exp_off,
+                                                          int32_t* __restrict__ trace,
+                                                          unsigned long long trace_cap,
+                                                          uint32_t* __restrict__ cache_ctl,
+                                                          SpecRec* __restrict__ rec) {
   pdl_wait();
 
   using ScanI = cub::BlockScan<int, kFT>;
@@ -636,6 +655,17 @@ __global__ void __launch_bounds__(kFT) frontier_spec_kernel(EpochState* st, Queu
   st->n_expand = rec[ep - 1].exp_end;
 }
 
+__global__ void __launch_bounds__(kFT) frontier_spec_kernel(EpochState* st, Queue q, GridView G,
+                                                            unsigned long long b, int k_max,
+                                                            uint32_t* __restrict__ exp_parent,
+                                                            uint32_t* __restrict__ exp_off,
+                                                            int32_t* __restrict__ trace,
+                                                            unsigned long long trace_cap,
+                                                            uint32_t* __restrict__ cache_ctl,
+                                                            SpecRec* __restrict__ rec) {
+  frontier_spec_kernel_body(st, q, G, b, k_max, exp_parent, exp_off, trace, trace_cap, cache_ctl, rec);
+}
+
 // E2: branch() (nodes.hpp:91-121) for every expanding parent, children in
 // pop order, each parent's children in (jr, jp, jw, jx, jy, jz) order.
 // Batch-split exact mode: the flush's runs of 8 children are
@@ -652,10 +682,15 @@ __device__ __forceinline__ uint32_t own_children(uint32_t n, uint32_t rank, uint
   return runs > rank ? ((runs - rank + world - 1) / world) * 8u : 0u;
 }
 
-__global__ void branch_kernel(EpochState* st, Queue q, GridView G,
-                              const uint32_t* __restrict__ exp_parent,
-                              const uint32_t* __restrict__ exp_off, bbs_node* __restrict__ pending,
-                              int32_t* __restrict__ pscores, RotCache cache, RunSplit split) {
+__device__ __forceinline__ void branch_kernel_body(EpochState* st,
+                                                   Queue q,
+                                                   const GridView& G,
+                                                   const uint32_t* __restrict__ exp_parent,
+                                                   const uint32_t* __restrict__ exp_off,
+                                                   bbs_node* __restrict__ pending,
+                                                   int32_t* __restrict__ pscores,
+                                                   const RotCache& cache,
+                                                   RunSplit split) {
   pdl_wait();
 
   const uint32_t n = st->n_children;
@@ -722,6 +757,13 @@ __global__ void branch_kernel(EpochState* st, Queue q, GridView G,
       cache_claim_run(cache, G, make_int4(ch.ix, ch.iy, ch.iz, ch.iroll),
                       make_int4(ch.ipitch, ch.iyaw, ch.level, ch.score));
   }
+}
+
+__global__ void branch_kernel(EpochState* st, Queue q, GridView G,
+                              const uint32_t* __restrict__ exp_parent,
+                              const uint32_t* __restrict__ exp_off, bbs_node* __restrict__ pending,
+                              int32_t* __restrict__ pscores, RotCache cache, RunSplit split) {
+  branch_kernel_body(st, q, G, exp_parent, exp_off, pending, pscores, cache, split);
 }
 
 constexpr int kST = 256;   // survivors: threads per tile
@@ -860,11 +902,13 @@ __device__ uint32_t warp_lookback(unsigned long long* tiles, uint32_t tile, uint
 // tiles take tickets in order and chain their prefix through `tiles`
 // (decoupled look-back; words tagged with the epoch so nothing is cleared).
 // Block 0's first warp also trims the queue remainder.
-__global__ void __launch_bounds__(kST) survivors_kernel(EpochState* st, Queue q, int strategy,
-                                                        const bbs_node* __restrict__ pending,
-                                                        const int32_t* __restrict__ scores,
-                                                        unsigned long long* __restrict__ s_key,
-                                                        unsigned long long* __restrict__ tiles) {
+__device__ __forceinline__ void survivors_kernel_body(EpochState* st,
+                                                      Queue q,
+                                                      int strategy,
+                                                      const bbs_node* __restrict__ pending,
+                                                      const int32_t* __restrict__ scores,
+                                                      unsigned long long* __restrict__ s_key,
+                                                      unsigned long long* __restrict__ tiles) {
   pdl_wait();
 
   using Load = cub::BlockLoad<int32_t, kST, kSIPT, cub::BLOCK_LOAD_WARP_TRANSPOSE>;
@@ -939,6 +983,14 @@ __global__ void __launch_bounds__(kST) survivors_kernel(EpochState* st, Queue q,
   }
 }
 
+__global__ void __launch_bounds__(kST) survivors_kernel(EpochState* st, Queue q, int strategy,
+                                                        const bbs_node* __restrict__ pending,
+                                                        const int32_t* __restrict__ scores,
+                                                        unsigned long long* __restrict__ s_key,
+                                                        unsigned long long* __restrict__ tiles) {
+  survivors_kernel_body(st, q, strategy, pending, scores, s_key, tiles);
+}
+
 
 // E4a, speculative round: survivors of EVERY formed epoch (each against its
 // own B) compacted in pending order -- the kept epochs' survivors are a
@@ -950,12 +1002,13 @@ __global__ void __launch_bounds__(kST) survivors_kernel(EpochState* st, Queue q,
 // earlier survivors) and commits the kept epochs into EpochState exactly as
 // the sequential loop would have (search.hpp:132-169).  The queue trim runs
 // in the next kernel (it needs the committed B and consumed count).
-__global__ void __launch_bounds__(kST) survivors_spec_kernel(EpochState* st, Queue q,
-                                                             const bbs_node* __restrict__ pending,
-                                                             const int32_t* __restrict__ scores,
-                                                             unsigned long long* __restrict__ s_key,
-                                                             unsigned long long* __restrict__ tiles,
-                                                             SpecRec* __restrict__ rec) {
+__device__ __forceinline__ void survivors_spec_kernel_body(EpochState* st,
+                                                           Queue q,
+                                                           const bbs_node* __restrict__ pending,
+                                                           const int32_t* __restrict__ scores,
+                                                           unsigned long long* __restrict__ s_key,
+                                                           unsigned long long* __restrict__ tiles,
+                                                           SpecRec* __restrict__ rec) {
   pdl_wait();
 
   using Load = cub::BlockLoad<int32_t, kST, kSIPT, cub::BLOCK_LOAD_WARP_TRANSPOSE>;
@@ -1130,13 +1183,23 @@ __global__ void __launch_bounds__(kST) survivors_spec_kernel(EpochState* st, Que
   }
 }
 
+__global__ void __launch_bounds__(kST) survivors_spec_kernel(EpochState* st, Queue q,
+                                                             const bbs_node* __restrict__ pending,
+                                                             const int32_t* __restrict__ scores,
+                                                             unsigned long long* __restrict__ s_key,
+                                                             unsigned long long* __restrict__ tiles,
+                                                             SpecRec* __restrict__ rec) {
+  survivors_spec_kernel_body(st, q, pending, scores, s_key, tiles, rec);
+}
+
 // E4b: order the survivors by key.  Keys are unique (they embed seq), so a
 // survivor's rank = #keys below it; ranks are computed against smem tiles.
 constexpr int kRT = 256;
-__global__ void __launch_bounds__(kRT) rank_sort_kernel(EpochState* st,
-                                                        const unsigned long long* __restrict__ key,
-                                                        unsigned long long* __restrict__ out_key,
-                                                        Queue q, int trim_strategy) {
+__device__ __forceinline__ void rank_sort_kernel_body(EpochState* st,
+                                                      const unsigned long long* __restrict__ key,
+                                                      unsigned long long* __restrict__ out_key,
+                                                      Queue q,
+                                                      int trim_strategy) {
   pdl_wait();
 
   __shared__ unsigned long long tile[kRT];
@@ -1160,6 +1223,13 @@ __global__ void __launch_bounds__(kRT) rank_sort_kernel(EpochState* st,
     }
     if (j < n) out_key[rank] = kj;
   }
+}
+
+__global__ void __launch_bounds__(kRT) rank_sort_kernel(EpochState* st,
+                                                        const unsigned long long* __restrict__ key,
+                                                        unsigned long long* __restrict__ out_key,
+                                                        Queue q, int trim_strategy) {
+  rank_sort_kernel_body(st, key, out_key, q, trim_strategy);
 }
 
 // E4b': large flushes (batch_size above kRankSortMax): the unused tail of
@@ -1216,8 +1286,10 @@ __device__ __forceinline__ uint32_t warp_merge_split(const RemView& A, uint32_t 
   return lo;
 }
 
-__global__ void __launch_bounds__(kMT) merge_kernel(EpochState* st, Queue q, int strategy,
-                                                    const unsigned long long* __restrict__ skey) {
+__device__ __forceinline__ void merge_kernel_body(EpochState* st,
+                                                  Queue q,
+                                                  int strategy,
+                                                  const unsigned long long* __restrict__ skey) {
   pdl_wait();
 
   __shared__ uint32_t s_lo[kMaxLevels], s_pre[kMaxLevels + 1];
@@ -1287,7 +1359,69 @@ __global__ void __launch_bounds__(kMT) merge_kernel(EpochState* st, Queue q, int
   }
 }
 
+__global__ void __launch_bounds__(kMT) merge_kernel(EpochState* st, Queue q, int strategy,
+                                                    const unsigned long long* __restrict__ skey) {
+  merge_kernel_body(st, q, strategy, skey);
+}
 
+
+
+// ---- co-batched flushes (bbs_search_scans) --------------------------------
+// One launch per epoch kernel for a group of searches: blockIdx.y = slot,
+// each slot's pointers and views in a device array.  The kernel bodies are
+// the single-search ones; a slot whose search has ended (or that holds no
+// search: a dummy state with active = 0) falls through them as a no-op.
+struct SlotArgs {
+  ScoreSlot sc;  // first: the score kernels read this prefix
+  EpochState* st;
+  Queue q;
+  uint32_t* exp_parent;
+  uint32_t* exp_off;
+  int32_t* trace;
+  unsigned long long trace_cap;
+  bbs_node* pending;
+  int32_t* pscores;
+  unsigned long long* s_key;
+  unsigned long long* s_key2;
+  unsigned long long* surv_tiles;
+  SpecRec* rec;
+  int k_max;
+  int spec;  // this round is speculative (BFS, from the search's second host check on)
+};
+
+__global__ void __launch_bounds__(kFT) frontier_group(const SlotArgs* __restrict__ ga, unsigned long long b,
+                                                      int strategy) {
+  const SlotArgs& a = ga[blockIdx.y];
+  uint32_t* ctl = a.sc.cache.enabled ? a.sc.cache.ctl : nullptr;
+  if (a.spec)
+    frontier_spec_kernel_body(a.st, a.q, a.sc.G, b, a.k_max, a.exp_parent, a.exp_off, a.trace, a.trace_cap, ctl,
+                              a.rec);
+  else
+    frontier_kernel_body(a.st, a.q, a.sc.G, b, a.exp_parent, a.exp_off, a.trace, a.trace_cap, strategy, ctl);
+}
+
+__global__ void branch_group(const SlotArgs* __restrict__ ga) {
+  const SlotArgs& a = ga[blockIdx.y];
+  branch_kernel_body(a.st, a.q, a.sc.G, a.exp_parent, a.exp_off, a.pending, a.pscores, a.sc.cache, RunSplit{});
+}
+
+__global__ void __launch_bounds__(kST) survivors_group(const SlotArgs* __restrict__ ga, int strategy) {
+  const SlotArgs& a = ga[blockIdx.y];
+  if (a.spec)
+    survivors_spec_kernel_body(a.st, a.q, a.pending, a.pscores, a.s_key, a.surv_tiles, a.rec);
+  else
+    survivors_kernel_body(a.st, a.q, strategy, a.pending, a.pscores, a.s_key, a.surv_tiles);
+}
+
+__global__ void __launch_bounds__(kRT) rank_sort_group(const SlotArgs* __restrict__ ga, int strategy) {
+  const SlotArgs& a = ga[blockIdx.y];
+  rank_sort_kernel_body(a.st, a.s_key, a.s_key2, a.q, a.spec ? strategy : -1);
+}
+
+__global__ void __launch_bounds__(kMT) merge_group(const SlotArgs* __restrict__ ga, int strategy) {
+  const SlotArgs& a = ga[blockIdx.y];
+  merge_kernel_body(a.st, a.q, strategy, a.s_key2);
+}
 
 // Exact mode: this rank's run scores back to their pending positions.
 __global__ void scatter_own_kernel(const EpochState* st, RunSplit split, int32_t* __restrict__ pscores) {
@@ -1765,6 +1899,225 @@ bbs_scan* upload_scan(bbs_map* m, const double* xyz, uint64_t k, bool sync) {
   return sc.release();
 }
 
+// ---- co-batched flushes: the group of searches ----------------------------
+// bbs_search_scans runs T searches on T host threads; each one's root batch
+// and queue build run on its own stream, then it joins the group and every
+// host check (E epochs) becomes a rendezvous: the last member to arrive
+// uploads the slots' arguments, launches ONE graph of E epochs whose kernels
+// cover every slot (blockIdx.y), and reads every member's EpochState back.
+// Members leave when their search ends; a thread's next search joins a free
+// slot (continuous batching).  The epoch kernels are the single-search
+// bodies, so every result equals the search's own (tests/test_search_gpu.py).
+struct SearchGroup {
+  int device = 0;
+  uint32_t n_slots = 0;
+  int strategy = 0;
+  unsigned long long b = 0;
+  int E = 8;
+  MapView map{};
+  std::mutex mu;
+  std::condition_variable cv;
+  uint32_t members = 0, arrived = 0;
+  uint64_t gen = 0;
+  std::vector<uint32_t> free_slots;
+  std::vector<char> present;
+  std::vector<cudaEvent_t> arrive_ev;
+  std::vector<std::pair<const EpochState*, EpochState*>> readback;
+  SlotArgs* h_args = nullptr;   // the members' current arguments
+  SlotArgs* h_stage = nullptr;  // pinned copy the step's upload reads (members may rewrite h_args
+                                // before the upload executes on the device)
+  SlotArgs* d_args = nullptr;
+  SlotArgs dummy{};
+  EpochState* d_dummy = nullptr;
+  cudaStream_t gs = nullptr;
+  cudaEvent_t done = nullptr;
+  cudaGraphExec_t gexec = nullptr;
+  std::exception_ptr err;
+  uint64_t steps = 0;
+
+  int debug = 0;  // BBS_DEBUG_GROUP=1: no graph, a checked sync after every kernel; 2: after every step
+  void check(const char* what) {
+    if (debug != 1) return;
+    const cudaError_t e = cudaStreamSynchronize(gs);
+    if (e != cudaSuccess) {
+      std::fprintf(stderr, "[group] step %llu: %s failed: %s\n", static_cast<unsigned long long>(steps), what,
+                   cudaGetErrorString(e));
+      for (uint32_t i = 0; i < n_slots; ++i)
+        std::fprintf(stderr, "[group]  slot %u: st %p present %d k_max %d cache %d stg %d\n", i,
+                     static_cast<void*>(h_args[i].st), present[i], h_args[i].k_max, h_args[i].sc.cache.enabled,
+                     h_args[i].sc.cache.stg_level);
+      throw Error(BBS_ERR_CUDA, "search group: kernel failed");
+    }
+  }
+  void enqueue_epoch() {
+    const uint32_t n = n_slots;
+    launch_pdl(frontier_group, dim3(1, n), kFT, 0, gs, static_cast<const SlotArgs*>(d_args), b, strategy);
+    BBS_CUDA(cudaGetLastError());
+    check("frontier");
+    launch_pdl(branch_group, dim3(per_slot(148 * 16, n), n), 256, 0, gs, static_cast<const SlotArgs*>(d_args));
+    BBS_CUDA(cudaGetLastError());
+    check("branch");
+    launch_epoch_score_group(map, reinterpret_cast<const ScoreSlot*>(d_args), sizeof(SlotArgs), n, gs);
+    check("score kernels");
+    launch_pdl(survivors_group, dim3(per_slot(148 * 4, n), n), kST, 0, gs, static_cast<const SlotArgs*>(d_args),
+               strategy);
+    BBS_CUDA(cudaGetLastError());
+    check("survivors");
+    launch_pdl(rank_sort_group, dim3(per_slot(148 * 16, n), n), kRT, 0, gs, static_cast<const SlotArgs*>(d_args),
+               strategy);
+    BBS_CUDA(cudaGetLastError());
+    check("rank_sort");
+    launch_pdl(merge_group, dim3(per_slot(148 * 8, n), n), kMT, 0, gs, static_cast<const SlotArgs*>(d_args), strategy);
+    BBS_CUDA(cudaGetLastError());
+    check("merge");
+  }
+
+  // the last arrival (lock held): one graph of E epochs over every slot
+  void coordinate() {
+    try {
+      for (uint32_t i = 0; i < n_slots; ++i)
+        if (present[i]) {
+          if (debug == 3) BBS_CUDA(cudaEventSynchronize(arrive_ev[i]));
+          BBS_CUDA(cudaStreamWaitEvent(gs, arrive_ev[i], 0));
+        }
+      // h_stage is free again: the previous upload ran before the previous
+      // step's `done`, which every member still in the group has waited for
+      std::memcpy(h_stage, h_args, n_slots * sizeof(SlotArgs));
+      BBS_CUDA(cudaMemcpyAsync(d_args, h_stage, n_slots * sizeof(SlotArgs), cudaMemcpyHostToDevice, gs));
+      if (debug == 1) {
+        for (int e = 0; e < E; ++e) enqueue_epoch();
+      } else if (!gexec) {
+        cudaGraph_t graph;
+        BBS_CUDA(cudaStreamBeginCapture(gs, cudaStreamCaptureModeRelaxed));
+        for (int e = 0; e < E; ++e) enqueue_epoch();
+        BBS_CUDA(cudaStreamEndCapture(gs, &graph));
+        const cudaError_t r = cudaGraphInstantiate(&gexec, graph, 0);
+        cudaGraphDestroy(graph);
+        BBS_CUDA(r);
+      }
+      if (debug != 1) BBS_CUDA(cudaGraphLaunch(gexec, gs));
+      if (debug == 2) {
+        debug = 1;
+        check("graph");
+        debug = 2;
+      }
+      for (uint32_t i = 0; i < n_slots; ++i)
+        if (present[i])
+          BBS_CUDA(cudaMemcpyAsync(readback[i].second, readback[i].first, sizeof(EpochState), cudaMemcpyDeviceToHost,
+                                   gs));
+      BBS_CUDA(cudaEventRecord(done, gs));
+      ++steps;
+    } catch (...) {
+      err = std::current_exception();
+    }
+    arrived = 0;
+    std::fill(present.begin(), present.end(), 0);
+    ++gen;
+    cv.notify_all();
+  }
+
+  uint32_t join() {
+    std::unique_lock<std::mutex> lk(mu);
+    if (err) std::rethrow_exception(err);
+    if (free_slots.empty()) throw Error(BBS_ERR_GENERIC, "search group: no free slot");
+    const uint32_t slot = free_slots.back();
+    free_slots.pop_back();
+    ++members;
+    return slot;
+  }
+
+  void leave(uint32_t slot) {
+    std::unique_lock<std::mutex> lk(mu);
+    h_args[slot] = dummy;
+    free_slots.push_back(slot);
+    --members;
+    if (arrived > 0 && arrived == members) coordinate();
+  }
+
+  // E epochs of this member's search (with every other member's); on return
+  // *h_dst holds its state after them
+  void step(uint32_t slot, const SlotArgs& a, cudaStream_t member_stream, const EpochState* d_src, EpochState* h_dst) {
+    BBS_CUDA(cudaEventRecord(arrive_ev[slot], member_stream));
+    std::unique_lock<std::mutex> lk(mu);
+    if (err) std::rethrow_exception(err);
+    h_args[slot] = a;
+    readback[slot] = {d_src, h_dst};
+    present[slot] = 1;
+    const uint64_t my = gen;
+    if (++arrived == members)
+      coordinate();
+    else
+      cv.wait(lk, [&] { return gen != my; });
+    if (err) std::rethrow_exception(err);
+    lk.unlock();
+    BBS_CUDA(cudaEventSynchronize(done));  // no later step can start before this member arrives again
+  }
+
+  void release() {
+    if (gexec) cudaGraphExecDestroy(gexec);
+    for (auto e : arrive_ev) cudaEventDestroy(e);
+    if (done) cudaEventDestroy(done);
+    if (gs) cudaStreamDestroy(gs);
+    if (h_args) cudaFreeHost(h_args);
+    if (h_stage) cudaFreeHost(h_stage);
+    if (d_args) cudaFree(d_args);
+    if (d_dummy) cudaFree(d_dummy);
+  }
+};
+
+thread_local SearchGroup* g_group = nullptr;
+
+SearchGroup* group_create(bbs_map* m, const bbs_search_config& cfg, uint32_t n_slots) {
+  DeviceGuard dg(m->device);
+  std::unique_ptr<SearchGroup> g(new SearchGroup());
+  struct Rel {
+    SearchGroup* g;
+    ~Rel() {
+      if (g) g->release();
+    }
+  } rel{g.get()};
+  g->device = m->device;
+  g->n_slots = n_slots;
+  g->strategy = cfg.strategy;
+  g->b = cfg.batch_size;
+  g->map = m->view;
+  if (const char* v = std::getenv("BBS_DEBUG_GROUP")) g->debug = std::atoi(v);
+  if (const char* v = std::getenv("BBS_GROUP_E")) g->E = std::max(1, std::atoi(v));
+  g->present.assign(n_slots, 0);
+  g->readback.assign(n_slots, {nullptr, nullptr});
+  for (uint32_t i = 0; i < n_slots; ++i) g->free_slots.push_back(n_slots - 1 - i);
+  BBS_CUDA(cudaStreamCreateWithFlags(&g->gs, cudaStreamNonBlocking));
+  BBS_CUDA(cudaEventCreateWithFlags(&g->done, cudaEventDisableTiming));
+  g->arrive_ev.resize(n_slots);
+  for (auto& e : g->arrive_ev) BBS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  BBS_CUDA(cudaMallocHost(reinterpret_cast<void**>(&g->h_args), n_slots * sizeof(SlotArgs)));
+  BBS_CUDA(cudaMallocHost(reinterpret_cast<void**>(&g->h_stage), n_slots * sizeof(SlotArgs)));
+  BBS_CUDA(cudaMalloc(reinterpret_cast<void**>(&g->d_args), n_slots * sizeof(SlotArgs)));
+  // a slot without a search: an ended state, no cache, no children
+  BBS_CUDA(cudaMalloc(reinterpret_cast<void**>(&g->d_dummy), sizeof(EpochState)));
+  BBS_CUDA(cudaMemset(g->d_dummy, 0, sizeof(EpochState)));
+  g->dummy.st = g->d_dummy;
+  g->dummy.sc.d_n = reinterpret_cast<const uint32_t*>(reinterpret_cast<char*>(g->d_dummy) +
+                                                      offsetof(EpochState, n_children));
+  g->dummy.sc.n_ptiles = 1;
+  g->dummy.sc.cache.enabled = 0;
+  g->dummy.sc.cache.stg_level = -1;
+  g->dummy.k_max = 1;
+  for (uint32_t i = 0; i < n_slots; ++i) g->h_args[i] = g->dummy;
+  rel.g = nullptr;
+  return g.release();
+}
+
+void group_destroy(SearchGroup* g) {
+  if (!g) return;
+  {
+    DeviceGuard dg(g->device);
+    if (g->gs) cudaStreamSynchronize(g->gs);
+    g->release();
+  }
+  delete g;
+}
+
 // search(), search.hpp:72-186, on the device.  `shard` may be null;
 // `stream` null = the map's stream (concurrent searches use their own).
 // NVTX range for profilers (nsys / ncu --nvtx); free when no tool is attached.
@@ -2171,7 +2524,7 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
 
   // survivors >= threshold among own roots, in initial_nodes order
   const bool dbg_spec = std::getenv("BBS_DEBUG_SPEC") != nullptr;  // per-round state (stderr)
-  const int E = (host_x || dump || dbg_spec) ? 1 : 8;  // epochs per host check
+  const int E = (host_x || dump || dbg_spec) ? 1 : (g_group ? g_group->E : 8);  // epochs per host check
   unsigned long long root_probes = 0;
   int n_root_surv = 0;       // host path only
   unsigned long long* surv_idx = nullptr;
@@ -2504,6 +2857,30 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
     BBS_CUDA(cudaEventRecord(W.block_ev, s));
     BBS_CUDA(cudaEventSynchronize(W.block_ev));
   };
+  // co-batched flushes (bbs_search_scans): a qualifying search runs its
+  // epochs inside the group's launches (SearchGroup), else on its own stream
+  SearchGroup* grp = g_group;
+  if (grp && (shard || dump || dbg_phases || dbg_spec || !rank_sorted || strategy != grp->strategy ||
+              cfg.batch_size != grp->b || E != grp->E))
+    grp = nullptr;
+  struct Member {
+    SearchGroup* g = nullptr;
+    uint32_t slot = 0;
+    void leave() {
+      if (g) g->leave(slot);
+      g = nullptr;
+    }
+    ~Member() { leave(); }
+  } member;
+  if (grp && self_active) {
+    // the group waits for this search's stream at every step: its root batch
+    // and queue build finish first, so a joiner never stalls the others
+    BBS_CUDA(cudaStreamSynchronize(s));
+    member.slot = grp->join();
+    member.g = grp;
+  }
+  const auto t_loop = std::chrono::steady_clock::now();
+  uint64_t group_checks = 0;
   tmark("loop");
   while (self_active || others_active) {
     // capacity: the queue grows by at most pend_cap per epoch
@@ -2526,7 +2903,33 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
     const int n_ep = (self_active || roots_dev_x) ? E : 1;
     NvtxRange nv_epochs("bbs::flush epochs");  // search.hpp:145-169, n_ep flushes per host check
     // graphs pay off for long searches (capture + instantiate ~0.2 ms)
-    if (n_ep == E && E > 1 && pass_ms.size() >= graph_after && !dbg_phases) {
+    if (member.g) {
+      SlotArgs sa{};
+      sa.sc.G = gv;
+      sa.sc.scan = sv;
+      sa.sc.cache = cache;
+      sa.sc.nodes = pending;
+      sa.sc.d_n = d_nchild;
+      sa.sc.scores = pscores;
+      sa.sc.n_ptiles = spec_on ? ptiles_round : ptiles_epoch;
+      sa.st = d_st;
+      sa.q = q;
+      sa.exp_parent = exp_parent;
+      sa.exp_off = exp_off;
+      sa.trace = d_trace;
+      sa.trace_cap = trace_cap;
+      sa.pending = pending;
+      sa.pscores = pscores;
+      sa.s_key = s_key;
+      sa.s_key2 = s_key2;
+      sa.surv_tiles = surv_tiles;
+      sa.rec = d_rec;
+      sa.k_max = spec_k;
+      sa.spec = spec_on ? 1 : 0;
+      member.g->step(member.slot, sa, s, d_st, W.h_st);
+      launches += 6ull * E;
+      ++group_checks;
+    } else if (n_ep == E && E > 1 && pass_ms.size() >= graph_after && !dbg_phases) {
       if (!batch_ok || batch_qcap != qcap || batch_pool != q.pool || batch_builds != builds_live ||
           batch_spec != spec_on) {
         cudaGraph_t graph;
@@ -2563,10 +2966,20 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
     } else {
       for (int e = 0; e < n_ep; ++e) enqueue_epoch(e);
     }
-    BBS_CUDA(cudaMemcpyAsync(W.h_st, d_st, sizeof(EpochState), cudaMemcpyDeviceToHost, s));
+    if (!member.g) {
+      BBS_CUDA(cudaMemcpyAsync(W.h_st, d_st, sizeof(EpochState), cudaMemcpyDeviceToHost, s));
+      host_wait();
+    }
     d2h += sizeof(EpochState);
-    host_wait();
+    // in the group the epochs are not timed one by one: host time since the
+    // loop began stands for every pass of the check
+    const float t_check =
+        std::chrono::duration<float, std::milli>(std::chrono::steady_clock::now() - t_loop).count();
     for (int e = 0; e < n_ep; ++e) {
+      if (member.g) {
+        pass_ms.push_back(t_check);
+        continue;
+      }
       pass_ms.push_back(elapsed(ev_loop, ev_pass[e]));
       esm += elapsed(ev_s0[e], ev_s1[e]);
       if (dbg_phases) {
@@ -2623,6 +3036,7 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
     else
       others_active = roots_dev_x && hs.any_active != 0;
   }
+  member.leave();  // the other members stop waiting for this one
   cudaEvent_t ev_end = W.next_event();
   BBS_CUDA(cudaEventRecord(ev_end, s));
   if (dbg_phases && total > 0) {
@@ -2738,6 +3152,7 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
     std::fprintf(stderr, " us (device %.1f us)\n", 1e3 * out->device_ms);
   }
   out->kernel_launches = launches;
+  out->group_checks = group_checks;
   for (int l = 0; l < kMaxLevels; ++l) out->evals_per_level[l] = hs.level_evals[l];
   out->evals_per_level[L] += n_scored_roots;  // the root batch
   int32_t best = hs.best;

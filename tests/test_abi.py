@@ -64,7 +64,7 @@ def test_struct_sizes(B):
 
 def test_abi_version(B):
     from paper_2310_10023_b200 import _lib
-    assert B.lib.bbs_abi_version() == _lib.ABI_VERSION == 4
+    assert B.lib.bbs_abi_version() == _lib.ABI_VERSION == 5
 
 
 def test_search_config_defaults_match_reference(B):

@@ -177,10 +177,11 @@ def _c2_map(B, m):
     return _C2_MAP["vm"]
 
 
-def test_c4_scans_match_reference(B):
+def test_c4_scans_match_reference(B, monkeypatch):
     """C4 (BASELINE configs[3]): 64 scans of the C2 map; the device search of
     scans 0, 8, ..., 56 equals the reference's search(), alone and inside the
-    throughput path (bbs_search_scans, all 64 in flight)."""
+    throughput path (bbs_search_scans, 16 in flight: per-search graphs on
+    their own streams, and co-batched flushes)."""
     if not has("c4_search.json"):
         pytest.skip("c4 golden not generated")
     g = golden_json("c4_search.json")
@@ -194,9 +195,12 @@ def test_c4_scans_match_reference(B):
     ds = [B.DeviceScan(vm, s) for s in scans]
     for j in C4_PICK:
         assert_same_search(B.search_scan(vm, ds[j], cfg), g["searches"][str(j)], f"c4 scan {j}")
-    many = B.search_scans(vm, ds, cfg, concurrency=16, trace_capacity=1 << 16)
-    for j in C4_PICK:
-        assert_same_search(many[j], g["searches"][str(j)], f"c4 scan {j} (search_scans)")
+    for cobatch in ("0", "1"):
+        monkeypatch.setenv("BBS_COBATCH", cobatch)
+        many = B.search_scans(vm, ds, cfg, concurrency=16, trace_capacity=1 << 16)
+        for j in C4_PICK:
+            assert_same_search(many[j], g["searches"][str(j)], f"c4 scan {j} (search_scans, co-batched {cobatch})")
+        assert (sum(r.group_checks for r in many) > 0) == (cobatch == "1")
 
 
 @pytest.fixture(scope="module")

@@ -304,23 +304,35 @@ def test_large_scan_paths_are_transparent(B, golden_scenes, monkeypatch):
     assert s.shape[0] > 65535
 
 
-def test_search_scans_throughput_mode_matches_single_searches(B):
-    """bbs_search_scans (native workers, one stream each, workspaces leased
-    concurrently) returns each scan's search() result."""
+@pytest.mark.parametrize("strategy", ["BFS", "DFS"])
+@pytest.mark.parametrize("cobatch", ["1", "0"])
+def test_search_scans_throughput_mode_matches_single_searches(B, monkeypatch, strategy, cobatch):
+    """bbs_search_scans (native workers, workspaces leased concurrently; the
+    flushes of the searches in flight co-batched into one launch per epoch
+    kernel, or each search on its own stream) returns each scan's search()
+    result: Stats, trace, pose."""
+    monkeypatch.setenv("BBS_COBATCH", cobatch)
     spec = H.SceneSpec.default(size_x=24.0, size_y=24.0, size_z=10.0, num_boxes=4, min_box_side=2.5,
                                max_box_side=6.0, min_box_height=3.0, map_spacing=0.3,
                                scan_spacing=0.45, scan_range=14.0, min_scan_points=300)
     m, _, _ = H.gen_scene(spec, 42)
-    scans, _ = H.gen_scans(spec, 42, 1000, 6)
+    scans, _ = H.gen_scans(spec, 42, 1000, 9)
     vm = B.MultiResVoxelMap.build(m, 0.5, 3)
     ds = [B.DeviceScan(vm, s) for s in scans]
-    cfg = B.SearchConfig(min_resolution=0.5, max_level=3, batch_size=400, collect_trace=True)
+    cfg = B.SearchConfig(min_resolution=0.5, max_level=3, batch_size=400, collect_trace=True,
+                         strategy=getattr(B.Strategy, strategy))
     many = B.search_scans(vm, ds, cfg, concurrency=4, trace_capacity=1 << 12)
     for d, r in zip(ds, many):
         one = B.search_scan(vm, d, cfg)
         assert (r.best_score, r.best_pose.as_tuple(), r.stats.nodes_generated, r.stats.nodes_pruned,
-                r.best_score_trace) == (one.best_score, one.best_pose.as_tuple(), one.stats.nodes_generated,
-                                        one.stats.nodes_pruned, one.best_score_trace)
+                r.stats.batches_flushed, r.best_score_trace) == (
+                    one.best_score, one.best_pose.as_tuple(), one.stats.nodes_generated, one.stats.nodes_pruned,
+                    one.stats.batches_flushed, one.best_score_trace)
+        assert one.group_checks == 0
+    if cobatch == "1":
+        assert sum(r.group_checks for r in many) > 0
+    else:
+        assert all(r.group_checks == 0 for r in many)
 
 
 @pytest.mark.parametrize("strategy", ["BFS", "DFS"])
