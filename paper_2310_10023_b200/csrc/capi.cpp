@@ -413,8 +413,13 @@ int bbs_search_scans(bbs_map_t map, const bbs_scan_t* scans, uint64_t n, const b
       const char* e = std::getenv("BBS_COBATCH");
       return e && e[0] == '1';
     }();
-    std::unique_ptr<bbs::SearchGroup, void (*)(bbs::SearchGroup*)> group(
-        cobatch ? bbs::group_create(map, *cfg, static_cast<uint32_t>(T)) : nullptr, bbs::group_destroy);
+    // BBS_GROUPS=g: g independent groups (own streams) of T/g searches each
+    int n_groups = 1;
+    if (const char* e = std::getenv("BBS_GROUPS")) n_groups = std::max(1, std::min(T, std::atoi(e)));
+    std::vector<std::unique_ptr<bbs::SearchGroup, void (*)(bbs::SearchGroup*)>> groups;
+    for (int i = 0; cobatch && i < n_groups; ++i)
+      groups.emplace_back(bbs::group_create(map, *cfg, static_cast<uint32_t>((T + n_groups - 1) / n_groups)),
+                          bbs::group_destroy);
     std::vector<cudaStream_t> streams(static_cast<size_t>(T));
     for (auto& st : streams) BBS_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
     std::atomic<uint64_t> next{0};
@@ -427,7 +432,7 @@ int bbs_search_scans(bbs_map_t map, const bbs_scan_t* scans, uint64_t n, const b
           bbs::DeviceGuard wg(map->device);
           bbs::g_grid_share = share;
           bbs::g_blocking_sync = blocking;
-          bbs::g_group = group.get();
+          bbs::g_group = groups.empty() ? nullptr : groups[static_cast<size_t>(t) % groups.size()].get();
           for (uint64_t j = next++; j < n; j = next++)
             bbs::run_search(map, scans[j], *cfg, nullptr, &results[j], streams[static_cast<size_t>(t)]);
         } catch (...) {
