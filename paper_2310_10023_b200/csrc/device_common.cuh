@@ -65,6 +65,14 @@ __device__ __forceinline__ bool level_contains(const LevelView& L, int32_t x, in
   }
 }
 
+// 32-bit load from a shared-memory byte address (ld.shared, no generic
+// address conversion)
+__device__ __forceinline__ uint32_t lds_u32(uint32_t addr) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+  return v;
+}
+
 // Programmatic dependent launch (launch_pdl): wait for the preceding grid
 // (complete, memory visible) before reading its output; let the next grid
 // launch once every CTA of this one has started.  No-ops without PDL.

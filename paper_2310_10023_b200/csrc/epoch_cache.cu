@@ -730,9 +730,8 @@ void launch_epoch_score(const MapView& map, const GridView& grid, const ScanView
   unsigned gp = g;
   if (win_smem > 0) {
     // persistent: each CTA stages the window once
-    int per_sm = 1;
-    BBS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cache_probe_kernel, kProbeThreads, win_smem));
-    gp = std::min<unsigned>(g, share_cap(148ull * static_cast<unsigned>(std::max(per_sm, 1))));
+    const int per_sm = ctas_per_sm(cache_probe_kernel, kProbeThreads, win_smem);
+    gp = std::min<unsigned>(g, share_cap(148ull * static_cast<unsigned>(per_sm)));
   }
   static const uint32_t hipw = [] {
     const char* v = std::getenv("BBS_PROBE_HIPW");  // A/B: 2x the warp items per warp
@@ -761,9 +760,8 @@ void launch_epoch_score_group(const MapView& map, const ScoreSlot* slots, size_t
   launch_pdl(cache_build_group, dim3(per_slot(148 * 2, n_slots), n_slots), kBuildThreads, build_smem, s, map, slots,
              stride);
   BBS_CUDA(cudaGetLastError());
-  int per_sm = 1;
-  BBS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cache_probe_group, kProbeThreads, probe_smem));
-  launch_pdl(cache_probe_group, dim3(per_slot(148u * static_cast<unsigned>(std::max(per_sm, 1)), n_slots, 4), n_slots),
+  const int per_sm = ctas_per_sm(cache_probe_group, kProbeThreads, probe_smem);
+  launch_pdl(cache_probe_group, dim3(per_slot(148u * static_cast<unsigned>(per_sm), n_slots, 4), n_slots),
              kProbeThreads, probe_smem, s, map, slots, stride, hipw);
   BBS_CUDA(cudaGetLastError());
   launch_score_cube8_group(map, slots, stride, n_slots, s);

@@ -40,6 +40,15 @@ struct StreamAllocs {
 // filling every SM (the epoch kernels are latency-bound at C4's sizes).
 extern thread_local unsigned g_grid_share;
 extern thread_local bool g_blocking_sync;  // host checks wait on a blocking-sync event
+// cudaOccupancyMaxActiveBlocksPerMultiprocessor, memoised per (device,
+// kernel, block, shared memory): the query costs ~10 us of host time and the
+// search loop asks the same questions every flush
+int ctas_per_sm(const void* kernel, int threads, int smem);
+template <typename K>
+int ctas_per_sm(K* kernel, int threads, int smem) {
+  return ctas_per_sm(reinterpret_cast<const void*>(kernel), threads, smem);
+}
+
 inline unsigned share_cap(uint64_t cap) {
   const uint64_t c = cap / (g_grid_share ? g_grid_share : 1u);
   return static_cast<unsigned>(c < 16 ? 16 : c);

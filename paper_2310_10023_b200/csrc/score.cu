@@ -553,8 +553,8 @@ constexpr int kRootListCap = 4096;  // dense root box: touched cells listed (bey
 
 // One histogram entry (f, cnt) of root_hist_kernel, appended warp-cooperatively
 // (every lane calls; has = false for lanes without an entry).  Staged mode
-// (root_colpad_kernel): (padded column offset << 8 | z shift + 8) words in
-// groups of 4 with their counts packed as bytes (counts > 255 split),
+// (root_colpad_kernel): (padded column byte offset << 8 | z shift + 8) words
+// in groups of 4 with their counts packed as bytes (counts > 255 split),
 // dropping entries whose z never meets a translation's column; otherwise plain
 // (fx, fy, fz, count).
 __device__ __forceinline__ void root_emit(bool has, int32_t fx, int32_t fy, int32_t fz, int32_t cnt,
@@ -582,7 +582,7 @@ __device__ __forceinline__ void root_emit(bool has, int32_t fx, int32_t fy, int3
   at = __shfl_sync(0xffffffffu, at, 0) + incl - parts;
   if (!parts) return;
   if (st.enabled) {
-    const uint32_t word = (static_cast<uint32_t>(fy * static_cast<int32_t>(st.pitch) + fx) << 8) |
+    const uint32_t word = (static_cast<uint32_t>(4 * (fy * static_cast<int32_t>(st.pitch) + fx)) << 8) |
                           static_cast<uint32_t>(sh + 8);
     int32_t* g = reinterpret_cast<int32_t*>(ent4);
     unsigned char* wb = reinterpret_cast<unsigned char*>(ent4);
@@ -606,6 +606,7 @@ __global__ void __launch_bounds__(512) root_hist_kernel(GridView grid, ScanView 
   int32_t* s_cnt = reinterpret_cast<int32_t*>(s_key + kHistSlots);          // 32 KB
   uint32_t* s_w = reinterpret_cast<uint32_t*>(smem);  // dense box: 16-bit counters (overlays the hash)
   __shared__ int s_distinct, s_namb, s_nent, s_skip, s_badpad, s_total, s_nl;
+  __shared__ typename cub::BlockScan<int, 512>::TempStorage s_rscan;
   const uint32_t nrot = bp.nr * bp.np * bp.nw;
   const int lane = threadIdx.x & 31;
   // dense box (coarse root levels): direct-mapped counters, no probing
@@ -803,6 +804,34 @@ __global__ void __launch_bounds__(512) root_hist_kernel(GridView grid, ScanView 
         reinterpret_cast<unsigned char*>(g)[((e >> 2) * 8 + 4) * 4 + (e & 3)] = 0;
       }
     }
+    if (!over && st.enabled) {
+      // counts still to come from each group on (suffix sums, in the .y of
+      // the group's count word): the column kernel's survivor bound reads
+      // them instead of subtracting every group's counts as it goes
+      __syncthreads();  // the padding group is complete
+      constexpr int kPer = (kColGroupCap + 511) / 512;
+      const int n_grp = (s_nent + 3) >> 2;
+      int32_t* g = reinterpret_cast<int32_t*>(h.entries + static_cast<uint64_t>(slot) * kHistCap);
+      // thread t holds groups n_grp - 1 - (t * kPer + k): a forward scan over
+      // the reversed order is the suffix sum
+      int v[kPer], sum = 0;
+#pragma unroll
+      for (int k = 0; k < kPer; ++k) {
+        const int r = static_cast<int>(threadIdx.x) * kPer + k;
+        const int i = n_grp - 1 - r;
+        v[k] = i >= 0 ? static_cast<int>(__dp4a(static_cast<uint32_t>(g[i * 8 + 4]), 0x01010101u, 0u)) : 0;
+        sum += v[k];
+      }
+      int excl;
+      cub::BlockScan<int, 512>(s_rscan).ExclusiveSum(sum, excl);
+#pragma unroll
+      for (int k = 0; k < kPer; ++k) {
+        const int r = static_cast<int>(threadIdx.x) * kPer + k;
+        const int i = n_grp - 1 - r;
+        excl += v[k];
+        if (i >= 0) g[i * 8 + 5] = excl;
+      }
+    }
     if (threadIdx.x == 0) {
       h.n_ent[slot] = over ? 0 : s_nent;
       h.n_amb[slot] = over ? 0 : s_namb;
@@ -913,7 +942,8 @@ __global__ void __launch_bounds__(256) root_col_kernel(GridView grid, ScanView s
 // bytes.  Per group: 4 LDS + 4 funnel shifts give each entry's z-translation
 // bits, 3 PRMT pack their low bytes, and per z-translation j one LOP3 keeps
 // bit j of every byte and one IDP4A adds 2^j * sum(count) of the hits.
-constexpr int kGrpTile = 1024;  // groups per shared-memory tile (16 KB + 4 KB)
+constexpr int kGrpTile = 1024;  // groups per shared-memory tile (16 KB + 4 KB + 0.5 KB)
+constexpr int kColPadHead = kGrpTile * 20 + kGrpTile / 2;  // shared memory before the window
 #ifndef BBS_COLPAD_MINB
 #define BBS_COLPAD_MINB 3  // <= 80 registers, no spills: 3 CTAs per SM (C2 root batch -13 us; 4 spills)
 #endif
@@ -927,7 +957,8 @@ __global__ void __launch_bounds__(256, BBS_COLPAD_MINB) root_colpad_kernel(GridV
   extern __shared__ __align__(16) unsigned char smem[];
   int4* s_go = reinterpret_cast<int4*>(smem);                     // group offsets/shifts
   uint32_t* s_gw = reinterpret_cast<uint32_t*>(s_go + kGrpTile);  // group counts (bytes)
-  uint32_t* s_col = s_gw + kGrpTile;
+  int32_t* s_rem = reinterpret_cast<int32_t*>(s_gw + kGrpTile);   // counts still to come, every 8th group
+  uint32_t* s_col = reinterpret_cast<uint32_t*>(s_rem + kGrpTile / 8);
   const uint32_t nrot = bp.nr * bp.np * bp.nw;
   const uint32_t dimx = L.dim[0], dimy = L.dim[1];
   for (uint32_t i = threadIdx.x; i < st.pitch * st.rows; i += blockDim.x) {
@@ -970,40 +1001,44 @@ __global__ void __launch_bounds__(256, BBS_COLPAD_MINB) root_colpad_kernel(GridV
     // best of this column's z-translations cannot reach the threshold, its
     // exact value is unobservable (search.hpp:117-123 only counts the root
     // as pruned) and the column stops early; entries come heaviest first.
-    int rem = h.total[slot] + n_amb;
+    // the translation's own column as a shared-memory byte address: an
+    // entry's word is one add away (offsets are stored in bytes)
+    const uint32_t col_b = static_cast<uint32_t>(__cvta_generic_to_shared(s_col)) + 4u * static_cast<uint32_t>(base);
     bool done = !valid;
     for (int t0 = 0; t0 < n_grp; t0 += kGrpTile) {
       const int tn = min(kGrpTile, n_grp - t0);
       __syncthreads();
       for (int i = threadIdx.x; i < tn; i += blockDim.x) {
         s_go[i] = grp[2 * (t0 + i)];
-        s_gw[i] = static_cast<uint32_t>(grp[2 * (t0 + i) + 1].x);
+        const int4 w = grp[2 * (t0 + i) + 1];
+        s_gw[i] = static_cast<uint32_t>(w.x);
+        if ((i & 7) == 0) s_rem[i >> 3] = w.y;  // root_hist_kernel's suffix sum
       }
       __syncthreads();
-#pragma unroll 2
-      for (int g = 0; g < tn && !done; ++g) {
+      int g = 0;
+#pragma unroll 4
+      for (; !done && g < tn; ++g) {
         if ((g & 7) == 0 && g) {
           uint32_t best = 0;
 #pragma unroll
           for (int j = 0; j < NZ; ++j) best = max(best, acc[j] >> j);
-          if (static_cast<int>(best) + rem < bp.threshold) {
+          if (static_cast<int>(best) + s_rem[g >> 3] + n_amb < bp.threshold) {
             done = true;
             break;
           }
         }
         const int4 o = s_go[g];
         const uint32_t w4 = s_gw[g];
-        n_words += 4;
-        rem -= static_cast<int>(__dp4a(w4, 0x01010101u, 0u));  // this group's counts
-        // shift amounts ride in the low 5 bits (wrap funnel shift)
-        const uint32_t b0 = __funnelshift_r(s_col[base + (o.x >> 8)], 0u, static_cast<uint32_t>(o.x));
-        const uint32_t b1 = __funnelshift_r(s_col[base + (o.y >> 8)], 0u, static_cast<uint32_t>(o.y));
-        const uint32_t b2 = __funnelshift_r(s_col[base + (o.z >> 8)], 0u, static_cast<uint32_t>(o.z));
-        const uint32_t b3 = __funnelshift_r(s_col[base + (o.w >> 8)], 0u, static_cast<uint32_t>(o.w));
+        // byte offsets above the low 8 bits, shift amounts in the low 5 (wrap funnel shift)
+        const uint32_t b0 = __funnelshift_r(lds_u32(col_b + static_cast<uint32_t>(o.x >> 8)), 0u, static_cast<uint32_t>(o.x));
+        const uint32_t b1 = __funnelshift_r(lds_u32(col_b + static_cast<uint32_t>(o.y >> 8)), 0u, static_cast<uint32_t>(o.y));
+        const uint32_t b2 = __funnelshift_r(lds_u32(col_b + static_cast<uint32_t>(o.z >> 8)), 0u, static_cast<uint32_t>(o.z));
+        const uint32_t b3 = __funnelshift_r(lds_u32(col_b + static_cast<uint32_t>(o.w >> 8)), 0u, static_cast<uint32_t>(o.w));
         const uint32_t x = __byte_perm(__byte_perm(b0, b1, 0x0040), __byte_perm(b2, b3, 0x0040), 0x5410);
 #pragma unroll
         for (int j = 0; j < NZ; ++j) acc[j] = __dp4a(x & (0x01010101u << j), w4, acc[j]);
       }
+      n_words += 4u * static_cast<uint32_t>(g);
     }
     int res[NZ];
 #pragma unroll
@@ -1126,16 +1161,14 @@ void launch_score_box_chunked(const MapView& map, const GridView& grid, const Sc
 }
 
 int colpad_ctas_per_sm(uint32_t nz, int smem) {
-  int n = 1;
   switch (nz) {
-#define BBS_OCC(NZ_)                                                                               \
-  case NZ_:                                                                                        \
-    BBS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, root_colpad_kernel<NZ_>, 256, smem)); \
-    break;
+#define BBS_OCC(NZ_) \
+  case NZ_:          \
+    return ctas_per_sm(root_colpad_kernel<NZ_>, 256, smem);
     BBS_OCC(1) BBS_OCC(2) BBS_OCC(3) BBS_OCC(4) BBS_OCC(5) BBS_OCC(6) BBS_OCC(7) BBS_OCC(8)
 #undef BBS_OCC
   }
-  return std::max(n, 1);
+  return 1;
 }
 
 void launch_score_roots(const MapView& map, const GridView& grid, const ScanView& scan,
@@ -1165,7 +1198,7 @@ void launch_score_roots(const MapView& map, const GridView& grid, const ScanView
                                   kEntTile * 16 + col_stage_max));
 #define BBS_COLPAD_ATTR(NZ_)                                                                      \
   BBS_CUDA(cudaFuncSetAttribute(root_colpad_kernel<NZ_>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                                kGrpTile * 20 + kColPadMax));
+                                kColPadHead + kColPadMax));
     BBS_COLPAD_ATTR(1) BBS_COLPAD_ATTR(2) BBS_COLPAD_ATTR(3) BBS_COLPAD_ATTR(4) BBS_COLPAD_ATTR(5)
     BBS_COLPAD_ATTR(6) BBS_COLPAD_ATTR(7) BBS_COLPAD_ATTR(8)
 #undef BBS_COLPAD_ATTR
@@ -1197,7 +1230,7 @@ void launch_score_roots(const MapView& map, const GridView& grid, const ScanView
       st.dimz = L.dim[2];
     }
   }
-  const int pad_smem = kGrpTile * 20 + static_cast<int>(st.pitch * st.rows * 4);
+  const int pad_smem = kColPadHead + static_cast<int>(st.pitch * st.rows * 4);
   uint32_t P, x0r;
   BoxParams b0 = bp;
   b0.rank = 0;
@@ -1243,9 +1276,36 @@ void launch_score_roots(const MapView& map, const GridView& grid, const ScanView
   }
 }
 
+int ctas_per_sm(const void* kernel, int threads, int smem) {
+  struct Key {
+    int dev;
+    const void* k;
+    int threads, smem;
+  };
+  static std::mutex mu;
+  static std::vector<std::pair<Key, int>> memo;
+  int dev = 0;
+  BBS_CUDA(cudaGetDevice(&dev));
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    for (const auto& e : memo)
+      if (e.first.dev == dev && e.first.k == kernel && e.first.threads == threads && e.first.smem == smem)
+        return e.second;
+  }
+  int n = 1;
+  BBS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kernel, threads, static_cast<size_t>(smem)));
+  n = std::max(n, 1);
+  std::lock_guard<std::mutex> lk(mu);
+  memo.push_back({Key{dev, kernel, threads, smem}, n});
+  return n;
+}
+
 bool pdl_enabled() {
-  const char* v = std::getenv("BBS_PDL");
-  return !(v && v[0] == '0');
+  static const bool on = [] {
+    const char* v = std::getenv("BBS_PDL");
+    return !(v && v[0] == '0');
+  }();
+  return on;
 }
 
 void launch_score_cube8(const MapView& map, const GridView& grid, const ScanView& scan,

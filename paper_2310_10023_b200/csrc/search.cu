@@ -2326,6 +2326,7 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
       *eps1 = 1.0 - *eps;
     }
   };
+  tmark("box");
   dense_box(m->view.level[L].cell, bp.tmax, &bp.dn_r, &bp.dn_zlo, &bp.dn_nz, &bp.dn_eps, &bp.dn_eps1);
   // parity dump: no survivor-bound early exit in the root column kernel
   if (dump && dump->exact_roots) bp.threshold = INT32_MIN;
@@ -2372,6 +2373,7 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
     rinit.ctl = W.rinit_ctl.get(kRCtlHist + 512, s);
     BBS_CUDA(cudaMemsetAsync(rinit.ctl, 0, (kRCtlHist + 512) * sizeof(uint32_t), s));
   }
+  tmark("root setup");
   cudaEvent_t ev_col0 = W.next_event(), ev_col1 = W.next_event();
   bool col_timed = false;
   BBS_CUDA(cudaEventRecord(ev_roots0, s));
