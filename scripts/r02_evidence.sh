@@ -2,7 +2,7 @@
 # Round-2 evidence refresh: GPU tests, bench lines (C2 default, C1, C3, C4,
 # reference arm), C2 launch list with DRAM traffic, ncu --set full of the
 # dominant C2 kernel and the C3 speculative-round kernels.
-O=gpurun_out/r02x
+O=gpurun_out/${EVID:-r02x}
 mkdir -p $O
 timeout 1500 python -m pytest tests -m gpu -q -p no:cacheprovider > $O/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $O/pytest_gpu.log
 python __graft_entry__.py > $O/smoke.log 2>&1; echo "smoke rc=$?" >> $O/smoke.log
@@ -10,6 +10,8 @@ python bench.py > $O/bench_c2.json 2> $O/bench_c2.err
 python bench.py --config c1 --steps 5 --no-cpu-baseline > $O/bench_c1.json 2> $O/bench_c1.err
 python bench.py --config c3 --steps 3 --no-cpu-baseline > $O/bench_c3.json 2> $O/bench_c3.err
 python bench.py --config c4 --steps 3 --no-cpu-baseline > $O/bench_c4.json 2> $O/bench_c4.err
+BBS_COBATCH=1 BBS_GROUPS=4 python bench.py --config c4 --steps 3 --no-cpu-baseline > $O/bench_c4_cobatch.json 2> $O/bench_c4_cobatch.err
+for cb in 0 1; do BBS_COBATCH=$cb BBS_GROUPS=4 C4_N=64 C4_SHARES=0 C4_CONCS=8,16,32 python scripts/c4_probe.py > $O/c4_probe_cobatch$cb.log 2>&1; done
 python bench.py --impl reference --steps 3 > $O/bench_reference.json 2> $O/bench_reference.err
 BBS_DEBUG_PHASES=1 python scripts/profile_search.py --config c2 --searches 2 > $O/c2_phases.log 2>&1
 BBS_DEBUG_PHASES=1 python scripts/profile_search.py --config c3 --searches 1 > $O/c3_phases.log 2>&1
