@@ -163,8 +163,10 @@ void launch_score_runs8(const MapView& map, const GridView& grid, const ScanView
 // for the flush batches (epoch_cache.cu).  info[slot] = {state, pool offset,
 // entries, ambiguous points}; slot = base[level] + dense rotation id.
 constexpr int32_t kCacheEmpty = -1, kCacheBuilding = -2, kCacheNone = -3, kCacheReady = 0;
-constexpr int kCacheCtl = 4 + kMaxLevels + 1;  // ... + [20] largest histogram (entries)
-constexpr int kCtlMaxEnt = 4 + kMaxLevels;
+constexpr int kCtlMaxEnt = 4 + kMaxLevels;      // [20] largest histogram (entries)
+constexpr int kCtlDirect = kCtlMaxEnt + 1;      // [21] runs branch listed as direct this flush
+constexpr int kCtlDirectItem = kCtlDirect + 1;  // [22] direct-run work items taken (probe kernel)
+constexpr int kCacheCtl = kCtlDirectItem + 1;
 constexpr int kCacheDenseCells = 48 * 1024;  // 96 KB of 16-bit counters
 constexpr int kStageWindowMax = 96 * 1024;   // bytes of the probe's staged column window
 struct RotCache {
@@ -178,6 +180,13 @@ struct RotCache {
   uint32_t* ctl;               // [kCacheCtl] pool used, amb used, builds this flush,
                                // fallback runs this flush, then per-level "raw" flags
   uint32_t* fb_runs;           // [max runs] runs the cube kernel scores (not cached)
+  // direct runs (single searches; null in co-batched launches): runs that can
+  // have no histogram this flush (uncached or given-up level, failed
+  // rotation) are listed by the branch kernel and scored by the probe
+  // kernel's CTAs after their histogram items, instead of by the cube kernel
+  // after the probe
+  uint32_t* direct_runs;       // [max runs]
+  uint8_t* direct_flag;        // [max runs] 1: the run is in direct_runs
   // dense-histogram box per level (dn_r = 0: hash build): offsets in
   // [-r, r]^2 x [zlo, zlo + nz), two 16-bit counts per shared word
   int32_t dn_r[kMaxLevels], dn_zlo[kMaxLevels], dn_nz[kMaxLevels];

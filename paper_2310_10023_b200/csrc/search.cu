@@ -291,6 +291,8 @@ __device__ __forceinline__ void frontier_kernel_body(EpochState* st,
   if (tid == 0 && cache_ctl) {
     cache_ctl[2] = 0;  // builds claimed this flush
     cache_ctl[3] = 0;  // runs listed for the cube kernel
+    cache_ctl[kCtlDirect] = 0;
+    cache_ctl[kCtlDirectItem] = 0;
     uint32_t raw = 0;
     for (int l = 0; l < kMaxLevels; ++l) raw |= cache_ctl[4 + l] ? 1u << l : 0u;
     st->cache_raw = raw;  // lets the host stop launching empty build kernels
@@ -645,6 +647,8 @@ __device__ __forceinline__ void frontier_spec_kernel_body(EpochState* st,
   if (cache_ctl) {
     cache_ctl[2] = 0;  // builds claimed this flush
     cache_ctl[3] = 0;  // runs listed for the cube kernel
+    cache_ctl[kCtlDirect] = 0;
+    cache_ctl[kCtlDirectItem] = 0;
     uint32_t raw = 0;
     for (int l = 0; l < kMaxLevels; ++l) raw |= cache_ctl[4 + l] ? 1u << l : 0u;
     st->cache_raw = raw;
@@ -752,10 +756,22 @@ __device__ __forceinline__ void branch_kernel_body(EpochState* st,
       pscores[i] = 0;  // the flush kernels accumulate into it
     }
     // first child of a run (8 translation siblings): claim its rotation's
-    // histogram slot (epoch_cache.cu)
-    if (cache.enabled && t == 0 && own)
-      cache_claim_run(cache, G, make_int4(ch.ix, ch.iy, ch.iz, ch.iroll),
-                      make_int4(ch.ipitch, ch.iyaw, ch.level, ch.score));
+    // histogram slot (epoch_cache.cu), or list the run as direct when it can
+    // have no histogram this flush
+    if (cache.enabled && t == 0 && own) {
+      const int4 ra = make_int4(ch.ix, ch.iy, ch.iz, ch.iroll), rb = make_int4(ch.ipitch, ch.iyaw, ch.level, ch.score);
+      if (cache.direct_flag) {
+        // the run's index in the array the score kernels read (exact mode:
+        // this rank's compact copy)
+        const uint32_t r = split.world ? (i >> 3) / split.world : (i >> 3);
+        const bool direct = run_is_direct(cache, G, ra, rb);
+        cache.direct_flag[r] = direct ? 1 : 0;
+        if (direct) cache.direct_runs[atomicAdd(&cache.ctl[kCtlDirect], 1u)] = r;
+        if (!direct) cache_claim_run(cache, G, ra, rb);
+      } else {
+        cache_claim_run(cache, G, ra, rb);
+      }
+    }
   }
 }
 
@@ -1771,7 +1787,8 @@ struct Workspace {
   Buf<uint32_t> perm0, perm1, sk0, sk1, exp_parent, exp_off;
   Buf<int32_t> pscores, trace, hist_n, pscores_own, xchg;
   Buf<int4> hist_ent, cache_info, cache_pool, cache_builds;
-  Buf<uint32_t> cache_u32, cache_amb, cache_fb, stage_win;
+  Buf<uint32_t> cache_u32, cache_amb, cache_fb, stage_win, cache_direct;
+  Buf<unsigned char> cache_dflag;
   Buf<int32_t> cache_builds_w;
   Buf<uint32_t> hist_amb, rinit_ctl;
   Buf<unsigned long long> rinit_tiles;
@@ -1814,6 +1831,8 @@ struct Workspace {
     cache_u32.release();
     cache_amb.release();
     cache_fb.release();
+    cache_direct.release();
+    cache_dflag.release();
     stage_win.release();
     cache_builds_w.release();
     st.release();
@@ -2483,6 +2502,15 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
       cache.builds = W.cache_builds.get(mr, s);
       cache.builds_w = W.cache_builds_w.get(mr, s);
       cache.fb_runs = W.cache_fb.get(mr, s);
+      // runs that can have no histogram are scored in the probe kernel's
+      // direct phase (BBS_DIRECT_RUNS=0: by the cube kernel after the probe)
+      if ([] {
+            const char* v = std::getenv("BBS_DIRECT_RUNS");
+            return !(v && v[0] == '0');
+          }()) {
+        cache.direct_runs = W.cache_direct.get(mr, s);
+        cache.direct_flag = W.cache_dflag.get(mr, s);
+      }
       if (cache.stg_level >= 0) {
         uint32_t* win = W.stage_win.get(((static_cast<size_t>(cache.stg_pitch) * cache.stg_rows + 3) & ~size_t(3)), s);
         build_stage_window(m->view, cache, win, s);
@@ -2741,6 +2769,15 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
   // (E single epochs): short searches (C2: 7 flushes, survivors that overtake
   // the next prefix every flush) keep the plain epoch chain
   bool spec_on = false;
+  // direct runs (scored in the probe kernel's last phase) only in
+  // speculative rounds: their probes carry enough histogram work to hide
+  // them (C3 13.8 -> 13.3 ms), while a plain C2 epoch's probe is too short
+  // and its 2 CTAs per SM score them slower than the cube kernel's 4
+  // (C2 0.83 -> 0.88 ms)
+  RotCache cache_plain = cache;
+  cache_plain.direct_runs = nullptr;
+  cache_plain.direct_flag = nullptr;
+  auto epoch_cache = [&]() -> const RotCache& { return spec_on ? cache : cache_plain; };
   auto enqueue_epoch = [&](int e) {
     if (spec_on)
       launch_pdl(frontier_spec_kernel, 1, kFT, 0, s, d_st, q, gv, cfg.batch_size, spec_k, exp_parent, exp_off,
@@ -2751,12 +2788,12 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
     BBS_CUDA(cudaGetLastError());
     record(ev_pass[e]);
     launch_pdl(branch_kernel, grid1(pend_cap), 256, 0, s, d_st, q, gv, exp_parent, exp_off, pending, pscores,
-               cache, split);
+               epoch_cache(), split);
     BBS_CUDA(cudaGetLastError());
     record(ev_s0[e]);
     if (exact) {
       launch_epoch_score(m->view, gv, sv, split.pending_own, d_nchild, static_cast<uint32_t>(pend_epoch),
-                         ptiles_epoch, split.pscores_own, cache, s, builds_live);
+                         ptiles_epoch, split.pscores_own, cache_plain, s, builds_live);
       record(ev_s1[e]);
       launch_pdl(scatter_own_kernel, grid1(pend_cap), 256, 0, s, d_st, split, pscores);
       BBS_CUDA(cudaGetLastError());
@@ -2764,7 +2801,7 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
       xmax(pscores, pend_cap);  // every rank: every score of the flush
     } else {
       launch_epoch_score(m->view, gv, sv, pending, d_nchild, static_cast<uint32_t>(spec_on ? pend_cap : pend_epoch),
-                         spec_on ? ptiles_round : ptiles_epoch, pscores, cache, s, builds_live);
+                         spec_on ? ptiles_round : ptiles_epoch, pscores, epoch_cache(), s, builds_live);
       record(ev_s1[e]);
     }
     if (spec_on)  // survivors of the round + validation + commit of the kept epochs
@@ -2909,7 +2946,7 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
       SlotArgs sa{};
       sa.sc.G = gv;
       sa.sc.scan = sv;
-      sa.sc.cache = cache;
+      sa.sc.cache = epoch_cache();
       sa.sc.nodes = pending;
       sa.sc.d_n = d_nchild;
       sa.sc.scores = pscores;
