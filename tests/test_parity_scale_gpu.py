@@ -213,15 +213,18 @@ def c3(B):
     return vm, s
 
 
-def test_c3_search_matches_reference(B, c3):
+@pytest.mark.parametrize("direct", ["1", "0"])
+def test_c3_search_matches_reference(B, c3, direct, monkeypatch):
     """C3 city (BASELINE configs[2]): 30M map points, K = 30k, 7 levels,
     +-5 deg roll/pitch: search() equals the reference's (score, pose, Stats,
-    trace)."""
+    trace) -- with the speculative rounds' direct runs scored in the probe
+    kernel (default) and by the cube kernel after it."""
+    monkeypatch.setenv("BBS_DIRECT_RUNS", direct)
     vm, s = c3
     want = golden_json("c3_search.json")["bfs_roto_b10000"]
     assert digest(s) == want["scan_digest"]
     res = B.search(vm, s, search_cfg(B, C3))
-    assert_same_search(res, want, "c3")
+    assert_same_search(res, want, f"c3 (direct runs {direct})")
 
 
 def test_c3_batches_match_reference(B, c3):
