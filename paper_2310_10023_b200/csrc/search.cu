@@ -2428,11 +2428,14 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
   RotCache cache{};
   cache.stg_level = -1;
   cache.pre_level = -1;
-  // a histogram build costs about one direct run; small scans (C1: K = 2000)
-  // rarely amortize it, large ones (C2/C3) reuse rotations across flushes
+  // a histogram build costs about one direct run, so small scans do not
+  // amortize it; measured crossover (C1 room / C2 campus maps, device ms
+  // with / without the cache): K 1000 2.17 / 1.66, 1500 2.43 / 1.98, 2000
+  // 1.61 / 2.04, 3000 2.47 / 4.04, 5000 2.62 / 5.53; C2 K 1000 1.60 / 1.19,
+  // K 3000 0.78 / 0.91
   const uint64_t cache_min_k = [] {
     const char* v = std::getenv("BBS_CACHE_MIN_K");  // A/B timing
-    return v ? static_cast<uint64_t>(std::atoll(v)) : uint64_t(4096);
+    return v ? static_cast<uint64_t>(std::atoll(v)) : uint64_t(2000);
   }();
   if (cache_on && K >= cache_min_k) {
     uint64_t slots = 0;

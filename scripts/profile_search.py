@@ -8,8 +8,11 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--searches", type=int, default=3)
 ap.add_argument("--config", default="c2")
 ap.add_argument("--layout", default="auto")
+ap.add_argument("--k", type=int, default=0, help="override the scan size K")
 a = ap.parse_args()
-cfgd = bench.CONFIGS[a.config]
+cfgd = dict(bench.CONFIGS[a.config])
+if a.k:
+    cfgd["K"] = a.k
 m, s, gt = bench.build_inputs(cfgd)
 vm = B.MultiResVoxelMap.build(m, cfgd["r"], cfgd["max_level"], layout=B.Layout[a.layout.upper()])
 ds = B.DeviceScan(vm, s)
