@@ -460,6 +460,7 @@ __device__ __forceinline__ void cache_probe_kernel_body(const RotCache& c,
   const uint32_t n_runs = *d_n / 8;
   const int lane = threadIdx.x & 31;
   const uint64_t n_warps = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
+  const bool direct_on = c.direct_flag && (!c.direct_gate || *c.direct_gate);
   // warp items = (run, chunk of the run's histogram): as few chunks per run
   // as keep ~2 items per warp (each item ends in 8 warp reductions and
   // atomics), sized by the largest histogram built so far
@@ -494,7 +495,7 @@ __device__ __forceinline__ void cache_probe_kernel_body(const RotCache& c,
         chunk = static_cast<uint32_t>(item % chunks_per_run);
         a = __ldg(reinterpret_cast<const int4*>(pending) + 16ull * run);
         b = __ldg(reinterpret_cast<const int4*>(pending) + 16ull * run + 1);
-        direct = c.direct_flag && c.direct_flag[run];  // scored by the direct phase below
+        direct = direct_on && c.direct_flag[run];  // scored by the direct phase below
         if (!direct && run_slot(c, G, a, b, &slot)) {
           inf = c.info[slot];
           has = inf.x == kCacheReady &&
@@ -619,7 +620,7 @@ __device__ __forceinline__ void cache_probe_kernel_body(const RotCache& c,
   // finish their histogram items early take more of them (these runs no
   // longer wait for a cube kernel after the probe)
   // (CTA items: warp items of 256 points measured slower, C3 13.57 vs 13.34 ms)
-  const uint32_t n_dir = c.direct_runs ? c.ctl[kCtlDirect] : 0u;
+  const uint32_t n_dir = direct_on ? c.ctl[kCtlDirect] : 0u;
   if (n_dir) {
     __shared__ double s_R[9];
     __shared__ int32_t s_hdr[4], s_cnt[8];

@@ -187,6 +187,7 @@ struct RotCache {
   // after the probe
   uint32_t* direct_runs;       // [max runs]
   uint8_t* direct_flag;        // [max runs] 1: the run is in direct_runs
+  const uint32_t* direct_gate; // non-null: direct runs only while *direct_gate (the search's spec_mode)
   // dense-histogram box per level (dn_r = 0: hash build): offsets in
   // [-r, r]^2 x [zlo, zlo + nz), two 16-bit counts per shared word
   int32_t dn_r[kMaxLevels], dn_zlo[kMaxLevels], dn_nz[kMaxLevels];

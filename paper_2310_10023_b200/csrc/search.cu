@@ -73,6 +73,8 @@ struct EpochState {
   uint32_t spec_acc;       // ... of which the validation accepted (a prefix)
   uint32_t spec_k;         // epochs the next round may form (adaptive, 1..spec_kmax)
   uint32_t spec_kmax;
+  uint32_t spec_mode;       // device-switched rounds (spec_auto): 1 = this epoch is a speculative round
+  uint32_t spec_votes;      // consecutive plain epochs whose next epoch a round would have kept
   unsigned long long level_evals[kMaxLevels];  // flush evaluations per level
   // kept ranges of the remainder: one per key segment (BFS: 1, DFS: level)
   uint32_t seg_lo[kMaxLevels], seg_len[kMaxLevels], seg_pre[kMaxLevels + 1];
@@ -760,7 +762,7 @@ __device__ __forceinline__ void branch_kernel_body(EpochState* st,
     // have no histogram this flush
     if (cache.enabled && t == 0 && own) {
       const int4 ra = make_int4(ch.ix, ch.iy, ch.iz, ch.iroll), rb = make_int4(ch.ipitch, ch.iyaw, ch.level, ch.score);
-      if (cache.direct_flag) {
+      if (cache.direct_flag && (!cache.direct_gate || *cache.direct_gate)) {
         // the run's index in the array the score kernels read (exact mode:
         // this rank's compact copy)
         const uint32_t r = split.world ? (i >> 3) / split.world : (i >> 3);
@@ -1305,7 +1307,8 @@ __device__ __forceinline__ uint32_t warp_merge_split(const RemView& A, uint32_t 
 __device__ __forceinline__ void merge_kernel_body(EpochState* st,
                                                   Queue q,
                                                   int strategy,
-                                                  const unsigned long long* __restrict__ skey) {
+                                                  const unsigned long long* __restrict__ skey,
+                                                  int vote = 0) {
   pdl_wait();
 
   __shared__ uint32_t s_lo[kMaxLevels], s_pre[kMaxLevels + 1];
@@ -1323,6 +1326,12 @@ __device__ __forceinline__ void merge_kernel_body(EpochState* st,
   const uint32_t n_s = st->n_surv;
   const RemView A{q.keys(cur) + st->n_cons, s_lo, s_pre, strategy == BBS_STRATEGY_BFS};
   unsigned long long* __restrict__ ok = q.keys(cur ^ 1u);
+  // the vote's two keys, loaded before the merge work (inputs, unchanged by it)
+  unsigned long long vote_s = 0, vote_a = 0;
+  if (vote && threadIdx.x == 0 && !st->spec_mode && n_s && n_keep) {
+    vote_s = __ldcg(skey);
+    vote_a = A[min(st->n_cons, n_keep) - 1u];
+  }
   const uint32_t total = n_keep + n_s;
   const uint32_t warp = threadIdx.x >> 5;
   for (uint32_t d0 = blockIdx.x * kMTile; d0 < total; d0 += gridDim.x * kMTile) {
@@ -1371,6 +1380,16 @@ __device__ __forceinline__ void merge_kernel_body(EpochState* st,
       st->q_peak = max(st->q_peak, len);
       if (len == 0) st->active = 0;
       st->merge_done = 0;
+      if (vote && !st->spec_mode) {
+        // would a speculative round have kept the next epoch?  It is formed
+        // from the remainder alone; the survivors displace it when the
+        // smallest survivor key precedes the remainder entry it would pop
+        // last (estimated at this epoch's pop count)
+        bool keep = n_s == 0;
+        if (n_s && n_keep) keep = vote_s > vote_a;
+        st->spec_votes = keep ? st->spec_votes + 1u : 0u;
+        if (st->spec_votes >= static_cast<uint32_t>(vote)) st->spec_mode = 1u;
+      }
     }
   }
 }
@@ -1378,6 +1397,57 @@ __device__ __forceinline__ void merge_kernel_body(EpochState* st,
 __global__ void __launch_bounds__(kMT) merge_kernel(EpochState* st, Queue q, int strategy,
                                                     const unsigned long long* __restrict__ skey) {
   merge_kernel_body(st, q, strategy, skey);
+}
+
+// ---- device-switched speculative rounds (BFS, single searches) -------------
+// Every epoch of a batch runs these kernels; each takes the plain or the
+// speculative body by st->spec_mode.  Plain epochs vote: the merge kernel's
+// finalising CTA turns speculation on once two consecutive epochs show that
+// a round would have kept their successor.  A search whose survivors keep
+// overtaking the next prefix (C2: 7 flushes) never switches; long searches
+// switch after their first epochs instead of after a whole host check.
+__global__ void __launch_bounds__(kFT) frontier_auto_kernel(EpochState* st, Queue q, GridView G,
+                                                            unsigned long long b, int k_max,
+                                                            uint32_t* __restrict__ exp_parent,
+                                                            uint32_t* __restrict__ exp_off,
+                                                            int32_t* __restrict__ trace,
+                                                            unsigned long long trace_cap, int strategy,
+                                                            uint32_t* __restrict__ cache_ctl,
+                                                            SpecRec* __restrict__ rec) {
+  pdl_wait();
+  __shared__ uint32_t s_mode;
+  if (threadIdx.x == 0) s_mode = st->spec_mode;
+  __syncthreads();
+  if (s_mode)
+    frontier_spec_kernel_body(st, q, G, b, k_max, exp_parent, exp_off, trace, trace_cap, cache_ctl, rec);
+  else
+    frontier_kernel_body(st, q, G, b, exp_parent, exp_off, trace, trace_cap, strategy, cache_ctl);
+}
+
+__global__ void __launch_bounds__(kST) survivors_auto_kernel(EpochState* st, Queue q, int strategy,
+                                                             const bbs_node* __restrict__ pending,
+                                                             const int32_t* __restrict__ scores,
+                                                             unsigned long long* __restrict__ s_key,
+                                                             unsigned long long* __restrict__ tiles,
+                                                             SpecRec* __restrict__ rec) {
+  pdl_wait();
+  if (st->spec_mode)
+    survivors_spec_kernel_body(st, q, pending, scores, s_key, tiles, rec);
+  else
+    survivors_kernel_body(st, q, strategy, pending, scores, s_key, tiles);
+}
+
+__global__ void __launch_bounds__(kRT) rank_sort_auto_kernel(EpochState* st,
+                                                             const unsigned long long* __restrict__ key,
+                                                             unsigned long long* __restrict__ out_key, Queue q,
+                                                             int strategy) {
+  pdl_wait();
+  rank_sort_kernel_body(st, key, out_key, q, st->spec_mode ? strategy : -1);
+}
+
+__global__ void __launch_bounds__(kMT) merge_auto_kernel(EpochState* st, Queue q, int strategy,
+                                                         const unsigned long long* __restrict__ skey, int votes) {
+  merge_kernel_body(st, q, strategy, skey, votes);
 }
 
 
@@ -2771,7 +2841,13 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
   // speculative rounds start once the search outlives its first host check
   // (E single epochs): short searches (C2: 7 flushes, survivors that overtake
   // the next prefix every flush) keep the plain epoch chain
-  bool spec_on = false;
+  // BBS_SPEC_AFTER=n (A/B): speculative rounds from the (n+1)-th host check
+  const int spec_after = [] {
+    const char* v = std::getenv("BBS_SPEC_AFTER");
+    return v ? std::max(0, std::atoi(v)) : 1;
+  }();
+  int checks_done = 0;
+  bool spec_on = spec_after == 0 && spec_k > 1;
   // direct runs (scored in the probe kernel's last phase) only in
   // speculative rounds: their probes carry enough histogram work to hide
   // them (C3 13.8 -> 13.3 ms), while a plain C2 epoch's probe is too short
@@ -2781,7 +2857,52 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
   cache_plain.direct_runs = nullptr;
   cache_plain.direct_flag = nullptr;
   auto epoch_cache = [&]() -> const RotCache& { return spec_on ? cache : cache_plain; };
+  // device-switched rounds (frontier_auto_kernel ...): BFS single searches
+  // with rank-sorted survivors; the host-switched schedule otherwise
+  // (BBS_SPEC_AUTO=0: plain epochs for the first host check, then rounds)
+  const bool spec_auto = spec_k > 1 && rank_sorted && !exact && !dbg_spec && [] {
+    const char* v = std::getenv("BBS_SPEC_AUTO");
+    return !(v && v[0] == '0');
+  }();
+  const int spec_votes_needed = [] {
+    const char* v = std::getenv("BBS_SPEC_VOTES");  // consecutive plain epochs voting for rounds
+    return v ? std::max(1, std::atoi(v)) : 2;
+  }();
+  RotCache cache_auto = cache;
+  cache_auto.direct_gate =
+      reinterpret_cast<const uint32_t*>(reinterpret_cast<const char*>(d_st) + offsetof(EpochState, spec_mode));
+  auto enqueue_auto_epoch = [&](int e) {
+    launch_pdl(frontier_auto_kernel, 1, kFT, 0, s, d_st, q, gv, cfg.batch_size, spec_k, exp_parent, exp_off, d_trace,
+               trace_cap, strategy, cache.enabled ? cache.ctl : nullptr, d_rec);
+    BBS_CUDA(cudaGetLastError());
+    record(ev_pass[e]);
+    launch_pdl(branch_kernel, grid1(pend_cap), 256, 0, s, d_st, q, gv, exp_parent, exp_off, pending, pscores,
+               cache_auto, split);
+    BBS_CUDA(cudaGetLastError());
+    record(ev_s0[e]);
+    launch_epoch_score(m->view, gv, sv, pending, d_nchild, static_cast<uint32_t>(pend_cap), ptiles_round, pscores,
+                       cache_auto, s, builds_live);
+    record(ev_s1[e]);
+    launch_pdl(survivors_auto_kernel, surv_grid, kST, 0, s, d_st, q, strategy, static_cast<const bbs_node*>(pending),
+               static_cast<const int32_t*>(pscores), s_key, surv_tiles, d_rec);
+    BBS_CUDA(cudaGetLastError());
+    if (dbg_phases) record(ev_dbg[3 * e]);
+    launch_pdl(rank_sort_auto_kernel, grid1(pend_cap, kRT), kRT, 0, s, d_st,
+               static_cast<const unsigned long long*>(s_key), s_key2, q, strategy);
+    BBS_CUDA(cudaGetLastError());
+    if (dbg_phases) record(ev_dbg[3 * e + 1]);
+    launch_pdl(merge_auto_kernel,
+               static_cast<unsigned>(std::min<uint64_t>((qcap + kMTile - 1) / kMTile, share_cap(148ull * 8))), kMT, 0,
+               s, d_st, q, strategy, static_cast<const unsigned long long*>(s_key2), spec_votes_needed);
+    BBS_CUDA(cudaGetLastError());
+    if (dbg_phases) record(ev_dbg[3 * e + 2]);
+    launches += 6;
+  };
   auto enqueue_epoch = [&](int e) {
+    if (spec_auto && !roots_dev_x) {
+      enqueue_auto_epoch(e);
+      return;
+    }
     if (spec_on)
       launch_pdl(frontier_spec_kernel, 1, kFT, 0, s, d_st, q, gv, cfg.batch_size, spec_k, exp_parent, exp_off,
                  d_trace, trace_cap, cache.enabled ? cache.ctl : nullptr, d_rec);
@@ -3072,7 +3193,9 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
     }
     self_active = hs.active != 0;
     builds_live = (claimable & ~hs.cache_raw) != 0;  // raw flags only ever get set
-    spec_on = spec_k > 1;  // from the second host check on
+    // host-switched rounds from the second host check on (device-switched
+    // searches keep the same batch graph)
+    spec_on = !(spec_auto && !member.g) && spec_k > 1 && ++checks_done >= spec_after;
     if (roots_host_x)
       exchange();
     else
@@ -3191,7 +3314,8 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
     tmark("results");
     std::fprintf(stderr, "[host]");
     for (const auto& m : th) std::fprintf(stderr, " %s %.1f", m.first, m.second);
-    std::fprintf(stderr, " us (device %.1f us)\n", 1e3 * out->device_ms);
+    std::fprintf(stderr, " us (device %.1f us; frontier passes %u, rounds on %u, votes %u)\n", 1e3 * out->device_ms,
+                 hs.pass, hs.spec_mode, hs.spec_votes);
   }
   out->kernel_launches = launches;
   out->group_checks = group_checks;

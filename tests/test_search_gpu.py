@@ -352,14 +352,20 @@ def test_large_batch_uses_radix_sorted_survivors(B, ref, golden_scenes, strategy
     assert got.best_score_trace == trace
 
 
-@pytest.mark.parametrize("spec", ["1", "2", "5", "16"])
+@pytest.mark.parametrize("spec", ["1", "2", "5", "16", "16-host", "16-votes1"])
 @pytest.mark.parametrize("name", ["small", "room"])
 def test_speculative_rounds_match_reference(B, golden_scenes, name, spec, monkeypatch):
     """Speculative flush rounds (BFS; frontier_spec_kernel + survivors_spec_
-    kernel, from the second host check on): any round depth gives the
-    reference's search() exactly -- score, pose, Stats, incumbent trace --
-    on searches with many flushes (small b=7: ~1.9k flushes; room: 73)."""
-    monkeypatch.setenv("BBS_SPEC", spec)
+    kernel): any round depth gives the reference's search() exactly -- score,
+    pose, Stats, incumbent trace -- on searches with many flushes (small b=7:
+    ~1.9k flushes; room: 73), with the rounds switched on by the device votes
+    (default; after one vote) or by the host after its first check."""
+    depth, _, mode = spec.partition("-")
+    monkeypatch.setenv("BBS_SPEC", depth)
+    if mode == "host":
+        monkeypatch.setenv("BBS_SPEC_AUTO", "0")
+    if mode == "votes1":
+        monkeypatch.setenv("BBS_SPEC_VOTES", "1")
     m, s, _, sc = load_case(B, golden_scenes, name)
     vm = B.MultiResVoxelMap.build(m, sc["r"], sc["max_level"])
     for label, want in golden_json(f"{name}_search.json").items():
