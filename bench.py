@@ -577,6 +577,12 @@ def run_b200_arm(args, cfgd):
                                              "l1tex_throughput_pct", "ipc_active", "achieved_occupancy_pct",
                                              "source")},
         "traffic_source": "profiles/ncu_traffic.json (dram__bytes_read.sum + dram__bytes_write.sum per launch)",
+        # the bound that actually limits it: instruction issue (4 schedulers
+        # per SM, one instruction each per cycle)
+        "issue": {"ipc_active": col_prof.get("ipc_active"), "peak_ipc": 4.0,
+                  "frac": (col_prof["ipc_active"] / 4.0) if col_prof.get("ipc_active") else None,
+                  "note": "ncu issued IPC per active SM over the 4-wide issue peak: ~8 instructions per "
+                          "gathered word (LDS, funnel shift, byte permute, LOP3 + IDP4A per z-translation)"},
         "context": {"hbm_copy_gbs": peaks.get("hbm_gbs"), "hbm_peak_source": f"MEASURED_PEAKS.json ({peak_kind})",
                     "l2_random_sector_gather_gbs": gather_l2, "hbm_random_sector_gather_gbs": gather_hbm,
                     "survey_lookup_model": {
