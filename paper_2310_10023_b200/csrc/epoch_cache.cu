@@ -68,7 +68,8 @@ constexpr uint32_t kEarlyAbortPoints = 2048;  // sample before judging a build's
 __device__ __forceinline__ void cache_build_kernel_body(const RotCache& c,
                                                         const MapView& map,
                                                         const GridView& G,
-                                                        ScanView scan) {
+                                                        ScanView scan,
+                                                        uint32_t n_fixed) {
   pdl_wait();
 
   extern __shared__ __align__(16) unsigned char smem[];
@@ -81,7 +82,8 @@ __device__ __forceinline__ void cache_build_kernel_body(const RotCache& c,
   __shared__ int s_distinct, s_namb, s_oob, s_nl;
   __shared__ uint32_t s_off, s_aoff;
   const int lane = threadIdx.x & 31;
-  const uint32_t n_build = c.ctl[2];
+  // the flush's claimed builds (ctl[2]), or a fixed list (the prebuild)
+  const uint32_t n_build = n_fixed ? n_fixed : c.ctl[2];
   for (uint32_t bi = blockIdx.x; bi < n_build; bi += gridDim.x) {
     const int4 bd = c.builds[bi];
     const uint32_t slot = static_cast<uint32_t>(bd.x);
@@ -386,8 +388,8 @@ __device__ __forceinline__ void cache_build_kernel_body(const RotCache& c,
 }
 
 __global__ void __launch_bounds__(kBuildThreads) cache_build_kernel(RotCache c, MapView map, GridView G,
-                                                                    ScanView scan) {
-  cache_build_kernel_body(c, map, G, scan);
+                                                                    ScanView scan, uint32_t n_fixed) {
+  cache_build_kernel_body(c, map, G, scan, n_fixed);
 }
 
 // Ambiguous points of one run (exact divide path), kept out of line so the
@@ -667,7 +669,7 @@ __global__ void __launch_bounds__(kBuildThreads) cache_build_group(MapView map, 
                                                                    size_t stride) {
   const ScoreSlot& a = score_slot(ga, stride);
   if (!a.cache.enabled) return;
-  cache_build_kernel_body(a.cache, map, a.G, a.scan);
+  cache_build_kernel_body(a.cache, map, a.G, a.scan, 0u);
 }
 
 __global__ void __launch_bounds__(BBS_PROBE_T, BBS_PROBE_B) cache_probe_group(MapView map,
@@ -704,18 +706,22 @@ __global__ void cache_prebuild_list_kernel(RotCache c, GridView G, int l, uint32
                             static_cast<int32_t>((i / nw) % np));
     c.builds_w[i] = static_cast<int32_t>(i % nw);
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0) c.ctl[2] = n_rot;
 }
 
-void launch_cache_prebuild(const MapView& map, const GridView& grid, const ScanView& scan,
-                           const RotCache& cache, int level, uint32_t n_rot, cudaStream_t s) {
+void launch_cache_prebuild_list(const GridView& grid, const RotCache& pre, int level, uint32_t n_rot,
+                                 cudaStream_t s) {
+  if (n_rot == 0) return;
+  cache_prebuild_list_kernel<<<(n_rot + 255) / 256, 256, 0, s>>>(pre, grid, level, n_rot);
+  BBS_CUDA(cudaGetLastError());
+}
+
+void launch_cache_prebuild(const MapView& map, const GridView& grid, const ScanView& scan, const RotCache& pre,
+                           uint32_t n_rot, cudaStream_t s) {
   if (n_rot == 0) return;
   const int build_smem = kCacheHashSlots * 12 + kCacheAmbCap * 4;
   BBS_CUDA(cudaFuncSetAttribute(cache_build_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, build_smem));
-  cache_prebuild_list_kernel<<<(n_rot + 255) / 256, 256, 0, s>>>(cache, grid, level, n_rot);
-  BBS_CUDA(cudaGetLastError());
-  cache_build_kernel<<<std::min<uint32_t>(n_rot, 148 * 2), kBuildThreads, build_smem, s>>>(cache, map, grid,
-                                                                                          scan);
+  cache_build_kernel<<<std::min<uint32_t>(n_rot, 148 * 2), kBuildThreads, build_smem, s>>>(pre, map, grid, scan,
+                                                                                          n_rot);
   BBS_CUDA(cudaGetLastError());
 }
 
@@ -741,7 +747,7 @@ void launch_epoch_score(const MapView& map, const GridView& grid, const ScanView
   // after its frontier reset ctl[2..3]
   if (builds) {  // false once no level can claim a build any more (host-known)
     launch_pdl(cache_build_kernel, std::min<uint32_t>(std::max<uint32_t>(max_runs, 1), share_cap(148 * 2)), kBuildThreads,
-               build_smem, s, cache, map, grid, scan);
+               build_smem, s, cache, map, grid, scan, 0u);
     BBS_CUDA(cudaGetLastError());
   }
   const uint32_t chunks = (scan.k + kProbeChunk - 1) / kProbeChunk;

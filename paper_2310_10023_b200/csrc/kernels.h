@@ -260,8 +260,13 @@ inline unsigned per_slot(unsigned full, uint32_t n_slots, unsigned at_least = 8)
 
 // Build the histograms of every rotation of `level` (n_rot slots from
 // cache.base[level]) in one launch; cache.builds must hold n_rot entries.
-void launch_cache_prebuild(const MapView& map, const GridView& grid, const ScanView& scan,
-                           const RotCache& cache, int level, uint32_t n_rot, cudaStream_t s);
+void launch_cache_prebuild(const MapView& map, const GridView& grid, const ScanView& scan, const RotCache& pre,
+                           uint32_t n_rot, cudaStream_t s);
+// marks the level's n_rot slots BUILDING and lists them in pre.builds /
+// pre.builds_w (a list of its own: the flush builds use cache.builds and
+// ctl[2] while the prebuild runs on its side stream)
+void launch_cache_prebuild_list(const GridView& grid, const RotCache& pre, int level, uint32_t n_rot,
+                                cudaStream_t s);
 
 // Score arbitrary nodes in place (node.score), grouping equal rotations on
 // the device.  Host-synchronous.

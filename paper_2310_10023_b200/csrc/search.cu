@@ -1856,10 +1856,10 @@ struct Workspace {
   Buf<bbs_node> pool, pending, pending_own;
   Buf<uint32_t> perm0, perm1, sk0, sk1, exp_parent, exp_off;
   Buf<int32_t> pscores, trace, hist_n, pscores_own, xchg;
-  Buf<int4> hist_ent, cache_info, cache_pool, cache_builds;
+  Buf<int4> hist_ent, cache_info, cache_pool, cache_builds, cache_pre;
   Buf<uint32_t> cache_u32, cache_amb, cache_fb, stage_win, cache_direct;
   Buf<unsigned char> cache_dflag;
-  Buf<int32_t> cache_builds_w;
+  Buf<int32_t> cache_builds_w, cache_pre_w;
   Buf<uint32_t> hist_amb, rinit_ctl;
   Buf<unsigned long long> rinit_tiles;
   unsigned long long rinit_tag = 0;
@@ -1905,6 +1905,8 @@ struct Workspace {
     cache_dflag.release();
     stage_win.release();
     cache_builds_w.release();
+    cache_pre.release();
+    cache_pre_w.release();
     st.release();
     if (h_st) cudaFreeHost(h_st);
     if (h_small) cudaFreeHost(h_small);
@@ -2571,7 +2573,7 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
         const char* v = std::getenv("BBS_PREBUILD");  // "0" disables (A/B timing)
         return !(v && v[0] == '0');
       }();
-      const uint64_t mr = std::max<uint64_t>((pend_cap + 7) / 8, prebuild ? pre_rot : 0);
+      const uint64_t mr = (pend_cap + 7) / 8;
       cache.builds = W.cache_builds.get(mr, s);
       cache.builds_w = W.cache_builds_w.get(mr, s);
       cache.fb_runs = W.cache_fb.get(mr, s);
@@ -2598,10 +2600,17 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
         cache.pre_level = pl;
         if (!W.side) BBS_CUDA(cudaStreamCreateWithFlags(&W.side, cudaStreamNonBlocking));
         cudaEvent_t e0 = W.next_event();
+        // the level's slots are marked BUILDING on this stream (so the first
+        // flush's branch kernel never claims them) and listed in a list of
+        // their own (the flush builds use cache.builds / ctl[2] meanwhile)
+        RotCache pre = cache;
+        pre.builds = W.cache_pre.get(pre_rot, s);
+        pre.builds_w = W.cache_pre_w.get(pre_rot, s);
+        launch_cache_prebuild_list(gv, pre, pl, static_cast<uint32_t>(pre_rot), s);
         BBS_CUDA(cudaEventRecord(ev_fork, s));
         BBS_CUDA(cudaStreamWaitEvent(W.side, ev_fork, 0));
         BBS_CUDA(cudaEventRecord(e0, W.side));
-        launch_cache_prebuild(m->view, gv, sv, cache, pl, static_cast<uint32_t>(pre_rot), W.side);
+        launch_cache_prebuild(m->view, gv, sv, pre, static_cast<uint32_t>(pre_rot), W.side);
         BBS_CUDA(cudaEventRecord(ev_prebuilt, W.side));
         prebuild_pending = true;
         launches += 2;
@@ -2799,7 +2808,14 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
   const uint32_t ptiles_round = choose_ptiles((pend_cap + 7) / 8, static_cast<uint32_t>(K));
   // the level L-1 prebuild ran on the side stream during the root survivor
   // selection and queue build
-  if (prebuild_pending) BBS_CUDA(cudaStreamWaitEvent(s, ev_prebuilt, 0));
+  // single searches wait for it only before the first flush's score
+  // kernels: the first frontier and branch run meanwhile (co-batched
+  // members wait here: the group waits on their stream)
+  const bool prebuild_defer = prebuild_pending && !g_group && [] {
+    const char* v = std::getenv("BBS_DEFER_PREBUILD");  // "0": wait before the first flush (A/B)
+    return !(v && v[0] == '0');
+  }();
+  if (prebuild_pending && !prebuild_defer) BBS_CUDA(cudaStreamWaitEvent(s, ev_prebuilt, 0));
 
   // per-epoch-slot events of one batch; timings are harvested after each batch
   std::vector<cudaEvent_t> ev_pass(E), ev_s0(E), ev_s1(E);
@@ -2817,6 +2833,12 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
     return v ? static_cast<size_t>(std::atoi(v)) : static_cast<size_t>(0);
   }();
   bool capturing = false;
+  // epoch 0 of every batch (a no-op once the prebuild is done; an external
+  // event-wait node inside a captured batch)
+  auto wait_prebuild = [&](int e) {
+    if (!prebuild_defer || e != 0) return;
+    BBS_CUDA(cudaStreamWaitEvent(s, ev_prebuilt, capturing ? cudaEventWaitExternal : 0));
+  };
   auto record = [&](cudaEvent_t ev) {
     // External: a real record node when captured into the batch graph
     BBS_CUDA(capturing ? cudaEventRecordWithFlags(ev, s, cudaEventRecordExternal)
@@ -2880,6 +2902,7 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
                cache_auto, split);
     BBS_CUDA(cudaGetLastError());
     record(ev_s0[e]);
+    wait_prebuild(e);
     launch_epoch_score(m->view, gv, sv, pending, d_nchild, static_cast<uint32_t>(pend_cap), ptiles_round, pscores,
                        cache_auto, s, builds_live);
     record(ev_s1[e]);
@@ -2915,6 +2938,7 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
                epoch_cache(), split);
     BBS_CUDA(cudaGetLastError());
     record(ev_s0[e]);
+    wait_prebuild(e);
     if (exact) {
       launch_epoch_score(m->view, gv, sv, split.pending_own, d_nchild, static_cast<uint32_t>(pend_epoch),
                          ptiles_epoch, split.pscores_own, cache_plain, s, builds_live);
