@@ -138,7 +138,8 @@ __device__ __forceinline__ void frontier_kernel_body(EpochState* st,
                                                      int32_t* __restrict__ trace,
                                                      unsigned long long trace_cap,
                                                      int strategy,
-                                                     uint32_t* __restrict__ cache_ctl) {
+                                                     uint32_t* __restrict__ cache_ctl,
+                                                     int active_pre = -1) {
   pdl_wait();
 
   using ScanI = cub::BlockScan<int, kFT>;
@@ -155,7 +156,7 @@ __device__ __forceinline__ void frontier_kernel_body(EpochState* st,
   __shared__ int s_active;
 
   const int tid = threadIdx.x;
-  if (tid == 0) s_active = st->active;
+  if (tid == 0) s_active = active_pre >= 0 ? active_pre : st->active;
   __syncthreads();
   if (!s_active) {
     if (tid == 0) st->n_children = 0;
@@ -381,7 +382,8 @@ __device__ __forceinline__ void frontier_spec_kernel_body(EpochState* st,
                                                           int32_t* __restrict__ trace,
                                                           unsigned long long trace_cap,
                                                           uint32_t* __restrict__ cache_ctl,
-                                                          SpecRec* __restrict__ rec) {
+                                                          SpecRec* __restrict__ rec,
+                                                          int active_pre = -1) {
   pdl_wait();
 
   using ScanI = cub::BlockScan<int, kFT>;
@@ -404,7 +406,7 @@ __device__ __forceinline__ void frontier_spec_kernel_body(EpochState* st,
   } sh;
 
   const int tid = threadIdx.x;
-  if (tid == 0) s_active = st->active;
+  if (tid == 0) s_active = active_pre >= 0 ? active_pre : st->active;
   __syncthreads();
   if (!s_active) {
     if (tid == 0) {
@@ -700,6 +702,8 @@ __device__ __forceinline__ void branch_kernel_body(EpochState* st,
   pdl_wait();
 
   const uint32_t n = st->n_children;
+  // read with the state above (one round trip), not per run
+  const bool direct_on = cache.direct_flag && (!cache.direct_gate || *cache.direct_gate);
   if (split.world && blockIdx.x == 0 && threadIdx.x == 0) st->n_own = own_children(n, split.rank, split.world);
   if (n == 0) return;
   const uint32_t ne = st->n_expand;
@@ -762,7 +766,7 @@ __device__ __forceinline__ void branch_kernel_body(EpochState* st,
     // have no histogram this flush
     if (cache.enabled && t == 0 && own) {
       const int4 ra = make_int4(ch.ix, ch.iy, ch.iz, ch.iroll), rb = make_int4(ch.ipitch, ch.iyaw, ch.level, ch.score);
-      if (cache.direct_flag && (!cache.direct_gate || *cache.direct_gate)) {
+      if (direct_on) {
         // the run's index in the array the score kernels read (exact mode:
         // this rank's compact copy)
         const uint32_t r = split.world ? (i >> 3) / split.world : (i >> 3);
@@ -1415,13 +1419,20 @@ __global__ void __launch_bounds__(kFT) frontier_auto_kernel(EpochState* st, Queu
                                                             uint32_t* __restrict__ cache_ctl,
                                                             SpecRec* __restrict__ rec) {
   pdl_wait();
+  // the mode and the activity flag in one round trip
   __shared__ uint32_t s_mode;
-  if (threadIdx.x == 0) s_mode = st->spec_mode;
+  __shared__ int s_act;
+  if (threadIdx.x == 0) {
+    const uint32_t mode = st->spec_mode;
+    const int act = st->active;
+    s_mode = mode;
+    s_act = act ? 1 : 0;
+  }
   __syncthreads();
   if (s_mode)
-    frontier_spec_kernel_body(st, q, G, b, k_max, exp_parent, exp_off, trace, trace_cap, cache_ctl, rec);
+    frontier_spec_kernel_body(st, q, G, b, k_max, exp_parent, exp_off, trace, trace_cap, cache_ctl, rec, s_act);
   else
-    frontier_kernel_body(st, q, G, b, exp_parent, exp_off, trace, trace_cap, strategy, cache_ctl);
+    frontier_kernel_body(st, q, G, b, exp_parent, exp_off, trace, trace_cap, strategy, cache_ctl, s_act);
 }
 
 __global__ void __launch_bounds__(kST) survivors_auto_kernel(EpochState* st, Queue q, int strategy,
