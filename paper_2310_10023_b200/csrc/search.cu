@@ -75,6 +75,7 @@ struct EpochState {
   uint32_t spec_kmax;
   uint32_t spec_mode;       // device-switched rounds (spec_auto): 1 = this epoch is a speculative round
   uint32_t spec_votes;      // consecutive plain epochs whose next epoch a round would have kept
+  unsigned long long look_key;  // plain epoch (voting): key of the entry the next epoch would pop last (~0 unknown)
   unsigned long long level_evals[kMaxLevels];  // flush evaluations per level
   // kept ranges of the remainder: one per key segment (BFS: 1, DFS: level)
   uint32_t seg_lo[kMaxLevels], seg_len[kMaxLevels], seg_pre[kMaxLevels + 1];
@@ -139,7 +140,8 @@ __device__ __forceinline__ void frontier_kernel_body(EpochState* st,
                                                      unsigned long long trace_cap,
                                                      int strategy,
                                                      uint32_t* __restrict__ cache_ctl,
-                                                     int active_pre = -1) {
+                                                     int active_pre = -1,
+                                                     bool look = false) {
   pdl_wait();
 
   using ScanI = cub::BlockScan<int, kFT>;
@@ -152,10 +154,11 @@ __device__ __forceinline__ void frontier_kernel_body(EpochState* st,
     typename cub::BlockReduce<unsigned long long, kFT>::TempStorage ru;
   } tmp;
   __shared__ int s_cut, s_lastlu;
-  __shared__ unsigned long long s_sum_at_cut;
+  __shared__ unsigned long long s_sum_at_cut, s_look;
   __shared__ int s_active;
 
   const int tid = threadIdx.x;
+  if (tid == 0) s_look = ~0ull;  // unknown unless the cut and the next one fall in one chunk
   if (tid == 0) s_active = active_pre >= 0 ? active_pre : st->active;
   __syncthreads();
   if (!s_active) {
@@ -244,6 +247,20 @@ __device__ __forceinline__ void frontier_kernel_body(EpochState* st,
     int tpos, ttot;
     ScanI(tmp.si).ExclusiveSum(nt, tpos, ttot);
     __syncthreads();
+    if (look && chunk_cut != INT_MAX) {
+      // lookahead for the round vote (merge kernel): the entry the NEXT
+      // epoch would pop last if it were formed from this chunk now
+      const unsigned long long lim2 = s_sum_at_cut + b;
+      int mycut2 = INT_MAX;
+#pragma unroll
+      for (int k = 0; k < kFIPT; ++k) {
+        const int i = static_cast<int>(base + tid * kFIPT + k);
+        if (valid[k] && i > chunk_cut && c[k] && sbefore[k] + c[k] > lim2 && mycut2 == INT_MAX) mycut2 = i;
+      }
+      const int cut2 = RedI(tmp.ri).Reduce(mycut2, cub::Min());
+      if (tid == 0) s_look = cut2 == INT_MAX ? ~0ull : qk[cut2];
+      __syncthreads();
+    }
 #pragma unroll
     for (int k = 0; k < kFIPT; ++k) {
       const long long i = base + tid * kFIPT + k;
@@ -301,6 +318,7 @@ __device__ __forceinline__ void frontier_kernel_body(EpochState* st,
     st->cache_raw = raw;  // lets the host stop launching empty build kernels
   }
   if (tid == 0) {
+    if (look) st->look_key = s_look;
     st->surv_ticket = 0;
     st->nodes_pruned += pruned_all;
     st->best = carry_best;
@@ -1332,9 +1350,9 @@ __device__ __forceinline__ void merge_kernel_body(EpochState* st,
   unsigned long long* __restrict__ ok = q.keys(cur ^ 1u);
   // the vote's two keys, loaded before the merge work (inputs, unchanged by it)
   unsigned long long vote_s = 0, vote_a = 0;
-  if (vote && threadIdx.x == 0 && !st->spec_mode && n_s && n_keep) {
+  if (vote && threadIdx.x == 0 && !st->spec_mode && n_s) {
     vote_s = __ldcg(skey);
-    vote_a = A[min(st->n_cons, n_keep) - 1u];
+    vote_a = st->look_key;
   }
   const uint32_t total = n_keep + n_s;
   const uint32_t warp = threadIdx.x >> 5;
@@ -1387,10 +1405,10 @@ __device__ __forceinline__ void merge_kernel_body(EpochState* st,
       if (vote && !st->spec_mode) {
         // would a speculative round have kept the next epoch?  It is formed
         // from the remainder alone; the survivors displace it when the
-        // smallest survivor key precedes the remainder entry it would pop
-        // last (estimated at this epoch's pop count)
+        // smallest survivor key precedes the entry it would pop last (the
+        // frontier's lookahead, ~0 when unknown: no vote)
         bool keep = n_s == 0;
-        if (n_s && n_keep) keep = vote_s > vote_a;
+        if (n_s) keep = vote_a != ~0ull && vote_s > vote_a;
         st->spec_votes = keep ? st->spec_votes + 1u : 0u;
         if (st->spec_votes >= static_cast<uint32_t>(vote)) st->spec_mode = 1u;
       }
@@ -1432,7 +1450,7 @@ __global__ void __launch_bounds__(kFT) frontier_auto_kernel(EpochState* st, Queu
   if (s_mode)
     frontier_spec_kernel_body(st, q, G, b, k_max, exp_parent, exp_off, trace, trace_cap, cache_ctl, rec, s_act);
   else
-    frontier_kernel_body(st, q, G, b, exp_parent, exp_off, trace, trace_cap, strategy, cache_ctl, s_act);
+    frontier_kernel_body(st, q, G, b, exp_parent, exp_off, trace, trace_cap, strategy, cache_ctl, s_act, true);
 }
 
 __global__ void __launch_bounds__(kST) survivors_auto_kernel(EpochState* st, Queue q, int strategy,
