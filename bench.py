@@ -445,8 +445,11 @@ def run_b200_arm(args, cfgd):
             return B.search_sharded(vmap, ds or dscan, cfg, rank, world, comm=comm,
                                     mode=args.shard_mode)
     else:
+        # on the stream the step's events and the L2 flush are recorded on:
+        # the search starts after the flush and the end event follows its
+        # last kernel (on the map's own stream it overlapped the flush)
         def one_search():
-            return B.search_scan(vmap, dscan, cfg)
+            return B.search_scan(vmap, dscan, cfg, stream=stream.cuda_stream)
 
     def barrier():
         if sharded:

@@ -9,6 +9,7 @@ ap.add_argument("--searches", type=int, default=3)
 ap.add_argument("--config", default="c2")
 ap.add_argument("--layout", default="auto")
 ap.add_argument("--k", type=int, default=0, help="override the scan size K")
+ap.add_argument("--flush", action="store_true", help="write 256 MiB before every search (cold L2, as bench.py)")
 a = ap.parse_args()
 cfgd = dict(bench.CONFIGS[a.config])
 if a.k:
@@ -17,7 +18,14 @@ m, s, gt = bench.build_inputs(cfgd)
 vm = B.MultiResVoxelMap.build(m, cfgd["r"], cfgd["max_level"], layout=B.Layout[a.layout.upper()])
 ds = B.DeviceScan(vm, s)
 cfg = bench.search_config(B, cfgd)
+flush = None
+if a.flush:
+    import torch
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 for i in range(a.searches):
+    if flush is not None:
+        flush.fill_(1)
+        torch.cuda.synchronize()
     r = B.search_scan(vm, ds, cfg)
     print(f"search {i}: best {r.best_score} evals {r.stats.nodes_generated} epochs {r.epochs} "
           f"device {r.device_ms:.3f} ms root {r.root_score_ms:.3f} epoch-score {r.epoch_score_ms:.3f} "
