@@ -444,6 +444,14 @@ __device__ __forceinline__ void frontier_spec_kernel_body(EpochState* st,
   int carry_lu = -1;                // queue index of the round's last leaf update
   int ep = 0;
 
+  // the next chunk's entries are loaded while this one is processed (a
+  // round scans several chunks one after another: C3 ~6)
+  bbs_node nd_next[kFIPT];
+#pragma unroll
+  for (int k = 0; k < kFIPT; ++k) {
+    const uint32_t i = tid * kFIPT + k;
+    if (i < qlen) nd_next[k] = pool[key_seq(BBS_STRATEGY_BFS, qk[i])];
+  }
   for (uint32_t base = 0; base < qlen && ep < k_max; base += kFChunk) {
     bbs_node nd[kFIPT];
     bool valid[kFIPT];
@@ -452,10 +460,13 @@ __device__ __forceinline__ void frontier_spec_kernel_body(EpochState* st,
     for (int k = 0; k < kFIPT; ++k) {
       const uint32_t i = base + tid * kFIPT + k;
       valid[k] = i < qlen;
-      if (valid[k]) {
-        nd[k] = pool[key_seq(BBS_STRATEGY_BFS, qk[i])];
-        if (nd[k].level == 0) lm = max(lm, nd[k].score);
-      }
+      nd[k] = nd_next[k];
+      if (valid[k] && nd[k].level == 0) lm = max(lm, nd[k].score);
+    }
+#pragma unroll
+    for (int k = 0; k < kFIPT; ++k) {
+      const uint32_t i = base + kFChunk + tid * kFIPT + k;
+      if (i < qlen) nd_next[k] = pool[key_seq(BBS_STRATEGY_BFS, qk[i])];
     }
     int excl;
     ScanI(tmp.si).ExclusiveScan(lm, excl, INT_MIN, cub::Max());
