@@ -858,20 +858,9 @@ __global__ void __launch_bounds__(256, BBS_COLPAD_MINB) root_colpad_kernel(GridV
         if ((i & 7) == 0) s_rem[i >> 3] = w.y;  // root_hist_kernel's suffix sum
       }
       __syncthreads();
-      int g = 0;
-#pragma unroll 4
-      for (; !done && g < tn; ++g) {
-        if ((g & 7) == 0 && g) {
-          uint32_t best = 0;
-#pragma unroll
-          for (int j = 0; j < NZ; ++j) best = max(best, acc[j] >> j);
-          if (static_cast<int>(best) + s_rem[g >> 3] + n_amb < bp.threshold) {
-            done = true;
-            break;
-          }
-        }
-        const int4 o = s_go[g];
-        const uint32_t w4 = s_gw[g];
+      auto group = [&](int gi) {
+        const int4 o = s_go[gi];
+        const uint32_t w4 = s_gw[gi];
         // byte offsets above the low 8 bits, shift amounts in the low 5 (wrap funnel shift)
         const uint32_t b0 = __funnelshift_r(lds_u32(col_b + static_cast<uint32_t>(o.x >> 8)), 0u, static_cast<uint32_t>(o.x));
         const uint32_t b1 = __funnelshift_r(lds_u32(col_b + static_cast<uint32_t>(o.y >> 8)), 0u, static_cast<uint32_t>(o.y));
@@ -880,6 +869,27 @@ __global__ void __launch_bounds__(256, BBS_COLPAD_MINB) root_colpad_kernel(GridV
         const uint32_t x = __byte_perm(__byte_perm(b0, b1, 0x0040), __byte_perm(b2, b3, 0x0040), 0x5410);
 #pragma unroll
         for (int j = 0; j < NZ; ++j) acc[j] = __dp4a(x & (0x01010101u << j), w4, acc[j]);
+      };
+      // blocks of 8 groups (no per-group exit test), the survivor bound
+      // checked between blocks
+      int g = 0;
+      while (!done && g < tn) {
+        if (g) {
+          uint32_t best = 0;
+#pragma unroll
+          for (int j = 0; j < NZ; ++j) best = max(best, acc[j] >> j);
+          if (static_cast<int>(best) + s_rem[g >> 3] + n_amb < bp.threshold) {
+            done = true;
+            break;
+          }
+        }
+        if (g + 8 <= tn) {
+#pragma unroll
+          for (int u = 0; u < 8; ++u) group(g + u);
+          g += 8;
+        } else {
+          for (; g < tn; ++g) group(g);
+        }
       }
       n_words += 4u * static_cast<uint32_t>(g);
     }
