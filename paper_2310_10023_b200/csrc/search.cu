@@ -1421,7 +1421,11 @@ __device__ __forceinline__ void merge_kernel_body(EpochState* st,
         bool keep = n_s == 0;
         if (n_s) keep = vote_a != ~0ull && vote_s > vote_a;
         st->spec_votes = keep ? st->spec_votes + 1u : 0u;
-        if (st->spec_votes >= static_cast<uint32_t>(vote)) st->spec_mode = 1u;
+        if (st->spec_votes >= static_cast<uint32_t>(vote & 0xFF)) {
+          st->spec_mode = 1u;
+          // first round depth (A/B: vote >> 8)
+          if (vote >> 8) st->spec_k = min(static_cast<uint32_t>(vote >> 8), st->spec_kmax);
+        }
       }
     }
   }
@@ -2928,7 +2932,8 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
   }();
   const int spec_votes_needed = [] {
     const char* v = std::getenv("BBS_SPEC_VOTES");  // consecutive plain epochs voting for rounds
-    return v ? std::max(1, std::atoi(v)) : 2;
+    const char* k0 = std::getenv("BBS_SPEC_K0");  // depth of the first round after the switch (C1 1.43 -> 1.40, C3 12.7 -> 12.3 ms at 4; 8: C3 12.8)
+    return (v ? std::max(1, std::atoi(v)) : 2) | ((k0 ? std::max(0, std::min(16, std::atoi(k0))) : 4) << 8);
   }();
   RotCache cache_auto = cache;
   cache_auto.direct_gate =
