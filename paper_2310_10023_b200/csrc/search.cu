@@ -2680,7 +2680,10 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
 
   // survivors >= threshold among own roots, in initial_nodes order
   const bool dbg_spec = std::getenv("BBS_DEBUG_SPEC") != nullptr;  // per-round state (stderr)
-  const int E = (host_x || dump || dbg_spec) ? 1 : (g_group ? g_group->E : 8);  // epochs per host check
+  const int E = (host_x || dump || dbg_spec) ? 1 : (g_group ? g_group->E : [] {
+    const char* v = std::getenv("BBS_E");  // A/B: epochs per host check
+    return v ? std::max(1, std::min(64, std::atoi(v))) : 8;
+  }());  // epochs per host check
   unsigned long long root_probes = 0;
   int n_root_surv = 0;       // host path only
   unsigned long long* surv_idx = nullptr;
