@@ -371,3 +371,30 @@ def test_speculative_rounds_match_reference(B, golden_scenes, name, spec, monkey
     for label, want in golden_json(f"{name}_search.json").items():
         res = B.search(vm, s, make_cfg(B, sc, name, want["overrides"]))
         assert_same(res, want, f"{name}/{label}/spec{spec}")
+
+
+_FAST_PATHS_OFF = {"BBS_SPEC_AUTO": "0", "BBS_DIRECT_RUNS": "0", "BBS_ROT_CACHE": "0", "BBS_ROOT_INIT": "host"}
+
+
+@pytest.mark.parametrize("strategy", ["BFS", "DFS"])
+@pytest.mark.parametrize("b", [10000, 37])
+def test_fast_paths_are_transparent(B, golden_scenes, monkeypatch, strategy, b):
+    """The room scene (K = 2000: flush cache, device-switched rounds, direct
+    runs all active) searched with the fast paths on and off: score, pose,
+    Stats and trace identical (scripts/transparency_matrix.py sweeps 36
+    configs on the C1 and C2 maps)."""
+    m, s, _, sc = load_case(B, golden_scenes, "room")
+    vm = B.MultiResVoxelMap.build(m, sc["r"], sc["max_level"])
+    ds = B.DeviceScan(vm, s)
+    cfg = make_cfg(B, sc, "room", dict(batch_size=b, strategy=getattr(B.Strategy, strategy)))
+    out = []
+    for env in ({}, _FAST_PATHS_OFF):
+        for k in _FAST_PATHS_OFF:
+            monkeypatch.delenv(k, raising=False)
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        r = B.search_scan(vm, ds, cfg)
+        out.append((r.best_score, r.best_pose.as_tuple(), r.stats.nodes_generated, r.stats.nodes_pruned,
+                    r.stats.batches_flushed, tuple(r.best_score_trace)))
+    assert out[0] == out[1]
+    assert s.shape[0] >= 2000  # the flush cache is on at this size
