@@ -1245,7 +1245,10 @@ __global__ void __launch_bounds__(kST) survivors_spec_kernel(EpochState* st, Que
 
 // E4b: order the survivors by key.  Keys are unique (they embed seq), so a
 // survivor's rank = #keys below it; ranks are computed against smem tiles.
+// Up to kMergeSortSmall survivors (C2: 14-107 per flush) are left to the
+// merge kernel, whose CTAs each rank them in shared memory.
 constexpr int kRT = 256;
+constexpr uint32_t kMergeSortSmall = 256;
 __device__ __forceinline__ void rank_sort_kernel_body(EpochState* st,
                                                       const unsigned long long* __restrict__ key,
                                                       unsigned long long* __restrict__ out_key,
@@ -1259,7 +1262,7 @@ __device__ __forceinline__ void rank_sort_kernel_body(EpochState* st,
   if (trim_strategy >= 0 && blockIdx.x == 0 && threadIdx.x < 32 && st->n_children)
     trim_remainder(st, q, trim_strategy, st->flush_best);
   const uint32_t n = st->n_children ? st->n_surv : 0;
-  if (n == 0) return;
+  if (n <= kMergeSortSmall) return;  // the merge kernel sorts these itself (none: nothing to do)
   for (uint32_t base = blockIdx.x * kRT; base < n; base += gridDim.x * kRT) {
     const uint32_t j = base + threadIdx.x;
     const unsigned long long kj = j < n ? key[j] : ~0ull;
@@ -1340,7 +1343,8 @@ __device__ __forceinline__ uint32_t warp_merge_split(const RemView& A, uint32_t 
 __device__ __forceinline__ void merge_kernel_body(EpochState* st,
                                                   Queue q,
                                                   int strategy,
-                                                  const unsigned long long* __restrict__ skey,
+                                                  const unsigned long long* __restrict__ sorted_key,
+                                                  const unsigned long long* __restrict__ unsorted_key,
                                                   int vote = 0) {
   pdl_wait();
 
@@ -1357,12 +1361,26 @@ __device__ __forceinline__ void merge_kernel_body(EpochState* st,
   const uint32_t cur = st->cur;
   const uint32_t n_keep = st->n_keep;
   const uint32_t n_s = st->n_surv;
+  // few survivors: every CTA ranks them in shared memory (no sort kernel)
+  __shared__ unsigned long long s_b[kMergeSortSmall];
+  const unsigned long long* __restrict__ skey = sorted_key;
+  if (n_s <= kMergeSortSmall) {
+    static_assert(kMergeSortSmall == kMT, "one survivor per thread");
+    const unsigned long long kj = threadIdx.x < n_s ? __ldcg(unsorted_key + threadIdx.x) : ~0ull;
+    s_ab[threadIdx.x] = kj;
+    __syncthreads();
+    uint32_t rank = 0;
+    for (uint32_t i = 0; i < n_s; ++i) rank += s_ab[i] < kj ? 1u : 0u;
+    if (threadIdx.x < n_s) s_b[rank] = kj;
+    __syncthreads();
+    skey = s_b;
+  }
   const RemView A{q.keys(cur) + st->n_cons, s_lo, s_pre, strategy == BBS_STRATEGY_BFS};
   unsigned long long* __restrict__ ok = q.keys(cur ^ 1u);
   // the vote's two keys, loaded before the merge work (inputs, unchanged by it)
   unsigned long long vote_s = 0, vote_a = 0;
   if (vote && threadIdx.x == 0 && !st->spec_mode && n_s) {
-    vote_s = __ldcg(skey);
+    vote_s = skey[0];  // sorted by rank_sort, or ranked in shared memory above
     vote_a = st->look_key;
   }
   const uint32_t total = n_keep + n_s;
@@ -1432,8 +1450,9 @@ __device__ __forceinline__ void merge_kernel_body(EpochState* st,
 }
 
 __global__ void __launch_bounds__(kMT) merge_kernel(EpochState* st, Queue q, int strategy,
-                                                    const unsigned long long* __restrict__ skey) {
-  merge_kernel_body(st, q, strategy, skey);
+                                                    const unsigned long long* __restrict__ skey,
+                                                    const unsigned long long* __restrict__ ukey) {
+  merge_kernel_body(st, q, strategy, skey, ukey);
 }
 
 // ---- device-switched speculative rounds (BFS, single searches) -------------
@@ -1490,8 +1509,9 @@ __global__ void __launch_bounds__(kRT) rank_sort_auto_kernel(EpochState* st,
 }
 
 __global__ void __launch_bounds__(kMT) merge_auto_kernel(EpochState* st, Queue q, int strategy,
-                                                         const unsigned long long* __restrict__ skey, int votes) {
-  merge_kernel_body(st, q, strategy, skey, votes);
+                                                         const unsigned long long* __restrict__ skey,
+                                                         const unsigned long long* __restrict__ ukey, int votes) {
+  merge_kernel_body(st, q, strategy, skey, ukey, votes);
 }
 
 
@@ -1550,7 +1570,7 @@ __global__ void __launch_bounds__(kRT) rank_sort_group(const SlotArgs* __restric
 
 __global__ void __launch_bounds__(kMT) merge_group(const SlotArgs* __restrict__ ga, int strategy) {
   const SlotArgs& a = ga[blockIdx.y];
-  merge_kernel_body(a.st, a.q, strategy, a.s_key2);
+  merge_kernel_body(a.st, a.q, strategy, a.s_key2, a.s_key);
 }
 
 // Exact mode: this rank's run scores back to their pending positions.
@@ -2964,7 +2984,8 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
     if (dbg_phases) record(ev_dbg[3 * e + 1]);
     launch_pdl(merge_auto_kernel,
                static_cast<unsigned>(std::min<uint64_t>((qcap + kMTile - 1) / kMTile, share_cap(148ull * 8))), kMT, 0,
-               s, d_st, q, strategy, static_cast<const unsigned long long*>(s_key2), spec_votes_needed);
+               s, d_st, q, strategy, static_cast<const unsigned long long*>(s_key2),
+               static_cast<const unsigned long long*>(s_key), spec_votes_needed);
     BBS_CUDA(cudaGetLastError());
     if (dbg_phases) record(ev_dbg[3 * e + 2]);
     launches += 6;
@@ -3021,7 +3042,8 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
     }
     if (dbg_phases) record(ev_dbg[3 * e + 1]);
     launch_pdl(merge_kernel, static_cast<unsigned>(std::min<uint64_t>((qcap + kMTile - 1) / kMTile, share_cap(148ull * 8))),
-               kMT, 0, s, d_st, q, strategy, s_key2);
+               kMT, 0, s, d_st, q, strategy, static_cast<const unsigned long long*>(s_key2),
+               static_cast<const unsigned long long*>(s_key));
     BBS_CUDA(cudaGetLastError());
     if (dbg_phases) record(ev_dbg[3 * e + 2]);
     launches += 6;  // frontier, branch, score, survivors, rank_sort, merge (+ finalize)
