@@ -9,7 +9,9 @@ import bench
 import paper_2310_10023_b200 as B
 
 OFF = {"BBS_SPEC_AUTO": "0", "BBS_DIRECT_RUNS": "0", "BBS_ROT_CACHE": "0", "BBS_ROOT_INIT": "host"}
-cfgd = bench.CONFIGS[sys.argv[1] if len(sys.argv) > 1 else "c2"]
+cfgd = dict(bench.CONFIGS[sys.argv[1] if len(sys.argv) > 1 else "c2"])
+if len(sys.argv) > 2:
+    cfgd["K"] = int(sys.argv[2])  # scan size override (e.g. 70000: hash-built histograms)
 m, s, gt = bench.build_inputs(cfgd)
 vm = B.MultiResVoxelMap.build(m, cfgd["r"], cfgd["max_level"])
 ds = B.DeviceScan(vm, s)
