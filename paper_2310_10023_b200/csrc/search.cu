@@ -417,6 +417,7 @@ __device__ __forceinline__ void frontier_spec_kernel_body(EpochState* st,
   __shared__ struct {
     unsigned long long S[kFChunk];  // inclusive children sums (round-global); ~0 past the queue
     unsigned long long C[kFChunk];  // inclusive packed counts (chunk)
+    unsigned long long K[kFChunk];  // the chunk's queue keys (an epoch record's last key)
     int L[kFChunk];                 // last leaf update through the pop
     int Bk[kFChunk];                // incumbent after the pop
     int ep, limit;
@@ -447,13 +448,16 @@ __device__ __forceinline__ void frontier_spec_kernel_body(EpochState* st,
   // the next chunk's entries are loaded while this one is processed (a
   // round scans several chunks one after another: C3 ~6)
   bbs_node nd_next[kFIPT];
+  unsigned long long key_next[kFIPT];
 #pragma unroll
   for (int k = 0; k < kFIPT; ++k) {
     const uint32_t i = tid * kFIPT + k;
-    if (i < qlen) nd_next[k] = pool[key_seq(BBS_STRATEGY_BFS, qk[i])];
+    key_next[k] = i < qlen ? qk[i] : ~0ull;
+    if (i < qlen) nd_next[k] = pool[key_seq(BBS_STRATEGY_BFS, key_next[k])];
   }
   for (uint32_t base = 0; base < qlen && ep < k_max; base += kFChunk) {
     bbs_node nd[kFIPT];
+    unsigned long long key[kFIPT];
     bool valid[kFIPT];
     int lm = INT_MIN;
 #pragma unroll
@@ -461,12 +465,14 @@ __device__ __forceinline__ void frontier_spec_kernel_body(EpochState* st,
       const uint32_t i = base + tid * kFIPT + k;
       valid[k] = i < qlen;
       nd[k] = nd_next[k];
+      key[k] = key_next[k];
       if (valid[k] && nd[k].level == 0) lm = max(lm, nd[k].score);
     }
 #pragma unroll
     for (int k = 0; k < kFIPT; ++k) {
       const uint32_t i = base + kFChunk + tid * kFIPT + k;
-      if (i < qlen) nd_next[k] = pool[key_seq(BBS_STRATEGY_BFS, qk[i])];
+      key_next[k] = i < qlen ? qk[i] : ~0ull;
+      if (i < qlen) nd_next[k] = pool[key_seq(BBS_STRATEGY_BFS, key_next[k])];
     }
     int excl;
     ScanI(tmp.si).ExclusiveScan(lm, excl, INT_MIN, cub::Max());
@@ -531,6 +537,7 @@ __device__ __forceinline__ void frontier_spec_kernel_body(EpochState* st,
       const int li = tid * kFIPT + k;
       sh.S[li] = valid[k] ? Sin[k] : ~0ull;
       sh.C[li] = Cin[k];
+      sh.K[li] = key[k];
       sh.L[li] = Lin[k];
       sh.Bk[li] = Bk[k];
     }
@@ -559,7 +566,7 @@ __device__ __forceinline__ void frontier_spec_kernel_body(EpochState* st,
         if (lane == 0) {
           const unsigned long long Cc = sh.C[l];
           SpecRec r;
-          r.lastkey = qk[base + l];
+          r.lastkey = sh.K[l];
           r.pruned = carry_pruned + (Cc >> 42);
           r.trace_end = carry_trace + ((Cc >> 21) & 0x1FFFFFull);
           r.minkey = ~0ull;
@@ -598,7 +605,7 @@ __device__ __forceinline__ void frontier_spec_kernel_body(EpochState* st,
       if (!valid[k] || i > limit) continue;
       if (c[k]) {
         const uint32_t e = carry_exp + static_cast<uint32_t>(Cin[k] & 0x1FFFFFull) - 1u;
-        exp_parent[e] = key_seq(BBS_STRATEGY_BFS, qk[i]);  // the parent's pool slot
+        exp_parent[e] = key_seq(BBS_STRATEGY_BFS, key[k]);  // the parent's pool slot
         exp_off[e] = static_cast<uint32_t>(Sin[k] - c[k]);
       }
       if (lu[k]) {

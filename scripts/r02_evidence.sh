@@ -28,8 +28,8 @@ full() {
 full c2 root_colpad 1
 full c2 cache_probe 9
 full c2 cache_build 0
-full c3 frontier_spec 40
-full c3 survivors_spec 40
+full c3 frontier_auto 40
+full c3 survivors_auto 40
 full c3 cache_probe 60
 }
 ls $O
