@@ -398,3 +398,25 @@ def test_fast_paths_are_transparent(B, golden_scenes, monkeypatch, strategy, b):
                     r.stats.batches_flushed, tuple(r.best_score_trace)))
     assert out[0] == out[1]
     assert s.shape[0] >= 2000  # the flush cache is on at this size
+
+
+def test_cobatched_group_mixes_cached_and_uncached_slots(B, golden_scenes, monkeypatch):
+    """Co-batched flushes with scans of K = 1,000 (no flush cache) and
+    K = 3,000 (flush cache, speculative rounds) in the same group: every
+    result equals the scan's own search."""
+    monkeypatch.setenv("BBS_COBATCH", "1")
+    m, _, _, sc = load_case(B, golden_scenes, "room")
+    spec = H.SceneSpec.default(**sc["spec"])
+    scans, _ = H.gen_scans(spec, sc["seed"], 500, 6)
+    scans = [H.cut_scan(s, min(1000 if j % 2 else 3000, s.shape[0]), 11) for j, s in enumerate(scans)]
+    vm = B.MultiResVoxelMap.build(m, sc["r"], sc["max_level"])
+    ds = [B.DeviceScan(vm, s) for s in scans]
+    cfg = make_cfg(B, sc, "room", dict(batch_size=2000))
+    many = B.search_scans(vm, ds, cfg, concurrency=6, trace_capacity=1 << 14)
+    assert sum(r.group_checks for r in many) > 0
+    for d, r in zip(ds, many):
+        one = B.search_scan(vm, d, cfg)
+        assert (r.best_score, r.best_pose.as_tuple(), r.stats.nodes_generated, r.stats.nodes_pruned,
+                r.stats.batches_flushed, r.best_score_trace) == (
+                    one.best_score, one.best_pose.as_tuple(), one.stats.nodes_generated, one.stats.nodes_pruned,
+                    one.stats.batches_flushed, one.best_score_trace)
