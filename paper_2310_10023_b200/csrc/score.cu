@@ -353,7 +353,10 @@ __device__ __forceinline__ void score_cube8_kernel_body(const MapView& map,
 }
 
 template <bool kILP>
-__global__ void __launch_bounds__(256, 4) score_cube8_kernel(MapView map, GridView grid, ScanView scan,
+#ifndef BBS_CUBE_MINB
+#define BBS_CUBE_MINB 4
+#endif
+__global__ void __launch_bounds__(256, BBS_CUBE_MINB) score_cube8_kernel(MapView map, GridView grid, ScanView scan,
                                                              const bbs_node* __restrict__ nodes,
                                                              const uint32_t* __restrict__ d_n,
                                                              uint32_t n_ptiles,
@@ -1168,7 +1171,7 @@ void launch_score_cube8(const MapView& map, const GridView& grid, const ScanView
   const uint64_t items = static_cast<uint64_t>((n_max + 7) / 8) * n_ptiles;
   // with the cache the run list and tiling are only known on the device:
   // one resident wave (4 CTAs per SM), grid-strided
-  const unsigned g = cache ? share_cap(148ull * 4)
+  const unsigned g = cache ? share_cap(148ull * BBS_CUBE_MINB)
                            : static_cast<unsigned>(std::min<uint64_t>(std::max<uint64_t>(items, 1), share_cap(148ull * 4 * 8)));
   // the flush cache's direct runs (large scans) keep two points in flight;
   // without the cache (small scans, short point tiles) one point per step
