@@ -66,6 +66,7 @@ struct EpochState {
   uint32_t n_keep;         // queue remainder kept after the incumbent trim
   uint32_t surv_ticket;    // survivors tile tickets (reset by the frontier)
   uint32_t merge_done;     // merge CTAs finished (the last one finalizes the epoch)
+  uint32_t fuse_claim, fuse_done;  // fused merge prologue: tasks claimed / finished
   uint32_t cache_raw;      // levels whose histogram builds gave up (flush cache, per frontier pass)
   uint32_t n_own;          // batch-split exact mode: children of this rank's runs
   int32_t any_active;      // sharded (device exchange): any rank still active
@@ -1347,30 +1348,81 @@ __device__ __forceinline__ uint32_t warp_merge_split(const RemView& A, uint32_t 
   return lo;
 }
 
+// fused: this kernel also does the rank-sort kernel's work first (the
+// incumbent trim of a round, trim >= 0 or -2 = by st->spec_mode; the rank
+// sort of more than kMergeSortSmall survivors into sorted_key), one launch
+// less per flush.  That work is split into tasks (trim, then one per tile of
+// kMT keys) that CTAs claim with an atomic counter; a CTA waits only for
+// tasks already claimed by running CTAs, so the wait cannot starve whatever
+// share of the grid is resident (other searches on other streams included).
 __device__ __forceinline__ void merge_kernel_body(EpochState* st,
                                                   Queue q,
                                                   int strategy,
-                                                  const unsigned long long* __restrict__ sorted_key,
+                                                  const unsigned long long* sorted_key,
                                                   const unsigned long long* __restrict__ unsorted_key,
-                                                  int vote = 0) {
+                                                  int vote = 0, bool fused = false, int trim = -1) {
   pdl_wait();
 
   __shared__ uint32_t s_lo[kMaxLevels], s_pre[kMaxLevels + 1];
   __shared__ uint32_t s_split[2];
   __shared__ unsigned long long s_ab[kMTile];
   if (st->n_children == 0) return;
-  if (threadIdx.x < kMaxLevels) {
-    s_lo[threadIdx.x] = st->seg_lo[threadIdx.x];
-    s_pre[threadIdx.x] = st->seg_pre[threadIdx.x];
+  if (fused) {
+    if (trim == -2) trim = st->spec_mode ? strategy : -1;
+    const uint32_t n = st->n_surv;
+    const uint32_t n_trim = trim >= 0 ? 1u : 0u;
+    const uint32_t tasks = n_trim + (n > kMergeSortSmall ? (n + kMT - 1u) / kMT : 0u);
+    if (tasks) {
+      __shared__ uint32_t s_task;
+      unsigned long long* out = const_cast<unsigned long long*>(sorted_key);
+      for (;;) {
+        if (threadIdx.x == 0) {  // no atomic once every task is out (most of the grid)
+          const uint32_t c = *reinterpret_cast<volatile uint32_t*>(&st->fuse_claim);
+          s_task = c >= tasks ? c : atomicAdd(&st->fuse_claim, 1u);
+        }
+        __syncthreads();
+        const uint32_t t = s_task;
+        __syncthreads();
+        if (t >= tasks) break;
+        if (t < n_trim) {
+          if (threadIdx.x < 32) trim_remainder(st, q, trim, st->flush_best);
+        } else {  // rank sort of one tile (rank_sort_kernel_body), smem tiles in s_ab
+          const uint32_t j = (t - n_trim) * kMT + threadIdx.x;
+          const unsigned long long kj = j < n ? __ldg(unsorted_key + j) : ~0ull;
+          uint32_t rank = 0;
+          for (uint32_t t0 = 0; t0 < n; t0 += kMT) {
+            __syncthreads();
+            s_ab[threadIdx.x] = (t0 + threadIdx.x < n) ? __ldg(unsorted_key + t0 + threadIdx.x) : ~0ull;
+            __syncthreads();
+            const uint32_t lim = min(static_cast<uint32_t>(kMT), n - t0);
+#pragma unroll 8
+            for (uint32_t i = 0; i < lim; ++i) rank += s_ab[i] < kj ? 1u : 0u;
+          }
+          if (j < n) out[rank] = kj;
+        }
+        __threadfence();
+        __syncthreads();
+        if (threadIdx.x == 0) atomicAdd(&st->fuse_done, 1u);
+      }
+      if (threadIdx.x == 0)
+        while (*reinterpret_cast<volatile uint32_t*>(&st->fuse_done) < tasks) __nanosleep(32);
+      __threadfence();
+      __syncthreads();
+    }
   }
-  if (threadIdx.x == 0) s_pre[kMaxLevels] = st->seg_pre[kMaxLevels];
+  // L2 reads: the trim may have written these in this launch
+  if (threadIdx.x < kMaxLevels) {
+    s_lo[threadIdx.x] = __ldcg(st->seg_lo + threadIdx.x);
+    s_pre[threadIdx.x] = __ldcg(st->seg_pre + threadIdx.x);
+  }
+  if (threadIdx.x == 0) s_pre[kMaxLevels] = __ldcg(st->seg_pre + kMaxLevels);
   __syncthreads();
   const uint32_t cur = st->cur;
-  const uint32_t n_keep = st->n_keep;
+  const uint32_t n_keep = __ldcg(&st->n_keep);
   const uint32_t n_s = st->n_surv;
   // few survivors: every CTA ranks them in shared memory (no sort kernel)
   __shared__ unsigned long long s_b[kMergeSortSmall];
-  const unsigned long long* __restrict__ skey = sorted_key;
+  const unsigned long long* skey = sorted_key;
   if (n_s <= kMergeSortSmall) {
     static_assert(kMergeSortSmall == kMT, "one survivor per thread");
     const unsigned long long kj = threadIdx.x < n_s ? __ldcg(unsorted_key + threadIdx.x) : ~0ull;
@@ -1438,6 +1490,8 @@ __device__ __forceinline__ void merge_kernel_body(EpochState* st,
       st->q_peak = max(st->q_peak, len);
       if (len == 0) st->active = 0;
       st->merge_done = 0;
+      st->fuse_claim = 0;  // every CTA is past the prologue
+      st->fuse_done = 0;
       if (vote && !st->spec_mode) {
         // would a speculative round have kept the next epoch?  It is formed
         // from the remainder alone; the survivors displace it when the
@@ -1457,9 +1511,10 @@ __device__ __forceinline__ void merge_kernel_body(EpochState* st,
 }
 
 __global__ void __launch_bounds__(kMT) merge_kernel(EpochState* st, Queue q, int strategy,
-                                                    const unsigned long long* __restrict__ skey,
-                                                    const unsigned long long* __restrict__ ukey) {
-  merge_kernel_body(st, q, strategy, skey, ukey);
+                                                    const unsigned long long* skey,
+                                                    const unsigned long long* __restrict__ ukey, int fused_trim) {
+  // fused_trim: -3 = not fused (a rank-sort kernel ran), else the trim strategy (-1 none)
+  merge_kernel_body(st, q, strategy, skey, ukey, 0, fused_trim != -3, fused_trim);
 }
 
 // ---- device-switched speculative rounds (BFS, single searches) -------------
@@ -1516,9 +1571,10 @@ __global__ void __launch_bounds__(kRT) rank_sort_auto_kernel(EpochState* st,
 }
 
 __global__ void __launch_bounds__(kMT) merge_auto_kernel(EpochState* st, Queue q, int strategy,
-                                                         const unsigned long long* __restrict__ skey,
-                                                         const unsigned long long* __restrict__ ukey, int votes) {
-  merge_kernel_body(st, q, strategy, skey, ukey, votes);
+                                                         const unsigned long long* skey,
+                                                         const unsigned long long* __restrict__ ukey, int votes,
+                                                         int fused) {
+  merge_kernel_body(st, q, strategy, skey, ukey, votes, fused != 0, -2);
 }
 
 
@@ -2956,6 +3012,12 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
   // device-switched rounds (frontier_auto_kernel ...): BFS single searches
   // with rank-sorted survivors; the host-switched schedule otherwise
   // (BBS_SPEC_AUTO=0: plain epochs for the first host check, then rounds)
+  // the merge kernel does the rank sort (and the round's trim) itself
+  // (BBS_FUSE_SORT=0: a rank-sort kernel before it)
+  const bool fuse_sort = [] {
+    const char* v = std::getenv("BBS_FUSE_SORT");
+    return !(v && v[0] == '0');
+  }();
   const bool spec_auto = spec_k > 1 && rank_sorted && !exact && !dbg_spec && [] {
     const char* v = std::getenv("BBS_SPEC_AUTO");
     return !(v && v[0] == '0');
@@ -2985,17 +3047,20 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
                static_cast<const int32_t*>(pscores), s_key, surv_tiles, d_rec);
     BBS_CUDA(cudaGetLastError());
     if (dbg_phases) record(ev_dbg[3 * e]);
-    launch_pdl(rank_sort_auto_kernel, grid1(pend_cap, kRT), kRT, 0, s, d_st,
-               static_cast<const unsigned long long*>(s_key), s_key2, q, strategy);
-    BBS_CUDA(cudaGetLastError());
+    if (!fuse_sort) {
+      launch_pdl(rank_sort_auto_kernel, grid1(pend_cap, kRT), kRT, 0, s, d_st,
+                 static_cast<const unsigned long long*>(s_key), s_key2, q, strategy);
+      BBS_CUDA(cudaGetLastError());
+      ++launches;
+    }
     if (dbg_phases) record(ev_dbg[3 * e + 1]);
     launch_pdl(merge_auto_kernel,
                static_cast<unsigned>(std::min<uint64_t>((qcap + kMTile - 1) / kMTile, share_cap(148ull * 8))), kMT, 0,
                s, d_st, q, strategy, static_cast<const unsigned long long*>(s_key2),
-               static_cast<const unsigned long long*>(s_key), spec_votes_needed);
+               static_cast<const unsigned long long*>(s_key), spec_votes_needed, fuse_sort ? 1 : 0);
     BBS_CUDA(cudaGetLastError());
     if (dbg_phases) record(ev_dbg[3 * e + 2]);
-    launches += 6;
+    launches += 5;
   };
   auto enqueue_epoch = [&](int e) {
     if (spec_auto && !roots_dev_x) {
@@ -3037,9 +3102,12 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
     BBS_CUDA(cudaGetLastError());
     if (dbg_phases) record(ev_dbg[3 * e]);
     if (rank_sorted) {
-      launch_pdl(rank_sort_kernel, grid1(pend_cap, kRT), kRT, 0, s, d_st, s_key, s_key2, q,
-                 spec_on ? strategy : -1);
-      BBS_CUDA(cudaGetLastError());
+      if (!fuse_sort) {
+        launch_pdl(rank_sort_kernel, grid1(pend_cap, kRT), kRT, 0, s, d_st, s_key, s_key2, q,
+                   spec_on ? strategy : -1);
+        BBS_CUDA(cudaGetLastError());
+        ++launches;
+      }
     } else {
       launch_pdl(pad_keys_kernel, grid1(pend_cap), 256, 0, s, d_st, s_key, static_cast<uint64_t>(pend_cap), q,
                  spec_on ? strategy : -1);
@@ -3050,10 +3118,11 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
     if (dbg_phases) record(ev_dbg[3 * e + 1]);
     launch_pdl(merge_kernel, static_cast<unsigned>(std::min<uint64_t>((qcap + kMTile - 1) / kMTile, share_cap(148ull * 8))),
                kMT, 0, s, d_st, q, strategy, static_cast<const unsigned long long*>(s_key2),
-               static_cast<const unsigned long long*>(s_key));
+               static_cast<const unsigned long long*>(s_key),
+               rank_sorted && fuse_sort ? (spec_on ? strategy : -1) : -3);
     BBS_CUDA(cudaGetLastError());
     if (dbg_phases) record(ev_dbg[3 * e + 2]);
-    launches += 6;  // frontier, branch, score, survivors, rank_sort, merge (+ finalize)
+    launches += rank_sorted ? 5 : 6;  // frontier, branch, score, survivors, (pad+sort,) merge
     if (roots_dev_x) {  // incumbent + activity over NCCL, no host round-trip
       xchg_pack_kernel<<<1, 1, 0, s>>>(d_st, d_x);
       BBS_CUDA(cudaGetLastError());
