@@ -1727,18 +1727,69 @@ __device__ __forceinline__ unsigned long long lookback_excl(unsigned long long* 
     return 0;
   }
   atomicExch(&words[static_cast<size_t>(tile) * stride], tag | (1ull << 32) | count);
+  // 8 predecessors per round trip (independent loads), nearest first; tile 0
+  // is always inclusive, so the walk stops at or above it
   uint32_t excl = 0;
-  for (int64_t t = static_cast<int64_t>(tile) - 1; t >= 0;) {
-    const unsigned long long w = atomicAdd(&words[static_cast<size_t>(t) * stride], 0ull);
-    if ((w & ~((1ull << 34) - 1)) != tag) continue;  // not published yet
-    excl += static_cast<uint32_t>(w);
-    if (((w >> 32) & 3u) == 2u) break;
-    --t;
+  constexpr int kB = 8;
+  for (int64_t t = static_cast<int64_t>(tile) - 1;; t -= kB) {
+    const volatile unsigned long long* p = words;
+    unsigned long long w[kB];
+#pragma unroll
+    for (int j = 0; j < kB; ++j) w[j] = t - j >= 0 ? p[static_cast<size_t>(t - j) * stride] : 0ull;
+    bool done = false;
+#pragma unroll
+    for (int j = 0; j < kB; ++j) {
+      if (done || t - j < 0) continue;
+      while ((w[j] & ~((1ull << 34) - 1)) != tag) w[j] = p[static_cast<size_t>(t - j) * stride];  // not published yet
+      excl += static_cast<uint32_t>(w[j]);
+      done = ((w[j] >> 32) & 3u) == 2u;
+    }
+    if (done) break;
   }
   atomicExch(&words[static_cast<size_t>(tile) * stride], tag | (2ull << 32) | (excl + count));
   return excl;
 }
 
+// The same with a whole warp: 32 predecessors per step (lane l reads tile
+// tile-1-l), stopping at the nearest inclusive one.  A single thread walked
+// the ~1000 tiles of C2's 4M roots one L2 round trip at a time (root_select
+// 36 us).
+__device__ __forceinline__ uint32_t warp_lookback_excl(unsigned long long* words, uint32_t tile,
+                                                       unsigned long long tag, uint32_t count) {
+  const int lane = threadIdx.x & 31;
+  if (tile == 0) {
+    if (lane == 0) atomicExch(&words[0], tag | (2ull << 32) | count);
+    return 0;
+  }
+  if (lane == 0) atomicExch(&words[tile], tag | (1ull << 32) | count);
+  uint32_t excl = 0;
+  for (int64_t hi = static_cast<int64_t>(tile) - 1;; hi -= 32) {
+    const int64_t t = hi - lane;
+    unsigned long long w = 0;
+    if (t >= 0) {
+      const volatile unsigned long long* p = words + t;
+      do {
+        w = *p;
+      } while ((w & ~((1ull << 34) - 1)) != tag);  // not published yet
+    }
+    const bool incl = t < 0 || ((w >> 32) & 3u) == 2u;
+    const unsigned ballot = __ballot_sync(0xffffffffu, incl);
+    const int first = ballot ? __ffs(ballot) - 1 : 32;  // the nearest inclusive predecessor
+    uint32_t v = (t >= 0 && lane <= first) ? static_cast<uint32_t>(w) : 0u;
+#pragma unroll
+    for (int d = 16; d; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
+    excl += v;
+    if (ballot) break;
+  }
+  if (lane == 0) atomicExch(&words[tile], tag | (2ull << 32) | (excl + count));
+  return excl;
+}
+
+// One contiguous chunk of tiles per CTA (grid = chunks): the chunk's
+// survivors are counted first, one warp look-back over the chunks gives its
+// output offset, then the chunk's tiles are scanned again (L1/L2 hits) and
+// the survivors scattered in order.  A look-back per 4096-root tile (969
+// tiles on C2, 1.3 waves of CTAs) chained ~20 round trips: 27 us.
 __global__ void __launch_bounds__(kRST) root_select_kernel(EpochState* st, const int32_t* __restrict__ scores,
                                                            uint32_t n, unsigned long long n_scored,
                                                            int32_t threshold, int32_t smax, BoxParams bp,
@@ -1747,47 +1798,68 @@ __global__ void __launch_bounds__(kRST) root_select_kernel(EpochState* st, const
 
   using Load = cub::BlockLoad<int32_t, kRST, kRSIPT, cub::BLOCK_LOAD_WARP_TRANSPOSE>;
   using ScanI = cub::BlockScan<int, kRST>;
+  using RedI = cub::BlockReduce<int, kRST>;
   __shared__ union {
     typename Load::TempStorage load;
     typename ScanI::TempStorage scan;
+    typename RedI::TempStorage red;
   } tmp;
   __shared__ uint32_t s_tile, s_excl;
   __shared__ uint32_t s_h[2 * 256];
   for (int i = threadIdx.x; i < 2 * 256; i += kRST) s_h[i] = 0;
   const uint32_t n_tiles = (n + kRSTile - 1) / kRSTile;
   const unsigned long long nrot = static_cast<unsigned long long>(bp.nr) * bp.np * bp.nw;
-  for (;;) {
-    if (threadIdx.x == 0) s_tile = atomicAdd(&ri.ctl[0], 1u);
-    __syncthreads();
-    const uint32_t tile = s_tile;
-    if (tile >= n_tiles) break;
+  // tickets in launch order: a chunk's predecessors belong to running CTAs
+  if (threadIdx.x == 0) s_tile = atomicAdd(&ri.ctl[0], 1u);
+  __syncthreads();
+  const uint32_t chunk = s_tile, n_chunks = gridDim.x;
+  const uint32_t t_lo = static_cast<uint32_t>(static_cast<unsigned long long>(chunk) * n_tiles / n_chunks);
+  const uint32_t t_hi = static_cast<uint32_t>(static_cast<unsigned long long>(chunk + 1) * n_tiles / n_chunks);
+  const uint32_t lo = t_lo * kRSTile, hi = min(n, t_hi * kRSTile);
+  // pass 1: the chunk's survivor count (order does not matter here)
+  int cnt = 0;
+  for (uint32_t i = lo + threadIdx.x; i < hi; i += kRST * 4) {
+    int32_t v[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) v[k] = i + k * kRST < hi ? scores[i + k * kRST] : INT_MIN;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) cnt += v[k] >= threshold ? 1 : 0;
+  }
+  const int tot = RedI(tmp.red).Sum(cnt);
+  if (threadIdx.x < 32) {
+    const uint32_t excl =
+        warp_lookback_excl(ri.sel_tiles, chunk, ri.tag, static_cast<uint32_t>(__shfl_sync(0xffffffffu, tot, 0)));
+    if (threadIdx.x == 0) s_excl = excl;
+    if (threadIdx.x == 0 && chunk == n_chunks - 1) {
+      // the loop's initial state (no host copy on this path)
+      const uint32_t kept = excl + static_cast<uint32_t>(tot);
+      h0.q_len = kept;
+      h0.seq = kept;
+      h0.q_peak = kept;
+      h0.nodes_pruned = n_scored - kept;
+      h0.active = kept > 0 ? 1 : 0;
+      h0.any_active = h0.active;
+      *st = h0;
+    }
+  }
+  __syncthreads();
+  uint32_t run = s_excl;
+  // pass 2: tiles in order, survivors scattered in initial_nodes order
+  for (uint32_t tile = t_lo; tile < t_hi; ++tile) {
     const uint32_t base = tile * kRSTile;
     const uint32_t valid = min(static_cast<uint32_t>(kRSTile), n - base);
     int32_t sc[kRSIPT];
+    __syncthreads();
     Load(tmp.load).Load(scores + base, sc, static_cast<int>(valid), INT_MIN);
     __syncthreads();
-    int cnt = 0;
+    int c = 0;
 #pragma unroll
-    for (int k = 0; k < kRSIPT; ++k) cnt += sc[k] >= threshold ? 1 : 0;
-    int pos, tot;
-    ScanI(tmp.scan).ExclusiveSum(cnt, pos, tot);
-    if (threadIdx.x == 0) {
-      const uint32_t excl = lookback_excl(ri.sel_tiles, tile, 1, ri.tag, static_cast<uint32_t>(tot));
-      s_excl = excl;
-      if (tile == n_tiles - 1) {
-        // the loop's initial state (no host copy on this path)
-        const uint32_t kept = excl + static_cast<uint32_t>(tot);
-        h0.q_len = kept;
-        h0.seq = kept;
-        h0.q_peak = kept;
-        h0.nodes_pruned = n_scored - kept;
-        h0.active = kept > 0 ? 1 : 0;
-        h0.any_active = h0.active;
-        *st = h0;
-      }
-    }
-    __syncthreads();
-    uint32_t o = s_excl + static_cast<uint32_t>(pos);
+    for (int k = 0; k < kRSIPT; ++k) c += sc[k] >= threshold ? 1 : 0;
+    int pos, ttot;
+    ScanI(tmp.scan).ExclusiveSum(c, pos, ttot);
+    uint32_t o = run + static_cast<uint32_t>(pos);
+    run += static_cast<uint32_t>(ttot);
+    if (c == 0) continue;
 #pragma unroll
     for (int k = 0; k < kRSIPT; ++k) {
       if (sc[k] < threshold) continue;
@@ -2850,15 +2922,25 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
   if (dev_init) {
     const uint32_t n = static_cast<uint32_t>(total);
     const uint32_t sel_tiles = (n + kRSTile - 1) / kRSTile;
+    static const uint32_t sel_chunks = [] {  // A/B: BBS_SEL_CHUNKS
+      const char* v = std::getenv("BBS_SEL_CHUNKS");
+      return v ? std::max(1u, static_cast<uint32_t>(std::atoi(v))) : 592u;
+    }();
+    static const uint32_t root_pass_ctas = [] {  // A/B: BBS_PASS_CTAS
+      const char* v = std::getenv("BBS_PASS_CTAS");
+      return v ? std::max(1u, static_cast<uint32_t>(std::atoi(v))) : 148u;
+    }();
     const uint32_t pass_tiles = (n + kRPTile - 1) / kRPTile;
     rinit.bkey = W.sk0.get(n, s);
     rinit.k1 = W.sk1.get(n, s);
     rinit.v1 = W.perm0.get(n, s);
-    launch_pdl(root_select_kernel, std::min<uint32_t>(sel_tiles, 148u * 8u), kRST, 0, s, d_st,
+    launch_pdl(root_select_kernel, std::min<uint32_t>(sel_tiles, sel_chunks), kRST, 0, s, d_st,
                static_cast<const int32_t*>(root_scores), n, static_cast<unsigned long long>(n_scored_roots),
                threshold, smax, bp, q.pool, rinit, h0);
     BBS_CUDA(cudaGetLastError());
-    const unsigned pgrid = std::min<uint32_t>(pass_tiles, 148u * 8u);
+    // the survivors (unknown here) are usually far fewer than the roots:
+    // one CTA per SM claims the tiles (1184 CTAs were 2-3 waves of no work)
+    const unsigned pgrid = std::min<uint32_t>(pass_tiles, root_pass_ctas);
     if (end_bit <= 8) {
       launch_pdl(root_pass_kernel<true>, pgrid, kRPT, 0, s, static_cast<const EpochState*>(d_st), rinit, 0u,
                  strategy, smax, L, static_cast<const uint32_t*>(rinit.bkey), static_cast<const uint32_t*>(nullptr),
