@@ -31,5 +31,7 @@ full c2 cache_build 0
 full c3 frontier_auto 40
 full c3 survivors_auto 40
 full c3 cache_probe 60
+full c3 merge_auto 40
+full c2 root_select 0
 }
 ls $O

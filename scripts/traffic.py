@@ -23,7 +23,10 @@ SEARCH_KERNELS = {"root_hist_kernel", "root_colpad_kernel", "root_col_kernel", "
                   "root_select_kernel", "root_pass_kernel", "stage_window_kernel",
                   "cache_prebuild_list_kernel", "cache_build_kernel", "cache_probe_kernel",
                   "score_cube8_kernel", "frontier_kernel", "branch_kernel", "survivors_kernel",
-                  "rank_sort_kernel", "merge_kernel", "soa_kernel", "score_runs_kernel"}
+                  "rank_sort_kernel", "merge_kernel", "soa_kernel", "score_runs_kernel",
+                  "frontier_auto_kernel", "frontier_spec_kernel", "survivors_auto_kernel",
+                  "survivors_spec_kernel", "rank_sort_auto_kernel", "merge_auto_kernel", "pad_keys_kernel",
+                  "cache_prebuild_kernel", "scatter_own_kernel"}
 
 
 def load(path, last=0):
