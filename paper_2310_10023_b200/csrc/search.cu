@@ -66,7 +66,8 @@ struct EpochState {
   uint32_t n_keep;         // queue remainder kept after the incumbent trim
   uint32_t surv_ticket;    // survivors tile tickets (reset by the frontier)
   uint32_t merge_done;     // merge CTAs finished (the last one finalizes the epoch)
-  uint32_t fuse_claim, fuse_done;  // fused merge prologue: tasks claimed / finished
+  uint32_t fuse_claim, fuse_done, fuse_a;  // fused merge prologue: tasks claimed / finished / tile sorts finished
+  uint32_t tile_rank_min;  // survivors from which the fused sort ranks against sorted tiles
   uint32_t cache_raw;      // levels whose histogram builds gave up (flush cache, per frontier pass)
   uint32_t n_own;          // batch-split exact mode: children of this rank's runs
   int32_t any_active;      // sharded (device exchange): any rank still active
@@ -1371,7 +1372,12 @@ __device__ __forceinline__ void merge_kernel_body(EpochState* st,
     if (trim == -2) trim = st->spec_mode ? strategy : -1;
     const uint32_t n = st->n_surv;
     const uint32_t n_trim = trim >= 0 ? 1u : 0u;
-    const uint32_t tasks = n_trim + (n > kMergeSortSmall ? (n + kMT - 1u) / kMT : 0u);
+    const uint32_t n_tiles = (n + kMT - 1u) / kMT;
+    // many survivors (a deep round): sort every tile in place first, then
+    // rank each key by binary searches in the other sorted tiles, n^2/32
+    // shared-memory reads instead of n^2 compares
+    const bool tiled = n > st->tile_rank_min;
+    const uint32_t tasks = n_trim + (n > kMergeSortSmall ? (tiled ? 2u : 1u) * n_tiles : 0u);
     if (tasks) {
       __shared__ uint32_t s_task;
       unsigned long long* out = const_cast<unsigned long long*>(sorted_key);
@@ -1384,8 +1390,54 @@ __device__ __forceinline__ void merge_kernel_body(EpochState* st,
         const uint32_t t = s_task;
         __syncthreads();
         if (t >= tasks) break;
+        bool phase_a = false;
         if (t < n_trim) {
           if (threadIdx.x < 32) trim_remainder(st, q, trim, st->flush_best);
+        } else if (tiled) {
+          unsigned long long* keys = const_cast<unsigned long long*>(unsorted_key);
+          const uint32_t u = t - n_trim;
+          if (u < n_tiles) {  // phase A: tile u sorted in place (its keys are touched by this task only)
+            phase_a = true;
+            const uint32_t j = u * kMT + threadIdx.x;
+            const unsigned long long kj = j < n ? __ldcg(keys + j) : ~0ull;
+            s_ab[threadIdx.x] = kj;
+            __syncthreads();
+            uint32_t rank = 0;
+#pragma unroll 8
+            for (uint32_t i = 0; i < kMT; ++i) rank += s_ab[i] < kj ? 1u : 0u;
+            if (j < n) keys[u * kMT + rank] = kj;
+          } else {  // phase B: tile u - n_tiles against every other sorted tile
+            const uint32_t tt = u - n_tiles;
+            if (threadIdx.x == 0)  // every tile sort was claimed before this task: running CTAs
+              while (*reinterpret_cast<volatile uint32_t*>(&st->fuse_a) < n_tiles) __nanosleep(32);
+            __syncthreads();
+            const uint32_t j = tt * kMT + threadIdx.x;
+            const unsigned long long kj = j < n ? __ldcg(keys + j) : ~0ull;
+            uint32_t rank = threadIdx.x;  // within its own sorted tile
+            for (uint32_t v0 = 0; v0 < n_tiles; v0 += kMItems) {
+              __syncthreads();
+              for (uint32_t i = threadIdx.x; i < kMTile; i += kMT) {
+                const uint32_t g = v0 * kMT + i;
+                s_ab[i] = g < n ? __ldcg(keys + g) : ~0ull;
+              }
+              __syncthreads();
+              const uint32_t nv = min(static_cast<uint32_t>(kMItems), n_tiles - v0);
+              for (uint32_t w = 0; w < nv; ++w) {
+                if (v0 + w == tt) continue;
+                const unsigned long long* a = s_ab + w * kMT;
+                uint32_t lo = 0, hi = min(static_cast<uint32_t>(kMT), n - (v0 + w) * kMT);
+                while (lo < hi) {
+                  const uint32_t mid = (lo + hi) >> 1;
+                  if (a[mid] < kj)
+                    lo = mid + 1u;
+                  else
+                    hi = mid;
+                }
+                rank += lo;
+              }
+            }
+            if (j < n) out[rank] = kj;
+          }
         } else {  // rank sort of one tile (rank_sort_kernel_body), smem tiles in s_ab
           const uint32_t j = (t - n_trim) * kMT + threadIdx.x;
           const unsigned long long kj = j < n ? __ldg(unsorted_key + j) : ~0ull;
@@ -1402,7 +1454,10 @@ __device__ __forceinline__ void merge_kernel_body(EpochState* st,
         }
         __threadfence();
         __syncthreads();
-        if (threadIdx.x == 0) atomicAdd(&st->fuse_done, 1u);
+        if (threadIdx.x == 0) {
+          if (phase_a) atomicAdd(&st->fuse_a, 1u);
+          atomicAdd(&st->fuse_done, 1u);
+        }
       }
       if (threadIdx.x == 0)
         while (*reinterpret_cast<volatile uint32_t*>(&st->fuse_done) < tasks) __nanosleep(32);
@@ -1492,6 +1547,7 @@ __device__ __forceinline__ void merge_kernel_body(EpochState* st,
       st->merge_done = 0;
       st->fuse_claim = 0;  // every CTA is past the prologue
       st->fuse_done = 0;
+      st->fuse_a = 0;
       if (vote && !st->spec_mode) {
         // would a speculative round have kept the next epoch?  It is formed
         // from the remainder alone; the survivors displace it when the
@@ -2912,6 +2968,10 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
   h0.q_peak = h0.q_len;
   h0.spec_k = std::min(2, spec_k);  // the first round's depth; adapted per round
   h0.spec_kmax = static_cast<uint32_t>(spec_k);
+  h0.tile_rank_min = [] {  // A/B and tests: BBS_TILE_RANK_MIN (survivors; 256 = always tiled)
+    const char* v = std::getenv("BBS_TILE_RANK_MIN");
+    return v ? static_cast<uint32_t>(std::max(256, std::atoi(v))) : 4096u;
+  }();
   EpochState* d_st = W.st.get(1, s);
   if (!dev_init) {
     *W.h_st = h0;
