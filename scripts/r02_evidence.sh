@@ -19,7 +19,7 @@ python scripts/profile_search.py --config c2 --searches 2 > $O/plain.log 2>&1 &&
 M=gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum
 ncu --metrics $M --clock-control none --csv --log-file $O/c2_traffic.csv \
   python scripts/profile_search.py --config c2 --searches 2 > /dev/null 2>&1
-ncu --metrics $M --clock-control none --csv --launch-skip 600 --launch-count 300 --log-file $O/c3_traffic.csv \
+ncu --metrics $M --clock-control none --csv --launch-skip 150 --launch-count 300 --log-file $O/c3_traffic.csv \
   python scripts/profile_search.py --config c3 --searches 1 > /dev/null 2>&1
 full() {
   ncu --set full --clock-control none --import-source on -k regex:$2 --launch-skip $3 -c 1 \
