@@ -68,6 +68,7 @@ struct EpochState {
   uint32_t merge_done;     // merge CTAs finished (the last one finalizes the epoch)
   uint32_t fuse_claim, fuse_done, fuse_a;  // fused merge prologue: tasks claimed / finished / tile sorts finished
   uint32_t tile_rank_min;  // survivors from which the fused sort ranks against sorted tiles
+  uint32_t merge_all;      // A/B: every merge CTA ranks the survivors (BBS_MERGE_IDLE=0)
   uint32_t cache_raw;      // levels whose histogram builds gave up (flush cache, per frontier pass)
   uint32_t n_own;          // batch-split exact mode: children of this rank's runs
   int32_t any_active;      // sharded (device exchange): any rank still active
@@ -1475,10 +1476,16 @@ __device__ __forceinline__ void merge_kernel_body(EpochState* st,
   const uint32_t cur = st->cur;
   const uint32_t n_keep = __ldcg(&st->n_keep);
   const uint32_t n_s = st->n_surv;
+  // the grid is sized for the queue's capacity (the root count on the first
+  // flushes: C2 1184 CTAs for ~20 output tiles): CTAs without an output
+  // tile skip the survivor ranking and the merge (they still count towards
+  // merge_done, so the finalising CTA is the last CTA of the grid -- every
+  // CTA is then past the claimed-task prologue)
+  const bool idle = !st->merge_all && static_cast<uint64_t>(blockIdx.x) * kMTile >= static_cast<uint64_t>(n_keep) + n_s;
   // few survivors: every CTA ranks them in shared memory (no sort kernel)
   __shared__ unsigned long long s_b[kMergeSortSmall];
   const unsigned long long* skey = sorted_key;
-  if (n_s <= kMergeSortSmall) {
+  if (n_s <= kMergeSortSmall && !idle) {
     static_assert(kMergeSortSmall == kMT, "one survivor per thread");
     const unsigned long long kj = threadIdx.x < n_s ? __ldcg(unsorted_key + threadIdx.x) : ~0ull;
     s_ab[threadIdx.x] = kj;
@@ -1493,13 +1500,21 @@ __device__ __forceinline__ void merge_kernel_body(EpochState* st,
   unsigned long long* __restrict__ ok = q.keys(cur ^ 1u);
   // the vote's two keys, loaded before the merge work (inputs, unchanged by it)
   unsigned long long vote_s = 0, vote_a = 0;
-  if (vote && threadIdx.x == 0 && !st->spec_mode && n_s) {
-    vote_s = skey[0];  // sorted by rank_sort, or ranked in shared memory above
+  if (vote && threadIdx.x < 32 && !st->spec_mode && n_s) {
+    if (idle && n_s <= kMergeSortSmall) {  // not ranked here: the smallest survivor key
+      unsigned long long m = ~0ull;
+      for (uint32_t i = threadIdx.x; i < n_s; i += 32) m = min(m, __ldcg(unsorted_key + i));
+#pragma unroll
+      for (int d = 16; d; d >>= 1) m = min(m, __shfl_xor_sync(0xffffffffu, m, d));
+      vote_s = m;
+    } else {
+      vote_s = skey[0];  // sorted (rank sort / the prologue), or ranked in shared memory above
+    }
     vote_a = st->look_key;
   }
   const uint32_t total = n_keep + n_s;
   const uint32_t warp = threadIdx.x >> 5;
-  for (uint32_t d0 = blockIdx.x * kMTile; d0 < total; d0 += gridDim.x * kMTile) {
+  for (uint32_t d0 = idle ? total : blockIdx.x * kMTile; d0 < total; d0 += gridDim.x * kMTile) {
     const uint32_t d1 = min(total, d0 + kMTile);
     if (warp < 2) {
       const uint32_t sp = warp_merge_split(A, n_keep, skey, n_s, warp ? d1 : d0);
@@ -2971,6 +2986,10 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
   h0.tile_rank_min = [] {  // A/B and tests: BBS_TILE_RANK_MIN (survivors; 256 = always tiled)
     const char* v = std::getenv("BBS_TILE_RANK_MIN");
     return v ? static_cast<uint32_t>(std::max(256, std::atoi(v))) : 4096u;
+  }();
+  h0.merge_all = [] {
+    const char* v = std::getenv("BBS_MERGE_IDLE");
+    return v && v[0] == '0' ? 1u : 0u;
   }();
   EpochState* d_st = W.st.get(1, s);
   if (!dev_init) {
