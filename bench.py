@@ -698,11 +698,26 @@ def run_b200_throughput(args, cfgd):
     barrier()
     clk = clocks.stop()
     t_local = sum(step_ms)
-    # e2e: host API with host scan buffers, sequential (bbs_search copies in/out)
+    # e2e: the throughput-mode public API from pinned host scans -- every scan
+    # uploaded (bbs_scan_upload), bbs_search_scans, results read back; the
+    # sequential bbs_search() loop is reported beside it
+    pinned = {}
+    for j in mine:
+        p = torch.empty(scans[j].shape, dtype=torch.float64, pin_memory=True)
+        p.copy_(torch.from_numpy(scans[j]))
+        pinned[j] = p.numpy()
+    flush.fill_(1)
+    torch.cuda.synchronize()
     t0 = time.perf_counter()
-    res_h = batch(host=True)
+    up = [B.DeviceScan(vmap, pinned[j]) for j in mine]
+    res_h = dict(zip(mine, B.search_scans(vmap, up, cfg, concurrency=T)))
     e2e_s = time.perf_counter() - t0
+    del up
     e2e_evals = sum(r.stats.nodes_generated for r in res_h.values())
+    t0 = time.perf_counter()
+    res_seq = batch(host=True)
+    seq_s = time.perf_counter() - t0
+    seq_evals = sum(r.stats.nodes_generated for r in res_seq.values())
     if world > 1:
         import torch.distributed as dist
         v = torch.tensor([t_local, e2e_s], dtype=torch.float64, device="cuda")
@@ -732,7 +747,9 @@ def run_b200_throughput(args, cfgd):
         "e2e": {"value": e2e_evals / e2e_s, "unit": "evals/s",
                 "h2d_bytes_per_step": int(sum(24 * scans[j].shape[0] for j in mine)),
                 "d2h_bytes_per_step": int(sum(r.d2h_bytes for r in res_h.values())),
-                "timing": "host wall clock, sequential bbs_search() with host scans"},
+                "timing": "host wall clock (rank max): pinned host scans uploaded with bbs_scan_upload, "
+                          "bbs_search_scans, results read back",
+                "sequential_bbs_search": {"value": seq_evals / seq_s, "unit": "evals/s"}},
         "clocks": clk, "gpu_launches": int(sum(r.kernel_launches for r in res.values())) * args.steps,
     }
     if rank == 0:
