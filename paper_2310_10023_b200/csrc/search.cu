@@ -371,6 +371,7 @@ __global__ void __launch_bounds__(kFT) frontier_kernel(EpochState* st, Queue q, 
 // kept epochs are a prefix; their Stats, trace and survivors are committed
 // exactly as the sequential schedule makes them (search.hpp:132-169), the
 // rest is discarded and re-formed by the next round from the true queue.
+constexpr uint64_t kTraceStage = 256;  // incumbent-trace entries staged with every host check
 constexpr int kSpecMax = 16;
 struct SpecRec {
   unsigned long long lastkey;    // key of the epoch's last pop (its cut entry)
@@ -2141,7 +2142,7 @@ struct Workspace {
   cudaStream_t side = nullptr;            // prebuild stream (forked per search)
   cudaGraphExec_t graph_exec = nullptr;   // epoch-batch graph, updated in place per search
   cudaEvent_t block_ev = nullptr;         // blocking-sync event (host checks of concurrent searches)
-  unsigned long long* h_small = nullptr;  // pinned: probes, n_root_surv
+  unsigned long long* h_small = nullptr;  // pinned: probes, n_root_surv, then kTraceStage trace entries
   std::vector<cudaEvent_t> ev;
   size_t ev_used = 0;
   cudaEvent_t next_event() {
@@ -2208,7 +2209,9 @@ struct Lease {
     if (!w) {
       w = new Workspace();
       BBS_CUDA(cudaMallocHost(reinterpret_cast<void**>(&w->h_st), sizeof(EpochState)));
-      BBS_CUDA(cudaMallocHost(reinterpret_cast<void**>(&w->h_small), 4 * sizeof(unsigned long long)));
+      // pinned: 4 counters + the staged head of the incumbent trace
+      BBS_CUDA(cudaMallocHost(reinterpret_cast<void**>(&w->h_small),
+                              4 * sizeof(unsigned long long) + kTraceStage * sizeof(int32_t)));
     }
     w->ev_used = 0;
   }
@@ -3373,6 +3376,18 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
     member.slot = grp->join();
     member.g = grp;
   }
+  // the root batch's counters are final: they ride along with the first
+  // host check (no extra round trip after the loop)
+  if (dev_init) {
+    BBS_CUDA(cudaMemcpyAsync(&W.h_small[0], d_probes, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+    d2h += sizeof(unsigned long long);
+  }
+  BBS_CUDA(cudaMemcpyAsync(&W.h_small[3], d_probes + 2, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+  d2h += sizeof(unsigned long long);
+  bool state_fresh = false;  // W.h_st holds the device state after the last enqueued work
+  const uint64_t trace_stage = cfg.collect_trace && out->best_score_trace
+                                   ? std::min<uint64_t>({trace_cap, out->trace_capacity, kTraceStage})
+                                   : 0;
   const auto t_loop = std::chrono::steady_clock::now();
   uint64_t group_checks = 0;
   tmark("loop");
@@ -3462,8 +3477,13 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
     }
     if (!member.g) {
       BBS_CUDA(cudaMemcpyAsync(W.h_st, d_st, sizeof(EpochState), cudaMemcpyDeviceToHost, s));
+      if (trace_stage) {  // the trace's head with the state: no round trip for it after the loop
+        BBS_CUDA(cudaMemcpyAsync(W.h_small + 4, d_trace, trace_stage * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+        d2h += trace_stage * sizeof(int32_t);
+      }
       host_wait();
     }
+    state_fresh = !member.g;
     d2h += sizeof(EpochState);
     // in the group the epochs are not timed one by one: host time since the
     // loop began stands for every pass of the check
@@ -3546,15 +3566,15 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
     for (int k = 0; k < 6; ++k) std::fprintf(stderr, " %s %.2f", names[k], 1e3 * dbg_sum[k] / dbg_n);
     std::fprintf(stderr, "\n");
   }
-  BBS_CUDA(cudaMemcpyAsync(W.h_st, d_st, sizeof(EpochState), cudaMemcpyDeviceToHost, s));
-  d2h += sizeof(EpochState);
-  if (dev_init) {
-    BBS_CUDA(cudaMemcpyAsync(&W.h_small[0], d_probes, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
-    d2h += sizeof(unsigned long long);
+  if (!state_fresh || shard) {
+    // the group path, a sharded search (its exchange may follow the last
+    // check) or no check at all: read the final state once more
+    BBS_CUDA(cudaMemcpyAsync(W.h_st, d_st, sizeof(EpochState), cudaMemcpyDeviceToHost, s));
+    d2h += sizeof(EpochState);
+    host_wait();
+  } else {
+    BBS_CUDA(cudaEventSynchronize(ev_end));  // nothing left on the stream: the event completes at once
   }
-  BBS_CUDA(cudaMemcpyAsync(&W.h_small[3], d_probes + 2, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
-  d2h += sizeof(unsigned long long);
-  host_wait();
   hs = *W.h_st;
   if (dev_init) root_probes = W.h_small[0];
   out->root_words = W.h_small[3];
@@ -3635,9 +3655,13 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
   out->trace_length = cfg.collect_trace ? hs.trace_len : 0;
   if (cfg.collect_trace && out->best_score_trace && hs.trace_len) {
     const uint64_t nt = std::min<uint64_t>(hs.trace_len, out->trace_capacity);
-    BBS_CUDA(cudaMemcpyAsync(out->best_score_trace, d_trace, nt * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
-    BBS_CUDA(cudaStreamSynchronize(s));
-    d2h += nt * sizeof(int32_t);
+    if (state_fresh && !shard && nt <= trace_stage) {
+      std::memcpy(out->best_score_trace, W.h_small + 4, nt * sizeof(int32_t));  // staged with the last state
+    } else {
+      BBS_CUDA(cudaMemcpyAsync(out->best_score_trace, d_trace, nt * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+      BBS_CUDA(cudaStreamSynchronize(s));
+      d2h += nt * sizeof(int32_t);
+    }
   }
   out->h2d_bytes = h2d;
   out->d2h_bytes = d2h;
