@@ -305,13 +305,18 @@ def test_large_scan_paths_are_transparent(B, golden_scenes, monkeypatch):
 
 
 @pytest.mark.parametrize("strategy", ["BFS", "DFS"])
-@pytest.mark.parametrize("cobatch", ["1", "0"])
+@pytest.mark.parametrize("cobatch", ["1", "0", "0-tiled"])
 def test_search_scans_throughput_mode_matches_single_searches(B, monkeypatch, strategy, cobatch):
     """bbs_search_scans (native workers, workspaces leased concurrently; the
     flushes of the searches in flight co-batched into one launch per epoch
     kernel, or each search on its own stream) returns each scan's search()
-    result: Stats, trace, pose."""
+    result: Stats, trace, pose.  "0-tiled": concurrent streams with the merge
+    kernel's claimed-task sort in its two-phase form from 257 survivors (the
+    concurrent merges' CTAs share the SMs; no co-residency is assumed)."""
+    cobatch, _, tiled = cobatch.partition("-")
     monkeypatch.setenv("BBS_COBATCH", cobatch)
+    if tiled:
+        monkeypatch.setenv("BBS_TILE_RANK_MIN", "256")
     spec = H.SceneSpec.default(size_x=24.0, size_y=24.0, size_z=10.0, num_boxes=4, min_box_side=2.5,
                                max_box_side=6.0, min_box_height=3.0, map_spacing=0.3,
                                scan_spacing=0.45, scan_range=14.0, min_scan_points=300)
