@@ -3224,7 +3224,7 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
                static_cast<const unsigned long long*>(s_key), spec_votes_needed, fuse_sort ? 1 : 0);
     BBS_CUDA(cudaGetLastError());
     if (dbg_phases) record(ev_dbg[3 * e + 2]);
-    launches += 5;
+    launches += 4 + (cache.enabled ? (builds_live ? 3 : 2) : 1);  // the score step: build + probe + cube
   };
   auto enqueue_epoch = [&](int e) {
     if (spec_auto && !roots_dev_x) {
@@ -3286,7 +3286,8 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
                rank_sorted && fuse_sort ? (spec_on ? strategy : -1) : -3);
     BBS_CUDA(cudaGetLastError());
     if (dbg_phases) record(ev_dbg[3 * e + 2]);
-    launches += rank_sorted ? 5 : 6;  // frontier, branch, score, survivors, (pad+sort,) merge
+    // frontier, branch, the score step (build + probe + cube), survivors, (pad + sort,) merge
+    launches += (rank_sorted ? 4 : 5) + (cache.enabled ? (builds_live ? 3 : 2) : 1);
     if (roots_dev_x) {  // incumbent + activity over NCCL, no host round-trip
       xchg_pack_kernel<<<1, 1, 0, s>>>(d_st, d_x);
       BBS_CUDA(cudaGetLastError());
@@ -3305,6 +3306,7 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
   uint64_t batch_qcap = 0;
   const bbs_node* batch_pool = nullptr;
   bool batch_builds = true, batch_spec = false;
+  uint64_t batch_launches = 0;
   EpochState hs = h0;
   bool self_active = h0.active != 0;
   if (dev_init) {  // upper bounds until the first device state comes back
@@ -3446,6 +3448,7 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
         capturing = true;
         const uint64_t l0 = launches;
         for (int e = 0; e < E; ++e) enqueue_epoch(e);
+        batch_launches = launches - l0;  // kernels per graph launch
         launches = l0;
         capturing = false;
         BBS_CUDA(cudaStreamEndCapture(s, &graph));
@@ -3471,7 +3474,7 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
         batch_spec = spec_on;
       }
       BBS_CUDA(cudaGraphLaunch(W.graph_exec, s));
-      launches += 6ull * E;
+      launches += batch_launches;
     } else {
       for (int e = 0; e < n_ep; ++e) enqueue_epoch(e);
     }
