@@ -213,13 +213,18 @@ def c3(B):
     return vm, s
 
 
-@pytest.mark.parametrize("direct", ["1", "0"])
+@pytest.mark.parametrize("direct", ["1", "0", "1-tiled"])
 def test_c3_search_matches_reference(B, c3, direct, monkeypatch):
     """C3 city (BASELINE configs[2]): 30M map points, K = 30k, 7 levels,
     +-5 deg roll/pitch: search() equals the reference's (score, pose, Stats,
     trace) -- with the speculative rounds' direct runs scored in the probe
-    kernel (default) and by the cube kernel after it."""
+    kernel (default) and by the cube kernel after it; "tiled": the merge
+    kernel's two-phase survivor sort forced from 257 survivors (72 rounds of
+    up to 16 flushes)."""
+    direct, _, tiled = direct.partition("-")
     monkeypatch.setenv("BBS_DIRECT_RUNS", direct)
+    if tiled:
+        monkeypatch.setenv("BBS_TILE_RANK_MIN", "256")
     vm, s = c3
     want = golden_json("c3_search.json")["bfs_roto_b10000"]
     assert digest(s) == want["scan_digest"]
