@@ -719,9 +719,17 @@ void launch_cache_prebuild(const MapView& map, const GridView& grid, const ScanV
                            uint32_t n_rot, cudaStream_t s) {
   if (n_rot == 0) return;
   const int build_smem = kCacheHashSlots * 12 + kCacheAmbCap * 4;
-  BBS_CUDA(cudaFuncSetAttribute(cache_build_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, build_smem));
-  cache_build_kernel<<<std::min<uint32_t>(n_rot, 148 * 2), kBuildThreads, build_smem, s>>>(pre, map, grid, scan,
-                                                                                          n_rot);
+  static std::atomic<uint64_t> attr_done{0};
+  static std::mutex attr_mu;
+  once_per_device(attr_done, attr_mu, [&] {
+    BBS_CUDA(cudaFuncSetAttribute(cache_build_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, build_smem));
+  });
+  // A/B: BBS_PREBUILD_CTAS (default 2 per SM)
+  const uint32_t ctas = [] {
+    const char* v = std::getenv("BBS_PREBUILD_CTAS");
+    return v ? std::max(1u, static_cast<uint32_t>(std::atoi(v))) : 148u * 2;
+  }();
+  cache_build_kernel<<<std::min<uint32_t>(n_rot, ctas), kBuildThreads, build_smem, s>>>(pre, map, grid, scan, n_rot);
   BBS_CUDA(cudaGetLastError());
 }
 
