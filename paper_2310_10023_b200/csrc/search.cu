@@ -1355,14 +1355,16 @@ __device__ __forceinline__ uint32_t warp_merge_split(const RemView& A, uint32_t 
 // incumbent trim of a round, trim >= 0 or -2 = by st->spec_mode; the rank
 // sort of more than kMergeSortSmall survivors into sorted_key), one launch
 // less per flush.  That work is split into tasks (trim, then one per tile of
-// kMT keys) that CTAs claim with an atomic counter; a CTA waits only for
-// tasks already claimed by running CTAs, so the wait cannot starve whatever
-// share of the grid is resident (other searches on other streams included).
+// kMT keys; above st->tile_rank_min survivors two per tile: the tiles sorted
+// in place in unsorted_key, then ranked against each other) that CTAs claim
+// with an atomic counter; a CTA waits only for tasks already claimed by
+// running CTAs, so the wait cannot starve whatever share of the grid is
+// resident (other searches on other streams included).
 __device__ __forceinline__ void merge_kernel_body(EpochState* st,
                                                   Queue q,
                                                   int strategy,
                                                   const unsigned long long* sorted_key,
-                                                  const unsigned long long* __restrict__ unsorted_key,
+                                                  const unsigned long long* unsorted_key,
                                                   int vote = 0, bool fused = false, int trim = -1) {
   pdl_wait();
 
@@ -1584,7 +1586,7 @@ __device__ __forceinline__ void merge_kernel_body(EpochState* st,
 
 __global__ void __launch_bounds__(kMT) merge_kernel(EpochState* st, Queue q, int strategy,
                                                     const unsigned long long* skey,
-                                                    const unsigned long long* __restrict__ ukey, int fused_trim) {
+                                                    const unsigned long long* ukey, int fused_trim) {
   // fused_trim: -3 = not fused (a rank-sort kernel ran), else the trim strategy (-1 none)
   merge_kernel_body(st, q, strategy, skey, ukey, 0, fused_trim != -3, fused_trim);
 }
@@ -1644,7 +1646,7 @@ __global__ void __launch_bounds__(kRT) rank_sort_auto_kernel(EpochState* st,
 
 __global__ void __launch_bounds__(kMT) merge_auto_kernel(EpochState* st, Queue q, int strategy,
                                                          const unsigned long long* skey,
-                                                         const unsigned long long* __restrict__ ukey, int votes,
+                                                         const unsigned long long* ukey, int votes,
                                                          int fused) {
   merge_kernel_body(st, q, strategy, skey, ukey, votes, fused != 0, -2);
 }
