@@ -829,7 +829,7 @@ __global__ void branch_kernel(EpochState* st, Queue q, GridView G,
 }
 
 constexpr int kST = 256;   // survivors: threads per tile
-constexpr int kSIPT = 16;  // items per thread (4096 per tile)
+constexpr int kSIPT = 8;  // items per thread (2048 per tile)
 constexpr int kSTile = kST * kSIPT;
 
 __device__ __forceinline__ uint32_t lower_bound_u64(const unsigned long long* a, uint32_t n,
@@ -1003,7 +1003,7 @@ __device__ __forceinline__ void survivors_kernel_body(EpochState* st,
     int32_t sc[kSIPT];
     Load(tmp.load).Load(scores + base, sc, static_cast<int>(valid), INT_MIN);
     __syncthreads();
-    // runs of 8 share a level; kSIPT = 16 covers two runs per thread
+    // runs of 8 share a level; a thread holds kSIPT / 8 whole runs
     static_assert(kSIPT % 8 == 0, "tile rows must hold whole runs");
 #pragma unroll
     for (int rr = 0; rr < kSIPT / 8; ++rr) {
@@ -1824,41 +1824,6 @@ __device__ __forceinline__ unsigned long long lookback_excl(unsigned long long* 
   return excl;
 }
 
-// The same with a whole warp: 32 predecessors per step (lane l reads tile
-// tile-1-l), stopping at the nearest inclusive one.  A single thread walked
-// the ~1000 tiles of C2's 4M roots one L2 round trip at a time (root_select
-// 36 us).
-__device__ __forceinline__ uint32_t warp_lookback_excl(unsigned long long* words, uint32_t tile,
-                                                       unsigned long long tag, uint32_t count) {
-  const int lane = threadIdx.x & 31;
-  if (tile == 0) {
-    if (lane == 0) atomicExch(&words[0], tag | (2ull << 32) | count);
-    return 0;
-  }
-  if (lane == 0) atomicExch(&words[tile], tag | (1ull << 32) | count);
-  uint32_t excl = 0;
-  for (int64_t hi = static_cast<int64_t>(tile) - 1;; hi -= 32) {
-    const int64_t t = hi - lane;
-    unsigned long long w = 0;
-    if (t >= 0) {
-      const volatile unsigned long long* p = words + t;
-      do {
-        w = *p;
-      } while ((w & ~((1ull << 34) - 1)) != tag);  // not published yet
-    }
-    const bool incl = t < 0 || ((w >> 32) & 3u) == 2u;
-    const unsigned ballot = __ballot_sync(0xffffffffu, incl);
-    const int first = ballot ? __ffs(ballot) - 1 : 32;  // the nearest inclusive predecessor
-    uint32_t v = (t >= 0 && lane <= first) ? static_cast<uint32_t>(w) : 0u;
-#pragma unroll
-    for (int d = 16; d; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
-    excl += v;
-    if (ballot) break;
-  }
-  if (lane == 0) atomicExch(&words[tile], tag | (2ull << 32) | (excl + count));
-  return excl;
-}
-
 // One contiguous chunk of tiles per CTA (grid = chunks): the chunk's
 // survivors are counted first, one warp look-back over the chunks gives its
 // output offset, then the chunk's tiles are scanned again (L1/L2 hits) and
@@ -1902,7 +1867,7 @@ __global__ void __launch_bounds__(kRST) root_select_kernel(EpochState* st, const
   const int tot = RedI(tmp.red).Sum(cnt);
   if (threadIdx.x < 32) {
     const uint32_t excl =
-        warp_lookback_excl(ri.sel_tiles, chunk, ri.tag, static_cast<uint32_t>(__shfl_sync(0xffffffffu, tot, 0)));
+        warp_lookback(ri.sel_tiles, chunk, static_cast<uint32_t>(__shfl_sync(0xffffffffu, tot, 0)), ri.tag);
     if (threadIdx.x == 0) s_excl = excl;
     if (threadIdx.x == 0 && chunk == n_chunks - 1) {
       // the loop's initial state (no host copy on this path)
