@@ -3442,6 +3442,7 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
       }
       BBS_CUDA(cudaGraphLaunch(W.graph_exec, s));
       launches += batch_launches;
+      if (group_checks == 0 && pass_ms.empty()) tmark("first batch launched");
     } else {
       for (int e = 0; e < n_ep; ++e) enqueue_epoch(e);
     }
