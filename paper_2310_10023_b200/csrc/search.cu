@@ -3143,6 +3143,12 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
   // device-switched rounds (frontier_auto_kernel ...): BFS single searches
   // with rank-sorted survivors; the host-switched schedule otherwise
   // (BBS_SPEC_AUTO=0: plain epochs for the first host check, then rounds)
+  // merge grid cap (A/B: BBS_MERGE_CTAS; CTAs beyond the queue's output
+  // tiles only take part in the sort tasks)
+  const uint64_t merge_ctas = [] {
+    const char* v = std::getenv("BBS_MERGE_CTAS");
+    return v ? static_cast<uint64_t>(std::max(1, std::atoi(v))) : 148ull * 4;
+  }();
   // the merge kernel does the rank sort (and the round's trim) itself
   // (BBS_FUSE_SORT=0: a rank-sort kernel before it)
   const bool fuse_sort = [] {
@@ -3186,7 +3192,7 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
     }
     if (dbg_phases) record(ev_dbg[3 * e + 1]);
     launch_pdl(merge_auto_kernel,
-               static_cast<unsigned>(std::min<uint64_t>((qcap + kMTile - 1) / kMTile, share_cap(148ull * 8))), kMT, 0,
+               static_cast<unsigned>(std::min<uint64_t>((qcap + kMTile - 1) / kMTile, share_cap(merge_ctas))), kMT, 0,
                s, d_st, q, strategy, static_cast<const unsigned long long*>(s_key2),
                static_cast<const unsigned long long*>(s_key), spec_votes_needed, fuse_sort ? 1 : 0);
     BBS_CUDA(cudaGetLastError());
@@ -3247,7 +3253,7 @@ void run_search(bbs_map* m, bbs_scan* scan, const bbs_search_config& cfg, const 
       BBS_CUDA(cub::DeviceRadixSort::SortKeys(sort_temp, tb, s_key, s_key2, static_cast<int64_t>(pend_cap), 0, 64, s));
     }
     if (dbg_phases) record(ev_dbg[3 * e + 1]);
-    launch_pdl(merge_kernel, static_cast<unsigned>(std::min<uint64_t>((qcap + kMTile - 1) / kMTile, share_cap(148ull * 8))),
+    launch_pdl(merge_kernel, static_cast<unsigned>(std::min<uint64_t>((qcap + kMTile - 1) / kMTile, share_cap(merge_ctas))),
                kMT, 0, s, d_st, q, strategy, static_cast<const unsigned long long*>(s_key2),
                static_cast<const unsigned long long*>(s_key),
                rank_sorted && fuse_sort ? (spec_on ? strategy : -1) : -3);
