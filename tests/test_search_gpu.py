@@ -378,18 +378,21 @@ def test_speculative_rounds_match_reference(B, golden_scenes, name, spec, monkey
         assert_same(res, want, f"{name}/{label}/spec{spec}")
 
 
-@pytest.mark.parametrize("variant", ["rank-kernel", "fused-tiled", "fused"])
+@pytest.mark.parametrize("variant", ["rank-kernel", "fused-tiled", "fused", "fused-tiled-3ctas"])
 @pytest.mark.parametrize("name", ["small", "room"])
 def test_survivor_sort_variants_match_reference(B, golden_scenes, name, variant, monkeypatch):
     """The flush survivors' sort: a separate rank-sort kernel
     (BBS_FUSE_SORT=0), the merge kernel's claimed-tile rank sort (default), or
     its two-phase variant (tiles sorted in place, then ranked by binary
-    searches in the other tiles; forced from 257 survivors) -- all give the
-    reference's search() exactly, plain epochs and speculative rounds."""
+    searches in the other tiles; forced from 257 survivors), also on a
+    3-CTA merge grid -- all give the reference's search() exactly, plain
+    epochs and speculative rounds."""
     if variant == "rank-kernel":
         monkeypatch.setenv("BBS_FUSE_SORT", "0")
-    if variant == "fused-tiled":
+    if variant.startswith("fused-tiled"):
         monkeypatch.setenv("BBS_TILE_RANK_MIN", "256")
+    if variant.endswith("3ctas"):  # a 3-CTA merge grid: every CTA loops over many tiles and sort tasks
+        monkeypatch.setenv("BBS_MERGE_CTAS", "3")
     m, s, _, sc = load_case(B, golden_scenes, name)
     vm = B.MultiResVoxelMap.build(m, sc["r"], sc["max_level"])
     for label, want in golden_json(f"{name}_search.json").items():
